@@ -1,0 +1,178 @@
+/*
+ * cacsi.h -- C ABI of the B200-native forward/backward operators of fan-beam
+ * coded-aperture X-ray coherent-scatter imaging (arXiv 1603.06400,
+ * "Joint System and Algorithm Design for Computationally Efficient Fan Beam
+ * Coded Aperture X-ray Coherent Scatter Imaging").
+ *
+ * The problem: an unknown object scatter density
+ * f(r, q) >= 0 over B fan-slice pixels r = (y, z) and Q momentum-transfer
+ * nodes q (J = B x Q unknowns), detector counts y with a known
+ * background r (Eq. poisson_model), the system matrix
+ * H = A of Eq. (1), and the penalized Poisson objective
+ * J = L + beta R minimised over f >= 0 by the EM-type iteration of Alg. 5
+ * (PAPER.md:363-377).
+ *
+ * Frame (config frame): source at the origin, beam along +z, fan
+ * in the x = 0 plane.  Voxel r = (0, y, z); detector pixel r' = (x, y, det_z)
+ * with rows along x (out of fan) and columns along y; the secondary mask lies
+ * in the plane z = mask_z.  Lengths in mm, q in 1/Angstrom, E in keV.
+ *
+ * Operator:
+ *   A[r'; (r, j)]      = P(r, r') sum_k phi_k E_k Lambda(u_k - j)   (energy-integrating)
+ *   A[(r', k); (r, j)] = P(r, r') phi_k E_k Lambda(u_k - j)         (energy-resolving)
+ *   P = scale * G_so(r) G_od(s) T(r, r') dtheta (1 + cos^2 theta) cos(theta / 2)
+ *   u_k = (E_k sin(theta/2) / hc - q_min) / dq,  hc = 12.3984193 keV A,
+ *   Lambda(x) = max(0, 1 - |x|)  (linear interpolation in q, zero outside).
+ *
+ * Memory layouts (all row-major, fp32, caller-owned DEVICE buffers unless a
+ * function name ends in _host):
+ *   f, b  : [ny][nz][nq]                 (object / backprojection)
+ *   g, w  : [det_nx][det_ny]             (energy_resolving = 0)
+ *           [det_nx][det_ny][ne]         (energy_resolving = 1)
+ *   y, r  : same shape as g              (counts, background)
+ *
+ * Conventions:
+ *   - Every call is asynchronous and ordered on `stream` (a cudaStream_t
+ *     passed as void*, NULL = legacy default stream) unless stated otherwise.
+ *   - Outputs are OVERWRITTEN, never accumulated into.
+ *   - A handle is immutable after create.  Calls on one handle may run
+ *     concurrently on different streams only if each uses its own workspace;
+ *     the operators' internal scratch comes from the stream-ordered allocator
+ *     (cudaMallocAsync) on the caller's stream.
+ *   - Run-time NaN / negative inputs are not checked (documented).
+ *   - There is no CPU fallback: without a usable sm_100 device every call
+ *     that launches work returns CACSI_ERR_CUDA.
+ */
+#ifndef CACSI_H
+#define CACSI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CACSI_API __attribute__((visibility("default")))
+#else
+#define CACSI_API
+#endif
+
+typedef enum {
+    CACSI_OK = 0,
+    CACSI_ERR_NULL = 1,    /* a required pointer was NULL                       */
+    CACSI_ERR_INVALID = 2, /* descriptor / argument violates a documented rule  */
+    CACSI_ERR_CUDA = 3,    /* CUDA launch / runtime failure, or no sm_100 device */
+    CACSI_ERR_NOMEM = 4    /* device or host allocation failed                  */
+} cacsi_status;
+
+typedef struct cacsi_geometry cacsi_geometry; /* opaque, immutable after create */
+
+/* Geometry descriptor.  Read only during cacsi_geometry_create (all arrays are
+ * copied).  Validation (-> CACSI_ERR_INVALID):
+ *   ny, nz, ne, mask_nx, mask_ny, det_nx, det_ny >= 1; 2 <= nq <= 400; ne <= 256
+ *       (shared-memory table limits);
+ *   y_min < y_max, 0 < z_min < z_max < mask_z < det_z   (plane order, so that
+ *       every scatter vector has s_z > 0 and crosses the mask plane);
+ *   q_min < q_max; mask_pitch > 0; det_pitch > 0; scale > 0 and finite;
+ *   energy_kev strictly increasing and > 0; phi >= 0; mask bytes in {0, 1};
+ *   energy_resolving in {0, 1}.                                              */
+typedef struct {
+    /* object slice: voxel centres y_i = y_min + (i + 1/2) (y_max - y_min)/ny,
+     * likewise z ("B spatial bins")                            */
+    int32_t ny, nz;
+    double y_min, y_max, z_min, z_max;
+    /* momentum-transfer nodes q_j = q_min + j (q_max - q_min)/(nq - 1)
+     * ("evenly spaced momentum transfer bins")                */
+    int32_t nq;
+    double q_min, q_max;
+    /* source spectrum sampled at ne energies E_k (keV, increasing) with
+     * weights phi_k >= 0 (the bin integral of Phi(E))        */
+    int32_t ne;
+    const double *energy_kev; /* host, [ne], copied */
+    const double *phi;        /* host, [ne], copied */
+    /* secondary mask: binary image [mask_nx][mask_ny] (1 = open) in the plane
+     * z = mask_z; cell (i, j) covers x in [m0x + i p, m0x + (i+1) p) with
+     * m0x = mask_cx - (0.5 mask_nx) p, likewise y            */
+    int32_t mask_nx, mask_ny;
+    double mask_z, mask_pitch, mask_cx, mask_cy;
+    const uint8_t *mask; /* host, [mask_nx][mask_ny], copied */
+    /* detector: pixel centres x_i = det_cx + ((i + 1/2) - det_nx/2) det_pitch,
+     * likewise y; plane z = det_z                            */
+    int32_t det_nx, det_ny;
+    double det_z, det_pitch, det_cx, det_cy;
+    int32_t energy_resolving; /* 0: g[dx][dy]; 1: g[dx][dy][ne]             */
+    double scale;             /* C_E, the calibration constant */
+} cacsi_geometry_desc;
+
+/* Validate `desc`, precompute the per-voxel / per-pixel / per-energy tables
+ * in fp64 (the offline part of the online/offline
+ * trade-off), bit-pack the mask and upload everything to `device`.
+ * Synchronous.  On success *out owns the device tables.
+ * Errors: CACSI_ERR_NULL (desc, out or a desc array NULL), CACSI_ERR_INVALID,
+ * CACSI_ERR_CUDA (no such device / not sm_100), CACSI_ERR_NOMEM.            */
+CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, int device, cacsi_geometry **out);
+
+/* Free the handle and its device tables (synchronises the device).  NULL ok. */
+CACSI_API void cacsi_geometry_destroy(cacsi_geometry *geom);
+
+/* Bytes of device workspace cacsi_iterate / cacsi_neg_loglik need (the caller
+ * allocates it; 256-byte aligned).  0 for a NULL handle.                    */
+CACSI_API size_t cacsi_workspace_bytes(const cacsi_geometry *geom);
+
+/* Sizes implied by the handle (elements, not bytes).  0 for NULL.           */
+CACSI_API size_t cacsi_object_size(const cacsi_geometry *geom);   /* ny*nz*nq            */
+CACSI_API size_t cacsi_detector_size(const cacsi_geometry *geom); /* det_nx*det_ny[*ne]  */
+
+/* Forward model g = A f  (Eq. 1; Alg. 1 computes the same sum,
+ * PAPER.md:129-153).  f: device [ny][nz][nq]; g: device, detector shape.
+ * Errors: CACSI_ERR_NULL, CACSI_ERR_CUDA, CACSI_ERR_NOMEM.                   */
+CACSI_API cacsi_status cacsi_forward(const cacsi_geometry *geom, const float *f, float *g, void *stream);
+
+/* Backward (adjoint) model b = A^T w  (Alg. 3).
+ * w: device, detector shape; b: device [ny][nz][nq].                        */
+CACSI_API cacsi_status cacsi_backward(const cacsi_geometry *geom, const float *w, float *b, void *stream);
+
+/* Penalized negative log-likelihood J(f) = L(f) + beta R(f)
+ * with L = sum_i (l_i + r_i) - y_i ln(l_i + r_i),
+ * l = A f (the constant sum ln y_i! is omitted), and
+ * R = sum_j sum_{k in N_j} (f_j - f_k)^2 / 2 over the 4-connected (y, z)
+ * neighbours within one q node (each unordered pair counted twice, as in
+ * Eq. 7).  Writes ONE double to DEVICE memory *out_dev (stream-ordered,
+ * deterministic).  ws: device workspace of cacsi_workspace_bytes() bytes.   */
+CACSI_API cacsi_status cacsi_neg_loglik(const cacsi_geometry *geom, const float *f, const float *y, const float *r,
+                              float beta, double *out_dev, void *ws, void *stream);
+
+/* n_iter iterations of the EM-type algorithm (Alg. 5),
+ * updating f IN PLACE:
+ *   z = A f + r;  b2 = A^T (y ./ z);  f <- Eq. f_update
+ * with the quadratic potential psi(x) = x^2/2, 4-connected (y, z) neighbours,
+ * unit weights.  b1 = A^T 1 is supplied by the caller (computed once,
+ * PAPER.md:370).  Ratio guard: y/z = 0 where y = 0 and z = 0, y / 1e-12
+ * where z = 0 < y.  f must be >= 0 on entry and stays >= 0.
+ * ws: device workspace of cacsi_workspace_bytes() bytes.                    */
+CACSI_API cacsi_status cacsi_iterate(const cacsi_geometry *geom, float *f, const float *y, const float *r,
+                           const float *b1, float beta, int32_t n_iter, void *ws, void *stream);
+
+/* End-to-end variants on HOST buffers (pageable or pinned): copy the inputs
+ * to device scratch owned by the handle, run the device call, copy the output
+ * back, and synchronise `stream` before returning.  Same shapes as above.
+ * Not re-entrant on one handle (they share the handle's staging buffers).   */
+CACSI_API cacsi_status cacsi_forward_host(const cacsi_geometry *geom, const float *f_host, float *g_host, void *stream);
+CACSI_API cacsi_status cacsi_backward_host(const cacsi_geometry *geom, const float *w_host, float *b_host, void *stream);
+CACSI_API cacsi_status cacsi_iterate_host(const cacsi_geometry *geom, float *f_host, const float *y_host,
+                                const float *r_host, const float *b1_host, float beta, int32_t n_iter,
+                                void *stream);
+
+/* Number of kernels the last successful device call on this handle enqueued
+ * (for the bench's gpu_launches count).                                     */
+CACSI_API int32_t cacsi_last_launch_count(const cacsi_geometry *geom);
+
+/* Static description of a status code (never NULL). */
+CACSI_API const char *cacsi_status_string(cacsi_status status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CACSI_H */

@@ -1,0 +1,367 @@
+// api.cu -- C ABI entry points and host setup.
+//
+// Host setup = the offline half of the paper's online/offline trade-off
+// (PAPER.md:236-241): per-voxel G_so, r^ and mask-plane parameters, per-pixel
+// centres, per-energy constants and the bit-packed mask are computed ONCE in
+// fp64 and uploaded; everything per pair is computed online by the kernels.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+using cacsi::Params;
+using cacsi::VoxelRec;
+
+namespace {
+
+// Voxel / pixel centres, exactly the op order of DESIGN.md reading R9 (the
+// fp64 guard path of the mask rule depends on bit-identical coordinates).
+double centre(double lo, double hi, int n, int i) {
+    double pitch = (hi - lo) / n;
+    return lo + (i + 0.5) * pitch;
+}
+double det_centre(double c, int n, double p, int i) { return c + ((i + 0.5) - 0.5 * n) * p; }
+
+cacsi_status validate(const cacsi_geometry_desc *d) {
+    if (!d->energy_kev || !d->phi || !d->mask) return CACSI_ERR_NULL;
+    if (d->ny < 1 || d->nz < 1 || d->nq < 2 || d->ne < 1 || d->mask_nx < 1 || d->mask_ny < 1 || d->det_nx < 1 ||
+        d->det_ny < 1)
+        return CACSI_ERR_INVALID;
+    if (d->ne > 256 || d->nq > 400) return CACSI_ERR_INVALID;  // shared-memory tables
+    if (!(d->y_min < d->y_max) || !(0.0 < d->z_min) || !(d->z_min < d->z_max) || !(d->z_max < d->mask_z) ||
+        !(d->mask_z < d->det_z))
+        return CACSI_ERR_INVALID;
+    if (!(d->q_min < d->q_max) || !(d->mask_pitch > 0.0) || !(d->det_pitch > 0.0)) return CACSI_ERR_INVALID;
+    if (!(d->scale > 0.0) || !std::isfinite(d->scale)) return CACSI_ERR_INVALID;
+    if (d->energy_resolving != 0 && d->energy_resolving != 1) return CACSI_ERR_INVALID;
+    for (int k = 0; k < d->ne; k++) {
+        if (!(d->energy_kev[k] > 0.0) || !std::isfinite(d->energy_kev[k])) return CACSI_ERR_INVALID;
+        if (k > 0 && !(d->energy_kev[k] > d->energy_kev[k - 1])) return CACSI_ERR_INVALID;
+        if (!(d->phi[k] >= 0.0) || !std::isfinite(d->phi[k])) return CACSI_ERR_INVALID;
+    }
+    size_t nm = (size_t)d->mask_nx * d->mask_ny;
+    for (size_t i = 0; i < nm; i++)
+        if (d->mask[i] > 1) return CACSI_ERR_INVALID;
+    const double v[] = {d->y_min, d->y_max, d->z_min, d->z_max, d->q_min, d->q_max, d->mask_z, d->mask_pitch,
+                        d->mask_cx, d->mask_cy, d->det_z, d->det_pitch, d->det_cx, d->det_cy};
+    for (double x : v)
+        if (!std::isfinite(x)) return CACSI_ERR_INVALID;
+    return CACSI_OK;
+}
+
+template <class T>
+cudaError_t upload(void **dst, const std::vector<T> &src) {
+    cudaError_t e = cudaMalloc(dst, src.size() * sizeof(T));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+cacsi_status map_err(cudaError_t e) {
+    if (e == cudaSuccess) return CACSI_OK;
+    if (e == cudaErrorMemoryAllocation) return CACSI_ERR_NOMEM;
+    return CACSI_ERR_CUDA;
+}
+
+void free_all(cacsi_geometry *g) {
+    void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
+                    g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
+                    g->d_stage_d, g->d_stage_ws};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *cacsi_status_string(cacsi_status s) {
+    switch (s) {
+        case CACSI_OK: return "ok";
+        case CACSI_ERR_NULL: return "null pointer";
+        case CACSI_ERR_INVALID: return "invalid argument";
+        case CACSI_ERR_CUDA: return "CUDA error";
+        case CACSI_ERR_NOMEM: return "out of memory";
+    }
+    return "unknown status";
+}
+
+cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cacsi_geometry **out) {
+    if (!d || !out) return CACSI_ERR_NULL;
+    *out = nullptr;
+    cacsi_status st = validate(d);
+    if (st != CACSI_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return CACSI_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return CACSI_ERR_CUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return CACSI_ERR_CUDA;
+
+    cacsi_geometry *g = (cacsi_geometry *)calloc(1, sizeof(cacsi_geometry));
+    if (!g) return CACSI_ERR_NOMEM;
+    g->device = device;
+    g->ny = d->ny;
+    g->nz = d->nz;
+    g->nq = d->nq;
+    g->ne = d->ne;
+    g->det_nx = d->det_nx;
+    g->det_ny = d->det_ny;
+    g->energy_resolving = d->energy_resolving;
+    const int nvox = d->ny * d->nz, ndet = d->det_nx * d->det_ny;
+    g->n_obj = (size_t)nvox * d->nq;
+    g->n_detout = (size_t)ndet * (d->energy_resolving ? d->ne : 1);
+
+    Params &p = g->p;
+    p.ny = d->ny;
+    p.nz = d->nz;
+    p.nq = d->nq;
+    p.ne = d->ne;
+    p.det_nx = d->det_nx;
+    p.det_ny = d->det_ny;
+    p.n_vox = nvox;
+    p.n_det = ndet;
+    p.mask_nx = d->mask_nx;
+    p.mask_ny = d->mask_ny;
+    p.mask_words = (d->mask_ny + 31) / 32;
+    p.energy_resolving = d->energy_resolving;
+
+    const double mp = d->mask_pitch;
+    const double m0x = d->mask_cx - (0.5 * d->mask_nx) * mp;  // reading R8 op order
+    const double m0y = d->mask_cy - (0.5 * d->mask_ny) * mp;
+    const double dq = (d->q_max - d->q_min) / (d->nq - 1);
+    p.m0x = m0x;
+    p.m0y = m0y;
+    p.mask_pitch64 = mp;
+    p.det_z = (float)d->det_z;
+    p.pitch_d = (float)d->det_pitch;
+    p.quarter_p2 = (float)(0.25 * d->det_pitch * d->det_pitch);
+    p.ax = (float)(-m0x / mp);
+    const double beta0 = d->q_min / dq;
+    p.nb = (float)(-beta0 - 0.5);
+    p.qm = (float)(d->nq - 0.5);
+    p.klo_num = (float)(beta0 - 1.0);
+    p.khi_num = (float)(beta0 + d->nq);
+
+    // per-voxel tables
+    std::vector<VoxelRec> vox(nvox);
+    std::vector<double> vy(nvox), vz(nvox), vt(nvox);
+    for (int iy = 0; iy < d->ny; iy++)
+        for (int iz = 0; iz < d->nz; iz++) {
+            const int v = iy * d->nz + iz;
+            const double y = centre(d->y_min, d->y_max, d->ny, iy);
+            const double z = centre(d->z_min, d->z_max, d->nz, iz);
+            const double rn = std::sqrt(y * y + z * z);
+            const double t = (d->mask_z - z) / (d->det_z - z);  // reading R8 op order
+            VoxelRec &r = vox[v];
+            r.y = (float)y;
+            r.z = (float)z;
+            r.ry = (float)(y / rn);
+            r.rz = (float)(z / rn);
+            r.sz = (float)(d->det_z - z);
+            r.gso = (float)(z / (rn * rn * rn));  // G_so, PAPER.md:633 (config frame)
+            r.tq = (float)(t / mp);
+            r.ay = (float)((y * (1.0 - t) - m0y) / mp);
+            vy[v] = y;
+            vz[v] = z;
+            vt[v] = t;
+        }
+    // per-pixel tables
+    std::vector<float2> det(ndet);
+    std::vector<double> dx(ndet), dy(ndet);
+    for (int ix = 0; ix < d->det_nx; ix++)
+        for (int jy = 0; jy < d->det_ny; jy++) {
+            const int q = ix * d->det_ny + jy;
+            dx[q] = det_centre(d->det_cx, d->det_nx, d->det_pitch, ix);
+            dy[q] = det_centre(d->det_cy, d->det_ny, d->det_pitch, jy);
+            det[q] = make_float2((float)dx[q], (float)dy[q]);
+        }
+    // per-energy constants; uniform spacing enables the closed-form k range
+    std::vector<float2> en(d->ne);
+    for (int k = 0; k < d->ne; k++)
+        en[k] = make_float2((float)(d->energy_kev[k] / (cacsi::kHc * dq)),
+                            (float)(d->scale * d->phi[k] * d->energy_kev[k]));
+    p.uniform_e = 0;
+    if (d->ne >= 2) {
+        const double e0 = d->energy_kev[0], de = (d->energy_kev[d->ne - 1] - e0) / (d->ne - 1);
+        bool uni = de > 0;
+        for (int k = 0; k < d->ne && uni; k++)
+            if (std::fabs(d->energy_kev[k] - (e0 + k * de)) > 1e-9 * d->energy_kev[d->ne - 1]) uni = false;
+        if (uni) {
+            p.uniform_e = 1;
+            p.a0 = (float)(e0 / (cacsi::kHc * dq));
+            p.inv_da = (float)((cacsi::kHc * dq) / de);
+        }
+    }
+    // bit-packed mask: word w of row i holds cells (i, 32w .. 32w+31)
+    std::vector<uint32_t> bits((size_t)d->mask_nx * p.mask_words, 0u);
+    for (int i = 0; i < d->mask_nx; i++)
+        for (int j = 0; j < d->mask_ny; j++)
+            if (d->mask[(size_t)i * d->mask_ny + j]) bits[(size_t)i * p.mask_words + j / 32] |= 1u << (j % 32);
+
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = upload(&g->d_vox, vox);
+    if (e == cudaSuccess) e = upload(&g->d_vy64, vy);
+    if (e == cudaSuccess) e = upload(&g->d_vz64, vz);
+    if (e == cudaSuccess) e = upload(&g->d_vt64, vt);
+    if (e == cudaSuccess) e = upload(&g->d_det, det);
+    if (e == cudaSuccess) e = upload(&g->d_dx64, dx);
+    if (e == cudaSuccess) e = upload(&g->d_dy64, dy);
+    if (e == cudaSuccess) e = upload(&g->d_mask, bits);
+    if (e == cudaSuccess) e = upload(&g->d_energy, en);
+    if (e != cudaSuccess) {
+        free_all(g);
+        free(g);
+        cudaGetLastError();
+        return map_err(e);
+    }
+    p.vox = (const VoxelRec *)g->d_vox;
+    p.vy64 = (const double *)g->d_vy64;
+    p.vz64 = (const double *)g->d_vz64;
+    p.vt64 = (const double *)g->d_vt64;
+    p.det = (const float2 *)g->d_det;
+    p.dx64 = (const double *)g->d_dx64;
+    p.dy64 = (const double *)g->d_dy64;
+    p.maskbits = (const uint32_t *)g->d_mask;
+    p.energy = (const float2 *)g->d_energy;
+    *out = g;
+    return CACSI_OK;
+}
+
+void cacsi_geometry_destroy(cacsi_geometry *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    cudaDeviceSynchronize();
+    free_all(g);
+    free(g);
+}
+
+size_t cacsi_workspace_bytes(const cacsi_geometry *g) { return g ? cacsi::recon_workspace_bytes(g) : 0; }
+size_t cacsi_object_size(const cacsi_geometry *g) { return g ? g->n_obj : 0; }
+size_t cacsi_detector_size(const cacsi_geometry *g) { return g ? g->n_detout : 0; }
+int32_t cacsi_last_launch_count(const cacsi_geometry *g) { return g ? g->last_launches : 0; }
+
+cacsi_status cacsi_forward(const cacsi_geometry *g, const float *f, float *out, void *stream) {
+    if (!g || !f || !out) return CACSI_ERR_NULL;
+    int n = 0;
+    cudaError_t e = cacsi::launch_forward(g, f, out, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_backward(const cacsi_geometry *g, const float *w, float *b, void *stream) {
+    if (!g || !w || !b) return CACSI_ERR_NULL;
+    int n = 0;
+    cudaError_t e = cacsi::launch_backward(g, w, b, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+// workspace layout (recon.cu: recon_workspace_bytes)
+static void ws_split(const cacsi_geometry *g, void *ws, float **l, float **b2, float **fnew, double **part) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    char *p = (char *)ws;
+    *l = (float *)p;
+    p += al(g->n_detout * sizeof(float));
+    *b2 = (float *)p;
+    p += al(g->n_obj * sizeof(float));
+    *fnew = (float *)p;
+    p += al(g->n_obj * sizeof(float));
+    *part = (double *)p;
+}
+
+cacsi_status cacsi_neg_loglik(const cacsi_geometry *g, const float *f, const float *y, const float *r, float beta,
+                              double *out_dev, void *ws, void *stream) {
+    if (!g || !f || !y || !r || !out_dev || !ws) return CACSI_ERR_NULL;
+    float *l, *b2, *fnew;
+    double *part;
+    ws_split(g, ws, &l, &b2, &fnew, &part);
+    cudaStream_t s = (cudaStream_t)stream;
+    int n = 0;
+    cudaError_t e = cacsi::launch_forward(g, f, l, s, &n);
+    if (e == cudaSuccess) e = cacsi::launch_loglik(g, l, y, r, f, beta, part, out_dev, s, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
+                           float beta, int32_t n_iter, void *ws, void *stream) {
+    if (!g || !f || !y || !r || !b1 || !ws) return CACSI_ERR_NULL;
+    if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
+    float *l, *b2, *fnew;
+    double *part;
+    ws_split(g, ws, &l, &b2, &fnew, &part);
+    cudaStream_t s = (cudaStream_t)stream;
+    int n = 0;
+    cudaError_t e = cudaSuccess;
+    for (int t = 0; t < n_iter && e == cudaSuccess; t++) {
+        e = cacsi::launch_forward(g, f, l, s, &n);                                   // z = A f (+ r below)
+        if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, &n);  // y ./ z
+        if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, &n);           // b2 = A^T (y ./ z)
+        if (e == cudaSuccess) e = cacsi::launch_update(g, f, b1, b2, beta, fnew, s, &n);  // Eq. f_update
+        if (e == cudaSuccess) e = cudaMemcpyAsync(f, fnew, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    }
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+// ---- host-buffer variants (end-to-end timing path) -------------------------
+static cudaError_t ensure_stage(const cacsi_geometry *gc) {
+    cacsi_geometry *g = const_cast<cacsi_geometry *>(gc);
+    cudaError_t e = cudaSuccess;
+    if (!g->d_stage_a) e = cudaMalloc((void **)&g->d_stage_a, g->n_obj * sizeof(float));
+    if (e == cudaSuccess && !g->d_stage_b) e = cudaMalloc((void **)&g->d_stage_b, g->n_detout * sizeof(float));
+    if (e == cudaSuccess && !g->d_stage_c) e = cudaMalloc((void **)&g->d_stage_c, g->n_detout * sizeof(float));
+    if (e == cudaSuccess && !g->d_stage_d) e = cudaMalloc((void **)&g->d_stage_d, g->n_obj * sizeof(float));
+    if (e == cudaSuccess && !g->d_stage_ws) e = cudaMalloc((void **)&g->d_stage_ws, cacsi::recon_workspace_bytes(g));
+    return e;
+}
+
+cacsi_status cacsi_forward_host(const cacsi_geometry *g, const float *fh, float *gh, void *stream) {
+    if (!g || !fh || !gh) return CACSI_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = ensure_stage(g);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    int n = 0;
+    if (e == cudaSuccess) e = cacsi::launch_forward(g, g->d_stage_a, g->d_stage_b, s, &n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(gh, g->d_stage_b, g->n_detout * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_backward_host(const cacsi_geometry *g, const float *wh, float *bh, void *stream) {
+    if (!g || !wh || !bh) return CACSI_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = ensure_stage(g);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, wh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
+    int n = 0;
+    if (e == cudaSuccess) e = cacsi::launch_backward(g, g->d_stage_b, g->d_stage_a, s, &n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bh, g->d_stage_a, g->n_obj * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float *yh, const float *rh,
+                                const float *b1h, float beta, int32_t n_iter, void *stream) {
+    if (!g || !fh || !yh || !rh || !b1h) return CACSI_ERR_NULL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = ensure_stage(g);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, yh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_c, rh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_d, b1h, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return map_err(e);
+    cacsi_status st = cacsi_iterate(g, g->d_stage_a, g->d_stage_b, g->d_stage_c, g->d_stage_d, beta, n_iter,
+                                    g->d_stage_ws, stream);
+    if (st != CACSI_OK) return st;
+    e = cudaMemcpyAsync(fh, g->d_stage_a, g->n_obj * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return map_err(e);
+}
+
+}  // extern "C"

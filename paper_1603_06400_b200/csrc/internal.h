@@ -1,0 +1,83 @@
+// internal.h -- library-private types of libcacsi (not shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cacsi.h"
+
+namespace cacsi {
+
+constexpr double kHc = 12.3984193;          // keV Angstrom
+constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
+constexpr int kMagicBits = 0x4B400000;       // __float_as_int(kMagic)
+constexpr float kMaskGuard = 5e-4f;          // mask-cell guard band, cells (K2)
+
+// fp32 per-voxel record (32 B, two float4 loads).  All derived in fp64 on the
+// host from the descriptor ("precompute G_so").
+struct alignas(16) VoxelRec {
+    float y, z;    // centre (config frame)
+    float ry, rz;  // r^ = r / |r|
+    float sz;      // det_z - z  (> 0 by validation)
+    float gso;     // G_so = z / |r|^3
+    float tq;      // t / mask_pitch,  t = (mask_z - z) / (det_z - z)
+    float ay;      // (y (1 - t) - m0y) / mask_pitch: u_y = tq * y_d + ay
+};
+
+// Everything a kernel needs, passed by value (lives in the constant bank).
+struct Params {
+    int ny, nz, nq, ne;
+    int det_nx, det_ny;
+    int n_vox, n_det;
+    int mask_nx, mask_ny, mask_words;  // mask_words = 32-bit words per mask row (x)
+    int energy_resolving;
+    int uniform_e;                     // energies uniformly spaced -> closed-form k range
+    float det_z;
+    float pitch_d;                     // detector pitch p
+    float quarter_p2;                  // p^2 / 4
+    float ax;                          // -m0x / mask_pitch: u_x = tq * x_d + ax
+    float nb;                          // -(q_min / dq) - 1/2   (u' = alpha_k sh + nb = u - 1/2)
+    float qm;                          // nq - 1/2               (clamp bound of u')
+    float klo_num, khi_num;            // (q_min/dq - 1), (q_min/dq + nq): alpha range numerators
+    float a0, inv_da;                  // alpha_k = a0 + k / inv_da when uniform_e
+    // fp64 guard path (exact oracle op order, reading R8)
+    double m0x, m0y, mask_pitch64;
+    // device tables
+    const VoxelRec *vox;
+    const double *vy64, *vz64, *vt64;  // voxel y, z, t in fp64
+    const float2 *det;                 // pixel (x, y) fp32
+    const double *dx64, *dy64;         // pixel x, y fp64
+    const uint32_t *maskbits;          // [mask_nx][mask_words], bit j of word w = cell (i, 32w + j)
+    const float2 *energy;              // (alpha_k, c_k): alpha_k = E_k/(hc dq), c_k = scale phi_k E_k
+};
+
+}  // namespace cacsi
+
+struct cacsi_geometry {
+    int device;
+    cacsi::Params p;
+    // copies of the descriptor scalars we need later
+    int32_t ny, nz, nq, ne, det_nx, det_ny, energy_resolving;
+    size_t n_obj, n_detout;
+    // device allocations (owned)
+    void *d_vox, *d_vy64, *d_vz64, *d_vt64, *d_det, *d_dx64, *d_dy64, *d_mask, *d_energy;
+    // host staging for the *_host entry points (device scratch)
+    float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
+    mutable int32_t last_launches;
+};
+
+namespace cacsi {
+
+// launchers (operators.cu / recon.cu).  Each returns a cudaError_t of the
+// first failing launch and adds the number of kernels enqueued to *launches.
+cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
+cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
+cudaError_t launch_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
+                         double *partials, int nblocks, cudaStream_t s, int *launches);
+cudaError_t launch_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2,
+                          float beta, float *f_new, cudaStream_t s, int *launches);
+cudaError_t launch_loglik(const cacsi_geometry *g, const float *l, const float *y, const float *r, const float *f,
+                          float beta, double *partials, double *out, cudaStream_t s, int *launches);
+size_t recon_workspace_bytes(const cacsi_geometry *g);
+
+}  // namespace cacsi

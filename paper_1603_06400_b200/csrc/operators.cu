@@ -1,0 +1,254 @@
+// operators.cu -- forward g = A f and backward b = A^T w (SURVEY.md §8 rows
+// a3, a4), direct per-term SIMT path for both detector modes.
+//
+// Forward (PAPER.md:129-153 computes the same sum): output-stationary, one
+// thread per detector pixel, voxels streamed in chunks whose q-profiles are
+// staged in shared memory as a zero-padded hat table (value at the midpoint,
+// slope) so each energy term is one LDS.64 + two FMAs; no atomics.  Voxels
+// are split across CTAs (split-K) and the partial images are summed in fp64
+// in a fixed order by a second kernel (deterministic).
+//
+// Backward: voxel-stationary, one CTA per voxel gathering
+// over its whole detector footprint; each thread owns a private column of a
+// [nq+4][threads] shared-memory histogram (bank = lane, conflict-free, no
+// atomics); the columns are summed in fp64 at the end.
+#include <cstdio>
+
+#include "pair.cuh"
+
+namespace cacsi {
+
+namespace {
+
+constexpr int FWD_T = 128;  // pixels per CTA
+constexpr int FWD_VC = 16;  // voxels per shared-memory chunk
+constexpr int BWD_T = 128;  // threads per voxel CTA
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- forward --
+template <bool RES>
+__global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *__restrict__ f, int vox_per_split,
+                                                   void *__restrict__ partial) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne, Q3 = Q + 3;
+    float2 *en = (float2 *)smem4;          // [K] (alpha_k, c_k)
+    float2 *tab = en + ((K + 1) & ~1);     // [VC][Q + 3] (mid, slope), entry n at index n + 2
+    float *acc_s = (float *)(tab + FWD_VC * Q3 + (FWD_VC * Q3 & 1));  // RES: [K][FWD_T]
+    const int tid = threadIdx.x;
+    const int pix = blockIdx.x * FWD_T + tid;
+    const bool valid = pix < p.n_det;
+    const float2 d = p.det[valid ? pix : 0];
+    const int v0 = blockIdx.y * vox_per_split;
+    const int v1 = min(p.n_vox, v0 + vox_per_split);
+    for (int k = tid; k < K; k += FWD_T) en[k] = p.energy[k];
+    if (RES)
+        for (int k = 0; k < K; k++) acc_s[k * FWD_T + tid] = 0.0f;
+    double tot = 0.0;
+    for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
+        const int nc = min(FWD_VC, v1 - c0);
+        __syncthreads();
+        for (int i = tid; i < nc * Q3; i += FWD_T) {
+            const int vv = i / Q3, n = i - vv * Q3 - 2;
+            const float *fr = f + (size_t)(c0 + vv) * Q;
+            const float a = (n >= 0 && n < Q) ? fr[n] : 0.0f;
+            const float b = (n + 1 >= 0 && n + 1 < Q) ? fr[n + 1] : 0.0f;
+            tab[i] = make_float2(0.5f * (a + b), b - a);
+        }
+        __syncthreads();
+        float csum = 0.0f;
+        for (int vv = 0; vv < nc; vv++) {
+            const int v = c0 + vv;
+            const VoxelRec vr = p.vox[v];
+            const bool open = valid && mask_open(p, v, pix, vr, d);
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1;
+            if (open) {
+                pair_geom(p, vr, d, P, sh);
+                k_range(p, sh, klo, khi);
+            }
+            const int wlo = __reduce_min_sync(FULL, klo);
+            const int whi = __reduce_max_sync(FULL, khi);
+            const float2 *tv = tab + vv * Q3 + 2;
+            if (!RES) {
+                float ap = 0.0f;  // sum_k c_k f~(u_k) of this pair
+                for (int k = wlo; k <= whi; k++) {
+                    const float2 e = en[k];
+                    float tt;
+                    const int n = hat_coord(p, e.x, sh, tt);
+                    const float2 t = tv[n];
+                    ap = fmaf(e.y, fmaf(tt, t.y, t.x), ap);
+                }
+                csum = fmaf(P, ap, csum);
+            } else {
+                for (int k = wlo; k <= whi; k++) {
+                    float tt;
+                    const int n = hat_coord(p, en[k].x, sh, tt);
+                    const float2 t = tv[n];
+                    float *a = acc_s + k * FWD_T + tid;
+                    *a = fmaf(P, fmaf(tt, t.y, t.x), *a);
+                }
+            }
+        }
+        tot += (double)csum;
+    }
+    if (!RES) {
+        if (valid) ((double *)partial)[(size_t)blockIdx.y * p.n_det + pix] = tot;
+    } else {
+        __syncthreads();
+        // coalesced store of this CTA's [pixels][K] block, scaled by c_k
+        float *out = (float *)partial + ((size_t)blockIdx.y * p.n_det + (size_t)blockIdx.x * FWD_T) * K;
+        const int npx = min(FWD_T, p.n_det - (int)blockIdx.x * FWD_T);
+        for (int i = tid; i < npx * K; i += FWD_T) {
+            const int px = i / K, k = i - px * K;
+            out[i] = en[k].y * acc_s[k * FWD_T + px];
+        }
+    }
+}
+
+__global__ void k_sum_f64(const double *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < S; j++) s += part[j * n + i];
+        out[i] = (float)s;
+    }
+}
+
+__global__ void k_sum_f32(const float *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < S; j++) s += (double)part[j * n + i];
+        out[i] = (float)s;
+    }
+}
+
+// --------------------------------------------------------------- backward --
+template <bool RES>
+__global__ void __launch_bounds__(BWD_T) k_backward(const Params p, const float *__restrict__ w,
+                                                    float *__restrict__ b) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne;
+    float2 *en = (float2 *)smem4;                  // [K]
+    float *hist = (float *)(en + ((K + 1) & ~1));  // [Q + 4][BWD_T]; bin = node + 2
+    const int tid = threadIdx.x;
+    const int v = blockIdx.x;
+    for (int k = tid; k < K; k += BWD_T) en[k] = p.energy[k];
+    for (int i = tid; i < (Q + 4) * BWD_T; i += BWD_T) hist[i] = 0.0f;
+    __syncthreads();
+    const VoxelRec vr = p.vox[v];
+    float *hb = hist + tid;
+    const int nd_round = (p.n_det + BWD_T - 1) / BWD_T * BWD_T;
+    for (int q = tid; q < nd_round; q += BWD_T) {
+        const bool valid = q < p.n_det;
+        const float2 d = p.det[valid ? q : 0];
+        const bool open = valid && mask_open(p, v, q, vr, d);
+        float P = 0.0f, sh = 1.0f;
+        int klo = K, khi = -1;
+        if (open) {
+            pair_geom(p, vr, d, P, sh);
+            k_range(p, sh, klo, khi);
+        }
+        const int wlo = __reduce_min_sync(FULL, klo);
+        const int whi = __reduce_max_sync(FULL, khi);
+        if (!RES) {
+            const float a = open ? P * w[q] : 0.0f;
+            for (int k = wlo; k <= whi; k++) {
+                const float2 e = en[k];
+                float tt;
+                const int n = hat_coord(p, e.x, sh, tt);
+                const float ca = e.y * a;
+                const float hi = fmaf(tt, ca, 0.5f * ca);
+                float *h0 = hb + (n + 2) * BWD_T;
+                h0[0] += ca - hi;
+                h0[BWD_T] += hi;
+            }
+        } else {
+            const float *wq = w + (size_t)(valid ? q : 0) * K;
+            for (int k = wlo; k <= whi; k++) {
+                const float2 e = en[k];
+                float tt;
+                const int n = hat_coord(p, e.x, sh, tt);
+                const float ca = (open && k >= klo && k <= khi) ? P * e.y * __ldg(wq + k) : 0.0f;
+                const float hi = fmaf(tt, ca, 0.5f * ca);
+                float *h0 = hb + (n + 2) * BWD_T;
+                h0[0] += ca - hi;
+                h0[BWD_T] += hi;
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < Q; j += BWD_T) {
+        const float *row = hist + (j + 2) * BWD_T;
+        double s = 0.0;
+        for (int t = 0; t < BWD_T; t++) s += (double)row[(t + j) % BWD_T];  // rotate: bank spread
+        b[(size_t)v * Q + j] = (float)s;
+    }
+}
+
+int num_sms(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    if (device >= 0 && device < 64) cached[device] = n;
+    return n;
+}
+
+}  // namespace
+
+cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
+    const Params &p = g->p;
+    const bool res = p.energy_resolving != 0;
+    const int tiles = (p.n_det + FWD_T - 1) / FWD_T;
+    const int target = 8 * num_sms(g->device);
+    int S = (target + tiles - 1) / tiles;
+    const int max_s = (p.n_vox + FWD_VC - 1) / FWD_VC;
+    if (res) S = max(S, (p.n_vox + 1023) / 1024);  // fp32 partial sums over <= 1024 voxels
+    S = max(1, min(S, max_s));
+    int vps = (p.n_vox + S - 1) / S;
+    vps = (vps + FWD_VC - 1) / FWD_VC * FWD_VC;
+    S = (p.n_vox + vps - 1) / vps;
+    const size_t n_out = (size_t)p.n_det * (res ? p.ne : 1);
+    const size_t part_bytes = (size_t)S * n_out * (res ? sizeof(float) : sizeof(double));
+    size_t smem = (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2);
+    if (res) smem += (size_t)p.ne * FWD_T * sizeof(float);
+    void *part = nullptr;
+    cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
+    if (e != cudaSuccess) return e;
+    dim3 grid(tiles, S);
+    if (res) {
+        cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_forward<true><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+    } else {
+        cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_forward<false><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+    }
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        const int nb = (int)min((n_out + 255) / 256, (size_t)(16 * num_sms(g->device)));
+        if (res)
+            k_sum_f32<<<nb, 256, 0, s>>>((const float *)part, S, n_out, out);
+        else
+            k_sum_f64<<<nb, 256, 0, s>>>((const double *)part, S, n_out, out);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(part, s);
+    *launches += 2;
+    return e;
+}
+
+cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
+    const Params &p = g->p;
+    const size_t smem =
+        (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
+    if (p.energy_resolving) {
+        cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+    } else {
+        cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_backward<false><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+    }
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace cacsi

@@ -1,0 +1,52 @@
+"""Quick CUDA-event timing of cacsi_forward / cacsi_backward per config (dev tool)."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1603_06400_b200 as P  # noqa: E402
+from workloads import make_config  # noqa: E402
+
+
+def time_op(fn, reps):
+    s = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(s)
+        fn()
+        b.record(s)
+    torch.cuda.synchronize()
+    return sorted(a.elapsed_time(b) for a, b in ev)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2")
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    out = {}
+    for ci in [int(c) for c in args.configs.split(",")]:
+        cfg = make_config(ci)
+        G = P.Geometry(cfg.desc())
+        f = torch.as_tensor(cfg.f).cuda()
+        g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+        w = torch.rand(G.g_shape, dtype=torch.float32, device="cuda")
+        b = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+        for _ in range(2):
+            G.forward(f, g)
+            G.backward(w, b)
+        tf = time_op(lambda: G.forward(f, g), args.reps)
+        tb = time_op(lambda: G.backward(w, b), args.reps)
+        pairs = cfg.n_vox * cfg.n_det
+        out[ci] = dict(fwd_ms=tf[len(tf) // 2], bwd_ms=tb[len(tb) // 2], pairs=pairs,
+                       fwd_pairs_per_s=pairs / tf[len(tf) // 2] * 1e3, bwd_pairs_per_s=pairs / tb[len(tb) // 2] * 1e3)
+        print(json.dumps({ci: out[ci]}), flush=True)
+        G.close()
+
+
+if __name__ == "__main__":
+    main()

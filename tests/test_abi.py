@@ -1,0 +1,99 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the
+header declares, and validates descriptors before touching a device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1603_06400_b200 as P
+from paper_1603_06400_b200 import binding
+from workloads import make_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    h = open(os.path.join(ROOT, "include", "cacsi.h")).read()
+    return sorted(set(re.findall(r"CACSI_API[^;(]*?\b(cacsi_\w+)\s*\(", h)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for name in ("cacsi_geometry_create", "cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = P.lib()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert sorted(binding.SYMBOLS) == declared_symbols()
+
+
+def test_status_strings():
+    assert P.status_string(0) == "ok"
+    assert P.status_string(2) == "invalid argument"
+    assert P.status_string(99) == "unknown status"
+
+
+def _desc(**over):
+    d = make_config(0).desc()
+    d.update(over)
+    return d
+
+
+def _create(d):
+    g = binding.GeometryDesc()
+    e = np.ascontiguousarray(d["energy_kev"], np.float64)
+    ph = np.ascontiguousarray(d["phi"], np.float64)
+    m = np.ascontiguousarray(d["mask"], np.uint8)
+    for name, _ in binding.GeometryDesc._fields_:
+        if name not in ("energy_kev", "phi", "mask"):
+            setattr(g, name, d[name])
+    g.energy_kev = e.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    g.phi = ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    g.mask = m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    h = ctypes.c_void_p()
+    st = P.lib().cacsi_geometry_create(ctypes.byref(g), 0, ctypes.byref(h))
+    if st == 0:
+        P.lib().cacsi_geometry_destroy(h)
+    return st
+
+
+@pytest.mark.parametrize("over", [
+    dict(ny=0), dict(nq=1), dict(nq=401), dict(ne=300, energy_kev=np.linspace(20, 150, 300), phi=np.ones(300)),
+    dict(z_min=-1.0), dict(z_max=900.0), dict(mask_z=1200.0), dict(det_pitch=0.0), dict(mask_pitch=-1.0),
+    dict(q_max=0.01), dict(scale=0.0), dict(energy_resolving=2),
+    dict(energy_kev=np.array([30, 40, 40, 50, 60, 70, 80, 90.0])),
+    dict(phi=-np.ones(8)), dict(y_min=9.0),
+])
+def test_invalid_descriptors_rejected(over):
+    assert _create(_desc(**over)) == binding.CACSI_ERR_INVALID
+
+
+def test_invalid_mask_byte_rejected():
+    d = _desc()
+    m = d["mask"].copy()
+    m[3, 4] = 2
+    d["mask"] = m
+    assert _create(d) == binding.CACSI_ERR_INVALID
+
+
+def test_null_pointers():
+    L = P.lib()
+    assert L.cacsi_geometry_create(None, 0, None) == binding.CACSI_ERR_NULL
+    assert L.cacsi_forward(None, None, None, None) == binding.CACSI_ERR_NULL
+    assert L.cacsi_backward(None, None, None, None) == binding.CACSI_ERR_NULL
+    assert L.cacsi_iterate(None, None, None, None, None, 0.0, 1, None, None) == binding.CACSI_ERR_NULL
+    assert L.cacsi_neg_loglik(None, None, None, None, 0.0, None, None, None) == binding.CACSI_ERR_NULL
+    assert L.cacsi_workspace_bytes(None) == 0
+    L.cacsi_geometry_destroy(None)
+
+
+def test_no_device_is_an_error_not_a_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    assert _create(_desc()) == binding.CACSI_ERR_CUDA

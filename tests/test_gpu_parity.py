@@ -1,0 +1,235 @@
+"""GPU parity: libcacsi (C ABI, CUDA sm_100a) vs the fp64 oracle on the same
+seeded inputs.  Tolerances (north_star):
+  relative L2 <= 1e-5, and max relative <= 1e-4 over entries with
+  |ref| >= 1e-3 * max|ref| (the floor below which fp32 hat weights cannot
+  carry 1e-4 relative accuracy).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import recon
+from workloads import make_config, poisson_data
+from workloads.configs import seeded_rng
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_1603_06400_b200")
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-5
+MAX_REL = 1e-4
+FLOOR = 1e-3
+
+
+def rel_l2(x, ref):
+    ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(np.asarray(x, np.float64) - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def max_rel(x, ref, floor=FLOOR):
+    ref = np.asarray(ref, np.float64).ravel()
+    x = np.asarray(x, np.float64).ravel()
+    sel = np.abs(ref) >= floor * np.abs(ref).max()
+    return float((np.abs(x[sel] - ref[sel]) / np.abs(ref[sel])).max())
+
+
+def assert_parity(x, ref, what, l2=REL_L2, mr=MAX_REL):
+    e2, em = rel_l2(x, ref), max_rel(x, ref)
+    print(f"{what}: rel_l2={e2:.3e} max_rel={em:.3e}")
+    assert e2 <= l2, f"{what}: rel L2 {e2:.3e} > {l2}"
+    assert em <= mr, f"{what}: max rel {em:.3e} > {mr}"
+
+
+def cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def gpu_forward(G, f):
+    g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+    G.forward(cuda(f), g)
+    torch.cuda.synchronize()
+    return g.cpu().numpy()
+
+
+def gpu_backward(G, w):
+    b = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+    G.backward(cuda(w), b)
+    torch.cuda.synchronize()
+    return b.cpu().numpy()
+
+
+def geoms(cfg_or_desc, **over):
+    d = cfg_or_desc.desc() if hasattr(cfg_or_desc, "desc") else dict(cfg_or_desc)
+    d.update(over)
+    return P.Geometry(d), oracle.Geometry(d)
+
+
+def rnd(shape, seed, stream):
+    # fp32-rounded once; the oracle consumes the same values upcast to fp64
+    return seeded_rng(seed, stream).random(shape).astype(np.float32)
+
+
+# ------------------------------------------------------------ full parity --
+@pytest.mark.parametrize("er", [0, 1])
+def test_config0_forward_backward(er):
+    cfg = make_config(0, energy_resolving=er)
+    G, O = geoms(cfg)
+    assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), f"c0 er={er} forward")
+    w = rnd(G.g_shape, 0, 10 + er)
+    assert_parity(gpu_backward(G, w), O.backward(w), f"c0 er={er} backward")
+
+
+def test_config1_forward_backward():
+    cfg = make_config(1)
+    G, O = geoms(cfg)
+    assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), "c1 forward")
+    w = rnd(G.g_shape, 1, 10)
+    assert_parity(gpu_backward(G, w), O.backward(w), "c1 backward")
+
+
+@pytest.mark.parametrize("over", [
+    # ragged: pixel tile / warp / chunk tails, odd nq, tiny grids
+    dict(ny=5, nz=7, nq=13, det_nx=9, det_ny=23),
+    dict(ny=1, nz=1, det_nx=1, det_ny=1),
+    dict(ny=3, nz=33, nq=2, det_nx=17, det_ny=31),
+    # non-uniform energies: exercises the full-range k loop
+    dict(energy_kev=np.array([30.0, 33.0, 41.0, 55.0, 60.0, 80.0, 101.0, 119.0])),
+    # q grid narrower than the Bragg reach: both tails zero-padded
+    dict(q_min=0.15, q_max=0.25, nq=9),
+    # q grid wider than the reach (all u inside)
+    dict(q_min=0.0, q_max=0.9, nq=40),
+])
+def test_ragged_and_edge_geometries(over):
+    cfg = make_config(0)
+    d = cfg.desc()
+    d.update(over)
+    G, O = geoms(d)
+    f = rnd(G.f_shape, 0, 20)
+    w = rnd(G.g_shape, 0, 21)
+    assert_parity(gpu_forward(G, f), O.forward(f), f"ragged {over} forward")
+    assert_parity(gpu_backward(G, w), O.backward(w), f"ragged {over} backward")
+
+
+def test_energy_resolving_ragged():
+    cfg = make_config(0, energy_resolving=1)
+    d = cfg.desc()
+    d.update(ny=6, nz=5, nq=21, det_nx=7, det_ny=19)
+    G, O = geoms(d)
+    f, w = rnd(G.f_shape, 0, 22), rnd(G.g_shape, 0, 23)
+    assert_parity(gpu_forward(G, f), O.forward(f), "er ragged forward")
+    assert_parity(gpu_backward(G, w), O.backward(w), "er ragged backward")
+
+
+def test_all_closed_mask_and_zero_input():
+    cfg = make_config(0)
+    d = cfg.desc()
+    d["mask"] = np.zeros_like(d["mask"])
+    G, _ = geoms(d)
+    assert (gpu_forward(G, cfg.f) == 0).all()
+    assert (gpu_backward(G, np.ones(G.g_shape, np.float32)) == 0).all()
+    G2, _ = geoms(cfg)
+    assert (gpu_forward(G2, np.zeros(G2.f_shape, np.float32)) == 0).all()
+
+
+# ----------------------------------------- full-size configs, sampled outputs --
+def _sample(n, k, seed):
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(n, size=min(k, n), replace=False)
+    return np.unique(np.concatenate([idx, [0, n - 1]]))
+
+
+@pytest.mark.parametrize("ci,npix,nvox", [(2, 160, 24), (4, 24, 4)])
+def test_full_size_sampled(ci, npix, nvox):
+    """BASELINE.json full sizes in the bench's launch configuration; the oracle
+    computes sampled outputs one by one."""
+    cfg = make_config(ci)
+    G, O = geoms(cfg)
+    g = gpu_forward(G, cfg.f).reshape(G.n_det // (cfg.ne if cfg.energy_resolving else 1), -1)
+    pix = _sample(cfg.n_det, npix, ci)
+    ref = O.forward_pixels(cfg.f, pix).reshape(pix.size, -1)
+    assert_parity(g[pix], ref, f"c{ci} forward sampled")
+    w = rnd(G.g_shape, ci, 10)
+    b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
+    vox = _sample(cfg.n_vox, nvox, ci + 100)
+    assert_parity(b[vox], O.backward_voxels(w, vox), f"c{ci} backward sampled")
+
+
+# --------------------------------------------------------------- adjoint --
+@pytest.mark.parametrize("ci", [1, 2])
+def test_adjoint_gpu(ci):
+    cfg = make_config(ci)
+    G, _ = geoms(cfg)
+    x = rnd(G.f_shape, ci, 30)
+    y = rnd(G.g_shape, ci, 31)
+    lhs = np.vdot(gpu_forward(G, x).astype(np.float64), y.astype(np.float64))
+    rhs = np.vdot(x.astype(np.float64), gpu_backward(G, y).astype(np.float64))
+    assert abs(lhs - rhs) <= 2e-6 * abs(lhs)
+
+
+# ------------------------------------------------ reconstruction (config 3) --
+@pytest.fixture(scope="module")
+def config3():
+    cfg = make_config(3)
+    O0 = oracle.Geometry(cfg)
+    f_true = cfg.f.astype(np.float64)
+    y, r, s = poisson_data(O0.forward(f_true), seed=3)
+    d = cfg.desc()
+    d["scale"] = s
+    O = oracle.Geometry(d)
+    G = P.Geometry(d)
+    b1 = O.backward(np.ones(O.g_shape))
+    return cfg, d, O, G, y, r, b1, s
+
+
+def test_config3_b1_and_iterates(config3):
+    cfg, d, O, G, y, r, b1_ref, s = config3
+    ones = torch.ones(G.g_shape, dtype=torch.float32, device="cuda")
+    b1 = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+    G.backward(ones, b1)
+    assert_parity(b1.cpu().numpy(), b1_ref, "c3 b1")
+    beta = 1e-3
+    f0 = np.full(G.f_shape, (y - r).sum() / b1_ref.sum(), dtype=np.float32)
+    ref_iters = recon.em_iterate(O, f0, y, r, b1_ref.astype(np.float32), beta, 3)
+    f = cuda(f0)
+    ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
+    yt, rt = cuda(y), cuda(r)
+    for t in range(3):
+        G.iterate(f, yt, rt, b1, beta, 1, ws)
+        torch.cuda.synchronize()
+        assert_parity(f.cpu().numpy(), ref_iters[t], f"c3 iterate {t + 1}", l2=1e-5 * (t + 1), mr=1e-4 * (t + 1))
+
+
+def test_config3_neg_loglik(config3):
+    cfg, d, O, G, y, r, b1_ref, s = config3
+    f = cfg.f.astype(np.float32)
+    beta = 1e-3
+    ref = recon.objective(O.forward(f), y, r, f, beta)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
+    G.neg_loglik(cuda(f), cuda(y), cuda(r), beta, out, ws)
+    v1 = out.item()
+    G.neg_loglik(cuda(f), cuda(y), cuda(r), beta, out, ws)
+    assert out.item() == v1  # deterministic
+    assert v1 == pytest.approx(ref, rel=1e-6)
+
+
+def test_host_entry_points_match_device(config3):
+    cfg, d, O, G, y, r, b1_ref, s = config3
+    f = cfg.f.astype(np.float32)
+    g_dev = gpu_forward(G, f)
+    g_host = np.empty(G.g_shape, np.float32)
+    G.forward_host(f, g_host)
+    np.testing.assert_array_equal(g_host, g_dev)
+    b_host = np.empty(G.f_shape, np.float32)
+    G.backward_host(np.ones(G.g_shape, np.float32), b_host)
+    np.testing.assert_array_equal(b_host, gpu_backward(G, np.ones(G.g_shape, np.float32)))
+
+
+def test_deterministic_operators():
+    cfg = make_config(1)
+    G, _ = geoms(cfg)
+    a, b = gpu_forward(G, cfg.f), gpu_forward(G, cfg.f)
+    np.testing.assert_array_equal(a, b)
+    w = rnd(G.g_shape, 1, 40)
+    np.testing.assert_array_equal(gpu_backward(G, w), gpu_backward(G, w))
