@@ -1,0 +1,344 @@
+"""Benchmark of the hot path: one step = one iteration of Alg. 5
+on the config-2 geometry (BASELINE.json configs[2], the headline roofline
+config): forward g = A f, ratio y/(g + r), backward b2 = A^T ratio, closed-form
+update -- every stage a libcacsi kernel called through the C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+
+Metric (BASELINE.json): forward+backward pairs/s (2 * N_vox * N_det voxel-pixel
+pairs per step), with voxel-pixel-energy terms/s and the roofline fraction of
+the dominant kernel reported beside it.  Multi-GPU: the path does not shard
+(north_star: one GPU, no collectives) -> N independent replicas, value =
+all ranks' pairs / max-over-ranks time, scaling "weak".
+
+--impl reference times the fp64 CPU oracle (the reference arm of this tier) on
+a bounded sample of the same workload, on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import make_config  # noqa: E402
+from workloads.configs import seeded_rng  # noqa: E402
+
+METRIC = "forward+backward pairs/s"
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="cacsi", choices=["cacsi", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0, help="target seconds of oracle work")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ work counts --
+def work_counts(cfg):
+    """Pairs and nominal terms per operator application."""
+    pairs = cfg.n_vox * cfg.n_det
+    return pairs, pairs * cfg.ne
+
+
+# ---------------------------------------------------------------- GPU arm --
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1603_06400_b200 as P
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    cfg = make_config(args.config)
+    if cfg.energy_resolving:
+        raise SystemExit("bench step is the energy-integrating EM iteration")
+    d = cfg.desc()
+    G0 = P.Geometry(d, device=local)
+    # synthetic Poisson data of the config-3 recipe on this geometry (input only)
+    f_true = torch.as_tensor(cfg.f).to(dev)
+    l_true = torch.empty(G0.g_shape, dtype=torch.float32, device=dev)
+    G0.forward(f_true, l_true)
+    torch.cuda.synchronize()
+    lt = l_true.double().cpu().numpy()
+    s = 1e4 / lt.mean()
+    y_np = seeded_rng(cfg.seed, 2).poisson(s * lt + 5.0).astype(np.float32)
+    r_np = np.full(G0.g_shape, 5.0, np.float32)
+    G0.close()
+    d["scale"] = s
+    G = P.Geometry(d, device=local)
+    y = torch.as_tensor(y_np).to(dev)
+    r = torch.as_tensor(r_np).to(dev)
+    ones = torch.ones(G.g_shape, dtype=torch.float32, device=dev)
+    b1 = torch.empty(G.f_shape, dtype=torch.float32, device=dev)
+    G.backward(ones, b1)
+    torch.cuda.synchronize()
+    f0 = float((y_np - r_np).sum() / b1.double().sum().item())
+    f = torch.full(G.f_shape, f0, dtype=torch.float32, device=dev)
+    l = torch.empty(G.g_shape, dtype=torch.float32, device=dev)
+    b2 = torch.empty(G.f_shape, dtype=torch.float32, device=dev)
+    fn = torch.empty(G.f_shape, dtype=torch.float32, device=dev)
+    beta = 1e-3
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    launches_per_step = [0]
+
+    def step(ev=None):
+        n = 0
+        if ev:
+            ev[0].record(stream)
+        G.forward(f, l)
+        n += G.last_launch_count
+        if ev:
+            ev[1].record(stream)
+        G.ratio(l, y, r, l)
+        n += G.last_launch_count
+        if ev:
+            ev[2].record(stream)
+        G.backward(l, b2)
+        n += G.last_launch_count
+        if ev:
+            ev[3].record(stream)
+        G.update(f, b1, b2, beta, fn)
+        n += G.last_launch_count
+        f.copy_(fn)  # torch copy kernel (not counted as ours)
+        if ev:
+            ev[4].record(stream)
+        launches_per_step[0] = n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [[E() for _ in range(5)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
+        step(evs[i])
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    t_fwd = [e[0].elapsed_time(e[1]) for e in evs]
+    t_bwd = [e[2].elapsed_time(e[3]) for e in evs]
+    t_step = [e[0].elapsed_time(e[4]) for e in evs]
+    total_ms = float(sum(t_step))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    ms_per_step = total_ms / args.steps
+    pairs, nominal_terms = work_counts(cfg)
+    units = 2 * pairs * args.steps * world
+    value = units / (total_ms / 1e3)
+
+    # ---- e2e: the same step through the host-buffer C ABI (pinned buffers)
+    fh = torch.full(G.f_shape, f0, dtype=torch.float32).pin_memory().numpy()
+    yh = torch.as_tensor(y_np).pin_memory().numpy()
+    rh = torch.as_tensor(r_np).pin_memory().numpy()
+    b1h = b1.cpu().pin_memory().numpy()
+    G.iterate_host(fh, yh, rh, b1h, beta, 1)  # warm the staging buffers
+    e2e_ms = []
+    for i in range(max(1, min(args.steps, 5))):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        G.iterate_host(fh, yh, rh, b1h, beta, 1)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_value = 2 * pairs * world / (np.mean(e2e_ms) / 1e3)
+    h2d = (fh.nbytes + yh.nbytes + rh.nbytes + b1h.nbytes)
+    d2h = fh.nbytes
+
+    # ---- roofline of the dominant kernel
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    mf, mb = float(np.mean(t_fwd)), float(np.mean(t_bwd))
+    eff = effective_terms(cfg)
+    dom = "backward" if mb >= mf else "forward"
+    flops_per_term = {"forward": 7.0, "backward": 9.0}[dom]
+    achieved = eff * flops_per_term / ((mb if dom == "backward" else mf) / 1e3) / 1e12
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_tf = sms * 128 * 2 * 1965e6 / 1e12  # FP32 lanes x FMA x max SM clock
+    roofline = {"bound": "alu", "kernel": f"cacsi_{dom}", "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": None,
+                "peak_note": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz (max clock); "
+                             f"{flops_per_term:g} algorithmic flops per effective term"}
+    if ck.get("sm_mhz"):
+        roofline["frac_at_observed_clock"] = round(achieved / (peak_tf * ck["sm_mhz"] / 1965.0), 4)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_vox": cfg.n_vox, "n_det": cfg.n_det, "nq": cfg.nq, "ne": cfg.ne,
+                   "step": "Alg.5 iteration: forward, ratio, backward, update (beta=1e-3)",
+                   "pairs_per_step": 2 * pairs, "l2": "flushed (256 MB write) between timed steps",
+                   "parallelism": f"replicas x{world}"},
+        "forward_ms": mf, "backward_ms": mb,
+        "forward_pairs_per_s": pairs / (mf / 1e3), "backward_pairs_per_s": pairs / (mb / 1e3),
+        "nominal_terms_per_s": 2 * nominal_terms * world / (ms_per_step / 1e3),
+        "effective_terms_per_s": 2 * eff * world / (ms_per_step / 1e3),
+        "gpu_launches": launches_per_step[0] * args.steps,
+        "clocks": ck, "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": float(np.mean(e2e_ms))},
+        "peaks_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_s)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    G.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def effective_terms(cfg) -> float:
+    """Effective terms (open pair x energy with -1 < u_k < nq) per operator
+    application: exact counts written by scripts/count_terms.py from the
+    oracle's counter (workloads/work_counts.json)."""
+    counts = json.load(open(os.path.join(ROOT, "workloads", "work_counts.json")))
+    return float(counts[str(cfg.seed if cfg.seed in (0, 1, 2, 4) else 1)]["effective_terms"])
+
+
+# --------------------------------------------------------- CPU (oracle) arm --
+def _oracle_sample(cfg, budget_s):
+    """Time the oracle's forward on a pixel sample and backward on a voxel sample,
+    sized to ~budget_s seconds on this host's cores.  Returns (pairs, seconds, desc)."""
+    import oracle
+    O = oracle.Geometry(cfg)
+    f = cfg.f.astype(np.float64)
+    w = np.ones(O.g_shape)
+    rng = np.random.default_rng(0)
+    # calibrate on a tiny sample
+    pix = rng.choice(cfg.n_det, 64, replace=False)
+    t0 = time.perf_counter()
+    O.forward_pixels(f, pix)
+    per_pix = (time.perf_counter() - t0) / 64
+    npix = int(max(64, min(cfg.n_det, 0.5 * budget_s / max(per_pix, 1e-9))))
+    vox_cost = per_pix * cfg.n_det / cfg.n_vox
+    nvox = int(max(8, min(cfg.n_vox, 0.5 * budget_s / max(vox_cost, 1e-9))))
+    pix = rng.choice(cfg.n_det, npix, replace=False)
+    vox = rng.choice(cfg.n_vox, nvox, replace=False)
+    t0 = time.perf_counter()
+    O.forward_pixels(f, pix)
+    t1 = time.perf_counter()
+    O.backward_voxels(w, vox)
+    t2 = time.perf_counter()
+    pairs = npix * cfg.n_vox + nvox * cfg.n_det
+    return pairs, t2 - t0, f"forward on {npix} random pixels x all {cfg.n_vox} voxels + backward on {nvox} " \
+                          f"random voxels x all {cfg.n_det} pixels of {cfg.name} ({t1 - t0:.1f}s + {t2 - t1:.1f}s)"
+
+
+def cpu_baseline(cfg, budget_s):
+    pairs, secs, desc = _oracle_sample(cfg, budget_s)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": pairs / secs, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    cfg = make_config(args.config)
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        _oracle_sample(cfg, budget)
+    tot_pairs, tot_s, desc = 0, 0.0, ""
+    for _ in range(args.steps):
+        p, s, desc = _oracle_sample(cfg, budget)
+        tot_pairs += p
+        tot_s += s
+    value = tot_pairs / tot_s
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": cfg.name, "n_vox": cfg.n_vox, "n_det": cfg.n_det, "nq": cfg.nq, "ne": cfg.ne},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_gpu(a)

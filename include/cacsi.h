@@ -155,6 +155,17 @@ CACSI_API cacsi_status cacsi_neg_loglik(const cacsi_geometry *geom, const float 
 CACSI_API cacsi_status cacsi_iterate(const cacsi_geometry *geom, float *f, const float *y, const float *r,
                            const float *b1, float beta, int32_t n_iter, void *ws, void *stream);
 
+/* The two fused elementwise steps of Alg. 5, exposed for stage timing (the
+ * same kernels cacsi_iterate runs):
+ *   cacsi_ratio : ratio = y ./ (l + r) with the guard above (K4); detector
+ *                 shape; ratio may alias l.
+ *   cacsi_update: f_new = Eq. f_update(f_hat, b1, b2, beta) (K5); object
+ *                 shape; f_new must not alias f_hat.                        */
+CACSI_API cacsi_status cacsi_ratio(const cacsi_geometry *geom, const float *l, const float *y, const float *r,
+                                   float *ratio, void *stream);
+CACSI_API cacsi_status cacsi_update(const cacsi_geometry *geom, const float *f_hat, const float *b1, const float *b2,
+                                    float beta, float *f_new, void *stream);
+
 /* End-to-end variants on HOST buffers (pageable or pinned): copy the inputs
  * to device scratch owned by the handle, run the device call, copy the output
  * back, and synchronise `stream` before returning.  Same shapes as above.

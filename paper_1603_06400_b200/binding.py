@@ -23,7 +23,7 @@ CACSI_OK, CACSI_ERR_NULL, CACSI_ERR_INVALID, CACSI_ERR_CUDA, CACSI_ERR_NOMEM = r
 SYMBOLS = ["cacsi_geometry_create", "cacsi_geometry_destroy", "cacsi_workspace_bytes", "cacsi_object_size",
            "cacsi_detector_size", "cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate",
            "cacsi_forward_host", "cacsi_backward_host", "cacsi_iterate_host", "cacsi_last_launch_count",
-           "cacsi_status_string"]
+           "cacsi_status_string", "cacsi_ratio", "cacsi_update"]
 
 
 class CacsiError(RuntimeError):
@@ -74,10 +74,13 @@ def lib():
         L.cacsi_backward.argtypes = [vp, fp, fp, vp]
         L.cacsi_neg_loglik.argtypes = [vp, fp, fp, fp, ctypes.c_float, vp, vp, vp]
         L.cacsi_iterate.argtypes = [vp, fp, fp, fp, fp, ctypes.c_float, ctypes.c_int32, vp, vp]
+        L.cacsi_ratio.argtypes = [vp, fp, fp, fp, fp, vp]
+        L.cacsi_update.argtypes = [vp, fp, fp, fp, ctypes.c_float, fp, vp]
         L.cacsi_forward_host.argtypes = [vp, fp, fp, vp]
         L.cacsi_backward_host.argtypes = [vp, fp, fp, vp]
         L.cacsi_iterate_host.argtypes = [vp, fp, fp, fp, fp, ctypes.c_float, ctypes.c_int32, vp]
         for n in ("cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate", "cacsi_forward_host",
+                  "cacsi_ratio", "cacsi_update",
                   "cacsi_backward_host", "cacsi_iterate_host"):
             getattr(L, n).restype = ctypes.c_int
         L.cacsi_last_launch_count.argtypes = [vp]
@@ -192,6 +195,18 @@ class Geometry:
                                    self._dev(r, self.n_det, "r"), self._dev(b1, self.n_obj, "b1"), float(beta),
                                    int(n_iter), ws.data_ptr(), _stream(stream)), "cacsi_iterate")
         return f
+
+    def ratio(self, l, y, r, out, stream=None):
+        _check(lib().cacsi_ratio(self.handle, self._dev(l, self.n_det, "l"), self._dev(y, self.n_det, "y"),
+                                 self._dev(r, self.n_det, "r"), self._dev(out, self.n_det, "ratio"),
+                                 _stream(stream)), "cacsi_ratio")
+        return out
+
+    def update(self, f_hat, b1, b2, beta, f_new, stream=None):
+        _check(lib().cacsi_update(self.handle, self._dev(f_hat, self.n_obj, "f_hat"), self._dev(b1, self.n_obj, "b1"),
+                                  self._dev(b2, self.n_obj, "b2"), float(beta), self._dev(f_new, self.n_obj, "f_new"),
+                                  _stream(stream)), "cacsi_update")
+        return f_new
 
     # -- host API (numpy fp32, end-to-end) -----------------------------------
     def forward_host(self, f, g, stream=None):

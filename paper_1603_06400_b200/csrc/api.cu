@@ -308,6 +308,25 @@ cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, co
     return map_err(e);
 }
 
+cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
+                         void *stream) {
+    if (!g || !l || !y || !r || !ratio) return CACSI_ERR_NULL;
+    int n = 0;
+    cudaError_t e = cacsi::launch_ratio(g, l, y, r, ratio, nullptr, 0, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
+                          float *f_new, void *stream) {
+    if (!g || !f_hat || !b1 || !b2 || !f_new) return CACSI_ERR_NULL;
+    if (!(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
+    int n = 0;
+    cudaError_t e = cacsi::launch_update(g, f_hat, b1, b2, beta, f_new, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
 // ---- host-buffer variants (end-to-end timing path) -------------------------
 static cudaError_t ensure_stage(const cacsi_geometry *gc) {
     cacsi_geometry *g = const_cast<cacsi_geometry *>(gc);
