@@ -67,7 +67,8 @@ cacsi_status map_err(cudaError_t e) {
 void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
-                    g->d_stage_d, g->d_stage_ws};
+                    g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_stab,
+                    g->d_esai_vwin, g->d_esai_ptot};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -227,6 +228,19 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     p.dy64 = (const double *)g->d_dy64;
     p.maskbits = (const uint32_t *)g->d_mask;
     p.energy = (const float2 *)g->d_energy;
+    // ESAI tables for the energy-integrating operators (CACSI_ALGO=direct keeps
+    // the per-term kernels, used as a cross-check in the tests)
+    const char *algo = getenv("CACSI_ALGO");
+    if (!d->energy_resolving && !(algo && strcmp(algo, "direct") == 0)) {
+        e = cacsi::esai_build(g, d);
+        if (e == cudaSuccess && g->esai.max_win * sizeof(int) > 200 * 1024) g->esai.enabled = 0;
+        if (e != cudaSuccess) {
+            free_all(g);
+            free(g);
+            cudaGetLastError();
+            return map_err(e);
+        }
+    }
     *out = g;
     return CACSI_OK;
 }

@@ -1,0 +1,370 @@
+// esai.cu -- Exact Scatter-Angle Interpolation (ESAI): the energy-integrating
+// forward and backward operators as (per-pair gather) x (dense contraction
+// over q).  DESIGN.md "ESAI".
+//
+// The paper accelerates the forward model by tabulating the spectral factor
+// on a uniform grid of scatter angles and interpolating the effective
+// spectral factor W(r, theta) = int S(theta, q) f(r, q) dq (scatter-angle
+// interpolation; Alg. 2, 176) -- an approximation
+// (NRMSE 6.2 %).  In the discrete energy form the spectral
+// factor of one pair is, with sigma = sin(theta/2),
+//     S~(sigma)[j] = sum_k c_k Lambda(alpha_k sigma - beta0 - j),
+// which is EXACTLY piecewise linear in sigma with kinks only where
+// alpha_k sigma - beta0 is an integer m in [-1, nq].  Tabulating S~ at those
+// kinks ("breakpoints" s_b) makes linear interpolation in sigma exact:
+//     S~(sigma) = (1 - tau) S~_b + tau S~_{b+1},  s_b <= sigma <= s_{b+1}.
+// Hence
+//     forward : g[r'] = sum_r P [(1 - tau) W[r, b] + tau W[r, b+1]],  W = F S~^T
+//     backward: A[r, b] = sum_{r'} P w[r'] hat_b(sigma),  b2 = A S~
+// The per-term energy loop disappears from the pair loop; the q contraction
+// becomes a dense GEMM.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pair.cuh"
+#include "sgemm.cuh"
+
+namespace cacsi {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- create --
+// Per voxel: min / max sigma over ALL pixels (superset of the open pairs, same
+// fp32 arithmetic as the operators) and sum_pixels P (fixed-point bound).
+__global__ void __launch_bounds__(256) k_pair_stats(const Params p, float *shmin, float *shmax, float *ptot) {
+    __shared__ float smin[8], smax[8];
+    __shared__ double ssum[8];
+    const int v = blockIdx.x, tid = threadIdx.x;
+    const VoxelRec vr = p.vox[v];
+    float lo = 3.0f, hi = -1.0f;
+    double sum = 0.0;
+    for (int q = tid; q < p.n_det; q += 256) {
+        float P, sh;
+        pair_geom(p, vr, p.det[q], P, sh);
+        lo = fminf(lo, sh);
+        hi = fmaxf(hi, sh);
+        sum += (double)fabsf(P);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(FULL, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
+        sum += __shfl_xor_sync(FULL, sum, o);
+    }
+    if ((tid & 31) == 0) {
+        smin[tid >> 5] = lo;
+        smax[tid >> 5] = hi;
+        ssum[tid >> 5] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 1; i < 8; i++) {
+            lo = fminf(lo, smin[i]);
+            hi = fmaxf(hi, smax[i]);
+        }
+        double s = 0.0;
+        for (int i = 0; i < 8; i++) s += ssum[i];
+        shmin[v] = smin[0] < lo ? smin[0] : lo;
+        shmax[v] = smax[0] > hi ? smax[0] : hi;
+        ptot[v] = (float)(s * (1.0 + 1e-5));  // round up: an upper bound
+    }
+}
+
+int host_locate(const std::vector<float> &sb, float s) {
+    const int nb = (int)sb.size();
+    int b = (int)(std::upper_bound(sb.begin(), sb.end(), s) - sb.begin()) - 1;
+    return std::max(0, std::min(nb - 2, b));
+}
+
+// ------------------------------------------------------------ device side --
+// b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0, 1].
+__device__ __forceinline__ int locate(const Esai &e, float s, float &tau) {
+    int c = (int)((s - e.s0) * e.inv_h);
+    c = min(max(c, 0), e.nl - 1);
+    int b = __ldg(e.lut + c);
+    while (b > 0 && __ldg(&e.bp[b].x) > s) b--;
+    while (b < e.nb - 2 && __ldg(&e.bp[b + 1].x) <= s) b++;
+    const float2 bp = __ldg(e.bp + b);
+    tau = fminf(fmaxf((s - bp.x) * bp.y, 0.0f), 1.0f);
+    return b;
+}
+
+constexpr int PF_TX = 8, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
+constexpr int PF_CH = 32;                                   // voxels per mask batch
+
+// Forward pair stage: g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
+// Lanes first test the mask for 32 voxels, then iterate only over their open
+// voxels (bitmask compaction: no lane idles on a closed pair).
+__global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e, const float *__restrict__ W,
+                                                   int vox_per_split, double *__restrict__ partial) {
+    const int tiles_y = (p.det_ny + PF_TY - 1) / PF_TY;
+    const int tx = blockIdx.x / tiles_y, ty = blockIdx.x % tiles_y;
+    const int ix = tx * PF_TX + threadIdx.x / PF_TY;
+    const int jy = ty * PF_TY + threadIdx.x % PF_TY;
+    const bool valid = ix < p.det_nx && jy < p.det_ny;
+    const int pix = valid ? ix * p.det_ny + jy : 0;
+    const float2 d = p.det[pix];
+    const int v0 = blockIdx.y * vox_per_split;
+    const int v1 = min(p.n_vox, v0 + vox_per_split);
+    double tot = 0.0;
+    for (int c0 = v0; c0 < v1; c0 += PF_CH) {
+        const int nc = min(PF_CH, v1 - c0);
+        uint32_t bits = 0;
+        if (valid)
+            for (int i = 0; i < nc; i++)
+                if (mask_open(p, c0 + i, pix, p.vox[c0 + i], d)) bits |= 1u << i;
+        float acc = 0.0f;
+        while (bits) {
+            const int i = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int v = c0 + i;
+            float P, sh, tau;
+            pair_geom(p, p.vox[v], d, P, sh);
+            const int b = locate(e, sh, tau);
+            const float *wr = W + (size_t)v * e.nb + b;
+            const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
+            acc = fmaf(P, fmaf(tau, w1 - w0, w0), acc);
+        }
+        tot += (double)acc;
+    }
+    if (valid) partial[(size_t)blockIdx.y * p.n_det + pix] = tot;
+}
+
+// max |w| over the detector (fixed-point scale of the backward histogram)
+__global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, size_t n, float *out) {
+    __shared__ float s[32];
+    float m = 0.0f;
+    for (size_t i = threadIdx.x; i < n; i += 1024) m = fmaxf(m, fabsf(w[i]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 32; i++) m = fmaxf(m, s[i]);
+        *out = fmaxf(m, s[0]);
+    }
+}
+
+constexpr int PB_T = 256;
+
+// Backward pair stage: A[v, b] = sum_pixels P w hat_b(sigma), one CTA per voxel.
+// Deposits go to a shared-memory histogram over the voxel's breakpoint window
+// in 32-bit FIXED POINT with native integer atomics (exact, order-independent,
+// so deterministic); the scale 2^30 / (sum_pixels P * max|w|) cannot overflow.
+__global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
+                                                   const float *__restrict__ wmax, float *__restrict__ A) {
+    extern __shared__ int hist[];
+    const int v = blockIdx.x, tid = threadIdx.x;
+    const int2 win = e.vwin[v];
+    const int nwin = win.y - win.x + 1;
+    for (int i = tid; i < nwin; i += PB_T) hist[i] = 0;
+    __syncthreads();
+    const float wm = *wmax;
+    const double bound = (double)e.ptot[v] * (double)wm;
+    const float inv_q = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+    const VoxelRec vr = p.vox[v];
+    int *h = hist - win.x;
+    if (inv_q > 0.0f) {
+        for (int q = tid; q < p.n_det; q += PB_T) {
+            const float2 d = p.det[q];
+            if (!mask_open(p, v, q, vr, d)) continue;
+            float P, sh, tau;
+            pair_geom(p, vr, d, P, sh);
+            const int b = locate(e, sh, tau);
+            const float a = P * __ldg(w + q) * inv_q;
+            const float a1 = a * tau;
+            atomicAdd(h + b, __float2int_rn(a - a1));
+            atomicAdd(h + b + 1, __float2int_rn(a1));
+        }
+    }
+    __syncthreads();
+    const float qv = inv_q > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+    float *Ar = A + (size_t)v * e.nb;
+    for (int b = tid; b < e.nb; b += PB_T) {
+        const int i = b - win.x;
+        Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * qv : 0.0f;
+    }
+}
+
+__global__ void k_sum_parts_f64(const double *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < S; j++) s += part[j * n + i];
+        out[i] = (float)s;
+    }
+}
+
+__global__ void k_sum_parts_f32(const float *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < S; j++) s += (double)part[j * n + i];
+        out[i] = (float)s;
+    }
+}
+
+int sm_count(int dev) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+}  // namespace
+
+// Build the ESAI tables (energy-integrating handles).  Host fp64 arithmetic
+// for the breakpoints and S~; DESIGN.md "ESAI tables".
+cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
+    const Params &p = g->p;
+    const int nv = p.n_vox, Q = p.nq, K = p.ne;
+    float *dmin = nullptr, *dmax = nullptr, *dpt = nullptr;
+    cudaError_t e = cudaMalloc(&dmin, nv * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&dmax, nv * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&dpt, nv * sizeof(float));
+    if (e == cudaSuccess) {
+        k_pair_stats<<<nv, 256>>>(p, dmin, dmax, dpt);
+        e = cudaGetLastError();
+    }
+    std::vector<float> shmin(nv), shmax(nv), ptot(nv);
+    if (e == cudaSuccess) e = cudaMemcpy(shmin.data(), dmin, nv * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(shmax.data(), dmax, nv * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(ptot.data(), dpt, nv * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dmin);
+    cudaFree(dmax);
+    if (e != cudaSuccess) {
+        cudaFree(dpt);
+        return e;
+    }
+    g->d_esai_ptot = dpt;
+    const float smin = *std::min_element(shmin.begin(), shmin.end());
+    const float smax = *std::max_element(shmax.begin(), shmax.end());
+    const double lo = (double)smin * (1.0 - 1e-6), hi = (double)smax * (1.0 + 1e-6);
+
+    // breakpoints s_{k,m} = (m + beta0) / alpha_k, m in [-1, nq]   (fp64)
+    const double dq = (d->q_max - d->q_min) / (d->nq - 1);
+    const double beta0 = d->q_min / dq;
+    std::vector<double> alpha(K), ck(K);
+    for (int k = 0; k < K; k++) {
+        alpha[k] = d->energy_kev[k] / (kHc * dq);
+        ck[k] = d->scale * d->phi[k] * d->energy_kev[k];
+    }
+    std::vector<float> sb;
+    sb.push_back((float)lo);
+    sb.push_back((float)hi);
+    for (int k = 0; k < K; k++)
+        for (int m = -1; m <= Q; m++) {
+            const double s = (m + beta0) / alpha[k];
+            if (s > lo && s < hi) sb.push_back((float)s);
+        }
+    std::sort(sb.begin(), sb.end());
+    sb.erase(std::unique(sb.begin(), sb.end()), sb.end());
+    const int nb = (int)sb.size();
+    // (s_b, 1 / (s_{b+1} - s_b)) and S~ at the fp32 nodes
+    std::vector<float2> bp(nb);
+    std::vector<float> stab((size_t)nb * Q, 0.0f);
+    std::vector<double> row(Q);
+    for (int b = 0; b < nb; b++) {
+        const double s = sb[b];
+        bp[b] = make_float2(sb[b], b + 1 < nb ? (float)(1.0 / ((double)sb[b + 1] - s)) : 0.0f);
+        std::fill(row.begin(), row.end(), 0.0);
+        for (int k = 0; k < K; k++) {
+            const double u = alpha[k] * s - beta0;
+            const double j0 = std::floor(u), t = u - j0;
+            const long j = (long)j0;
+            if (j >= 0 && j < Q) row[j] += ck[k] * (1.0 - t);
+            if (j + 1 >= 0 && j + 1 < Q) row[j + 1] += ck[k] * t;
+        }
+        for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)row[j];
+    }
+    // uniform LUT over [s_0, s_{nb-1}]
+    const int nl = std::max(64, 8 * nb);
+    const double span = (double)sb[nb - 1] - sb[0];
+    std::vector<int> lut(nl);
+    for (int c = 0; c < nl; c++) lut[c] = host_locate(sb, (float)(sb[0] + span * c / nl));
+    // per-voxel breakpoint windows (deposits land in [locate(min), locate(max) + 1])
+    std::vector<int2> vwin(nv);
+    int max_win = 1;
+    for (int v = 0; v < nv; v++) {
+        vwin[v] = make_int2(host_locate(sb, shmin[v]), host_locate(sb, shmax[v]) + 1);
+        max_win = std::max(max_win, vwin[v].y - vwin[v].x + 1);
+    }
+    e = cudaMalloc(&g->d_esai_bp, nb * sizeof(float2));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_bp, bp.data(), nb * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_stab, stab.size() * sizeof(float));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_esai_stab, stab.data(), stab.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_vwin, nv * sizeof(int2));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_vwin, vwin.data(), nv * sizeof(int2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    Esai &E = g->esai;
+    E.nb = nb;
+    E.nl = nl;
+    E.s0 = sb[0];
+    E.inv_h = (float)(nl / span);
+    E.bp = (const float2 *)g->d_esai_bp;
+    E.lut = (const int *)g->d_esai_lut;
+    E.stab = (const float *)g->d_esai_stab;
+    E.vwin = (const int2 *)g->d_esai_vwin;
+    E.ptot = (const float *)g->d_esai_ptot;
+    E.max_win = max_win;
+    E.enabled = 1;
+    return cudaSuccess;
+}
+
+cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
+    const Params &p = g->p;
+    const Esai &E = g->esai;
+    float *W = nullptr;
+    double *part = nullptr;
+    const int tiles = ((p.det_nx + PF_TX - 1) / PF_TX) * ((p.det_ny + PF_TY - 1) / PF_TY);
+    const int target = 8 * sm_count(g->device);
+    int S = std::max(1, std::min((target + tiles - 1) / tiles, (p.n_vox + PF_CH - 1) / PF_CH));
+    int vps = (p.n_vox + S - 1) / S;
+    vps = (vps + PF_CH - 1) / PF_CH * PF_CH;
+    S = (p.n_vox + vps - 1) / vps;
+    cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.nb * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+    if (e == cudaSuccess) {
+        // W[v][b] = sum_j f[v][j] S~[b][j]
+        dim3 gg((E.nb + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, 1);
+        k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
+        k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
+        k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
+        e = cudaGetLastError();
+        *launches += 3;
+    }
+    if (part) cudaFreeAsync(part, s);
+    if (W) cudaFreeAsync(W, s);
+    return e;
+}
+
+cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
+    const Params &p = g->p;
+    const Esai &E = g->esai;
+    float *A = nullptr, *part = nullptr, *wmax = nullptr;
+    const int S = 8;  // split-K of the A S~ contraction (fp32 partials, fp64 sum)
+    const int kps = ((E.nb + S - 1) / S + GM_BK - 1) / GM_BK * GM_BK;
+    const int S_eff = (E.nb + kps - 1) / kps;
+    cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.nb * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
+    if (e == cudaSuccess) {
+        k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
+        const size_t smem = (size_t)E.max_win * sizeof(int);
+        cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_esai_bwd<<<p.n_vox, PB_T, smem, s>>>(p, E, w, wmax, A);
+        dim3 gg((p.nq + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, S_eff);
+        k_sgemm<false><<<gg, GM_T, 0, s>>>(p.n_vox, p.nq, E.nb, kps, A, E.stab, part);
+        const size_t n = (size_t)p.n_vox * p.nq;
+        k_sum_parts_f32<<<(int)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S_eff, n, b);
+        e = cudaGetLastError();
+        *launches += 4;
+    }
+    if (wmax) cudaFreeAsync(wmax, s);
+    if (part) cudaFreeAsync(part, s);
+    if (A) cudaFreeAsync(A, s);
+    return e;
+}
+
+}  // namespace cacsi

@@ -51,6 +51,20 @@ struct Params {
     const float2 *energy;              // (alpha_k, c_k): alpha_k = E_k/(hc dq), c_k = scale phi_k E_k
 };
 
+// ESAI tables (energy-integrating handles; esai.cu).
+struct Esai {
+    int enabled;
+    int nb;             // breakpoints s_0 < ... < s_{nb-1} (fp32, strictly increasing)
+    int nl;             // uniform lookup cells over [s_0, s_{nb-1}]
+    int max_win;        // max per-voxel breakpoint window (backward histogram size)
+    float s0, inv_h;    // cell c = (sigma - s0) * inv_h
+    const float2 *bp;   // (s_b, 1 / (s_{b+1} - s_b))
+    const int *lut;     // first-guess b per cell
+    const float *stab;  // S~ [nb][nq] (scale, phi_k, E_k folded in)
+    const int2 *vwin;   // per voxel [b_lo, b_hi] reachable by any of its pairs
+    const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)
+};
+
 }  // namespace cacsi
 
 struct cacsi_geometry {
@@ -61,6 +75,9 @@ struct cacsi_geometry {
     size_t n_obj, n_detout;
     // device allocations (owned)
     void *d_vox, *d_vy64, *d_vz64, *d_vt64, *d_det, *d_dx64, *d_dy64, *d_mask, *d_energy;
+    // ESAI (energy-integrating only)
+    cacsi::Esai esai;
+    void *d_esai_bp, *d_esai_lut, *d_esai_stab, *d_esai_vwin, *d_esai_ptot;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;
@@ -79,5 +96,8 @@ cudaError_t launch_update(const cacsi_geometry *g, const float *f_hat, const flo
 cudaError_t launch_loglik(const cacsi_geometry *g, const float *l, const float *y, const float *r, const float *f,
                           float beta, double *partials, double *out, cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
+cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
+cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
+cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 
 }  // namespace cacsi
