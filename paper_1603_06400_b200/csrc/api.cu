@@ -233,7 +233,7 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     const char *algo = getenv("CACSI_ALGO");
     if (!d->energy_resolving && !(algo && strcmp(algo, "direct") == 0)) {
         e = cacsi::esai_build(g, d);
-        if (e == cudaSuccess && g->esai.max_win * sizeof(int) > 200 * 1024) g->esai.enabled = 0;
+        if (e == cudaSuccess && g->esai.max_win * 2 * sizeof(int) > 200 * 1024) g->esai.enabled = 0;
         if (e != cudaSuccess) {
             free_all(g);
             free(g);

@@ -150,40 +150,57 @@ constexpr int PB_T = 256;
 
 // Backward pair stage: A[v, b] = sum_pixels P w hat_b(sigma), one CTA per voxel.
 // Deposits go to a shared-memory histogram over the voxel's breakpoint window
-// in 32-bit FIXED POINT with native integer atomics (exact, order-independent,
-// so deterministic); the scale 2^30 / (sum_pixels P * max|w|) cannot overflow.
+// in FIXED POINT with native 32-bit integer shared atomics (fp32 atomicAdd on
+// shared memory is a CAS loop on sm_100).  Each deposit x = d * scale (an
+// integer-valued float, < 2^(30+lb)) is split exactly into hi = floor(x / 2^lb)
+// and lo = x - hi 2^lb in [0, 2^lb): sum(hi) fits int32 by the choice of scale
+// (2^(30+lb) / (sum_pixels |P| max|w|)), sum(lo) fits uint32 because a bin gets
+// at most 2 n_det deposits (lb = 31 - log2(2 n_det)).  ~45-bit resolution,
+// exact and order-independent (deterministic).
 __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
                                                    const float *__restrict__ wmax, float *__restrict__ A) {
-    extern __shared__ int hist[];
+    extern __shared__ int hist[];  // [nwin] hi words, then [nwin] lo words
     const int v = blockIdx.x, tid = threadIdx.x;
     const int2 win = e.vwin[v];
     const int nwin = win.y - win.x + 1;
-    for (int i = tid; i < nwin; i += PB_T) hist[i] = 0;
+    for (int i = tid; i < 2 * nwin; i += PB_T) hist[i] = 0;
     __syncthreads();
     const float wm = *wmax;
     const double bound = (double)e.ptot[v] * (double)wm;
-    const float inv_q = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+    const double full = ldexp(1.0, 30 + e.lo_bits);
+    const float scale = bound > 0.0 ? (float)(full / bound) : 0.0f;
+    const float inv_lo = ldexpf(1.0f, -e.lo_bits), lo_unit = ldexpf(1.0f, e.lo_bits);
     const VoxelRec vr = p.vox[v];
-    int *h = hist - win.x;
-    if (inv_q > 0.0f) {
+    int *hh = hist - win.x;
+    unsigned *hl = (unsigned *)(hist + nwin) - win.x;
+    if (scale > 0.0f) {
         for (int q = tid; q < p.n_det; q += PB_T) {
             const float2 d = p.det[q];
             if (!mask_open(p, v, q, vr, d)) continue;
             float P, sh, tau;
             pair_geom(p, vr, d, P, sh);
             const int b = locate(e, sh, tau);
-            const float a = P * __ldg(w + q) * inv_q;
-            const float a1 = a * tau;
-            atomicAdd(h + b, __float2int_rn(a - a1));
-            atomicAdd(h + b + 1, __float2int_rn(a1));
+            const float a = P * __ldg(w + q) * scale;
+            const float x1 = rintf(a * tau);
+            const float x0 = rintf(a) - x1;
+            const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
+            atomicAdd(hh + b, (int)h0);
+            atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
+            atomicAdd(hh + b + 1, (int)h1);
+            atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
         }
     }
     __syncthreads();
-    const float qv = inv_q > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+    const double qv = scale > 0.0f ? bound / full : 0.0;
     float *Ar = A + (size_t)v * e.nb;
     for (int b = tid; b < e.nb; b += PB_T) {
         const int i = b - win.x;
-        Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * qv : 0.0f;
+        float val = 0.0f;
+        if (i >= 0 && i < nwin) {
+            const long long t = (long long)hist[i] * (1ll << e.lo_bits) + (long long)(unsigned)hist[nwin + i];
+            val = (float)((double)t * qv);
+        }
+        Ar[b] = val;
     }
 }
 
@@ -308,6 +325,10 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.ptot = (const float *)g->d_esai_ptot;
     E.max_win = max_win;
+    // low-word bits of the fixed-point deposits: a bin receives <= 2 n_det deposits < 2^(32 - lo_bits)
+    int lb = 31;
+    while (lb > 0 && (2.0 * p.n_det + 1.0) * std::ldexp(1.0, lb) >= 4294967296.0) lb--;
+    E.lo_bits = std::min(lb, 20);
     E.enabled = 1;
     return cudaSuccess;
 }
@@ -351,7 +372,7 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
     if (e == cudaSuccess) {
         k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
-        const size_t smem = (size_t)E.max_win * sizeof(int);
+        const size_t smem = (size_t)E.max_win * 2 * sizeof(int);
         cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_esai_bwd<<<p.n_vox, PB_T, smem, s>>>(p, E, w, wmax, A);
         dim3 gg((p.nq + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, S_eff);

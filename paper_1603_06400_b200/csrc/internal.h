@@ -57,6 +57,7 @@ struct Esai {
     int nb;             // breakpoints s_0 < ... < s_{nb-1} (fp32, strictly increasing)
     int nl;             // uniform lookup cells over [s_0, s_{nb-1}]
     int max_win;        // max per-voxel breakpoint window (backward histogram size)
+    int lo_bits;        // fixed-point split of the backward deposits (esai.cu)
     float s0, inv_h;    // cell c = (sigma - s0) * inv_h
     const float2 *bp;   // (s_b, 1 / (s_{b+1} - s_b))
     const int *lut;     // first-guess b per cell

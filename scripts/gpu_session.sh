@@ -22,6 +22,6 @@ if [[ $STAGES == *ncu* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches.csv $CMD > $OUT/${TAG}_ncu_launch.log 2>&1
   echo "launch rc=$?" >> $OUT/${TAG}_ncu_launch.log
   KREGEX=${KREGEX:-k_backward}
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KREGEX -s 2 -c 1 -o $OUT/${TAG}_prof $CMD > $OUT/${TAG}_ncu_full.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$KREGEX" -s ${NCU_SKIP:-2} -c ${NCU_COUNT:-1} -o $OUT/${TAG}_prof $CMD > $OUT/${TAG}_ncu_full.log 2>&1
   echo "full rc=$?" >> $OUT/${TAG}_ncu_full.log
 fi
