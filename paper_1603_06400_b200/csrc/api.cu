@@ -228,6 +228,17 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     p.dy64 = (const double *)g->d_dy64;
     p.maskbits = (const uint32_t *)g->d_mask;
     p.energy = (const float2 *)g->d_energy;
+    // translation symmetry: voxel y pitch an integer multiple rho of the detector pitch
+    {
+        const double dyv = (d->y_max - d->y_min) / d->ny;
+        const double rho = std::floor(dyv / d->det_pitch + 0.5);
+        p.ts_rho = 0;
+        if (rho >= 1.0 && rho <= 64.0 && std::fabs(dyv - rho * d->det_pitch) <= 1e-9 * d->det_pitch &&
+            !getenv("CACSI_NO_TS")) {
+            p.ts_rho = (int)rho;
+            p.ts_c0 = (float)(det_centre(d->det_cy, d->det_ny, d->det_pitch, 0) - centre(d->y_min, d->y_max, d->ny, 0));
+        }
+    }
     // ESAI tables for the energy-integrating operators (CACSI_ALGO=direct keeps
     // the per-term kernels, used as a cross-check in the tests)
     const char *algo = getenv("CACSI_ALGO");

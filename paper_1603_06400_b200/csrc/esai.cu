@@ -92,7 +92,7 @@ __device__ __forceinline__ int locate(const Esai &e, float s, float &tau) {
 }
 
 constexpr int PF_TX = 8, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
-constexpr int PF_CH = 32;                                   // voxels per mask batch
+constexpr int PF_CH = 64;                                   // voxels per mask batch
 
 // Forward pair stage: g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
 // Lanes first test the mask for 32 voxels, then iterate only over their open
@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
     double tot = 0.0;
     for (int c0 = v0; c0 < v1; c0 += PF_CH) {
         const int nc = min(PF_CH, v1 - c0);
-        uint32_t bits = 0;
+        unsigned long long bits = 0;
         if (valid)
             for (int i = 0; i < nc; i++)
-                if (mask_open(p, c0 + i, pix, p.vox[c0 + i], d)) bits |= 1u << i;
+                if (mask_open(p, c0 + i, pix, p.vox[c0 + i], d)) bits |= 1ull << i;
         float acc = 0.0f;
         while (bits) {
-            const int i = __ffs(bits) - 1;
+            const int i = __ffsll((long long)bits) - 1;
             bits &= bits - 1;
             const int v = c0 + i;
             float P, sh, tau;
@@ -126,6 +126,116 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
             const float *wr = W + (size_t)v * e.nb + b;
             const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
             acc = fmaf(P, fmaf(tau, w1 - w0, w0), acc);
+        }
+        tot += (double)acc;
+    }
+    if (valid) partial[(size_t)blockIdx.y * p.n_det + pix] = tot;
+}
+
+
+// ---- translation-symmetric forward (Alg. 2) --
+// When the voxel y pitch is rho detector pitches, s = r' - r depends only on
+// (iz, ix, d = jy - rho iy): |s|, G_od and dtheta of every pair of a detector
+// row and a voxel row z are one "footprint" of n_jy + rho (ny - 1) entries.  A
+// CTA owns a 128-pixel segment of one detector row, builds the footprint of
+// each voxel row z in shared memory (the paper's "compute once, shift by rho
+// columns"), and reuses it for all ny voxels of that row as integer shifts.
+// Only the source-side quantities (r^, G_so) and the mask stay per pair.
+constexpr int TS_T = 128;
+
+__device__ __forceinline__ bool mask_open_ts(const Params &p, int v, int q, int cx, int xstate, float uy) {
+    // xstate: 0 = x cell outside the raster, 1 = inside and clear of edges, 2 = near an x edge
+    if (xstate == 0) return false;
+    const float fy = floorf(uy);
+    const float ry = uy - fy;
+    int cy;
+    if (xstate == 2 || ry < kMaskGuard || ry > 1.0f - kMaskGuard) {
+        const double t = p.vt64[v], yr = p.vy64[v];
+        const double xd = p.dx64[q], yd = p.dy64[q];
+        const double px = __dmul_rn(t, xd);
+        const double py = __dadd_rn(yr, __dmul_rn(t, __dsub_rn(yd, yr)));
+        const double gx = floor(__ddiv_rn(__dsub_rn(px, p.m0x), p.mask_pitch64));
+        const double gy = floor(__ddiv_rn(__dsub_rn(py, p.m0y), p.mask_pitch64));
+        if (!(gx >= 0.0 && gy >= 0.0 && gx < (double)p.mask_nx && gy < (double)p.mask_ny)) return false;
+        cx = (int)gx;
+        cy = (int)gy;
+    } else {
+        cy = (int)fy;
+        if (fy < 0.0f || cy >= p.mask_ny) return false;
+    }
+    const uint32_t w = __ldg(p.maskbits + (size_t)cx * p.mask_words + (cy >> 5));
+    return (w >> (cy & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai e, const float *__restrict__ W,
+                                                      int iz_per_split, double *__restrict__ partial) {
+    extern __shared__ float4 sm4[];
+    const int rho = p.ts_rho, ny = p.ny, nz = p.nz;
+    const int segs = (p.det_ny + TS_T - 1) / TS_T;
+    const int ix = blockIdx.x / segs, jy0 = (blockIdx.x % segs) * TS_T;
+    const int tid = threadIdx.x;
+    const int jy = jy0 + tid;
+    const bool valid = jy < p.det_ny;
+    const int pix = ix * p.det_ny + (valid ? jy : p.det_ny - 1);
+    const float2 dd = p.det[pix];
+    const float sx = dd.x;
+    const int nfoot = TS_T + rho * (ny - 1);
+    const int dmin = jy0 - rho * (ny - 1);
+    float4 *foot = sm4;          // [nfoot] (1/|s|, G_od dtheta, s_y, -)
+    float4 *vp = sm4 + nfoot;    // [ny]    (r^_y, r^_z, G_so, ay)
+    const int iz0 = blockIdx.y * iz_per_split, iz1 = min(nz, iz0 + iz_per_split);
+    double tot = 0.0;
+    for (int iz = iz0; iz < iz1; iz++) {
+        const VoxelRec r0 = p.vox[iz];  // iy = 0: z-row quantities
+        const float sz = r0.sz, tq = r0.tq;
+        __syncthreads();
+        for (int i = tid; i < nfoot; i += TS_T) {
+            const float sy = fmaf(p.pitch_d, (float)(dmin + i), p.ts_c0);
+            const float syz2 = fmaf(sy, sy, sz * sz);
+            const float rs = rsqrtf(fmaf(sx, sx, syz2));
+            const float rs2 = rs * rs;
+            const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
+            const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
+            foot[i] = make_float4(rs, sz * rs * rs2 * dth, sy, 0.0f);
+        }
+        for (int iy = tid; iy < ny; iy += TS_T) {
+            const VoxelRec r = p.vox[iy * nz + iz];
+            vp[iy] = make_float4(r.ry, r.rz, r.gso, r.ay);
+        }
+        __syncthreads();
+        // x part of the mask cell is uniform over the row segment
+        const float ux = fmaf(tq, sx, p.ax);
+        const float fx = floorf(ux), rx = ux - fx;
+        const int cx = (int)fx;
+        int xstate = (fx >= 0.0f && cx < p.mask_nx) ? 1 : 0;
+        if (rx < kMaskGuard || rx > 1.0f - kMaskGuard) xstate = 2;
+        float acc = 0.0f;
+        for (int iyb = 0; iyb < ny; iyb += 64) {
+            const int nb_ = min(64, ny - iyb);
+            unsigned long long bits = 0;
+            if (valid)
+                for (int k = 0; k < nb_; k++) {
+                    const int iy = iyb + k;
+                    if (mask_open_ts(p, iy * nz + iz, pix, cx, xstate, fmaf(tq, dd.y, vp[iy].w))) bits |= 1ull << k;
+                }
+            while (bits) {
+                const int k = __ffsll((long long)bits) - 1;
+                bits &= bits - 1;
+                const int iy = iyb + k;
+                const float4 v = vp[iy];
+                const float4 f = foot[tid + rho * (ny - 1 - iy)];
+                const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
+                const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
+                const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
+                const float h = fmaf(0.5f, cos_t, 0.5f);
+                const float rh = rsqrtf(h);
+                const float P = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
+                float tau;
+                const int b = locate(e, 0.5f * sin_t * rh, tau);
+                const float *wr = W + (size_t)(iy * nz + iz) * e.nb + b;
+                const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
+                acc = fmaf(P, fmaf(tau, w1 - w0, w0), acc);
+            }
         }
         tot += (double)acc;
     }
@@ -174,20 +284,30 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     int *hh = hist - win.x;
     unsigned *hl = (unsigned *)(hist + nwin) - win.x;
     if (scale > 0.0f) {
-        for (int q = tid; q < p.n_det; q += PB_T) {
-            const float2 d = p.det[q];
-            if (!mask_open(p, v, q, vr, d)) continue;
-            float P, sh, tau;
-            pair_geom(p, vr, d, P, sh);
-            const int b = locate(e, sh, tau);
-            const float a = P * __ldg(w + q) * scale;
-            const float x1 = rintf(a * tau);
-            const float x0 = rintf(a) - x1;
-            const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
-            atomicAdd(hh + b, (int)h0);
-            atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
-            atomicAdd(hh + b + 1, (int)h1);
-            atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
+        // lanes first test the mask for 64 of their pixels, then iterate only
+        // over the open ones (no lane idles on a closed pair)
+        for (int base = 0; base < p.n_det; base += PB_T * 64) {
+            unsigned long long bits = 0;
+            for (int k = 0; k < 64; k++) {
+                const int q = base + k * PB_T + tid;
+                if (q < p.n_det && mask_open(p, v, q, vr, p.det[q])) bits |= 1ull << k;
+            }
+            while (bits) {
+                const int k = __ffsll((long long)bits) - 1;
+                bits &= bits - 1;
+                const int q = base + k * PB_T + tid;
+                float P, sh, tau;
+                pair_geom(p, vr, p.det[q], P, sh);
+                const int b = locate(e, sh, tau);
+                const float a = P * __ldg(w + q) * scale;
+                const float x1 = rintf(a * tau);
+                const float x0 = rintf(a) - x1;
+                const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
+                atomicAdd(hh + b, (int)h0);
+                atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
+                atomicAdd(hh + b + 1, (int)h1);
+                atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
+            }
         }
     }
     __syncthreads();
@@ -345,12 +465,23 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
     vps = (vps + PF_CH - 1) / PF_CH * PF_CH;
     S = (p.n_vox + vps - 1) / vps;
     cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.nb * sizeof(float), s);
-    if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)std::max(S, p.nz) * p.n_det * sizeof(double), s);
     if (e == cudaSuccess) {
         // W[v][b] = sum_j f[v][j] S~[b][j]
         dim3 gg((E.nb + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, 1);
         k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
-        k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
+        if (p.ts_rho > 0) {
+            const int segs = p.det_nx * ((p.det_ny + TS_T - 1) / TS_T);
+            int St = std::max(1, std::min((target + segs - 1) / segs, p.nz));
+            const int izps = (p.nz + St - 1) / St;
+            St = (p.nz + izps - 1) / izps;
+            const size_t smem = (size_t)(TS_T + p.ts_rho * (p.ny - 1) + p.ny) * sizeof(float4);
+            cudaFuncSetAttribute(k_esai_fwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_fwd_ts<<<dim3(segs, St), TS_T, smem, s>>>(p, E, W, izps, part);
+            S = St;
+        } else {
+            k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
+        }
         k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
         e = cudaGetLastError();
         *launches += 3;

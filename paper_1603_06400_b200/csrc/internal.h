@@ -40,6 +40,10 @@ struct Params {
     float qm;                          // nq - 1/2               (clamp bound of u')
     float klo_num, khi_num;            // (q_min/dq - 1), (q_min/dq + nq): alpha range numerators
     float a0, inv_da;                  // alpha_k = a0 + k / inv_da when uniform_e
+    // translation symmetry: voxel y pitch = ts_rho * detector pitch
+    // => y_d(jy) - y_r(iy) = ts_c0 + pitch_d * (jy - ts_rho * iy); 0 = not applicable
+    int ts_rho;
+    float ts_c0;
     // fp64 guard path (exact oracle op order, reading R8)
     double m0x, m0y, mask_pitch64;
     // device tables

@@ -197,9 +197,21 @@ def test_config3_b1_and_iterates(config3):
     f = cuda(f0)
     ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
     yt, rt = cuda(y), cuda(r)
+    # the backward on the actual EM weights y / (A f0 + r)
+    rat = recon.ratio(O.forward(f0), y, r).astype(np.float32)
+    b2g = gpu_backward(G, rat)
+    b2r = O.backward(rat)
+    assert_parity(b2g, b2r, "c3 b2 on EM weights")
     for t in range(3):
         G.iterate(f, yt, rt, b1, beta, 1, ws)
         torch.cuda.synchronize()
+        if t == 0:
+            x, ref = f.cpu().numpy(), ref_iters[0]
+            sel = np.abs(ref) >= 1e-3 * np.abs(ref).max()
+            rel = np.where(sel, np.abs(x - ref) / np.maximum(np.abs(ref), 1e-300), 0)
+            k = np.unravel_index(np.argmax(rel), rel.shape)
+            print("worst", k, x[k], ref[k], "b1", b1.cpu().numpy()[k], b1_ref[k], "b2", b2g[k], b2r[k],
+                  "f0", f0[k])
         assert_parity(f.cpu().numpy(), ref_iters[t], f"c3 iterate {t + 1}", l2=1e-5 * (t + 1), mr=1e-4 * (t + 1))
 
 
@@ -260,3 +272,27 @@ def test_esai_matches_direct_config2(monkeypatch):
     w = rnd(G.g_shape, 2, 51)
     assert rel_l2(gpu_forward(G, cfg.f), gpu_forward(D, cfg.f)) < 2e-6
     assert rel_l2(gpu_backward(G, w), gpu_backward(D, w)) < 2e-6
+
+
+# ------------------------------------------------- translation symmetry (TS) --
+@pytest.mark.parametrize("over", [
+    dict(det_pitch=1.0),                                  # rho = 2
+    dict(det_pitch=2.0, det_cx=28.0),                     # rho = 1
+    dict(det_pitch=0.5, det_nx=20, det_ny=150),           # rho = 4, two ragged 128-pixel segments
+    dict(det_pitch=1.0, ny=70, y_min=-70.0, y_max=70.0, det_ny=23, mask_ny=200),  # ny > 64 batch, ragged
+])
+def test_translation_symmetric_forward(over, monkeypatch):
+    """TS forward kernel (footprint per z row reused as integer shifts) vs the
+    oracle, and vs the same handle without TS."""
+    cfg = make_config(0)
+    d = cfg.desc()
+    d.update(over)
+    if "mask_ny" in over:
+        d["mask"] = seeded_rng(0, 60).integers(0, 2, (d["mask_nx"], d["mask_ny"])).astype(np.uint8)
+    G, O = geoms(d)
+    f = rnd(G.f_shape, 0, 61)
+    g = gpu_forward(G, f)
+    assert_parity(g, O.forward(f), f"TS {over} forward")
+    monkeypatch.setenv("CACSI_NO_TS", "1")
+    G2 = P.Geometry(d)
+    assert rel_l2(g, gpu_forward(G2, f)) < 1e-6
