@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libcacsi.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
-    "-O3", "-std=c++17", "-lineinfo",
+    "-O3", "-std=c++17", "-lineinfo", "--ftz=true",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "--expt-relaxed-constexpr",

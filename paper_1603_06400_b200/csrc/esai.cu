@@ -20,6 +20,7 @@
 // becomes a dense GEMM.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "pair.cuh"
@@ -72,6 +73,12 @@ __global__ void __launch_bounds__(256) k_pair_stats(const Params p, float *shmin
     }
 }
 
+float __int_as_float_host(int i) {
+    float f;
+    memcpy(&f, &i, sizeof f);
+    return f;
+}
+
 int host_locate(const std::vector<float> &sb, float s) {
     const int nb = (int)sb.size();
     int b = (int)(std::upper_bound(sb.begin(), sb.end(), s) - sb.begin()) - 1;
@@ -80,23 +87,38 @@ int host_locate(const std::vector<float> &sb, float s) {
 
 // ------------------------------------------------------------ device side --
 // b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0, 1].
+// One 16-byte LUT load {s_b, 1/(s_{b+1}-s_b), s_{b+1}, b} settles the common
+// case; the walk over the breakpoint array is only needed when the cell holds
+// a breakpoint below sigma.
 __device__ __forceinline__ int locate(const Esai &e, float s, float &tau) {
     int c = (int)((s - e.s0) * e.inv_h);
     c = min(max(c, 0), e.nl - 1);
-    int b = __ldg(e.lut + c);
-    while (b > 0 && __ldg(&e.bp[b].x) > s) b--;
-    while (b < e.nb - 2 && __ldg(&e.bp[b + 1].x) <= s) b++;
-    const float2 bp = __ldg(e.bp + b);
-    tau = fminf(fmaxf((s - bp.x) * bp.y, 0.0f), 1.0f);
+    const float4 L = __ldg(e.lut4 + c);
+    int b = __float_as_int(L.w);
+    float sb = L.x, ig = L.y;
+    if (s >= L.z || s < L.x) {
+        while (b < e.nb - 2 && __ldg(&e.bp[b + 1].x) <= s) b++;
+        while (b > 0 && __ldg(&e.bp[b].x) > s) b--;
+        const float2 bp = __ldg(e.bp + b);
+        sb = bp.x;
+        ig = bp.y;
+    }
+    tau = fminf(fmaxf((s - sb) * ig, 0.0f), 1.0f);
     return b;
 }
 
+__device__ __forceinline__ float lerp_w(const float *__restrict__ wr, float tau) {
+    const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
+    return fmaf(tau, w1 - w0, w0);
+}
+
 constexpr int PF_TX = 8, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
-constexpr int PF_CH = 64;                                   // voxels per mask batch
+constexpr int PF_CH = 32;                                   // voxels per mask batch
 
 // Forward pair stage: g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
-// Lanes first test the mask for 32 voxels, then iterate only over their open
-// voxels (bitmask compaction: no lane idles on a closed pair).
+// Lanes first test the mask for 32 voxels (fp32 fast path; the rare
+// near-edge cells are re-tested exactly in a second pass so the warp stays
+// converged), then iterate only over their open voxels.
 __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e, const float *__restrict__ W,
                                                    int vox_per_split, double *__restrict__ partial) {
     const int tiles_y = (p.det_ny + PF_TY - 1) / PF_TY;
@@ -111,27 +133,34 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
     double tot = 0.0;
     for (int c0 = v0; c0 < v1; c0 += PF_CH) {
         const int nc = min(PF_CH, v1 - c0);
-        unsigned long long bits = 0;
+        uint32_t bits = 0, nearb = 0;
         if (valid)
-            for (int i = 0; i < nc; i++)
-                if (mask_open(p, c0 + i, pix, p.vox[c0 + i], d)) bits |= 1ull << i;
+            for (int i = 0; i < nc; i++) {
+                bool nr;
+                const bool o = mask_fast(p, p.vox[c0 + i], d, nr);
+                bits |= (uint32_t)o << i;
+                nearb |= (uint32_t)nr << i;
+            }
+        while (nearb) {
+            const int i = __ffs(nearb) - 1;
+            nearb &= nearb - 1;
+            if (mask_exact(p, c0 + i, pix)) bits |= 1u << i;
+            else bits &= ~(1u << i);
+        }
         float acc = 0.0f;
         while (bits) {
-            const int i = __ffsll((long long)bits) - 1;
+            const int i = __ffs(bits) - 1;
             bits &= bits - 1;
             const int v = c0 + i;
             float P, sh, tau;
             pair_geom(p, p.vox[v], d, P, sh);
             const int b = locate(e, sh, tau);
-            const float *wr = W + (size_t)v * e.nb + b;
-            const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
-            acc = fmaf(P, fmaf(tau, w1 - w0, w0), acc);
+            acc = fmaf(P, lerp_w(W + (size_t)v * e.nb + b, tau), acc);
         }
         tot += (double)acc;
     }
     if (valid) partial[(size_t)blockIdx.y * p.n_det + pix] = tot;
 }
-
 
 // ---- translation-symmetric forward (Alg. 2) --
 // When the voxel y pitch is rho detector pitches, s = r' - r depends only on
@@ -142,30 +171,6 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
 // columns"), and reuses it for all ny voxels of that row as integer shifts.
 // Only the source-side quantities (r^, G_so) and the mask stay per pair.
 constexpr int TS_T = 128;
-
-__device__ __forceinline__ bool mask_open_ts(const Params &p, int v, int q, int cx, int xstate, float uy) {
-    // xstate: 0 = x cell outside the raster, 1 = inside and clear of edges, 2 = near an x edge
-    if (xstate == 0) return false;
-    const float fy = floorf(uy);
-    const float ry = uy - fy;
-    int cy;
-    if (xstate == 2 || ry < kMaskGuard || ry > 1.0f - kMaskGuard) {
-        const double t = p.vt64[v], yr = p.vy64[v];
-        const double xd = p.dx64[q], yd = p.dy64[q];
-        const double px = __dmul_rn(t, xd);
-        const double py = __dadd_rn(yr, __dmul_rn(t, __dsub_rn(yd, yr)));
-        const double gx = floor(__ddiv_rn(__dsub_rn(px, p.m0x), p.mask_pitch64));
-        const double gy = floor(__ddiv_rn(__dsub_rn(py, p.m0y), p.mask_pitch64));
-        if (!(gx >= 0.0 && gy >= 0.0 && gx < (double)p.mask_nx && gy < (double)p.mask_ny)) return false;
-        cx = (int)gx;
-        cy = (int)gy;
-    } else {
-        cy = (int)fy;
-        if (fy < 0.0f || cy >= p.mask_ny) return false;
-    }
-    const uint32_t w = __ldg(p.maskbits + (size_t)cx * p.mask_words + (cy >> 5));
-    return (w >> (cy & 31)) & 1u;
-}
 
 __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai e, const float *__restrict__ W,
                                                       int iz_per_split, double *__restrict__ partial) {
@@ -203,23 +208,36 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
             vp[iy] = make_float4(r.ry, r.rz, r.gso, r.ay);
         }
         __syncthreads();
-        // x part of the mask cell is uniform over the row segment
+        // the x part of the mask cell is uniform over the row segment
         const float ux = fmaf(tq, sx, p.ax);
-        const float fx = floorf(ux), rx = ux - fx;
+        const float fx = floorf(ux);
         const int cx = (int)fx;
-        int xstate = (fx >= 0.0f && cx < p.mask_nx) ? 1 : 0;
-        if (rx < kMaskGuard || rx > 1.0f - kMaskGuard) xstate = 2;
+        const bool x_near = fabsf(ux - fx - 0.5f) > 0.5f - kMaskGuard;
+        const bool x_in = (unsigned)cx < (unsigned)p.mask_nx;
+        const uint32_t *mrow = p.maskbits + (size_t)(x_in ? cx : 0) * p.mask_words;
         float acc = 0.0f;
-        for (int iyb = 0; iyb < ny; iyb += 64) {
-            const int nb_ = min(64, ny - iyb);
-            unsigned long long bits = 0;
-            if (valid)
+        for (int iyb = 0; iyb < ny; iyb += 32) {
+            const int nb_ = min(32, ny - iyb);
+            uint32_t bits = 0, nearb = 0;
+            if (valid && (x_in || x_near))
                 for (int k = 0; k < nb_; k++) {
-                    const int iy = iyb + k;
-                    if (mask_open_ts(p, iy * nz + iz, pix, cx, xstate, fmaf(tq, dd.y, vp[iy].w))) bits |= 1ull << k;
+                    const float uy = fmaf(tq, dd.y, vp[iyb + k].w);
+                    const float fy = floorf(uy);
+                    const int cy = (int)fy;
+                    const bool nr = x_near || fabsf(uy - fy - 0.5f) > 0.5f - kMaskGuard;
+                    bool o = false;
+                    if (x_in && (unsigned)cy < (unsigned)p.mask_ny) o = (__ldg(mrow + (cy >> 5)) >> (cy & 31)) & 1u;
+                    bits |= (uint32_t)o << k;
+                    nearb |= (uint32_t)nr << k;
                 }
+            while (nearb) {
+                const int k = __ffs(nearb) - 1;
+                nearb &= nearb - 1;
+                if (mask_exact(p, (iyb + k) * nz + iz, pix)) bits |= 1u << k;
+                else bits &= ~(1u << k);
+            }
             while (bits) {
-                const int k = __ffsll((long long)bits) - 1;
+                const int k = __ffs(bits) - 1;
                 bits &= bits - 1;
                 const int iy = iyb + k;
                 const float4 v = vp[iy];
@@ -232,9 +250,7 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
                 const float P = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
                 float tau;
                 const int b = locate(e, 0.5f * sin_t * rh, tau);
-                const float *wr = W + (size_t)(iy * nz + iz) * e.nb + b;
-                const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
-                acc = fmaf(P, fmaf(tau, w1 - w0, w0), acc);
+                acc = fmaf(P, lerp_w(W + (size_t)(iy * nz + iz) * e.nb + b, tau), acc);
             }
         }
         tot += (double)acc;
@@ -284,16 +300,27 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     int *hh = hist - win.x;
     unsigned *hl = (unsigned *)(hist + nwin) - win.x;
     if (scale > 0.0f) {
-        // lanes first test the mask for 64 of their pixels, then iterate only
-        // over the open ones (no lane idles on a closed pair)
-        for (int base = 0; base < p.n_det; base += PB_T * 64) {
-            unsigned long long bits = 0;
-            for (int k = 0; k < 64; k++) {
+        // lanes first test the mask for 32 of their pixels (exact re-tests of
+        // near-edge cells in a second pass), then iterate over the open ones
+        for (int base = 0; base < p.n_det; base += PB_T * 32) {
+            uint32_t bits = 0, nearb = 0;
+            for (int k = 0; k < 32; k++) {
                 const int q = base + k * PB_T + tid;
-                if (q < p.n_det && mask_open(p, v, q, vr, p.det[q])) bits |= 1ull << k;
+                if (q < p.n_det) {
+                    bool nr;
+                    const bool o = mask_fast(p, vr, p.det[q], nr);
+                    bits |= (uint32_t)o << k;
+                    nearb |= (uint32_t)nr << k;
+                }
+            }
+            while (nearb) {
+                const int k = __ffs(nearb) - 1;
+                nearb &= nearb - 1;
+                if (mask_exact(p, v, base + k * PB_T + tid)) bits |= 1u << k;
+                else bits &= ~(1u << k);
             }
             while (bits) {
-                const int k = __ffsll((long long)bits) - 1;
+                const int k = __ffs(bits) - 1;
                 bits &= bits - 1;
                 const int q = base + k * PB_T + tid;
                 float P, sh, tau;
@@ -384,24 +411,32 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         alpha[k] = d->energy_kev[k] / (kHc * dq);
         ck[k] = d->scale * d->phi[k] * d->energy_kev[k];
     }
-    std::vector<float> sb;
-    sb.push_back((float)lo);
-    sb.push_back((float)hi);
+    // (fp32 node, exact fp64 kink) pairs; S~ is evaluated at the exact kink so
+    // that nodes which are exactly unreachable stay exactly zero
+    std::vector<std::pair<float, double>> nodes;
+    nodes.push_back({(float)lo, (double)(float)lo});
+    nodes.push_back({(float)hi, (double)(float)hi});
     for (int k = 0; k < K; k++)
         for (int m = -1; m <= Q; m++) {
             const double s = (m + beta0) / alpha[k];
-            if (s > lo && s < hi) sb.push_back((float)s);
+            if (s > lo && s < hi) nodes.push_back({(float)s, s});
         }
-    std::sort(sb.begin(), sb.end());
-    sb.erase(std::unique(sb.begin(), sb.end()), sb.end());
+    std::sort(nodes.begin(), nodes.end());
+    std::vector<float> sb;
+    std::vector<double> sx;
+    for (auto &n : nodes)
+        if (sb.empty() || n.first != sb.back()) {
+            sb.push_back(n.first);
+            sx.push_back(n.second);
+        }
     const int nb = (int)sb.size();
-    // (s_b, 1 / (s_{b+1} - s_b)) and S~ at the fp32 nodes
+    // (s_b, 1 / (s_{b+1} - s_b)) and S~ at the kinks
     std::vector<float2> bp(nb);
     std::vector<float> stab((size_t)nb * Q, 0.0f);
     std::vector<double> row(Q);
     for (int b = 0; b < nb; b++) {
-        const double s = sb[b];
-        bp[b] = make_float2(sb[b], b + 1 < nb ? (float)(1.0 / ((double)sb[b + 1] - s)) : 0.0f);
+        const double s = sx[b];
+        bp[b] = make_float2(sb[b], b + 1 < nb ? (float)(1.0 / ((double)sb[b + 1] - (double)sb[b])) : 0.0f);
         std::fill(row.begin(), row.end(), 0.0);
         for (int k = 0; k < K; k++) {
             const double u = alpha[k] * s - beta0;
@@ -412,11 +447,14 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         }
         for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)row[j];
     }
-    // uniform LUT over [s_0, s_{nb-1}]
+    // uniform LUT over [s_0, s_{nb-1}]: {s_b, 1/gap_b, s_{b+1}, b} of the cell start
     const int nl = std::max(64, 8 * nb);
     const double span = (double)sb[nb - 1] - sb[0];
-    std::vector<int> lut(nl);
-    for (int c = 0; c < nl; c++) lut[c] = host_locate(sb, (float)(sb[0] + span * c / nl));
+    std::vector<float4> lut(nl);
+    for (int c = 0; c < nl; c++) {
+        const int b = host_locate(sb, (float)(sb[0] + span * c / nl));
+        lut[c] = make_float4(bp[b].x, bp[b].y, sb[b + 1], __int_as_float_host(b));
+    }
     // per-voxel breakpoint windows (deposits land in [locate(min), locate(max) + 1])
     std::vector<int2> vwin(nv);
     int max_win = 1;
@@ -426,8 +464,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     }
     e = cudaMalloc(&g->d_esai_bp, nb * sizeof(float2));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_bp, bp.data(), nb * sizeof(float2), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(int));
-    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(float4));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(float4), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_stab, stab.size() * sizeof(float));
     if (e == cudaSuccess)
         e = cudaMemcpy(g->d_esai_stab, stab.data(), stab.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -440,7 +478,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.s0 = sb[0];
     E.inv_h = (float)(nl / span);
     E.bp = (const float2 *)g->d_esai_bp;
-    E.lut = (const int *)g->d_esai_lut;
+    E.lut4 = (const float4 *)g->d_esai_lut;
     E.stab = (const float *)g->d_esai_stab;
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.ptot = (const float *)g->d_esai_ptot;

@@ -64,7 +64,7 @@ struct Esai {
     int lo_bits;        // fixed-point split of the backward deposits (esai.cu)
     float s0, inv_h;    // cell c = (sigma - s0) * inv_h
     const float2 *bp;   // (s_b, 1 / (s_{b+1} - s_b))
-    const int *lut;     // first-guess b per cell
+    const float4 *lut4; // per cell {s_b, 1/(s_{b+1}-s_b), s_{b+1}, b (int bits)} at the cell start
     const float *stab;  // S~ [nb][nq] (scale, phi_k, E_k folded in)
     const int2 *vwin;   // per voxel [b_lo, b_hi] reachable by any of its pairs
     const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)

@@ -17,33 +17,42 @@ namespace cacsi {
 
 __device__ __forceinline__ float fast_sqrt(float x) { return x * rsqrtf(fmaxf(x, 1e-30f)); }
 
-// T(r, r') in {0, 1}.  fp32 fast path; within kMaskGuard cells of a cell edge
-// the exact fp64 rule of reading R8 (same op order as the definition, no FMA
-// contraction: __d*_rn intrinsics) decides, so T is bit-identical to the
-// definition whenever the fp32 error is below the guard (K2).
-__device__ __forceinline__ bool mask_open(const Params &p, int v, int q, const VoxelRec &vr, float2 d) {
+// T(r, r') in {0, 1} by the exact fp64 rule of reading R8: same op order as
+// the definition, no FMA contraction (__d*_rn intrinsics), on the fp64 centre
+// tables.  Bit-identical to the definition.
+__device__ __forceinline__ bool mask_exact(const Params &p, int v, int q) {
+    const double t = p.vt64[v], yr = p.vy64[v];
+    const double xd = p.dx64[q], yd = p.dy64[q];
+    const double px = __dmul_rn(t, xd);
+    const double py = __dadd_rn(yr, __dmul_rn(t, __dsub_rn(yd, yr)));
+    const double gx = floor(__ddiv_rn(__dsub_rn(px, p.m0x), p.mask_pitch64));
+    const double gy = floor(__ddiv_rn(__dsub_rn(py, p.m0y), p.mask_pitch64));
+    if (!(gx >= 0.0 && gy >= 0.0 && gx < (double)p.mask_nx && gy < (double)p.mask_ny)) return false;
+    const int ix = (int)gx, iy = (int)gy;
+    const uint32_t w = __ldg(p.maskbits + (size_t)ix * p.mask_words + (iy >> 5));
+    return (w >> (iy & 31)) & 1u;
+}
+
+// fp32 fast path of T: u = (t/p) x + const per axis, cell = floor(u).  *near is
+// set when u lies within kMaskGuard cells of a cell edge (the fp32 error bound
+// is well below the guard, K2); the result is then undefined and the
+// caller must use mask_exact.  Kept branch-free so batched callers stay
+// converged; the exact re-tests run in a separate pass.
+__device__ __forceinline__ bool mask_fast(const Params &p, const VoxelRec &vr, float2 d, bool &near) {
     const float ux = fmaf(vr.tq, d.x, p.ax);
     const float uy = fmaf(vr.tq, d.y, vr.ay);
     const float fx = floorf(ux), fy = floorf(uy);
-    const float rx = ux - fx, ry = uy - fy;
-    int ix, iy;
-    if (rx < kMaskGuard || rx > 1.0f - kMaskGuard || ry < kMaskGuard || ry > 1.0f - kMaskGuard) {
-        const double t = p.vt64[v], yr = p.vy64[v];
-        const double xd = p.dx64[q], yd = p.dy64[q];
-        const double px = __dmul_rn(t, xd);
-        const double py = __dadd_rn(yr, __dmul_rn(t, __dsub_rn(yd, yr)));
-        const double gx = floor(__ddiv_rn(__dsub_rn(px, p.m0x), p.mask_pitch64));
-        const double gy = floor(__ddiv_rn(__dsub_rn(py, p.m0y), p.mask_pitch64));
-        if (!(gx >= 0.0 && gy >= 0.0 && gx < (double)p.mask_nx && gy < (double)p.mask_ny)) return false;
-        ix = (int)gx;
-        iy = (int)gy;
-    } else {
-        ix = (int)fx;
-        iy = (int)fy;
-        if (fx < 0.0f || fy < 0.0f || ix >= p.mask_nx || iy >= p.mask_ny) return false;
-    }
+    near = fabsf(ux - fx - 0.5f) > 0.5f - kMaskGuard || fabsf(uy - fy - 0.5f) > 0.5f - kMaskGuard;
+    const int ix = (int)fx, iy = (int)fy;
+    if ((unsigned)ix >= (unsigned)p.mask_nx || (unsigned)iy >= (unsigned)p.mask_ny) return false;
     const uint32_t w = __ldg(p.maskbits + (size_t)ix * p.mask_words + (iy >> 5));
     return (w >> (iy & 31)) & 1u;
+}
+
+__device__ __forceinline__ bool mask_open(const Params &p, int v, int q, const VoxelRec &vr, float2 d) {
+    bool near;
+    const bool o = mask_fast(p, vr, d, near);
+    return near ? mask_exact(p, v, q) : o;
 }
 
 // P (without C_E) and sin(theta/2) of one pair.
