@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
     const int v1 = min(p.n_vox, v0 + vox_per_split);
     double tot = 0.0;
     for (int c0 = v0; c0 < v1; c0 += PF_CH) {
+        __syncwarp();  // reconverge after the previous batch's divergent pair loop
         const int nc = min(PF_CH, v1 - c0);
         uint32_t bits = 0, nearb = 0;
         if (valid)
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
         const uint32_t *mrow = p.maskbits + (size_t)(x_in ? cx : 0) * p.mask_words;
         float acc = 0.0f;
         for (int iyb = 0; iyb < ny; iyb += 32) {
+            __syncwarp();  // reconverge after the previous batch's divergent pair loop
             const int nb_ = min(32, ny - iyb);
             uint32_t bits = 0, nearb = 0;
             if (valid && (x_in || x_near))
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
         // lanes first test the mask for 32 of their pixels (exact re-tests of
         // near-edge cells in a second pass), then iterate over the open ones
         for (int base = 0; base < p.n_det; base += PB_T * 32) {
+            __syncwarp();  // reconverge after the previous batch's divergent pair loop
             uint32_t bits = 0, nearb = 0;
             for (int k = 0; k < 32; k++) {
                 const int q = base + k * PB_T + tid;
