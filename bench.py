@@ -183,6 +183,8 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    G.kernel_times()   # discard
+    G.set_timing(True)  # CUDA events around every libcacsi kernel (same stream)
     clocks = ClockSampler(local)
     clocks.start()
     evs = [[E() for _ in range(5)] for _ in range(args.steps)]
@@ -191,6 +193,8 @@ def run_gpu(args):
         step(evs[i])
     torch.cuda.synchronize()
     ck = clocks.stop()
+    G.set_timing(False)
+    ktimes = G.kernel_times()
     t_fwd = [e[0].elapsed_time(e[1]) for e in evs]
     t_bwd = [e[2].elapsed_time(e[3]) for e in evs]
     t_step = [e[0].elapsed_time(e[4]) for e in evs]
@@ -221,25 +225,29 @@ def run_gpu(args):
     h2d = (fh.nbytes + yh.nbytes + rh.nbytes + b1h.nbytes)
     d2h = fh.nbytes
 
-    # ---- roofline of the dominant kernel (DESIGN.md §Measurement)
+    # ---- roofline of the dominant kernel (DESIGN.md §8)
+    mf, mb = float(np.mean(t_fwd)), float(np.mean(t_bwd))
+    counts = json.load(open(os.path.join(ROOT, "workloads", "work_counts.json")))[str(cfg.seed)]
+    nb_bp = G.query("esai_breakpoints")
+    kern = {k: {"avg_ms": v[0] / v[1], "launches": v[1]} for k, v in ktimes.items()}
+    dom = max(kern, key=lambda k: kern[k]["avg_ms"] * kern[k]["launches"])
+    flops = alg_flops(dom, cfg, counts, nb_bp)
+    achieved = flops / (kern[dom]["avg_ms"] / 1e3) / 1e12
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_tf = sms * 128 * 2 * 1965e6 / 1e12  # FP32 lanes x FMA x max SM clock
+    roofline = {"bound": "alu", "kernel": dom, "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": None,
+                "algorithmic_flops_per_launch": flops, "avg_launch_ms": kern[dom]["avg_ms"],
+                "peak_note": f"{sms} SMs x 128 FP32 lanes x 2 flop (FMA) x 1965 MHz max clock, derived "
+                             "(DESIGN.md §8); algorithmic flops per DESIGN.md §8 table"}
+    if ck.get("sm_mhz"):
+        roofline["frac_at_observed_clock"] = round(achieved / (peak_tf * ck["sm_mhz"] / 1965.0), 4)
+    eff = counts["effective_terms"]
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    mf, mb = float(np.mean(t_fwd)), float(np.mean(t_bwd))
-    eff = effective_terms(cfg)
-    dom = "backward" if mb >= mf else "forward"
-    flops_per_term = {"forward": 7.0, "backward": 9.0}[dom]
-    achieved = eff * flops_per_term / ((mb if dom == "backward" else mf) / 1e3) / 1e12
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    peak_tf = sms * 128 * 2 * 1965e6 / 1e12  # FP32 lanes x FMA x max SM clock
-    roofline = {"bound": "alu", "kernel": f"cacsi_{dom}", "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": None,
-                "peak_note": f"{sms} SMs x 128 FP32 lanes x 2 x 1965 MHz (max clock); "
-                             f"{flops_per_term:g} algorithmic flops per effective term"}
-    if ck.get("sm_mhz"):
-        roofline["frac_at_observed_clock"] = round(achieved / (peak_tf * ck["sm_mhz"] / 1965.0), 4)
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -252,8 +260,9 @@ def run_gpu(args):
         "forward_ms": mf, "backward_ms": mb,
         "forward_pairs_per_s": pairs / (mf / 1e3), "backward_pairs_per_s": pairs / (mb / 1e3),
         "nominal_terms_per_s": 2 * nominal_terms * world / (ms_per_step / 1e3),
-        "effective_terms_per_s": 2 * eff * world / (ms_per_step / 1e3),
+        "effective_terms_per_s": 2 * float(eff) * world / (ms_per_step / 1e3),
         "gpu_launches": launches_per_step[0] * args.steps,
+        "kernels": kern, "esai_breakpoints": nb_bp, "ts_rho": G.query("ts_rho"),
         "clocks": ck, "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": float(np.mean(e2e_ms))},
@@ -269,12 +278,22 @@ def run_gpu(args):
         print(json.dumps(out), flush=True)
 
 
-def effective_terms(cfg) -> float:
-    """Effective terms (open pair x energy with -1 < u_k < nq) per operator
-    application: exact counts written by scripts/count_terms.py from the
-    oracle's counter (workloads/work_counts.json)."""
-    counts = json.load(open(os.path.join(ROOT, "workloads", "work_counts.json")))
-    return float(counts[str(cfg.seed if cfg.seed in (0, 1, 2, 4) else 1)]["effective_terms"])
+def alg_flops(kernel, cfg, counts, nb):
+    """Algorithmic FP32 flops (FMA = 2) of one launch of a libcacsi kernel on
+    this workload (DESIGN.md §8 table): the minimal arithmetic of the formulas
+    the kernel evaluates, times the units it processes."""
+    pairs, open_ = counts["pairs"], counts["open_pairs"]
+    gemm = 2.0 * cfg.n_vox * nb * cfg.nq
+    table = {
+        "k_sgemm_W": gemm,                             # W = F S~^T
+        "k_sgemm_b2": gemm,                            # b2 = A S~
+        "k_esai_fwd": 10 * pairs + (46 + 11) * open_,  # mask, pair geometry, locate + lerp + accumulate
+        "k_esai_fwd_ts": 5 * pairs + (23 + 11) * open_,  # TS: footprint shared, x-mask uniform
+        "k_esai_bwd": 10 * pairs + (46 + 6 + 12) * open_,  # mask, geometry, locate, fixed-point deposits
+        "k_forward": 10 * pairs + 46 * open_ + 7 * counts["effective_terms"],
+        "k_backward": 10 * pairs + 46 * open_ + 9 * counts["effective_terms"],
+    }
+    return float(table.get(kernel, 0.0))
 
 
 # --------------------------------------------------------- CPU (oracle) arm --

@@ -180,6 +180,20 @@ CACSI_API cacsi_status cacsi_iterate_host(const cacsi_geometry *geom, float *f_h
  * (for the bench's gpu_launches count).                                     */
 CACSI_API int32_t cacsi_last_launch_count(const cacsi_geometry *geom);
 
+/* Per-kernel timing: when enabled, every kernel the handle launches is
+ * bracketed by a CUDA event pair on the launching stream.
+ * cacsi_kernel_times synchronises those events, returns the number of distinct
+ * kernel names (<= max) and fills names[i] (static strings), total_ms[i] and
+ * launches[i] accumulated since the previous query, then resets.            */
+CACSI_API cacsi_status cacsi_set_timing(const cacsi_geometry *geom, int32_t enable);
+CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, const char **names, double *total_ms,
+                                     int32_t *launches);
+
+/* Integer facts about a handle: "esai_breakpoints" (0 if the per-term
+ * kernels are used), "esai_max_window", "ts_rho" (0 = no translation
+ * symmetry), "energy_resolving".  -1 for an unknown key or NULL.           */
+CACSI_API int64_t cacsi_query(const cacsi_geometry *geom, const char *key);
+
 /* Static description of a status code (never NULL). */
 CACSI_API const char *cacsi_status_string(cacsi_status status);
 

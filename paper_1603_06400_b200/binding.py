@@ -23,7 +23,8 @@ CACSI_OK, CACSI_ERR_NULL, CACSI_ERR_INVALID, CACSI_ERR_CUDA, CACSI_ERR_NOMEM = r
 SYMBOLS = ["cacsi_geometry_create", "cacsi_geometry_destroy", "cacsi_workspace_bytes", "cacsi_object_size",
            "cacsi_detector_size", "cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate",
            "cacsi_forward_host", "cacsi_backward_host", "cacsi_iterate_host", "cacsi_last_launch_count",
-           "cacsi_status_string", "cacsi_ratio", "cacsi_update"]
+           "cacsi_status_string", "cacsi_ratio", "cacsi_update", "cacsi_set_timing", "cacsi_kernel_times",
+           "cacsi_query"]
 
 
 class CacsiError(RuntimeError):
@@ -85,6 +86,13 @@ def lib():
             getattr(L, n).restype = ctypes.c_int
         L.cacsi_last_launch_count.argtypes = [vp]
         L.cacsi_last_launch_count.restype = ctypes.c_int32
+        L.cacsi_set_timing.argtypes = [vp, ctypes.c_int32]
+        L.cacsi_set_timing.restype = ctypes.c_int
+        L.cacsi_kernel_times.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_char_p),
+                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]
+        L.cacsi_kernel_times.restype = ctypes.c_int32
+        L.cacsi_query.argtypes = [vp, ctypes.c_char_p]
+        L.cacsi_query.restype = ctypes.c_int64
         L.cacsi_status_string.argtypes = [ctypes.c_int]
         L.cacsi_status_string.restype = ctypes.c_char_p
         _lib = L
@@ -163,6 +171,21 @@ class Geometry:
             self.close()
         except Exception:
             pass
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().cacsi_set_timing(self.handle, int(enable)), "cacsi_set_timing")
+
+    def kernel_times(self) -> dict:
+        """{kernel name: (total ms, launches)} since the previous call."""
+        n = 64
+        names = (ctypes.c_char_p * n)()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int32 * n)()
+        k = lib().cacsi_kernel_times(self.handle, n, names, ms, cnt)
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(k)}
+
+    def query(self, key: str) -> int:
+        return lib().cacsi_query(self.handle, key.encode())
 
     @property
     def last_launch_count(self) -> int:

@@ -260,6 +260,13 @@ void cacsi_geometry_destroy(cacsi_geometry *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
+    if (g->timers) {
+        const char *names[64];
+        double ms[64];
+        int32_t n[64];
+        cacsi_kernel_times(g, 64, names, ms, n);  // releases the recorded events
+        delete (cacsi::Timers *)g->timers;
+    }
     free_all(g);
     free(g);
 }
@@ -406,6 +413,70 @@ cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float 
     e = cudaMemcpyAsync(fh, g->d_stage_a, g->n_obj * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return map_err(e);
+}
+
+}  // extern "C"
+
+// ---- per-kernel CUDA-event timing ------------------------------------------
+namespace cacsi {
+KScope::KScope(const cacsi_geometry *g_, cudaStream_t s_, const char *name_) : g(g_), s(s_), name(name_) {
+    if (g && g->timing && g->timers) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+    }
+}
+KScope::~KScope() {
+    if (a) {
+        cudaEventRecord(b, s);
+        ((Timers *)g->timers)->recs.push_back({name, a, b});
+    }
+}
+}  // namespace cacsi
+
+extern "C" {
+
+cacsi_status cacsi_set_timing(const cacsi_geometry *g, int32_t enable) {
+    if (!g) return CACSI_ERR_NULL;
+    if (!g->timers) const_cast<cacsi_geometry *>(g)->timers = new cacsi::Timers();
+    g->timing = enable ? 1 : 0;
+    return CACSI_OK;
+}
+
+int32_t cacsi_kernel_times(const cacsi_geometry *g, int32_t max, const char **names, double *total_ms,
+                           int32_t *launches) {
+    if (!g || !g->timers) return 0;
+    auto &recs = ((cacsi::Timers *)g->timers)->recs;
+    int32_t n = 0;
+    for (auto &r : recs) {
+        float ms = 0.0f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+        int i = 0;
+        while (i < n && strcmp(names[i], r.name) != 0) i++;
+        if (i == n) {
+            if (n >= max) continue;
+            names[n] = r.name;
+            total_ms[n] = 0.0;
+            launches[n] = 0;
+            n++;
+        }
+        total_ms[i] += ms;
+        launches[i] += 1;
+    }
+    recs.clear();
+    return n;
+}
+
+int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
+    if (!g || !key) return -1;
+    if (!strcmp(key, "esai_breakpoints")) return g->esai.enabled ? g->esai.nb : 0;
+    if (!strcmp(key, "ts_rho")) return g->p.ts_rho;
+    if (!strcmp(key, "esai_max_window")) return g->esai.enabled ? g->esai.max_win : 0;
+    if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
+    return -1;
 }
 
 }  // extern "C"

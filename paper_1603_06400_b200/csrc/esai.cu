@@ -238,21 +238,34 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
                 if (mask_exact(p, (iyb + k) * nz + iz, pix)) bits |= 1u << k;
                 else bits &= ~(1u << k);
             }
+            // two open pairs per iteration: independent load chains overlap
             while (bits) {
-                const int k = __ffs(bits) - 1;
+                const int k1 = __ffs(bits) - 1;
                 bits &= bits - 1;
-                const int iy = iyb + k;
-                const float4 v = vp[iy];
-                const float4 f = foot[tid + rho * (ny - 1 - iy)];
-                const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
-                const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
-                const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
-                const float h = fmaf(0.5f, cos_t, 0.5f);
-                const float rh = rsqrtf(h);
-                const float P = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
-                float tau;
-                const int b = locate(e, 0.5f * sin_t * rh, tau);
-                acc = fmaf(P, lerp_w(W + (size_t)(iy * nz + iz) * e.nb + b, tau), acc);
+                const bool two = bits != 0;
+                const int k2 = two ? __ffs(bits) - 1 : k1;
+                bits &= bits - 1;
+                float Pp[2], sh[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const int iy = iyb + (u ? k2 : k1);
+                    const float4 v = vp[iy];
+                    const float4 f = foot[tid + rho * (ny - 1 - iy)];
+                    const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
+                    const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
+                    const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
+                    const float h = fmaf(0.5f, cos_t, 0.5f);
+                    const float rh = rsqrtf(h);
+                    Pp[u] = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
+                    sh[u] = 0.5f * sin_t * rh;
+                }
+                float t1, t2;
+                const int b1 = locate(e, sh[0], t1);
+                const int b2 = locate(e, sh[1], t2);
+                const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.nb + b1, t1);
+                const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.nb + b2, t2);
+                acc = fmaf(Pp[0], w1, acc);
+                acc = fmaf(two ? Pp[1] : 0.0f, w2, acc);
             }
         }
         tot += (double)acc;
@@ -275,6 +288,18 @@ __global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, si
 }
 
 constexpr int PB_T = 256;
+
+// fixed-point deposit of a (1 - tau) into bin b and a tau into bin b + 1
+__device__ __forceinline__ void deposit(int *hh, unsigned *hl, int b, float a, float tau, float inv_lo,
+                                        float lo_unit) {
+    const float x1 = rintf(a * tau);
+    const float x0 = rintf(a) - x1;
+    const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
+    atomicAdd(hh + b, (int)h0);
+    atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
+    atomicAdd(hh + b + 1, (int)h1);
+    atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
+}
 
 // Backward pair stage: A[v, b] = sum_pixels P w hat_b(sigma), one CTA per voxel.
 // Deposits go to a shared-memory histogram over the voxel's breakpoint window
@@ -322,21 +347,23 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
                 if (mask_exact(p, v, base + k * PB_T + tid)) bits |= 1u << k;
                 else bits &= ~(1u << k);
             }
+            // two open pairs per iteration: independent load chains overlap
             while (bits) {
-                const int k = __ffs(bits) - 1;
+                const int k1 = __ffs(bits) - 1;
                 bits &= bits - 1;
-                const int q = base + k * PB_T + tid;
-                float P, sh, tau;
-                pair_geom(p, vr, p.det[q], P, sh);
-                const int b = locate(e, sh, tau);
-                const float a = P * __ldg(w + q) * scale;
-                const float x1 = rintf(a * tau);
-                const float x0 = rintf(a) - x1;
-                const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
-                atomicAdd(hh + b, (int)h0);
-                atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
-                atomicAdd(hh + b + 1, (int)h1);
-                atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
+                const bool two = bits != 0;
+                const int k2 = two ? __ffs(bits) - 1 : k1;
+                bits &= bits - 1;
+                const int q1 = base + k1 * PB_T + tid, q2 = base + k2 * PB_T + tid;
+                float P1, s1, P2, s2, t1, t2;
+                pair_geom(p, vr, p.det[q1], P1, s1);
+                pair_geom(p, vr, p.det[q2], P2, s2);
+                const int b1 = locate(e, s1, t1);
+                const int b2 = locate(e, s2, t2);
+                const float a1 = P1 * __ldg(w + q1) * scale;
+                const float a2 = two ? P2 * __ldg(w + q2) * scale : 0.0f;
+                deposit(hh, hl, b1, a1, t1, inv_lo, lo_unit);
+                deposit(hh, hl, b2, a2, t2, inv_lo, lo_unit);
             }
         }
     }
@@ -510,20 +537,32 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
     if (e == cudaSuccess) {
         // W[v][b] = sum_j f[v][j] S~[b][j]
         dim3 gg((E.nb + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, 1);
-        k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
+        {
+            KScope kt_(g, s, "k_sgemm_W");
+            k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
+        }
         if (p.ts_rho > 0) {
             const int segs = p.det_nx * ((p.det_ny + TS_T - 1) / TS_T);
-            int St = std::max(1, std::min((target + segs - 1) / segs, p.nz));
+            int St = std::max(1, std::min((4 * target + segs - 1) / segs, p.nz));
             const int izps = (p.nz + St - 1) / St;
             St = (p.nz + izps - 1) / izps;
             const size_t smem = (size_t)(TS_T + p.ts_rho * (p.ny - 1) + p.ny) * sizeof(float4);
             cudaFuncSetAttribute(k_esai_fwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_fwd_ts<<<dim3(segs, St), TS_T, smem, s>>>(p, E, W, izps, part);
+            {
+                KScope kt_(g, s, "k_esai_fwd_ts");
+                k_esai_fwd_ts<<<dim3(segs, St), TS_T, smem, s>>>(p, E, W, izps, part);
+            }
             S = St;
         } else {
-            k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
+            {
+                KScope kt_(g, s, "k_esai_fwd");
+                k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
+            }
         }
-        k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
+        {
+            KScope kt_(g, s, "k_sum_parts_f64");
+            k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
+        }
         e = cudaGetLastError();
         *launches += 3;
     }
@@ -543,14 +582,26 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
     if (e == cudaSuccess) {
-        k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
+        {
+            KScope kt_(g, s, "k_absmax");
+            k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
+        }
         const size_t smem = (size_t)E.max_win * 2 * sizeof(int);
         cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_esai_bwd<<<p.n_vox, PB_T, smem, s>>>(p, E, w, wmax, A);
+        {
+            KScope kt_(g, s, "k_esai_bwd");
+            k_esai_bwd<<<p.n_vox, PB_T, smem, s>>>(p, E, w, wmax, A);
+        }
         dim3 gg((p.nq + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, S_eff);
-        k_sgemm<false><<<gg, GM_T, 0, s>>>(p.n_vox, p.nq, E.nb, kps, A, E.stab, part);
+        {
+            KScope kt_(g, s, "k_sgemm_b2");
+            k_sgemm<false><<<gg, GM_T, 0, s>>>(p.n_vox, p.nq, E.nb, kps, A, E.stab, part);
+        }
         const size_t n = (size_t)p.n_vox * p.nq;
-        k_sum_parts_f32<<<(int)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S_eff, n, b);
+        {
+            KScope kt_(g, s, "k_sum_parts_f32");
+            k_sum_parts_f32<<<(int)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S_eff, n, b);
+        }
         e = cudaGetLastError();
         *launches += 4;
     }

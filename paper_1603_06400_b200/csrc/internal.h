@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "cacsi.h"
 
 namespace cacsi {
@@ -86,9 +88,31 @@ struct cacsi_geometry {
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;
+    // per-kernel CUDA-event timing (cacsi_set_timing / cacsi_kernel_times)
+    mutable int32_t timing;
+    void *timers;  // cacsi::Timers*
 };
 
 namespace cacsi {
+
+struct TimerRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+struct Timers {
+    std::vector<TimerRec> recs;
+};
+
+// Records a CUDA event pair around one kernel launch when timing is enabled
+// on the handle (the bench's "kernel duration measured live with events").
+struct KScope {
+    const cacsi_geometry *g;
+    cudaStream_t s;
+    const char *name;
+    cudaEvent_t a = nullptr, b = nullptr;
+    KScope(const cacsi_geometry *g_, cudaStream_t s_, const char *name_);
+    ~KScope();
+};
 
 // launchers (operators.cu / recon.cu).  Each returns a cudaError_t of the
 // first failing launch and adds the number of kernels enqueued to *launches.

@@ -218,18 +218,30 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     dim3 grid(tiles, S);
     if (res) {
         cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_forward<true><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+        {
+            KScope kt_(g, s, "k_forward_er");
+            k_forward<true><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+        }
     } else {
         cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_forward<false><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+        {
+            KScope kt_(g, s, "k_forward");
+            k_forward<false><<<grid, FWD_T, smem, s>>>(p, f, vps, part);
+        }
     }
     e = cudaGetLastError();
     if (e == cudaSuccess) {
         const int nb = (int)min((n_out + 255) / 256, (size_t)(16 * num_sms(g->device)));
         if (res)
-            k_sum_f32<<<nb, 256, 0, s>>>((const float *)part, S, n_out, out);
+            {
+                KScope kt_(g, s, "k_sum_f32");
+                k_sum_f32<<<nb, 256, 0, s>>>((const float *)part, S, n_out, out);
+            }
         else
-            k_sum_f64<<<nb, 256, 0, s>>>((const double *)part, S, n_out, out);
+            {
+                KScope kt_(g, s, "k_sum_f64");
+                k_sum_f64<<<nb, 256, 0, s>>>((const double *)part, S, n_out, out);
+            }
         e = cudaGetLastError();
     }
     cudaFreeAsync(part, s);
@@ -244,10 +256,16 @@ cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, c
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
     if (p.energy_resolving) {
         cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+        {
+            KScope kt_(g, s, "k_backward_er");
+            k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+        }
     } else {
         cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_backward<false><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+        {
+            KScope kt_(g, s, "k_backward");
+            k_backward<false><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+        }
     }
     *launches += 1;
     return cudaGetLastError();

@@ -129,14 +129,20 @@ size_t recon_workspace_bytes(const cacsi_geometry *g) {
 
 cudaError_t launch_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
                          double *, int, cudaStream_t s, int *launches) {
-    k_ratio<<<grid_for(g->n_detout), RT, 0, s>>>(l, y, r, ratio, g->n_detout);
+    {
+        KScope kt_(g, s, "k_ratio");
+        k_ratio<<<grid_for(g->n_detout), RT, 0, s>>>(l, y, r, ratio, g->n_detout);
+    }
     *launches += 1;
     return cudaGetLastError();
 }
 
 cudaError_t launch_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
                           float *f_new, cudaStream_t s, int *launches) {
-    k_update<<<grid_for(g->n_obj), RT, 0, s>>>(g->p, f_hat, b1, b2, beta, f_new);
+    {
+        KScope kt_(g, s, "k_update");
+        k_update<<<grid_for(g->n_obj), RT, 0, s>>>(g->p, f_hat, b1, b2, beta, f_new);
+    }
     *launches += 1;
     return cudaGetLastError();
 }
