@@ -68,7 +68,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_tb_fwd, g->d_tb_bwd};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -101,6 +101,15 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return CACSI_ERR_CUDA;
     if (cudaSetDevice(device) != cudaSuccess) return CACSI_ERR_CUDA;
+    // keep stream-ordered scratch (W / A, split partials) cached across calls
+    // instead of returning it to the OS at every synchronisation
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
 
     cacsi_geometry *g = (cacsi_geometry *)calloc(1, sizeof(cacsi_geometry));
     if (!g) return CACSI_ERR_NOMEM;

@@ -85,6 +85,65 @@ int host_locate(const std::vector<float> &sb, float s) {
     return std::max(0, std::min(nb - 2, b));
 }
 
+
+// ---- transmission bitmaps (built once at create) ---------------------------
+// One thread per 32-bit word: 32 mask tests by the exact rule (fp32 fast path,
+// fp64 re-test near cell edges), packed in the order the pair kernels visit.
+__global__ void k_tbits_fwd_tiled(const Params p, uint32_t *tb) {
+    // word (c, pix): bit i = T(voxel 32c + i, pix)
+    const size_t n = (size_t)((p.n_vox + 31) / 32) * p.n_det;
+    for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n; w += (size_t)gridDim.x * blockDim.x) {
+        const int c = (int)(w / p.n_det), pix = (int)(w % p.n_det);
+        const float2 d = p.det[pix];
+        uint32_t bits = 0;
+        for (int i = 0; i < 32; i++) {
+            const int v = c * 32 + i;
+            if (v < p.n_vox && mask_open(p, v, pix, p.vox[v], d)) bits |= 1u << i;
+        }
+        tb[w] = bits;
+    }
+}
+
+__global__ void k_tbits_fwd_ts(const Params p, uint32_t *tb) {
+    // word ((iz * det_nx + ix) * nyb + c) * det_ny + jy: bit k = T(voxel (32c + k, iz), pixel (ix, jy))
+    const int nyb = (p.ny + 31) / 32;
+    const size_t n = (size_t)p.nz * p.det_nx * nyb * p.det_ny;
+    for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n; w += (size_t)gridDim.x * blockDim.x) {
+        const int jy = (int)(w % p.det_ny);
+        size_t r = w / p.det_ny;
+        const int c = (int)(r % nyb);
+        r /= nyb;
+        const int ix = (int)(r % p.det_nx), iz = (int)(r / p.det_nx);
+        const int pix = ix * p.det_ny + jy;
+        const float2 d = p.det[pix];
+        uint32_t bits = 0;
+        for (int k = 0; k < 32; k++) {
+            const int iy = c * 32 + k;
+            if (iy < p.ny && mask_open(p, iy * p.nz + iz, pix, p.vox[iy * p.nz + iz], d)) bits |= 1u << k;
+        }
+        tb[w] = bits;
+    }
+}
+
+template <int T>
+__global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
+    // word (v * nbatch + batch) * T + lane: bit k = T(v, pixel batch*32*T + k*T + lane)
+    const int nbatch = (p.n_det + 32 * T - 1) / (32 * T);
+    const size_t n = (size_t)p.n_vox * nbatch * T;
+    for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n; w += (size_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(w % T);
+        const size_t r = w / T;
+        const int batch = (int)(r % nbatch), v = (int)(r / nbatch);
+        const VoxelRec vr = p.vox[v];
+        uint32_t bits = 0;
+        for (int k = 0; k < 32; k++) {
+            const int q = batch * 32 * T + k * T + lane;
+            if (q < p.n_det && mask_open(p, v, q, vr, p.det[q])) bits |= 1u << k;
+        }
+        tb[w] = bits;
+    }
+}
+
 // ------------------------------------------------------------ device side --
 // b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0, 1].
 // One 16-byte LUT load {s_b, 1/(s_{b+1}-s_b), s_{b+1}, b} settles the common
@@ -134,20 +193,8 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
     for (int c0 = v0; c0 < v1; c0 += PF_CH) {
         __syncwarp();  // reconverge after the previous batch's divergent pair loop
         const int nc = min(PF_CH, v1 - c0);
-        uint32_t bits = 0, nearb = 0;
-        if (valid)
-            for (int i = 0; i < nc; i++) {
-                bool nr;
-                const bool o = mask_fast(p, p.vox[c0 + i], d, nr);
-                bits |= (uint32_t)o << i;
-                nearb |= (uint32_t)nr << i;
-            }
-        while (nearb) {
-            const int i = __ffs(nearb) - 1;
-            nearb &= nearb - 1;
-            if (mask_exact(p, c0 + i, pix)) bits |= 1u << i;
-            else bits &= ~(1u << i);
-        }
+        uint32_t bits = valid ? __ldg(e.tb_fwd + (size_t)(c0 / PF_CH) * p.n_det + pix) : 0u;
+        (void)nc;
         float acc = 0.0f;
         while (bits) {
             const int i = __ffs(bits) - 1;
@@ -193,7 +240,7 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
     double tot = 0.0;
     for (int iz = iz0; iz < iz1; iz++) {
         const VoxelRec r0 = p.vox[iz];  // iy = 0: z-row quantities
-        const float sz = r0.sz, tq = r0.tq;
+        const float sz = r0.sz;
         __syncthreads();
         for (int i = tid; i < nfoot; i += TS_T) {
             const float sy = fmaf(p.pitch_d, (float)(dmin + i), p.ts_c0);
@@ -209,35 +256,12 @@ __global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai
             vp[iy] = make_float4(r.ry, r.rz, r.gso, r.ay);
         }
         __syncthreads();
-        // the x part of the mask cell is uniform over the row segment
-        const float ux = fmaf(tq, sx, p.ax);
-        const float fx = floorf(ux);
-        const int cx = (int)fx;
-        const bool x_near = fabsf(ux - fx - 0.5f) > 0.5f - kMaskGuard;
-        const bool x_in = (unsigned)cx < (unsigned)p.mask_nx;
-        const uint32_t *mrow = p.maskbits + (size_t)(x_in ? cx : 0) * p.mask_words;
+        const int nyb = (ny + 31) / 32;
+        const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + ix) * nyb) * p.det_ny + (valid ? jy : 0);
         float acc = 0.0f;
         for (int iyb = 0; iyb < ny; iyb += 32) {
             __syncwarp();  // reconverge after the previous batch's divergent pair loop
-            const int nb_ = min(32, ny - iyb);
-            uint32_t bits = 0, nearb = 0;
-            if (valid && (x_in || x_near))
-                for (int k = 0; k < nb_; k++) {
-                    const float uy = fmaf(tq, dd.y, vp[iyb + k].w);
-                    const float fy = floorf(uy);
-                    const int cy = (int)fy;
-                    const bool nr = x_near || fabsf(uy - fy - 0.5f) > 0.5f - kMaskGuard;
-                    bool o = false;
-                    if (x_in && (unsigned)cy < (unsigned)p.mask_ny) o = (__ldg(mrow + (cy >> 5)) >> (cy & 31)) & 1u;
-                    bits |= (uint32_t)o << k;
-                    nearb |= (uint32_t)nr << k;
-                }
-            while (nearb) {
-                const int k = __ffs(nearb) - 1;
-                nearb &= nearb - 1;
-                if (mask_exact(p, (iyb + k) * nz + iz, pix)) bits |= 1u << k;
-                else bits &= ~(1u << k);
-            }
+            uint32_t bits = valid ? __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny) : 0u;
             // two open pairs per iteration: independent load chains overlap
             while (bits) {
                 const int k1 = __ffs(bits) - 1;
@@ -326,27 +350,13 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     const VoxelRec vr = p.vox[v];
     int *hh = hist - win.x;
     unsigned *hl = (unsigned *)(hist + nwin) - win.x;
+    const uint32_t *tbv = e.tb_bwd + (size_t)v * ((p.n_det + 32 * PB_T - 1) / (32 * PB_T)) * PB_T;
     if (scale > 0.0f) {
         // lanes first test the mask for 32 of their pixels (exact re-tests of
         // near-edge cells in a second pass), then iterate over the open ones
         for (int base = 0; base < p.n_det; base += PB_T * 32) {
             __syncwarp();  // reconverge after the previous batch's divergent pair loop
-            uint32_t bits = 0, nearb = 0;
-            for (int k = 0; k < 32; k++) {
-                const int q = base + k * PB_T + tid;
-                if (q < p.n_det) {
-                    bool nr;
-                    const bool o = mask_fast(p, vr, p.det[q], nr);
-                    bits |= (uint32_t)o << k;
-                    nearb |= (uint32_t)nr << k;
-                }
-            }
-            while (nearb) {
-                const int k = __ffs(nearb) - 1;
-                nearb &= nearb - 1;
-                if (mask_exact(p, v, base + k * PB_T + tid)) bits |= 1u << k;
-                else bits &= ~(1u << k);
-            }
+            uint32_t bits = __ldg(tbv + (base / (32 * PB_T)) * PB_T + tid);
             // two open pairs per iteration: independent load chains overlap
             while (bits) {
                 const int k1 = __ffs(bits) - 1;
@@ -513,6 +523,25 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.ptot = (const float *)g->d_esai_ptot;
     E.max_win = max_win;
+    // transmission bitmaps
+    {
+        const size_t nfw = p.ts_rho > 0 ? (size_t)p.nz * p.det_nx * ((p.ny + 31) / 32) * p.det_ny
+                                        : (size_t)((p.n_vox + 31) / 32) * p.n_det;
+        const size_t nbw = (size_t)p.n_vox * ((p.n_det + 32 * PB_T - 1) / (32 * PB_T)) * PB_T;
+        e = cudaMalloc(&g->d_tb_fwd, nfw * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_tb_bwd, nbw * sizeof(uint32_t));
+        if (e != cudaSuccess) return e;
+        const int blocks = 8 * sm_count(g->device);
+        if (p.ts_rho > 0)
+            k_tbits_fwd_ts<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_fwd);
+        else
+            k_tbits_fwd_tiled<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_fwd);
+        k_tbits_bwd<PB_T><<<blocks, 256>>>(p, (uint32_t *)g->d_tb_bwd);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return e;
+        E.tb_fwd = (const uint32_t *)g->d_tb_fwd;
+        E.tb_bwd = (const uint32_t *)g->d_tb_bwd;
+    }
     // low-word bits of the fixed-point deposits: a bin receives <= 2 n_det deposits < 2^(32 - lo_bits)
     int lb = 31;
     while (lb > 0 && (2.0 * p.n_det + 1.0) * std::ldexp(1.0, lb) >= 4294967296.0) lb--;
