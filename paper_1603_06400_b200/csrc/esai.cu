@@ -73,12 +73,6 @@ __global__ void __launch_bounds__(256) k_pair_stats(const Params p, float *shmin
     }
 }
 
-float __int_as_float_host(int i) {
-    float f;
-    memcpy(&f, &i, sizeof f);
-    return f;
-}
-
 int host_locate(const std::vector<float> &sb, float s) {
     const int nb = (int)sb.size();
     int b = (int)(std::upper_bound(sb.begin(), sb.end(), s) - sb.begin()) - 1;
@@ -145,25 +139,29 @@ __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
 }
 
 // ------------------------------------------------------------ device side --
-// b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0, 1].
-// One 16-byte LUT load {s_b, 1/(s_{b+1}-s_b), s_{b+1}, b} settles the common
-// case; the walk over the breakpoint array is only needed when the cell holds
-// a breakpoint below sigma.
-__device__ __forceinline__ int locate(const Esai &e, float s, float &tau) {
-    int c = (int)((s - e.s0) * e.inv_h);
+// Breakpoint location in SHARED memory.  The sorted fp32 breakpoints s_b and a
+// LUT over log2(sigma) (cells of roughly equal breakpoint count; the density in
+// sigma varies ~30x, in log sigma ~7x) are staged once per persistent CTA:
+//   c = (log2 sigma - x0) * inv_hx,  b = lut[c], then a short walk on s_b.
+// Returns b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0,1].
+__device__ __forceinline__ void load_bp(const Esai &e, float *sb, uint16_t *lut) {
+    for (int i = threadIdx.x; i < e.nb; i += blockDim.x) sb[i] = __ldg(e.sb + i);
+    for (int i = threadIdx.x; i < e.nl; i += blockDim.x) lut[i] = __ldg(e.lut16 + i);
+}
+
+__device__ __forceinline__ int locate(const Esai &e, const float *sb, const uint16_t *lut, float s, float &tau) {
+    int c = (int)((__log2f(s) - e.x0) * e.inv_hx);
     c = min(max(c, 0), e.nl - 1);
-    const float4 L = __ldg(e.lut4 + c);
-    int b = __float_as_int(L.w);
-    float sb = L.x, ig = L.y;
-    if (s >= L.z || s < L.x) {
-        while (b < e.nb - 2 && __ldg(&e.bp[b + 1].x) <= s) b++;
-        while (b > 0 && __ldg(&e.bp[b].x) > s) b--;
-        const float2 bp = __ldg(e.bp + b);
-        sb = bp.x;
-        ig = bp.y;
-    }
-    tau = fminf(fmaxf((s - sb) * ig, 0.0f), 1.0f);
+    int b = lut[c];
+    while (b < e.nb - 2 && sb[b + 1] <= s) b++;
+    while (b > 0 && sb[b] > s) b--;
+    const float s0 = sb[b], s1 = sb[b + 1];
+    tau = fminf(fmaxf(__fdividef(s - s0, s1 - s0), 0.0f), 1.0f);
     return b;
+}
+
+__device__ __forceinline__ size_t bp_smem_bytes(const Esai &e) {
+    return ((size_t)e.nb * sizeof(float) + (size_t)e.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
 }
 
 __device__ __forceinline__ float lerp_w(const float *__restrict__ wr, float tau) {
@@ -171,130 +169,153 @@ __device__ __forceinline__ float lerp_w(const float *__restrict__ wr, float tau)
     return fmaf(tau, w1 - w0, w0);
 }
 
-constexpr int PF_TX = 8, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
-constexpr int PF_CH = 32;                                   // voxels per mask batch
+constexpr int PF_TX = 16, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
+constexpr int PF_CH = 32;                                     // voxels per transmission word
 
-// Forward pair stage: g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
-// Lanes first test the mask for 32 voxels (fp32 fast path; the rare
-// near-edge cells are re-tested exactly in a second pass so the warp stays
-// converged), then iterate only over their open voxels.
+// Forward pair stage (persistent): items (tile, voxel split);
+// g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
+// The transmission bits of 32 voxels come in one word; lanes iterate only
+// over their open voxels, two pairs per iteration.
 __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e, const float *__restrict__ W,
-                                                   int vox_per_split, double *__restrict__ partial) {
+                                                   int vox_per_split, int n_tiles, int n_items,
+                                                   double *__restrict__ partial) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb);
+    load_bp(e, sb, lut);
+    __syncthreads();
     const int tiles_y = (p.det_ny + PF_TY - 1) / PF_TY;
-    const int tx = blockIdx.x / tiles_y, ty = blockIdx.x % tiles_y;
-    const int ix = tx * PF_TX + threadIdx.x / PF_TY;
-    const int jy = ty * PF_TY + threadIdx.x % PF_TY;
-    const bool valid = ix < p.det_nx && jy < p.det_ny;
-    const int pix = valid ? ix * p.det_ny + jy : 0;
-    const float2 d = p.det[pix];
-    const int v0 = blockIdx.y * vox_per_split;
-    const int v1 = min(p.n_vox, v0 + vox_per_split);
-    double tot = 0.0;
-    for (int c0 = v0; c0 < v1; c0 += PF_CH) {
-        __syncwarp();  // reconverge after the previous batch's divergent pair loop
-        const int nc = min(PF_CH, v1 - c0);
-        uint32_t bits = valid ? __ldg(e.tb_fwd + (size_t)(c0 / PF_CH) * p.n_det + pix) : 0u;
-        (void)nc;
-        float acc = 0.0f;
-        while (bits) {
-            const int i = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int v = c0 + i;
-            float P, sh, tau;
-            pair_geom(p, p.vox[v], d, P, sh);
-            const int b = locate(e, sh, tau);
-            acc = fmaf(P, lerp_w(W + (size_t)v * e.nb + b, tau), acc);
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int tile = item % n_tiles, split = item / n_tiles;
+        const int tx = tile / tiles_y, ty = tile % tiles_y;
+        const int ix = tx * PF_TX + threadIdx.x / PF_TY;
+        const int jy = ty * PF_TY + threadIdx.x % PF_TY;
+        const bool valid = ix < p.det_nx && jy < p.det_ny;
+        const int pix = valid ? ix * p.det_ny + jy : 0;
+        const float2 d = p.det[pix];
+        const int v0 = split * vox_per_split;
+        const int v1 = min(p.n_vox, v0 + vox_per_split);
+        double tot = 0.0;
+        for (int c0 = v0; c0 < v1; c0 += PF_CH) {
+            __syncwarp();  // reconverge after the previous batch's divergent pair loop
+            uint32_t bits = valid ? __ldg(e.tb_fwd + (size_t)(c0 / PF_CH) * p.n_det + pix) : 0u;
+            float acc = 0.0f;
+            while (bits) {
+                const int i1 = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const bool two = bits != 0;
+                const int i2 = two ? __ffs(bits) - 1 : i1;
+                bits &= bits - 1;
+                float P1, s1, P2, s2, t1, t2;
+                pair_geom(p, p.vox[c0 + i1], d, P1, s1);
+                pair_geom(p, p.vox[c0 + i2], d, P2, s2);
+                const int b1 = locate(e, sb, lut, s1, t1);
+                const int b2 = locate(e, sb, lut, s2, t2);
+                const float w1 = lerp_w(W + (size_t)(c0 + i1) * e.nb + b1, t1);
+                const float w2 = lerp_w(W + (size_t)(c0 + i2) * e.nb + b2, t2);
+                acc = fmaf(P1, w1, acc);
+                acc = fmaf(two ? P2 : 0.0f, w2, acc);
+            }
+            tot += (double)acc;
         }
-        tot += (double)acc;
+        if (valid) partial[(size_t)split * p.n_det + pix] = tot;
     }
-    if (valid) partial[(size_t)blockIdx.y * p.n_det + pix] = tot;
 }
 
 // ---- translation-symmetric forward (Alg. 2) --
 // When the voxel y pitch is rho detector pitches, s = r' - r depends only on
 // (iz, ix, d = jy - rho iy): |s|, G_od and dtheta of every pair of a detector
 // row and a voxel row z are one "footprint" of n_jy + rho (ny - 1) entries.  A
-// CTA owns a 128-pixel segment of one detector row, builds the footprint of
-// each voxel row z in shared memory (the paper's "compute once, shift by rho
-// columns"), and reuses it for all ny voxels of that row as integer shifts.
-// Only the source-side quantities (r^, G_so) and the mask stay per pair.
-constexpr int TS_T = 128;
+// CTA owns TS_R 128-pixel row segments, builds the footprint of each voxel row
+// z in shared memory (the paper's "compute once, shift by rho columns"), and
+// reuses it for all ny voxels of that row as integer shifts.  Only the
+// source-side quantities (r^, G_so) stay per pair.  Persistent CTAs over items
+// (row group, z chunk).
+constexpr int TS_T = 128, TS_R = 4;
 
-__global__ void __launch_bounds__(TS_T) k_esai_fwd_ts(const Params p, const Esai e, const float *__restrict__ W,
-                                                      int iz_per_split, double *__restrict__ partial) {
-    extern __shared__ float4 sm4[];
+__global__ void __launch_bounds__(TS_T * TS_R) k_esai_fwd_ts(const Params p, const Esai e,
+                                                             const float *__restrict__ W, int iz_per_chunk,
+                                                             int n_groups, int n_items, double *__restrict__ partial) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const int rho = p.ts_rho, ny = p.ny, nz = p.nz;
-    const int segs = (p.det_ny + TS_T - 1) / TS_T;
-    const int ix = blockIdx.x / segs, jy0 = (blockIdx.x % segs) * TS_T;
-    const int tid = threadIdx.x;
-    const int jy = jy0 + tid;
-    const bool valid = jy < p.det_ny;
-    const int pix = ix * p.det_ny + (valid ? jy : p.det_ny - 1);
-    const float2 dd = p.det[pix];
-    const float sx = dd.x;
     const int nfoot = TS_T + rho * (ny - 1);
-    const int dmin = jy0 - rho * (ny - 1);
-    float4 *foot = sm4;          // [nfoot] (1/|s|, G_od dtheta, s_y, -)
-    float4 *vp = sm4 + nfoot;    // [ny]    (r^_y, r^_z, G_so, ay)
-    const int iz0 = blockIdx.y * iz_per_split, iz1 = min(nz, iz0 + iz_per_split);
-    double tot = 0.0;
-    for (int iz = iz0; iz < iz1; iz++) {
-        const VoxelRec r0 = p.vox[iz];  // iy = 0: z-row quantities
-        const float sz = r0.sz;
-        __syncthreads();
-        for (int i = tid; i < nfoot; i += TS_T) {
-            const float sy = fmaf(p.pitch_d, (float)(dmin + i), p.ts_c0);
-            const float syz2 = fmaf(sy, sy, sz * sz);
-            const float rs = rsqrtf(fmaf(sx, sx, syz2));
-            const float rs2 = rs * rs;
-            const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
-            const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
-            foot[i] = make_float4(rs, sz * rs * rs2 * dth, sy, 0.0f);
-        }
-        for (int iy = tid; iy < ny; iy += TS_T) {
-            const VoxelRec r = p.vox[iy * nz + iz];
-            vp[iy] = make_float4(r.ry, r.rz, r.gso, r.ay);
-        }
-        __syncthreads();
-        const int nyb = (ny + 31) / 32;
-        const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + ix) * nyb) * p.det_ny + (valid ? jy : 0);
-        float acc = 0.0f;
-        for (int iyb = 0; iyb < ny; iyb += 32) {
-            __syncwarp();  // reconverge after the previous batch's divergent pair loop
-            uint32_t bits = valid ? __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny) : 0u;
-            // two open pairs per iteration: independent load chains overlap
-            while (bits) {
-                const int k1 = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const bool two = bits != 0;
-                const int k2 = two ? __ffs(bits) - 1 : k1;
-                bits &= bits - 1;
-                float Pp[2], sh[2];
-#pragma unroll
-                for (int u = 0; u < 2; u++) {
-                    const int iy = iyb + (u ? k2 : k1);
-                    const float4 v = vp[iy];
-                    const float4 f = foot[tid + rho * (ny - 1 - iy)];
-                    const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
-                    const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
-                    const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
-                    const float h = fmaf(0.5f, cos_t, 0.5f);
-                    const float rh = rsqrtf(h);
-                    Pp[u] = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
-                    sh[u] = 0.5f * sin_t * rh;
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb);
+    float4 *vp = (float4 *)(smem + bp_smem_bytes(e));  // [ny] (r^_y, r^_z, G_so, -)
+    float4 *foot_all = vp + ny;                        // [TS_R][nfoot] (1/|s|, G_od dtheta, s_y, -)
+    load_bp(e, sb, lut);
+    const int r = threadIdx.x / TS_T, tid = threadIdx.x % TS_T;
+    float4 *foot = foot_all + r * nfoot;
+    const int segs = (p.det_ny + TS_T - 1) / TS_T;
+    const int nyb = (ny + 31) / 32;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int grp = item % n_groups, chunk = item / n_groups;
+        const int ix = (grp / segs) * TS_R + r, jy0 = (grp % segs) * TS_T;
+        const int jy = jy0 + tid;
+        const bool valid = ix < p.det_nx && jy < p.det_ny;
+        const int pix = valid ? ix * p.det_ny + jy : 0;
+        const float2 dd = p.det[pix];
+        const float sx = dd.x;
+        const int dmin = jy0 - rho * (ny - 1);
+        const int iz0 = chunk * iz_per_chunk, iz1 = min(nz, iz0 + iz_per_chunk);
+        double tot = 0.0;
+        for (int iz = iz0; iz < iz1; iz++) {
+            const float sz = p.vox[iz].sz;  // iy = 0 record: z-row quantity
+            __syncthreads();
+            if (ix < p.det_nx)
+                for (int i = tid; i < nfoot; i += TS_T) {
+                    const float sy = fmaf(p.pitch_d, (float)(dmin + i), p.ts_c0);
+                    const float syz2 = fmaf(sy, sy, sz * sz);
+                    const float rs = rsqrtf(fmaf(sx, sx, syz2));
+                    const float rs2 = rs * rs;
+                    const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
+                    const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
+                    foot[i] = make_float4(rs, sz * rs * rs2 * dth, sy, 0.0f);
                 }
-                float t1, t2;
-                const int b1 = locate(e, sh[0], t1);
-                const int b2 = locate(e, sh[1], t2);
-                const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.nb + b1, t1);
-                const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.nb + b2, t2);
-                acc = fmaf(Pp[0], w1, acc);
-                acc = fmaf(two ? Pp[1] : 0.0f, w2, acc);
+            for (int iy = threadIdx.x; iy < ny; iy += TS_T * TS_R) {
+                const VoxelRec rr = p.vox[iy * nz + iz];
+                vp[iy] = make_float4(rr.ry, rr.rz, rr.gso, 0.0f);
             }
+            __syncthreads();
+            const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + (valid ? ix : 0)) * nyb) * p.det_ny +
+                                    (valid ? jy : 0);
+            float acc = 0.0f;
+            for (int iyb = 0; iyb < ny; iyb += 32) {
+                __syncwarp();  // reconverge after the previous batch's divergent pair loop
+                uint32_t bits = valid ? __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny) : 0u;
+                while (bits) {
+                    const int k1 = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const bool two = bits != 0;
+                    const int k2 = two ? __ffs(bits) - 1 : k1;
+                    bits &= bits - 1;
+                    float Pp[2], sh[2];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const int iy = iyb + (u ? k2 : k1);
+                        const float4 v = vp[iy];
+                        const float4 f = foot[tid + rho * (ny - 1 - iy)];
+                        const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
+                        const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
+                        const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
+                        const float h = fmaf(0.5f, cos_t, 0.5f);
+                        const float rh = rsqrtf(h);
+                        Pp[u] = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
+                        sh[u] = 0.5f * sin_t * rh;
+                    }
+                    float t1, t2;
+                    const int b1 = locate(e, sb, lut, sh[0], t1);
+                    const int b2 = locate(e, sb, lut, sh[1], t2);
+                    const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.nb + b1, t1);
+                    const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.nb + b2, t2);
+                    acc = fmaf(Pp[0], w1, acc);
+                    acc = fmaf(two ? Pp[1] : 0.0f, w2, acc);
+                }
+            }
+            tot += (double)acc;
         }
-        tot += (double)acc;
+        if (valid) partial[(size_t)chunk * p.n_det + pix] = tot;
     }
-    if (valid) partial[(size_t)blockIdx.y * p.n_det + pix] = tot;
 }
 
 // max |w| over the detector (fixed-point scale of the backward histogram)
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, si
     }
 }
 
-constexpr int PB_T = 256;
+constexpr int PB_T = 512;
 
 // fixed-point deposit of a (1 - tau) into bin b and a tau into bin b + 1
 __device__ __forceinline__ void deposit(int *hh, unsigned *hl, int b, float a, float tau, float inv_lo,
@@ -325,7 +346,7 @@ __device__ __forceinline__ void deposit(int *hh, unsigned *hl, int b, float a, f
     atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
 }
 
-// Backward pair stage: A[v, b] = sum_pixels P w hat_b(sigma), one CTA per voxel.
+// Backward pair stage (persistent over voxels): A[v, b] = sum_pixels P w hat_b(sigma).
 // Deposits go to a shared-memory histogram over the voxel's breakpoint window
 // in FIXED POINT with native 32-bit integer shared atomics (fp32 atomicAdd on
 // shared memory is a CAS loop on sm_100).  Each deposit x = d * scale (an
@@ -336,58 +357,64 @@ __device__ __forceinline__ void deposit(int *hh, unsigned *hl, int b, float a, f
 // exact and order-independent (deterministic).
 __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
                                                    const float *__restrict__ wmax, float *__restrict__ A) {
-    extern __shared__ int hist[];  // [nwin] hi words, then [nwin] lo words
-    const int v = blockIdx.x, tid = threadIdx.x;
-    const int2 win = e.vwin[v];
-    const int nwin = win.y - win.x + 1;
-    for (int i = tid; i < 2 * nwin; i += PB_T) hist[i] = 0;
-    __syncthreads();
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb);
+    int *hist = (int *)(smem + bp_smem_bytes(e));  // [max_win] hi words, then [max_win] lo words
+    load_bp(e, sb, lut);
+    const int tid = threadIdx.x;
     const float wm = *wmax;
-    const double bound = (double)e.ptot[v] * (double)wm;
     const double full = ldexp(1.0, 30 + e.lo_bits);
-    const float scale = bound > 0.0 ? (float)(full / bound) : 0.0f;
     const float inv_lo = ldexpf(1.0f, -e.lo_bits), lo_unit = ldexpf(1.0f, e.lo_bits);
-    const VoxelRec vr = p.vox[v];
-    int *hh = hist - win.x;
-    unsigned *hl = (unsigned *)(hist + nwin) - win.x;
-    const uint32_t *tbv = e.tb_bwd + (size_t)v * ((p.n_det + 32 * PB_T - 1) / (32 * PB_T)) * PB_T;
-    if (scale > 0.0f) {
-        // lanes first test the mask for 32 of their pixels (exact re-tests of
-        // near-edge cells in a second pass), then iterate over the open ones
-        for (int base = 0; base < p.n_det; base += PB_T * 32) {
-            __syncwarp();  // reconverge after the previous batch's divergent pair loop
-            uint32_t bits = __ldg(tbv + (base / (32 * PB_T)) * PB_T + tid);
-            // two open pairs per iteration: independent load chains overlap
-            while (bits) {
-                const int k1 = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const bool two = bits != 0;
-                const int k2 = two ? __ffs(bits) - 1 : k1;
-                bits &= bits - 1;
-                const int q1 = base + k1 * PB_T + tid, q2 = base + k2 * PB_T + tid;
-                float P1, s1, P2, s2, t1, t2;
-                pair_geom(p, vr, p.det[q1], P1, s1);
-                pair_geom(p, vr, p.det[q2], P2, s2);
-                const int b1 = locate(e, s1, t1);
-                const int b2 = locate(e, s2, t2);
-                const float a1 = P1 * __ldg(w + q1) * scale;
-                const float a2 = two ? P2 * __ldg(w + q2) * scale : 0.0f;
-                deposit(hh, hl, b1, a1, t1, inv_lo, lo_unit);
-                deposit(hh, hl, b2, a2, t2, inv_lo, lo_unit);
+    const int nbatch = (p.n_det + 32 * PB_T - 1) / (32 * PB_T);
+    for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        __syncthreads();  // previous voxel's histogram has been written out
+        for (int i = tid; i < 2 * nwin; i += PB_T) hist[i] = 0;
+        __syncthreads();
+        const double bound = (double)e.ptot[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(full / bound) : 0.0f;
+        const VoxelRec vr = p.vox[v];
+        int *hh = hist - win.x;
+        unsigned *hl = (unsigned *)(hist + nwin) - win.x;
+        const uint32_t *tbv = e.tb_bwd + (size_t)v * nbatch * PB_T;
+        if (scale > 0.0f) {
+            for (int batch = 0; batch < nbatch; batch++) {
+                __syncwarp();  // reconverge after the previous batch's divergent pair loop
+                const int base = batch * 32 * PB_T;
+                uint32_t bits = __ldg(tbv + batch * PB_T + tid);
+                while (bits) {
+                    const int k1 = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const bool two = bits != 0;
+                    const int k2 = two ? __ffs(bits) - 1 : k1;
+                    bits &= bits - 1;
+                    const int q1 = base + k1 * PB_T + tid, q2 = base + k2 * PB_T + tid;
+                    float P1, s1, P2, s2, t1, t2;
+                    pair_geom(p, vr, p.det[q1], P1, s1);
+                    pair_geom(p, vr, p.det[q2], P2, s2);
+                    const int b1 = locate(e, sb, lut, s1, t1);
+                    const int b2 = locate(e, sb, lut, s2, t2);
+                    const float a1 = P1 * __ldg(w + q1) * scale;
+                    const float a2 = two ? P2 * __ldg(w + q2) * scale : 0.0f;
+                    deposit(hh, hl, b1, a1, t1, inv_lo, lo_unit);
+                    deposit(hh, hl, b2, a2, t2, inv_lo, lo_unit);
+                }
             }
         }
-    }
-    __syncthreads();
-    const double qv = scale > 0.0f ? bound / full : 0.0;
-    float *Ar = A + (size_t)v * e.nb;
-    for (int b = tid; b < e.nb; b += PB_T) {
-        const int i = b - win.x;
-        float val = 0.0f;
-        if (i >= 0 && i < nwin) {
-            const long long t = (long long)hist[i] * (1ll << e.lo_bits) + (long long)(unsigned)hist[nwin + i];
-            val = (float)((double)t * qv);
+        __syncthreads();
+        const double qv = scale > 0.0f ? bound / full : 0.0;
+        float *Ar = A + (size_t)v * e.nb;
+        for (int b = tid; b < e.nb; b += PB_T) {
+            const int i = b - win.x;
+            float val = 0.0f;
+            if (i >= 0 && i < nwin) {
+                const long long t = (long long)hist[i] * (1ll << e.lo_bits) + (long long)(unsigned)hist[nwin + i];
+                val = (float)((double)t * qv);
+            }
+            Ar[b] = val;
         }
-        Ar[b] = val;
     }
 }
 
@@ -487,14 +514,12 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         }
         for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)row[j];
     }
-    // uniform LUT over [s_0, s_{nb-1}]: {s_b, 1/gap_b, s_{b+1}, b} of the cell start
-    const int nl = std::max(64, 8 * nb);
-    const double span = (double)sb[nb - 1] - sb[0];
-    std::vector<float4> lut(nl);
-    for (int c = 0; c < nl; c++) {
-        const int b = host_locate(sb, (float)(sb[0] + span * c / nl));
-        lut[c] = make_float4(bp[b].x, bp[b].y, sb[b + 1], __int_as_float_host(b));
-    }
+    // LUT over log2(sigma): nl cells, lut[c] = locate(2^(x0 + c / inv_hx))
+    if (nb > 65535) return cudaErrorInvalidValue;  // uint16 LUT entries (DESIGN.md limits)
+    const int nl = std::max(64, nb);
+    const double x0 = std::log2((double)sb[0]), x1 = std::log2((double)sb[nb - 1]);
+    std::vector<uint16_t> lut(nl);
+    for (int c = 0; c < nl; c++) lut[c] = (uint16_t)host_locate(sb, (float)std::exp2(x0 + (x1 - x0) * c / nl));
     // per-voxel breakpoint windows (deposits land in [locate(min), locate(max) + 1])
     std::vector<int2> vwin(nv);
     int max_win = 1;
@@ -504,8 +529,10 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     }
     e = cudaMalloc(&g->d_esai_bp, nb * sizeof(float2));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_bp, bp.data(), nb * sizeof(float2), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(float4));
-    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(float4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(uint16_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_sb, nb * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_sb, sb.data(), nb * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_stab, stab.size() * sizeof(float));
     if (e == cudaSuccess)
         e = cudaMemcpy(g->d_esai_stab, stab.data(), stab.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -515,10 +542,10 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     Esai &E = g->esai;
     E.nb = nb;
     E.nl = nl;
-    E.s0 = sb[0];
-    E.inv_h = (float)(nl / span);
-    E.bp = (const float2 *)g->d_esai_bp;
-    E.lut4 = (const float4 *)g->d_esai_lut;
+    E.x0 = (float)x0;
+    E.inv_hx = (float)(nl / (x1 - x0));
+    E.lut16 = (const uint16_t *)g->d_esai_lut;
+    E.sb = (const float *)g->d_esai_sb;
     E.stab = (const float *)g->d_esai_stab;
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.ptot = (const float *)g->d_esai_ptot;
@@ -550,53 +577,68 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     return cudaSuccess;
 }
 
+static size_t host_bp_bytes(const Esai &E) {
+    return ((size_t)E.nb * sizeof(float) + (size_t)E.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
+}
+
+// persistent grid: CTAs per SM limited by shared memory and threads
+static int persistent_grid(const cacsi_geometry *g, size_t smem, int threads) {
+    int per_sm = std::max(1, std::min((int)(227 * 1024 / (smem + 1024)), 2048 / threads));
+    return per_sm * sm_count(g->device);
+}
+
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *W = nullptr;
     double *part = nullptr;
-    const int tiles = ((p.det_nx + PF_TX - 1) / PF_TX) * ((p.det_ny + PF_TY - 1) / PF_TY);
-    const int target = 8 * sm_count(g->device);
-    int S = std::max(1, std::min((target + tiles - 1) / tiles, (p.n_vox + PF_CH - 1) / PF_CH));
-    int vps = (p.n_vox + S - 1) / S;
-    vps = (vps + PF_CH - 1) / PF_CH * PF_CH;
-    S = (p.n_vox + vps - 1) / vps;
+    const size_t bpb = host_bp_bytes(E);
+    int S;  // number of partial images
     cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.nb * sizeof(float), s);
-    if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)std::max(S, p.nz) * p.n_det * sizeof(double), s);
-    if (e == cudaSuccess) {
+    if (e != cudaSuccess) return e;
+    {
         // W[v][b] = sum_j f[v][j] S~[b][j]
+        KScope kt_(g, s, "k_sgemm_W");
         dim3 gg((E.nb + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, 1);
-        {
-            KScope kt_(g, s, "k_sgemm_W");
-            k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
-        }
-        if (p.ts_rho > 0) {
-            const int segs = p.det_nx * ((p.det_ny + TS_T - 1) / TS_T);
-            int St = std::max(1, std::min((4 * target + segs - 1) / segs, p.nz));
-            const int izps = (p.nz + St - 1) / St;
-            St = (p.nz + izps - 1) / izps;
-            const size_t smem = (size_t)(TS_T + p.ts_rho * (p.ny - 1) + p.ny) * sizeof(float4);
-            cudaFuncSetAttribute(k_esai_fwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            {
-                KScope kt_(g, s, "k_esai_fwd_ts");
-                k_esai_fwd_ts<<<dim3(segs, St), TS_T, smem, s>>>(p, E, W, izps, part);
-            }
-            S = St;
-        } else {
-            {
-                KScope kt_(g, s, "k_esai_fwd");
-                k_esai_fwd<<<dim3(tiles, S), PF_T, 0, s>>>(p, E, W, vps, part);
-            }
-        }
-        {
-            KScope kt_(g, s, "k_sum_parts_f64");
-            k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
-        }
-        e = cudaGetLastError();
-        *launches += 3;
+        k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
     }
+    if (p.ts_rho > 0) {
+        const int segs = (p.det_ny + TS_T - 1) / TS_T;
+        const int n_groups = ((p.det_nx + TS_R - 1) / TS_R) * segs;
+        const size_t smem = bpb + (size_t)p.ny * sizeof(float4) + (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * sizeof(float4);
+        const int grid = persistent_grid(g, smem, TS_T * TS_R);
+        int izc = std::max(1, (p.nz * n_groups) / (4 * grid));  // >= ~4 items per CTA
+        izc = std::min(izc, p.nz);
+        S = (p.nz + izc - 1) / izc;
+        e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_esai_fwd_ts");
+            cudaFuncSetAttribute(k_esai_fwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_fwd_ts<<<grid, TS_T * TS_R, smem, s>>>(p, E, W, izc, n_groups, n_groups * S, part);
+        }
+    } else {
+        const int n_tiles = ((p.det_nx + PF_TX - 1) / PF_TX) * ((p.det_ny + PF_TY - 1) / PF_TY);
+        const size_t smem = bpb;
+        const int grid = persistent_grid(g, smem, PF_T);
+        S = std::max(1, std::min((4 * grid + n_tiles - 1) / n_tiles, (p.n_vox + PF_CH - 1) / PF_CH));
+        int vps = (p.n_vox + S - 1) / S;
+        vps = (vps + PF_CH - 1) / PF_CH * PF_CH;
+        S = (p.n_vox + vps - 1) / vps;
+        e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_esai_fwd");
+            cudaFuncSetAttribute(k_esai_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_fwd<<<grid, PF_T, smem, s>>>(p, E, W, vps, n_tiles, n_tiles * S, part);
+        }
+    }
+    if (e == cudaSuccess) {
+        KScope kt_(g, s, "k_sum_parts_f64");
+        k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    *launches += 3;
     if (part) cudaFreeAsync(part, s);
-    if (W) cudaFreeAsync(W, s);
+    cudaFreeAsync(W, s);
     return e;
 }
 
@@ -615,11 +657,11 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
             KScope kt_(g, s, "k_absmax");
             k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
         }
-        const size_t smem = (size_t)E.max_win * 2 * sizeof(int);
-        cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * 2 * sizeof(int);
         {
             KScope kt_(g, s, "k_esai_bwd");
-            k_esai_bwd<<<p.n_vox, PB_T, smem, s>>>(p, E, w, wmax, A);
+            cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_bwd<<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, A);
         }
         dim3 gg((p.nq + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, S_eff);
         {

@@ -61,12 +61,12 @@ struct Params {
 struct Esai {
     int enabled;
     int nb;             // breakpoints s_0 < ... < s_{nb-1} (fp32, strictly increasing)
-    int nl;             // uniform lookup cells over [s_0, s_{nb-1}]
+    int nl;             // lookup cells, uniform in log2(sigma) over [s_0, s_{nb-1}]
     int max_win;        // max per-voxel breakpoint window (backward histogram size)
     int lo_bits;        // fixed-point split of the backward deposits (esai.cu)
-    float s0, inv_h;    // cell c = (sigma - s0) * inv_h
-    const float2 *bp;   // (s_b, 1 / (s_{b+1} - s_b))
-    const float4 *lut4; // per cell {s_b, 1/(s_{b+1}-s_b), s_{b+1}, b (int bits)} at the cell start
+    float x0, inv_hx;   // cell c = (log2 sigma - x0) * inv_hx
+    const float *sb;    // breakpoints s_b (fp32, strictly increasing)
+    const uint16_t *lut16;  // b at each cell start
     const float *stab;  // S~ [nb][nq] (scale, phi_k, E_k folded in)
     const int2 *vwin;   // per voxel [b_lo, b_hi] reachable by any of its pairs
     const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)
@@ -88,7 +88,7 @@ struct cacsi_geometry {
     void *d_vox, *d_vy64, *d_vz64, *d_vt64, *d_det, *d_dx64, *d_dy64, *d_mask, *d_energy;
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
-    void *d_esai_bp, *d_esai_lut, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd;
+    void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;
