@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(TS_T * TS_R) k_esai_fwd_ts(const Params p, con
         const int ix = (grp / segs) * TS_R + r, jy0 = (grp % segs) * TS_T;
         const int jy = jy0 + tid;
         const bool valid = ix < p.det_nx && jy < p.det_ny;
-        const int pix = valid ? ix * p.det_ny + jy : 0;
+        // lanes past the row end still build footprint entries: they need the row's x
+        const int pix = min(ix, p.det_nx - 1) * p.det_ny + min(jy, p.det_ny - 1);
         const float2 dd = p.det[pix];
         const float sx = dd.x;
         const int dmin = jy0 - rho * (ny - 1);
