@@ -232,9 +232,9 @@ def run_gpu(args):
     counts = json.load(open(os.path.join(ROOT, "workloads", "work_counts.json")))[str(cfg.seed)]
     nb_bp = G.query("esai_breakpoints")
     kern = {k: {"avg_ms": v[0] / v[1], "launches": v[1]} for k, v in ktimes.items()}
-    fwd_k = [k for k in kern if k in ("k_sgemm_W", "k_esai_fwd", "k_esai_fwd_ts", "k_sum_parts_f64", "k_forward",
-                                      "k_sum_f64")]
-    bwd_k = [k for k in kern if k in ("k_absmax", "k_esai_bwd", "k_sgemm_b2", "k_sum_parts_f32", "k_backward")]
+    fwd_k = [k for k in kern if k in ("k_pad_rows", "k_tc_gemm_W", "k_esai_fwd", "k_esai_fwd_ts", "k_sum_parts_f64",
+                                      "k_forward", "k_sum_f64")]
+    bwd_k = [k for k in kern if k in ("k_absmax", "k_esai_bwd", "k_tc_gemm_b2", "k_sum_parts_f32", "k_backward")]
     op_ms = {"cacsi_forward": sum(kern[k]["avg_ms"] for k in fwd_k),
              "cacsi_backward": sum(kern[k]["avg_ms"] for k in bwd_k)}
     dom = max(op_ms, key=op_ms.get)
@@ -306,8 +306,8 @@ def alg_flops(kernel, cfg, counts, nb):
     pairs, open_ = counts["pairs"], counts["open_pairs"]
     gemm = 2.0 * cfg.n_vox * nb * cfg.nq
     table = {
-        "k_sgemm_W": gemm,                             # W = F S~^T
-        "k_sgemm_b2": gemm,                            # b2 = A S~
+        "k_tc_gemm_W": gemm,                           # W = F S~^T (tensor cores, 3xTF32: 3 MMAs per product)
+        "k_tc_gemm_b2": gemm,                          # b2 = A S~
         "k_esai_fwd": 10 * pairs + (46 + 11) * open_,  # mask, pair geometry, locate + lerp + accumulate
         "k_esai_fwd_ts": 5 * pairs + (23 + 11) * open_,  # TS: footprint shared, x-mask uniform
         "k_esai_bwd": 10 * pairs + (46 + 6 + 12) * open_,  # mask, geometry, locate, fixed-point deposits

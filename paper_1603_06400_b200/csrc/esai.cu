@@ -24,7 +24,7 @@
 #include <vector>
 
 #include "pair.cuh"
-#include "sgemm.cuh"
+#include "tcgemm.cuh"
 
 namespace cacsi {
 
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
                 pair_geom(p, p.vox[c0 + i2], d, P2, s2);
                 const int b1 = locate(e, sb, lut, s1, t1);
                 const int b2 = locate(e, sb, lut, s2, t2);
-                const float w1 = lerp_w(W + (size_t)(c0 + i1) * e.nb + b1, t1);
-                const float w2 = lerp_w(W + (size_t)(c0 + i2) * e.nb + b2, t2);
+                const float w1 = lerp_w(W + (size_t)(c0 + i1) * e.ldw + b1, t1);
+                const float w2 = lerp_w(W + (size_t)(c0 + i2) * e.ldw + b2, t2);
                 acc = fmaf(P1, w1, acc);
                 acc = fmaf(two ? P2 : 0.0f, w2, acc);
             }
@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(TS_T * TS_R) k_esai_fwd_ts(const Params p, con
                     float t1, t2;
                     const int b1 = locate(e, sb, lut, sh[0], t1);
                     const int b2 = locate(e, sb, lut, sh[1], t2);
-                    const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.nb + b1, t1);
-                    const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.nb + b2, t2);
+                    const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.ldw + b1, t1);
+                    const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.ldw + b2, t2);
                     acc = fmaf(Pp[0], w1, acc);
                     acc = fmaf(two ? Pp[1] : 0.0f, w2, acc);
                 }
@@ -406,8 +406,8 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
         }
         __syncthreads();
         const double qv = scale > 0.0f ? bound / full : 0.0;
-        float *Ar = A + (size_t)v * e.nb;
-        for (int b = tid; b < e.nb; b += PB_T) {
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = tid; b < e.ldw; b += PB_T) {
             const int i = b - win.x;
             float val = 0.0f;
             if (i >= 0 && i < nwin) {
@@ -416,6 +416,15 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
             }
             Ar[b] = val;
         }
+    }
+}
+
+// f [n][nq] -> fp [n][ld] (zero padded) so the GEMM can load 16-byte vectors
+__global__ void k_pad_rows(const float *__restrict__ f, int n, int nq, int ld, float *__restrict__ fp) {
+    const size_t tot = (size_t)n * ld;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i % ld);
+        fp[i] = j < nq ? f[(i / ld) * nq + j] : 0.0f;
     }
 }
 
@@ -551,6 +560,26 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.ptot = (const float *)g->d_esai_ptot;
     E.max_win = max_win;
+    // tensor-core operands: S~ (N = nb, K = nq) for W = F S~^T and S~^T (N = nq, K = nb) for b2 = A S~,
+    // pre-split into TF32 hi / lo and pre-swizzled (tcgemm.cuh)
+    E.ldw = (nb + 31) / 32 * 32;
+    {
+        const int nkcW = (Q + TC_KC - 1) / TC_KC, nkcB = E.ldw / TC_KC;
+        std::vector<float> tW((size_t)((nb + TC_N - 1) / TC_N) * nkcW * 2 * TC_N * TC_KC);
+        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data());
+        std::vector<float> stT((size_t)Q * nb);
+        for (int b = 0; b < nb; b++)
+            for (int j = 0; j < Q; j++) stT[(size_t)j * nb + b] = stab[(size_t)b * Q + j];
+        std::vector<float> tB((size_t)((Q + TC_N - 1) / TC_N) * nkcB * 2 * TC_N * TC_KC);
+        tc_pack_b(stT.data(), Q, nb, nb, nkcB, tB.data());
+        e = cudaMalloc(&g->d_tc_w, tW.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_w, tW.data(), tW.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_tc_b, tB.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_b, tB.data(), tB.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
+        E.tc_w = (const float *)g->d_tc_w;
+        E.tc_b = (const float *)g->d_tc_b;
+    }
     // transmission bitmaps
     {
         const size_t nfw = p.ts_rho > 0 ? (size_t)p.nz * p.det_nx * ((p.ny + 31) / 32) * p.det_ny
@@ -595,13 +624,25 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
     double *part = nullptr;
     const size_t bpb = host_bp_bytes(E);
     int S;  // number of partial images
-    cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.nb * sizeof(float), s);
-    if (e != cudaSuccess) return e;
+    float *fp = nullptr;
+    const int ldf = (p.nq + TC_KC - 1) / TC_KC * TC_KC;
+    cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.ldw * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&fp, (size_t)p.n_vox * ldf * sizeof(float), s);
+    if (e != cudaSuccess) {
+        if (W) cudaFreeAsync(W, s);
+        return e;
+    }
     {
-        // W[v][b] = sum_j f[v][j] S~[b][j]
-        KScope kt_(g, s, "k_sgemm_W");
-        dim3 gg((E.nb + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, 1);
-        k_sgemm<true><<<gg, GM_T, 0, s>>>(p.n_vox, E.nb, p.nq, p.nq, f, E.stab, W);
+        KScope kt_(g, s, "k_pad_rows");
+        k_pad_rows<<<4 * sm_count(g->device), 256, 0, s>>>(f, p.n_vox, p.nq, ldf, fp);
+    }
+    {
+        // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
+        KScope kt_(g, s, "k_tc_gemm_W");
+        const int nkc = ldf / TC_KC;
+        dim3 gg((E.nb + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, 1);
+        cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+        k_tc_gemm<<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, E.nb, p.nq, ldf, nkc, nkc, fp, E.tc_w, W, E.ldw);
     }
     if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
@@ -639,6 +680,7 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
     if (e == cudaSuccess) e = cudaGetLastError();
     *launches += 3;
     if (part) cudaFreeAsync(part, s);
+    cudaFreeAsync(fp, s);
     cudaFreeAsync(W, s);
     return e;
 }
@@ -647,10 +689,12 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
-    const int S = 8;  // split-K of the A S~ contraction (fp32 partials, fp64 sum)
-    const int kps = ((E.nb + S - 1) / S + GM_BK - 1) / GM_BK * GM_BK;
-    const int S_eff = (E.nb + kps - 1) / kps;
-    cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.nb * sizeof(float), s);
+    // split-K of the A S~ contraction: 16 splits keep the TMEM accumulation
+    // error ~3e-6 (tcgemm.cuh); fp32 partials, fp64 sum
+    const int nkc = E.ldw / TC_KC;
+    const int cps = (nkc + 15) / 16;
+    const int S_eff = (nkc + cps - 1) / cps;
+    cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.ldw * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
     if (e == cudaSuccess) {
@@ -664,10 +708,11 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
             cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             k_esai_bwd<<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, A);
         }
-        dim3 gg((p.nq + GM_BN - 1) / GM_BN, (p.n_vox + GM_BM - 1) / GM_BM, S_eff);
         {
-            KScope kt_(g, s, "k_sgemm_b2");
-            k_sgemm<false><<<gg, GM_T, 0, s>>>(p.n_vox, p.nq, E.nb, kps, A, E.stab, part);
+            KScope kt_(g, s, "k_tc_gemm_b2");
+            dim3 gg((p.nq + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, S_eff);
+            cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+            k_tc_gemm<<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
         }
         const size_t n = (size_t)p.n_vox * p.nq;
         {

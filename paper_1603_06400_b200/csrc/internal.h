@@ -73,6 +73,9 @@ struct Esai {
     // precomputed transmission bits T(r, r') (mask factors computed
     // offline), one bit per pair in the order each pair kernel visits them
     const uint32_t *tb_fwd;  // forward (TS or tiled layout, esai.cu)
+    int ldw;                 // row stride of W / A (nb rounded up to 32, zero padded)
+    const float *tc_w;       // S~ as pre-split, pre-swizzled tensor-core B tiles (W = F S~^T)
+    const float *tc_b;       // S~^T likewise (b2 = A S~)
     const uint32_t *tb_bwd;  // backward: [voxel][batch][PB_T], bit k = pixel batch*32*PB_T + k*PB_T + lane
 };
 
@@ -88,7 +91,7 @@ struct cacsi_geometry {
     void *d_vox, *d_vy64, *d_vz64, *d_vt64, *d_det, *d_dx64, *d_dy64, *d_mask, *d_energy;
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
-    void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd;
+    void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;

@@ -1,0 +1,237 @@
+// tcgemm.cuh -- fp32-accurate GEMM on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulator in TMEM) for the ESAI contractions
+// over q (W = F S~^T, b2 = A S~).
+//
+//   C[z][M][ldc] = sum_{k in split z} A[M][lda] B[N][K]^T     (both operands K-major)
+//
+// 3xTF32: x = hi + lo with hi = x truncated to TF32 and lo = x - hi (exact in
+// fp32); C = A_hi B_hi + (A_hi B_lo + A_lo B_hi) (relative error ~2^-21 per
+// product).  The main and the cross terms accumulate in two separate TMEM
+// accumulators (columns [0,128) and [128,256)), so the small cross terms do
+// not add to the main accumulator's rounding count; the TMEM accumulation
+// error still grows with the number of k-steps (measured ~6e-8 per
+// accumulate), so long-K contractions are split (split-K partials are summed
+// in fp64 by the caller).
+//
+// B is a CONSTANT of the geometry (S~ or S~^T): it is split into hi / lo once
+// at create time and stored pre-swizzled as tiles [n_tile][k_chunk] of
+// {hi 128x32, lo 128x32} fp32 (32 KB), so one cp.async.bulk per chunk lands it
+// in shared memory.  A is split on the fly by the 128 threads (one row each).
+//
+// Shared-memory operand layout = canonical K-major SWIZZLE_128B: 8-row x
+// 128-byte atoms (1 KB, 1024-aligned), 16-byte chunk index XOR (row % 8).
+// Pipeline: 2 stages; chunk c+1's A loads and B bulk copy overlap chunk c's
+// 12 MMAs (4 k-steps x 3 products, M = N = 128, K = 8), which one elected
+// thread issues and commits to an mbarrier.  Epilogue: tcgen05.ld, warp w
+// owns TMEM lanes (tile rows) 32w..32w+31.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cacsi {
+
+constexpr int TC_M = 128, TC_N = 128, TC_KC = 32;   // tile and K chunk (32 fp32 = one 128-byte swizzle row)
+constexpr int TC_T = 128;                            // threads
+constexpr int TC_OPB = TC_M * TC_KC * 4;             // bytes of one operand half-tile (16 KB)
+constexpr int TC_STAGE = 4 * TC_OPB;                 // A_hi, A_lo, B_hi, B_lo
+constexpr int TC_SMEM = 2 * TC_STAGE + 1024 + 128;   // 2 stages + alignment + barriers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 "version 1"):
+// start >> 4 in [0,14), LBO = 1 (16 B, unused for swizzled K-major), SBO = 1024 B
+// between 8-row atoms, version 1 at bit 46, layout type 2 (SWIZZLE_128B) at bit 61.
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// instruction descriptor: D fp32, A/B TF32, both K-major, N = 128, M = 128
+__host__ __device__ constexpr uint32_t tc_idesc_tf32() {
+    return (1u << 4)                        // c_format F32
+           | (2u << 7)                      // a_format TF32
+           | (2u << 10)                     // b_format TF32
+           | ((uint32_t)(TC_N >> 3) << 17)  // n_dim
+           | ((uint32_t)(TC_M >> 4) << 24); // m_dim
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// byte offset of element (row, k) (k in [0, 32)) inside a 128 x 32 fp32 tile
+__host__ __device__ __forceinline__ uint32_t tc_swz(int row, int k) {
+    const int chunk = k >> 2;  // 16-byte chunk within the 128-byte row
+    return (uint32_t)(row * 128 + (((chunk ^ (row & 7)) << 4) | ((k & 3) << 2)));
+}
+
+__host__ __device__ __forceinline__ float tf32_hi(float x) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#else
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    float y;
+    memcpy(&y, &u, 4);
+    return y;
+#endif
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+        "r"(phase));
+}
+
+// C[z] (rows < M, columns < N) = A * B^T over k-chunks [z * cps, min(nkc, (z+1) * cps)).
+//   A: [M][lda] fp32, lda % 4 == 0, columns >= nkc * 32 read as zero beyond K
+//   Bt: pre-split tiles [ceil(N/128)][nkc][2][128 x 32] (see tc_pack_b)
+__global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, int nkc, int cps,
+                                                  const float *__restrict__ A, const float *__restrict__ Bt,
+                                                  float *__restrict__ C, int ldc) {
+    extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *bars = (uint64_t *)(base + 2 * TC_STAGE);  // [0,1] B landed, [2,3] MMAs of stage done
+    uint32_t *tmem_slot = (uint32_t *)(bars + 4);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int m0 = blockIdx.y * TC_M, nt = blockIdx.x, n0 = nt * TC_N;
+    const int kc0 = blockIdx.z * cps, kc1 = min(nkc, kc0 + cps);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 4; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bars + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = tc_idesc_tf32();
+    const int row = tid, gm = m0 + row;
+    const float *arow = A + (size_t)(gm < M ? gm : 0) * lda;
+
+    for (int c = kc0; c < kc1; c++) {
+        const int it = c - kc0, st = it & 1;
+        unsigned char *sA_hi = base + st * TC_STAGE, *sA_lo = sA_hi + TC_OPB, *sB = sA_hi + 2 * TC_OPB;
+        // the MMAs that last read this stage (iteration it - 2) must be done
+        if (it >= 2) mbar_wait(smem_u32(bars + 2 + st), ((it >> 1) - 1) & 1);
+        if (tid == 0) {
+            const uint32_t mb = smem_u32(bars + st);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(2 * TC_OPB));
+            const float *src = Bt + ((size_t)nt * nkc + c) * (2 * TC_M * TC_KC);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_u32(sB)),
+                "l"(src), "r"(2 * TC_OPB), "r"(mb)
+                : "memory");
+        }
+        // A: this thread's row, 32 columns of chunk c, split into hi / lo
+        const int k0 = c * TC_KC;
+#pragma unroll
+        for (int k4 = 0; k4 < TC_KC; k4 += 4) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gm < M && k0 + k4 < K) v = __ldg((const float4 *)(arow + k0 + k4));
+            const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+            const uint32_t off = tc_swz(row, k4);
+            *(float4 *)(sA_hi + off) = h;
+            *(float4 *)(sA_lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n");
+        __syncthreads();
+        if (tid == 0) {
+            mbar_wait(smem_u32(bars + st), (it >> 1) & 1);  // B tile landed
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const uint32_t ah0 = smem_u32(sA_hi), al0 = smem_u32(sA_lo);
+            const uint32_t bh0 = smem_u32(sB), bl0 = smem_u32(sB + TC_OPB);
+#pragma unroll
+            for (int ks = 0; ks < TC_KC / 8; ks++) {
+                const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
+                tc_mma(tmem, tc_desc(ah0 + off), tc_desc(bh0 + off), idesc, (it | ks) != 0);
+                tc_mma(tmem + TC_N, tc_desc(ah0 + off), tc_desc(bl0 + off), idesc, (it | ks) != 0);
+                tc_mma(tmem + TC_N, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(bars + 2 + st)));
+        }
+    }
+    // all MMAs done (the last commit covers every earlier MMA of this thread)
+    const int nit = kc1 - kc0;
+    if (nit > 0) mbar_wait(smem_u32(bars + 2 + ((nit - 1) & 1)), ((nit - 1) >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+
+    // ---- epilogue: TMEM -> registers -> global (warp w reads lanes 32w..32w+31)
+    float *Cz = C + (size_t)blockIdx.z * M * ldc;
+    const int orow = m0 + warp * 32 + (tid & 31);
+#pragma unroll 1
+    for (int c0 = 0; c0 < TC_N; c0 += 32) {
+        uint32_t r[32], x[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        tmem_ld32(taddr, r);
+        tmem_ld32(taddr + TC_N, x);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
+        if (orow < M) {
+            float *cr = Cz + (size_t)orow * ldc + n0 + c0;
+            if (n0 + c0 + 32 <= N && (ldc & 3) == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) *(float4 *)(cr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; j++)
+                    if (n0 + c0 + j < N) cr[j] = v[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * TC_N));
+}
+
+// Host: pack B (N x K, row-major, ldb) into pre-split swizzled tiles
+// [ceil(N/128)][nkc][hi, lo][128 x 32].  out must hold ntiles * nkc * 8192 floats.
+inline void tc_pack_b(const float *B, int N, int K, int ldb, int nkc, float *out) {
+    const int ntiles = (N + TC_N - 1) / TC_N;
+    for (int nt = 0; nt < ntiles; nt++)
+        for (int c = 0; c < nkc; c++) {
+            unsigned char *tile = (unsigned char *)(out + ((size_t)nt * nkc + c) * (2 * TC_N * TC_KC));
+            for (int r = 0; r < TC_N; r++)
+                for (int k = 0; k < TC_KC; k++) {
+                    const int n = nt * TC_N + r, kk = c * TC_KC + k;
+                    const float x = (n < N && kk < K) ? B[(size_t)n * ldb + kk] : 0.0f;
+                    const float h = tf32_hi(x);
+                    *(float *)(tile + tc_swz(r, k)) = h;
+                    *(float *)(tile + TC_OPB + tc_swz(r, k)) = x - h;
+                }
+        }
+}
+
+}  // namespace cacsi
