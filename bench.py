@@ -100,6 +100,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+# ----------------------------------------------------------- replicas (N>1) --
+def max_over_ranks(ms: float, world: int, device=None) -> float:
+    """Timed-region duration of the job = max over ranks (the path does not
+    shard: N independent replicas)."""
+    if world <= 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(units_per_rank_step: float, steps: int, world: int, total_ms: float) -> float:
+    """Whole-job value: units all ranks processed / max-over-ranks time."""
+    return units_per_rank_step * steps * world / (total_ms / 1e3)
+
+
 # ------------------------------------------------------------ work counts --
 def work_counts(cfg):
     """Pairs and nominal terms per operator application."""
@@ -198,15 +216,10 @@ def run_gpu(args):
     t_fwd = [e[0].elapsed_time(e[1]) for e in evs]
     t_bwd = [e[2].elapsed_time(e[3]) for e in evs]
     t_step = [e[0].elapsed_time(e[4]) for e in evs]
-    total_ms = float(sum(t_step))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = t.item()
+    total_ms = max_over_ranks(float(sum(t_step)), world, dev)
     ms_per_step = total_ms / args.steps
     pairs, nominal_terms = work_counts(cfg)
-    units = 2 * pairs * args.steps * world
-    value = units / (total_ms / 1e3)
+    value = job_throughput(2 * pairs, args.steps, world, total_ms)
 
     # ---- e2e: the same step through the host-buffer C ABI (pinned buffers)
     fh = torch.full(G.f_shape, f0, dtype=torch.float32).pin_memory().numpy()

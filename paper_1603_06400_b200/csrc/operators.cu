@@ -105,6 +105,21 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
     }
 }
 
+// [rows][cols] -> [cols][rows] (32 x 32 shared-memory tiles)
+__global__ void k_transpose(const float *__restrict__ in, int rows, int cols, float *__restrict__ out) {
+    __shared__ float t[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) t[i][threadIdx.x] = in[(size_t)r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[(size_t)c * rows + r] = t[threadIdx.x][i];
+    }
+}
+
 __global__ void k_sum_f64(const double *__restrict__ part, int S, size_t n, float *__restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -162,12 +177,14 @@ __global__ void __launch_bounds__(BWD_T) k_backward(const Params p, const float 
                 h0[BWD_T] += hi;
             }
         } else {
-            const float *wq = w + (size_t)(valid ? q : 0) * K;
+            // w is passed TRANSPOSED here ([ne][n_det], launch_backward): lanes = consecutive
+            // pixels read consecutive addresses for the same energy (coalesced)
+            const float *wq = w + (valid ? q : 0);
             for (int k = wlo; k <= whi; k++) {
                 const float2 e = en[k];
                 float tt;
                 const int n = hat_coord(p, e.x, sh, tt);
-                const float ca = (open && k >= klo && k <= khi) ? P * e.y * __ldg(wq + k) : 0.0f;
+                const float ca = (open && k >= klo && k <= khi) ? P * e.y * __ldg(wq + (size_t)k * p.n_det) : 0.0f;
                 const float hi = fmaf(tt, ca, 0.5f * ca);
                 float *h0 = hb + (n + 2) * BWD_T;
                 h0[0] += ca - hi;
@@ -255,11 +272,20 @@ cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, c
     const size_t smem =
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
     if (p.energy_resolving) {
+        float *wT = nullptr;
+        cudaError_t e = cudaMallocAsync(&wT, (size_t)p.n_det * p.ne * sizeof(float), s);
+        if (e != cudaSuccess) return e;
+        {
+            KScope kt_(g, s, "k_transpose");
+            k_transpose<<<dim3((p.ne + 31) / 32, (p.n_det + 31) / 32), dim3(32, 8), 0, s>>>(w, p.n_det, p.ne, wT);
+        }
         cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         {
             KScope kt_(g, s, "k_backward_er");
-            k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, w, b);
+            k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, wT, b);
         }
+        cudaFreeAsync(wT, s);
+        *launches += 1;
     } else {
         cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         {

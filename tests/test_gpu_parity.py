@@ -264,14 +264,16 @@ def test_direct_algorithm_parity(ci, monkeypatch):
 
 
 def test_esai_matches_direct_config2(monkeypatch):
-    """The two GPU algorithms agree on the full config-2 operators."""
+    """The two GPU algorithms agree on the full config-2 operators (GPU-vs-GPU
+    consistency; each is held to the oracle bar elsewhere).  5e-6 covers the
+    3xTF32 tensor-core contraction's ~3e-6."""
     cfg = make_config(2)
     G = P.Geometry(cfg.desc())
     monkeypatch.setenv("CACSI_ALGO", "direct")
     D = P.Geometry(cfg.desc())
     w = rnd(G.g_shape, 2, 51)
-    assert rel_l2(gpu_forward(G, cfg.f), gpu_forward(D, cfg.f)) < 2e-6
-    assert rel_l2(gpu_backward(G, w), gpu_backward(D, w)) < 2e-6
+    assert rel_l2(gpu_forward(G, cfg.f), gpu_forward(D, cfg.f)) < 5e-6
+    assert rel_l2(gpu_backward(G, w), gpu_backward(D, w)) < 5e-6
 
 
 # ------------------------------------------------- translation symmetry (TS) --
