@@ -281,14 +281,19 @@ __global__ void __launch_bounds__(TS_T * TS_R) k_esai_fwd_ts(const Params p, con
             const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + (valid ? ix : 0)) * nyb) * p.det_ny +
                                     (valid ? jy : 0);
             float acc = 0.0f;
-            for (int iyb = 0; iyb < ny; iyb += 32) {
+            // 64 voxels per batch (two transmission words): less lane imbalance
+            for (int iyb = 0; iyb < ny; iyb += 64) {
                 __syncwarp();  // reconverge after the previous batch's divergent pair loop
-                uint32_t bits = valid ? __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny) : 0u;
+                unsigned long long bits = 0;
+                if (valid) {
+                    bits = __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny);
+                    if (iyb + 32 < ny) bits |= (unsigned long long)__ldg(tbrow + (size_t)(iyb / 32 + 1) * p.det_ny) << 32;
+                }
                 while (bits) {
-                    const int k1 = __ffs(bits) - 1;
+                    const int k1 = __ffsll((long long)bits) - 1;
                     bits &= bits - 1;
                     const bool two = bits != 0;
-                    const int k2 = two ? __ffs(bits) - 1 : k1;
+                    const int k2 = two ? __ffsll((long long)bits) - 1 : k1;
                     bits &= bits - 1;
                     float Pp[2], sh[2];
 #pragma unroll
@@ -381,15 +386,17 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
         unsigned *hl = (unsigned *)(hist + nwin) - win.x;
         const uint32_t *tbv = e.tb_bwd + (size_t)v * nbatch * PB_T;
         if (scale > 0.0f) {
-            for (int batch = 0; batch < nbatch; batch++) {
+            // 64 pixels per lane per batch (two transmission words): less lane imbalance
+            for (int batch = 0; batch < nbatch; batch += 2) {
                 __syncwarp();  // reconverge after the previous batch's divergent pair loop
                 const int base = batch * 32 * PB_T;
-                uint32_t bits = __ldg(tbv + batch * PB_T + tid);
+                unsigned long long bits = __ldg(tbv + batch * PB_T + tid);
+                if (batch + 1 < nbatch) bits |= (unsigned long long)__ldg(tbv + (batch + 1) * PB_T + tid) << 32;
                 while (bits) {
-                    const int k1 = __ffs(bits) - 1;
+                    const int k1 = __ffsll((long long)bits) - 1;
                     bits &= bits - 1;
                     const bool two = bits != 0;
-                    const int k2 = two ? __ffs(bits) - 1 : k1;
+                    const int k2 = two ? __ffsll((long long)bits) - 1 : k1;
                     bits &= bits - 1;
                     const int q1 = base + k1 * PB_T + tid, q2 = base + k2 * PB_T + tid;
                     float P1, s1, P2, s2, t1, t2;
