@@ -251,6 +251,19 @@ def test_deterministic_operators():
 
 
 # ------------------------------------------------ direct per-term algorithm --
+def test_direct_algorithm_energy_resolving(monkeypatch):
+    """CACSI_ALGO=direct for the energy-resolving operators (per-pixel
+    threads) -- an independent GPU cross-check of the lanes-as-energies kernels."""
+    monkeypatch.setenv("CACSI_ALGO", "direct")
+    cfg = make_config(0, energy_resolving=1)
+    d = cfg.desc()
+    d.update(ny=6, nz=5, nq=21, det_nx=7, det_ny=19)
+    G, O = geoms(d)
+    f, w = rnd(G.f_shape, 0, 70), rnd(G.g_shape, 0, 71)
+    assert_parity(gpu_forward(G, f), O.forward(f), "direct er forward")
+    assert_parity(gpu_backward(G, w), O.backward(w), "direct er backward")
+
+
 @pytest.mark.parametrize("ci", [0, 1])
 def test_direct_algorithm_parity(ci, monkeypatch):
     """CACSI_ALGO=direct: the per-term kernels (no ESAI tables) for the
