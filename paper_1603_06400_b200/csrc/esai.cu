@@ -139,29 +139,43 @@ __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
 }
 
 // ------------------------------------------------------------ device side --
-// Breakpoint location in SHARED memory.  The sorted fp32 breakpoints s_b and a
-// LUT over log2(sigma) (cells of roughly equal breakpoint count; the density in
-// sigma varies ~30x, in log sigma ~7x) are staged once per persistent CTA:
-//   c = (log2 sigma - x0) * inv_hx,  b = lut[c], then a short walk on s_b.
+// Breakpoint location in SHARED memory, branch-free in the common case.  The
+// sorted fp32 breakpoints s_b (+ kLocD +inf pads) and a LUT over the fp32 BIT
+// PATTERN of sigma are staged once per persistent CTA.  For positive floats
+// the bit pattern is monotone and piecewise linear in log2 (exponent,
+// mantissa), so equal-width cells in bit space track the breakpoint density
+// (~7x variation in log sigma) without a MUFU.LG2, and the cell index is
+// exact integer arithmetic:
+//   c = (bits(sigma) - lut_b0) >> lut_sh,  b = lut[c] + #{i = 1..kLocD : s_{lut[c]+i} <= sigma}
+// lut[c] = the last breakpoint <= the cell's first float; a cell holding more
+// than kLocD breakpoints is flagged (kLutSlow, ~0.1 % of cells) and walked.
 // Returns b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0,1].
+constexpr int kLocD = 3;
+constexpr unsigned kLutSlow = 0x8000u;
+
 __device__ __forceinline__ void load_bp(const Esai &e, float *sb, uint16_t *lut) {
-    for (int i = threadIdx.x; i < e.nb; i += blockDim.x) sb[i] = __ldg(e.sb + i);
+    for (int i = threadIdx.x; i < e.nb + kLocD; i += blockDim.x) sb[i] = __ldg(e.sb + i);
     for (int i = threadIdx.x; i < e.nl; i += blockDim.x) lut[i] = __ldg(e.lut16 + i);
 }
 
 __device__ __forceinline__ int locate(const Esai &e, const float *sb, const uint16_t *lut, float s, float &tau) {
-    int c = (int)((__log2f(s) - e.x0) * e.inv_hx);
+    int c = (__float_as_int(s) - e.lut_b0) >> e.lut_sh;
     c = min(max(c, 0), e.nl - 1);
-    int b = lut[c];
-    while (b < e.nb - 2 && sb[b + 1] <= s) b++;
-    while (b > 0 && sb[b] > s) b--;
+    const unsigned ent = lut[c];
+    int b = (int)(ent & (kLutSlow - 1u));
+    if (ent & kLutSlow) {
+        while (b < e.nb - 2 && sb[b + 1] <= s) b++;
+    } else {
+        b += (int)(sb[b + 1] <= s) + (int)(sb[b + 2] <= s) + (int)(sb[b + 3] <= s);
+        b = min(b, e.nb - 2);
+    }
     const float s0 = sb[b], s1 = sb[b + 1];
     tau = fminf(fmaxf(__fdividef(s - s0, s1 - s0), 0.0f), 1.0f);
     return b;
 }
 
 __device__ __forceinline__ size_t bp_smem_bytes(const Esai &e) {
-    return ((size_t)e.nb * sizeof(float) + (size_t)e.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
+    return ((size_t)(e.nb + kLocD) * sizeof(float) + (size_t)e.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
 }
 
 __device__ __forceinline__ float lerp_w(const float *__restrict__ wr, float tau) {
@@ -181,7 +195,7 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
                                                    double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sb = (float *)smem;
-    uint16_t *lut = (uint16_t *)(sb + e.nb);
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
     load_bp(e, sb, lut);
     __syncthreads();
     const int tiles_y = (p.det_ny + PF_TY - 1) / PF_TY;
@@ -233,14 +247,14 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
 // (row group, z chunk).
 constexpr int TS_T = 128, TS_R = 4;
 
-__global__ void __launch_bounds__(TS_T * TS_R) k_esai_fwd_ts(const Params p, const Esai e,
+__global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, const Esai e,
                                                              const float *__restrict__ W, int iz_per_chunk,
                                                              int n_groups, int n_items, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int rho = p.ts_rho, ny = p.ny, nz = p.nz;
     const int nfoot = TS_T + rho * (ny - 1);
     float *sb = (float *)smem;
-    uint16_t *lut = (uint16_t *)(sb + e.nb);
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
     float4 *vp = (float4 *)(smem + bp_smem_bytes(e));  // [ny] (r^_y, r^_z, G_so, -)
     float4 *foot_all = vp + ny;                        // [TS_R][nfoot] (1/|s|, G_od dtheta, s_y, -)
     load_bp(e, sb, lut);
@@ -338,52 +352,43 @@ __global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, si
     }
 }
 
-constexpr int PB_T = 512;
-
-// fixed-point deposit of a (1 - tau) into bin b and a tau into bin b + 1
-__device__ __forceinline__ void deposit(int *hh, unsigned *hl, int b, float a, float tau, float inv_lo,
-                                        float lo_unit) {
-    const float x1 = rintf(a * tau);
-    const float x0 = rintf(a) - x1;
-    const float h0 = floorf(x0 * inv_lo), h1 = floorf(x1 * inv_lo);
-    atomicAdd(hh + b, (int)h0);
-    atomicAdd(hl + b, (unsigned)(x0 - h0 * lo_unit));
-    atomicAdd(hh + b + 1, (int)h1);
-    atomicAdd(hl + b + 1, (unsigned)(x1 - h1 * lo_unit));
-}
+constexpr int PB_T = 1024;
 
 // Backward pair stage (persistent over voxels): A[v, b] = sum_pixels P w hat_b(sigma).
 // Deposits go to a shared-memory histogram over the voxel's breakpoint window
 // in FIXED POINT with native 32-bit integer shared atomics (fp32 atomicAdd on
-// shared memory is a CAS loop on sm_100).  Each deposit x = d * scale (an
-// integer-valued float, < 2^(30+lb)) is split exactly into hi = floor(x / 2^lb)
-// and lo = x - hi 2^lb in [0, 2^lb): sum(hi) fits int32 by the choice of scale
-// (2^(30+lb) / (sum_pixels |P| max|w|)), sum(lo) fits uint32 because a bin gets
-// at most 2 n_det deposits (lb = 31 - log2(2 n_det)).  ~45-bit resolution,
-// exact and order-independent (deterministic).
+// shared memory is a CAS loop on sm_100).  The per-voxel scale
+//     2^30 / (vbound[v] max|w|),   vbound[v] >= max_b sum_pixels P hat_b(sigma)
+// (a bound measured once at create with w = 1, esai_build) keeps every partial
+// bin sum below 2^30 (|sum P w hat| <= max|w| sum P hat); the deposit
+// x = P w scale is split exactly into the integers rint(x tau) -> b + 1 and
+// rint(x) - rint(x tau) -> b.  One unit is 2^-30 of the voxel's largest bin
+// (~2^-40 of its total response); integer adds are exact and
+// order-independent, so the backward is deterministic.
+// BOUND = true: w = 1, scale from the conservative bound sum_pixels |P| (used
+// once to measure vbound).
+template <bool BOUND>
 __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
-                                                   const float *__restrict__ wmax, float *__restrict__ A) {
+                                                   const float *__restrict__ wmax, const float *__restrict__ vbound,
+                                                   float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sb = (float *)smem;
-    uint16_t *lut = (uint16_t *)(sb + e.nb);
-    int *hist = (int *)(smem + bp_smem_bytes(e));  // [max_win] hi words, then [max_win] lo words
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
+    int *hist = (int *)(smem + bp_smem_bytes(e));  // [max_win]
     load_bp(e, sb, lut);
     const int tid = threadIdx.x;
-    const float wm = *wmax;
-    const double full = ldexp(1.0, 30 + e.lo_bits);
-    const float inv_lo = ldexpf(1.0f, -e.lo_bits), lo_unit = ldexpf(1.0f, e.lo_bits);
+    const float wm = BOUND ? 1.0f : *wmax;
     const int nbatch = (p.n_det + 32 * PB_T - 1) / (32 * PB_T);
     for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
         const int2 win = e.vwin[v];
         const int nwin = win.y - win.x + 1;
         __syncthreads();  // previous voxel's histogram has been written out
-        for (int i = tid; i < 2 * nwin; i += PB_T) hist[i] = 0;
+        for (int i = tid; i < nwin; i += PB_T) hist[i] = 0;
         __syncthreads();
-        const double bound = (double)e.ptot[v] * (double)wm;
-        const float scale = bound > 0.0 ? (float)(full / bound) : 0.0f;
+        const double bound = (double)vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
         const VoxelRec vr = p.vox[v];
-        int *hh = hist - win.x;
-        unsigned *hl = (unsigned *)(hist + nwin) - win.x;
+        int *hv = hist - win.x;
         const uint32_t *tbv = e.tb_bwd + (size_t)v * nbatch * PB_T;
         if (scale > 0.0f) {
             // 64 pixels per lane per batch (two transmission words): less lane imbalance
@@ -404,25 +409,43 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
                     pair_geom(p, vr, p.det[q2], P2, s2);
                     const int b1 = locate(e, sb, lut, s1, t1);
                     const int b2 = locate(e, sb, lut, s2, t2);
-                    const float a1 = P1 * __ldg(w + q1) * scale;
-                    const float a2 = two ? P2 * __ldg(w + q2) * scale : 0.0f;
-                    deposit(hh, hl, b1, a1, t1, inv_lo, lo_unit);
-                    deposit(hh, hl, b2, a2, t2, inv_lo, lo_unit);
+                    const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
+                    const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
+                    const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
+                    atomicAdd(hv + b1, __float2int_rn(a1) - x1);
+                    atomicAdd(hv + b1 + 1, x1);
+                    atomicAdd(hv + b2, __float2int_rn(a2) - x2);
+                    atomicAdd(hv + b2 + 1, x2);
                 }
             }
         }
         __syncthreads();
-        const double qv = scale > 0.0f ? bound / full : 0.0;
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
         float *Ar = A + (size_t)v * e.ldw;
         for (int b = tid; b < e.ldw; b += PB_T) {
             const int i = b - win.x;
-            float val = 0.0f;
-            if (i >= 0 && i < nwin) {
-                const long long t = (long long)hist[i] * (1ll << e.lo_bits) + (long long)(unsigned)hist[nwin + i];
-                val = (float)((double)t * qv);
-            }
-            Ar[b] = val;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * unit : 0.0f;
         }
+    }
+}
+
+// vbound[v] = (max_b A1[v, b] + n_det units) (1 + 1e-3): a bound on every bin of
+// the voxel with w = 1, A1 measured by k_esai_bwd<true> (units of its
+// conservative scale; each of <= n_det deposits per bin rounds by <= 1/2 unit).
+__global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ A1, int ldw, const float *__restrict__ ptot,
+                                                int n_det, float *__restrict__ vbound) {
+    __shared__ float sm[8];
+    const int v = blockIdx.x;
+    float m = 0.0f;
+    for (int b = threadIdx.x; b < ldw; b += 256) m = fmaxf(m, A1[(size_t)v * ldw + b]);
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; i++) m = fmaxf(m, sm[i]);
+        m = fmaxf(m, sm[0]);
+        const double unit = (double)ptot[v] / 1073741824.0;
+        vbound[v] = (float)(((double)m + n_det * unit) * (1.0 + 1e-3));
     }
 }
 
@@ -458,6 +481,27 @@ int sm_count(int dev) {
 }
 
 }  // namespace
+
+int fbits(float x) {
+    int i;
+    std::memcpy(&i, &x, 4);
+    return i;
+}
+float ffrom(int i) {
+    float x;
+    std::memcpy(&x, &i, 4);
+    return x;
+}
+
+static size_t host_bp_bytes(const Esai &E) {
+    return ((size_t)(E.nb + kLocD) * sizeof(float) + (size_t)E.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
+}
+
+// persistent grid: CTAs per SM limited by shared memory and threads
+static int persistent_grid(const cacsi_geometry *g, size_t smem, int threads) {
+    int per_sm = std::max(1, std::min((int)(227 * 1024 / (smem + 1024)), 2048 / threads));
+    return per_sm * sm_count(g->device);
+}
 
 // Build the ESAI tables (energy-integrating handles).  Host fp64 arithmetic
 // for the breakpoints and S~; DESIGN.md "ESAI tables".
@@ -531,12 +575,33 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         }
         for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)row[j];
     }
-    // LUT over log2(sigma): nl cells, lut[c] = locate(2^(x0 + c / inv_hx))
-    if (nb > 65535) return cudaErrorInvalidValue;  // uint16 LUT entries (DESIGN.md limits)
-    const int nl = std::max(64, nb);
-    const double x0 = std::log2((double)sb[0]), x1 = std::log2((double)sb[nb - 1]);
+    // LUT over the fp32 bit patterns of [s_0, s_{nb-1}]: nl = (span >> sh) + 1
+    // <= ~4 nb cells (device locate above); 15-bit entries + the slow flag
+    if (nb > (int)kLutSlow - 1) {  // outside the LUT's index range: per-term kernels
+        g->esai.enabled = 0;
+        return cudaSuccess;
+    }
+    const int b0 = fbits(sb[0]);
+    const long long span = (long long)fbits(sb[nb - 1]) - b0;
+    const long long target = std::min<long long>(32768, std::max(64, 4 * nb));
+    int sh = 0;
+    while ((span >> sh) + 1 > target) sh++;
+    const int nl = (int)(span >> sh) + 1;
     std::vector<uint16_t> lut(nl);
-    for (int c = 0; c < nl; c++) lut[c] = (uint16_t)host_locate(sb, (float)std::exp2(x0 + (x1 - x0) * c / nl));
+    int n_slow = 0;
+    for (int c = 0; c < nl; c++) {
+        const int c0 = b0 + (int)((long long)c << sh);
+        const long long c1 = (long long)b0 + ((long long)(c + 1) << sh) - 1;  // last float of the cell
+        int b = host_locate(sb, ffrom(c0));
+        int inside = 0;
+        for (int i = b + 1; i < nb && fbits(sb[i]) <= c1; i++)
+            if (fbits(sb[i]) > c0) inside++;
+        lut[c] = (uint16_t)b;
+        if (inside > kLocD) {
+            lut[c] |= (uint16_t)kLutSlow;
+            n_slow++;
+        }
+    }
     // per-voxel breakpoint windows (deposits land in [locate(min), locate(max) + 1])
     std::vector<int2> vwin(nv);
     int max_win = 1;
@@ -548,8 +613,10 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_bp, bp.data(), nb * sizeof(float2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_lut, nl * sizeof(uint16_t));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_lut, lut.data(), nl * sizeof(uint16_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_sb, nb * sizeof(float));
-    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_sb, sb.data(), nb * sizeof(float), cudaMemcpyHostToDevice);
+    std::vector<float> sbp(sb);
+    for (int i = 0; i < kLocD; i++) sbp.push_back(INFINITY);  // pads: the branch-free count never passes them
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_sb, sbp.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_sb, sbp.data(), sbp.size() * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_stab, stab.size() * sizeof(float));
     if (e == cudaSuccess)
         e = cudaMemcpy(g->d_esai_stab, stab.data(), stab.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -559,8 +626,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     Esai &E = g->esai;
     E.nb = nb;
     E.nl = nl;
-    E.x0 = (float)x0;
-    E.inv_hx = (float)(nl / (x1 - x0));
+    E.lut_b0 = b0;
+    E.lut_sh = sh;
+    E.n_slow = n_slow;
     E.lut16 = (const uint16_t *)g->d_esai_lut;
     E.sb = (const float *)g->d_esai_sb;
     E.stab = (const float *)g->d_esai_stab;
@@ -606,22 +674,37 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         E.tb_fwd = (const uint32_t *)g->d_tb_fwd;
         E.tb_bwd = (const uint32_t *)g->d_tb_bwd;
     }
-    // low-word bits of the fixed-point deposits: a bin receives <= 2 n_det deposits < 2^(32 - lo_bits)
-    int lb = 31;
-    while (lb > 0 && (2.0 * p.n_det + 1.0) * std::ldexp(1.0, lb) >= 4294967296.0) lb--;
-    E.lo_bits = std::min(lb, 20);
+    // shared-memory budgets of the pair kernels (227 KB per CTA); beyond them the
+    // per-term kernels serve the handle
+    {
+        const size_t fwd = p.ts_rho > 0 ? host_bp_bytes(E) + (size_t)p.ny * 16 +
+                                              (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * 16
+                                        : host_bp_bytes(E);
+        const size_t bwd = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
+        if (fwd > 227 * 1024 || bwd > 227 * 1024) {
+            E.enabled = 0;
+            return cudaSuccess;
+        }
+    }
+    // backward fixed-point bound: vbound[v] >= max_b sum_pixels P hat_b, measured
+    // with w = 1 under the conservative scale sum_pixels |P| (k_esai_bwd)
+    {
+        float *A1 = nullptr;
+        e = cudaMalloc(&g->d_esai_vbound, nv * sizeof(float));
+        if (e == cudaSuccess) e = cudaMalloc(&A1, (size_t)nv * E.ldw * sizeof(float));
+        if (e == cudaSuccess) {
+            const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
+            cudaFuncSetAttribute(k_esai_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_bwd<true><<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, A1);
+            k_vbound<<<nv, 256>>>(A1, E.ldw, E.ptot, p.n_det, (float *)g->d_esai_vbound);
+            e = cudaDeviceSynchronize();
+        }
+        cudaFree(A1);
+        if (e != cudaSuccess) return e;
+        E.vbound = (const float *)g->d_esai_vbound;
+    }
     E.enabled = 1;
     return cudaSuccess;
-}
-
-static size_t host_bp_bytes(const Esai &E) {
-    return ((size_t)E.nb * sizeof(float) + (size_t)E.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
-}
-
-// persistent grid: CTAs per SM limited by shared memory and threads
-static int persistent_grid(const cacsi_geometry *g, size_t smem, int threads) {
-    int per_sm = std::max(1, std::min((int)(227 * 1024 / (smem + 1024)), 2048 / threads));
-    return per_sm * sm_count(g->device);
 }
 
 // Tables of the energy-resolving kernels (er.cu): transmission bits in the
@@ -748,11 +831,11 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
             KScope kt_(g, s, "k_absmax");
             k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
         }
-        const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * 2 * sizeof(int);
+        const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
         {
             KScope kt_(g, s, "k_esai_bwd");
-            cudaFuncSetAttribute(k_esai_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_bwd<<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, A);
+            cudaFuncSetAttribute(k_esai_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_esai_bwd<false><<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, A);
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");

@@ -61,12 +61,13 @@ struct Params {
 struct Esai {
     int enabled;
     int nb;             // breakpoints s_0 < ... < s_{nb-1} (fp32, strictly increasing)
-    int nl;             // lookup cells, uniform in log2(sigma) over [s_0, s_{nb-1}]
+    int nl;             // lookup cells over the fp32 bit patterns of [s_0, s_{nb-1}]
     int max_win;        // max per-voxel breakpoint window (backward histogram size)
-    int lo_bits;        // fixed-point split of the backward deposits (esai.cu)
-    float x0, inv_hx;   // cell c = (log2 sigma - x0) * inv_hx
-    const float *sb;    // breakpoints s_b (fp32, strictly increasing)
-    const uint16_t *lut16;  // b at each cell start
+    int n_slow;         // LUT cells flagged kLutSlow (diagnostic)
+    int lut_b0, lut_sh; // cell c = (float_as_int(sigma) - lut_b0) >> lut_sh
+    const float *sb;    // breakpoints s_b (fp32, strictly increasing), kLocD +inf pads
+    const uint16_t *lut16;  // per cell: b at the cell start | kLutSlow if > kLocD breakpoints inside
+    const float *vbound;    // per voxel max_b sum_pixels P hat_b (backward fixed-point bound)
     const float *stab;  // S~ [nb][nq] (scale, phi_k, E_k folded in)
     const int2 *vwin;   // per voxel [b_lo, b_hi] reachable by any of its pairs
     const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)
@@ -100,7 +101,8 @@ struct cacsi_geometry {
     void *d_vox, *d_vy64, *d_vz64, *d_vt64, *d_det, *d_dx64, *d_dy64, *d_mask, *d_energy;
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
-    void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b;
+    void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
+        *d_esai_vbound;
     cacsi::Er er;
     void *d_er_tb, *d_er_ptot;
     // host staging for the *_host entry points (device scratch)
