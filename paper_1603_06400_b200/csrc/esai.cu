@@ -119,20 +119,17 @@ __global__ void k_tbits_fwd_ts(const Params p, uint32_t *tb) {
     }
 }
 
-template <int T>
 __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
-    // word (v * nbatch + batch) * T + lane: bit k = T(v, pixel batch*32*T + k*T + lane)
-    const int nbatch = (p.n_det + 32 * T - 1) / (32 * T);
-    const size_t n = (size_t)p.n_vox * nbatch * T;
+    // word v * nw + j (nw = ceil(n_det / 32)): bit i = T(v, pixel 32 j + i)
+    const int nw = (p.n_det + 31) / 32;
+    const size_t n = (size_t)p.n_vox * nw;
     for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n; w += (size_t)gridDim.x * blockDim.x) {
-        const int lane = (int)(w % T);
-        const size_t r = w / T;
-        const int batch = (int)(r % nbatch), v = (int)(r / nbatch);
+        const int j = (int)(w % nw), v = (int)(w / nw);
         const VoxelRec vr = p.vox[v];
         uint32_t bits = 0;
-        for (int k = 0; k < 32; k++) {
-            const int q = batch * 32 * T + k * T + lane;
-            if (q < p.n_det && mask_open(p, v, q, vr, p.det[q])) bits |= 1u << k;
+        for (int i = 0; i < 32; i++) {
+            const int q = 32 * j + i;
+            if (q < p.n_det && mask_open(p, v, q, vr, p.det[q])) bits |= 1u << i;
         }
         tb[w] = bits;
     }
@@ -152,6 +149,18 @@ __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
 // Returns b with s_b <= sigma < s_{b+1} (clamped to [0, nb-2]) and tau in [0,1].
 constexpr int kLocD = 3;
 constexpr unsigned kLutSlow = 0x8000u;
+
+// Pop one set bit (the highest of the low word, else of the high word) of a
+// 64-voxel transmission batch: 32-bit FLO + SEL instead of 64-bit ffs.
+__device__ __forceinline__ int pop_bit(uint32_t &lo, uint32_t &hi) {
+    const bool l = lo != 0u;
+    const uint32_t w = l ? lo : hi;
+    const int i = 31 - __clz(w);
+    const uint32_t m = 1u << i;
+    lo = l ? lo ^ m : lo;
+    hi = l ? hi : hi ^ m;
+    return l ? i : i + 32;
+}
 
 __device__ __forceinline__ void load_bp(const Esai &e, float *sb, uint16_t *lut) {
     for (int i = threadIdx.x; i < e.nb + kLocD; i += blockDim.x) sb[i] = __ldg(e.sb + i);
@@ -178,10 +187,6 @@ __device__ __forceinline__ size_t bp_smem_bytes(const Esai &e) {
     return ((size_t)(e.nb + kLocD) * sizeof(float) + (size_t)e.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
 }
 
-__device__ __forceinline__ float lerp_w(const float *__restrict__ wr, float tau) {
-    const float w0 = __ldg(wr), w1 = __ldg(wr + 1);
-    return fmaf(tau, w1 - w0, w0);
-}
 
 constexpr int PF_TX = 16, PF_TY = 16, PF_T = PF_TX * PF_TY;  // 2D pixel tile
 constexpr int PF_CH = 32;                                     // voxels per transmission word
@@ -214,6 +219,7 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
             __syncwarp();  // reconverge after the previous batch's divergent pair loop
             uint32_t bits = valid ? __ldg(e.tb_fwd + (size_t)(c0 / PF_CH) * p.n_det + pix) : 0u;
             float acc = 0.0f;
+            float qP1 = 0.0f, qP2 = 0.0f, qt1 = 0.0f, qt2 = 0.0f, qa1 = 0.0f, qb1 = 0.0f, qa2 = 0.0f, qb2 = 0.0f;
             while (bits) {
                 const int i1 = __ffs(bits) - 1;
                 bits &= bits - 1;
@@ -225,11 +231,22 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
                 pair_geom(p, p.vox[c0 + i2], d, P2, s2);
                 const int b1 = locate(e, sb, lut, s1, t1);
                 const int b2 = locate(e, sb, lut, s2, t2);
-                const float w1 = lerp_w(W + (size_t)(c0 + i1) * e.ldw + b1, t1);
-                const float w2 = lerp_w(W + (size_t)(c0 + i2) * e.ldw + b2, t2);
-                acc = fmaf(P1, w1, acc);
-                acc = fmaf(two ? P2 : 0.0f, w2, acc);
+                // consume the previous couple first, then load into the same registers
+                acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
+                acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
+                const float *r1 = W + (size_t)(c0 + i1) * e.ldw + b1;
+                const float *r2 = W + (size_t)(c0 + i2) * e.ldw + b2;
+                qa1 = __ldg(r1);
+                qb1 = __ldg(r1 + 1);
+                qa2 = __ldg(r2);
+                qb2 = __ldg(r2 + 1);
+                qP1 = P1;
+                qP2 = two ? P2 : 0.0f;
+                qt1 = t1;
+                qt2 = t2;
             }
+            acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
+            acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
             tot += (double)acc;
         }
         if (valid) partial[(size_t)split * p.n_det + pix] = tot;
@@ -292,23 +309,28 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
                 vp[iy] = make_float4(rr.ry, rr.rz, rr.gso, 0.0f);
             }
             __syncthreads();
+            // W row of voxel (iy, iz) = Wz + iy * wstride (32-bit offsets: n_vox * ldw < 2^32, esai_build)
+            const float *Wz = W + (size_t)iz * e.ldw;
+            const unsigned wstride = (unsigned)nz * (unsigned)e.ldw;
             const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + (valid ? ix : 0)) * nyb) * p.det_ny +
                                     (valid ? jy : 0);
             float acc = 0.0f;
+            // software pipeline: the W gathers of one pair couple are consumed one
+            // iteration later, so their L2 latency overlaps the next couple's
+            // geometry and locate (pending P = 0 contributes nothing)
+            float qP1 = 0.0f, qP2 = 0.0f, qt1 = 0.0f, qt2 = 0.0f, qa1 = 0.0f, qb1 = 0.0f, qa2 = 0.0f, qb2 = 0.0f;
             // 64 voxels per batch (two transmission words): less lane imbalance
             for (int iyb = 0; iyb < ny; iyb += 64) {
                 __syncwarp();  // reconverge after the previous batch's divergent pair loop
-                unsigned long long bits = 0;
+                uint32_t blo = 0u, bhi = 0u;
                 if (valid) {
-                    bits = __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny);
-                    if (iyb + 32 < ny) bits |= (unsigned long long)__ldg(tbrow + (size_t)(iyb / 32 + 1) * p.det_ny) << 32;
+                    blo = __ldg(tbrow + (size_t)(iyb / 32) * p.det_ny);
+                    if (iyb + 32 < ny) bhi = __ldg(tbrow + (size_t)(iyb / 32 + 1) * p.det_ny);
                 }
-                while (bits) {
-                    const int k1 = __ffsll((long long)bits) - 1;
-                    bits &= bits - 1;
-                    const bool two = bits != 0;
-                    const int k2 = two ? __ffsll((long long)bits) - 1 : k1;
-                    bits &= bits - 1;
+                while (blo | bhi) {
+                    const int k1 = pop_bit(blo, bhi);
+                    const bool two = (blo | bhi) != 0u;
+                    const int k2 = two ? pop_bit(blo, bhi) : k1;
                     float Pp[2], sh[2];
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
@@ -326,12 +348,23 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
                     float t1, t2;
                     const int b1 = locate(e, sb, lut, sh[0], t1);
                     const int b2 = locate(e, sb, lut, sh[1], t2);
-                    const float w1 = lerp_w(W + (size_t)((iyb + k1) * nz + iz) * e.ldw + b1, t1);
-                    const float w2 = lerp_w(W + (size_t)((iyb + k2) * nz + iz) * e.ldw + b2, t2);
-                    acc = fmaf(Pp[0], w1, acc);
-                    acc = fmaf(two ? Pp[1] : 0.0f, w2, acc);
+                    // consume the previous couple first, then load into the same registers
+                    acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
+                    acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
+                    const float *r1 = Wz + ((unsigned)(iyb + k1) * wstride + (unsigned)b1);
+                    const float *r2 = Wz + ((unsigned)(iyb + k2) * wstride + (unsigned)b2);
+                    qa1 = __ldg(r1);
+                    qb1 = __ldg(r1 + 1);
+                    qa2 = __ldg(r2);
+                    qb2 = __ldg(r2 + 1);
+                    qP1 = Pp[0];
+                    qP2 = two ? Pp[1] : 0.0f;
+                    qt1 = t1;
+                    qt2 = t2;
                 }
             }
+            acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
+            acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
             tot += (double)acc;
         }
         if (valid) partial[(size_t)chunk * p.n_det + pix] = tot;
@@ -352,7 +385,8 @@ __global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, si
     }
 }
 
-constexpr int PB_T = 1024;
+constexpr int PB_T = 1024, PB_WARPS = PB_T / 32;
+constexpr int PB_QW = 32;  // transmission words (1024 pixels) per warp chunk
 
 // Backward pair stage (persistent over voxels): A[v, b] = sum_pixels P w hat_b(sigma).
 // Deposits go to a shared-memory histogram over the voxel's breakpoint window
@@ -365,6 +399,10 @@ constexpr int PB_T = 1024;
 // rint(x) - rint(x tau) -> b.  One unit is 2^-30 of the voxel's largest bin
 // (~2^-40 of its total response); integer adds are exact and
 // order-independent, so the backward is deterministic.
+// Pairs are interchangeable between lanes here (no per-lane accumulator), so
+// each warp first COMPACTS the open pixels of a 1024-pixel chunk (transmission
+// words, warp prefix sum of popcounts) into a pixel-sorted shared queue and
+// then sweeps it with all 32 lanes: converged lanes, coalesced pixel / w loads.
 // BOUND = true: w = 1, scale from the conservative bound sum_pixels |P| (used
 // once to measure vbound).
 template <bool BOUND>
@@ -375,10 +413,12 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     float *sb = (float *)smem;
     uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
     int *hist = (int *)(smem + bp_smem_bytes(e));  // [max_win]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint16_t *queue = (uint16_t *)(hist + ((e.max_win + 3) & ~3)) + warp * (PB_QW * 32);
     load_bp(e, sb, lut);
-    const int tid = threadIdx.x;
     const float wm = BOUND ? 1.0f : *wmax;
-    const int nbatch = (p.n_det + 32 * PB_T - 1) / (32 * PB_T);
+    const int nw = (p.n_det + 31) / 32;
+    const int nchunk = (nw + PB_QW - 1) / PB_QW;
     for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
         const int2 win = e.vwin[v];
         const int nwin = win.y - win.x + 1;
@@ -389,35 +429,44 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
         const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
         const VoxelRec vr = p.vox[v];
         int *hv = hist - win.x;
-        const uint32_t *tbv = e.tb_bwd + (size_t)v * nbatch * PB_T;
-        if (scale > 0.0f) {
-            // 64 pixels per lane per batch (two transmission words): less lane imbalance
-            for (int batch = 0; batch < nbatch; batch += 2) {
-                __syncwarp();  // reconverge after the previous batch's divergent pair loop
-                const int base = batch * 32 * PB_T;
-                unsigned long long bits = __ldg(tbv + batch * PB_T + tid);
-                if (batch + 1 < nbatch) bits |= (unsigned long long)__ldg(tbv + (batch + 1) * PB_T + tid) << 32;
-                while (bits) {
-                    const int k1 = __ffsll((long long)bits) - 1;
-                    bits &= bits - 1;
-                    const bool two = bits != 0;
-                    const int k2 = two ? __ffsll((long long)bits) - 1 : k1;
-                    bits &= bits - 1;
-                    const int q1 = base + k1 * PB_T + tid, q2 = base + k2 * PB_T + tid;
-                    float P1, s1, P2, s2, t1, t2;
-                    pair_geom(p, vr, p.det[q1], P1, s1);
-                    pair_geom(p, vr, p.det[q2], P2, s2);
-                    const int b1 = locate(e, sb, lut, s1, t1);
-                    const int b2 = locate(e, sb, lut, s2, t2);
-                    const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
-                    const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
-                    const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
-                    atomicAdd(hv + b1, __float2int_rn(a1) - x1);
-                    atomicAdd(hv + b1 + 1, x1);
-                    atomicAdd(hv + b2, __float2int_rn(a2) - x2);
-                    atomicAdd(hv + b2 + 1, x2);
-                }
+        const uint32_t *tbv = e.tb_bwd + (size_t)v * nw;
+        for (int ch = warp; scale > 0.0f && ch < nchunk; ch += PB_WARPS) {
+            // compaction: lane l owns word ch * PB_QW + l (pixels 32 j .. 32 j + 31)
+            const int j = ch * PB_QW + lane;
+            uint32_t m = j < nw ? __ldg(tbv + j) : 0u;
+            const int cnt = __popc(m);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += t;
             }
+            const int total = __shfl_sync(FULL, incl, 31);
+            int off = incl - cnt;
+            while (m) {
+                const int i = 31 - __clz(m);
+                queue[off++] = (uint16_t)(lane * 32 + i);
+                m ^= 1u << i;
+            }
+            __syncwarp();
+            const int qbase = ch * PB_QW * 32;
+            for (int k = lane; k < total; k += 64) {
+                const bool two = k + 32 < total;
+                const int q1 = qbase + queue[k], q2 = two ? qbase + queue[k + 32] : q1;
+                float P1, s1, P2, s2, t1, t2;
+                pair_geom(p, vr, p.det[q1], P1, s1);
+                pair_geom(p, vr, p.det[q2], P2, s2);
+                const int b1 = locate(e, sb, lut, s1, t1);
+                const int b2 = locate(e, sb, lut, s2, t2);
+                const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
+                const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
+                const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
+                atomicAdd(hv + b1, __float2int_rn(a1) - x1);
+                atomicAdd(hv + b1 + 1, x1);
+                atomicAdd(hv + b2, __float2int_rn(a2) - x2);
+                atomicAdd(hv + b2 + 1, x2);
+            }
+            __syncwarp();  // queue reuse
         }
         __syncthreads();
         const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
@@ -427,6 +476,10 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
             Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * unit : 0.0f;
         }
     }
+}
+
+static size_t bwd_smem_bytes(size_t bpb, int max_win) {
+    return bpb + (size_t)((max_win + 3) & ~3) * sizeof(int) + (size_t)PB_WARPS * PB_QW * 32 * sizeof(uint16_t);
 }
 
 // vbound[v] = (max_b A1[v, b] + n_det units) (1 + 1e-3): a bound on every bin of
@@ -659,7 +712,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     {
         const size_t nfw = p.ts_rho > 0 ? (size_t)p.nz * p.det_nx * ((p.ny + 31) / 32) * p.det_ny
                                         : (size_t)((p.n_vox + 31) / 32) * p.n_det;
-        const size_t nbw = (size_t)p.n_vox * ((p.n_det + 32 * PB_T - 1) / (32 * PB_T)) * PB_T;
+        const size_t nbw = (size_t)p.n_vox * ((p.n_det + 31) / 32);
         e = cudaMalloc(&g->d_tb_fwd, nfw * sizeof(uint32_t));
         if (e == cudaSuccess) e = cudaMalloc(&g->d_tb_bwd, nbw * sizeof(uint32_t));
         if (e != cudaSuccess) return e;
@@ -668,11 +721,15 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             k_tbits_fwd_ts<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_fwd);
         else
             k_tbits_fwd_tiled<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_fwd);
-        k_tbits_bwd<PB_T><<<blocks, 256>>>(p, (uint32_t *)g->d_tb_bwd);
+        k_tbits_bwd<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_bwd);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return e;
         E.tb_fwd = (const uint32_t *)g->d_tb_fwd;
         E.tb_bwd = (const uint32_t *)g->d_tb_bwd;
+    }
+    if ((double)nv * E.ldw >= 4294967296.0) {  // W / A offsets are 32-bit in the pair kernels
+        E.enabled = 0;
+        return cudaSuccess;
     }
     // shared-memory budgets of the pair kernels (227 KB per CTA); beyond them the
     // per-term kernels serve the handle
@@ -680,7 +737,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         const size_t fwd = p.ts_rho > 0 ? host_bp_bytes(E) + (size_t)p.ny * 16 +
                                               (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * 16
                                         : host_bp_bytes(E);
-        const size_t bwd = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
+        const size_t bwd = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         if (fwd > 227 * 1024 || bwd > 227 * 1024) {
             E.enabled = 0;
             return cudaSuccess;
@@ -693,7 +750,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         e = cudaMalloc(&g->d_esai_vbound, nv * sizeof(float));
         if (e == cudaSuccess) e = cudaMalloc(&A1, (size_t)nv * E.ldw * sizeof(float));
         if (e == cudaSuccess) {
-            const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
+            const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
             cudaFuncSetAttribute(k_esai_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             k_esai_bwd<true><<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, A1);
             k_vbound<<<nv, 256>>>(A1, E.ldw, E.ptot, p.n_det, (float *)g->d_esai_vbound);
@@ -831,7 +888,7 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
             KScope kt_(g, s, "k_absmax");
             k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
         }
-        const size_t smem = host_bp_bytes(E) + (size_t)E.max_win * sizeof(int);
+        const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {
             KScope kt_(g, s, "k_esai_bwd");
             cudaFuncSetAttribute(k_esai_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

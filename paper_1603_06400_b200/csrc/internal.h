@@ -77,7 +77,7 @@ struct Esai {
     int ldw;                 // row stride of W / A (nb rounded up to 32, zero padded)
     const float *tc_w;       // S~ as pre-split, pre-swizzled tensor-core B tiles (W = F S~^T)
     const float *tc_b;       // S~^T likewise (b2 = A S~)
-    const uint32_t *tb_bwd;  // backward: [voxel][batch][PB_T], bit k = pixel batch*32*PB_T + k*PB_T + lane
+    const uint32_t *tb_bwd;  // backward: [voxel][ceil(n_det/32)], bit i of word j = pixel 32 j + i
 };
 
 // energy-resolving handles (er.cu)
