@@ -1,10 +1,12 @@
 """Reconstruction oracle (TEST INFRASTRUCTURE): objective, closed-form update,
 Alg. 5.  fp64 numpy, written in the paper's notation (App. B, C).
 
-Readings: R13 quadratic psi(x) = x^2/2 (omega = 1), 4-connected
-(y, z) neighbourhood inside one q bin, w_jk = 1, symmetric (N^b = N);
-R14 update edge cases; R15 neg_loglik omits sum ln y! and keeps the paper's
-double-counted R.
+Readings: R13 quadratic psi(x) = x^2/2 (omega = 1) by default,
+Huber psi_delta as the edge-preserving option (R21), 4-connected (y, z)
+neighbourhood inside one q bin, w_jk = 1, symmetric (N^b = N); R14 update
+edge cases; R15 neg_loglik omits sum ln y! and keeps the paper's
+double-counted R; R20 ordered subsets (Alg. 6): row-group-major subset
+order, penalty weight beta / P per sub-iteration.
 """
 from __future__ import annotations
 
@@ -56,24 +58,66 @@ def _neighbour_shifts(f):
     _ = ny, nz
 
 
+class Penalty:
+    """Edge-preserving potential psi_delta of Eq. 7 with its
+    derivative psi_dot and the surrogate curvature omega(x) = psi_dot(x) / x
+    (PAPER.md:686-698).
+
+    kind "quadratic": psi(x) = x^2 / 2 (the default reading R13).
+    kind "huber":     psi(x) = x^2 / 2 for |x| <= delta, delta |x| - delta^2 / 2
+                      otherwise (Huber 1981, one of the potentials the paper
+                      cites at PAPER.md:346; reading R21), omega(0) = 1.
+    """
+
+    def __init__(self, kind: str = "quadratic", delta: float = float("inf")):
+        assert kind in ("quadratic", "huber")
+        if kind == "huber":
+            assert delta > 0
+        self.kind, self.delta = kind, float(delta)
+
+    def psi(self, x):
+        x = np.asarray(x, np.float64)
+        if self.kind == "quadratic":
+            return 0.5 * x * x
+        ax, d = np.abs(x), self.delta
+        return np.where(ax <= d, 0.5 * x * x, d * ax - 0.5 * d * d)
+
+    def psi_dot(self, x):
+        x = np.asarray(x, np.float64)
+        if self.kind == "quadratic":
+            return x
+        return np.clip(x, -self.delta, self.delta)
+
+    def omega(self, x):
+        x = np.asarray(x, np.float64)
+        if self.kind == "quadratic":
+            return np.ones_like(x)
+        ax = np.abs(x)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            return np.where(ax <= self.delta, 1.0, self.delta / ax)
+
+
+QUADRATIC = Penalty()
+
+
 def psi(x):
-    return 0.5 * x * x
+    return QUADRATIC.psi(x)
 
 
 def psi_dot(x):
-    return x
+    return QUADRATIC.psi_dot(x)
 
 
 def omega(x):
-    return np.ones_like(x)
+    return QUADRATIC.omega(x)
 
 
-def penalty(f):
+def penalty(f, pen: Penalty = QUADRATIC):
     """R(f) = sum_j sum_{k in N_j} w_jk psi(f_j - f_k)   (each pair counted twice)."""
     f = np.asarray(f, dtype=np.float64)
     R = 0.0
     for fk, valid in _neighbour_shifts(f):
-        R += psi(f - fk)[valid].sum()
+        R += pen.psi(f - fk)[valid].sum()
     return float(R)
 
 
@@ -86,9 +130,9 @@ def neg_loglik(l, y, r):
     return float(np.sum(z - ylogz))
 
 
-def objective(l, y, r, f, beta):
+def objective(l, y, r, f, beta, pen: Penalty = QUADRATIC):
     """J = L + beta R (Eq. overall_objective)."""
-    return neg_loglik(l, y, r) + beta * penalty(f)
+    return neg_loglik(l, y, r) + beta * penalty(f, pen)
 
 
 def ratio(l, y, r, eps=1e-12):
@@ -103,7 +147,7 @@ def ratio(l, y, r, eps=1e-12):
 
 
 # ---- closed-form update (Eq. f_update) -------------------
-def update(f_hat, b1, b2, beta):
+def update(f_hat, b1, b2, beta, pen: Penalty = QUADRATIC):
     """f^{t+1} from f^t = f_hat, b^(1) = A^T 1, b^(2) = A^T (y / (l + r))."""
     f_hat = np.asarray(f_hat, np.float64)
     b1 = np.asarray(b1, np.float64)
@@ -112,8 +156,8 @@ def update(f_hat, b1, b2, beta):
     b5 = np.zeros_like(f_hat)
     for fk, valid in _neighbour_shifts(f_hat):
         # b3 = 2 sum_{k in N_j} w_jk omega(f_j - f_k); b5 = sum w_jk psi_dot(f_j - f_k)
-        b3 += np.where(valid, 2.0 * omega(f_hat - fk), 0.0)
-        b5 += np.where(valid, psi_dot(f_hat - fk), 0.0)
+        b3 += np.where(valid, 2.0 * pen.omega(f_hat - fk), 0.0)
+        b5 += np.where(valid, pen.psi_dot(f_hat - fk), 0.0)
     b4, b6 = b3, b5  # symmetric neighbourhood: N^b = N, w_jk = w_kj
     chi1 = beta * (b3 + b4)
     chi2 = b1 + beta * (-f_hat * (b3 + b4) + b5 + b6)
@@ -125,7 +169,7 @@ def update(f_hat, b1, b2, beta):
     return out
 
 
-def em_iterate(geom, f0, y, r, b1, beta, n_iter, trace=None):
+def em_iterate(geom, f0, y, r, b1, beta, n_iter, trace=None, pen: Penalty = QUADRATIC):
     """Alg. 5 with the oracle's fp64 operators.
 
     Returns the list of iterates [f^1, ..., f^n].  If `trace` is a list, the
@@ -134,13 +178,68 @@ def em_iterate(geom, f0, y, r, b1, beta, n_iter, trace=None):
     iterates = []
     l = geom.forward(f)
     if trace is not None:
-        trace.append(objective(l, y, r, f, beta))
+        trace.append(objective(l, y, r, f, beta, pen))
     for _ in range(n_iter):
         rat = ratio(l, y, r)                  # y ./ (A f + r)
         b2 = geom.backward(rat)               # Back_project(y ./ z)
-        f = update(f, b1, b2, beta)           # Eq. f_update
+        f = update(f, b1, b2, beta, pen)      # Eq. f_update
         iterates.append(f.copy())
         l = geom.forward(f)
         if trace is not None:
-            trace.append(objective(l, y, r, f, beta))
+            trace.append(objective(l, y, r, f, beta, pen))
     return iterates
+
+
+# ---- ordered subsets (Alg. 6; Fig. 6) --------
+def symmetric_partition(M: int, N: int, rho_z: int, rho_y: int) -> np.ndarray:
+    """Symmetry-preserving measurement-space partition of an M x N detector
+    (PAPER.md:383-387), written as the paper's MATLAB index lists (1-based):
+
+      vertical:   rows m:rho_z:M/2 and M-m+1:-rho_z:M/2+1, 1 <= m <= rho_z
+      horizontal: columns n:rho_y:N and N-n+1:-rho_y:1,   1 <= n <= rho_y/2
+
+    Subset (m, n) = (row group, column group); P = rho_z rho_y / 2.  Returns
+    sub[row][col] in 0..P-1 with p = (m-1) (rho_y/2) + (n-1) (reading R20:
+    row-group-major order).  Rows are the paper's vertical (z) index = the
+    config frame's det x rows; columns its horizontal (y) index."""
+    if M % 2 or (M // 2) % rho_z or rho_y % 2 or N % rho_y or rho_z < 1 or rho_y < 2:
+        raise ValueError("partition needs rho_z | M/2, rho_y even, rho_y | N")
+    sub = -np.ones((M, N), dtype=np.int64)
+    half = rho_y // 2
+    for m in range(1, rho_z + 1):
+        rows = list(range(m, M // 2 + 1, rho_z)) + list(range(M - m + 1, M // 2, -rho_z))
+        for n in range(1, half + 1):
+            cols = list(range(n, N + 1, rho_y)) + list(range(N - n + 1, 0, -rho_y))
+            for i in rows:
+                for j in cols:
+                    assert sub[i - 1, j - 1] < 0, "subsets overlap"
+                    sub[i - 1, j - 1] = (m - 1) * half + (n - 1)
+    assert (sub >= 0).all(), "subsets do not cover the detector"
+    return sub
+
+
+def osem_iterate(geom, f0, y, r, subsets, beta, n_outer, trace=None, pen: Penalty = QUADRATIC):
+    """Alg. 6: per outer iteration sweep p = 0..P-1:
+    z_p = A_p f + r_p,  b2_p = A_p^T (y_p ./ z_p),  f <- Eq. f_update with
+    b1_p = A_p^T 1 and penalty weight beta / P (reading R20: the subset
+    data term stands for 1/P of L).  A_p f = (A f) restricted to subset p and
+    A_p^T w = A^T (w 1_p) -- the plain definitions.  Returns [f^1, ...]
+    (after each OUTER iteration); `trace` gets J(f^t) of the FULL objective."""
+    sub = np.asarray(subsets)
+    P = int(sub.max()) + 1
+    ind = [(sub == p).astype(np.float64) for p in range(P)]
+    b1 = [geom.backward(ind[p]) for p in range(P)]
+    f = np.asarray(f0, np.float64).copy()
+    out = []
+    if trace is not None:
+        trace.append(objective(geom.forward(f), y, r, f, beta, pen))
+    for _ in range(n_outer):
+        for p in range(P):
+            l = geom.forward(f)
+            rat = ratio(l, y, r) * ind[p]
+            b2 = geom.backward(rat)
+            f = update(f, b1[p], b2, beta / P, pen)
+        out.append(f.copy())
+        if trace is not None:
+            trace.append(objective(geom.forward(f), y, r, f, beta, pen))
+    return out
