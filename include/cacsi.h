@@ -176,6 +176,72 @@ CACSI_API cacsi_status cacsi_iterate_host(const cacsi_geometry *geom, float *f_h
                                 const float *r_host, const float *b1_host, float beta, int32_t n_iter,
                                 void *stream);
 
+/* ---- Edge-preserving penalty ---------------------
+ * psi_delta of Eq. 7 with the separable quadratic
+ * surrogate of PAPER.md:686-698 (curvature omega = psi_dot / x).
+ *   CACSI_PENALTY_QUADRATIC: psi(x) = x^2 / 2 (delta ignored) -- the default
+ *                            of the non-_ex calls (reading R13);
+ *   CACSI_PENALTY_HUBER:     psi(x) = x^2/2 for |x| <= delta,
+ *                            delta |x| - delta^2/2 otherwise; delta > 0 finite
+ *                            (reading R21).
+ * A NULL descriptor means quadratic; an invalid one -> CACSI_ERR_INVALID.  */
+typedef enum { CACSI_PENALTY_QUADRATIC = 0, CACSI_PENALTY_HUBER = 1 } cacsi_penalty_kind;
+typedef struct {
+    int32_t kind;  /* cacsi_penalty_kind */
+    double delta;  /* Huber scale (> 0), same units as f */
+} cacsi_penalty;
+
+/* As cacsi_update / cacsi_iterate / cacsi_neg_loglik with the potential `pen`
+ * (R = sum_j sum_{k in N_j} psi(f_j - f_k), each unordered pair twice).     */
+CACSI_API cacsi_status cacsi_update_ex(const cacsi_geometry *geom, const float *f_hat, const float *b1,
+                                       const float *b2, float beta, const cacsi_penalty *pen, float *f_new,
+                                       void *stream);
+CACSI_API cacsi_status cacsi_iterate_ex(const cacsi_geometry *geom, float *f, const float *y, const float *r,
+                                        const float *b1, float beta, const cacsi_penalty *pen, int32_t n_iter,
+                                        void *ws, void *stream);
+CACSI_API cacsi_status cacsi_neg_loglik_ex(const cacsi_geometry *geom, const float *f, const float *y,
+                                           const float *r, float beta, const cacsi_penalty *pen, double *out_dev,
+                                           void *ws, void *stream);
+
+/* ---- Ordered subsets (Alg. 6) ----
+ * cacsi_symmetric_subsets: the symmetry-preserving partition of the detector
+ * (Fig. 6): rows i (the paper's vertical index, config x)
+ * grouped as m:rho_x:M/2 with their up-down mirrors, columns j (y) as
+ * n:rho_y:N with their left-right mirrors; subset id = m (rho_y/2) + n
+ * (0-based, row-group-major), P = rho_x rho_y / 2 equal subsets.  HOST only
+ * (no device work): subset_of_pixel is a caller-owned host array
+ * [det_nx * det_ny].  Errors: CACSI_ERR_NULL; CACSI_ERR_INVALID unless
+ * det_nx is even, rho_x >= 1 divides det_nx/2, rho_y >= 2 is even and
+ * divides det_ny.                                                           */
+CACSI_API cacsi_status cacsi_symmetric_subsets(int32_t det_nx, int32_t det_ny, int32_t rho_x, int32_t rho_y,
+                                               int32_t *subset_of_pixel, int32_t *n_subsets);
+
+/* Subset-restricted operators of Alg. 6: `pixels` is a DEVICE list of
+ * n_pixels distinct detector pixel indices (ix * det_ny + jy).
+ *   cacsi_forward_subset : g = A_p f on the listed pixels, 0 elsewhere
+ *                          (detector shape, overwritten);
+ *   cacsi_backward_subset: b = A_p^T w = A^T (w restricted to the list).
+ * Energy-integrating (ESAI) handles run only the listed pixels' pairs; other
+ * handles run the full operator and restrict it.  Errors: CACSI_ERR_NULL,
+ * CACSI_ERR_INVALID (n_pixels < 0 or > det_nx * det_ny), CACSI_ERR_CUDA.  */
+CACSI_API cacsi_status cacsi_forward_subset(const cacsi_geometry *geom, const float *f, const int32_t *pixels,
+                                            int32_t n_pixels, float *g, void *stream);
+CACSI_API cacsi_status cacsi_backward_subset(const cacsi_geometry *geom, const float *w, const int32_t *pixels,
+                                             int32_t n_pixels, float *b, void *stream);
+
+/* n_outer outer iterations of Alg. 6, updating f in place.  Subset p owns the
+ * device pixels[offsets[p] .. offsets[p+1]) (offsets: HOST [n_subsets + 1],
+ * offsets[0] = 0); b1_subsets: DEVICE [n_subsets][ny][nz][nq] with
+ * b1_p = A_p^T 1 (cacsi_backward_subset of ones, computed once by the
+ * caller).  Each sub-iteration: z_p = A_p f + r, b2_p = A_p^T (y ./ z_p),
+ * f <- Eq. f_update(f, b1_p, b2_p) with penalty weight beta / n_subsets
+ * (reading R20: the subset data term stands for 1/P of L).  Subsets are swept
+ * in index order.  ws: cacsi_workspace_bytes() bytes.                      */
+CACSI_API cacsi_status cacsi_osem(const cacsi_geometry *geom, float *f, const float *y, const float *r,
+                                  const float *b1_subsets, const int32_t *pixels, const int32_t *offsets,
+                                  int32_t n_subsets, float beta, const cacsi_penalty *pen, int32_t n_outer,
+                                  void *ws, void *stream);
+
 /* Number of kernels the last successful device call on this handle enqueued
  * (for the bench's gpu_launches count).                                     */
 CACSI_API int32_t cacsi_last_launch_count(const cacsi_geometry *geom);

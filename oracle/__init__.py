@@ -73,6 +73,7 @@ def _L():
         lib.oracle_backward.argtypes = [P(_Desc), dp, dp]
         lib.oracle_forward_pixels.argtypes = [P(_Desc), dp, ctypes.c_long, i64p, dp]
         lib.oracle_backward_voxels.argtypes = [P(_Desc), dp, ctypes.c_long, i64p, dp]
+        lib.oracle_backward_pixels.argtypes = [P(_Desc), dp, ctypes.c_long, i64p, dp]
         lib.oracle_pair.argtypes = [P(_Desc), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
         lib.oracle_mask_cell.argtypes = [P(_Desc), ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, P(ctypes.c_int), P(ctypes.c_int)]
@@ -150,6 +151,14 @@ class Geometry:
         out = np.zeros((vox.size, self.nq))
         _L().oracle_backward_voxels(ctypes.byref(self.s), _dp(w), vox.size, _ip(vox), _dp(out))
         return out
+
+    def backward_pixels(self, w, pix) -> np.ndarray:
+        """A_p^T w: the backward sum restricted to flat pixel indices pix (Alg. 6)."""
+        w = np.ascontiguousarray(w, dtype=np.float64).reshape(self.g_shape)
+        pix = np.ascontiguousarray(pix, dtype=np.int64)
+        b = np.zeros(self.f_shape)
+        _L().oracle_backward_pixels(ctypes.byref(self.s), _dp(w), pix.size, _ip(pix), _dp(b))
+        return b
 
     def pair(self, iy, iz, ix, jy) -> dict:
         out = np.zeros(8)

@@ -267,6 +267,37 @@ void oracle_backward_voxels(const oracle_desc *d, const double *w, long n, const
         backward_voxel(d, w, (int)(vox[i] / d->nz), (int)(vox[i] % d->nz), out + i * d->nq);
 }
 
+/* backward restricted to a list of detector pixels (A_p^T w of Alg. 6,
+ * PAPER.md:393-412): b[r, j] = sum_{r' in list} sum_k P phi_k E_k w Lambda(u_k - j) */
+void oracle_backward_pixels(const oracle_desc *d, const double *w, long npix, const int64_t *pix, double *b) {
+    long nvox = (long)d->ny * d->nz;
+    int K = d->ne, Q = d->nq;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long v = 0; v < nvox; v++) {
+        int iy = (int)(v / d->nz), iz = (int)(v % d->nz);
+        double *bv = b + v * Q;
+        for (int j = 0; j < Q; j++) bv[j] = 0.0;
+        for (long i = 0; i < npix; i++) {
+            int ix = (int)(pix[i] / d->det_ny), jy = (int)(pix[i] % d->det_ny);
+            double fac[8];
+            oracle_pair(d, iy, iz, ix, jy, fac);
+            double P = fac[0], sh = fac[1];
+            if (P == 0.0) continue;
+            long p = pix[i];
+            for (int k = 0; k < K; k++) {
+                double wk = d->energy_resolving ? w[p * K + k] : w[p];
+                double u = node_coord(d, d->energy_kev[k], sh);
+                double j0 = floor(u);
+                for (int jj = 0; jj < 2; jj++) {
+                    double j = j0 + jj;
+                    if (j >= 0.0 && j <= (double)(Q - 1))
+                        bv[(int)j] += P * d->phi[k] * d->energy_kev[k] * wk * hat(u - j);
+                }
+            }
+        }
+    }
+}
+
 /* ---- work accounting ---------------------------
  * counts[0] = pairs, counts[1] = open pairs (T = 1),
  * counts[2] = effective terms: open pairs x energies with -1 < u_k < Q.     */

@@ -218,26 +218,41 @@ def symmetric_partition(M: int, N: int, rho_z: int, rho_y: int) -> np.ndarray:
     return sub
 
 
-def osem_iterate(geom, f0, y, r, subsets, beta, n_outer, trace=None, pen: Penalty = QUADRATIC):
+def osem_iterate(geom, f0, y, r, subsets, beta, n_outer, trace=None, pen: Penalty = QUADRATIC,
+                 restricted: bool = False):
     """Alg. 6: per outer iteration sweep p = 0..P-1:
     z_p = A_p f + r_p,  b2_p = A_p^T (y_p ./ z_p),  f <- Eq. f_update with
     b1_p = A_p^T 1 and penalty weight beta / P (reading R20: the subset
     data term stands for 1/P of L).  A_p f = (A f) restricted to subset p and
-    A_p^T w = A^T (w 1_p) -- the plain definitions.  Returns [f^1, ...]
-    (after each OUTER iteration); `trace` gets J(f^t) of the FULL objective."""
-    sub = np.asarray(subsets)
+    A_p^T w = A^T (w 1_p) -- the plain definitions; restricted=True evaluates
+    the same sums over the subset's pixels only (forward_pixels /
+    backward_pixels; pinned equal in tests).  Returns [f^1, ...] (after each
+    OUTER iteration); `trace` gets J(f^t) of the FULL objective."""
+    sub = np.asarray(subsets).reshape(-1)
     P = int(sub.max()) + 1
-    ind = [(sub == p).astype(np.float64) for p in range(P)]
-    b1 = [geom.backward(ind[p]) for p in range(P)]
+    pix = [np.flatnonzero(sub == p) for p in range(P)]
+    ind = [(sub == p).astype(np.float64).reshape(geom.g_shape) for p in range(P)]
+    ones = np.ones(geom.g_shape)
+
+    def fwd_p(f, p):
+        if restricted:
+            out = np.zeros(geom.g_shape).reshape(-1)
+            out[pix[p]] = geom.forward_pixels(f, pix[p])
+            return out.reshape(geom.g_shape)
+        return geom.forward(f) * ind[p]
+
+    def bwd_p(w, p):
+        return geom.backward_pixels(w, pix[p]) if restricted else geom.backward(w * ind[p])
+
+    b1 = [bwd_p(ones, p) for p in range(P)]
     f = np.asarray(f0, np.float64).copy()
     out = []
     if trace is not None:
         trace.append(objective(geom.forward(f), y, r, f, beta, pen))
     for _ in range(n_outer):
         for p in range(P):
-            l = geom.forward(f)
-            rat = ratio(l, y, r) * ind[p]
-            b2 = geom.backward(rat)
+            rat = ratio(fwd_p(f, p), y, r) * ind[p]
+            b2 = bwd_p(rat, p)
             f = update(f, b1[p], b2, beta / P, pen)
         out.append(f.copy())
         if trace is not None:

@@ -24,13 +24,34 @@ SYMBOLS = ["cacsi_geometry_create", "cacsi_geometry_destroy", "cacsi_workspace_b
            "cacsi_detector_size", "cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate",
            "cacsi_forward_host", "cacsi_backward_host", "cacsi_iterate_host", "cacsi_last_launch_count",
            "cacsi_status_string", "cacsi_ratio", "cacsi_update", "cacsi_set_timing", "cacsi_kernel_times",
-           "cacsi_query"]
+           "cacsi_query", "cacsi_update_ex", "cacsi_iterate_ex", "cacsi_neg_loglik_ex", "cacsi_symmetric_subsets",
+           "cacsi_forward_subset", "cacsi_backward_subset", "cacsi_osem"]
+
+CACSI_PENALTY_QUADRATIC, CACSI_PENALTY_HUBER = 0, 1
 
 
 class CacsiError(RuntimeError):
     def __init__(self, status: int, where: str):
         self.status = status
         super().__init__(f"{where}: {status_string(status)} (status {status})")
+
+
+class Penalty(ctypes.Structure):
+    """cacsi_penalty (include/cacsi.h): kind 0 quadratic, 1 Huber with scale delta."""
+    _fields_ = [("kind", ctypes.c_int32), ("delta", ctypes.c_double)]
+
+    @staticmethod
+    def make(kind="quadratic", delta=0.0):
+        return Penalty(CACSI_PENALTY_HUBER if kind == "huber" else CACSI_PENALTY_QUADRATIC, float(delta))
+
+
+def _pen(pen):
+    if pen is None:
+        return None
+    if isinstance(pen, Penalty):
+        return ctypes.byref(pen)
+    kind, delta = pen
+    return ctypes.byref(Penalty.make(kind, delta))
 
 
 class GeometryDesc(ctypes.Structure):
@@ -93,6 +114,18 @@ def lib():
         L.cacsi_kernel_times.restype = ctypes.c_int32
         L.cacsi_query.argtypes = [vp, ctypes.c_char_p]
         L.cacsi_query.restype = ctypes.c_int64
+        pp = ctypes.POINTER(Penalty)
+        i32 = ctypes.c_int32
+        L.cacsi_update_ex.argtypes = [vp, fp, fp, fp, ctypes.c_float, pp, fp, vp]
+        L.cacsi_iterate_ex.argtypes = [vp, fp, fp, fp, fp, ctypes.c_float, pp, i32, vp, vp]
+        L.cacsi_neg_loglik_ex.argtypes = [vp, fp, fp, fp, ctypes.c_float, pp, vp, vp, vp]
+        L.cacsi_symmetric_subsets.argtypes = [i32, i32, i32, i32, vp, ctypes.POINTER(i32)]
+        L.cacsi_forward_subset.argtypes = [vp, fp, vp, i32, fp, vp]
+        L.cacsi_backward_subset.argtypes = [vp, fp, vp, i32, fp, vp]
+        L.cacsi_osem.argtypes = [vp, fp, fp, fp, fp, vp, vp, i32, ctypes.c_float, pp, i32, vp, vp]
+        for n in ("cacsi_update_ex", "cacsi_iterate_ex", "cacsi_neg_loglik_ex", "cacsi_symmetric_subsets",
+                  "cacsi_forward_subset", "cacsi_backward_subset", "cacsi_osem"):
+            getattr(L, n).restype = ctypes.c_int
         L.cacsi_status_string.argtypes = [ctypes.c_int]
         L.cacsi_status_string.restype = ctypes.c_char_p
         _lib = L
@@ -116,6 +149,24 @@ def _ptr(t) -> int:
     if not t.is_contiguous():
         raise ValueError("tensor must be contiguous")
     return t.data_ptr()
+
+
+def _iptr(t) -> int:
+    """Device pointer of a contiguous int32 CUDA tensor."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.int32 or not t.is_contiguous():
+        raise TypeError("expected a contiguous int32 CUDA tensor")
+    return t.data_ptr()
+
+
+def symmetric_subsets(det_nx: int, det_ny: int, rho_x: int, rho_y: int) -> np.ndarray:
+    """cacsi_symmetric_subsets (host only): subset id per pixel, [det_nx][det_ny]."""
+    out = np.empty((det_nx, det_ny), dtype=np.int32)
+    n = ctypes.c_int32()
+    _check(lib().cacsi_symmetric_subsets(det_nx, det_ny, rho_x, rho_y, out.ctypes.data, ctypes.byref(n)),
+           "cacsi_symmetric_subsets")
+    assert n.value == int(out.max()) + 1
+    return out
 
 
 def _stream(stream):
@@ -230,6 +281,47 @@ class Geometry:
                                   self._dev(b2, self.n_obj, "b2"), float(beta), self._dev(f_new, self.n_obj, "f_new"),
                                   _stream(stream)), "cacsi_update")
         return f_new
+
+    # -- penalties (Huber) and ordered subsets (Alg. 6) ---------------------
+    def update_ex(self, f_hat, b1, b2, beta, pen, f_new, stream=None):
+        _check(lib().cacsi_update_ex(self.handle, self._dev(f_hat, self.n_obj, "f_hat"),
+                                     self._dev(b1, self.n_obj, "b1"), self._dev(b2, self.n_obj, "b2"), float(beta),
+                                     _pen(pen), self._dev(f_new, self.n_obj, "f_new"), _stream(stream)),
+               "cacsi_update_ex")
+        return f_new
+
+    def iterate_ex(self, f, y, r, b1, beta, pen, n_iter, ws, stream=None):
+        _check(lib().cacsi_iterate_ex(self.handle, self._dev(f, self.n_obj, "f"), self._dev(y, self.n_det, "y"),
+                                      self._dev(r, self.n_det, "r"), self._dev(b1, self.n_obj, "b1"), float(beta),
+                                      _pen(pen), int(n_iter), ws.data_ptr(), _stream(stream)), "cacsi_iterate_ex")
+        return f
+
+    def neg_loglik_ex(self, f, y, r, beta, pen, out, ws, stream=None):
+        _check(lib().cacsi_neg_loglik_ex(self.handle, self._dev(f, self.n_obj, "f"), self._dev(y, self.n_det, "y"),
+                                         self._dev(r, self.n_det, "r"), float(beta), _pen(pen), out.data_ptr(),
+                                         ws.data_ptr(), _stream(stream)), "cacsi_neg_loglik_ex")
+        return out
+
+    def forward_subset(self, f, pixels, g, stream=None):
+        _check(lib().cacsi_forward_subset(self.handle, self._dev(f, self.n_obj, "f"), _iptr(pixels), pixels.numel(),
+                                          self._dev(g, self.n_det, "g"), _stream(stream)), "cacsi_forward_subset")
+        return g
+
+    def backward_subset(self, w, pixels, b, stream=None):
+        _check(lib().cacsi_backward_subset(self.handle, self._dev(w, self.n_det, "w"), _iptr(pixels),
+                                           pixels.numel(), self._dev(b, self.n_obj, "b"), _stream(stream)),
+               "cacsi_backward_subset")
+        return b
+
+    def osem(self, f, y, r, b1_subsets, pixels, offsets, beta, pen, n_outer, ws, stream=None):
+        """offsets: host int sequence of length P + 1; b1_subsets: [P, *f_shape] fp32 CUDA."""
+        off = np.ascontiguousarray(offsets, dtype=np.int32)
+        P = len(off) - 1
+        _check(lib().cacsi_osem(self.handle, self._dev(f, self.n_obj, "f"), self._dev(y, self.n_det, "y"),
+                                self._dev(r, self.n_det, "r"), self._dev(b1_subsets, P * self.n_obj, "b1_subsets"),
+                                _iptr(pixels), off.ctypes.data, P, float(beta), _pen(pen), int(n_outer),
+                                ws.data_ptr(), _stream(stream)), "cacsi_osem")
+        return f
 
     # -- host API (numpy fp32, end-to-end) -----------------------------------
     def forward_host(self, f, g, stream=None):

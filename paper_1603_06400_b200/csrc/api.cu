@@ -322,24 +322,39 @@ static void ws_split(const cacsi_geometry *g, void *ws, float **l, float **b2, f
     *part = (double *)p;
 }
 
-cacsi_status cacsi_neg_loglik(const cacsi_geometry *g, const float *f, const float *y, const float *r, float beta,
-                              double *out_dev, void *ws, void *stream) {
+// penalty descriptor -> delta (<= 0: quadratic), or -1 on an invalid descriptor
+static double pen_delta(const cacsi_penalty *pen) {
+    if (!pen || pen->kind == CACSI_PENALTY_QUADRATIC) return 0.0;
+    if (pen->kind == CACSI_PENALTY_HUBER && pen->delta > 0.0 && std::isfinite(pen->delta)) return pen->delta;
+    return -1.0;
+}
+
+cacsi_status cacsi_neg_loglik_ex(const cacsi_geometry *g, const float *f, const float *y, const float *r, float beta,
+                                 const cacsi_penalty *pen, double *out_dev, void *ws, void *stream) {
     if (!g || !f || !y || !r || !out_dev || !ws) return CACSI_ERR_NULL;
+    const double delta = pen_delta(pen);
+    if (delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
     double *part;
     ws_split(g, ws, &l, &b2, &fnew, &part);
     cudaStream_t s = (cudaStream_t)stream;
     int n = 0;
     cudaError_t e = cacsi::launch_forward(g, f, l, s, &n);
-    if (e == cudaSuccess) e = cacsi::launch_loglik(g, l, y, r, f, beta, part, out_dev, s, &n);
+    if (e == cudaSuccess) e = cacsi::launch_loglik(g, l, y, r, f, beta, delta, part, out_dev, s, &n);
     if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
 }
 
-cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
-                           float beta, int32_t n_iter, void *ws, void *stream) {
+cacsi_status cacsi_neg_loglik(const cacsi_geometry *g, const float *f, const float *y, const float *r, float beta,
+                              double *out_dev, void *ws, void *stream) {
+    return cacsi_neg_loglik_ex(g, f, y, r, beta, nullptr, out_dev, ws, stream);
+}
+
+cacsi_status cacsi_iterate_ex(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
+                              float beta, const cacsi_penalty *pen, int32_t n_iter, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1 || !ws) return CACSI_ERR_NULL;
-    if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
+    const double delta = pen_delta(pen);
+    if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
     double *part;
     ws_split(g, ws, &l, &b2, &fnew, &part);
@@ -350,11 +365,16 @@ cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, co
         e = cacsi::launch_forward(g, f, l, s, &n);                                   // z = A f (+ r below)
         if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, &n);  // y ./ z
         if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, &n);           // b2 = A^T (y ./ z)
-        if (e == cudaSuccess) e = cacsi::launch_update(g, f, b1, b2, beta, fnew, s, &n);  // Eq. f_update
+        if (e == cudaSuccess) e = cacsi::launch_update(g, f, b1, b2, beta, delta, fnew, s, &n);  // Eq. f_update
         if (e == cudaSuccess) e = cudaMemcpyAsync(f, fnew, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
     }
     if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
+}
+
+cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
+                           float beta, int32_t n_iter, void *ws, void *stream) {
+    return cacsi_iterate_ex(g, f, y, r, b1, beta, nullptr, n_iter, ws, stream);
 }
 
 cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
@@ -366,12 +386,94 @@ cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y
     return map_err(e);
 }
 
+cacsi_status cacsi_update_ex(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
+                             const cacsi_penalty *pen, float *f_new, void *stream) {
+    if (!g || !f_hat || !b1 || !b2 || !f_new) return CACSI_ERR_NULL;
+    const double delta = pen_delta(pen);
+    if (!(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
+    int n = 0;
+    cudaError_t e = cacsi::launch_update(g, f_hat, b1, b2, beta, delta, f_new, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
 cacsi_status cacsi_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
                           float *f_new, void *stream) {
-    if (!g || !f_hat || !b1 || !b2 || !f_new) return CACSI_ERR_NULL;
-    if (!(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
+    return cacsi_update_ex(g, f_hat, b1, b2, beta, nullptr, f_new, stream);
+}
+
+// ---- ordered subsets (Alg. 6) ----------------------------
+cacsi_status cacsi_symmetric_subsets(int32_t det_nx, int32_t det_ny, int32_t rho_x, int32_t rho_y,
+                                     int32_t *subset_of_pixel, int32_t *n_subsets) {
+    if (!subset_of_pixel || !n_subsets) return CACSI_ERR_NULL;
+    if (det_nx < 2 || det_ny < 2 || det_nx % 2 || rho_x < 1 || (det_nx / 2) % rho_x || rho_y < 2 || rho_y % 2 ||
+        det_ny % rho_y)
+        return CACSI_ERR_INVALID;
+    const int M = det_nx, N = det_ny, half = rho_y / 2;
+    for (int i = 0; i < M; i++) {
+        // vertical group: row i and its up-down mirror M-1-i share m = (min(i, M-1-i) mod rho_x)
+        const int iu = i < M / 2 ? i : M - 1 - i;
+        const int m = iu % rho_x;
+        for (int j = 0; j < N; j++) {
+            // horizontal group: columns n + k rho_y (r = j mod rho_y < rho_y/2) and their
+            // left-right mirrors N-1-(n + k rho_y) (r >= rho_y/2 -> n = (N-1-j) mod rho_y)
+            const int rj = j % rho_y;
+            const int n = rj < half ? rj : (N - 1 - j) % rho_y;
+            subset_of_pixel[(size_t)i * N + j] = m * half + n;
+        }
+    }
+    *n_subsets = rho_x * half;
+    return CACSI_OK;
+}
+
+cacsi_status cacsi_forward_subset(const cacsi_geometry *g, const float *f, const int32_t *pixels, int32_t n_pixels,
+                                  float *out, void *stream) {
+    if (!g || !f || !out || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
+    if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
     int n = 0;
-    cudaError_t e = cacsi::launch_update(g, f_hat, b1, b2, beta, f_new, (cudaStream_t)stream, &n);
+    cudaError_t e = cacsi::launch_forward_subset(g, f, pixels, n_pixels, out, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_backward_subset(const cacsi_geometry *g, const float *w, const int32_t *pixels, int32_t n_pixels,
+                                   float *b, void *stream) {
+    if (!g || !w || !b || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
+    if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
+    int n = 0;
+    cudaError_t e = cacsi::launch_backward_subset(g, w, pixels, n_pixels, b, (cudaStream_t)stream, &n);
+    if (e == cudaSuccess) g->last_launches = n;
+    return map_err(e);
+}
+
+cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1_subsets,
+                        const int32_t *pixels, const int32_t *offsets, int32_t n_subsets, float beta,
+                        const cacsi_penalty *pen, int32_t n_outer, void *ws, void *stream) {
+    if (!g || !f || !y || !r || !b1_subsets || !pixels || !offsets || !ws) return CACSI_ERR_NULL;
+    const double delta = pen_delta(pen);
+    if (n_subsets < 1 || n_outer < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0)
+        return CACSI_ERR_INVALID;
+    if (offsets[0] != 0) return CACSI_ERR_INVALID;
+    for (int p = 0; p < n_subsets; p++)
+        if (offsets[p + 1] < offsets[p] || offsets[p + 1] > g->p.n_det) return CACSI_ERR_INVALID;
+    float *l, *b2, *fnew;
+    double *part;
+    ws_split(g, ws, &l, &b2, &fnew, &part);
+    cudaStream_t s = (cudaStream_t)stream;
+    const float beta_p = beta / (float)n_subsets;  // reading R20: the subset term stands for 1/P of L
+    int n = 0;
+    cudaError_t e = cudaSuccess;
+    for (int t = 0; t < n_outer && e == cudaSuccess; t++)
+        for (int p = 0; p < n_subsets && e == cudaSuccess; p++) {
+            const int32_t *px = pixels + offsets[p];
+            const int np = offsets[p + 1] - offsets[p];
+            e = cacsi::launch_forward_subset(g, f, px, np, l, s, &n);                  // z_p = A_p f (+ r_p)
+            if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, &n);  // y_p ./ z_p
+            if (e == cudaSuccess) e = cacsi::launch_backward_subset(g, l, px, np, b2, s, &n);  // b2_p
+            if (e == cudaSuccess)
+                e = cacsi::launch_update(g, f, b1_subsets + (size_t)p * g->n_obj, b2, beta_p, delta, fnew, s, &n);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(f, fnew, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        }
     if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
 }

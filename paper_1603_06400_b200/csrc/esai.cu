@@ -371,11 +371,78 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
     }
 }
 
+// Subset forward (ordered subsets, Alg. 6): lanes = LISTED pixels, items =
+// (256-pixel chunk of the list, voxel split).  T is evaluated per pair by the
+// exact rule (mask_open; the transmission bitmaps are laid out for the full
+// detector), 32 voxels per bit batch as in k_esai_fwd.
+constexpr int PL_T = 256;
+
+__global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Esai e, const float *__restrict__ W,
+                                                        const int32_t *__restrict__ list, int n, int vox_per_split,
+                                                        int n_items, double *__restrict__ partial) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
+    load_bp(e, sb, lut);
+    __syncthreads();
+    const int n_chunks = (n + PL_T - 1) / PL_T;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int chunk = item % n_chunks, split = item / n_chunks;
+        const int i = chunk * PL_T + threadIdx.x;
+        const bool valid = i < n;
+        const int pix = valid ? list[i] : list[0];
+        const float2 d = p.det[pix];
+        const int v0 = split * vox_per_split;
+        const int v1 = min(p.n_vox, v0 + vox_per_split);
+        double tot = 0.0;
+        for (int c0 = v0; c0 < v1; c0 += 32) {
+            __syncwarp();
+            uint32_t bits = 0u;
+            if (valid)
+                for (int k = 0; k < 32 && c0 + k < v1; k++)
+                    if (mask_open(p, c0 + k, pix, p.vox[c0 + k], d)) bits |= 1u << k;
+            float acc = 0.0f;
+            while (bits) {
+                const int k = 31 - __clz(bits);
+                bits ^= 1u << k;
+                float P, sh, t;
+                pair_geom(p, p.vox[c0 + k], d, P, sh);
+                const int b = locate(e, sb, lut, sh, t);
+                const float *r = W + (size_t)(c0 + k) * e.ldw + b;
+                const float w0 = __ldg(r), w1 = __ldg(r + 1);
+                acc = fmaf(P, fmaf(t, w1 - w0, w0), acc);
+            }
+            tot += (double)acc;
+        }
+        if (valid) partial[(size_t)split * n + i] = tot;
+    }
+}
+
+// out[list[i]] = sum_s partial[s][i]   (fixed order, fp64)
+__global__ void k_sum_list(const double *__restrict__ part, int S, const int32_t *__restrict__ list, int n,
+                           float *__restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < S; j++) s += part[(size_t)j * n + i];
+        out[list[i]] = (float)s;
+    }
+}
+
+// pixel list -> detector bitmap (bit i of word j = pixel 32 j + i)
+__global__ void k_list_to_mask(const int32_t *__restrict__ list, int n, uint32_t *__restrict__ mask) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicOr(mask + (list[i] >> 5), 1u << (list[i] & 31));
+}
+
 // max |w| over the detector (fixed-point scale of the backward histogram)
-__global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, size_t n, float *out) {
+// (pmask != nullptr: only the subset's pixels count -- the fixed-point unit of a
+// subset backward must not be set by weights it never deposits)
+__global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, size_t n, const uint32_t *pmask,
+                                                 float *out) {
     __shared__ float s[32];
     float m = 0.0f;
-    for (size_t i = threadIdx.x; i < n; i += 1024) m = fmaxf(m, fabsf(w[i]));
+    for (size_t i = threadIdx.x; i < n; i += 1024)
+        if (pmask == nullptr || ((pmask[i >> 5] >> (i & 31)) & 1u)) m = fmaxf(m, fabsf(w[i]));
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -408,7 +475,7 @@ constexpr int PB_QW = 32;  // transmission words (1024 pixels) per warp chunk
 template <bool BOUND>
 __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
                                                    const float *__restrict__ wmax, const float *__restrict__ vbound,
-                                                   float *__restrict__ A) {
+                                                   const uint32_t *__restrict__ pmask, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sb = (float *)smem;
     uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
@@ -434,6 +501,7 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
             // compaction: lane l owns word ch * PB_QW + l (pixels 32 j .. 32 j + 31)
             const int j = ch * PB_QW + lane;
             uint32_t m = j < nw ? __ldg(tbv + j) : 0u;
+            if (pmask != nullptr && j < nw) m &= __ldg(pmask + j);  // subset-restricted (Alg. 6)
             const int cnt = __popc(m);
             int incl = cnt;
 #pragma unroll
@@ -752,7 +820,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e == cudaSuccess) {
             const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
             cudaFuncSetAttribute(k_esai_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_bwd<true><<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, A1);
+            k_esai_bwd<true><<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, nullptr, A1);
             k_vbound<<<nv, 256>>>(A1, E.ldw, E.ptot, p.n_det, (float *)g->d_esai_vbound);
             e = cudaDeviceSynchronize();
         }
@@ -803,7 +871,20 @@ cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     return cudaSuccess;
 }
 
+static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
+                                     float *out, cudaStream_t s, int *launches);
+
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
+    return esai_forward_impl(g, f, nullptr, 0, out, s, launches);
+}
+
+cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
+                              cudaStream_t s, int *launches) {
+    return esai_forward_impl(g, f, pixels, n, out, s, launches);
+}
+
+static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
+                                     float *out, cudaStream_t s, int *launches) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *W = nullptr;
@@ -830,7 +911,34 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
         cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
         k_tc_gemm<<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, E.nb, p.nq, ldf, nkc, nkc, fp, E.tc_w, W, E.ldw);
     }
-    if (p.ts_rho > 0) {
+    if (pixels != nullptr) {
+        // subset: g = 0 outside the list, listed pixels by k_esai_fwd_list
+        e = cudaMemsetAsync(out, 0, (size_t)p.n_det * sizeof(float), s);
+        const int n_chunks = (n_pix + PL_T - 1) / PL_T;
+        const int grid = persistent_grid(g, bpb, PL_T);
+        S = std::max(1, std::min((4 * grid + n_chunks - 1) / n_chunks, (p.n_vox + 31) / 32));
+        int vps = (p.n_vox + S - 1) / S;
+        vps = (vps + 31) / 32 * 32;
+        S = (p.n_vox + vps - 1) / vps;
+        if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S * n_pix * sizeof(double), s);
+        if (e == cudaSuccess) {
+            {
+                KScope kt_(g, s, "k_esai_fwd_list");
+                cudaFuncSetAttribute(k_esai_fwd_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bpb);
+                k_esai_fwd_list<<<grid, PL_T, bpb, s>>>(p, E, W, pixels, n_pix, vps, n_chunks * S, part);
+            }
+            {
+                KScope kt_(g, s, "k_sum_list");
+                k_sum_list<<<(n_pix + 255) / 256, 256, 0, s>>>(part, S, pixels, n_pix, out);
+            }
+        }
+        if (e == cudaSuccess) e = cudaGetLastError();
+        *launches += 4;
+        if (part) cudaFreeAsync(part, s);
+        cudaFreeAsync(fp, s);
+        cudaFreeAsync(W, s);
+        return e;
+    } else if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
         const int n_groups = ((p.det_nx + TS_R - 1) / TS_R) * segs;
         const size_t smem = bpb + (size_t)p.ny * sizeof(float4) + (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * sizeof(float4);
@@ -872,6 +980,11 @@ cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cu
 }
 
 cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
+    return esai_backward_masked(g, w, nullptr, b, s, launches);
+}
+
+cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
+                                 cudaStream_t s, int *launches) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
@@ -886,13 +999,13 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     if (e == cudaSuccess) {
         {
             KScope kt_(g, s, "k_absmax");
-            k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, wmax);
+            k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, pmask, wmax);
         }
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {
             KScope kt_(g, s, "k_esai_bwd");
             cudaFuncSetAttribute(k_esai_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_bwd<false><<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, A);
+            k_esai_bwd<false><<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, pmask, A);
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
@@ -911,6 +1024,73 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     if (wmax) cudaFreeAsync(wmax, s);
     if (part) cudaFreeAsync(part, s);
     if (A) cudaFreeAsync(A, s);
+    return e;
+}
+
+
+// Subset-restricted operators of Alg. 6.  ESAI handles run
+// only the listed pixels' pairs; other handles run the full operator on the
+// GPU and restrict its input / output (the plain definitions A_p f = (A f)|_p,
+// A_p^T w = A^T (w 1_p)).
+__global__ void k_restrict(float *__restrict__ x, int per_pixel, const uint32_t *__restrict__ mask, size_t n_det) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_det * per_pixel;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const size_t q = i / per_pixel;
+        if (!((mask[q >> 5] >> (q & 31)) & 1u)) x[i] = 0.0f;
+    }
+}
+
+static cudaError_t make_mask(const cacsi_geometry *g, const int32_t *pixels, int n, uint32_t **mask, cudaStream_t s) {
+    const size_t nw = (size_t)(g->p.n_det + 31) / 32;
+    cudaError_t e = cudaMallocAsync((void **)mask, nw * sizeof(uint32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(*mask, 0, nw * sizeof(uint32_t), s);
+    if (e == cudaSuccess && n > 0) {
+        KScope kt_(g, s, "k_list_to_mask");
+        k_list_to_mask<<<(n + 255) / 256, 256, 0, s>>>(pixels, n, *mask);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
+cudaError_t launch_forward_subset(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
+                                  cudaStream_t s, int *launches) {
+    if (n <= 0) return cudaMemsetAsync(out, 0, g->n_detout * sizeof(float), s);
+    if (g->esai.enabled) return esai_forward_list(g, f, pixels, n, out, s, launches);
+    uint32_t *mask = nullptr;
+    cudaError_t e = make_mask(g, pixels, n, &mask, s);
+    if (e == cudaSuccess) e = launch_forward(g, f, out, s, launches);
+    if (e == cudaSuccess) {
+        KScope kt_(g, s, "k_restrict");
+        k_restrict<<<4 * sm_count(g->device), 256, 0, s>>>(out, g->energy_resolving ? g->ne : 1, mask, g->p.n_det);
+        e = cudaGetLastError();
+        *launches += 2;
+    }
+    if (mask) cudaFreeAsync(mask, s);
+    return e;
+}
+
+cudaError_t launch_backward_subset(const cacsi_geometry *g, const float *w, const int32_t *pixels, int n, float *b,
+                                   cudaStream_t s, int *launches) {
+    if (n <= 0) return cudaMemsetAsync(b, 0, g->n_obj * sizeof(float), s);
+    uint32_t *mask = nullptr;
+    cudaError_t e = make_mask(g, pixels, n, &mask, s);
+    *launches += 1;
+    if (e == cudaSuccess && g->esai.enabled) {
+        e = esai_backward_masked(g, w, mask, b, s, launches);
+    } else if (e == cudaSuccess) {
+        float *wr = nullptr;
+        e = cudaMallocAsync(&wr, g->n_detout * sizeof(float), s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(wr, w, g->n_detout * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_restrict");
+            k_restrict<<<4 * sm_count(g->device), 256, 0, s>>>(wr, g->energy_resolving ? g->ne : 1, mask, g->p.n_det);
+            e = cudaGetLastError();
+            *launches += 1;
+        }
+        if (e == cudaSuccess) e = launch_backward(g, wr, b, s, launches);
+        if (wr) cudaFreeAsync(wr, s);
+    }
+    if (mask) cudaFreeAsync(mask, s);
     return e;
 }
 

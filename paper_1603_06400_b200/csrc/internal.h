@@ -140,10 +140,20 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
 cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 cudaError_t launch_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
                          double *partials, int nblocks, cudaStream_t s, int *launches);
+// delta <= 0: quadratic potential; delta > 0: Huber psi_delta (recon.cu)
 cudaError_t launch_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2,
-                          float beta, float *f_new, cudaStream_t s, int *launches);
+                          float beta, double delta, float *f_new, cudaStream_t s, int *launches);
 cudaError_t launch_loglik(const cacsi_geometry *g, const float *l, const float *y, const float *r, const float *f,
-                          float beta, double *partials, double *out, cudaStream_t s, int *launches);
+                          float beta, double delta, double *partials, double *out, cudaStream_t s, int *launches);
+// subset-restricted operators (Alg. 6): `pixels` = device list of n distinct detector pixels
+cudaError_t launch_forward_subset(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
+                                  cudaStream_t s, int *launches);
+cudaError_t launch_backward_subset(const cacsi_geometry *g, const float *w, const int32_t *pixels, int n, float *b,
+                                   cudaStream_t s, int *launches);
+cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
+                              cudaStream_t s, int *launches);
+cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
+                                 cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d);

@@ -53,8 +53,27 @@ __global__ void __launch_bounds__(RT) k_loglik_part(const float *__restrict__ l,
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-// partial[blockIdx] = sum over elements j of sum_{k in N_j} (f_j - f_k)^2 / 2
-__global__ void __launch_bounds__(RT) k_penalty_part(const Params p, const float *__restrict__ f, double *partial) {
+// Edge-preserving potential (Eq. 7): psi, psi_dot and the
+// surrogate curvature omega = psi_dot / x.  delta <= 0
+// selects the quadratic psi(x) = x^2/2 (reading R13), else Huber (R21).
+__device__ __forceinline__ double pen_psi(double x, double delta) {
+    const double ax = fabs(x);
+    return (delta <= 0.0 || ax <= delta) ? 0.5 * x * x : delta * ax - 0.5 * delta * delta;
+}
+__device__ __forceinline__ void pen_dot_omega(double x, double delta, double &pd, double &om) {
+    const double ax = fabs(x);
+    if (delta <= 0.0 || ax <= delta) {
+        pd = x;
+        om = 1.0;
+    } else {
+        pd = x > 0.0 ? delta : -delta;
+        om = delta / ax;
+    }
+}
+
+// partial[blockIdx] = sum over elements j of sum_{k in N_j} psi(f_j - f_k)
+__global__ void __launch_bounds__(RT) k_penalty_part(const Params p, const float *__restrict__ f, double delta,
+                                                     double *partial) {
     __shared__ double sh[RT];
     const size_t n = (size_t)p.n_vox * p.nq;
     const size_t sz = p.nq, sy = (size_t)p.nz * p.nq;
@@ -63,11 +82,11 @@ __global__ void __launch_bounds__(RT) k_penalty_part(const Params p, const float
         const int iy = (int)(i / sy), iz = (int)((i / sz) % p.nz);
         const double fj = f[i];
         double s = 0.0;
-        if (iy > 0) s += (fj - f[i - sy]) * (fj - f[i - sy]);
-        if (iy + 1 < p.ny) s += (fj - f[i + sy]) * (fj - f[i + sy]);
-        if (iz > 0) s += (fj - f[i - sz]) * (fj - f[i - sz]);
-        if (iz + 1 < p.nz) s += (fj - f[i + sz]) * (fj - f[i + sz]);
-        acc += 0.5 * s;
+        if (iy > 0) s += pen_psi(fj - f[i - sy], delta);
+        if (iy + 1 < p.ny) s += pen_psi(fj - f[i + sy], delta);
+        if (iz > 0) s += pen_psi(fj - f[i - sz], delta);
+        if (iz + 1 < p.nz) s += pen_psi(fj - f[i + sz], delta);
+        acc += s;
     }
     const double s = block_sum(acc, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -82,29 +101,30 @@ __global__ void k_loglik_final(const double *lpart, const double *rpart, int nb,
     }
 }
 
-// Eq. f_update with psi(x) = x^2/2 (omega = 1), 4-connected (y, z), w = 1:
-//   chi1 = beta (b3 + b4) = 4 beta |N_j|
-//   chi2 = b1 + beta (-f^ (b3 + b4) + b5 + b6) = b1 - 2 beta (|N_j| f^ + sum_k f^_k)
-//   chi3 = f^ b2
+// Eq. f_update, 4-connected (y, z) neighbours, w = 1,
+// symmetric (N^b = N, so b4 = b3 and b6 = b5):
+//   b3 = 2 sum_k omega(f^_j - f^_k),  b5 = sum_k psi_dot(f^_j - f^_k)
+//   chi1 = beta (b3 + b4),  chi2 = b1 + beta (-f^ (b3 + b4) + b5 + b6),  chi3 = f^ b2
+// (quadratic psi: chi1 = 4 beta |N_j|, chi2 = b1 - 2 beta (|N_j| f^ + sum_k f^_k)).
 // root = 2 chi3 / (chi2 + sqrt(D)) if chi2 > 0 (same number as the paper's
 // (-chi2 + sqrt D)/(2 chi1), no cancellation), else (-chi2 + sqrt D)/(2 chi1);
 // chi1 = 0 and chi2 <= 0 (voxel never seen): keep f^ (reading R14).
 __global__ void k_update(const Params p, const float *__restrict__ f_hat, const float *__restrict__ b1,
-                         const float *__restrict__ b2, float beta, float *__restrict__ f_new) {
+                         const float *__restrict__ b2, float beta, double delta, float *__restrict__ f_new) {
     const size_t n = (size_t)p.n_vox * p.nq;
     const size_t sz = p.nq, sy = (size_t)p.nz * p.nq;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const int iy = (int)(i / sy), iz = (int)((i / sz) % p.nz);
         const double fj = f_hat[i];
-        double sk = 0.0;
-        int nb = 0;
-        if (iy > 0) { sk += f_hat[i - sy]; nb++; }
-        if (iy + 1 < p.ny) { sk += f_hat[i + sy]; nb++; }
-        if (iz > 0) { sk += f_hat[i - sz]; nb++; }
-        if (iz + 1 < p.nz) { sk += f_hat[i + sz]; nb++; }
+        double som = 0.0, spd = 0.0, pd, om;
+        if (iy > 0) { pen_dot_omega(fj - f_hat[i - sy], delta, pd, om); som += om; spd += pd; }
+        if (iy + 1 < p.ny) { pen_dot_omega(fj - f_hat[i + sy], delta, pd, om); som += om; spd += pd; }
+        if (iz > 0) { pen_dot_omega(fj - f_hat[i - sz], delta, pd, om); som += om; spd += pd; }
+        if (iz + 1 < p.nz) { pen_dot_omega(fj - f_hat[i + sz], delta, pd, om); som += om; spd += pd; }
         const double bt = beta;
-        const double chi1 = 4.0 * bt * nb;
-        const double chi2 = (double)b1[i] - 2.0 * bt * (nb * fj + sk);
+        const double b34 = 4.0 * som, b56 = 2.0 * spd;
+        const double chi1 = bt * b34;
+        const double chi2 = (double)b1[i] + bt * (-fj * b34 + b56);
         const double chi3 = fj * (double)b2[i];
         const double sq = sqrt(fmax(chi2 * chi2 + 4.0 * chi1 * chi3, 0.0));
         double x;
@@ -138,19 +158,19 @@ cudaError_t launch_ratio(const cacsi_geometry *g, const float *l, const float *y
 }
 
 cudaError_t launch_update(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
-                          float *f_new, cudaStream_t s, int *launches) {
+                          double delta, float *f_new, cudaStream_t s, int *launches) {
     {
         KScope kt_(g, s, "k_update");
-        k_update<<<grid_for(g->n_obj), RT, 0, s>>>(g->p, f_hat, b1, b2, beta, f_new);
+        k_update<<<grid_for(g->n_obj), RT, 0, s>>>(g->p, f_hat, b1, b2, beta, delta, f_new);
     }
     *launches += 1;
     return cudaGetLastError();
 }
 
 cudaError_t launch_loglik(const cacsi_geometry *g, const float *l, const float *y, const float *r, const float *f,
-                          float beta, double *partials, double *out, cudaStream_t s, int *launches) {
+                          float beta, double delta, double *partials, double *out, cudaStream_t s, int *launches) {
     k_loglik_part<<<RED_BLOCKS, RT, 0, s>>>(l, y, r, g->n_detout, partials);
-    k_penalty_part<<<RED_BLOCKS, RT, 0, s>>>(g->p, f, partials + RED_BLOCKS);
+    k_penalty_part<<<RED_BLOCKS, RT, 0, s>>>(g->p, f, delta, partials + RED_BLOCKS);
     k_loglik_final<<<1, 32, 0, s>>>(partials, partials + RED_BLOCKS, RED_BLOCKS, beta, out);
     *launches += 3;
     return cudaGetLastError();

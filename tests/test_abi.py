@@ -97,3 +97,20 @@ def test_no_device_is_an_error_not_a_fallback():
     if torch.cuda.is_available():
         pytest.skip("has a GPU")
     assert _create(_desc()) == binding.CACSI_ERR_CUDA
+
+
+@pytest.mark.parametrize("args", [(32, 64, 8, 16), (16, 16, 4, 8), (128, 128, 8, 16), (256, 256, 8, 16),
+                                  (6, 10, 3, 2), (8, 12, 2, 6), (4, 4, 1, 2)])
+def test_symmetric_subsets_match_oracle_partition(args):
+    """cacsi_symmetric_subsets (closed-form modular rule, host only) equals the
+    oracle's literal MATLAB-list enumeration of PAPER.md:383-387."""
+    from oracle import recon
+    np.testing.assert_array_equal(binding.symmetric_subsets(*args), recon.symmetric_partition(*args))
+
+
+@pytest.mark.parametrize("args", [(32, 64, 3, 16), (32, 64, 8, 15), (32, 60, 8, 16), (31, 64, 8, 16),
+                                  (32, 64, 0, 16), (32, 64, 8, 0)])
+def test_symmetric_subsets_rejects_bad_steps(args):
+    with pytest.raises(binding.CacsiError) as ei:
+        binding.symmetric_subsets(*args)
+    assert ei.value.status == binding.CACSI_ERR_INVALID

@@ -196,3 +196,28 @@ def test_osem_accelerates():
     recon.osem_iterate(G, f0, y, r, sub, beta, 1, t_os)
     recon.em_iterate(G, f0, y, r, b1, beta, 8, t_em)
     assert t_os[-1] <= t_em[-1]
+
+
+def test_restricted_operators_equal_masked_definitions():
+    """forward_pixels / backward_pixels (sums over the subset's pixels only)
+    equal the masked full operators (A f)|_p and A^T (w 1_p) -- the oracle's
+    two ways of writing A_p agree."""
+    cfg = make_config(0)
+    G = oracle.Geometry(cfg)
+    sub = recon.symmetric_partition(cfg.det_nx, cfg.det_ny, 4, 8).ravel()
+    f = cfg.f.astype(np.float64)
+    w = seeded_rng(6, 1).uniform(0, 1, G.g_shape)
+    g = G.forward(f).ravel()
+    for p in (0, 5, 15):
+        pix = np.flatnonzero(sub == p)
+        np.testing.assert_allclose(G.forward_pixels(f, pix), g[pix], rtol=1e-15)
+        np.testing.assert_allclose(G.backward_pixels(w, pix), G.backward(w * (sub == p).reshape(G.g_shape)),
+                                   rtol=1e-12, atol=1e-300)
+
+
+def test_osem_restricted_matches_definition():
+    G, f_true, y, r, b1, f0 = _em_setup()
+    sub = recon.symmetric_partition(16, 16, 4, 8)
+    a = recon.osem_iterate(G, f0, y, r, sub, 1e-3, 1)
+    b = recon.osem_iterate(G, f0, y, r, sub, 1e-3, 1, restricted=True)
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-10)
