@@ -58,6 +58,7 @@ class _Desc(ctypes.Structure):
         ("det_z", ctypes.c_double), ("det_pitch", ctypes.c_double),
         ("det_cx", ctypes.c_double), ("det_cy", ctypes.c_double),
         ("energy_resolving", ctypes.c_int32), ("scale", ctypes.c_double),
+        ("sai_n_theta", ctypes.c_int32), ("sai_theta_min", ctypes.c_double), ("sai_theta_max", ctypes.c_double),
     ]
 
 
@@ -78,6 +79,8 @@ def _L():
         lib.oracle_mask_cell.argtypes = [P(_Desc), ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, P(ctypes.c_int), P(ctypes.c_int)]
         lib.oracle_count_terms.argtypes = [P(_Desc), ctypes.c_long, i64p, i64p]
+        lib.oracle_sai_angle.argtypes = [P(_Desc), ctypes.c_double]
+        lib.oracle_sai_angle.restype = ctypes.c_double
         for fn in ("oracle_G_so", "oracle_G_od"):
             getattr(lib, fn).argtypes = [dp]
             getattr(lib, fn).restype = ctypes.c_double
@@ -95,6 +98,9 @@ class Geometry:
     def __init__(self, cfg, **override):
         d = cfg.desc() if hasattr(cfg, "desc") else dict(cfg)
         d.update(override)
+        d.setdefault("sai_n_theta", 0)
+        d.setdefault("sai_theta_min", 0.0)
+        d.setdefault("sai_theta_max", 0.0)
         self.d = d
         self._e = np.ascontiguousarray(d["energy_kev"], dtype=np.float64)
         self._phi = np.ascontiguousarray(d["phi"], dtype=np.float64)
@@ -159,6 +165,10 @@ class Geometry:
         b = np.zeros(self.f_shape)
         _L().oracle_backward_pixels(ctypes.byref(self.s), _dp(w), pix.size, _ip(pix), _dp(b))
         return b
+
+    def sai_angle(self, theta: float) -> float:
+        """The tabulated angle scatter-angle interpolation uses for theta."""
+        return _L().oracle_sai_angle(ctypes.byref(self.s), float(theta))
 
     def pair(self, iy, iz, ix, jy) -> dict:
         out = np.zeros(8)

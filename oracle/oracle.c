@@ -50,6 +50,12 @@ typedef struct {
     double det_z, det_pitch, det_cx, det_cy;
     int32_t energy_resolving;
     double scale; /* C_E */
+    /* scatter-angle interpolation:
+     * sai_n_theta > 0 replaces the spectral-angular factor of every pair by its
+     * value at the nearest of sai_n_theta uniform angles on
+     * [sai_theta_min, sai_theta_max] (reading R22); 0 = the exact operator. */
+    int32_t sai_n_theta;
+    double sai_theta_min, sai_theta_max;
 } oracle_desc;
 
 /* ---- discretisation (readings R4, R9) ------------------------- */
@@ -140,6 +146,20 @@ static double mask_T(const oracle_desc *d, double y_r, double z_r, double x_d, d
     return d->mask[(size_t)cx * d->mask_ny + cy] ? 1.0 : 0.0;
 }
 
+/* Scatter-angle interpolation: the nearest of the N
+ * uniformly spaced angles theta_i = theta_min + i h, h = (theta_max -
+ * theta_min) / (N - 1), i = 0 .. N-1 (reading R22).  Written as the plain
+ * rounding rule i = floor((theta - theta_min) / h + 1/2), clamped. */
+double oracle_sai_angle(const oracle_desc *d, double theta) {
+    int N = d->sai_n_theta;
+    if (N <= 1) return d->sai_theta_min;
+    double h = (d->sai_theta_max - d->sai_theta_min) / (N - 1);
+    double i = floor((theta - d->sai_theta_min) / h + 0.5);
+    if (i < 0.0) i = 0.0;
+    if (i > (double)(N - 1)) i = (double)(N - 1);
+    return d->sai_theta_min + i * h;
+}
+
 /* Per-pair factors.  out[0..7] = P, sin(theta/2), cos(theta/2), theta,
  * dtheta, T, G_so, G_od.  P = C_E G_so G_od T dtheta (1+cos^2 theta) cos(theta/2) */
 void oracle_pair(const oracle_desc *d, int iy, int iz, int ix, int jy, double out[8]) {
@@ -151,10 +171,16 @@ void oracle_pair(const oracle_desc *d, int iy, int iz, int ix, int jy, double ou
     double th = oracle_theta(r, rp);
     double dth = oracle_dtheta(r, rp, d->det_pitch);
     double T = mask_T(d, r[1], r[2], rp[0], rp[1]);
-    double c = cos(th);
-    out[0] = d->scale * gso * god * T * dth * (1.0 + c * c) * cos(0.5 * th);
-    out[1] = sin(0.5 * th);
-    out[2] = cos(0.5 * th);
+    /* the angle at which the spectral factor S(theta, q) -- here its energy
+     * form (1 + cos^2 th) cos(th/2) sum_k phi_k E_k Lambda(u_k - j) -- is
+     * evaluated: theta itself, or under scatter-angle interpolation the
+     * nearest tabulated angle (nearest neighbour) */
+    double ts = th;
+    if (d->sai_n_theta > 0) ts = oracle_sai_angle(d, th);
+    double c = cos(ts);
+    out[0] = d->scale * gso * god * T * dth * (1.0 + c * c) * cos(0.5 * ts);
+    out[1] = sin(0.5 * ts);
+    out[2] = cos(0.5 * ts);
     out[3] = th;
     out[4] = dth;
     out[5] = T;
