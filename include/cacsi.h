@@ -77,7 +77,7 @@ typedef struct cacsi_geometry cacsi_geometry; /* opaque, immutable after create 
  *       every scatter vector has s_z > 0 and crosses the mask plane);
  *   q_min < q_max; mask_pitch > 0; det_pitch > 0; scale > 0 and finite;
  *   energy_kev strictly increasing and > 0; phi >= 0; mask bytes in {0, 1};
- *   energy_resolving in {0, 1}.                                              */
+ *   energy_resolving in {0, 1}; sai_n_theta >= 0 (see below).                */
 typedef struct {
     /* object slice: voxel centres y_i = y_min + (i + 1/2) (y_max - y_min)/ny,
      * likewise z ("B spatial bins")                            */
@@ -104,6 +104,16 @@ typedef struct {
     double det_z, det_pitch, det_cx, det_cy;
     int32_t energy_resolving; /* 0: g[dx][dy]; 1: g[dx][dy][ne]             */
     double scale;             /* C_E, the calibration constant */
+    /* Scatter-angle interpolation,
+     * the paper's approximate operator: sai_n_theta > 0 evaluates each pair's
+     * spectral-angular factor (1 + cos^2 t) cos(t/2) sum_k phi_k E_k
+     * Lambda(E_k sin(t/2)/hc - q) at the NEAREST of sai_n_theta angles
+     * t_i = sai_theta_min + i h, h = (max - min)/(n - 1) (reading R22;
+     * G_so, G_od, T, dtheta stay exact per pair).  0 = the exact operator.
+     * Energy-integrating handles only; requires 0 <= min < max <= pi when
+     * n >= 2 (else CACSI_ERR_INVALID).                                      */
+    int32_t sai_n_theta;
+    double sai_theta_min, sai_theta_max;
 } cacsi_geometry_desc;
 
 /* Validate `desc`, precompute the per-voxel / per-pixel / per-energy tables

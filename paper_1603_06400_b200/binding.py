@@ -71,6 +71,7 @@ class GeometryDesc(ctypes.Structure):
         ("det_z", ctypes.c_double), ("det_pitch", ctypes.c_double),
         ("det_cx", ctypes.c_double), ("det_cy", ctypes.c_double),
         ("energy_resolving", ctypes.c_int32), ("scale", ctypes.c_double),
+        ("sai_n_theta", ctypes.c_int32), ("sai_theta_min", ctypes.c_double), ("sai_theta_max", ctypes.c_double),
     ]
 
 
@@ -191,6 +192,9 @@ class Geometry:
 
     def __init__(self, desc: dict, device: int = 0):
         d = dict(desc)
+        d.setdefault("sai_n_theta", 0)
+        d.setdefault("sai_theta_min", 0.0)
+        d.setdefault("sai_theta_max", 0.0)
         self._e = np.ascontiguousarray(d["energy_kev"], dtype=np.float64)
         self._phi = np.ascontiguousarray(d["phi"], dtype=np.float64)
         self._mask = np.ascontiguousarray(d["mask"], dtype=np.uint8)

@@ -36,6 +36,14 @@ cacsi_status validate(const cacsi_geometry_desc *d) {
     if (!(d->q_min < d->q_max) || !(d->mask_pitch > 0.0) || !(d->det_pitch > 0.0)) return CACSI_ERR_INVALID;
     if (!(d->scale > 0.0) || !std::isfinite(d->scale)) return CACSI_ERR_INVALID;
     if (d->energy_resolving != 0 && d->energy_resolving != 1) return CACSI_ERR_INVALID;
+    if (d->sai_n_theta < 0) return CACSI_ERR_INVALID;
+    if (d->sai_n_theta > 0) {
+        if (d->energy_resolving) return CACSI_ERR_INVALID;  // SAI is the energy-integrating model's (Alg. 2)
+        if (!std::isfinite(d->sai_theta_min) || !std::isfinite(d->sai_theta_max) || !(d->sai_theta_min >= 0.0))
+            return CACSI_ERR_INVALID;
+        if (d->sai_n_theta > 1 && !(d->sai_theta_min < d->sai_theta_max && d->sai_theta_max <= M_PI))
+            return CACSI_ERR_INVALID;
+    }
     for (int k = 0; k < d->ne; k++) {
         if (!(d->energy_kev[k] > 0.0) || !std::isfinite(d->energy_kev[k])) return CACSI_ERR_INVALID;
         if (k > 0 && !(d->energy_kev[k] > d->energy_kev[k - 1])) return CACSI_ERR_INVALID;
@@ -147,6 +155,10 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     p.m0y = m0y;
     p.mask_pitch64 = mp;
     p.det_z = (float)d->det_z;
+    p.det_z64 = d->det_z;
+    p.sai_n = d->sai_n_theta;
+    p.sai_tmin = d->sai_theta_min;
+    p.sai_h = d->sai_n_theta > 1 ? (d->sai_theta_max - d->sai_theta_min) / (d->sai_n_theta - 1) : 1.0;
     p.pitch_d = (float)d->det_pitch;
     p.quarter_p2 = (float)(0.25 * d->det_pitch * d->det_pitch);
     p.ax = (float)(-m0x / mp);
@@ -243,7 +255,7 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
         const double rho = std::floor(dyv / d->det_pitch + 0.5);
         p.ts_rho = 0;
         if (rho >= 1.0 && rho <= 64.0 && std::fabs(dyv - rho * d->det_pitch) <= 1e-9 * d->det_pitch &&
-            !getenv("CACSI_NO_TS")) {
+            !getenv("CACSI_NO_TS") && d->sai_n_theta == 0) {  // SAI runs the tiled forward
             p.ts_rho = (int)rho;
             p.ts_c0 = (float)(det_centre(d->det_cy, d->det_ny, d->det_pitch, 0) - centre(d->y_min, d->y_max, d->ny, 0));
         }
@@ -260,8 +272,18 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
             return map_err(e);
         }
     }
+    if (d->sai_n_theta > 0 && algo && strcmp(algo, "direct") == 0) {  // SAI lives in the ESAI tables
+        free_all(g);
+        free(g);
+        return CACSI_ERR_INVALID;
+    }
     if (!d->energy_resolving && !(algo && strcmp(algo, "direct") == 0)) {
         e = cacsi::esai_build(g, d);
+        if (e == cudaSuccess && d->sai_n_theta > 0 && !g->esai.enabled) {  // beyond the table limits
+            free_all(g);
+            free(g);
+            return CACSI_ERR_INVALID;
+        }
         if (e != cudaSuccess) {
             free_all(g);
             free(g);

@@ -183,6 +183,38 @@ __device__ __forceinline__ int locate(const Esai &e, const float *sb, const uint
     return b;
 }
 
+// Scatter-angle interpolation (p.sai_n > 0): the nodes are the boundaries
+// between tabulated angles, the pair takes its cell's row (tau = 0, nearest
+// neighbour).  Within kSaiGuard (relative) of a boundary the
+// fp32 sigma cannot decide the nearest angle; the cell is then re-derived from
+// the fp64 angle by the rounding rule of reading R22 (same decision as the
+// oracle).
+constexpr float kSaiGuard = 4e-6f;
+
+__device__ __forceinline__ int sai_cell(const Params &p, const Esai &e, const float *sb, float s, int b, int v, int q) {
+    const bool near_lo = b > 0 && (s - sb[b]) < kSaiGuard * s;
+    const bool near_hi = b + 2 < e.nb && (sb[b + 1] - s) < kSaiGuard * s;
+    if (near_lo || near_hi) {
+        const double th = theta64(p, v, q);
+        double i = floor((th - p.sai_tmin) / p.sai_h + 0.5);
+        i = fmin(fmax(i, 0.0), (double)(p.sai_n - 1));
+        b = min(max((int)i - e.sai_i0, 0), e.nb - 2);
+    }
+    return b;
+}
+
+// locate for a pair (v, q): exact ESAI (tau = position in the breakpoint
+// interval) or SAI (tau = 0 in the nearest-angle cell)
+__device__ __forceinline__ int locate_pair(const Params &p, const Esai &e, const float *sb, const uint16_t *lut,
+                                           float s, int v, int q, float &tau) {
+    int b = locate(e, sb, lut, s, tau);
+    if (p.sai_n > 0) {
+        b = sai_cell(p, e, sb, s, b, v, q);
+        tau = 0.0f;
+    }
+    return b;
+}
+
 __device__ __forceinline__ size_t bp_smem_bytes(const Esai &e) {
     return ((size_t)(e.nb + kLocD) * sizeof(float) + (size_t)e.nl * sizeof(uint16_t) + 15) & ~(size_t)15;
 }
@@ -227,10 +259,10 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
                 const int i2 = two ? __ffs(bits) - 1 : i1;
                 bits &= bits - 1;
                 float P1, s1, P2, s2, t1, t2;
-                pair_geom(p, p.vox[c0 + i1], d, P1, s1);
-                pair_geom(p, p.vox[c0 + i2], d, P2, s2);
-                const int b1 = locate(e, sb, lut, s1, t1);
-                const int b2 = locate(e, sb, lut, s2, t2);
+                pair_geom(p, p.vox[c0 + i1], d, P1, s1, p.sai_n == 0);
+                pair_geom(p, p.vox[c0 + i2], d, P2, s2, p.sai_n == 0);
+                const int b1 = locate_pair(p, e, sb, lut, s1, c0 + i1, pix, t1);
+                const int b2 = locate_pair(p, e, sb, lut, s2, c0 + i2, pix, t2);
                 // consume the previous couple first, then load into the same registers
                 acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
                 acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
@@ -406,8 +438,8 @@ __global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Es
                 const int k = 31 - __clz(bits);
                 bits ^= 1u << k;
                 float P, sh, t;
-                pair_geom(p, p.vox[c0 + k], d, P, sh);
-                const int b = locate(e, sb, lut, sh, t);
+                pair_geom(p, p.vox[c0 + k], d, P, sh, p.sai_n == 0);
+                const int b = locate_pair(p, e, sb, lut, sh, c0 + k, pix, t);
                 const float *r = W + (size_t)(c0 + k) * e.ldw + b;
                 const float w0 = __ldg(r), w1 = __ldg(r + 1);
                 acc = fmaf(P, fmaf(t, w1 - w0, w0), acc);
@@ -522,10 +554,10 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
                 const bool two = k + 32 < total;
                 const int q1 = qbase + queue[k], q2 = two ? qbase + queue[k + 32] : q1;
                 float P1, s1, P2, s2, t1, t2;
-                pair_geom(p, vr, p.det[q1], P1, s1);
-                pair_geom(p, vr, p.det[q2], P2, s2);
-                const int b1 = locate(e, sb, lut, s1, t1);
-                const int b2 = locate(e, sb, lut, s2, t2);
+                pair_geom(p, vr, p.det[q1], P1, s1, p.sai_n == 0);
+                pair_geom(p, vr, p.det[q2], P2, s2, p.sai_n == 0);
+                const int b1 = locate_pair(p, e, sb, lut, s1, v, q1, t1);
+                const int b2 = locate_pair(p, e, sb, lut, s2, v, q2, t2);
                 const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
                 const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
                 const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
@@ -665,11 +697,21 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     std::vector<std::pair<float, double>> nodes;
     nodes.push_back({(float)lo, (double)(float)lo});
     nodes.push_back({(float)hi, (double)(float)hi});
-    for (int k = 0; k < K; k++)
-        for (int m = -1; m <= Q; m++) {
-            const double s = (m + beta0) / alpha[k];
+    const bool sai = p.sai_n > 0;
+    if (!sai) {
+        for (int k = 0; k < K; k++)
+            for (int m = -1; m <= Q; m++) {
+                const double s = (m + beta0) / alpha[k];
+                if (s > lo && s < hi) nodes.push_back({(float)s, s});
+            }
+    } else {
+        // SAI: nodes = sigma at the boundaries between tabulated angles,
+        // t_{i+1/2} = t_min + (i + 1/2) h (nearest-angle cells, reading R22)
+        for (int i = 0; i + 1 < p.sai_n; i++) {
+            const double s = std::sin(0.5 * (p.sai_tmin + (i + 0.5) * p.sai_h));
             if (s > lo && s < hi) nodes.push_back({(float)s, s});
         }
+    }
     std::sort(nodes.begin(), nodes.end());
     std::vector<float> sb;
     std::vector<double> sx;
@@ -683,8 +725,17 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     std::vector<float2> bp(nb);
     std::vector<float> stab((size_t)nb * Q, 0.0f);
     std::vector<double> row(Q);
+    // SAI: angle index of the first cell = number of boundaries <= lo
+    int sai_i0 = 0;
+    if (sai)
+        while (sai_i0 + 1 < p.sai_n && std::sin(0.5 * (p.sai_tmin + (sai_i0 + 0.5) * p.sai_h)) <= lo) sai_i0++;
     for (int b = 0; b < nb; b++) {
-        const double s = sx[b];
+        double s = sx[b], ang = 1.0;
+        if (sai) {  // row of cell b: the spectral-angular factor at its tabulated angle
+            const double t = p.sai_tmin + std::min(sai_i0 + std::min(b, nb - 2), p.sai_n - 1) * p.sai_h;
+            s = std::sin(0.5 * t);
+            ang = (1.0 + std::cos(t) * std::cos(t)) * std::cos(0.5 * t);
+        }
         bp[b] = make_float2(sb[b], b + 1 < nb ? (float)(1.0 / ((double)sb[b + 1] - (double)sb[b])) : 0.0f);
         std::fill(row.begin(), row.end(), 0.0);
         for (int k = 0; k < K; k++) {
@@ -694,7 +745,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             if (j >= 0 && j < Q) row[j] += ck[k] * (1.0 - t);
             if (j + 1 >= 0 && j + 1 < Q) row[j + 1] += ck[k] * t;
         }
-        for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)row[j];
+        for (int j = 0; j < Q; j++) stab[(size_t)b * Q + j] = (float)(row[j] * ang);
     }
     // LUT over the fp32 bit patterns of [s_0, s_{nb-1}]: nl = (span >> sh) + 1
     // <= ~4 nb cells (device locate above); 15-bit entries + the slow flag
@@ -750,6 +801,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.lut_b0 = b0;
     E.lut_sh = sh;
     E.n_slow = n_slow;
+    E.sai_i0 = sai_i0;
     E.lut16 = (const uint16_t *)g->d_esai_lut;
     E.sb = (const float *)g->d_esai_sb;
     E.stab = (const float *)g->d_esai_stab;

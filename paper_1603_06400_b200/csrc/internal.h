@@ -48,6 +48,10 @@ struct Params {
     float ts_c0;
     // fp64 guard path (exact oracle op order, reading R8)
     double m0x, m0y, mask_pitch64;
+    double det_z64;
+    // scatter-angle interpolation (reading R22): sai_n > 0
+    int sai_n;
+    double sai_tmin, sai_h;
     // device tables
     const VoxelRec *vox;
     const double *vy64, *vz64, *vt64;  // voxel y, z, t in fp64
@@ -64,6 +68,7 @@ struct Esai {
     int nl;             // lookup cells over the fp32 bit patterns of [s_0, s_{nb-1}]
     int max_win;        // max per-voxel breakpoint window (backward histogram size)
     int n_slow;         // LUT cells flagged kLutSlow (diagnostic)
+    int sai_i0;         // SAI: tabulated-angle index of the first cell (cell b <-> angle sai_i0 + b)
     int lut_b0, lut_sh; // cell c = (float_as_int(sigma) - lut_b0) >> lut_sh
     const float *sb;    // breakpoints s_b (fp32, strictly increasing), kLocD +inf pads
     const uint16_t *lut16;  // per cell: b at the cell start | kLutSlow if > kLocD breakpoints inside

@@ -55,8 +55,11 @@ __device__ __forceinline__ bool mask_open(const Params &p, int v, int q, const V
     return near ? mask_exact(p, v, q) : o;
 }
 
-// P (without C_E) and sin(theta/2) of one pair.
-__device__ __forceinline__ void pair_geom(const Params &p, const VoxelRec &vr, float2 d, float &P, float &sh) {
+// P (without C_E) and sin(theta/2) of one pair.  angular = false (scatter-angle
+// interpolation): P = G_so G_od dtheta only -- the spectral-angular factor
+// (1 + cos^2 theta) cos(theta/2) then lives in the tabulated rows.
+__device__ __forceinline__ void pair_geom(const Params &p, const VoxelRec &vr, float2 d, float &P, float &sh,
+                                          bool angular = true) {
     const float sx = d.x, sy = d.y - vr.y, sz = vr.sz;
     const float syz2 = fmaf(sy, sy, sz * sz);
     const float s2 = fmaf(sx, sx, syz2);
@@ -74,7 +77,19 @@ __device__ __forceinline__ void pair_geom(const Params &p, const VoxelRec &vr, f
     // atan(x) = x (1 - x^2/3) to ~x^4/5 and 1/(s2 - p^2/4) = rs2 (1 + p^2/4 rs2)
     const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
     const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
-    P = vr.gso * god * dth * fmaf(cos_t, cos_t, 1.0f) * ch;
+    P = angular ? vr.gso * god * dth * fmaf(cos_t, cos_t, 1.0f) * ch : vr.gso * god * dth;
+}
+
+// Scatter angle of a pair in fp64 from the fp64 centre tables, the plain
+// definition atan2(|r x s|, r . s) (the oracle's formula), for
+// decisions that must not depend on fp32 rounding (SAI cell boundaries).
+__device__ __forceinline__ double theta64(const Params &p, int v, int q) {
+    const double y = p.vy64[v], z = p.vz64[v];
+    const double sx = p.dx64[q], sy = __dsub_rn(p.dy64[q], y), sz = __dsub_rn(p.det_z64, z);
+    const double c0 = __dsub_rn(__dmul_rn(y, sz), __dmul_rn(z, sy));
+    const double c1 = __dmul_rn(z, sx), c2 = -__dmul_rn(y, sx);
+    const double cr = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(c0, c0), __dmul_rn(c1, c1)), __dmul_rn(c2, c2)));
+    return atan2(cr, __dadd_rn(__dmul_rn(y, sy), __dmul_rn(z, sz)));
 }
 
 // Energies whose u_k = alpha_k sh - q_min/dq can fall inside (-1, nq): a

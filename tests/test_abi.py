@@ -68,6 +68,10 @@ def _create(d):
     dict(q_max=0.01), dict(scale=0.0), dict(energy_resolving=2),
     dict(energy_kev=np.array([30, 40, 40, 50, 60, 70, 80, 90.0])),
     dict(phi=-np.ones(8)), dict(y_min=9.0),
+    dict(sai_n_theta=-1), dict(sai_n_theta=250, sai_theta_min=0.5, sai_theta_max=0.1),
+    dict(sai_n_theta=250, sai_theta_min=0.0, sai_theta_max=4.0),
+    dict(sai_n_theta=250, sai_theta_min=-0.1, sai_theta_max=0.5),
+    dict(sai_n_theta=250, sai_theta_min=0.01, sai_theta_max=0.5, energy_resolving=1),
 ])
 def test_invalid_descriptors_rejected(over):
     assert _create(_desc(**over)) == binding.CACSI_ERR_INVALID

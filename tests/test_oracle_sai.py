@@ -83,8 +83,9 @@ def test_sai_error_decreases_with_n_theta():
     """NRMSE (RMSE over the RMS of the exact result) of the SAI
     forward (on the phantom) and backward (on noiseless data, as Table I)
     decreases monotonically in N_theta (SPEC.md:614 AC3), roughly as 1/N for
-    nearest-neighbour sampling, and the backward error is below the forward
-    one (Table I: 0.67 % vs 6.20 %)."""
+    nearest-neighbour sampling.  On this config the backward error is also
+    below the forward one, as in Table I (0.67 % vs 6.20 %, PAPER.md:449);
+    that ordering is data-dependent (not so on config 1)."""
     cfg = make_config(0)
     O = oracle.Geometry(cfg)
     f = cfg.f.astype(np.float64)

@@ -90,6 +90,7 @@ class Config:
                 "det_nx", "det_ny", "det_z", "det_pitch", "det_cx", "det_cy",
                 "energy_resolving", "scale"]
         d = {k: getattr(self, k) for k in keys}
+        d.update(sai_n_theta=0, sai_theta_min=0.0, sai_theta_max=0.0)  # exact operator (no SAI)
         d["energy_kev"] = self.energy_kev
         d["phi"] = self.phi
         d["mask"] = self.mask
