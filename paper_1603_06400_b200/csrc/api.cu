@@ -76,7 +76,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_tb, g->d_er_ptot};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -263,15 +263,6 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     // ESAI tables for the energy-integrating operators (CACSI_ALGO=direct keeps
     // the per-term kernels, used as a cross-check in the tests)
     const char *algo = getenv("CACSI_ALGO");
-    if (d->energy_resolving && !(algo && strcmp(algo, "direct") == 0)) {
-        e = cacsi::er_build(g, d);
-        if (e != cudaSuccess) {
-            free_all(g);
-            free(g);
-            cudaGetLastError();
-            return map_err(e);
-        }
-    }
     if (d->sai_n_theta > 0 && algo && strcmp(algo, "direct") == 0) {  // SAI lives in the ESAI tables
         free_all(g);
         free(g);

@@ -884,45 +884,6 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     return cudaSuccess;
 }
 
-// Tables of the energy-resolving kernels (er.cu): transmission bits in the
-// tiled layout, per-voxel sum_pixels |P|, max c_k and the fixed-point split.
-cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
-    const Params &p = g->p;
-    float *dmin = nullptr, *dmax = nullptr, *dpt = nullptr;
-    cudaError_t e = cudaMalloc(&dmin, p.n_vox * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&dmax, p.n_vox * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&dpt, p.n_vox * sizeof(float));
-    if (e == cudaSuccess) {
-        k_pair_stats<<<p.n_vox, 256>>>(p, dmin, dmax, dpt);
-        e = cudaGetLastError();
-    }
-    cudaFree(dmin);
-    cudaFree(dmax);
-    if (e != cudaSuccess) {
-        cudaFree(dpt);
-        return e;
-    }
-    g->d_er_ptot = dpt;
-    const size_t ntb = (size_t)((p.n_vox + 31) / 32) * p.n_det;
-    e = cudaMalloc(&g->d_er_tb, ntb * sizeof(uint32_t));
-    if (e != cudaSuccess) return e;
-    k_tbits_fwd_tiled<<<8 * sm_count(g->device), 256>>>(p, (uint32_t *)g->d_er_tb);
-    e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return e;
-    double cmax = 0.0;
-    for (int k = 0; k < d->ne; k++) cmax = std::max(cmax, d->scale * d->phi[k] * d->energy_kev[k]);
-    int lb = 31;
-    const double deposits = (double)p.n_det * p.ne + 1.0;  // per bin
-    while (lb > 0 && deposits * std::ldexp(1.0, lb) >= 4294967296.0) lb--;
-    Er &R = g->er;
-    R.tb = (const uint32_t *)g->d_er_tb;
-    R.ptot = (const float *)g->d_er_ptot;
-    R.cmax = (float)cmax * 1.000001f;
-    R.lo_bits = std::min(lb, 20);
-    R.enabled = 1;
-    return cudaSuccess;
-}
-
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
                                      float *out, cudaStream_t s, int *launches);
 

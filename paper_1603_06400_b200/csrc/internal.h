@@ -85,15 +85,6 @@ struct Esai {
     const uint32_t *tb_bwd;  // backward: [voxel][ceil(n_det/32)], bit i of word j = pixel 32 j + i
 };
 
-// energy-resolving handles (er.cu)
-struct Er {
-    int enabled;
-    const uint32_t *tb;  // transmission bits, word (c, pix): bit i = T(voxel 32c + i, pix)
-    const float *ptot;   // per voxel sum_pixels |P| (fixed-point bound)
-    float cmax;          // max_k c_k
-    int lo_bits;         // fixed-point split of the backward deposits
-};
-
 }  // namespace cacsi
 
 struct cacsi_geometry {
@@ -108,8 +99,6 @@ struct cacsi_geometry {
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
         *d_esai_vbound;
-    cacsi::Er er;
-    void *d_er_tb, *d_er_ptot;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;
@@ -161,9 +150,6 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                                  cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
-cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
-cudaError_t er_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
-cudaError_t er_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
 cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 

@@ -22,6 +22,7 @@ namespace {
 
 constexpr int FWD_T = 128;  // pixels per CTA
 constexpr int FWD_VC = 16;  // voxels per shared-memory chunk
+constexpr int FWD_KU = 8;   // energies per iteration of the resolving forward (ILP)
 constexpr int BWD_T = 128;  // threads per voxel CTA
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -31,18 +32,19 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
                                                    void *__restrict__ partial) {
     extern __shared__ float4 smem4[];
     const int Q = p.nq, K = p.ne, Q3 = Q + 3;
-    float2 *en = (float2 *)smem4;          // [K] (alpha_k, c_k)
-    float2 *tab = en + ((K + 1) & ~1);     // [VC][Q + 3] (mid, slope), entry n at index n + 2
-    float *acc_s = (float *)(tab + FWD_VC * Q3 + (FWD_VC * Q3 & 1));  // RES: [K][FWD_T]
+    const int K4 = (K + FWD_KU - 1) / FWD_KU * FWD_KU;
+    float2 *en = (float2 *)smem4;          // [K4] (alpha_k, c_k), padded with copies of the last energy
+    float2 *tab = en + K4;                 // [VC][Q + 3] (mid, slope), entry n at index n + 2
+    float *acc_s = (float *)(tab + FWD_VC * Q3 + (FWD_VC * Q3 & 1));  // RES: [K4][FWD_T]
     const int tid = threadIdx.x;
     const int pix = blockIdx.x * FWD_T + tid;
     const bool valid = pix < p.n_det;
     const float2 d = p.det[valid ? pix : 0];
     const int v0 = blockIdx.y * vox_per_split;
     const int v1 = min(p.n_vox, v0 + vox_per_split);
-    for (int k = tid; k < K; k += FWD_T) en[k] = p.energy[k];
+    for (int k = tid; k < K4; k += FWD_T) en[k] = p.energy[min(k, K - 1)];
     if (RES)
-        for (int k = 0; k < K; k++) acc_s[k * FWD_T + tid] = 0.0f;
+        for (int k = 0; k < K4; k++) acc_s[k * FWD_T + tid] = 0.0f;
     double tot = 0.0;
     for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
         const int nc = min(FWD_VC, v1 - c0);
@@ -80,12 +82,25 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
                 }
                 csum = fmaf(P, ap, csum);
             } else {
-                for (int k = wlo; k <= whi; k++) {
-                    float tt;
-                    const int n = hat_coord(p, en[k].x, sh, tt);
-                    const float2 t = tv[n];
-                    float *a = acc_s + k * FWD_T + tid;
-                    *a = fmaf(P, fmaf(tt, t.y, t.x), *a);
+                // FWD_KU energies per iteration: their accumulator and table loads
+                // are independent (no read-after-write through shared memory
+                // between them), so their latencies overlap; the accumulator
+                // rows are padded to a multiple of FWD_KU (acc_s has K4 rows)
+                for (int k = wlo; k <= whi; k += FWD_KU) {
+                    float tt[FWD_KU], a[FWD_KU];
+                    float2 t[FWD_KU];
+#pragma unroll
+                    for (int j = 0; j < FWD_KU; j++) {
+                        const int n = hat_coord(p, en[k + j].x, sh, tt[j]);
+                        t[j] = tv[n];
+                        a[j] = acc_s[(k + j) * FWD_T + tid];
+                    }
+#pragma unroll
+                    for (int j = 0; j < FWD_KU; j++) {
+                        // energies past the window end: P is applied only inside it
+                        const float Pj = (k + j <= whi) ? P : 0.0f;
+                        acc_s[(k + j) * FWD_T + tid] = fmaf(Pj, fmaf(tt[j], t[j].y, t[j].x), a[j]);
+                    }
                 }
             }
         }
@@ -214,7 +229,6 @@ int num_sms(int device) {
 
 cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
     if (g->esai.enabled) return esai_forward(g, f, out, s, launches);
-    if (g->er.enabled) return er_forward(g, f, out, s, launches);
     const Params &p = g->p;
     const bool res = p.energy_resolving != 0;
     const int tiles = (p.n_det + FWD_T - 1) / FWD_T;
@@ -228,8 +242,9 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     S = (p.n_vox + vps - 1) / vps;
     const size_t n_out = (size_t)p.n_det * (res ? p.ne : 1);
     const size_t part_bytes = (size_t)S * n_out * (res ? sizeof(float) : sizeof(double));
-    size_t smem = (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2);
-    if (res) smem += (size_t)p.ne * FWD_T * sizeof(float);
+    const size_t K4 = (size_t)(p.ne + FWD_KU - 1) / FWD_KU * FWD_KU;
+    size_t smem = K4 * sizeof(float2) + (size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2);
+    if (res) smem += K4 * FWD_T * sizeof(float);
     void *part = nullptr;
     cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
     if (e != cudaSuccess) return e;
@@ -269,7 +284,6 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
 
 cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
     if (g->esai.enabled) return esai_backward(g, w, b, s, launches);
-    if (g->er.enabled) return er_backward(g, w, b, s, launches);
     const Params &p = g->p;
     const size_t smem =
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
