@@ -258,6 +258,8 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
             !getenv("CACSI_NO_TS") && d->sai_n_theta == 0) {  // SAI runs the tiled forward
             p.ts_rho = (int)rho;
             p.ts_c0 = (float)(det_centre(d->det_cy, d->det_ny, d->det_pitch, 0) - centre(d->y_min, d->y_max, d->ny, 0));
+            p.vy0 = (float)centre(d->y_min, d->y_max, d->ny, 0);
+            p.vy_step = (float)dyv;
         }
     }
     // ESAI tables for the energy-integrating operators (CACSI_ALGO=direct keeps

@@ -150,6 +150,11 @@ __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
 constexpr int kLocD = 3;
 constexpr unsigned kLutSlow = 0x8000u;
 
+// (float)i for |i| < 2^22 without I2F (an XU instruction): integer add + FADD
+__device__ __forceinline__ float exact_float(int i) {
+    return __int_as_float(i + 0x4B400000) - 12582912.0f;
+}
+
 // Pop one set bit (the highest of the low word, else of the high word) of a
 // 64-voxel transmission batch: 32-bit FLO + SEL instead of 64-bit ffs.
 __device__ __forceinline__ int pop_bit(uint32_t &lo, uint32_t &hi) {
@@ -304,11 +309,10 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
     const int nfoot = TS_T + rho * (ny - 1);
     float *sb = (float *)smem;
     uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
-    float4 *vp = (float4 *)(smem + bp_smem_bytes(e));  // [ny] (r^_y, r^_z, G_so, -)
-    float4 *foot_all = vp + ny;                        // [TS_R][nfoot] (1/|s|, G_od dtheta, s_y, -)
+    float2 *foot_all = (float2 *)(smem + bp_smem_bytes(e));  // [TS_R][nfoot] (1/|s|, G_od dtheta)
     load_bp(e, sb, lut);
     const int r = threadIdx.x / TS_T, tid = threadIdx.x % TS_T;
-    float4 *foot = foot_all + r * nfoot;
+    float2 *foot = foot_all + r * nfoot;
     const int segs = (p.det_ny + TS_T - 1) / TS_T;
     const int nyb = (ny + 31) / 32;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -334,13 +338,15 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
                     const float rs2 = rs * rs;
                     const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
                     const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
-                    foot[i] = make_float4(rs, sz * rs * rs2 * dth, sy, 0.0f);
+                    foot[i] = make_float2(rs, sz * rs * rs2 * dth);
                 }
-            for (int iy = threadIdx.x; iy < ny; iy += TS_T * TS_R) {
-                const VoxelRec rr = p.vox[iy * nz + iz];
-                vp[iy] = make_float4(rr.ry, rr.rz, rr.gso, 0.0f);
-            }
             __syncthreads();
+            // source-side quantities of voxel (iy, iz) are evaluated per pair
+            // (y = y_0 + iy dy, r^ = r / |r|, G_so = z / |r|^3) and s_y from the
+            // integer offset jy - rho iy (the footprint's own expression): the
+            // pair reads only an 8-byte footprint entry from shared memory
+            // (the L1/LSU data pipe is these kernels' bound)
+            const float zr = p.vox[iz].z, z2 = zr * zr;
             // W row of voxel (iy, iz) = Wz + iy * wstride (32-bit offsets: n_vox * ldw < 2^32, esai_build)
             const float *Wz = W + (size_t)iz * e.ldw;
             const unsigned wstride = (unsigned)nz * (unsigned)e.ldw;
@@ -367,14 +373,18 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
                         const int iy = iyb + (u ? k2 : k1);
-                        const float4 v = vp[iy];
-                        const float4 f = foot[tid + rho * (ny - 1 - iy)];
-                        const float cos_t = fmaf(v.x, f.z, v.y * sz) * f.x;
-                        const float e1 = fmaf(v.x, p.det_z, -v.y * dd.y);
+                        const float2 f = foot[tid + rho * (ny - 1 - iy)];
+                        const float fiy = exact_float(iy);
+                        const float sy = fmaf(p.pitch_d, exact_float(jy - rho * iy), p.ts_c0);
+                        const float yr = fmaf(fiy, p.vy_step, p.vy0);
+                        const float ir = rsqrtf(fmaf(yr, yr, z2));
+                        const float ry = yr * ir, rz = zr * ir;
+                        const float cos_t = fmaf(ry, sy, rz * sz) * f.x;
+                        const float e1 = fmaf(ry, p.det_z, -rz * dd.y);
                         const float sin_t = fast_sqrt(fmaf(e1, e1, sx * sx)) * f.x;
                         const float h = fmaf(0.5f, cos_t, 0.5f);
                         const float rh = rsqrtf(h);
-                        Pp[u] = v.z * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);
+                        Pp[u] = rz * ir * ir * f.y * fmaf(cos_t, cos_t, 1.0f) * (h * rh);  // G_so = z/|r|^3
                         sh[u] = 0.5f * sin_t * rh;
                     }
                     float t1, t2;
@@ -854,8 +864,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     // shared-memory budgets of the pair kernels (227 KB per CTA); beyond them the
     // per-term kernels serve the handle
     {
-        const size_t fwd = p.ts_rho > 0 ? host_bp_bytes(E) + (size_t)p.ny * 16 +
-                                              (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * 16
+        const size_t fwd = p.ts_rho > 0 ? host_bp_bytes(E) + (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * 8
                                         : host_bp_bytes(E);
         const size_t bwd = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         if (fwd > 227 * 1024 || bwd > 227 * 1024) {
@@ -954,7 +963,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     } else if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
         const int n_groups = ((p.det_nx + TS_R - 1) / TS_R) * segs;
-        const size_t smem = bpb + (size_t)p.ny * sizeof(float4) + (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * sizeof(float4);
+        const size_t smem = bpb + (size_t)TS_R * (TS_T + p.ts_rho * (p.ny - 1)) * sizeof(float2);
         const int grid = persistent_grid(g, smem, TS_T * TS_R);
         int izc = std::max(1, (p.nz * n_groups) / (4 * grid));  // >= ~4 items per CTA
         izc = std::min(izc, p.nz);

@@ -46,6 +46,7 @@ struct Params {
     // => y_d(jy) - y_r(iy) = ts_c0 + pitch_d * (jy - ts_rho * iy); 0 = not applicable
     int ts_rho;
     float ts_c0;
+    float vy0, vy_step;                // voxel centre y = vy0 + iy * vy_step (fp32, the TS forward's r^)
     // fp64 guard path (exact oracle op order, reading R8)
     double m0x, m0y, mask_pitch64;
     double det_z64;
