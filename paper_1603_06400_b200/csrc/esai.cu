@@ -210,10 +210,11 @@ __device__ __forceinline__ int sai_cell(const Params &p, const Esai &e, const fl
 
 // locate for a pair (v, q): exact ESAI (tau = position in the breakpoint
 // interval) or SAI (tau = 0 in the nearest-angle cell)
+template <bool SAI>
 __device__ __forceinline__ int locate_pair(const Params &p, const Esai &e, const float *sb, const uint16_t *lut,
                                            float s, int v, int q, float &tau) {
     int b = locate(e, sb, lut, s, tau);
-    if (p.sai_n > 0) {
+    if (SAI) {
         b = sai_cell(p, e, sb, s, b, v, q);
         tau = 0.0f;
     }
@@ -232,7 +233,8 @@ constexpr int PF_CH = 32;                                     // voxels per tran
 // g_partial[split][pix] = sum_{v in split} P [(1-tau) W[v,b] + tau W[v,b+1]].
 // The transmission bits of 32 voxels come in one word; lanes iterate only
 // over their open voxels, two pairs per iteration.
-__global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e, const float *__restrict__ W,
+template <bool SAI>
+__global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e, const float2 *__restrict__ W,
                                                    int vox_per_split, int n_tiles, int n_items,
                                                    double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -264,19 +266,19 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
                 const int i2 = two ? __ffs(bits) - 1 : i1;
                 bits &= bits - 1;
                 float P1, s1, P2, s2, t1, t2;
-                pair_geom(p, p.vox[c0 + i1], d, P1, s1, p.sai_n == 0);
-                pair_geom(p, p.vox[c0 + i2], d, P2, s2, p.sai_n == 0);
-                const int b1 = locate_pair(p, e, sb, lut, s1, c0 + i1, pix, t1);
-                const int b2 = locate_pair(p, e, sb, lut, s2, c0 + i2, pix, t2);
+                pair_geom(p, p.vox[c0 + i1], d, P1, s1, !SAI);
+                pair_geom(p, p.vox[c0 + i2], d, P2, s2, !SAI);
+                const int b1 = locate_pair<SAI>(p, e, sb, lut, s1, c0 + i1, pix, t1);
+                const int b2 = locate_pair<SAI>(p, e, sb, lut, s2, c0 + i2, pix, t2);
                 // consume the previous couple first, then load into the same registers
                 acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
                 acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
-                const float *r1 = W + (size_t)(c0 + i1) * e.ldw + b1;
-                const float *r2 = W + (size_t)(c0 + i2) * e.ldw + b2;
-                qa1 = __ldg(r1);
-                qb1 = __ldg(r1 + 1);
-                qa2 = __ldg(r2);
-                qb2 = __ldg(r2 + 1);
+                const float2 w1 = __ldg(W + (size_t)(c0 + i1) * e.ldw + b1);  // (W_b, W_{b+1})
+                const float2 w2 = __ldg(W + (size_t)(c0 + i2) * e.ldw + b2);
+                qa1 = w1.x;
+                qb1 = w1.y;
+                qa2 = w2.x;
+                qb2 = w2.y;
                 qP1 = P1;
                 qP2 = two ? P2 : 0.0f;
                 qt1 = t1;
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(PF_T) k_esai_fwd(const Params p, const Esai e,
 constexpr int TS_T = 128, TS_R = 4;
 
 __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, const Esai e,
-                                                             const float *__restrict__ W, int iz_per_chunk,
+                                                             const float2 *__restrict__ W, int iz_per_chunk,
                                                              int n_groups, int n_items, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int rho = p.ts_rho, ny = p.ny, nz = p.nz;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
             // (the L1/LSU data pipe is these kernels' bound)
             const float zr = p.vox[iz].z, z2 = zr * zr;
             // W row of voxel (iy, iz) = Wz + iy * wstride (32-bit offsets: n_vox * ldw < 2^32, esai_build)
-            const float *Wz = W + (size_t)iz * e.ldw;
+            const float2 *Wz = W + (size_t)iz * e.ldw;
             const unsigned wstride = (unsigned)nz * (unsigned)e.ldw;
             const uint32_t *tbrow = e.tb_fwd + ((size_t)(iz * p.det_nx + (valid ? ix : 0)) * nyb) * p.det_ny +
                                     (valid ? jy : 0);
@@ -393,12 +395,13 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
                     // consume the previous couple first, then load into the same registers
                     acc = fmaf(qP1, fmaf(qt1, qb1 - qa1, qa1), acc);
                     acc = fmaf(qP2, fmaf(qt2, qb2 - qa2, qa2), acc);
-                    const float *r1 = Wz + ((unsigned)(iyb + k1) * wstride + (unsigned)b1);
-                    const float *r2 = Wz + ((unsigned)(iyb + k2) * wstride + (unsigned)b2);
-                    qa1 = __ldg(r1);
-                    qb1 = __ldg(r1 + 1);
-                    qa2 = __ldg(r2);
-                    qb2 = __ldg(r2 + 1);
+                    // one 8-byte gather per pair: (W_b, W_{b+1}) (k_tc_gemm<true> pairs)
+                    const float2 w1 = __ldg(Wz + ((unsigned)(iyb + k1) * wstride + (unsigned)b1));
+                    const float2 w2 = __ldg(Wz + ((unsigned)(iyb + k2) * wstride + (unsigned)b2));
+                    qa1 = w1.x;
+                    qb1 = w1.y;
+                    qa2 = w2.x;
+                    qb2 = w2.y;
                     qP1 = Pp[0];
                     qP2 = two ? Pp[1] : 0.0f;
                     qt1 = t1;
@@ -419,7 +422,8 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
 // detector), 32 voxels per bit batch as in k_esai_fwd.
 constexpr int PL_T = 256;
 
-__global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Esai e, const float *__restrict__ W,
+template <bool SAI>
+__global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Esai e, const float2 *__restrict__ W,
                                                         const int32_t *__restrict__ list, int n, int vox_per_split,
                                                         int n_items, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -448,11 +452,10 @@ __global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Es
                 const int k = 31 - __clz(bits);
                 bits ^= 1u << k;
                 float P, sh, t;
-                pair_geom(p, p.vox[c0 + k], d, P, sh, p.sai_n == 0);
-                const int b = locate_pair(p, e, sb, lut, sh, c0 + k, pix, t);
-                const float *r = W + (size_t)(c0 + k) * e.ldw + b;
-                const float w0 = __ldg(r), w1 = __ldg(r + 1);
-                acc = fmaf(P, fmaf(t, w1 - w0, w0), acc);
+                pair_geom(p, p.vox[c0 + k], d, P, sh, !SAI);
+                const int b = locate_pair<SAI>(p, e, sb, lut, sh, c0 + k, pix, t);
+                const float2 w = __ldg(W + (size_t)(c0 + k) * e.ldw + b);
+                acc = fmaf(P, fmaf(t, w.y - w.x, w.x), acc);
             }
             tot += (double)acc;
         }
@@ -514,7 +517,7 @@ constexpr int PB_QW = 32;  // transmission words (1024 pixels) per warp chunk
 // then sweeps it with all 32 lanes: converged lanes, coalesced pixel / w loads.
 // BOUND = true: w = 1, scale from the conservative bound sum_pixels |P| (used
 // once to measure vbound).
-template <bool BOUND>
+template <bool BOUND, bool SAI>
 __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e, const float *__restrict__ w,
                                                    const float *__restrict__ wmax, const float *__restrict__ vbound,
                                                    const uint32_t *__restrict__ pmask, float *__restrict__ A) {
@@ -564,10 +567,10 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
                 const bool two = k + 32 < total;
                 const int q1 = qbase + queue[k], q2 = two ? qbase + queue[k + 32] : q1;
                 float P1, s1, P2, s2, t1, t2;
-                pair_geom(p, vr, p.det[q1], P1, s1, p.sai_n == 0);
-                pair_geom(p, vr, p.det[q2], P2, s2, p.sai_n == 0);
-                const int b1 = locate_pair(p, e, sb, lut, s1, v, q1, t1);
-                const int b2 = locate_pair(p, e, sb, lut, s2, v, q2, t2);
+                pair_geom(p, vr, p.det[q1], P1, s1, !SAI);
+                pair_geom(p, vr, p.det[q2], P2, s2, !SAI);
+                const int b1 = locate_pair<SAI>(p, e, sb, lut, s1, v, q1, t1);
+                const int b2 = locate_pair<SAI>(p, e, sb, lut, s2, v, q2, t2);
                 const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
                 const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
                 const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
@@ -823,8 +826,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.ldw = (nb + 31) / 32 * 32;
     {
         const int nkcW = (Q + TC_KC - 1) / TC_KC, nkcB = E.ldw / TC_KC;
-        std::vector<float> tW((size_t)((nb + TC_N - 1) / TC_N) * nkcW * 2 * TC_N * TC_KC);
-        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data());
+        // W2 = F S~^T as (W_b, W_{b+1}) pairs: overlapping tiles of stride 127
+        std::vector<float> tW((size_t)tc_ntiles(nb, TC_N - 1) * nkcW * 2 * TC_N * TC_KC);
+        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data(), TC_N - 1);
         std::vector<float> stT((size_t)Q * nb);
         for (int b = 0; b < nb; b++)
             for (int j = 0; j < Q; j++) stT[(size_t)j * nb + b] = stab[(size_t)b * Q + j];
@@ -880,8 +884,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e == cudaSuccess) e = cudaMalloc(&A1, (size_t)nv * E.ldw * sizeof(float));
         if (e == cudaSuccess) {
             const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
-            cudaFuncSetAttribute(k_esai_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_bwd<true><<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, nullptr, A1);
+            auto kb = sai ? k_esai_bwd<true, true> : k_esai_bwd<true, false>;
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kb<<<persistent_grid(g, smem, PB_T), PB_T, smem>>>(p, E, nullptr, nullptr, E.ptot, nullptr, A1);
             k_vbound<<<nv, 256>>>(A1, E.ldw, E.ptot, p.n_det, (float *)g->d_esai_vbound);
             e = cudaDeviceSynchronize();
         }
@@ -915,7 +920,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     int S;  // number of partial images
     float *fp = nullptr;
     const int ldf = (p.nq + TC_KC - 1) / TC_KC * TC_KC;
-    cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.ldw * sizeof(float), s);
+    cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.ldw * sizeof(float2), s);  // W2 pairs
     if (e == cudaSuccess) e = cudaMallocAsync(&fp, (size_t)p.n_vox * ldf * sizeof(float), s);
     if (e != cudaSuccess) {
         if (W) cudaFreeAsync(W, s);
@@ -929,9 +934,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
         KScope kt_(g, s, "k_tc_gemm_W");
         const int nkc = ldf / TC_KC;
-        dim3 gg((E.nb + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, 1);
-        cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-        k_tc_gemm<<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, E.nb, p.nq, ldf, nkc, nkc, fp, E.tc_w, W, E.ldw);
+        dim3 gg(tc_ntiles(E.nb, TC_N - 1), (p.n_vox + TC_M - 1) / TC_M, 1);
+        cudaFuncSetAttribute(k_tc_gemm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+        k_tc_gemm<true, 1><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkc, nkc, fp, E.tc_w, W, E.ldw);
     }
     if (pixels != nullptr) {
         // subset: g = 0 outside the list, listed pixels by k_esai_fwd_list
@@ -946,8 +951,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         if (e == cudaSuccess) {
             {
                 KScope kt_(g, s, "k_esai_fwd_list");
-                cudaFuncSetAttribute(k_esai_fwd_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bpb);
-                k_esai_fwd_list<<<grid, PL_T, bpb, s>>>(p, E, W, pixels, n_pix, vps, n_chunks * S, part);
+                auto kl = p.sai_n > 0 ? k_esai_fwd_list<true> : k_esai_fwd_list<false>;
+                cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bpb);
+                kl<<<grid, PL_T, bpb, s>>>(p, E, (const float2 *)W, pixels, n_pix, vps, n_chunks * S, part);
             }
             {
                 KScope kt_(g, s, "k_sum_list");
@@ -972,7 +978,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         if (e == cudaSuccess) {
             KScope kt_(g, s, "k_esai_fwd_ts");
             cudaFuncSetAttribute(k_esai_fwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_fwd_ts<<<grid, TS_T * TS_R, smem, s>>>(p, E, W, izc, n_groups, n_groups * S, part);
+            k_esai_fwd_ts<<<grid, TS_T * TS_R, smem, s>>>(p, E, (const float2 *)W, izc, n_groups, n_groups * S, part);
         }
     } else {
         const int n_tiles = ((p.det_nx + PF_TX - 1) / PF_TX) * ((p.det_ny + PF_TY - 1) / PF_TY);
@@ -985,8 +991,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
         if (e == cudaSuccess) {
             KScope kt_(g, s, "k_esai_fwd");
-            cudaFuncSetAttribute(k_esai_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_fwd<<<grid, PF_T, smem, s>>>(p, E, W, vps, n_tiles, n_tiles * S, part);
+            auto kf = p.sai_n > 0 ? k_esai_fwd<true> : k_esai_fwd<false>;
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kf<<<grid, PF_T, smem, s>>>(p, E, (const float2 *)W, vps, n_tiles, n_tiles * S, part);
         }
     }
     if (e == cudaSuccess) {
@@ -1026,14 +1033,15 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {
             KScope kt_(g, s, "k_esai_bwd");
-            cudaFuncSetAttribute(k_esai_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_esai_bwd<false><<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, pmask, A);
+            auto kb = p.sai_n > 0 ? k_esai_bwd<false, true> : k_esai_bwd<false, false>;
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kb<<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, pmask, A);
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
             dim3 gg((p.nq + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, S_eff);
-            cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-            k_tc_gemm<<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
+            cudaFuncSetAttribute(k_tc_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+            k_tc_gemm<false><<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
         }
         const size_t n = (size_t)p.n_vox * p.nq;
         {

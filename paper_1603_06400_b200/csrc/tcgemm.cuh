@@ -35,6 +35,7 @@ constexpr int TC_T = 128;                            // threads
 constexpr int TC_OPB = TC_M * TC_KC * 4;             // bytes of one operand half-tile (16 KB)
 constexpr int TC_STAGE = 4 * TC_OPB;                 // A_hi, A_lo, B_hi, B_lo
 constexpr int TC_SMEM = 2 * TC_STAGE + 1024 + 128;   // 2 stages + alignment + barriers
+constexpr int tc_smem(int stages) { return stages * TC_STAGE + 1024 + 128; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -108,16 +109,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
 
 // C[z] (rows < M, columns < N) = A * B^T over k-chunks [z * cps, min(nkc, (z+1) * cps)).
 //   A: [M][lda] fp32, lda % 4 == 0, columns >= nkc * 32 read as zero beyond K
-//   Bt: pre-split tiles [ceil(N/128)][nkc][2][128 x 32] (see tc_pack_b)
+//   Bt: pre-split tiles [ntiles][nkc][2][128 x 32] (see tc_pack_b)
+// PAIRS: tiles overlap by one column (tile nt covers B rows 127 nt .. 127 nt + 127,
+// tc_pack_b with stride 127) and the epilogue writes C as float2 pairs
+// (C[m][n], C[m][n + 1]) for n < N - 1, so a consumer interpolating between
+// neighbouring columns gathers one 8-byte entry (ldc in float2 units).
+// STAGES = 2: chunk c+1's loads overlap chunk c's MMAs (long K); STAGES = 1:
+// half the shared memory, so two CTAs share an SM and one CTA's epilogue
+// overlaps the other's loads and MMAs (short K, store-heavy epilogue).
+template <bool PAIRS, int STAGES = 2>
 __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, int nkc, int cps,
                                                   const float *__restrict__ A, const float *__restrict__ Bt,
                                                   float *__restrict__ C, int ldc) {
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *bars = (uint64_t *)(base + 2 * TC_STAGE);  // [0,1] B landed, [2,3] MMAs of stage done
+    uint64_t *bars = (uint64_t *)(base + STAGES * TC_STAGE);  // [0, S) B landed, [S, 2S) MMAs of stage done
     uint32_t *tmem_slot = (uint32_t *)(bars + 4);
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int m0 = blockIdx.y * TC_M, nt = blockIdx.x, n0 = nt * TC_N;
+    const int m0 = blockIdx.y * TC_M, nt = blockIdx.x, n0 = nt * (PAIRS ? TC_N - 1 : TC_N);
     const int kc0 = blockIdx.z * cps, kc1 = min(nkc, kc0 + cps);
 
     if (warp == 0) {
@@ -126,7 +135,8 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
-        for (int i = 0; i < 4; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bars + i)));
+        for (int i = 0; i < 2 * STAGES; i++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bars + i)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -138,10 +148,10 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     const float *arow = A + (size_t)(gm < M ? gm : 0) * lda;
 
     for (int c = kc0; c < kc1; c++) {
-        const int it = c - kc0, st = it & 1;
+        const int it = c - kc0, st = it % STAGES, use = it / STAGES;
         unsigned char *sA_hi = base + st * TC_STAGE, *sA_lo = sA_hi + TC_OPB, *sB = sA_hi + 2 * TC_OPB;
-        // the MMAs that last read this stage (iteration it - 2) must be done
-        if (it >= 2) mbar_wait(smem_u32(bars + 2 + st), ((it >> 1) - 1) & 1);
+        // the MMAs that last read this stage (iteration it - STAGES) must be done
+        if (it >= STAGES) mbar_wait(smem_u32(bars + STAGES + st), (use - 1) & 1);
         if (tid == 0) {
             const uint32_t mb = smem_u32(bars + st);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(2 * TC_OPB));
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
         asm volatile("fence.proxy.async.shared::cta;\n");
         __syncthreads();
         if (tid == 0) {
-            mbar_wait(smem_u32(bars + st), (it >> 1) & 1);  // B tile landed
+            mbar_wait(smem_u32(bars + st), use & 1);  // B tile landed
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const uint32_t ah0 = smem_u32(sA_hi), al0 = smem_u32(sA_lo);
             const uint32_t bh0 = smem_u32(sB), bl0 = smem_u32(sB + TC_OPB);
@@ -178,37 +188,78 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
                 tc_mma(tmem + TC_N, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(bars + 2 + st)));
+                smem_u32(bars + STAGES + st)));
         }
     }
     // all MMAs done (the last commit covers every earlier MMA of this thread)
     const int nit = kc1 - kc0;
-    if (nit > 0) mbar_wait(smem_u32(bars + 2 + ((nit - 1) & 1)), ((nit - 1) >> 1) & 1);
+    if (nit > 0) mbar_wait(smem_u32(bars + STAGES + (nit - 1) % STAGES), ((nit - 1) / STAGES) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;\n");
 
     // ---- epilogue: TMEM -> registers -> global (warp w reads lanes 32w..32w+31)
-    float *Cz = C + (size_t)blockIdx.z * M * ldc;
     const int orow = m0 + warp * 32 + (tid & 31);
+    if (!PAIRS) {
+        float *Cz = C + (size_t)blockIdx.z * M * ldc;
 #pragma unroll 1
-    for (int c0 = 0; c0 < TC_N; c0 += 32) {
-        uint32_t r[32], x[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-        tmem_ld32(taddr, r);
-        tmem_ld32(taddr + TC_N, x);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-        float v[32];
+        for (int c0 = 0; c0 < TC_N; c0 += 32) {
+            uint32_t r[32], x[32];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+            tmem_ld32(taddr, r);
+            tmem_ld32(taddr + TC_N, x);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+            float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; j++) v[j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
-        if (orow < M) {
-            float *cr = Cz + (size_t)orow * ldc + n0 + c0;
-            if (n0 + c0 + 32 <= N && (ldc & 3) == 0) {
+            for (int j = 0; j < 32; j++) v[j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
+            if (orow < M) {
+                float *cr = Cz + (size_t)orow * ldc + n0 + c0;
+                if (n0 + c0 + 32 <= N && (ldc & 3) == 0) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 4) *(float4 *)(cr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
+                    for (int j = 0; j < 32; j += 4) *(float4 *)(cr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 32; j++)
-                    if (n0 + c0 + j < N) cr[j] = v[j];
+                    for (int j = 0; j < 32; j++)
+                        if (n0 + c0 + j < N) cr[j] = v[j];
+                }
             }
+        }
+    } else {
+        // pairs (v[c], v[c + 1]) for tile columns c = 0 .. 126.  Each warp
+        // transposes its 32 rows x 32 columns through a [32][33] shared buffer
+        // (conflict-free both ways; column 32 = the next chunk's first column)
+        // so every store writes 32 consecutive pairs of ONE row (coalesced).
+        // The operand stages are free: every MMA has completed (waited above).
+        float2 *Cz = (float2 *)C + (size_t)blockIdx.z * M * ldc;
+        float *buf = (float *)base + warp * (32 * 33);
+        const int lane = tid & 31;
+        float cur[32], nxt[32];
+        auto load = [&](int c0, float (&v)[32]) {
+            uint32_t r[32], x[32];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+            tmem_ld32(taddr, r);
+            tmem_ld32(taddr + TC_N, x);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int j = 0; j < 32; j++) v[j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
+        };
+        load(0, cur);
+#pragma unroll 1
+        for (int c0 = 0; c0 < TC_N; c0 += 32) {
+            if (c0 + 32 < TC_N) load(c0 + 32, nxt);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 32; j++) buf[lane * 33 + j] = cur[j];
+            buf[lane * 33 + 32] = c0 + 32 < TC_N ? nxt[0] : 0.0f;
+            __syncwarp();
+            const int n = n0 + c0 + lane;
+            const bool ok = c0 + lane + 1 < TC_N && n + 1 < N;
+#pragma unroll 4
+            for (int rr = 0; rr < 32; rr++) {
+                const int grow = m0 + warp * 32 + rr;
+                if (ok && grow < M)
+                    Cz[(size_t)grow * ldc + n] = make_float2(buf[rr * 33 + lane], buf[rr * 33 + lane + 1]);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j++) cur[j] = nxt[j];
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -218,14 +269,18 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
 
 // Host: pack B (N x K, row-major, ldb) into pre-split swizzled tiles
 // [ceil(N/128)][nkc][hi, lo][128 x 32].  out must hold ntiles * nkc * 8192 floats.
-inline void tc_pack_b(const float *B, int N, int K, int ldb, int nkc, float *out) {
-    const int ntiles = (N + TC_N - 1) / TC_N;
+// stride = TC_N (disjoint tiles) or TC_N - 1 (overlapping tiles of k_tc_gemm<true>);
+// ntiles = ceil(N / 128) resp. ceil((N - 1) / 127).
+inline int tc_ntiles(int N, int stride) { return stride == TC_N ? (N + TC_N - 1) / TC_N : (N - 1 + stride - 1) / stride; }
+
+inline void tc_pack_b(const float *B, int N, int K, int ldb, int nkc, float *out, int stride = TC_N) {
+    const int ntiles = tc_ntiles(N, stride);
     for (int nt = 0; nt < ntiles; nt++)
         for (int c = 0; c < nkc; c++) {
             unsigned char *tile = (unsigned char *)(out + ((size_t)nt * nkc + c) * (2 * TC_N * TC_KC));
             for (int r = 0; r < TC_N; r++)
                 for (int k = 0; k < TC_KC; k++) {
-                    const int n = nt * TC_N + r, kk = c * TC_KC + k;
+                    const int n = nt * stride + r, kk = c * TC_KC + k;
                     const float x = (n < N && kk < K) ? B[(size_t)n * ldb + kk] : 0.0f;
                     const float h = tf32_hi(x);
                     *(float *)(tile + tc_swz(r, k)) = h;
