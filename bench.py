@@ -321,9 +321,11 @@ def alg_flops(kernel, cfg, counts, nb):
     table = {
         "k_tc_gemm_W": gemm,                           # W = F S~^T (tensor cores, 3xTF32: 3 MMAs per product)
         "k_tc_gemm_b2": gemm,                          # b2 = A S~
-        "k_esai_fwd": 10 * pairs + (46 + 11) * open_,  # mask, pair geometry, locate + lerp + accumulate
-        "k_esai_fwd_ts": 5 * pairs + (23 + 11) * open_,  # TS: footprint shared, x-mask uniform
-        "k_esai_bwd": 10 * pairs + (46 + 6 + 12) * open_,  # mask, geometry, locate, fixed-point deposits
+        "k_esai_fwd": 2 * pairs + (46 + 11) * open_,   # bit pop, pair geometry, locate + lerp + accumulate
+        # TS: footprint shared; per open pair the source-side terms (r^, G_so: 9), the r^-dependent
+        # geometry (23), locate (6) and lerp + accumulate (4)
+        "k_esai_fwd_ts": 2 * pairs + (9 + 23 + 10) * open_,
+        "k_esai_bwd": 2 * pairs + (46 + 6 + 6) * open_,  # compaction, geometry, locate, fixed-point deposits
         "k_forward": 10 * pairs + 46 * open_ + 7 * counts["effective_terms"],
         "k_backward": 10 * pairs + 46 * open_ + 9 * counts["effective_terms"],
     }
