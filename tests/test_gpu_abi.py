@@ -1,0 +1,134 @@
+"""GPU-side ABI behaviour: error codes of the §8(f) entry points, empty and
+degenerate subsets, determinism, host/device agreement and concurrent calls
+on one handle from two streams (include/cacsi.h conventions)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import make_config
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_1603_06400_b200")
+
+from test_gpu_parity import assert_parity, cuda, gpu_backward, gpu_forward, rnd  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+B = P.binding
+
+
+def _status(fn):
+    try:
+        fn()
+    except P.CacsiError as e:
+        return e.status
+    return B.CACSI_OK
+
+
+def test_subset_argument_errors():
+    cfg = make_config(0)
+    G = P.Geometry(cfg.desc())
+    f = cuda(cfg.f)
+    g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+    too_many = torch.arange(cfg.n_det + 1, dtype=torch.int32, device="cuda")
+    assert _status(lambda: G.forward_subset(f, too_many, g)) == B.CACSI_ERR_INVALID
+    # NULL pixel list with a positive count
+    st = B.lib().cacsi_forward_subset(G.handle, f.data_ptr(), None, 3, g.data_ptr(), None)
+    assert st == B.CACSI_ERR_NULL
+    # empty subset: zero output
+    g.fill_(7.0)
+    G.forward_subset(f, torch.empty(0, dtype=torch.int32, device="cuda"), g)
+    b = torch.full(G.f_shape, 7.0, dtype=torch.float32, device="cuda")
+    G.backward_subset(cuda(np.ones(G.g_shape)), torch.empty(0, dtype=torch.int32, device="cuda"), b)
+    torch.cuda.synchronize()
+    assert not g.any() and not b.any()
+    G.close()
+
+
+def test_osem_argument_errors():
+    cfg = make_config(0)
+    G = P.Geometry(cfg.desc())
+    f = cuda(np.ones(G.f_shape))
+    y = cuda(np.ones(G.g_shape))
+    ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
+    pix = torch.arange(cfg.n_det, dtype=torch.int32, device="cuda")
+    b1 = cuda(np.ones((2,) + G.f_shape))
+    for offs in ([1, 128, 256], [0, 200, 100], [0, 128, 300]):
+        assert _status(lambda: G.osem(f, y, y, b1, pix, offs, 1e-3, None, 1, ws)) == B.CACSI_ERR_INVALID
+    assert _status(lambda: G.osem(f, y, y, b1, pix, [0, 128, 256], -1.0, None, 1, ws)) == B.CACSI_ERR_INVALID
+    assert _status(lambda: G.osem(f, y, y, b1, pix, [0, 128, 256], 1e-3, ("huber", 0.0), 1, ws)) == \
+        B.CACSI_ERR_INVALID
+    G.osem(f, y, y, b1, pix, [0, 128, 256], 1e-3, None, 0, ws)  # zero iterations: ok, f untouched
+    torch.cuda.synchronize()
+    assert torch.equal(f, cuda(np.ones(G.f_shape)))
+    G.close()
+
+
+def test_subset_operators_deterministic():
+    cfg = make_config(1)
+    G = P.Geometry(cfg.desc())
+    sub = B.symmetric_subsets(cfg.det_nx, cfg.det_ny, 8, 16).ravel()
+    pix = torch.as_tensor(np.flatnonzero(sub == 5).astype(np.int32)).cuda()
+    w = cuda(rnd(G.g_shape, 1, 60))
+    b1 = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+    b2 = torch.empty_like(b1)
+    G.backward_subset(w, pix, b1)
+    G.backward_subset(w, pix, b2)
+    f = cuda(cfg.f)
+    g1 = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+    g2 = torch.empty_like(g1)
+    G.forward_subset(f, pix, g1)
+    G.forward_subset(f, pix, g2)
+    torch.cuda.synchronize()
+    assert torch.equal(b1, b2) and torch.equal(g1, g2)
+    G.close()
+
+
+def test_sai_subset_operators():
+    """Subset operators of a scatter-angle-interpolation handle against the SAI
+    oracle restricted to the subset."""
+    cfg = make_config(1)
+    d = cfg.desc()
+    d.update(sai_n_theta=250, sai_theta_min=0.2 * math.pi / 180, sai_theta_max=math.pi / 6)
+    G, O = P.Geometry(d), oracle.Geometry(d)
+    sub = B.symmetric_subsets(cfg.det_nx, cfg.det_ny, 8, 16).ravel()
+    pixn = np.flatnonzero(sub == 9).astype(np.int32)
+    pix = torch.as_tensor(pixn).cuda()
+    g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+    G.forward_subset(cuda(cfg.f), pix, g)
+    w = rnd(G.g_shape, 1, 61)
+    b = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+    G.backward_subset(cuda(w), pix, b)
+    torch.cuda.synchronize()
+    assert_parity(g.cpu().numpy().ravel()[pixn], O.forward_pixels(cfg.f, pixn), "SAI forward subset")
+    assert_parity(b.cpu().numpy(), O.backward_pixels(w, pixn), "SAI backward subset")
+    G.close()
+
+
+def test_two_streams_one_handle():
+    """Calls on one handle from two streams (internal scratch is stream-ordered,
+    include/cacsi.h) give the same results as sequential calls."""
+    cfg = make_config(1)
+    G = P.Geometry(cfg.desc())
+    f1, f2 = cuda(cfg.f), cuda(rnd(G.f_shape, 1, 62))
+    w1, w2 = cuda(rnd(G.g_shape, 1, 63)), cuda(rnd(G.g_shape, 1, 64))
+    ref = [gpu_forward(G, f1.cpu().numpy()), gpu_forward(G, f2.cpu().numpy()),
+           gpu_backward(G, w1.cpu().numpy()), gpu_backward(G, w2.cpu().numpy())]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    g1 = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
+    g2 = torch.empty_like(g1)
+    b1 = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")
+    b2 = torch.empty_like(b1)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            G.forward(f1, g1)
+            G.backward(w1, b1)
+        with torch.cuda.stream(s2):
+            G.forward(f2, g2)
+            G.backward(w2, b2)
+    torch.cuda.synchronize()
+    for got, want in zip((g1, g2, b1, b2), ref):
+        np.testing.assert_array_equal(got.cpu().numpy(), want)
+    G.close()
