@@ -1040,8 +1040,8 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
             dim3 gg((p.nq + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, S_eff);
-            cudaFuncSetAttribute(k_tc_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-            k_tc_gemm<false><<<gg, TC_T, TC_SMEM, s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
+            cudaFuncSetAttribute(k_tc_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+            k_tc_gemm<false, 1><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
         }
         const size_t n = (size_t)p.n_vox * p.nq;
         {
