@@ -615,15 +615,6 @@ __global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ A1, in
     }
 }
 
-// f [n][nq] -> fp [n][ld] (zero padded) so the GEMM can load 16-byte vectors
-__global__ void k_pad_rows(const float *__restrict__ f, int n, int nq, int ld, float *__restrict__ fp) {
-    const size_t tot = (size_t)n * ld;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
-        const int j = (int)(i % ld);
-        fp[i] = j < nq ? f[(i / ld) * nq + j] : 0.0f;
-    }
-}
-
 __global__ void k_sum_parts_f64(const double *__restrict__ part, int S, size_t n, float *__restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -826,9 +817,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.ldw = (nb + 31) / 32 * 32;
     {
         const int nkcW = (Q + TC_KC - 1) / TC_KC, nkcB = E.ldw / TC_KC;
-        // W2 = F S~^T as (W_b, W_{b+1}) pairs: overlapping tiles of stride 127
-        std::vector<float> tW((size_t)tc_ntiles(nb, TC_N - 1) * nkcW * 2 * TC_N * TC_KC);
-        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data(), TC_N - 1);
+        // W2 = F S~^T as (W_b, W_{b+1}) pairs: overlapping tiles of stride 126
+        std::vector<float> tW((size_t)tc_ntiles(nb, TC_PSTRIDE) * nkcW * 2 * TC_N * TC_KC);
+        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data(), TC_PSTRIDE);
         std::vector<float> stT((size_t)Q * nb);
         for (int b = 0; b < nb; b++)
             for (int j = 0; j < Q; j++) stT[(size_t)j * nb + b] = stab[(size_t)b * Q + j];
@@ -921,22 +912,25 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     float *fp = nullptr;
     const int ldf = (p.nq + TC_KC - 1) / TC_KC * TC_KC;
     cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.ldw * sizeof(float2), s);  // W2 pairs
-    if (e == cudaSuccess) e = cudaMallocAsync(&fp, (size_t)p.n_vox * ldf * sizeof(float), s);
+    // packed A tiles: [ceil(n_vox / 128)][ldf / 32][hi, lo][128 x 32]
+    if (e == cudaSuccess) e = cudaMallocAsync(&fp, (size_t)(p.n_vox + TC_M - 1) / TC_M * TC_M * ldf * 2 * sizeof(float), s);
     if (e != cudaSuccess) {
         if (W) cudaFreeAsync(W, s);
         return e;
     }
+    const int nkcA = ldf / TC_KC;
     {
-        KScope kt_(g, s, "k_pad_rows");
-        k_pad_rows<<<4 * sm_count(g->device), 256, 0, s>>>(f, p.n_vox, p.nq, ldf, fp);
+        // f -> pre-split (TF32 hi / lo), pre-swizzled A tiles: the GEMM lands them by bulk copy
+        KScope kt_(g, s, "k_tc_pack_a");
+        k_tc_pack_a<<<4 * sm_count(g->device), 256, 0, s>>>(f, p.n_vox, p.nq, p.nq, nkcA, fp);
     }
     {
         // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
         KScope kt_(g, s, "k_tc_gemm_W");
-        const int nkc = ldf / TC_KC;
-        dim3 gg(tc_ntiles(E.nb, TC_N - 1), (p.n_vox + TC_M - 1) / TC_M, 1);
-        cudaFuncSetAttribute(k_tc_gemm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
-        k_tc_gemm<true, 1><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkc, nkc, fp, E.tc_w, W, E.ldw);
+        dim3 gg(tc_ntiles(E.nb, TC_PSTRIDE), (p.n_vox + TC_M - 1) / TC_M, 1);
+        cudaFuncSetAttribute(k_tc_gemm<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+        k_tc_gemm<true, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp, E.tc_w, W,
+                                                             E.ldw);
     }
     if (pixels != nullptr) {
         // subset: g = 0 outside the list, listed pixels by k_esai_fwd_list

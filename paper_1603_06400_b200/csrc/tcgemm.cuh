@@ -32,6 +32,7 @@ namespace cacsi {
 
 constexpr int TC_M = 128, TC_N = 128, TC_KC = 32;   // tile and K chunk (32 fp32 = one 128-byte swizzle row)
 constexpr int TC_T = 128;                            // threads
+constexpr int TC_PSTRIDE = TC_N - 2;                 // column stride of the overlapping PAIRS tiles
 constexpr int TC_OPB = TC_M * TC_KC * 4;             // bytes of one operand half-tile (16 KB)
 constexpr int TC_STAGE = 4 * TC_OPB;                 // A_hi, A_lo, B_hi, B_lo
 constexpr int TC_SMEM = 2 * TC_STAGE + 1024 + 128;   // 2 stages + alignment + barriers
@@ -110,14 +111,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
 // C[z] (rows < M, columns < N) = A * B^T over k-chunks [z * cps, min(nkc, (z+1) * cps)).
 //   A: [M][lda] fp32, lda % 4 == 0, columns >= nkc * 32 read as zero beyond K
 //   Bt: pre-split tiles [ntiles][nkc][2][128 x 32] (see tc_pack_b)
-// PAIRS: tiles overlap by one column (tile nt covers B rows 127 nt .. 127 nt + 127,
-// tc_pack_b with stride 127) and the epilogue writes C as float2 pairs
-// (C[m][n], C[m][n + 1]) for n < N - 1, so a consumer interpolating between
+// PAIRS: tiles overlap by two columns (tile nt covers B rows 126 nt .. 126 nt + 127,
+// tc_pack_b with stride TC_PSTRIDE = 126) and the epilogue writes C as float2
+// pairs (C[m][n], C[m][n + 1]) for n < N - 1, 126 per tile (an even stride keeps
+// every 2-pair store 16-byte aligned), so a consumer interpolating between
 // neighbouring columns gathers one 8-byte entry (ldc in float2 units).
 // STAGES = 2: chunk c+1's loads overlap chunk c's MMAs (long K); STAGES = 1:
 // half the shared memory, so two CTAs share an SM and one CTA's epilogue
 // overlaps the other's loads and MMAs (short K, store-heavy epilogue).
-template <bool PAIRS, int STAGES = 2>
+// A_PACKED: A is given as pre-split, pre-swizzled tiles [ceil(M/128)][nkc][hi, lo]
+// (the layout of tc_pack_b, built on the device by k_tc_pack_a) and lands in
+// shared memory by one cp.async.bulk per chunk like B -- the threads only run
+// the epilogue.
+template <bool PAIRS, int STAGES = 2, bool A_PACKED = false>
 __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, int nkc, int cps,
                                                   const float *__restrict__ A, const float *__restrict__ Bt,
                                                   float *__restrict__ C, int ldc) {
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     uint64_t *bars = (uint64_t *)(base + STAGES * TC_STAGE);  // [0, S) B landed, [S, 2S) MMAs of stage done
     uint32_t *tmem_slot = (uint32_t *)(bars + 4);
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int m0 = blockIdx.y * TC_M, nt = blockIdx.x, n0 = nt * (PAIRS ? TC_N - 1 : TC_N);
+    const int m0 = blockIdx.y * TC_M, nt = blockIdx.x, n0 = nt * (PAIRS ? TC_PSTRIDE : TC_N);
     const int kc0 = blockIdx.z * cps, kc1 = min(nkc, kc0 + cps);
 
     if (warp == 0) {
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     const uint32_t tmem = *tmem_slot;
     const uint32_t idesc = tc_idesc_tf32();
     const int row = tid, gm = m0 + row;
-    const float *arow = A + (size_t)(gm < M ? gm : 0) * lda;
+    const float *arow = A + (size_t)(gm < M ? gm : 0) * (A_PACKED ? 0 : lda);
 
     for (int c = kc0; c < kc1; c++) {
         const int it = c - kc0, st = it % STAGES, use = it / STAGES;
@@ -154,26 +160,37 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
         if (it >= STAGES) mbar_wait(smem_u32(bars + STAGES + st), (use - 1) & 1);
         if (tid == 0) {
             const uint32_t mb = smem_u32(bars + st);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(2 * TC_OPB));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"((A_PACKED ? 4 : 2) * TC_OPB));
             const float *src = Bt + ((size_t)nt * nkc + c) * (2 * TC_M * TC_KC);
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                     smem_u32(sB)),
                 "l"(src), "r"(2 * TC_OPB), "r"(mb)
                 : "memory");
+            if (A_PACKED) {
+                const float *asrc = A + ((size_t)blockIdx.y * nkc + c) * (2 * TC_M * TC_KC);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        smem_u32(sA_hi)),
+                    "l"(asrc), "r"(2 * TC_OPB), "r"(mb)
+                    : "memory");
+            }
         }
-        // A: this thread's row, 32 columns of chunk c, split into hi / lo
-        const int k0 = c * TC_KC;
+        if (!A_PACKED) {
+            // A: this thread's row, 32 columns of chunk c, split into hi / lo
+            const int k0 = c * TC_KC;
 #pragma unroll
-        for (int k4 = 0; k4 < TC_KC; k4 += 4) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gm < M && k0 + k4 < K) v = __ldg((const float4 *)(arow + k0 + k4));
-            const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-            const uint32_t off = tc_swz(row, k4);
-            *(float4 *)(sA_hi + off) = h;
-            *(float4 *)(sA_lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            for (int k4 = 0; k4 < TC_KC; k4 += 4) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gm < M && k0 + k4 < K) v = __ldg((const float4 *)(arow + k0 + k4));
+                const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                const uint32_t off = tc_swz(row, k4);
+                *(float4 *)(sA_hi + off) = h;
+                *(float4 *)(sA_lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n");
         }
-        asm volatile("fence.proxy.async.shared::cta;\n");
         __syncthreads();
         if (tid == 0) {
             mbar_wait(smem_u32(bars + st), use & 1);  // B tile landed
@@ -250,13 +267,24 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
             for (int j = 0; j < 32; j++) buf[lane * 33 + j] = cur[j];
             buf[lane * 33 + 32] = c0 + 32 < TC_N ? nxt[0] : 0.0f;
             __syncwarp();
-            const int n = n0 + c0 + lane;
-            const bool ok = c0 + lane + 1 < TC_N && n + 1 < N;
+            // lane l: row 2 i + (l >> 4) of the pass, pairs jp, jp + 1 (jp = 2 (l & 15)):
+            // one 16-byte store per lane, two 256-byte row segments per warp store
+            const int jp = 2 * (lane & 15);
+            const int n = n0 + c0 + jp;
+            const bool ok0 = c0 + jp < TC_PSTRIDE && n + 1 < N;
+            const bool ok1 = c0 + jp + 1 < TC_PSTRIDE && n + 2 < N;
 #pragma unroll 4
-            for (int rr = 0; rr < 32; rr++) {
+            for (int i = 0; i < 16; i++) {
+                const int rr = 2 * i + (lane >> 4);
                 const int grow = m0 + warp * 32 + rr;
-                if (ok && grow < M)
-                    Cz[(size_t)grow * ldc + n] = make_float2(buf[rr * 33 + lane], buf[rr * 33 + lane + 1]);
+                if (grow < M && ok0) {
+                    const float *br = buf + rr * 33 + jp;
+                    float2 *dst = Cz + (size_t)grow * ldc + n;
+                    if (ok1)
+                        *(float4 *)dst = make_float4(br[0], br[1], br[1], br[2]);
+                    else
+                        *dst = make_float2(br[0], br[1]);
+                }
             }
 #pragma unroll
             for (int j = 0; j < 32; j++) cur[j] = nxt[j];
@@ -267,11 +295,30 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * TC_N));
 }
 
+// Device: pack A (M x K, row-major, lda) into the tile layout of tc_pack_b
+// (rows zero-padded to a multiple of 128, K to nkc * 32): one thread per element.
+__global__ void k_tc_pack_a(const float *__restrict__ A, int M, int K, int lda, int nkc, float *__restrict__ out) {
+    const size_t n = (size_t)((M + TC_M - 1) / TC_M) * nkc * TC_M * TC_KC;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % TC_KC);
+        const int r = (int)((i / TC_KC) % TC_M);
+        const size_t tile = i / ((size_t)TC_M * TC_KC);  // mt * nkc + c
+        const int c = (int)(tile % nkc);
+        const int m = (int)(tile / nkc) * TC_M + r, kk = c * TC_KC + k;
+        const float x = (m < M && kk < K) ? A[(size_t)m * lda + kk] : 0.0f;
+        const float h = tf32_hi(x);
+        unsigned char *t = (unsigned char *)(out + tile * (2 * TC_M * TC_KC));
+        *(float *)(t + tc_swz(r, k)) = h;
+        *(float *)(t + TC_OPB + tc_swz(r, k)) = x - h;
+    }
+}
+
 // Host: pack B (N x K, row-major, ldb) into pre-split swizzled tiles
 // [ceil(N/128)][nkc][hi, lo][128 x 32].  out must hold ntiles * nkc * 8192 floats.
-// stride = TC_N (disjoint tiles) or TC_N - 1 (overlapping tiles of k_tc_gemm<true>);
-// ntiles = ceil(N / 128) resp. ceil((N - 1) / 127).
+// stride = TC_N (disjoint tiles) or TC_PSTRIDE (overlapping tiles of k_tc_gemm<true>);
+// ntiles = ceil(N / 128) resp. ceil((N - 1) / TC_PSTRIDE).
 inline int tc_ntiles(int N, int stride) { return stride == TC_N ? (N + TC_N - 1) / TC_N : (N - 1 + stride - 1) / stride; }
+// (PAIRS tiles: pairs n = 0 .. N - 2, stride TC_PSTRIDE per tile)
 
 inline void tc_pack_b(const float *B, int N, int K, int ldb, int nkc, float *out, int stride = TC_N) {
     const int ntiles = tc_ntiles(N, stride);
