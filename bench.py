@@ -245,9 +245,11 @@ def run_gpu(args):
     counts = json.load(open(os.path.join(ROOT, "workloads", "work_counts.json")))[str(cfg.seed)]
     nb_bp = G.query("esai_breakpoints")
     kern = {k: {"avg_ms": v[0] / v[1], "launches": v[1]} for k, v in ktimes.items()}
-    fwd_k = [k for k in kern if k in ("k_pad_rows", "k_tc_pack_a", "k_tc_gemm_W", "k_esai_fwd", "k_esai_fwd_ts", "k_sum_parts_f64",
+    fwd_k = [k for k in kern if k in ("k_pad_rows", "k_tc_pack_a", "k_tc_gemm_W", "k_esai_fwd", "k_esai_fwd_ts", "k_pc_fwd",
+                                      "k_sum_parts_f64",
                                       "k_forward", "k_sum_f64")]
-    bwd_k = [k for k in kern if k in ("k_absmax", "k_esai_bwd", "k_tc_gemm_b2", "k_sum_parts_f32", "k_backward")]
+    bwd_k = [k for k in kern if k in ("k_absmax", "k_esai_bwd", "k_pc_bwd", "k_tc_gemm_b2", "k_sum_parts_f32",
+                                      "k_backward")]
     op_ms = {"cacsi_forward": sum(kern[k]["avg_ms"] for k in fwd_k),
              "cacsi_backward": sum(kern[k]["avg_ms"] for k in bwd_k)}
     dom = max(op_ms, key=op_ms.get)

@@ -591,6 +591,179 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     }
 }
 
+// ---- pair cache: the online/offline trade-off taken to HBM --
+// Every open pair's interpolation weights into the breakpoint basis depend on
+// the geometry only, so they can be computed ONCE at create and streamed by
+// every later operator call: per list (voxel v, detector row ix), the open
+// pixels in increasing jy, record key = (jy << 16) | b and w = (P (1 - tau),
+// P tau) -- 12 bytes per open pair (config 2: 5.4e8 pairs, 6.4 GB of 180 GB).
+// The paper precomputes what is cheaper to load than to recompute ("if the cost
+// of computing the factor is equivalent to the speed of loading the factor from
+// main memory, then the computations should be performed online"); on a B200,
+// streaming 12 bytes is cheaper than the ~100 instructions of pair geometry and
+// breakpoint location.  Both operators read the same records: the forward by
+// (z, row, y) with the W gathers of one list on one W row, the backward by
+// voxel.  Built only if it fits (cacsi_query "pair_cache_records" > 0).
+
+// records per list (v, ix) = open pixels of row ix (transmission bitmap tb_bwd)
+__global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) {
+    const int nw = (p.n_det + 31) / 32;
+    const size_t n = (size_t)p.n_vox * p.det_nx;
+    for (size_t l = blockIdx.x * (size_t)blockDim.x + threadIdx.x; l < n; l += (size_t)gridDim.x * blockDim.x) {
+        const int v = (int)(l / p.det_nx), ix = (int)(l % p.det_nx);
+        const uint32_t *tb = e.tb_bwd + (size_t)v * nw;
+        const int q0 = ix * p.det_ny, q1 = q0 + p.det_ny;  // [q0, q1)
+        int c = 0;
+        for (int wd = q0 >> 5; wd <= (q1 - 1) >> 5; wd++) {
+            uint32_t m = __ldg(tb + wd);
+            const int lo = max(q0 - 32 * wd, 0), hi = min(q1 - 32 * wd, 32);  // bits [lo, hi)
+            m &= (hi == 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo);
+            c += __popc(m);
+        }
+        cnt[l] = c;
+    }
+}
+
+// fill: one warp per list, 32 pixels per step, ballot-compacted records
+template <bool SAI>
+__global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ key,
+                                                 float2 *__restrict__ w) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
+    load_bp(e, sb, lut);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (p.n_det + 31) / 32;
+    const size_t n = (size_t)p.n_vox * p.det_nx;
+    for (size_t l = (size_t)blockIdx.x * 8 + warp; l < n; l += (size_t)gridDim.x * 8) {
+        const int v = (int)(l / p.det_nx), ix = (int)(l % p.det_nx);
+        const VoxelRec vr = p.vox[v];
+        long long base = e.pc_off[l];
+        for (int jy0 = 0; jy0 < p.det_ny; jy0 += 32) {
+            const int jy = jy0 + lane, q = ix * p.det_ny + jy;
+            const bool open = jy < p.det_ny && ((__ldg(e.tb_bwd + (size_t)v * nw + (q >> 5)) >> (q & 31)) & 1u);
+            float P = 0.0f, sh = 0.0f, t = 0.0f;
+            int b = 0;
+            if (open) {
+                pair_geom(p, vr, p.det[q], P, sh, !SAI);
+                b = locate_pair<SAI>(p, e, sb, lut, sh, v, q, t);
+            }
+            const uint32_t m = __ballot_sync(FULL, open);
+            if (open) {
+                const long long o = base + __popc(m & ((1u << lane) - 1u));
+                key[o] = ((uint32_t)jy << 16) | (uint32_t)b;
+                w[o] = make_float2(P * (1.0f - t), P * t);
+            }
+            base += __popc(m);
+        }
+    }
+}
+
+// forward from the cache: items (z chunk, detector row); warps take voxel rows
+// y, lanes the list's records; per-warp row accumulators in shared memory (the
+// jy of one list are distinct: conflict-free, no atomics), fp64 partials per z chunk
+constexpr int PCF_W = 8;
+__global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float2 *__restrict__ W,
+                                                     int iz_per_chunk, int n_items, double *__restrict__ partial) {
+    extern __shared__ float acc_s[];  // [PCF_W][det_ny]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *acc = acc_s + warp * p.det_ny;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int chunk = item / p.det_nx, ix = item % p.det_nx;
+        for (int i = lane; i < p.det_ny; i += 32) acc[i] = 0.0f;
+        __syncwarp();
+        const int iz0 = chunk * iz_per_chunk, iz1 = min(p.nz, iz0 + iz_per_chunk);
+        for (int iz = iz0; iz < iz1; iz++)
+            for (int iy = warp; iy < p.ny; iy += PCF_W) {
+                const int v = iy * p.nz + iz;
+                const size_t list = (size_t)v * p.det_nx + ix;
+                const long long o0 = e.pc_off[list], o1 = e.pc_off[list + 1];
+                const float2 *Wv = W + (size_t)v * e.ldw;
+                // four records per lane per step: their loads are issued together
+                // (memory-level parallelism); the jy of one list are distinct, so
+                // the four accumulator updates never alias
+                for (long long o = o0 + lane; o < o1; o += 128) {
+                    uint32_t k[4];
+                    float2 a[4], wb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const bool in = o + 32 * u < o1;
+                        k[u] = in ? __ldg(e.pc_key + o + 32 * u) : 0u;
+                        a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) wb[u] = __ldg(Wv + (k[u] & 0xFFFFu));
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (o + 32 * u < o1) {
+                            float *ap = acc + (k[u] >> 16);
+                            *ap = fmaf(a[u].x, wb[u].x, fmaf(a[u].y, wb[u].y, *ap));
+                        }
+                }
+            }
+        __syncthreads();
+        for (int jy = threadIdx.x; jy < p.det_ny; jy += PCF_W * 32) {
+            double t = 0.0;
+            for (int ww = 0; ww < PCF_W; ww++) t += (double)acc_s[ww * p.det_ny + jy];
+            partial[(size_t)chunk * p.n_det + (size_t)ix * p.det_ny + jy] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// backward from the cache: one CTA per voxel (grid-stride), warps take detector
+// rows, lanes the records; fixed-point deposits as k_esai_bwd (same scale rule)
+constexpr int PCB_T = 256;
+__global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, const float *__restrict__ w,
+                                                  const float *__restrict__ wmax, float *__restrict__ A) {
+    extern __shared__ int hist_s[];  // [max_win]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float wm = *wmax;
+    for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        __syncthreads();
+        for (int i = tid; i < nwin; i += PCB_T) hist_s[i] = 0;
+        __syncthreads();
+        const double bound = (double)e.vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+        int *hv = hist_s - win.x;
+        for (int ix = warp; scale > 0.0f && ix < p.det_nx; ix += PCB_T / 32) {
+            const size_t list = (size_t)v * p.det_nx + ix;
+            const long long o0 = e.pc_off[list], o1 = e.pc_off[list + 1];
+            const float *wr = w + (size_t)ix * p.det_ny;
+            for (long long o = o0 + lane; o < o1; o += 128) {
+                uint32_t k[4];
+                float2 a[4];
+                float wq[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const bool in = o + 32 * u < o1;
+                    k[u] = in ? __ldg(e.pc_key + o + 32 * u) : 0u;
+                    a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) wq[u] = __ldg(wr + (k[u] >> 16)) * scale;
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (o + 32 * u < o1) {
+                        const int b = (int)(k[u] & 0xFFFFu);
+                        atomicAdd(hv + b, __float2int_rn(a[u].x * wq[u]));
+                        atomicAdd(hv + b + 1, __float2int_rn(a[u].y * wq[u]));
+                    }
+            }
+        }
+        __syncthreads();
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = tid; b < e.ldw; b += PCB_T) {
+            const int i = b - win.x;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist_s[i] * unit : 0.0f;
+        }
+    }
+}
+
 static size_t bwd_smem_bytes(size_t bpb, int max_win) {
     return bpb + (size_t)((max_win + 3) & ~3) * sizeof(int) + (size_t)PB_WARPS * PB_QW * 32 * sizeof(uint16_t);
 }
@@ -885,6 +1058,46 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e != cudaSuccess) return e;
         E.vbound = (const float *)g->d_esai_vbound;
     }
+    // pair cache (above): counts -> host scan -> fill, if it fits in half the free memory
+    E.pc = 0;
+    const char *pce = getenv("CACSI_PAIR_CACHE");
+    if (!(pce && strcmp(pce, "0") == 0) && (size_t)p.det_ny <= 65535) {
+        const size_t nl = (size_t)nv * p.det_nx;
+        int *cnt = nullptr;
+        e = cudaMalloc(&cnt, nl * sizeof(int));
+        if (e == cudaSuccess) {
+            k_pc_count<<<8 * sm_count(g->device), 256>>>(p, E, cnt);
+            e = cudaDeviceSynchronize();
+        }
+        std::vector<int> hc(nl);
+        if (e == cudaSuccess) e = cudaMemcpy(hc.data(), cnt, nl * sizeof(int), cudaMemcpyDeviceToHost);
+        cudaFree(cnt);
+        if (e != cudaSuccess) return e;
+        std::vector<long long> off(nl + 1, 0);
+        for (size_t i = 0; i < nl; i++) off[i + 1] = off[i] + hc[i];
+        const long long nrec = off[nl];
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const size_t need = (size_t)nrec * (sizeof(uint32_t) + sizeof(float2)) + (nl + 1) * sizeof(long long);
+        if (need <= free_b / 2) {
+            e = cudaMalloc(&g->d_pc_off, (nl + 1) * sizeof(long long));
+            if (e == cudaSuccess) e = cudaMemcpy(g->d_pc_off, off.data(), (nl + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_key, (size_t)std::max(nrec, 1ll) * sizeof(uint32_t));
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_w, (size_t)std::max(nrec, 1ll) * sizeof(float2));
+            if (e != cudaSuccess) return e;
+            E.pc_off = (const long long *)g->d_pc_off;
+            E.pc_key = (const uint32_t *)g->d_pc_key;
+            E.pc_w = (const float2 *)g->d_pc_w;
+            E.pc_n = nrec;
+            const size_t smem = host_bp_bytes(E);
+            auto kf = sai ? k_pc_fill<true> : k_pc_fill<false>;
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kf<<<persistent_grid(g, smem, 256), 256, smem>>>(p, E, (uint32_t *)g->d_pc_key, (float2 *)g->d_pc_w);
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return e;
+            E.pc = 1;
+        }
+    }
     E.enabled = 1;
     return cudaSuccess;
 }
@@ -960,6 +1173,19 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         cudaFreeAsync(fp, s);
         cudaFreeAsync(W, s);
         return e;
+    } else if (E.pc) {
+        // pair cache: items (z chunk, detector row), fp64 partials per z chunk
+        int izc = std::max(1, (p.nz * p.det_nx) / (8 * sm_count(g->device) * 4));  // >= ~4 items per resident CTA
+        izc = std::min(izc, p.nz);
+        S = (p.nz + izc - 1) / izc;
+        e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_pc_fwd");
+            const size_t smem = (size_t)PCF_W * p.det_ny * sizeof(float);
+            const int n_items = S * p.det_nx;
+            k_pc_fwd<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, (const float2 *)W, izc,
+                                                                                        n_items, part);
+        }
     } else if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
         const int n_groups = ((p.det_nx + TS_R - 1) / TS_R) * segs;
@@ -1024,12 +1250,19 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
             KScope kt_(g, s, "k_absmax");
             k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, pmask, wmax);
         }
+        if (E.pc && pmask == nullptr) {
+            KScope kt_(g, s, "k_pc_bwd");
+            const size_t hs = (size_t)E.max_win * sizeof(int);
+            cudaFuncSetAttribute(k_pc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+            k_pc_bwd<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, A);
+        } else {
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {
             KScope kt_(g, s, "k_esai_bwd");
             auto kb = p.sai_n > 0 ? k_esai_bwd<false, true> : k_esai_bwd<false, false>;
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kb<<<persistent_grid(g, smem, PB_T), PB_T, smem, s>>>(p, E, w, wmax, E.vbound, pmask, A);
+        }
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");

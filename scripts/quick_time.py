@@ -45,7 +45,7 @@ def main():
         out[ci] = dict(fwd_ms=tf[len(tf) // 2], bwd_ms=tb[len(tb) // 2], pairs=pairs,
                        fwd_pairs_per_s=pairs / tf[len(tf) // 2] * 1e3, bwd_pairs_per_s=pairs / tb[len(tb) // 2] * 1e3,
                        **{k: G.query(k) for k in ("esai_breakpoints", "esai_max_window", "esai_lut_cells",
-                                                  "esai_lut_slow_cells", "ts_rho")})
+                                                  "esai_lut_slow_cells", "ts_rho", "pair_cache_records")})
         print(json.dumps({ci: out[ci]}), flush=True)
         G.close()
 
