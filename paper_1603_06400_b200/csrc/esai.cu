@@ -729,9 +729,18 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
         const double bound = (double)e.vbound[v] * (double)wm;
         const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
         int *hv = hist_s - win.x;
-        for (int ix = warp; scale > 0.0f && ix < p.det_nx; ix += PCB_T / 32) {
-            const size_t list = (size_t)v * p.det_nx + ix;
-            const long long o0 = e.pc_off[list], o1 = e.pc_off[list + 1];
+        // the warp's rows ix = warp, warp + 8, ...: 32 at a time, lane i loads row i's bounds
+        const int n_rows = scale > 0.0f ? (p.det_nx - warp + PCB_T / 32 - 1) / (PCB_T / 32) : 0;
+        for (int rb = 0; rb < n_rows; rb += 32) {
+            long long my0 = 0, my1 = 0;
+            if (rb + lane < n_rows) {
+                const size_t list = (size_t)v * p.det_nx + warp + (rb + lane) * (PCB_T / 32);
+                my0 = __ldg(e.pc_off + list);
+                my1 = __ldg(e.pc_off + list + 1);
+            }
+            for (int ri = 0; ri < min(32, n_rows - rb); ri++) {
+            const int ix = warp + (rb + ri) * (PCB_T / 32);
+            const long long o0 = __shfl_sync(FULL, my0, ri), o1 = __shfl_sync(FULL, my1, ri);
             const float *wr = w + (size_t)ix * p.det_ny;
             for (long long o = o0 + lane; o < o1; o += 128) {
                 uint32_t k[4];
@@ -752,6 +761,7 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
                         atomicAdd(hv + b, __float2int_rn(a[u].x * wq[u]));
                         atomicAdd(hv + b + 1, __float2int_rn(a[u].y * wq[u]));
                     }
+            }
             }
         }
         __syncthreads();
