@@ -154,7 +154,11 @@ def run_gpu(args):
     r_np = np.full(G0.g_shape, 5.0, np.float32)
     G0.close()
     d["scale"] = s
-    G = P.Geometry(d, device=local)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
+    G = P.Geometry(d, device=local)  # host tables, ESAI tables, bitmaps, pair cache (once per geometry)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t_setup) * 1e3
     y = torch.as_tensor(y_np).to(dev)
     r = torch.as_tensor(r_np).to(dev)
     ones = torch.ones(G.g_shape, dtype=torch.float32, device=dev)
@@ -238,6 +242,31 @@ def run_gpu(args):
     h2d = (fh.nbytes + yh.nbytes + rh.nbytes + b1h.nbytes)
     d2h = fh.nbytes
 
+    # ---- the same step without the pair cache (geometry and breakpoint location
+    # recomputed per pair inside the operators, CACSI_PAIR_CACHE=0), for comparison
+    on_the_fly = None
+    if G.query("pair_cache_records") > 0:
+        os.environ["CACSI_PAIR_CACHE"] = "0"
+        try:
+            G2 = P.Geometry(d, device=local)
+        finally:
+            del os.environ["CACSI_PAIR_CACHE"]
+        G, Gc = G2, G
+        f.fill_(f0)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        ev2 = [[E() for _ in range(5)] for _ in range(max(1, min(args.steps, 5)))]
+        for i, ev in enumerate(ev2):
+            flush.fill_(float(i))
+            step(ev)
+        torch.cuda.synchronize()
+        ms2 = float(np.mean([e[0].elapsed_time(e[4]) for e in ev2]))
+        on_the_fly = {"ms_per_step": ms2, "value": 2 * pairs / (ms2 / 1e3),
+                      "note": "CACSI_PAIR_CACHE=0: pair geometry and breakpoint location recomputed per pair per call"}
+        G.close()
+        G = Gc
+
     # ---- roofline: the dominant operator call, work per
     # SURVEY.md §8(d)'s per-unit figures (FP32 lane-ops: 4 per effective term
     # forward, 6 backward, 60 per open pair geometry, 12 per pair mask test)
@@ -288,6 +317,33 @@ def run_gpu(args):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
+    # HBM roofline of the dominant pair-cache kernel: algorithmic bytes
+    # per launch = 12 B per open pair (the pair record: key + two weights, read once)
+    # + the operator's table it gathers from once (k_pc_fwd: the W pairs,
+    # n_vox x ldw x 8 B; k_pc_bwd: w, n_det x 4 B, and the A rows it writes,
+    # n_vox x ldw x 4 B), against the measured copy bandwidth
+    roofline_hbm = None
+    kpc = [k for k in ("k_pc_fwd", "k_pc_bwd") if k in kern]
+    if kpc:
+        kd = max(kpc, key=lambda k: kern[k]["avg_ms"])
+        ldw = G.query("esai_ldw")
+        nrec = G.query("pair_cache_records")
+        tab = cfg.n_vox * ldw * 8 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
+        bytes_ = 12.0 * nrec + tab
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        ach = bytes_ / (kern[kd]["avg_ms"] / 1e3) / 1e9
+        roofline_hbm = {"bound": "hbm", "kernel": kd, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "traffic": None, "algorithmic_bytes_per_launch": bytes_,
+                        "avg_launch_ms": kern[kd]["avg_ms"],
+                        "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else
+                        "fallback 6650 GB/s (B200_PROFILING.md)",
+                        "bytes_note": "12 B per open pair (pair record) + the gathered table once (DESIGN.md §8)"}
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r1s2_dram_traffic.json")))["kernels"]
+            if kd in tr:
+                roofline_hbm["traffic"] = tr[kd]["dram_read_bytes"] + tr[kd]["dram_write_bytes"]
+        except Exception:
+            pass
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -307,7 +363,14 @@ def run_gpu(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": float(np.mean(e2e_ms))},
         "peaks_source": "MEASURED_PEAKS.json" if peaks else "fallback",
+        "setup_ms": setup_ms, "pair_cache_records": G.query("pair_cache_records"),
+        "on_the_fly": on_the_fly,
     }
+    if roofline_hbm is not None:
+        # the dominant kernels stream the pair cache: HBM is their roof; the SURVEY
+        # FP32 accounting of the whole operator is kept beside it
+        out["roofline_alu_survey"] = out["roofline"]
+        out["roofline"] = roofline_hbm
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample_s)
     if world > 1:
@@ -340,6 +403,8 @@ def alg_flops(kernel, cfg, counts, nb):
         # geometry (23), locate (6) and lerp + accumulate (4)
         "k_esai_fwd_ts": 2 * pairs + (9 + 23 + 10) * open_,
         "k_esai_bwd": 2 * pairs + (46 + 6 + 6) * open_,  # compaction, geometry, locate, fixed-point deposits
+        "k_pc_fwd": 4 * open_,                         # pair cache: a0 W_b + a1 W_b+1 accumulated (2 FFMA)
+        "k_pc_bwd": 6 * open_,                         # pair cache: w scale, two weighted deposits
         "k_forward": 10 * pairs + 46 * open_ + 7 * counts["effective_terms"],
         "k_backward": 10 * pairs + 46 * open_ + 9 * counts["effective_terms"],
     }

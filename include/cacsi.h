@@ -266,8 +266,14 @@ CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, co
                                      int32_t *launches);
 
 /* Integer facts about a handle: "esai_breakpoints" (0 if the per-term
- * kernels are used), "esai_max_window", "ts_rho" (0 = no translation
- * symmetry), "energy_resolving".  -1 for an unknown key or NULL.           */
+ * kernels are used), "esai_max_window", "esai_lut_cells",
+ * "esai_lut_slow_cells", "esai_ldw" (row stride of the breakpoint tables),
+ * "pair_cache_records" (open pairs held in the pair cache, 0 if not built),
+ * "ts_rho" (0 = no translation symmetry), "energy_resolving".  -1 for an
+ * unknown key or NULL.
+ * The pair cache is built at create when it fits in half of the
+ * free device memory; the environment variable CACSI_PAIR_CACHE=0 disables it
+ * (the operators then recompute the pair geometry per call).               */
 CACSI_API int64_t cacsi_query(const cacsi_geometry *geom, const char *key);
 
 /* Static description of a status code (never NULL). */

@@ -612,6 +612,7 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "esai_lut_cells")) return g->esai.enabled ? g->esai.nl : 0;
     if (!strcmp(key, "esai_lut_slow_cells")) return g->esai.enabled ? g->esai.n_slow : 0;
     if (!strcmp(key, "pair_cache_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_n : 0;
+    if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
     return -1;
 }

@@ -1,0 +1,82 @@
+"""The pair cache: both operators with and without it
+(CACSI_PAIR_CACHE=0) against the oracle, its record count against the
+oracle's exact count of open pairs, and the two paths against each other."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import make_config
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_1603_06400_b200")
+
+from test_gpu_parity import _sample, assert_parity, gpu_backward, gpu_forward, rnd  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+COUNTS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "workloads", "work_counts.json")))
+
+
+def handles(d, monkeypatch):
+    Gc = P.Geometry(d)
+    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
+    Gn = P.Geometry(d)
+    monkeypatch.delenv("CACSI_PAIR_CACHE")
+    return Gc, Gn
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_record_count_is_the_open_pair_count(ci, monkeypatch):
+    cfg = make_config(ci)
+    Gc, Gn = handles(cfg.desc(), monkeypatch)
+    assert Gc.query("pair_cache_records") == COUNTS[str(cfg.seed)]["open_pairs"]
+    assert Gn.query("pair_cache_records") == 0
+    Gc.close()
+    Gn.close()
+
+
+def test_cache_on_off_config1(monkeypatch):
+    cfg = make_config(1)
+    O = oracle.Geometry(cfg)
+    Gc, Gn = handles(cfg.desc(), monkeypatch)
+    gr = O.forward(cfg.f)
+    w = rnd(Gc.g_shape, 1, 70)
+    br = O.backward(w)
+    for tag, G in (("cache", Gc), ("on-the-fly", Gn)):
+        assert_parity(gpu_forward(G, cfg.f), gr, f"c1 {tag} forward")
+        assert_parity(gpu_backward(G, w), br, f"c1 {tag} backward")
+    assert_parity(gpu_forward(Gc, cfg.f), gpu_forward(Gn, cfg.f), "c1 cache vs on-the-fly forward", l2=1e-6, mr=1e-5)
+    Gc.close()
+    Gn.close()
+
+
+def test_on_the_fly_config2_sampled(monkeypatch):
+    """Full-size config 2 on the kernels that recompute the pair geometry per
+    call (the subset operators and the no-cache fallback use them)."""
+    cfg = make_config(2)
+    O = oracle.Geometry(cfg)
+    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
+    G = P.Geometry(cfg.desc())
+    g = gpu_forward(G, cfg.f).ravel()
+    pix = _sample(cfg.n_det, 96, 11)
+    assert_parity(g[pix], O.forward_pixels(cfg.f, pix), "c2 on-the-fly forward sampled")
+    w = rnd(G.g_shape, 2, 71)
+    b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
+    vox = _sample(cfg.n_vox, 12, 12)
+    assert_parity(b[vox], O.backward_voxels(w, vox), "c2 on-the-fly backward sampled")
+    G.close()
+
+
+def test_sai_without_cache(monkeypatch):
+    cfg = make_config(1)
+    d = cfg.desc()
+    d.update(sai_n_theta=250, sai_theta_min=0.2 * math.pi / 180, sai_theta_max=math.pi / 6)
+    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
+    G, O = P.Geometry(d), oracle.Geometry(d)
+    assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), "c1 SAI on-the-fly forward")
+    w = rnd(G.g_shape, 1, 72)
+    assert_parity(gpu_backward(G, w), O.backward(w), "c1 SAI on-the-fly backward")
+    G.close()
