@@ -746,21 +746,22 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
                 uint32_t k[4];
                 float2 a[4];
                 float wq[4];
+                // branch-free: slots past the list end deposit zero into the
+                // window's first bin (a valid address)
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const bool in = o + 32 * u < o1;
-                    k[u] = in ? __ldg(e.pc_key + o + 32 * u) : 0u;
+                    k[u] = in ? __ldg(e.pc_key + o + 32 * u) : (uint32_t)win.x;
                     a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; u++) wq[u] = __ldg(wr + (k[u] >> 16)) * scale;
 #pragma unroll
-                for (int u = 0; u < 4; u++)
-                    if (o + 32 * u < o1) {
-                        const int b = (int)(k[u] & 0xFFFFu);
-                        atomicAdd(hv + b, __float2int_rn(a[u].x * wq[u]));
-                        atomicAdd(hv + b + 1, __float2int_rn(a[u].y * wq[u]));
-                    }
+                for (int u = 0; u < 4; u++) {
+                    const int b = (int)(k[u] & 0xFFFFu);
+                    atomicAdd(hv + b, __float2int_rn(a[u].x * wq[u]));
+                    atomicAdd(hv + b + 1, __float2int_rn(a[u].y * wq[u]));
+                }
             }
             }
         }
