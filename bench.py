@@ -319,8 +319,8 @@ def run_gpu(args):
         pass
     # HBM roofline of the dominant pair-cache kernel: algorithmic bytes
     # per launch = 12 B per open pair (the pair record: key + two weights, read once)
-    # + the operator's table it gathers from once (k_pc_fwd: the W pairs,
-    # n_vox x ldw x 8 B; k_pc_bwd: w, n_det x 4 B, and the A rows it writes,
+    # + the operator's table it gathers from once (k_pc_fwd: the W rows,
+    # n_vox x ldw x 4 B; k_pc_bwd: w, n_det x 4 B, and the A rows it writes,
     # n_vox x ldw x 4 B), against the measured copy bandwidth
     roofline_hbm = None
     kpc = [k for k in ("k_pc_fwd", "k_pc_bwd") if k in kern]
@@ -328,7 +328,7 @@ def run_gpu(args):
         kd = max(kpc, key=lambda k: kern[k]["avg_ms"])
         ldw = G.query("esai_ldw")
         nrec = G.query("pair_cache_records")
-        tab = cfg.n_vox * ldw * 8 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
+        tab = cfg.n_vox * ldw * 4 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
         bytes_ = 12.0 * nrec + tab
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         ach = bytes_ / (kern[kd]["avg_ms"] / 1e3) / 1e9

@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // y, lanes the list's records; per-warp row accumulators in shared memory (the
 // jy of one list are distinct: conflict-free, no atomics), fp64 partials per z chunk
 constexpr int PCF_W = 8;
-__global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float2 *__restrict__ W,
+__global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float *__restrict__ W,
                                                      int iz_per_chunk, int n_items, double *__restrict__ partial) {
     extern __shared__ float acc_s[];  // [PCF_W][det_ny]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
                 const int v = iy * p.nz + iz;
                 const size_t list = (size_t)v * p.det_nx + ix;
                 const long long o0 = e.pc_off[list], o1 = e.pc_off[list + 1];
-                const float2 *Wv = W + (size_t)v * e.ldw;
+                const float *Wv = W + (size_t)v * e.ldw;
                 // four records per lane per step: their loads are issued together
                 // (memory-level parallelism); the jy of one list are distinct, so
                 // the four accumulator updates never alias
@@ -693,7 +693,10 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
                         a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; u++) wb[u] = __ldg(Wv + (k[u] & 0xFFFFu));
+                    for (int u = 0; u < 4; u++) {
+                        const float *wp = Wv + (k[u] & 0xFFFFu);
+                        wb[u] = make_float2(__ldg(wp), __ldg(wp + 1));
+                    }
 #pragma unroll
                     for (int u = 0; u < 4; u++)
                         if (o + 32 * u < o1) {
@@ -1015,6 +1018,13 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_b, tB.data(), tB.size() * sizeof(float), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return e;
         E.tc_w = (const float *)g->d_tc_w;
+        // the same S~ packed in disjoint tiles: the plain W = F S~^T read by the pair-cache forward
+        std::vector<float> tW1((size_t)tc_ntiles(nb, TC_N) * nkcW * 2 * TC_N * TC_KC);
+        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW1.data(), TC_N);
+        e = cudaMalloc(&g->d_tc_w1, tW1.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_w1, tW1.data(), tW1.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
+        E.tc_w1 = (const float *)g->d_tc_w1;
         E.tc_b = (const float *)g->d_tc_b;
     }
     // transmission bitmaps
@@ -1151,10 +1161,18 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     {
         // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
         KScope kt_(g, s, "k_tc_gemm_W");
-        dim3 gg(tc_ntiles(E.nb, TC_PSTRIDE), (p.n_vox + TC_M - 1) / TC_M, 1);
-        cudaFuncSetAttribute(k_tc_gemm<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
-        k_tc_gemm<true, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp, E.tc_w, W,
-                                                             E.ldw);
+        if (E.pc && pixels == nullptr) {
+            // plain W rows (n_vox x ldw fp32): the pair-cache forward gathers W_b and W_{b+1}
+            dim3 gg(tc_ntiles(E.nb, TC_N), (p.n_vox + TC_M - 1) / TC_M, 1);
+            cudaFuncSetAttribute(k_tc_gemm<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+            k_tc_gemm<false, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp, E.tc_w1,
+                                                                  W, E.ldw);
+        } else {
+            dim3 gg(tc_ntiles(E.nb, TC_PSTRIDE), (p.n_vox + TC_M - 1) / TC_M, 1);
+            cudaFuncSetAttribute(k_tc_gemm<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+            k_tc_gemm<true, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp, E.tc_w, W,
+                                                                 E.ldw);
+        }
     }
     if (pixels != nullptr) {
         // subset: g = 0 outside the list, listed pixels by k_esai_fwd_list
@@ -1194,7 +1212,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             KScope kt_(g, s, "k_pc_fwd");
             const size_t smem = (size_t)PCF_W * p.det_ny * sizeof(float);
             const int n_items = S * p.det_nx;
-            k_pc_fwd<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, (const float2 *)W, izc,
+            k_pc_fwd<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, W, izc,
                                                                                         n_items, part);
         }
     } else if (p.ts_rho > 0) {

@@ -81,7 +81,8 @@ struct Esai {
     // offline), one bit per pair in the order each pair kernel visits them
     const uint32_t *tb_fwd;  // forward (TS or tiled layout, esai.cu)
     int ldw;                 // row stride of W / A (nb rounded up to 32, zero padded)
-    const float *tc_w;       // S~ as pre-split, pre-swizzled tensor-core B tiles (W = F S~^T)
+    const float *tc_w;       // S~ as pre-split, pre-swizzled tensor-core B tiles (W = F S~^T), pair tiles
+    const float *tc_w1;      // the same in disjoint tiles (plain W rows)
     const float *tc_b;       // S~^T likewise (b2 = A S~)
     const uint32_t *tb_bwd;  // backward: [voxel][ceil(n_det/32)], bit i of word j = pixel 32 j + i
     // pair cache (esai.cu "pair cache"): per open pair of list (voxel v, detector row ix),
@@ -106,7 +107,7 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_key, *d_pc_w;
+        *d_esai_vbound, *d_pc_off, *d_pc_key, *d_pc_w, *d_tc_w1;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;
