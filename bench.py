@@ -318,7 +318,8 @@ def run_gpu(args):
     except Exception:
         pass
     # HBM roofline of the dominant pair-cache kernel: algorithmic bytes
-    # per launch = 12 B per open pair (the pair record: key + two weights, read once)
+    # per launch = the record bytes per open pair (P, packed (b, tau), jy: 9 B on
+    # config 2, read once) + the 8-byte list offsets
     # + the operator's table it gathers from once (k_pc_fwd: the W rows,
     # n_vox x ldw x 4 B; k_pc_bwd: w, n_det x 4 B, and the A rows it writes,
     # n_vox x ldw x 4 B), against the measured copy bandwidth
@@ -329,7 +330,8 @@ def run_gpu(args):
         ldw = G.query("esai_ldw")
         nrec = G.query("pair_cache_records")
         tab = cfg.n_vox * ldw * 4 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
-        bytes_ = 12.0 * nrec + tab
+        rb = G.query("pair_cache_record_bytes")
+        bytes_ = float(rb) * nrec + 8.0 * cfg.n_vox * cfg.det_nx + tab
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         ach = bytes_ / (kern[kd]["avg_ms"] / 1e3) / 1e9
         roofline_hbm = {"bound": "hbm", "kernel": kd, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
@@ -337,7 +339,8 @@ def run_gpu(args):
                         "avg_launch_ms": kern[kd]["avg_ms"],
                         "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else
                         "fallback 6650 GB/s (B200_PROFILING.md)",
-                        "bytes_note": "12 B per open pair (pair record) + the gathered table once (DESIGN.md §8)"}
+                        "bytes_note": f"{rb} B per open pair (pair record) + list offsets + the gathered table "
+                                      "once (DESIGN.md §8)"}
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "r1s2_dram_traffic.json")))["kernels"]
             if kd in tr:

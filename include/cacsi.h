@@ -269,6 +269,8 @@ CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, co
  * kernels are used), "esai_max_window", "esai_lut_cells",
  * "esai_lut_slow_cells", "esai_ldw" (row stride of the breakpoint tables),
  * "pair_cache_records" (open pairs held in the pair cache, 0 if not built),
+ * "pair_cache_record_bytes" (bytes per record: P, packed (b, tau), jy),
+ * "pair_cache_tau_bits" (fraction bits of the stored tau),
  * "ts_rho" (0 = no translation symmetry), "energy_resolving".  -1 for an
  * unknown key or NULL.
  * The pair cache is built at create when it fits in half of the

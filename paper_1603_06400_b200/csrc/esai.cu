@@ -595,12 +595,15 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
 // Every open pair's interpolation weights into the breakpoint basis depend on
 // the geometry only, so they can be computed ONCE at create and streamed by
 // every later operator call: per list (voxel v, detector row ix), the open
-// pixels in increasing jy, record key = (jy << 16) | b and w = (P (1 - tau),
-// P tau) -- 12 bytes per open pair (config 2: 5.4e8 pairs, 6.4 GB of 180 GB).
+// pixels in increasing jy, each a record of P (fp32), (b, tau) packed in 32 bits
+// (b in the high bits, tau in the remaining >= 16 fraction bits: |tau error| <=
+// 2^-(tbits+1), i.e. a weight error P |dtau| |W_{b+1} - W_b|, below fp32
+// rounding for tbits = 20) and jy (1 byte for det_ny <= 256, else 2): 9 bytes
+// per open pair on config 2 (5.8e8 pairs, 5.2 GB of 180 GB).
 // The paper precomputes what is cheaper to load than to recompute ("if the cost
 // of computing the factor is equivalent to the speed of loading the factor from
 // main memory, then the computations should be performed online"); on a B200,
-// streaming 12 bytes is cheaper than the ~100 instructions of pair geometry and
+// streaming 9 bytes is cheaper than the ~100 instructions of pair geometry and
 // breakpoint location.  Both operators read the same records: the forward by
 // (z, row, y) with the W gathers of one list on one W row, the backward by
 // voxel.  Built only if it fits (cacsi_query "pair_cache_records" > 0).
@@ -625,9 +628,11 @@ __global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) 
 }
 
 // fill: one warp per list, 32 pixels per step, ballot-compacted records
-template <bool SAI>
-__global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ key,
-                                                 float2 *__restrict__ w) {
+template <bool SAI, typename JY>
+__global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ bt,
+                                                 float *__restrict__ Pout, JY *__restrict__ jyout) {
+    const float tone = (float)(1u << e.pc_tbits);
+    const uint32_t tmax = (1u << e.pc_tbits) - 1u;
     extern __shared__ __align__(16) unsigned char smem[];
     float *sb = (float *)smem;
     uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
@@ -652,8 +657,9 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
             const uint32_t m = __ballot_sync(FULL, open);
             if (open) {
                 const long long o = base + __popc(m & ((1u << lane) - 1u));
-                key[o] = ((uint32_t)jy << 16) | (uint32_t)b;
-                w[o] = make_float2(P * (1.0f - t), P * t);
+                bt[o] = ((uint32_t)b << e.pc_tbits) | min(__float2uint_rn(t * tone), tmax);
+                Pout[o] = P;
+                jyout[o] = (JY)jy;
             }
             base += __popc(m);
         }
@@ -664,10 +670,15 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // y, lanes the list's records; per-warp row accumulators in shared memory (the
 // jy of one list are distinct: conflict-free, no atomics), fp64 partials per z chunk
 constexpr int PCF_W = 8;
+template <typename JY>
 __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float *__restrict__ W,
                                                      int iz_per_chunk, int n_items, double *__restrict__ partial) {
     extern __shared__ float acc_s[];  // [PCF_W][det_ny]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const JY *pjy = (const JY *)e.pc_jy;
     float *acc = acc_s + warp * p.det_ny;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int chunk = item / p.det_nx, ix = item % p.det_nx;
@@ -684,24 +695,27 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
                 // (memory-level parallelism); the jy of one list are distinct, so
                 // the four accumulator updates never alias
                 for (long long o = o0 + lane; o < o1; o += 128) {
-                    uint32_t k[4];
-                    float2 a[4], wb[4];
+                    uint32_t k[4], jy[4];
+                    float P[4], wa[4], wb[4];
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         const bool in = o + 32 * u < o1;
-                        k[u] = in ? __ldg(e.pc_key + o + 32 * u) : 0u;
-                        a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
+                        k[u] = in ? __ldg(e.pc_bt + o + 32 * u) : 0u;
+                        P[u] = in ? __ldg(e.pc_P + o + 32 * u) : 0.0f;
+                        jy[u] = in ? (uint32_t)__ldg(pjy + o + 32 * u) : 0u;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
-                        const float *wp = Wv + (k[u] & 0xFFFFu);
-                        wb[u] = make_float2(__ldg(wp), __ldg(wp + 1));
+                        const float *wp = Wv + (k[u] >> tb);
+                        wa[u] = __ldg(wp);
+                        wb[u] = __ldg(wp + 1);
                     }
 #pragma unroll
                     for (int u = 0; u < 4; u++)
                         if (o + 32 * u < o1) {
-                            float *ap = acc + (k[u] >> 16);
-                            *ap = fmaf(a[u].x, wb[u].x, fmaf(a[u].y, wb[u].y, *ap));
+                            const float t = (float)(k[u] & tmask) * tunit;
+                            float *ap = acc + jy[u];
+                            *ap = fmaf(P[u], fmaf(t, wb[u] - wa[u], wa[u]), *ap);
                         }
                 }
             }
@@ -718,10 +732,15 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
 // backward from the cache: one CTA per voxel (grid-stride), warps take detector
 // rows, lanes the records; fixed-point deposits as k_esai_bwd (same scale rule)
 constexpr int PCB_T = 256;
+template <typename JY>
 __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, const float *__restrict__ w,
                                                   const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ int hist_s[];  // [max_win]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const JY *pjy = (const JY *)e.pc_jy;
     const float wm = *wmax;
     for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
         const int2 win = e.vwin[v];
@@ -746,24 +765,27 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
             const long long o0 = __shfl_sync(FULL, my0, ri), o1 = __shfl_sync(FULL, my1, ri);
             const float *wr = w + (size_t)ix * p.det_ny;
             for (long long o = o0 + lane; o < o1; o += 128) {
-                uint32_t k[4];
-                float2 a[4];
-                float wq[4];
+                uint32_t k[4], jy[4];
+                float P[4], wq[4];
                 // branch-free: slots past the list end deposit zero into the
                 // window's first bin (a valid address)
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const bool in = o + 32 * u < o1;
-                    k[u] = in ? __ldg(e.pc_key + o + 32 * u) : (uint32_t)win.x;
-                    a[u] = in ? __ldg(e.pc_w + o + 32 * u) : make_float2(0.0f, 0.0f);
+                    k[u] = in ? __ldg(e.pc_bt + o + 32 * u) : ((uint32_t)win.x << tb);
+                    P[u] = in ? __ldg(e.pc_P + o + 32 * u) : 0.0f;
+                    jy[u] = in ? (uint32_t)__ldg(pjy + o + 32 * u) : 0u;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) wq[u] = __ldg(wr + (k[u] >> 16)) * scale;
+                for (int u = 0; u < 4; u++) wq[u] = __ldg(wr + jy[u]) * scale;
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const int b = (int)(k[u] & 0xFFFFu);
-                    atomicAdd(hv + b, __float2int_rn(a[u].x * wq[u]));
-                    atomicAdd(hv + b + 1, __float2int_rn(a[u].y * wq[u]));
+                    // the pair's P w scale split exactly between bins b and b + 1
+                    const int b = (int)(k[u] >> tb);
+                    const float a = P[u] * wq[u];
+                    const int x1 = __float2int_rn(a * ((float)(k[u] & tmask) * tunit));
+                    atomicAdd(hv + b, __float2int_rn(a) - x1);
+                    atomicAdd(hv + b + 1, x1);
                 }
             }
             }
@@ -1099,21 +1121,36 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         const long long nrec = off[nl];
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const size_t need = (size_t)nrec * (sizeof(uint32_t) + sizeof(float2)) + (nl + 1) * sizeof(long long);
-        if (need <= free_b / 2) {
+        const size_t jyb = p.det_ny <= 256 ? 1 : 2;
+        const size_t rec = (size_t)std::max(nrec, 1ll);
+        const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb) + (nl + 1) * sizeof(long long);
+        int bbits = 1;
+        while ((1 << bbits) < E.nb) bbits++;
+        if (need <= free_b / 2 && bbits <= 16) {
             e = cudaMalloc(&g->d_pc_off, (nl + 1) * sizeof(long long));
             if (e == cudaSuccess) e = cudaMemcpy(g->d_pc_off, off.data(), (nl + 1) * sizeof(long long), cudaMemcpyHostToDevice);
-            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_key, (size_t)std::max(nrec, 1ll) * sizeof(uint32_t));
-            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_w, (size_t)std::max(nrec, 1ll) * sizeof(float2));
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_bt, rec * sizeof(uint32_t));
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_P, rec * sizeof(float));
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_jy, rec * jyb);
             if (e != cudaSuccess) return e;
             E.pc_off = (const long long *)g->d_pc_off;
-            E.pc_key = (const uint32_t *)g->d_pc_key;
-            E.pc_w = (const float2 *)g->d_pc_w;
+            E.pc_bt = (const uint32_t *)g->d_pc_bt;
+            E.pc_P = (const float *)g->d_pc_P;
+            E.pc_jy = g->d_pc_jy;
+            E.pc_tbits = std::min(32 - bbits, 24);  // tau's fp32 mantissa carries 24 bits
+            E.pc_jyb = (int)jyb;
             E.pc_n = nrec;
             const size_t smem = host_bp_bytes(E);
-            auto kf = sai ? k_pc_fill<true> : k_pc_fill<false>;
-            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            kf<<<persistent_grid(g, smem, 256), 256, smem>>>(p, E, (uint32_t *)g->d_pc_key, (float2 *)g->d_pc_w);
+            const int gr = persistent_grid(g, smem, 256);
+            if (jyb == 1) {
+                auto kf = sai ? k_pc_fill<true, uint8_t> : k_pc_fill<false, uint8_t>;
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint8_t *)g->d_pc_jy);
+            } else {
+                auto kf = sai ? k_pc_fill<true, uint16_t> : k_pc_fill<false, uint16_t>;
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint16_t *)g->d_pc_jy);
+            }
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
             E.pc = 1;
@@ -1212,8 +1249,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             KScope kt_(g, s, "k_pc_fwd");
             const size_t smem = (size_t)PCF_W * p.det_ny * sizeof(float);
             const int n_items = S * p.det_nx;
-            k_pc_fwd<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, W, izc,
-                                                                                        n_items, part);
+            auto kf = E.pc_jyb == 1 ? k_pc_fwd<uint8_t> : k_pc_fwd<uint16_t>;
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kf<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, W, izc, n_items, part);
         }
     } else if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
@@ -1282,8 +1320,9 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         if (E.pc && pmask == nullptr) {
             KScope kt_(g, s, "k_pc_bwd");
             const size_t hs = (size_t)E.max_win * sizeof(int);
-            cudaFuncSetAttribute(k_pc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
-            k_pc_bwd<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, A);
+            auto kb = E.pc_jyb == 1 ? k_pc_bwd<uint8_t> : k_pc_bwd<uint16_t>;
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+            kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, A);
         } else {
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {

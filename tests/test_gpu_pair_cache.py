@@ -34,6 +34,9 @@ def test_record_count_is_the_open_pair_count(ci, monkeypatch):
     Gc, Gn = handles(cfg.desc(), monkeypatch)
     assert Gc.query("pair_cache_records") == COUNTS[str(cfg.seed)]["open_pairs"]
     assert Gn.query("pair_cache_records") == 0
+    # P (4 B) + packed (b, tau) (4 B) + jy (1 B for det_ny <= 256)
+    assert Gc.query("pair_cache_record_bytes") == 8 + (1 if cfg.det_ny <= 256 else 2)
+    assert Gc.query("pair_cache_tau_bits") >= 16
     Gc.close()
     Gn.close()
 
