@@ -591,6 +591,19 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
     }
 }
 
+// bulk prefetch of [ptr, ptr + bytes) into L2 by the TMA unit (one thread issues
+// it; no registers, no completion to wait for): the next voxel's record ranges
+// are in L2 by the time the CTA's loads reach them
+__device__ __forceinline__ void l2_prefetch(const void *ptr, size_t bytes) {
+    uintptr_t a = (uintptr_t)ptr & ~(uintptr_t)15;
+    const uintptr_t end = ((uintptr_t)ptr + bytes + 15) & ~(uintptr_t)15;
+    while (a < end) {
+        const uint32_t n = (uint32_t)min((uintptr_t)65536, end - a);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+        a += n;
+    }
+}
+
 // ---- pair cache: the online/offline trade-off taken to HBM --
 // Every open pair's interpolation weights into the breakpoint basis depend on
 // the geometry only, so they can be computed ONCE at create and streamed by
@@ -598,12 +611,14 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
 // pixels in increasing jy, each a record of P (fp32), (b, tau) packed in 32 bits
 // (b in the high bits, tau in the remaining >= 16 fraction bits: |tau error| <=
 // 2^-(tbits+1), i.e. a weight error P |dtau| |W_{b+1} - W_b|, below fp32
-// rounding for tbits = 20) and jy (1 byte for det_ny <= 256, else 2): 9 bytes
-// per open pair on config 2 (5.8e8 pairs, 5.2 GB of 180 GB).
+// rounding for tbits = 20) and the pixel q (2 bytes for n_det <= 65536, else
+// 4): 10 bytes per open pair on config 2 (5.8e8 pairs, 5.8 GB of 180 GB).  A
+// voxel's records are contiguous (lists v * det_nx + ix), so both operators
+// stream them flat.
 // The paper precomputes what is cheaper to load than to recompute ("if the cost
 // of computing the factor is equivalent to the speed of loading the factor from
 // main memory, then the computations should be performed online"); on a B200,
-// streaming 9 bytes is cheaper than the ~100 instructions of pair geometry and
+// streaming 10 bytes is cheaper than the ~100 instructions of pair geometry and
 // breakpoint location.  Both operators read the same records: the forward by
 // (z, row, y) with the W gathers of one list on one W row, the backward by
 // voxel.  Built only if it fits (cacsi_query "pair_cache_records" > 0).
@@ -628,9 +643,9 @@ __global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) 
 }
 
 // fill: one warp per list, 32 pixels per step, ballot-compacted records
-template <bool SAI, typename JY>
+template <bool SAI, typename QT>
 __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ bt,
-                                                 float *__restrict__ Pout, JY *__restrict__ jyout) {
+                                                 float *__restrict__ Pout, QT *__restrict__ qout) {
     const float tone = (float)(1u << e.pc_tbits);
     const uint32_t tmax = (1u << e.pc_tbits) - 1u;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -659,7 +674,7 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
                 const long long o = base + __popc(m & ((1u << lane) - 1u));
                 bt[o] = ((uint32_t)b << e.pc_tbits) | min(__float2uint_rn(t * tone), tmax);
                 Pout[o] = P;
-                jyout[o] = (JY)jy;
+                qout[o] = (QT)q;
             }
             base += __popc(m);
         }
@@ -670,7 +685,7 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // y, lanes the list's records; per-warp row accumulators in shared memory (the
 // jy of one list are distinct: conflict-free, no atomics), fp64 partials per z chunk
 constexpr int PCF_W = 8;
-template <typename JY>
+template <typename QT>
 __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float *__restrict__ W,
                                                      int iz_per_chunk, int n_items, double *__restrict__ partial) {
     extern __shared__ float acc_s[];  // [PCF_W][det_ny]
@@ -678,7 +693,7 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
     const int tb = e.pc_tbits;
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
-    const JY *pjy = (const JY *)e.pc_jy;
+    const QT *pq = (const QT *)e.pc_q;
     float *acc = acc_s + warp * p.det_ny;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int chunk = item / p.det_nx, ix = item % p.det_nx;
@@ -702,7 +717,7 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
                         const bool in = o + 32 * u < o1;
                         k[u] = in ? __ldg(e.pc_bt + o + 32 * u) : 0u;
                         P[u] = in ? __ldg(e.pc_P + o + 32 * u) : 0.0f;
-                        jy[u] = in ? (uint32_t)__ldg(pjy + o + 32 * u) : 0u;
+                        jy[u] = in ? (uint32_t)__ldg(pq + o + 32 * u) - (uint32_t)(ix * p.det_ny) : 0u;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
@@ -729,18 +744,109 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
     }
 }
 
-// backward from the cache: one CTA per voxel (grid-stride), warps take detector
-// rows, lanes the records; fixed-point deposits as k_esai_bwd (same scale rule)
-constexpr int PCB_T = 256;
-template <typename JY>
-__global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, const float *__restrict__ w,
-                                                  const float *__restrict__ wmax, float *__restrict__ A) {
-    extern __shared__ int hist_s[];  // [max_win]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// forward from the cache, voxel-major: items (voxel chunk, block of R detector
+// rows), chunks of consecutive voxels; per voxel the CTA holds the voxel's W
+// window in shared memory (one cp.async.bulk per voxel, issued a voxel ahead
+// into the other of two buffers, completion on an mbarrier) and streams the
+// voxel's records of those rows -- one contiguous range -- 4 per thread per
+// step; the W reads are shared-memory gathers and each record adds into the
+// CTA's row-block accumulator acc[q - q0].  The pixels of one voxel's records
+// are distinct (no two updates of one voxel alias); voxels are separated by a
+// barrier, so the sums are plain fp32 in a fixed order (deterministic).
+constexpr int PCV_T = 512;
+__device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, float *dst, uint64_t *mbar) {
+    const int2 win = e.vwin[v];
+    const int a = win.x & ~3;
+    const uint32_t bytes = (uint32_t)(((win.y + 1 - a) + 3) & ~3) * 4u;
+    const uint32_t mb = smem_u32(mbar);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(W + (size_t)v * e.ldw + a), "r"(bytes), "r"(mb)
+                 : "memory");
+}
+template <typename QT>
+__global__ void __launch_bounds__(PCV_T, 2) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
+                                                     int R, int vchunk, int n_rb, int n_items, int pf,
+                                                     double *__restrict__ partial) {
+    extern __shared__ __align__(16) float smv[];
+    const int wcap = (e.max_win + 3 + 3) & ~3;
+    float *acc = smv;                                   // [R * det_ny]
+    float *ws = smv + ((R * p.det_ny + 3) & ~3);        // [2][wcap]
+    uint64_t *mbar = (uint64_t *)(ws + 2 * wcap);       // [2]
+    const int tid = threadIdx.x;
     const int tb = e.pc_tbits;
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
-    const JY *pjy = (const JY *)e.pc_jy;
+    const QT *pq = (const QT *)e.pc_q;
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    __syncthreads();
+    uint32_t uses = 0;  // bit i: parity of buffer i's next completion
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int c = item / n_rb, rb = item % n_rb;
+        const int r0 = rb * R, r1 = min(p.det_nx, r0 + R);
+        const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);
+        const int q0 = r0 * p.det_ny, nacc = (r1 - r0) * p.det_ny;
+        for (int i = tid; i < nacc; i += PCV_T) acc[i] = 0.0f;
+        if (tid == 0) pcv_stage(e, W, v0, ws, mbar);
+        for (int v = v0; v < v1; v++) {
+            const int buf = (v - v0) & 1;
+            if (tid == 0 && v + 1 < v1) pcv_stage(e, W, v + 1, ws + (buf ^ 1) * wcap, mbar + (buf ^ 1));
+            const size_t l0 = (size_t)v * p.det_nx;
+            const long long o0 = __ldg(e.pc_off + l0 + r0), o1 = __ldg(e.pc_off + l0 + r1);
+            if (tid == 0 && pf > 0 && v + pf < v1) {
+                const size_t l2 = (size_t)(v + pf) * p.det_nx;
+                const long long a0 = __ldg(e.pc_off + l2 + r0), a1 = __ldg(e.pc_off + l2 + r1);
+                l2_prefetch(e.pc_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
+                l2_prefetch(e.pc_P + a0, (size_t)(a1 - a0) * sizeof(float));
+                l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
+            }
+            mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
+            uses ^= 1u << buf;
+            const float *wv = ws + buf * wcap - (e.vwin[v].x & ~3);
+            for (long long o = o0 + tid; o < o1; o += 4 * PCV_T) {
+                uint32_t k[4], q[4];
+                float P[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const bool in = o + u * PCV_T < o1;
+                    k[u] = in ? __ldg(e.pc_bt + o + u * PCV_T) : 0u;
+                    P[u] = in ? __ldg(e.pc_P + o + u * PCV_T) : 0.0f;
+                    q[u] = in ? (uint32_t)__ldg(pq + o + u * PCV_T) : (uint32_t)q0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (o + u * PCV_T < o1) {
+                        const int b = (int)(k[u] >> tb);
+                        const float wa = wv[b], wb = wv[b + 1];
+                        const float t = (float)(k[u] & tmask) * tunit;
+                        float *ap = acc + (q[u] - (uint32_t)q0);
+                        *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
+                    }
+            }
+            __syncthreads();
+        }
+        for (int i = tid; i < nacc; i += PCV_T) partial[(size_t)c * p.n_det + q0 + i] = (double)acc[i];
+        __syncthreads();
+    }
+}
+
+// backward from the cache: one CTA per voxel (grid-stride), warps take detector
+// rows, lanes the records; fixed-point deposits as k_esai_bwd (same scale rule)
+constexpr int PCB_T = 256;
+template <typename QT>
+__global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, const float *__restrict__ w,
+                                                  const float *__restrict__ wmax, int pf, float *__restrict__ A) {
+    extern __shared__ int hist_s[];  // [max_win]
+    const int tid = threadIdx.x;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pc_q;
     const float wm = *wmax;
     for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
         const int2 win = e.vwin[v];
@@ -751,43 +857,39 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
         const double bound = (double)e.vbound[v] * (double)wm;
         const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
         int *hv = hist_s - win.x;
-        // the warp's rows ix = warp, warp + 8, ...: 32 at a time, lane i loads row i's bounds
-        const int n_rows = scale > 0.0f ? (p.det_nx - warp + PCB_T / 32 - 1) / (PCB_T / 32) : 0;
-        for (int rb = 0; rb < n_rows; rb += 32) {
-            long long my0 = 0, my1 = 0;
-            if (rb + lane < n_rows) {
-                const size_t list = (size_t)v * p.det_nx + warp + (rb + lane) * (PCB_T / 32);
-                my0 = __ldg(e.pc_off + list);
-                my1 = __ldg(e.pc_off + list + 1);
-            }
-            for (int ri = 0; ri < min(32, n_rows - rb); ri++) {
-            const int ix = warp + (rb + ri) * (PCB_T / 32);
-            const long long o0 = __shfl_sync(FULL, my0, ri), o1 = __shfl_sync(FULL, my1, ri);
-            const float *wr = w + (size_t)ix * p.det_ny;
-            for (long long o = o0 + lane; o < o1; o += 128) {
-                uint32_t k[4], jy[4];
-                float P[4], wq[4];
-                // branch-free: slots past the list end deposit zero into the
-                // window's first bin (a valid address)
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const bool in = o + 32 * u < o1;
-                    k[u] = in ? __ldg(e.pc_bt + o + 32 * u) : ((uint32_t)win.x << tb);
-                    P[u] = in ? __ldg(e.pc_P + o + 32 * u) : 0.0f;
-                    jy[u] = in ? (uint32_t)__ldg(pjy + o + 32 * u) : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) wq[u] = __ldg(wr + jy[u]) * scale;
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    // the pair's P w scale split exactly between bins b and b + 1
-                    const int b = (int)(k[u] >> tb);
-                    const float a = P[u] * wq[u];
-                    const int x1 = __float2int_rn(a * ((float)(k[u] & tmask) * tunit));
-                    atomicAdd(hv + b, __float2int_rn(a) - x1);
-                    atomicAdd(hv + b + 1, x1);
+        // the voxel's records (all its lists) are one contiguous range, streamed flat
+        const long long o0 = __ldg(e.pc_off + (size_t)v * p.det_nx);
+        const long long o1 = scale > 0.0f ? __ldg(e.pc_off + (size_t)(v + 1) * p.det_nx) : o0;
+        for (long long o = o0 + tid; o < o1; o += 4 * PCB_T) {
+            if (tid == 0 && pf > 0) {
+                // rolling L2 prefetch of the records pf steps ahead
+                const long long a0 = o + (long long)pf * 4 * PCB_T, a1 = min(o1, a0 + 4 * PCB_T);
+                if (a0 < a1) {
+                    l2_prefetch(e.pc_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
+                    l2_prefetch(e.pc_P + a0, (size_t)(a1 - a0) * sizeof(float));
+                    l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
                 }
             }
+            uint32_t k[4], q[4];
+            float P[4], wq[4];
+            // branch-free: slots past the end deposit zero into the window's first bin
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool in = o + u * PCB_T < o1;
+                k[u] = in ? __ldg(e.pc_bt + o + u * PCB_T) : ((uint32_t)win.x << tb);
+                P[u] = in ? __ldg(e.pc_P + o + u * PCB_T) : 0.0f;
+                q[u] = in ? (uint32_t)__ldg(pq + o + u * PCB_T) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) wq[u] = __ldg(w + q[u]) * scale;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                // the pair's P w scale split exactly between bins b and b + 1
+                const int b = (int)(k[u] >> tb);
+                const float a = P[u] * wq[u];
+                const int x1 = __float2int_rn(a * ((float)(k[u] & tmask) * tunit));
+                atomicAdd(hv + b, __float2int_rn(a) - x1);
+                atomicAdd(hv + b + 1, x1);
             }
         }
         __syncthreads();
@@ -1121,7 +1223,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         const long long nrec = off[nl];
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const size_t jyb = p.det_ny <= 256 ? 1 : 2;
+        const size_t jyb = p.n_det <= 65536 ? 2 : 4;
         const size_t rec = (size_t)std::max(nrec, 1ll);
         const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb) + (nl + 1) * sizeof(long long);
         int bbits = 1;
@@ -1131,25 +1233,25 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             if (e == cudaSuccess) e = cudaMemcpy(g->d_pc_off, off.data(), (nl + 1) * sizeof(long long), cudaMemcpyHostToDevice);
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_bt, rec * sizeof(uint32_t));
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_P, rec * sizeof(float));
-            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_jy, rec * jyb);
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_q, rec * jyb);
             if (e != cudaSuccess) return e;
             E.pc_off = (const long long *)g->d_pc_off;
             E.pc_bt = (const uint32_t *)g->d_pc_bt;
             E.pc_P = (const float *)g->d_pc_P;
-            E.pc_jy = g->d_pc_jy;
+            E.pc_q = g->d_pc_q;
             E.pc_tbits = std::min(32 - bbits, 24);  // tau's fp32 mantissa carries 24 bits
-            E.pc_jyb = (int)jyb;
+            E.pc_qb = (int)jyb;
             E.pc_n = nrec;
             const size_t smem = host_bp_bytes(E);
             const int gr = persistent_grid(g, smem, 256);
-            if (jyb == 1) {
-                auto kf = sai ? k_pc_fill<true, uint8_t> : k_pc_fill<false, uint8_t>;
-                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint8_t *)g->d_pc_jy);
-            } else {
+            if (jyb == 2) {
                 auto kf = sai ? k_pc_fill<true, uint16_t> : k_pc_fill<false, uint16_t>;
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint16_t *)g->d_pc_jy);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint16_t *)g->d_pc_q);
+            } else {
+                auto kf = sai ? k_pc_fill<true, uint32_t> : k_pc_fill<false, uint32_t>;
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint32_t *)g->d_pc_q);
             }
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
@@ -1240,7 +1342,32 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         cudaFreeAsync(W, s);
         return e;
     } else if (E.pc) {
-        // pair cache: items (z chunk, detector row), fp64 partials per z chunk
+        const int wcap = (E.max_win + 3 + 3) & ~3;
+        const size_t budget = 108 * 1024;  // two CTAs per SM
+        const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
+        const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
+        const char *pv = getenv("CACSI_PC_FWD");
+        if (r_max >= 1 && !(pv && strcmp(pv, "list") == 0)) {
+            // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
+            const int n_rb = (p.det_nx + r_max - 1) / r_max;
+            const int R = (p.det_nx + n_rb - 1) / n_rb;
+            int Sv = std::max(1, std::min(p.n_vox, (8 * sm_count(g->device) + n_rb - 1) / n_rb));
+            const int vchunk = (p.n_vox + Sv - 1) / Sv;
+            S = (p.n_vox + vchunk - 1) / vchunk;
+            e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
+            if (e == cudaSuccess) {
+                KScope kt_(g, s, "k_pc_fwd");
+                const size_t smem = ((size_t)((R * p.det_ny + 3) & ~3) + 2 * (size_t)wcap) * sizeof(float) + 16;
+                const char *pfs = getenv("CACSI_PCV_PF");  // tuning knob (voxels ahead)
+                const int pf = pfs ? atoi(pfs) : 1;
+                const int n_items = S * n_rb;
+                auto kf = E.pc_qb == 2 ? k_pc_fwd_v<uint16_t> : k_pc_fwd_v<uint32_t>;
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kf<<<std::min(n_items, 2 * sm_count(g->device)), PCV_T, smem, s>>>(p, E, W, R, vchunk, n_rb, n_items,
+                                                                                   pf, part);
+            }
+        } else {
+        // pair cache, per list: items (z chunk, detector row), fp64 partials per z chunk
         int izc = std::max(1, (p.nz * p.det_nx) / (8 * sm_count(g->device) * 4));  // >= ~4 items per resident CTA
         izc = std::min(izc, p.nz);
         S = (p.nz + izc - 1) / izc;
@@ -1249,9 +1376,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             KScope kt_(g, s, "k_pc_fwd");
             const size_t smem = (size_t)PCF_W * p.det_ny * sizeof(float);
             const int n_items = S * p.det_nx;
-            auto kf = E.pc_jyb == 1 ? k_pc_fwd<uint8_t> : k_pc_fwd<uint16_t>;
+            auto kf = E.pc_qb == 2 ? k_pc_fwd<uint16_t> : k_pc_fwd<uint32_t>;
             cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             kf<<<std::min(n_items, 16 * sm_count(g->device)), PCF_W * 32, smem, s>>>(p, E, W, izc, n_items, part);
+        }
         }
     } else if (p.ts_rho > 0) {
         const int segs = (p.det_ny + TS_T - 1) / TS_T;
@@ -1320,9 +1448,11 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         if (E.pc && pmask == nullptr) {
             KScope kt_(g, s, "k_pc_bwd");
             const size_t hs = (size_t)E.max_win * sizeof(int);
-            auto kb = E.pc_jyb == 1 ? k_pc_bwd<uint8_t> : k_pc_bwd<uint16_t>;
+            const char *pfs = getenv("CACSI_PCB_PF");  // tuning knob (steps ahead)
+            const int pf = pfs ? atoi(pfs) : 2;
+            auto kb = E.pc_qb == 2 ? k_pc_bwd<uint16_t> : k_pc_bwd<uint32_t>;
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
-            kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, A);
+            kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, pf, A);
         } else {
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {

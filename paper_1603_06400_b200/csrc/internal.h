@@ -92,9 +92,9 @@ struct Esai {
     const long long *pc_off;  // [n_vox * det_nx + 1] first record of list (v, ix)
     const uint32_t *pc_bt;    // (b << pc_tbits) | round(tau 2^pc_tbits)
     const float *pc_P;        // P (the pair's geometric-spectral factor, transmission included)
-    const void *pc_jy;        // jy, uint8 (det_ny <= 256) or uint16
+    const void *pc_q;         // pixel q, uint16 (n_det <= 65536) or uint32
     int pc_tbits;             // fraction bits of tau (>= 16)
-    int pc_jyb;               // bytes per jy (1 or 2)
+    int pc_qb;                // bytes per q (2 or 4)
 };
 
 }  // namespace cacsi
@@ -110,7 +110,7 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_jy, *d_tc_w1;
+        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     mutable int32_t last_launches;

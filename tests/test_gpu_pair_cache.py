@@ -34,8 +34,8 @@ def test_record_count_is_the_open_pair_count(ci, monkeypatch):
     Gc, Gn = handles(cfg.desc(), monkeypatch)
     assert Gc.query("pair_cache_records") == COUNTS[str(cfg.seed)]["open_pairs"]
     assert Gn.query("pair_cache_records") == 0
-    # P (4 B) + packed (b, tau) (4 B) + jy (1 B for det_ny <= 256)
-    assert Gc.query("pair_cache_record_bytes") == 8 + (1 if cfg.det_ny <= 256 else 2)
+    # P (4 B) + packed (b, tau) (4 B) + pixel q (2 B for n_det <= 65536)
+    assert Gc.query("pair_cache_record_bytes") == 8 + (2 if cfg.n_det <= 65536 else 4)
     assert Gc.query("pair_cache_tau_bits") >= 16
     Gc.close()
     Gn.close()
@@ -82,4 +82,21 @@ def test_sai_without_cache(monkeypatch):
     assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), "c1 SAI on-the-fly forward")
     w = rnd(G.g_shape, 1, 72)
     assert_parity(gpu_backward(G, w), O.backward(w), "c1 SAI on-the-fly backward")
+    G.close()
+
+
+def test_per_list_forward_config1(monkeypatch):
+    """The per-list pair-cache forward (used when the voxel-major kernel's
+    shared-memory window does not fit; CACSI_PC_FWD=list forces it) against
+    the oracle and against the voxel-major kernel."""
+    cfg = make_config(1)
+    O = oracle.Geometry(cfg)
+    G = P.Geometry(cfg.desc())
+    assert G.query("pair_cache_records") > 0
+    gv = gpu_forward(G, cfg.f)
+    monkeypatch.setenv("CACSI_PC_FWD", "list")
+    gl = gpu_forward(G, cfg.f)
+    monkeypatch.delenv("CACSI_PC_FWD")
+    assert_parity(gl, O.forward(cfg.f), "c1 per-list cache forward")
+    assert_parity(gl, gv, "c1 per-list vs voxel-major forward", l2=1e-6, mr=1e-5)
     G.close()
