@@ -753,21 +753,19 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
 // CTA's row-block accumulator acc[q - q0].  The pixels of one voxel's records
 // are distinct (no two updates of one voxel alias); voxels are separated by a
 // barrier, so the sums are plain fp32 in a fixed order (deterministic).
-constexpr int PCV_T = 512;
 __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, float *dst, uint64_t *mbar) {
     const int2 win = e.vwin[v];
     const int a = win.x & ~3;
     const uint32_t bytes = (uint32_t)(((win.y + 1 - a) + 3) & ~3) * 4u;
     const uint32_t mb = smem_u32(mbar);
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)),
                  "l"(W + (size_t)v * e.ldw + a), "r"(bytes), "r"(mb)
                  : "memory");
 }
-template <typename QT>
-__global__ void __launch_bounds__(PCV_T, 2) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
+template <typename QT, int U, int PCV_T>
+__global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
     extern __shared__ __align__(16) float smv[];
@@ -808,18 +806,18 @@ __global__ void __launch_bounds__(PCV_T, 2) k_pc_fwd_v(const Params p, const Esa
             mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
             uses ^= 1u << buf;
             const float *wv = ws + buf * wcap - (e.vwin[v].x & ~3);
-            for (long long o = o0 + tid; o < o1; o += 4 * PCV_T) {
-                uint32_t k[4], q[4];
-                float P[4];
+            for (long long o = o0 + tid; o < o1; o += U * PCV_T) {
+                uint32_t k[U], q[U];
+                float P[U];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < U; u++) {
                     const bool in = o + u * PCV_T < o1;
                     k[u] = in ? __ldg(e.pc_bt + o + u * PCV_T) : 0u;
                     P[u] = in ? __ldg(e.pc_P + o + u * PCV_T) : 0.0f;
                     q[u] = in ? (uint32_t)__ldg(pq + o + u * PCV_T) : (uint32_t)q0;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++)
+                for (int u = 0; u < U; u++)
                     if (o + u * PCV_T < o1) {
                         const int b = (int)(k[u] >> tb);
                         const float wa = wv[b], wb = wv[b + 1];
@@ -828,6 +826,9 @@ __global__ void __launch_bounds__(PCV_T, 2) k_pc_fwd_v(const Params p, const Esa
                         *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                     }
             }
+            // this thread's reads of the W buffer (generic proxy) before its next
+            // bulk copy (async proxy), then the barrier that hands it to thread 0
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncthreads();
         }
         for (int i = tid; i < nacc; i += PCV_T) partial[(size_t)c * p.n_det + q0 + i] = (double)acc[i];
@@ -899,6 +900,125 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
             const int i = b - win.x;
             Ar[b] = (i >= 0 && i < nwin) ? (float)hist_s[i] * unit : 0.0f;
         }
+    }
+}
+
+// backward from the cache with the records fed through shared memory: thread 0
+// streams the CTA's chunks (PBT_CH records, 16-byte-aligned groups of 8) with
+// cp.async.bulk into a PBT_NS-stage ring ("full" mbarrier: bytes landed;
+// "empty" mbarrier: every warp has read the stage), PBT_NS - 1 chunks ahead of
+// the consumers and across voxel boundaries; the threads only gather w and
+// deposit.  Same deposits and order-free integer sums as k_pc_bwd.
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS>
+__global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
+                                                      const float *__restrict__ wmax, float *__restrict__ A) {
+    extern __shared__ __align__(16) unsigned char smb[];
+    constexpr int PBT_CH = PBT_T * PBT_U;
+    constexpr int SB = PBT_CH * (8 + (int)sizeof(QT));
+    uint64_t *full = (uint64_t *)(smb + PBT_NS * SB);
+    uint64_t *empty = full + PBT_NS;
+    int *hist_s = (int *)(empty + PBT_NS);
+    const int tid = threadIdx.x;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pc_q;
+    const float wm = *wmax;
+    if (tid == 0) {
+        for (int i = 0; i < PBT_NS; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(PBT_T));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    __syncthreads();
+    // producer state (thread 0): voxel pv, next chunk start pa, range end pe, chunks issued
+    int pv = blockIdx.x;
+    long long pa = 0, pe = 0;
+    uint32_t issued = 0;
+    if (tid == 0 && pv < p.n_vox) {
+        pa = __ldg(e.pc_off + (size_t)pv * p.det_nx) & ~7ll;
+        pe = __ldg(e.pc_off + (size_t)(pv + 1) * p.det_nx);
+    }
+    auto produce = [&](uint32_t limit) {
+        while (issued < limit) {
+            while (pv < p.n_vox && pa >= pe) {
+                pv += gridDim.x;
+                if (pv < p.n_vox) {
+                    pa = __ldg(e.pc_off + (size_t)pv * p.det_nx) & ~7ll;
+                    pe = __ldg(e.pc_off + (size_t)(pv + 1) * p.det_nx);
+                }
+            }
+            if (pv >= p.n_vox) return;
+            const int st = issued % PBT_NS;
+            const uint32_t use = issued / PBT_NS;
+            if (use > 0) mbar_wait(smem_u32(empty + st), (use - 1) & 1);
+            const uint32_t n = (uint32_t)((min((long long)PBT_CH, pe - pa) + 7) & ~7ll);
+            const uint32_t mb = smem_u32(full + st);
+            unsigned char *dst = smb + st * SB;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"(n * (8u + (uint32_t)sizeof(QT))));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst)), "l"(e.pc_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst + PBT_CH * 4)), "l"(e.pc_P + pa), "r"(n * 4u), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
+            pa += PBT_CH;
+            issued++;
+        }
+    };
+    if (tid == 0) produce(PBT_NS - 1);
+    uint32_t consumed = 0;
+    for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        for (int i = tid; i < nwin; i += PBT_T) hist_s[i] = 0;
+        __syncthreads();
+        const double bound = (double)e.vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+        int *hv = hist_s - win.x;
+        const long long o0 = __ldg(e.pc_off + (size_t)v * p.det_nx), o1 = __ldg(e.pc_off + (size_t)(v + 1) * p.det_nx);
+        for (long long a = o0 & ~7ll; a < o1; a += PBT_CH) {
+            if (tid == 0) produce(consumed + PBT_NS);
+            const int st = consumed % PBT_NS;
+            mbar_wait(smem_u32(full + st), (consumed / PBT_NS) & 1);
+            const unsigned char *src = smb + st * SB;
+            uint32_t k[PBT_U], q[PBT_U];
+            float P[PBT_U];
+#pragma unroll
+            for (int u = 0; u < PBT_U; u++) {
+                const int i = tid + u * PBT_T;
+                const bool in = a + i >= o0 && a + i < o1;
+                k[u] = in ? ((const uint32_t *)src)[i] : ((uint32_t)win.x << tb);
+                P[u] = in ? ((const float *)(src + PBT_CH * 4))[i] : 0.0f;
+                q[u] = in ? (uint32_t)((const QT *)(src + PBT_CH * 8))[i] : 0u;
+            }
+            // every thread releases its own reads: the proxy fence orders them (generic
+            // proxy) before the next bulk copy into the stage (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + st)) : "memory");
+            consumed++;
+            float wq[PBT_U];
+#pragma unroll
+            for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]) * scale;
+#pragma unroll
+            for (int u = 0; u < PBT_U; u++) {
+                const int b = (int)(k[u] >> tb);
+                const float av = P[u] * wq[u];
+                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                atomicAdd(hv + b, __float2int_rn(av) - x1);
+                atomicAdd(hv + b + 1, x1);
+            }
+        }
+        __syncthreads();
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = tid; b < e.ldw; b += PBT_T) {
+            const int i = b - win.x;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist_s[i] * unit : 0.0f;
+        }
+        __syncthreads();
     }
 }
 
@@ -1224,7 +1344,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
         const size_t jyb = p.n_det <= 65536 ? 2 : 4;
-        const size_t rec = (size_t)std::max(nrec, 1ll);
+        // + 8 records of padding: bulk copies read whole 8-record groups (16-byte aligned)
+        const size_t rec = (size_t)std::max(nrec, 1ll) + 8;
         const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb) + (nl + 1) * sizeof(long long);
         int bbits = 1;
         while ((1 << bbits) < E.nb) bbits++;
@@ -1343,7 +1464,8 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         return e;
     } else if (E.pc) {
         const int wcap = (E.max_win + 3 + 3) & ~3;
-        const size_t budget = 108 * 1024;  // two CTAs per SM
+        const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
+        const size_t budget = (bs ? atoi(bs) : 108) * 1024;  // two CTAs per SM
         const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
         const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
         const char *pv = getenv("CACSI_PC_FWD");
@@ -1351,7 +1473,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
             const int n_rb = (p.det_nx + r_max - 1) / r_max;
             const int R = (p.det_nx + n_rb - 1) / n_rb;
-            int Sv = std::max(1, std::min(p.n_vox, (8 * sm_count(g->device) + n_rb - 1) / n_rb));
+            const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
+            const int ipsm = is ? atoi(is) : 8;
+            int Sv = std::max(1, std::min(p.n_vox, (ipsm * sm_count(g->device) + n_rb - 1) / n_rb));
             const int vchunk = (p.n_vox + Sv - 1) / Sv;
             S = (p.n_vox + vchunk - 1) / vchunk;
             e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
@@ -1361,10 +1485,16 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const char *pfs = getenv("CACSI_PCV_PF");  // tuning knob (voxels ahead)
                 const int pf = pfs ? atoi(pfs) : 1;
                 const int n_items = S * n_rb;
-                auto kf = E.pc_qb == 2 ? k_pc_fwd_v<uint16_t> : k_pc_fwd_v<uint32_t>;
+                const char *us = getenv("CACSI_PCV_U");  // tuning knob (records per thread per step)
+                const int U = us ? atoi(us) : 4;
+                const int cps = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
+                const int T = cps == 1 ? 1024 : 512;
+                auto kf = E.pc_qb == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024>
+                                                    : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512> : k_pc_fwd_v<uint16_t, 4, 512>)
+                                       : (T == 1024 ? k_pc_fwd_v<uint32_t, 4, 1024> : k_pc_fwd_v<uint32_t, 4, 512>);
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<std::min(n_items, 2 * sm_count(g->device)), PCV_T, smem, s>>>(p, E, W, R, vchunk, n_rb, n_items,
-                                                                                   pf, part);
+                kf<<<std::min(n_items, cps * sm_count(g->device)), T, smem, s>>>(p, E, W, R, vchunk, n_rb,
+                                                                                 n_items, pf, part);
             }
         } else {
         // pair cache, per list: items (z chunk, detector row), fp64 partials per z chunk
@@ -1448,11 +1578,24 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         if (E.pc && pmask == nullptr) {
             KScope kt_(g, s, "k_pc_bwd");
             const size_t hs = (size_t)E.max_win * sizeof(int);
+            const char *bv = getenv("CACSI_PC_BWD");  // "flat": the register-fed kernel (A/B reference)
+            if (!(bv && strcmp(bv, "flat") == 0)) {
+                // 256 threads x 3 records, two stages: ~49 KB of shared memory with the
+                // histogram, four CTAs per SM (measured best of 10 ring shapes)
+                constexpr int T = 256, U = 3, NS = 2;
+                auto kb = E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
+                const size_t sm = (size_t)NS * T * U * (8 + E.pc_qb) + 2 * NS * sizeof(uint64_t) + hs;
+                cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                int nb = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, T, sm);
+                kb<<<std::min(p.n_vox, std::max(1, nb) * sm_count(g->device)), T, sm, s>>>(p, E, w, wmax, A);
+            } else {
             const char *pfs = getenv("CACSI_PCB_PF");  // tuning knob (steps ahead)
             const int pf = pfs ? atoi(pfs) : 2;
             auto kb = E.pc_qb == 2 ? k_pc_bwd<uint16_t> : k_pc_bwd<uint32_t>;
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
             kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, pf, A);
+            }
         } else {
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {

@@ -105,7 +105,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
         "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
-        "r"(phase));
+        "r"(phase)
+        : "memory");  // no shared-memory access may move above the wait
 }
 
 // C[z] (rows < M, columns < N) = A * B^T over k-chunks [z * cps, min(nkc, (z+1) * cps)).
