@@ -784,12 +784,16 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     }
     __syncthreads();
     uint32_t uses = 0;  // bit i: parity of buffer i's next completion
+    // gridDim.x = G n_rb: the CTA keeps ONE row block (blockIdx.x % n_rb) for all its
+    // voxel chunks, accumulates them in shared memory and writes one fp64 partial
+    // (index blockIdx.x / n_rb) at the end -- G partials, not one per chunk
+    const int rb = blockIdx.x % n_rb;
+    const int r0 = rb * R, r1 = min(p.det_nx, r0 + R);
+    const int q0 = r0 * p.det_ny, nacc = (r1 - r0) * p.det_ny;
+    for (int i = tid; i < nacc; i += PCV_T) acc[i] = 0.0f;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int c = item / n_rb, rb = item % n_rb;
-        const int r0 = rb * R, r1 = min(p.det_nx, r0 + R);
+        const int c = item / n_rb;
         const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);
-        const int q0 = r0 * p.det_ny, nacc = (r1 - r0) * p.det_ny;
-        for (int i = tid; i < nacc; i += PCV_T) acc[i] = 0.0f;
         if (tid == 0) pcv_stage(e, W, v0, ws, mbar);
         for (int v = v0; v < v1; v++) {
             const int buf = (v - v0) & 1;
@@ -806,34 +810,47 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
             uses ^= 1u << buf;
             const float *wv = ws + buf * wcap - (e.vwin[v].x & ~3);
-            for (long long o = o0 + tid; o < o1; o += U * PCV_T) {
+            float *accq = acc - q0;
+            // 32-bit indices from the voxel's first record; full steps unchecked, then the tail
+            const uint32_t *kb = e.pc_bt + o0;
+            const float *Pb = e.pc_P + o0;
+            const QT *qb = pq + o0;
+            const int n = (int)(o1 - o0);
+            int i = tid;
+            for (; i + (U - 1) * PCV_T < n; i += U * PCV_T) {
                 uint32_t k[U], q[U];
                 float P[U];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    const bool in = o + u * PCV_T < o1;
-                    k[u] = in ? __ldg(e.pc_bt + o + u * PCV_T) : 0u;
-                    P[u] = in ? __ldg(e.pc_P + o + u * PCV_T) : 0.0f;
-                    q[u] = in ? (uint32_t)__ldg(pq + o + u * PCV_T) : (uint32_t)q0;
+                    k[u] = __ldg(kb + i + u * PCV_T);
+                    P[u] = __ldg(Pb + i + u * PCV_T);
+                    q[u] = (uint32_t)__ldg(qb + i + u * PCV_T);
                 }
 #pragma unroll
-                for (int u = 0; u < U; u++)
-                    if (o + u * PCV_T < o1) {
-                        const int b = (int)(k[u] >> tb);
-                        const float wa = wv[b], wb = wv[b + 1];
-                        const float t = (float)(k[u] & tmask) * tunit;
-                        float *ap = acc + (q[u] - (uint32_t)q0);
-                        *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
-                    }
+                for (int u = 0; u < U; u++) {
+                    const int b = (int)(k[u] >> tb);
+                    const float wa = wv[b], wb = wv[b + 1];
+                    const float t = (float)(k[u] & tmask) * tunit;
+                    float *ap = accq + q[u];
+                    *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
+                }
+            }
+            for (; i < n; i += PCV_T) {
+                const uint32_t k = __ldg(kb + i);
+                const float P = __ldg(Pb + i);
+                const int b = (int)(k >> tb);
+                const float wa = wv[b], wb = wv[b + 1];
+                const float t = (float)(k & tmask) * tunit;
+                float *ap = accq + __ldg(qb + i);
+                *ap = fmaf(P, fmaf(t, wb - wa, wa), *ap);
             }
             // this thread's reads of the W buffer (generic proxy) before its next
             // bulk copy (async proxy), then the barrier that hands it to thread 0
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncthreads();
         }
-        for (int i = tid; i < nacc; i += PCV_T) partial[(size_t)c * p.n_det + q0 + i] = (double)acc[i];
-        __syncthreads();
     }
+    for (int i = tid; i < nacc; i += PCV_T) partial[(size_t)(blockIdx.x / n_rb) * p.n_det + q0 + i] = (double)acc[i];
 }
 
 // backward from the cache: one CTA per voxel (grid-stride), warps take detector
@@ -1465,7 +1482,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     } else if (E.pc) {
         const int wcap = (E.max_win + 3 + 3) & ~3;
         const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
-        const size_t budget = (bs ? atoi(bs) : 108) * 1024;  // two CTAs per SM
+        // one 1024-thread CTA per SM with a large row block (fewer W window re-stagings,
+        // longer per-voxel record runs) measured faster than two 512-thread CTAs
+        const size_t budget = (bs ? atoi(bs) : 200) * 1024;
         const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
         const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
         const char *pv = getenv("CACSI_PC_FWD");
@@ -1474,27 +1493,29 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             const int n_rb = (p.det_nx + r_max - 1) / r_max;
             const int R = (p.det_nx + n_rb - 1) / n_rb;
             const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
-            const int ipsm = is ? atoi(is) : 8;
+            const int ipsm = is ? atoi(is) : 4;
             int Sv = std::max(1, std::min(p.n_vox, (ipsm * sm_count(g->device) + n_rb - 1) / n_rb));
             const int vchunk = (p.n_vox + Sv - 1) / Sv;
-            S = (p.n_vox + vchunk - 1) / vchunk;
+            const int n_chunks = (p.n_vox + vchunk - 1) / vchunk;
+            const size_t smem = ((size_t)((R * p.det_ny + 3) & ~3) + 2 * (size_t)wcap) * sizeof(float) + 16;
+            const int cps = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
+            // G CTAs per row block, each owning n_chunks / G voxel chunks: G partials
+            const int G = std::max(1, std::min(n_chunks, cps * sm_count(g->device) / n_rb));
+            S = G;
             e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
             if (e == cudaSuccess) {
                 KScope kt_(g, s, "k_pc_fwd");
-                const size_t smem = ((size_t)((R * p.det_ny + 3) & ~3) + 2 * (size_t)wcap) * sizeof(float) + 16;
                 const char *pfs = getenv("CACSI_PCV_PF");  // tuning knob (voxels ahead)
                 const int pf = pfs ? atoi(pfs) : 1;
-                const int n_items = S * n_rb;
+                const int n_items = n_chunks * n_rb;
                 const char *us = getenv("CACSI_PCV_U");  // tuning knob (records per thread per step)
                 const int U = us ? atoi(us) : 4;
-                const int cps = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
                 const int T = cps == 1 ? 1024 : 512;
                 auto kf = E.pc_qb == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024>
                                                     : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512> : k_pc_fwd_v<uint16_t, 4, 512>)
                                        : (T == 1024 ? k_pc_fwd_v<uint32_t, 4, 1024> : k_pc_fwd_v<uint32_t, 4, 512>);
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<std::min(n_items, cps * sm_count(g->device)), T, smem, s>>>(p, E, W, R, vchunk, n_rb,
-                                                                                 n_items, pf, part);
+                kf<<<G * n_rb, T, smem, s>>>(p, E, W, R, vchunk, n_rb, n_items, pf, part);
             }
         } else {
         // pair cache, per list: items (z chunk, detector row), fp64 partials per z chunk

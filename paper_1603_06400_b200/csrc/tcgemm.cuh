@@ -215,9 +215,15 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     asm volatile("tcgen05.fence::after_thread_sync;\n");
 
     // ---- epilogue: TMEM -> registers -> global (warp w reads lanes 32w..32w+31)
-    const int orow = m0 + warp * 32 + (tid & 31);
     if (!PAIRS) {
+        // each warp transposes its 32 rows x 32 columns through a [32][33] shared
+        // buffer (conflict-free both ways) so that every store instruction writes
+        // four 128-byte row segments (coalesced) instead of 32 scattered 16-byte
+        // pieces.  The operand stages are free: every MMA has completed.
         float *Cz = C + (size_t)blockIdx.z * M * ldc;
+        float *buf = (float *)base + warp * (32 * 33);
+        const int lane = tid & 31;
+        const int cq = 4 * (lane & 7);
 #pragma unroll 1
         for (int c0 = 0; c0 < TC_N; c0 += 32) {
             uint32_t r[32], x[32];
@@ -225,18 +231,23 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
             tmem_ld32(taddr, r);
             tmem_ld32(taddr + TC_N, x);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-            float v[32];
+            __syncwarp();
 #pragma unroll
-            for (int j = 0; j < 32; j++) v[j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
-            if (orow < M) {
-                float *cr = Cz + (size_t)orow * ldc + n0 + c0;
-                if (n0 + c0 + 32 <= N && (ldc & 3) == 0) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) *(float4 *)(cr + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; j++)
-                        if (n0 + c0 + j < N) cr[j] = v[j];
+            for (int j = 0; j < 32; j++) buf[lane * 33 + j] = nit > 0 ? __uint_as_float(r[j]) + __uint_as_float(x[j]) : 0.0f;
+            __syncwarp();
+            const int n = n0 + c0 + cq;
+#pragma unroll 4
+            for (int i = 0; i < 8; i++) {
+                const int rr = 4 * i + (lane >> 3);
+                const int grow = m0 + warp * 32 + rr;
+                if (grow < M && n < N) {
+                    const float *br = buf + rr * 33 + cq;
+                    float *dst = Cz + (size_t)grow * ldc + n;
+                    if (n + 4 <= N && (ldc & 3) == 0) {
+                        *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
+                    } else {
+                        for (int j = 0; j < 4 && n + j < N; j++) dst[j] = br[j];
+                    }
                 }
             }
         }

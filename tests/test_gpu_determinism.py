@@ -1,0 +1,39 @@
+"""Bitwise reproducibility of the operators: the pair-cache
+kernels stage data through shared memory with cp.async.bulk and mbarrier rings;
+a missing proxy fence or phase error shows up as a run-to-run difference long
+before it shows up as a parity failure.  The backward's sums are integers
+(order-free), the forward's are fixed-order fp32 per voxel chunk, so every
+repeat must be bit-identical -- and the two backward kernels (bulk-copy ring,
+register-fed "flat") must agree bit for bit."""
+import numpy as np
+import pytest
+
+from workloads import make_config
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_1603_06400_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_repeat_bitwise(ci, monkeypatch):
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    f = torch.as_tensor(cfg.f).cuda()
+    w = torch.as_tensor(np.random.default_rng(3).uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
+    g0, b0 = torch.empty(G.g_shape, device="cuda"), torch.empty(G.f_shape, device="cuda")
+    G.forward(f, g0)
+    G.backward(w, b0)
+    reps = 12 if ci == 1 else 4
+    for _ in range(reps):
+        g, b = torch.empty_like(g0), torch.empty_like(b0)
+        G.forward(f, g)
+        G.backward(w, b)
+        assert torch.equal(g, g0)
+        assert torch.equal(b, b0)
+    monkeypatch.setenv("CACSI_PC_BWD", "flat")
+    b = torch.empty_like(b0)
+    G.backward(w, b)
+    assert torch.equal(b, b0)
+    G.close()
