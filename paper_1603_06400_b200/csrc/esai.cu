@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
     if (tid == 0) {
         for (int i = 0; i < PBT_NS; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(PBT_T));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(PBT_T / 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
@@ -1001,20 +1001,24 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             const int st = consumed % PBT_NS;
             mbar_wait(smem_u32(full + st), (consumed / PBT_NS) & 1);
             const unsigned char *src = smb + st * SB;
+            // this chunk's valid slots [lo, hi) (32-bit)
+            const int lo = (int)max(o0 - a, 0ll), hi = (int)min(o1 - a, (long long)PBT_CH);
             uint32_t k[PBT_U], q[PBT_U];
             float P[PBT_U];
 #pragma unroll
             for (int u = 0; u < PBT_U; u++) {
                 const int i = tid + u * PBT_T;
-                const bool in = a + i >= o0 && a + i < o1;
+                const bool in = i >= lo && i < hi;
                 k[u] = in ? ((const uint32_t *)src)[i] : ((uint32_t)win.x << tb);
                 P[u] = in ? ((const float *)(src + PBT_CH * 4))[i] : 0.0f;
                 q[u] = in ? (uint32_t)((const QT *)(src + PBT_CH * 8))[i] : 0u;
             }
-            // every thread releases its own reads: the proxy fence orders them (generic
-            // proxy) before the next bulk copy into the stage (async proxy)
+            // every thread orders its reads (generic proxy) before the next bulk copy
+            // into the stage (async proxy); then one arrival per warp
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + st)) : "memory");
+            __syncwarp();
+            if ((tid & 31) == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + st)) : "memory");
             consumed++;
             float wq[PBT_U];
 #pragma unroll
