@@ -1444,10 +1444,18 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         KScope kt_(g, s, "k_tc_gemm_W");
         if (E.pc && pixels == nullptr) {
             // plain W rows (n_vox x ldw fp32): the pair-cache forward gathers W_b and W_{b+1}
-            dim3 gg(tc_ntiles(E.nb, TC_N), (p.n_vox + TC_M - 1) / TC_M, 1);
-            cudaFuncSetAttribute(k_tc_gemm<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
-            k_tc_gemm<false, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp, E.tc_w1,
-                                                                  W, E.ldw);
+            const int nt = tc_ntiles(E.nb, TC_N), mt = (p.n_vox + TC_M - 1) / TC_M;
+            const char *gv = getenv("CACSI_WGEMM");  // "tiles": the per-tile kernel (A/B reference)
+            if (nkcA <= 4 && !(gv && strcmp(gv, "tiles") == 0)) {
+                cudaFuncSetAttribute(k_tc_gemm_ar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA));
+                k_tc_gemm_ar<<<std::min(mt * nt, sm_count(g->device)), TCA_T, tca_smem(nkcA), s>>>(
+                    p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw);
+            } else {
+                dim3 gg(nt, mt, 1);
+                cudaFuncSetAttribute(k_tc_gemm<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+                k_tc_gemm<false, 1, true><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, E.nb, p.nq, ldf, nkcA, nkcA, fp,
+                                                                      E.tc_w1, W, E.ldw);
+            }
         } else {
             dim3 gg(tc_ntiles(E.nb, TC_PSTRIDE), (p.n_vox + TC_M - 1) / TC_M, 1);
             cudaFuncSetAttribute(k_tc_gemm<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));

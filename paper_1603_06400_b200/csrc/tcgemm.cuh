@@ -307,6 +307,170 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * TC_N));
 }
 
+// ---- A-resident persistent GEMM (short K): C = A B^T with K <= 128 -------------
+// The whole A panel of an M tile (nkc <= 4 chunks, hi + lo: <= 128 KB) stays in
+// shared memory while the CTA walks its contiguous range of output tiles (M-major
+// order: at most a few panel loads per CTA), so each output tile costs only its
+// B panel in L2 -> SM traffic (the A + B reload of k_tc_gemm halved).  Warp
+// roles: warp 4 lane 0 issues the bulk copies (A panels, B chunks into a 2-stage
+// ring), warp 5 lane 0 issues the MMAs into one of two TMEM accumulator pairs
+// (512 columns), warps 0-3 drain the other pair (tcgen05.ld -> transposed
+// shared buffer -> coalesced row stores), so loads, MMAs and stores of
+// consecutive tiles overlap.  Barriers: a_full / a_empty (panel), b_full /
+// b_empty (ring), t_full / t_empty (accumulators).
+constexpr int TCA_T = 192;
+constexpr int tca_smem(int nkc) { return nkc * TC_STAGE / 2 + TC_STAGE + 4 * 32 * 33 * 4 + 1024 + 256; }
+__global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
+                                                         const float *__restrict__ Ap, const float *__restrict__ Bt,
+                                                         float *__restrict__ C, int ldc) {
+    extern __shared__ __align__(1024) unsigned char tca_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;                              // [nkc][hi, lo] 32 KB each
+    unsigned char *sB = sA + nkc * (TC_STAGE / 2);         // [2][hi, lo]
+    float *ebuf = (float *)(sB + TC_STAGE);                // [4][32][33]
+    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 4, *t_full = bars + 6,
+             *t_empty = bars + 8;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 10);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long T = (long long)mtiles * ntiles;
+    const int t0 = (int)(T * blockIdx.x / gridDim.x), t1 = (int)(T * (blockIdx.x + 1) / gridDim.x);
+    constexpr uint32_t CHB = TC_STAGE / 2;  // bytes of one hi + lo chunk (32 KB)
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < 10; i++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 8 ? 4 : 1));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            int cur_m = -1;
+            uint32_t loads = 0, bc = 0;
+            for (int t = t0; t < t1; t++) {
+                const int m = t / ntiles, n = t % ntiles;
+                if (m != cur_m) {
+                    if (loads > 0) mbar_wait(smem_u32(a_empty), (loads - 1) & 1);
+                    const uint32_t mb = smem_u32(a_full);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nkc * CHB)
+                                 : "memory");
+                    for (int c = 0; c < nkc; c++)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                smem_u32(sA + c * CHB)),
+                            "l"(Ap + ((size_t)m * nkc + c) * (2 * TC_M * TC_KC)), "r"(CHB), "r"(mb)
+                            : "memory");
+                    cur_m = m;
+                    loads++;
+                }
+                for (int c = 0; c < nkc; c++, bc++) {
+                    const int st = bc & 1;
+                    if (bc >= 2) mbar_wait(smem_u32(b_empty + st), ((bc >> 1) - 1) & 1);
+                    const uint32_t mb = smem_u32(b_full + st);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(CHB)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(sB + st * CHB)),
+                        "l"(Bt + ((size_t)n * nkc + c) * (2 * TC_N * TC_KC)), "r"(CHB), "r"(mb)
+                        : "memory");
+                }
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            const uint32_t idesc = tc_idesc_tf32();
+            int cur_m = -1;
+            uint32_t loads = 0, bc = 0, tc = 0;
+            for (int t = t0; t < t1; t++, tc++) {
+                const int m = t / ntiles;
+                if (m != cur_m) {
+                    mbar_wait(smem_u32(a_full), loads & 1);
+                    loads++;
+                    cur_m = m;
+                }
+                const int ab = tc & 1;
+                if (tc >= 2) mbar_wait(smem_u32(t_empty + ab), ((tc >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t dmain = tmem + ab * 2 * TC_N, dcross = dmain + TC_N;
+                for (int c = 0; c < nkc; c++, bc++) {
+                    const int st = bc & 1;
+                    mbar_wait(smem_u32(b_full + st), (bc >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+                    const uint32_t ah0 = smem_u32(sA + c * CHB), al0 = ah0 + TC_OPB;
+                    const uint32_t bh0 = smem_u32(sB + st * CHB), bl0 = bh0 + TC_OPB;
+#pragma unroll
+                    for (int ks = 0; ks < TC_KC / 8; ks++) {
+                        const uint32_t off = ks * 32;
+                        tc_mma(dmain, tc_desc(ah0 + off), tc_desc(bh0 + off), idesc, (c | ks) != 0);
+                        tc_mma(dcross, tc_desc(ah0 + off), tc_desc(bl0 + off), idesc, (c | ks) != 0);
+                        tc_mma(dcross, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(b_empty + st)));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(t_full + ab)));
+                if (t + 1 == t1 || (t + 1) / ntiles != m)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(a_empty)));
+            }
+        }
+    } else {
+        // epilogue warps 0-3: TMEM lanes 32 warp .. 32 warp + 31 = tile rows
+        float *buf = ebuf + warp * (32 * 33);
+        const int cq = 4 * (lane & 7);
+        uint32_t tc = 0;
+        for (int t = t0; t < t1; t++, tc++) {
+            const int m = t / ntiles, n = t % ntiles;
+            const int ab = tc & 1;
+            mbar_wait(smem_u32(t_full + ab), (tc >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const int m0 = m * TC_M, n0 = n * TC_N;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TC_N; c0 += 32) {
+                uint32_t r[32], x[32];
+                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 2 * TC_N + c0);
+                tmem_ld32(taddr, r);
+                tmem_ld32(taddr + TC_N, x);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                __syncwarp();
+                const int nn = n0 + c0 + cq;
+#pragma unroll 4
+                for (int i = 0; i < 8; i++) {
+                    const int rr = 4 * i + (lane >> 3);
+                    const int grow = m0 + warp * 32 + rr;
+                    if (grow < M && nn < N) {
+                        const float *br = buf + rr * 33 + cq;
+                        float *dst = C + (size_t)grow * ldc + nn;
+                        if (nn + 4 <= N && (ldc & 3) == 0)
+                            *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
+                        else
+                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 // Device: pack A (M x K, row-major, lda) into the tile layout of tc_pack_b
 // (rows zero-padded to a multiple of 128, K to nkc * 32): one thread per element.
 __global__ void k_tc_pack_a(const float *__restrict__ A, int M, int K, int lda, int nkc, float *__restrict__ out) {
