@@ -23,6 +23,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "pair.cuh"
 #include "tcgemm.cuh"
 
@@ -1590,6 +1592,26 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
     return esai_backward_masked(g, w, nullptr, b, s, launches);
 }
 
+// TMA tensor map of a row-major fp32 matrix (rows x cols, row stride ld floats),
+// box 128 rows x 32 columns, 128-byte swizzle (the tcgen05 K-major operand layout)
+static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            enc = nullptr;
+        if (!enc) return false;
+    }
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {ld * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_KC, (cuuint32_t)TC_M};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
                                  cudaStream_t s, int *launches) {
     const Params &p = g->p;
@@ -1640,9 +1662,20 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
-            dim3 gg((p.nq + TC_N - 1) / TC_N, (p.n_vox + TC_M - 1) / TC_M, S_eff);
-            cudaFuncSetAttribute(k_tc_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
-            k_tc_gemm<false, 1><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part, p.nq);
+            const int mt = (p.n_vox + TC_M - 1) / TC_M;
+            CUtensorMap tm;
+            const char *gv = getenv("CACSI_B2GEMM");  // "tiles": the per-tile kernel (A/B reference)
+            if (p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
+                tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw)) {
+                cudaFuncSetAttribute(k_tc_gemm_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
+                k_tc_gemm_splitk<<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
+                    tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq);
+            } else {
+                dim3 gg((p.nq + TC_N - 1) / TC_N, mt, S_eff);
+                cudaFuncSetAttribute(k_tc_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+                k_tc_gemm<false, 1><<<gg, TC_T, tc_smem(1), s>>>(p.n_vox, p.nq, E.nb, E.ldw, nkc, cps, A, E.tc_b, part,
+                                                               p.nq);
+            }
         }
         const size_t n = (size_t)p.n_vox * p.nq;
         {

@@ -25,6 +25,7 @@
 // thread issues and commits to an mbarrier.  Epilogue: tcgen05.ld, warp w
 // owns TMEM lanes (tile rows) 32w..32w+31.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -454,6 +455,188 @@ __global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, 
                     if (grow < M && nn < N) {
                         const float *br = buf + rr * 33 + cq;
                         float *dst = C + (size_t)grow * ldc + nn;
+                        if (nn + 4 <= N && (ldc & 3) == 0)
+                            *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
+                        else
+                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ---- split-K GEMM with a streamed fp32 A (long K): C[z] = A B^T over split z --
+// For b2 = A S~ (A: n_vox x ldw fp32, written by the backward; B = S~^T packed).
+// Persistent CTAs walk units (split z, M tile) -- consecutive units share z, so
+// concurrently running CTAs read the same B chunks from L2.  Warp roles:
+//   warp 8 lane 0: producer -- per K chunk, a TMA tensor load of the raw fp32 A
+//     tile (128 rows x 32, SWIZZLE_128B: the MMA operand layout) into the stage's
+//     A_hi slot and one cp.async.bulk of the pre-split B chunk (load_full);
+//   warps 4-7: split the A tile in place (hi = TF32 truncation, lo = rest into
+//     A_lo; one row per thread), proxy fence, arrive conv_full;
+//   warp 9 lane 0: 12 MMAs per chunk into one of two TMEM accumulator pairs,
+//     commit -> empty (stage free) and, after a unit's last chunk, -> t_full;
+//   warps 0-3: drain the accumulator pair (transposed, coalesced stores of the
+//     fp32 partial), arrive t_empty.
+constexpr int TCS_T = 320, TCS_NS = 3;
+constexpr int tcs_smem() { return TCS_NS * TC_STAGE + 4 * 32 * 33 * 4 + 1024 + 256; }
+__global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_constant__ CUtensorMap tmA, int M, int N,
+                                                             int nkc, int cps, int nsplit, int mtiles,
+                                                             const float *__restrict__ Bt, float *__restrict__ C,
+                                                             int ldc) {
+    extern __shared__ __align__(1024) unsigned char tcs_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)tcs_raw + 1023) & ~(uintptr_t)1023);
+    float *ebuf = (float *)(base + TCS_NS * TC_STAGE);
+    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    uint64_t *load_full = bars, *conv_full = bars + TCS_NS, *empty = bars + 2 * TCS_NS, *t_full = bars + 3 * TCS_NS,
+             *t_empty = t_full + 2;
+    uint32_t *tmem_slot = (uint32_t *)(t_empty + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nunits = nsplit * mtiles;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < TCS_NS; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(load_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(smem_u32(conv_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(empty + i)));
+        }
+        for (int i = 0; i < 2; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(t_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(smem_u32(t_empty + i)));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    if (tid == 256) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 8) {
+        if (lane == 0) {
+            uint32_t cnt = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const int z = u / mtiles, m = u % mtiles;
+                const int c1 = min(nkc, (z + 1) * cps);
+                for (int c = z * cps; c < c1; c++, cnt++) {
+                    const int st = cnt % TCS_NS;
+                    if (cnt >= TCS_NS) mbar_wait(smem_u32(empty + st), ((cnt / TCS_NS) - 1) & 1);
+                    unsigned char *sa = base + st * TC_STAGE;
+                    const uint32_t mb = smem_u32(load_full + st);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                                 "r"((uint32_t)(3 * TC_OPB))
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                        "[%4];\n" ::"r"(smem_u32(sa)),
+                        "l"(&tmA), "r"(c * TC_KC), "r"(m * TC_M), "r"(mb)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(sa + 2 * TC_OPB)),
+                        "l"(Bt + (size_t)c * (2 * TC_N * TC_KC)), "r"((uint32_t)(2 * TC_OPB)), "r"(mb)
+                        : "memory");
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        const int row = tid - 128;
+        uint32_t cnt = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const int z = u / mtiles;
+            const int c1 = min(nkc, (z + 1) * cps);
+            for (int c = z * cps; c < c1; c++, cnt++) {
+                const int st = cnt % TCS_NS;
+                mbar_wait(smem_u32(load_full + st), (cnt / TCS_NS) & 1);
+                unsigned char *sa = base + st * TC_STAGE;
+#pragma unroll
+                for (int k4 = 0; k4 < TC_KC; k4 += 4) {
+                    const uint32_t off = tc_swz(row, k4);
+                    const float4 v = *(const float4 *)(sa + off);
+                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                    *(float4 *)(sa + off) = h;
+                    *(float4 *)(sa + TC_OPB + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(conv_full + st)) : "memory");
+            }
+        }
+    } else if (warp == 9) {
+        if (lane == 0) {
+            const uint32_t idesc = tc_idesc_tf32();
+            uint32_t cnt = 0, uc = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x, uc++) {
+                const int z = u / mtiles;
+                const int c0 = z * cps, c1 = min(nkc, (z + 1) * cps);
+                const int ab = uc & 1;
+                if (uc >= 2) mbar_wait(smem_u32(t_empty + ab), ((uc >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t dmain = tmem + ab * 2 * TC_N, dcross = dmain + TC_N;
+                for (int c = c0; c < c1; c++, cnt++) {
+                    const int st = cnt % TCS_NS;
+                    mbar_wait(smem_u32(conv_full + st), (cnt / TCS_NS) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+                    const uint32_t ah0 = smem_u32(base + st * TC_STAGE), al0 = ah0 + TC_OPB;
+                    const uint32_t bh0 = ah0 + 2 * TC_OPB, bl0 = ah0 + 3 * TC_OPB;
+#pragma unroll
+                    for (int ks = 0; ks < TC_KC / 8; ks++) {
+                        const uint32_t off = ks * 32;
+                        const uint32_t accf = (c != c0 || ks != 0) ? 1u : 0u;
+                        tc_mma(dmain, tc_desc(ah0 + off), tc_desc(bh0 + off), idesc, accf);
+                        tc_mma(dcross, tc_desc(ah0 + off), tc_desc(bl0 + off), idesc, accf);
+                        tc_mma(dcross, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(empty + st)));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(t_full + ab)));
+            }
+        }
+    } else {
+        // warps 0-3: TMEM lanes 32 warp .. 32 warp + 31 = tile rows
+        float *buf = ebuf + warp * (32 * 33);
+        const int cq = 4 * (lane & 7);
+        uint32_t uc = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x, uc++) {
+            const int z = u / mtiles, m = u % mtiles;
+            const int ab = uc & 1;
+            mbar_wait(smem_u32(t_full + ab), (uc >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            float *Cz = C + (size_t)z * M * ldc;
+            const int m0 = m * TC_M;
+#pragma unroll 1
+            for (int c0 = 0; c0 < TC_N && c0 < N; c0 += 32) {
+                uint32_t r[32], x[32];
+                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 2 * TC_N + c0);
+                tmem_ld32(taddr, r);
+                tmem_ld32(taddr + TC_N, x);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                __syncwarp();
+                const int nn = c0 + cq;
+#pragma unroll 4
+                for (int i = 0; i < 8; i++) {
+                    const int rr = 4 * i + (lane >> 3);
+                    const int grow = m0 + warp * 32 + rr;
+                    if (grow < M && nn < N) {
+                        const float *br = buf + rr * 33 + cq;
+                        float *dst = Cz + (size_t)grow * ldc + nn;
                         if (nn + 4 <= N && (ldc & 3) == 0)
                             *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
                         else
