@@ -299,6 +299,9 @@ void cacsi_geometry_destroy(cacsi_geometry *g) {
         cacsi_kernel_times(g, 64, names, ms, n);  // releases the recorded events
         delete (cacsi::Timers *)g->timers;
     }
+    if (g->stage_stream) cudaStreamDestroy(g->stage_stream);
+    for (int i = 0; i < 3; i++)
+        if (g->stage_ev[i]) cudaEventDestroy(g->stage_ev[i]);
     free_all(g);
     free(g);
 }
@@ -534,18 +537,46 @@ cacsi_status cacsi_backward_host(const cacsi_geometry *g, const float *wh, float
 cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float *yh, const float *rh,
                                 const float *b1h, float beta, int32_t n_iter, void *stream) {
     if (!g || !fh || !yh || !rh || !b1h) return CACSI_ERR_NULL;
+    if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
+    cacsi_geometry *gm = const_cast<cacsi_geometry *>(g);
     cudaError_t e = ensure_stage(g);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, yh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_c, rh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_d, b1h, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !gm->stage_stream) {
+        e = cudaStreamCreateWithFlags(&gm->stage_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 3 && e == cudaSuccess; i++)
+            e = cudaEventCreateWithFlags(&gm->stage_ev[i], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) return map_err(e);
-    cacsi_status st = cacsi_iterate(g, g->d_stage_a, g->d_stage_b, g->d_stage_c, g->d_stage_d, beta, n_iter,
-                                    g->d_stage_ws, stream);
-    if (st != CACSI_OK) return st;
-    e = cudaMemcpyAsync(fh, g->d_stage_a, g->n_obj * 4, cudaMemcpyDeviceToHost, s);
+    cudaStream_t s2 = g->stage_stream;
+    // f first on the caller's stream (the forward needs only f); y, r, then b1 on the
+    // side stream, overlapping the forward -- the ratio waits for y, r, the update for b1
+    e = cudaEventRecord(g->stage_ev[0], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, g->stage_ev[0], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, yh, g->n_detout * 4, cudaMemcpyHostToDevice, s2);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_c, rh, g->n_detout * 4, cudaMemcpyHostToDevice, s2);
+    if (e == cudaSuccess) e = cudaEventRecord(g->stage_ev[1], s2);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_d, b1h, g->n_obj * 4, cudaMemcpyHostToDevice, s2);
+    if (e == cudaSuccess) e = cudaEventRecord(g->stage_ev[2], s2);
+    if (e != cudaSuccess) return map_err(e);
+    float *l, *b2, *fnew;
+    double *part;
+    ws_split(g, g->d_stage_ws, &l, &b2, &fnew, &part);
+    float *fc = g->d_stage_a, *fn = fnew;  // ping-pong: no device copy between iterations
+    int n = 0;
+    for (int t = 0; t < n_iter && e == cudaSuccess; t++) {
+        e = cacsi::launch_forward(g, fc, l, s, &n);
+        if (e == cudaSuccess && t == 0) e = cudaStreamWaitEvent(s, g->stage_ev[1], 0);
+        if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, g->d_stage_b, g->d_stage_c, l, nullptr, 0, s, &n);
+        if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, &n);
+        if (e == cudaSuccess && t == 0) e = cudaStreamWaitEvent(s, g->stage_ev[2], 0);
+        if (e == cudaSuccess) e = cacsi::launch_update(g, fc, g->d_stage_d, b2, beta, 0.0, fn, s, &n);
+        std::swap(fc, fn);
+    }
+    if (e == cudaSuccess && n_iter == 0) e = cudaStreamWaitEvent(s, g->stage_ev[2], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(fh, fc, g->n_obj * 4, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
 }
 

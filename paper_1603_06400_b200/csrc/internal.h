@@ -113,6 +113,9 @@ struct cacsi_geometry {
         *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
+    // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs
+    cudaStream_t stage_stream;
+    cudaEvent_t stage_ev[3];
     mutable int32_t last_launches;
     // per-kernel CUDA-event timing (cacsi_set_timing / cacsi_kernel_times)
     mutable int32_t timing;
