@@ -120,8 +120,9 @@ typedef struct {
  * in fp64 (the offline part of the online/offline
  * trade-off), bit-pack the mask and upload everything to `device`.
  * Synchronous.  On success *out owns the device tables.
- * Errors: CACSI_ERR_NULL (desc, out or a desc array NULL), CACSI_ERR_INVALID,
- * CACSI_ERR_CUDA (no such device / not sm_100), CACSI_ERR_NOMEM.            */
+ * Errors: CACSI_ERR_NULL (desc, out or a desc array NULL), CACSI_ERR_INVALID
+ * (including ny nz nq >= 2^31 or det_nx det_ny ne >= 2^31: 32-bit element
+ * indexing), CACSI_ERR_CUDA (no such device / not sm_100), CACSI_ERR_NOMEM. */
 CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, int device, cacsi_geometry **out);
 
 /* Free the handle and its device tables (synchronises the device).  NULL ok. */

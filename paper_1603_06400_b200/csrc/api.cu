@@ -30,6 +30,9 @@ cacsi_status validate(const cacsi_geometry_desc *d) {
         d->det_ny < 1)
         return CACSI_ERR_INVALID;
     if (d->ne > 256 || d->nq > 400) return CACSI_ERR_INVALID;  // shared-memory tables
+    // 32-bit element indexing of the object and the detector in the elementwise kernels
+    if ((long long)d->ny * d->nz * d->nq >= (1ll << 31) || (long long)d->det_nx * d->det_ny * d->ne >= (1ll << 31))
+        return CACSI_ERR_INVALID;
     if (!(d->y_min < d->y_max) || !(0.0 < d->z_min) || !(d->z_min < d->z_max) || !(d->z_max < d->mask_z) ||
         !(d->mask_z < d->det_z))
         return CACSI_ERR_INVALID;

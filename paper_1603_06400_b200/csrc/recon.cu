@@ -111,10 +111,13 @@ __global__ void k_loglik_final(const double *lpart, const double *rpart, int nb,
 // chi1 = 0 and chi2 <= 0 (voxel never seen): keep f^ (reading R14).
 __global__ void k_update(const Params p, const float *__restrict__ f_hat, const float *__restrict__ b1,
                          const float *__restrict__ b2, float beta, double delta, float *__restrict__ f_new) {
-    const size_t n = (size_t)p.n_vox * p.nq;
-    const size_t sz = p.nq, sy = (size_t)p.nz * p.nq;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int iy = (int)(i / sy), iz = (int)((i / sz) % p.nz);
+    // 32-bit index arithmetic (n_vox * nq < 2^31, checked at create): the 64-bit
+    // divisions of the neighbour indexing dominated this kernel
+    const unsigned n = (unsigned)p.n_vox * (unsigned)p.nq;
+    const unsigned sz = (unsigned)p.nq, sy = (unsigned)p.nz * (unsigned)p.nq;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned vq = i / sz;  // voxel index iy * nz + iz
+        const int iy = (int)(vq / (unsigned)p.nz), iz = (int)(vq - (unsigned)iy * (unsigned)p.nz);
         const double fj = f_hat[i];
         double som = 0.0, spd = 0.0, pd, om;
         if (iy > 0) { pen_dot_omega(fj - f_hat[i - sy], delta, pd, om); som += om; spd += pd; }
