@@ -272,6 +272,8 @@ CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, co
  * "pair_cache_records" (open pairs held in the pair cache, 0 if not built),
  * "pair_cache_record_bytes" (bytes per record: P, packed (b, tau), jy),
  * "pair_cache_tau_bits" (fraction bits of the stored tau),
+ * "pair_cache_fwd_row_blocks" (detector row blocks of the voxel-major
+ * forward; 0 = the per-list forward runs),
  * "ts_rho" (0 = no translation symmetry), "energy_resolving".  -1 for an
  * unknown key or NULL.
  * The pair cache is built at create when it fits in half of the

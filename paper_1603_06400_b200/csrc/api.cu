@@ -649,6 +649,8 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "pair_cache_record_bytes"))
         return g->esai.enabled && g->esai.pc ? 2 * (long long)sizeof(float) + g->esai.pc_qb : 0;
     if (!strcmp(key, "pair_cache_tau_bits")) return g->esai.enabled && g->esai.pc ? g->esai.pc_tbits : 0;
+    if (!strcmp(key, "pair_cache_fwd_row_blocks"))
+        return g->esai.enabled && g->esai.pc ? cacsi::pcv_row_blocks(g) : 0;
     if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
     return -1;

@@ -1409,6 +1409,21 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
                                      float *out, cudaStream_t s, int *launches);
 
+// Row blocks of the voxel-major pair-cache forward (0: the W windows do not fit
+// shared memory, the per-list kernel runs).  One 1024-thread CTA per SM with a
+// large row block (fewer W window re-stagings, longer per-voxel record runs)
+// measured faster than two 512-thread CTAs.
+int pcv_row_blocks(const cacsi_geometry *g) {
+    const Esai &E = g->esai;
+    const Params &p = g->p;
+    const int wcap = (E.max_win + 3 + 3) & ~3;
+    const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
+    const size_t budget = (bs ? atoi(bs) : 200) * 1024;
+    const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
+    const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
+    return r_max >= 1 ? (p.det_nx + r_max - 1) / r_max : 0;
+}
+
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
     return esai_forward_impl(g, f, nullptr, 0, out, s, launches);
 }
@@ -1495,16 +1510,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         return e;
     } else if (E.pc) {
         const int wcap = (E.max_win + 3 + 3) & ~3;
-        const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
-        // one 1024-thread CTA per SM with a large row block (fewer W window re-stagings,
-        // longer per-voxel record runs) measured faster than two 512-thread CTAs
-        const size_t budget = (bs ? atoi(bs) : 200) * 1024;
-        const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
-        const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
+        const int n_rb = pcv_row_blocks(g);
         const char *pv = getenv("CACSI_PC_FWD");
-        if (r_max >= 1 && !(pv && strcmp(pv, "list") == 0)) {
+        if (n_rb > 0 && !(pv && strcmp(pv, "list") == 0)) {
             // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
-            const int n_rb = (p.det_nx + r_max - 1) / r_max;
             const int R = (p.det_nx + n_rb - 1) / n_rb;
             const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
             const int ipsm = is ? atoi(is) : 4;

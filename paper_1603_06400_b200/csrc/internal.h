@@ -165,6 +165,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                                  cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
+int pcv_row_blocks(const cacsi_geometry *g);
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
 cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 

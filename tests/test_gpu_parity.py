@@ -96,6 +96,10 @@ def test_config1_forward_backward():
     dict(ny=5, nz=7, nq=13, det_nx=9, det_ny=23),
     dict(ny=1, nz=1, det_nx=1, det_ny=1),
     dict(ny=3, nz=33, nq=2, det_nx=17, det_ny=31),
+    # several ragged 128-voxel GEMM tiles, three K chunks (nq = 70), ragged W / A columns
+    dict(ny=13, nz=23, nq=70, det_nx=37, det_ny=41),
+    # long detector rows: the voxel-major forward splits the rows into >= 2 blocks
+    dict(ny=4, nz=5, nq=16, det_nx=64, det_ny=1024, det_pitch=0.05),
     # non-uniform energies: exercises the full-range k loop
     dict(energy_kev=np.array([30.0, 33.0, 41.0, 55.0, 60.0, 80.0, 101.0, 119.0])),
     # q grid narrower than the Bragg reach: both tails zero-padded
@@ -108,6 +112,8 @@ def test_ragged_and_edge_geometries(over):
     d = cfg.desc()
     d.update(over)
     G, O = geoms(d)
+    if over.get("det_ny") == 1024:
+        assert G.query("pair_cache_fwd_row_blocks") >= 2
     f = rnd(G.f_shape, 0, 20)
     w = rnd(G.g_shape, 0, 21)
     assert_parity(gpu_forward(G, f), O.forward(f), f"ragged {over} forward")
