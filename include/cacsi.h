@@ -180,7 +180,10 @@ CACSI_API cacsi_status cacsi_update(const cacsi_geometry *geom, const float *f_h
 /* End-to-end variants on HOST buffers (pageable or pinned): copy the inputs
  * to device scratch owned by the handle, run the device call, copy the output
  * back, and synchronise `stream` before returning.  Same shapes as above.
- * Not re-entrant on one handle (they share the handle's staging buffers).   */
+ * Not re-entrant on one handle (they share the handle's staging buffers).
+ * cacsi_iterate_host uploads f on `stream` and y, r, b1 on a side stream the
+ * handle owns (created on first use), so those copies overlap the first
+ * forward; the ratio and the update wait on events for them.               */
 CACSI_API cacsi_status cacsi_forward_host(const cacsi_geometry *geom, const float *f_host, float *g_host, void *stream);
 CACSI_API cacsi_status cacsi_backward_host(const cacsi_geometry *geom, const float *w_host, float *b_host, void *stream);
 CACSI_API cacsi_status cacsi_iterate_host(const cacsi_geometry *geom, float *f_host, const float *y_host,
