@@ -645,7 +645,8 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "esai_max_window")) return g->esai.enabled ? g->esai.max_win : 0;
     if (!strcmp(key, "esai_lut_cells")) return g->esai.enabled ? g->esai.nl : 0;
     if (!strcmp(key, "esai_lut_slow_cells")) return g->esai.enabled ? g->esai.n_slow : 0;
-    if (!strcmp(key, "pair_cache_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_n : 0;
+    if (!strcmp(key, "pair_cache_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_nopen : 0;
+    if (!strcmp(key, "pair_cache_padded_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_n : 0;
     if (!strcmp(key, "pair_cache_record_bytes"))
         return g->esai.enabled && g->esai.pc ? 2 * (long long)sizeof(float) + g->esai.pc_qb : 0;
     if (!strcmp(key, "pair_cache_tau_bits")) return g->esai.enabled && g->esai.pc ? g->esai.pc_tbits : 0;

@@ -680,6 +680,63 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
             }
             base += __popc(m);
         }
+        // segment padding (last list of a segment): P = 0 records, bins spread over
+        // the voxel's window (their zero deposits must not pile onto one bank)
+        const long long end = e.pc_off[l + 1];
+        if (base < end) {
+            const int2 win = e.vwin[v];
+            const int span = max(1, win.y - win.x);
+            for (long long o = base + lane; o < end; o += 32) {
+                bt[o] = (uint32_t)(win.x + (int)((o - base) % span)) << e.pc_tbits;
+                Pout[o] = 0.0f;
+                qout[o] = (QT)(ix * p.det_ny);
+            }
+        }
+    }
+}
+
+// Bank-aware order (build time): within each 128-record window of a padded
+// segment, assign the records greedily to the window's 32-record groups (one
+// warp access each) so that within a group the breakpoint cells b (histogram /
+// W-window bank = b mod 32 up to a per-voxel shift) and the pixels q (forward
+// accumulator bank) repeat as little as possible.  One thread per window.
+template <typename QT>
+__global__ void k_pc_perm(const Params p, const Esai e, int R, const uint32_t *__restrict__ bt_in,
+                          const float *__restrict__ P_in, const QT *__restrict__ q_in, uint32_t *__restrict__ bt_out,
+                          float *__restrict__ P_out, QT *__restrict__ q_out) {
+    const int nseg_v = (p.det_nx + R - 1) / R;
+    const size_t nseg = (size_t)p.n_vox * nseg_v;
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (size_t)blockDim.x) >> 5;
+    for (size_t sg = warp0; sg < nseg; sg += nwarps) {
+        const int v = (int)(sg / nseg_v), s = (int)(sg % nseg_v);
+        const size_t l0 = (size_t)v * p.det_nx;
+        const long long a = e.pc_off[l0 + s * R], z = e.pc_off[l0 + min(p.det_nx, (s + 1) * R)];
+        for (long long w0 = a + 128ll * lane; w0 < z; w0 += 128ll * 32) {
+            const int n = (int)min(128ll, z - w0), ng = n >> 5;
+            uint8_t cb[4][32], cq[4][32], fill[4];
+            for (int g = 0; g < 4; g++) {
+                fill[g] = 0;
+                for (int c = 0; c < 32; c++) cb[g][c] = cq[g][c] = 0;
+            }
+            for (int i = 0; i < n; i++) {
+                const uint32_t k = bt_in[w0 + i];
+                const int b = (int)(k >> e.pc_tbits) & 31, qq = (int)q_in[w0 + i] & 31;
+                int best = -1, bs = 1 << 30;
+                for (int g = 0; g < ng; g++)
+                    if (fill[g] < 32) {
+                        const int sc = 2 * cb[g][b] + cq[g][qq];
+                        if (sc < bs) { bs = sc; best = g; }
+                    }
+                const long long o = w0 + best * 32 + fill[best];
+                fill[best]++;
+                cb[best][b]++;
+                cq[best][qq]++;
+                bt_out[o] = k;
+                P_out[o] = P_in[w0 + i];
+                q_out[o] = q_in[w0 + i];
+            }
+        }
     }
 }
 
@@ -772,8 +829,9 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                                                      double *__restrict__ partial) {
     extern __shared__ __align__(16) float smv[];
     const int wcap = (e.max_win + 3 + 3) & ~3;
-    float *acc = smv;                                   // [R * det_ny]
-    float *ws = smv + ((R * p.det_ny + 3) & ~3);        // [2][wcap]
+    float *acc = smv;                                   // [R * det_ny] + 32 dummy slots
+    float *dummy = acc + R * p.det_ny + (threadIdx.x & 31);
+    float *ws = smv + ((R * p.det_ny + 32 + 3) & ~3);   // [2][wcap]
     uint64_t *mbar = (uint64_t *)(ws + 2 * wcap);       // [2]
     const int tid = threadIdx.x;
     const int tb = e.pc_tbits;
@@ -828,12 +886,14 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     P[u] = __ldg(Pb + i + u * PCV_T);
                     q[u] = (uint32_t)__ldg(qb + i + u * PCV_T);
                 }
+                // P = 0: segment padding, whose pixel may repeat a real record's -- it
+                // adds into the lane's dummy slot past the row block (branch-free)
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
                     const float wa = wv[b], wb = wv[b + 1];
                     const float t = (float)(k[u] & tmask) * tunit;
-                    float *ap = accq + q[u];
+                    float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
             }
@@ -843,7 +903,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                 const int b = (int)(k >> tb);
                 const float wa = wv[b], wb = wv[b + 1];
                 const float t = (float)(k & tmask) * tunit;
-                float *ap = accq + __ldg(qb + i);
+                float *ap = P != 0.0f ? accq + __ldg(qb + i) : dummy;
                 *ap = fmaf(P, fmaf(t, wb - wa, wa), *ap);
             }
             // this thread's reads of the W buffer (generic proxy) before its next
@@ -1361,8 +1421,20 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e == cudaSuccess) e = cudaMemcpy(hc.data(), cnt, nl * sizeof(int), cudaMemcpyDeviceToHost);
         cudaFree(cnt);
         if (e != cudaSuccess) return e;
+        // segments (voxel, block of R rows) of the voxel-major forward, padded to
+        // multiples of 32 records (the padding belongs to the segment's last list)
+        long long nopen = 0;
+        for (size_t i = 0; i < nl; i++) nopen += hc[i];
+        const int n_rb = pcv_row_blocks(g);
+        const int R = n_rb > 0 ? (p.det_nx + n_rb - 1) / n_rb : 0;
+        const char *pl = getenv("CACSI_PC_LAYOUT");  // "plain": no padding / bank-aware order (A/B reference)
+        const int segR = (R > 0 && !(pl && strcmp(pl, "plain") == 0)) ? R : 0;
         std::vector<long long> off(nl + 1, 0);
-        for (size_t i = 0; i < nl; i++) off[i + 1] = off[i] + hc[i];
+        for (size_t i = 0; i < nl; i++) {
+            off[i + 1] = off[i] + hc[i];
+            const int ix = (int)(i % p.det_nx);
+            if (segR > 0 && ((ix + 1) % segR == 0 || ix + 1 == p.det_nx)) off[i + 1] = (off[i + 1] + 31) & ~31ll;
+        }
         const long long nrec = off[nl];
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
@@ -1386,6 +1458,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             E.pc_tbits = std::min(32 - bbits, 24);  // tau's fp32 mantissa carries 24 bits
             E.pc_qb = (int)jyb;
             E.pc_n = nrec;
+            E.pc_nopen = nopen;
+            E.pc_R = segR;
             const size_t smem = host_bp_bytes(E);
             const int gr = persistent_grid(g, smem, 256);
             if (jyb == 2) {
@@ -1399,6 +1473,40 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             }
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
+            if (segR > 0) {
+                // bank-aware order: permute into fresh arrays, then swap
+                void *nbt = nullptr, *nP = nullptr, *nq = nullptr;
+                e = cudaMalloc(&nbt, rec * sizeof(uint32_t));
+                if (e == cudaSuccess) e = cudaMalloc(&nP, rec * sizeof(float));
+                if (e == cudaSuccess) e = cudaMalloc(&nq, rec * jyb);
+                if (e == cudaSuccess) {
+                    const int gr2 = 8 * sm_count(g->device);
+                    if (jyb == 2)
+                        k_pc_perm<uint16_t><<<gr2, 256>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
+                                                          (const float *)g->d_pc_P, (const uint16_t *)g->d_pc_q,
+                                                          (uint32_t *)nbt, (float *)nP, (uint16_t *)nq);
+                    else
+                        k_pc_perm<uint32_t><<<gr2, 256>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
+                                                          (const float *)g->d_pc_P, (const uint32_t *)g->d_pc_q,
+                                                          (uint32_t *)nbt, (float *)nP, (uint32_t *)nq);
+                    e = cudaDeviceSynchronize();
+                }
+                if (e != cudaSuccess) {
+                    cudaFree(nbt);
+                    cudaFree(nP);
+                    cudaFree(nq);
+                    return e;
+                }
+                cudaFree(g->d_pc_bt);
+                cudaFree(g->d_pc_P);
+                cudaFree(g->d_pc_q);
+                g->d_pc_bt = (decltype(g->d_pc_bt))nbt;
+                g->d_pc_P = (decltype(g->d_pc_P))nP;
+                g->d_pc_q = (decltype(g->d_pc_q))nq;
+                E.pc_bt = (const uint32_t *)g->d_pc_bt;
+                E.pc_P = (const float *)g->d_pc_P;
+                E.pc_q = g->d_pc_q;
+            }
             E.pc = 1;
         }
     }
@@ -1416,10 +1524,13 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
 int pcv_row_blocks(const cacsi_geometry *g) {
     const Esai &E = g->esai;
     const Params &p = g->p;
+    // a bank-ordered cache fixes the segments (records are permuted across the
+    // lists of a segment): the forward must use exactly those row blocks
+    if (E.pc && E.pc_R > 0) return (p.det_nx + E.pc_R - 1) / E.pc_R;
     const int wcap = (E.max_win + 3 + 3) & ~3;
     const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
     const size_t budget = (bs ? atoi(bs) : 200) * 1024;
-    const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32;
+    const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32 - 128;
     const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
     return r_max >= 1 ? (p.det_nx + r_max - 1) / r_max : 0;
 }
@@ -1511,8 +1622,8 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     } else if (E.pc) {
         const int wcap = (E.max_win + 3 + 3) & ~3;
         const int n_rb = pcv_row_blocks(g);
-        const char *pv = getenv("CACSI_PC_FWD");
-        if (n_rb > 0 && !(pv && strcmp(pv, "list") == 0)) {
+        const char *pv = getenv("CACSI_PC_FWD");  // "list": the per-list kernel (plain layout only)
+        if (n_rb > 0 && (E.pc_R > 0 || !(pv && strcmp(pv, "list") == 0))) {
             // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
             const int R = (p.det_nx + n_rb - 1) / n_rb;
             const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
@@ -1520,7 +1631,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             int Sv = std::max(1, std::min(p.n_vox, (ipsm * sm_count(g->device) + n_rb - 1) / n_rb));
             const int vchunk = (p.n_vox + Sv - 1) / Sv;
             const int n_chunks = (p.n_vox + vchunk - 1) / vchunk;
-            const size_t smem = ((size_t)((R * p.det_ny + 3) & ~3) + 2 * (size_t)wcap) * sizeof(float) + 16;
+            const size_t smem = ((size_t)((R * p.det_ny + 32 + 3) & ~3) + 2 * (size_t)wcap) * sizeof(float) + 16;
             const int cps = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
             // G CTAs per row block, each owning n_chunks / G voxel chunks: G partials
             const int G = std::max(1, std::min(n_chunks, cps * sm_count(g->device) / n_rb));

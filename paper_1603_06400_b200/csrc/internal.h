@@ -86,9 +86,13 @@ struct Esai {
     const float *tc_b;       // S~^T likewise (b2 = A S~)
     const uint32_t *tb_bwd;  // backward: [voxel][ceil(n_det/32)], bit i of word j = pixel 32 j + i
     // pair cache (esai.cu "pair cache"): per open pair of list (voxel v, detector row ix),
-    // pixels in increasing jy: key = (jy << 16) | b, w = (P (1 - tau), P tau)
+    // pixels; with pc_R > 0 each (voxel, block of pc_R rows) segment
+    // is padded to a multiple of 32 records (P = 0) and permuted in 128-record
+    // windows so that the 32 records of each warp access hit distinct banks
     int pc;                   // built
-    long long pc_n;           // open pairs (records)
+    long long pc_n;           // records incl. padding
+    long long pc_nopen;       // open pairs
+    int pc_R;                 // rows per segment (0: plain per-list layout)
     const long long *pc_off;  // [n_vox * det_nx + 1] first record of list (v, ix)
     const uint32_t *pc_bt;    // (b << pc_tbits) | round(tau 2^pc_tbits)
     const float *pc_P;        // P (the pair's geometric-spectral factor, transmission included)

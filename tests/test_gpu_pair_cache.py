@@ -94,9 +94,19 @@ def test_per_list_forward_config1(monkeypatch):
     G = P.Geometry(cfg.desc())
     assert G.query("pair_cache_records") > 0
     gv = gpu_forward(G, cfg.f)
+    # the per-list kernel needs the plain (list-ordered, unpadded) layout
+    monkeypatch.setenv("CACSI_PC_LAYOUT", "plain")
+    Gp = P.Geometry(cfg.desc())
+    monkeypatch.delenv("CACSI_PC_LAYOUT")
+    assert Gp.query("pair_cache_padded_records") == Gp.query("pair_cache_records")
     monkeypatch.setenv("CACSI_PC_FWD", "list")
-    gl = gpu_forward(G, cfg.f)
+    gl = gpu_forward(Gp, cfg.f)
+    assert torch.equal(torch.as_tensor(gpu_forward(G, cfg.f)), torch.as_tensor(gv))  # ignored by a bank-ordered cache
     monkeypatch.delenv("CACSI_PC_FWD")
     assert_parity(gl, O.forward(cfg.f), "c1 per-list cache forward")
     assert_parity(gl, gv, "c1 per-list vs voxel-major forward", l2=1e-6, mr=1e-5)
+    w = rnd(G.g_shape, 1, 73)
+    bp, bo = gpu_backward(Gp, w), gpu_backward(G, w)
+    assert np.array_equal(np.asarray(bp), np.asarray(bo))  # integer sums: the record order is irrelevant
     G.close()
+    Gp.close()
