@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // W-window bank = b mod 32 up to a per-voxel shift) and the pixels q (forward
 // accumulator bank) repeat as little as possible.  One thread per window.
 template <typename QT>
-__global__ void k_pc_perm(const Params p, const Esai e, int R, const uint32_t *__restrict__ bt_in,
+__global__ void k_pc_perm(const Params p, const Esai e, int R, int win, const uint32_t *__restrict__ bt_in,
                           const float *__restrict__ P_in, const QT *__restrict__ q_in, uint32_t *__restrict__ bt_out,
                           float *__restrict__ P_out, QT *__restrict__ q_out) {
     const int nseg_v = (p.det_nx + R - 1) / R;
@@ -712,8 +712,9 @@ __global__ void k_pc_perm(const Params p, const Esai e, int R, const uint32_t *_
         const int v = (int)(sg / nseg_v), s = (int)(sg % nseg_v);
         const size_t l0 = (size_t)v * p.det_nx;
         const long long a = e.pc_off[l0 + s * R], z = e.pc_off[l0 + min(p.det_nx, (s + 1) * R)];
-        for (long long w0 = a + 128ll * lane; w0 < z; w0 += 128ll * 32) {
-            const int n = (int)min(128ll, z - w0), ng = n >> 5;
+        for (long long w0 = a + (long long)win * lane; w0 < z; w0 += (long long)win * 32) {
+            const int n = (int)min((long long)win, z - w0), ng = n >> 5;
+
             uint8_t cb[4][32], cq[4][32], fill[4];
             for (int g = 0; g < 4; g++) {
                 fill[g] = 0;
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
     const int tb = e.pc_tbits;
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
-    const QT *pq = (const QT *)e.pc_q;
+    const QT *pq = (const QT *)e.pcb_q;
     const float wm = *wmax;
     for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
         const int2 win = e.vwin[v];
@@ -945,8 +946,8 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
                 // rolling L2 prefetch of the records pf steps ahead
                 const long long a0 = o + (long long)pf * 4 * PCB_T, a1 = min(o1, a0 + 4 * PCB_T);
                 if (a0 < a1) {
-                    l2_prefetch(e.pc_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
-                    l2_prefetch(e.pc_P + a0, (size_t)(a1 - a0) * sizeof(float));
+                    l2_prefetch(e.pcb_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
+                    l2_prefetch(e.pcb_P + a0, (size_t)(a1 - a0) * sizeof(float));
                     l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
                 }
             }
@@ -956,8 +957,8 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const bool in = o + u * PCB_T < o1;
-                k[u] = in ? __ldg(e.pc_bt + o + u * PCB_T) : ((uint32_t)win.x << tb);
-                P[u] = in ? __ldg(e.pc_P + o + u * PCB_T) : 0.0f;
+                k[u] = in ? __ldg(e.pcb_bt + o + u * PCB_T) : ((uint32_t)win.x << tb);
+                P[u] = in ? __ldg(e.pcb_P + o + u * PCB_T) : 0.0f;
                 q[u] = in ? (uint32_t)__ldg(pq + o + u * PCB_T) : 0u;
             }
 #pragma unroll
@@ -1001,7 +1002,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
     const int tb = e.pc_tbits;
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
-    const QT *pq = (const QT *)e.pc_q;
+    const QT *pq = (const QT *)e.pcb_q;
     const float wm = *wmax;
     if (tid == 0) {
         for (int i = 0; i < PBT_NS; i++) {
@@ -1038,9 +1039,9 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
                          "r"(n * (8u + (uint32_t)sizeof(QT))));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                             smem_u32(dst)), "l"(e.pc_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
+                             smem_u32(dst)), "l"(e.pcb_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                             smem_u32(dst + PBT_CH * 4)), "l"(e.pc_P + pa), "r"(n * 4u), "r"(mb) : "memory");
+                             smem_u32(dst + PBT_CH * 4)), "l"(e.pcb_P + pa), "r"(n * 4u), "r"(mb) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                              smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
             pa += PBT_CH;
@@ -1087,11 +1088,15 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]) * scale;
 #pragma unroll
             for (int u = 0; u < PBT_U; u++) {
-                const int b = (int)(k[u] >> tb);
-                const float av = P[u] * wq[u];
-                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
-                atomicAdd(hv + b, __float2int_rn(av) - x1);
-                atomicAdd(hv + b + 1, x1);
+                // slots outside the voxel's range make no deposit (they would all hit one address)
+                const int i = tid + u * PBT_T;
+                if (i >= lo && i < hi) {
+                    const int b = (int)(k[u] >> tb);
+                    const float av = P[u] * wq[u];
+                    const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                    atomicAdd(hv + b, __float2int_rn(av) - x1);
+                    atomicAdd(hv + b + 1, x1);
+                }
             }
         }
         __syncthreads();
@@ -1444,7 +1449,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb) + (nl + 1) * sizeof(long long);
         int bbits = 1;
         while ((1 << bbits) < E.nb) bbits++;
-        if (need <= free_b / 2 && bbits <= 16) {
+        // transient peak at build: the fill's arrays + the ordered copy
+        if (2 * need <= free_b / 2 && bbits <= 16) {
             e = cudaMalloc(&g->d_pc_off, (nl + 1) * sizeof(long long));
             if (e == cudaSuccess) e = cudaMemcpy(g->d_pc_off, off.data(), (nl + 1) * sizeof(long long), cudaMemcpyHostToDevice);
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_bt, rec * sizeof(uint32_t));
@@ -1473,39 +1479,44 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             }
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
+            E.pcb_bt = E.pc_bt;
+            E.pcb_P = E.pc_P;
+            E.pcb_q = E.pc_q;
             if (segR > 0) {
-                // bank-aware order: permute into fresh arrays, then swap
-                void *nbt = nullptr, *nP = nullptr, *nq = nullptr;
-                e = cudaMalloc(&nbt, rec * sizeof(uint32_t));
-                if (e == cudaSuccess) e = cudaMalloc(&nP, rec * sizeof(float));
-                if (e == cudaSuccess) e = cudaMalloc(&nq, rec * jyb);
+                // bank-aware order, permuted into fresh arrays (one copy serves both
+                // operators: a separate cells-only copy for the backward measured no faster)
+                void *arr[3] = {nullptr, nullptr, nullptr};
+                e = cudaMalloc(&arr[0], rec * sizeof(uint32_t));
+                if (e == cudaSuccess) e = cudaMalloc(&arr[1], rec * sizeof(float));
+                if (e == cudaSuccess) e = cudaMalloc(&arr[2], rec * jyb);
                 if (e == cudaSuccess) {
                     const int gr2 = 8 * sm_count(g->device);
                     if (jyb == 2)
-                        k_pc_perm<uint16_t><<<gr2, 256>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
+                        k_pc_perm<uint16_t><<<gr2, 256>>>(p, E, segR, 128, (const uint32_t *)g->d_pc_bt,
                                                           (const float *)g->d_pc_P, (const uint16_t *)g->d_pc_q,
-                                                          (uint32_t *)nbt, (float *)nP, (uint16_t *)nq);
+                                                          (uint32_t *)arr[0], (float *)arr[1], (uint16_t *)arr[2]);
                     else
-                        k_pc_perm<uint32_t><<<gr2, 256>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
+                        k_pc_perm<uint32_t><<<gr2, 256>>>(p, E, segR, 128, (const uint32_t *)g->d_pc_bt,
                                                           (const float *)g->d_pc_P, (const uint32_t *)g->d_pc_q,
-                                                          (uint32_t *)nbt, (float *)nP, (uint32_t *)nq);
+                                                          (uint32_t *)arr[0], (float *)arr[1], (uint32_t *)arr[2]);
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) {
-                    cudaFree(nbt);
-                    cudaFree(nP);
-                    cudaFree(nq);
+                    for (void *x : arr) cudaFree(x);
                     return e;
                 }
                 cudaFree(g->d_pc_bt);
                 cudaFree(g->d_pc_P);
                 cudaFree(g->d_pc_q);
-                g->d_pc_bt = (decltype(g->d_pc_bt))nbt;
-                g->d_pc_P = (decltype(g->d_pc_P))nP;
-                g->d_pc_q = (decltype(g->d_pc_q))nq;
+                g->d_pc_bt = arr[0];
+                g->d_pc_P = arr[1];
+                g->d_pc_q = arr[2];
                 E.pc_bt = (const uint32_t *)g->d_pc_bt;
                 E.pc_P = (const float *)g->d_pc_P;
                 E.pc_q = g->d_pc_q;
+                E.pcb_bt = E.pc_bt;
+                E.pcb_P = E.pc_P;
+                E.pcb_q = E.pc_q;
             }
             E.pc = 1;
         }

@@ -97,6 +97,10 @@ struct Esai {
     const uint32_t *pc_bt;    // (b << pc_tbits) | round(tau 2^pc_tbits)
     const float *pc_P;        // P (the pair's geometric-spectral factor, transmission included)
     const void *pc_q;         // pixel q, uint16 (n_det <= 65536) or uint32
+    // the records the backward reads (= pc_*; kept separate for layout experiments)
+    const uint32_t *pcb_bt;
+    const float *pcb_P;
+    const void *pcb_q;
     int pc_tbits;             // fraction bits of tau (>= 16)
     int pc_qb;                // bytes per q (2 or 4)
 };
