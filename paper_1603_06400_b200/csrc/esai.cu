@@ -1059,6 +1059,9 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
         const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
         int *hv = hist_s - win.x;
         const long long o0 = __ldg(e.pc_off + (size_t)v * p.det_nx), o1 = __ldg(e.pc_off + (size_t)(v + 1) * p.det_nx);
+        // slots outside the voxel's range deposit zero (branch-free) into lane-spread bins,
+        // not all into one address
+        const uint32_t kinv = (uint32_t)(win.x + (tid & 31) % max(1, nwin - 1)) << tb;
         for (long long a = o0 & ~7ll; a < o1; a += PBT_CH) {
             if (tid == 0) produce(consumed + PBT_NS);
             const int st = consumed % PBT_NS;
@@ -1072,7 +1075,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             for (int u = 0; u < PBT_U; u++) {
                 const int i = tid + u * PBT_T;
                 const bool in = i >= lo && i < hi;
-                k[u] = in ? ((const uint32_t *)src)[i] : ((uint32_t)win.x << tb);
+                k[u] = in ? ((const uint32_t *)src)[i] : kinv;
                 P[u] = in ? ((const float *)(src + PBT_CH * 4))[i] : 0.0f;
                 q[u] = in ? (uint32_t)((const QT *)(src + PBT_CH * 8))[i] : 0u;
             }
@@ -1088,15 +1091,11 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]) * scale;
 #pragma unroll
             for (int u = 0; u < PBT_U; u++) {
-                // slots outside the voxel's range make no deposit (they would all hit one address)
-                const int i = tid + u * PBT_T;
-                if (i >= lo && i < hi) {
-                    const int b = (int)(k[u] >> tb);
-                    const float av = P[u] * wq[u];
-                    const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
-                    atomicAdd(hv + b, __float2int_rn(av) - x1);
-                    atomicAdd(hv + b + 1, x1);
-                }
+                const int b = (int)(k[u] >> tb);
+                const float av = P[u] * wq[u];
+                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                atomicAdd(hv + b, __float2int_rn(av) - x1);
+                atomicAdd(hv + b + 1, x1);
             }
         }
         __syncthreads();
