@@ -13,6 +13,7 @@
 // [nq+4][threads] shared-memory histogram (bank = lane, conflict-free, no
 // atomics); the columns are summed in fp64 at the end.
 #include <cstdio>
+#include <cstring>
 
 #include "pair.cuh"
 
@@ -216,6 +217,96 @@ __global__ void __launch_bounds__(BWD_T) k_backward(const Params p, const float 
     }
 }
 
+// Energy-resolving backward with compacted open pairs: as k_backward<true>
+// (one CTA per voxel, lane-private histogram columns), but each warp first
+// evaluates the mask and geometry of 64 pixels, appends the OPEN ones to a
+// per-warp queue (P, sin(theta/2), pixel, energy window) and processes full
+// batches of 32 queued pairs -- lanes never idle on closed pairs (about half of
+// all pairs), and each batch's energy loop spans its lanes' windows only.
+struct ErQ {
+    float P, sh;
+    int q, kw;  // kw = klo | khi << 16
+};
+constexpr int ERQ_CAP = 96;
+__global__ void __launch_bounds__(BWD_T) k_backward_er_c(const Params p, const float *__restrict__ w,
+                                                         float *__restrict__ b) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne;
+    float2 *en = (float2 *)smem4;                  // [K]
+    float *hist = (float *)(en + ((K + 1) & ~1));  // [Q + 4][BWD_T]; bin = node + 2
+    ErQ *queue = (ErQ *)(hist + (Q + 4) * BWD_T);  // [BWD_T / 32][ERQ_CAP]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int v = blockIdx.x;
+    for (int k = tid; k < K; k += BWD_T) en[k] = p.energy[k];
+    for (int i = tid; i < (Q + 4) * BWD_T; i += BWD_T) hist[i] = 0.0f;
+    __syncthreads();
+    const VoxelRec vr = p.vox[v];
+    float *hb = hist + tid;
+    ErQ *wq = queue + warp * ERQ_CAP;
+    int qn = 0;  // queued pairs (warp-uniform)
+    auto batch = [&](int cnt) {
+        // lanes < cnt take queue entries 0 .. cnt - 1
+        ErQ e = {0.0f, 1.0f, 0, K};
+        if (lane < cnt) e = wq[lane];
+        const int klo = e.kw & 0xFFFF, khi = (e.kw >> 16) - 1;  // stored as khi + 1 (empty: klo = K, khi = -1)
+        const int wlo = __reduce_min_sync(FULL, klo);
+        const int whi = __reduce_max_sync(FULL, khi);
+        const float *wp = w + e.q;
+        for (int k = wlo; k <= whi; k++) {
+            const float2 en_k = en[k];
+            float tt;
+            const int n = hat_coord(p, en_k.x, e.sh, tt);
+            const float ca = (k >= klo && k <= khi) ? e.P * en_k.y * __ldg(wp + (size_t)k * p.n_det) : 0.0f;
+            const float hi = fmaf(tt, ca, 0.5f * ca);
+            float *h0 = hb + (n + 2) * BWD_T;
+            h0[0] += ca - hi;
+            h0[BWD_T] += hi;
+        }
+    };
+    for (int base = warp * 64; base < p.n_det; base += (BWD_T / 32) * 64) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = base + 32 * h + lane;
+            const bool valid = q < p.n_det;
+            const float2 d = p.det[valid ? q : 0];
+            bool open = valid && mask_open(p, v, q, vr, d);
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1;
+            if (open) {
+                pair_geom(p, vr, d, P, sh);
+                k_range(p, sh, klo, khi);
+                open = klo <= khi;
+            }
+            const unsigned m = __ballot_sync(FULL, open);
+            if (open) wq[qn + __popc(m & ((1u << lane) - 1u))] = ErQ{P, sh, q, klo | ((khi + 1) << 16)};
+            qn += __popc(m);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+            batch(32);
+            __syncwarp();
+            // move the remainder (< 64 entries) to the front
+            const int rem = qn - 32;
+            ErQ t0, t1;
+            if (lane < rem) t0 = wq[32 + lane];
+            if (lane + 32 < rem) t1 = wq[64 + lane];
+            __syncwarp();
+            if (lane < rem) wq[lane] = t0;
+            if (lane + 32 < rem) wq[lane + 32] = t1;
+            __syncwarp();
+            qn = rem;
+        }
+    }
+    if (qn > 0) batch(qn);
+    __syncthreads();
+    for (int j = tid; j < Q; j += BWD_T) {
+        const float *row = hist + (j + 2) * BWD_T;
+        double s = 0.0;
+        for (int t = 0; t < BWD_T; t++) s += (double)row[(t + j) % BWD_T];  // rotate: bank spread
+        b[(size_t)v * Q + j] = (float)s;
+    }
+}
+
 int num_sms(int device) {
     static int cached[64] = {0};
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
@@ -295,8 +386,14 @@ cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, c
             KScope kt_(g, s, "k_transpose");
             k_transpose<<<dim3((p.ne + 31) / 32, (p.n_det + 31) / 32), dim3(32, 8), 0, s>>>(w, p.n_det, p.ne, wT);
         }
-        cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        {
+        const char *ev = getenv("CACSI_ER_BWD");  // "dense": lanes on all pixels (A/B reference)
+        if (!(ev && strcmp(ev, "dense") == 0)) {
+            const size_t smc = smem + (size_t)(BWD_T / 32) * ERQ_CAP * sizeof(ErQ);
+            cudaFuncSetAttribute(k_backward_er_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+            KScope kt_(g, s, "k_backward_er");
+            k_backward_er_c<<<p.n_vox, BWD_T, smc, s>>>(p, wT, b);
+        } else {
+            cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             KScope kt_(g, s, "k_backward_er");
             k_backward<true><<<p.n_vox, BWD_T, smem, s>>>(p, wT, b);
         }
