@@ -258,8 +258,8 @@ def test_deterministic_operators():
 
 # ------------------------------------------------ direct per-term algorithm --
 def test_direct_algorithm_energy_resolving(monkeypatch):
-    """CACSI_ALGO=direct for the energy-resolving operators (per-pixel
-    threads) -- an independent GPU cross-check of the lanes-as-energies kernels."""
+    """CACSI_ALGO=direct for the energy-resolving operators on a ragged shape
+    (per-pixel forward threads, compacted-open-pair backward)."""
     monkeypatch.setenv("CACSI_ALGO", "direct")
     cfg = make_config(0, energy_resolving=1)
     d = cfg.desc()
