@@ -1566,7 +1566,13 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     const int ldf = (p.nq + TC_KC - 1) / TC_KC * TC_KC;
     cudaError_t e = cudaMallocAsync(&W, (size_t)p.n_vox * E.ldw * sizeof(float2), s);  // W2 pairs
     // packed A tiles: [ceil(n_vox / 128)][ldf / 32][hi, lo][128 x 32]
-    if (e == cudaSuccess) e = cudaMallocAsync(&fp, (size_t)(p.n_vox + TC_M - 1) / TC_M * TC_M * ldf * 2 * sizeof(float), s);
+    // (an even tile count: the CTA-pair W GEMM takes M tiles two at a time; the spare tile is zero)
+    const size_t mt_even = ((size_t)(p.n_vox + TC_M - 1) / TC_M + 1) & ~(size_t)1;
+    if (e == cudaSuccess) e = cudaMallocAsync(&fp, mt_even * TC_M * ldf * 2 * sizeof(float), s);
+    if (e == cudaSuccess && mt_even * TC_M > (size_t)(p.n_vox + TC_M - 1) / TC_M * TC_M) {
+        const size_t tile = (size_t)TC_M * ldf * 2;
+        e = cudaMemsetAsync(fp + (mt_even - 1) * tile, 0, tile * sizeof(float), s);
+    }
     if (e != cudaSuccess) {
         if (W) cudaFreeAsync(W, s);
         return e;
@@ -1584,9 +1590,16 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             // plain W rows (n_vox x ldw fp32): the pair-cache forward gathers W_b and W_{b+1}
             const int nt = tc_ntiles(E.nb, TC_N), mt = (p.n_vox + TC_M - 1) / TC_M;
             const char *gv = getenv("CACSI_WGEMM");  // "tiles": the per-tile kernel (A/B reference)
-            if (nkcA <= 4 && !(gv && strcmp(gv, "tiles") == 0)) {
+            if (nkcA <= 4 && gv && strcmp(gv, "ar2") == 0) {
+                // the CTA-pair (cta_group::2) variant: bit-identical, measured slower
+                const int mp = (int)(mt_even / 2);
+                cudaFuncSetAttribute(k_tc_gemm_ar2, cudaFuncAttributeMaxDynamicSharedMemorySize, tca2_smem(nkcA));
+                const int npairs = std::max(1, std::min(mp * nt, sm_count(g->device) / 2));
+                k_tc_gemm_ar2<<<2 * npairs, TCA_T, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
+                                                                        E.ldw);
+            } else if (nkcA <= 4 && !(gv && strcmp(gv, "tiles") == 0)) {
                 cudaFuncSetAttribute(k_tc_gemm_ar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA));
-                k_tc_gemm_ar<<<std::min(mt * nt, sm_count(g->device)), TCA_T, tca_smem(nkcA), s>>>(
+                k_tc_gemm_ar<<<std::min(mt * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA), s>>>(
                     p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw);
             } else {
                 dim3 gg(nt, mt, 1);

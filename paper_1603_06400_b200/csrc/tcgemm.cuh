@@ -319,17 +319,18 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
 // shared buffer -> coalesced row stores), so loads, MMAs and stores of
 // consecutive tiles overlap.  Barriers: a_full / a_empty (panel), b_full /
 // b_empty (ring), t_full / t_empty (accumulators).
-constexpr int TCA_T = 192;
-constexpr int tca_smem(int nkc) { return nkc * TC_STAGE / 2 + TC_STAGE + 4 * 32 * 33 * 4 + 1024 + 256; }
-__global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
+constexpr int TCA_T = 192;   // warp roles of k_tc_gemm_ar2 (4 epilogue warps)
+constexpr int TCA_T1 = 320;  // k_tc_gemm_ar: 8 epilogue warps
+constexpr int tca_smem(int nkc) { return nkc * TC_STAGE / 2 + TC_STAGE + 8 * 32 * 33 * 4 + 1024 + 256; }
+__global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
                                                          const float *__restrict__ Ap, const float *__restrict__ Bt,
                                                          float *__restrict__ C, int ldc) {
     extern __shared__ __align__(1024) unsigned char tca_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                              // [nkc][hi, lo] 32 KB each
     unsigned char *sB = sA + nkc * (TC_STAGE / 2);         // [2][hi, lo]
-    float *ebuf = (float *)(sB + TC_STAGE);                // [4][32][33]
-    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    float *ebuf = (float *)(sB + TC_STAGE);                // [8][32][33]
+    uint64_t *bars = (uint64_t *)(ebuf + 8 * 32 * 33);
     uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 4, *t_full = bars + 6,
              *t_empty = bars + 8;
     uint32_t *tmem_slot = (uint32_t *)(bars + 10);
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, 
     }
     if (tid == 32) {
         for (int i = 0; i < 10; i++)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 8 ? 4 : 1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 8 ? 8 : 1));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -426,8 +427,10 @@ __global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, 
             }
         }
     } else {
-        // epilogue warps 0-3: TMEM lanes 32 warp .. 32 warp + 31 = tile rows
-        float *buf = ebuf + warp * (32 * 33);
+        // epilogue warps 0-3 and 6-9: TMEM lanes 32 (warp % 4) .. + 31 = tile rows; warps
+        // 0-3 drain columns 0-63, warps 6-9 columns 64-127
+        const int ew = warp < 4 ? warp : warp - 2, lq = warp & 3, ch = warp < 4 ? 0 : TC_N / 2;
+        float *buf = ebuf + ew * (32 * 33);
         const int cq = 4 * (lane & 7);
         uint32_t tc = 0;
         for (int t = t0; t < t1; t++, tc++) {
@@ -436,16 +439,267 @@ __global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, 
             mbar_wait(smem_u32(t_full + ab), (tc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const int m0 = m * TC_M, n0 = n * TC_N;
+            // software-pipelined drain: chunk c0 + 32's TMEM loads are in flight while
+            // chunk c0 is transposed and stored
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * 2 * TC_N);
+            uint32_t r[32], x[32];
+            tmem_ld32(tbase + ch, r);
+            tmem_ld32(tbase + TC_N + ch, x);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll 1
-            for (int c0 = 0; c0 < TC_N; c0 += 32) {
-                uint32_t r[32], x[32];
-                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 2 * TC_N + c0);
-                tmem_ld32(taddr, r);
-                tmem_ld32(taddr + TC_N, x);
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+            for (int c0 = ch; c0 < ch + TC_N / 2; c0 += 32) {
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                if (c0 + 32 < ch + TC_N / 2) {
+                    tmem_ld32(tbase + c0 + 32, r);
+                    tmem_ld32(tbase + TC_N + c0 + 32, x);
+                }
+                __syncwarp();
+                const int nn = n0 + c0 + cq;
+#pragma unroll 4
+                for (int i = 0; i < 8; i++) {
+                    const int rr = 4 * i + (lane >> 3);
+                    const int grow = m0 + lq * 32 + rr;
+                    if (grow < M && nn < N) {
+                        const float *br = buf + rr * 33 + cq;
+                        float *dst = C + (size_t)grow * ldc + nn;
+                        if (nn + 4 <= N && (ldc & 3) == 0)
+                            *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
+                        else
+                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
+                    }
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ---- the same on CTA pairs (tcgen05 cta_group::2, M = 256 per pair) ----------
+// A cluster of two CTAs on one TPC computes 256 x 128 output tiles: each CTA
+// keeps ITS 128-row A panel resident and loads only HALF of each B chunk (64
+// rows, 16 KB hi + lo), the leader's single thread issues the pair MMA
+// (A rows from both CTAs' shared memory, B halves from both, each CTA's TMEM
+// holding its 128 rows), so every SM moves half the B bytes of k_tc_gemm_ar
+// and the B ring gets four stages.  Synchronisation across the pair: the
+// follower's copies land on its own barriers and a forwarding thread re-arrives
+// them on the leader's (pa_full, pb_full); MMA completion is committed to both
+// CTAs' barriers by multicast; both epilogues arrive on the leader's t_empty.
+constexpr int TCA2_NS = 4;
+constexpr int TCA2_HB = TC_OPB / 2;  // one 64-row half of a 128 x 32 operand tile (8 KB)
+constexpr int tca2_smem(int nkc) { return nkc * TC_STAGE / 2 + TCA2_NS * 2 * TCA2_HB + 4 * 32 * 33 * 4 + 1024 + 256; }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void remote_arrive(uint32_t local_bar, uint32_t rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}\n" ::"r"(local_bar),
+        "r"(rank)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit2_mc(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__host__ __device__ constexpr uint32_t tc_idesc_tf32_m256() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
+    k_tc_gemm_ar2(int M, int N, int nkc, int mpairs, int ntiles, const float *__restrict__ Ap,
+                  const float *__restrict__ Bt, float *__restrict__ C, int ldc) {
+    extern __shared__ __align__(1024) unsigned char tca_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;                                  // [nkc][hi, lo] 32 KB each
+    unsigned char *sB = sA + nkc * (TC_STAGE / 2);             // [NS][hi, lo] 8 KB each
+    float *ebuf = (float *)(sB + TCA2_NS * 2 * TCA2_HB);       // [4][32][33]
+    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    uint64_t *a_full = bars, *a_empty = bars + 1, *pa_full = bars + 2, *t_full = bars + 3, *t_empty = bars + 5,
+             *b_full = bars + 7, *b_empty = b_full + TCA2_NS, *pb_full = b_empty + TCA2_NS;
+    uint32_t *tmem_slot = (uint32_t *)(pb_full + TCA2_NS);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const long long T = (long long)mpairs * ntiles;
+    const int t0 = (int)(T * pair / npairs), t1 = (int)(T * (pair + 1) / npairs);
+    constexpr uint32_t CHB = TC_STAGE / 2;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(a_full)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(a_empty)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(pa_full)));
+        for (int i = 0; i < 2; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(t_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(t_empty + i)));
+        }
+        for (int i = 0; i < TCA2_NS; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b_empty + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(pb_full + i)));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            int cur_mp = -1;
+            uint32_t loads = 0, bc = 0;
+            for (int t = t0; t < t1; t++) {
+                const int mp = t / ntiles, n = t % ntiles;
+                const int m = 2 * mp + (int)rank;
+                if (mp != cur_mp) {
+                    if (loads > 0) mbar_wait(smem_u32(a_empty), (loads - 1) & 1);
+                    const uint32_t mb = smem_u32(a_full);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nkc * CHB)
+                                 : "memory");
+                    for (int c = 0; c < nkc; c++)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                smem_u32(sA + c * CHB)),
+                            "l"(Ap + ((size_t)m * nkc + c) * (2 * TC_M * TC_KC)), "r"(CHB), "r"(mb)
+                            : "memory");
+                    cur_mp = mp;
+                    loads++;
+                }
+                for (int c = 0; c < nkc; c++, bc++) {
+                    const int st = bc % TCA2_NS;
+                    if (bc >= TCA2_NS) mbar_wait(smem_u32(b_empty + st), ((bc / TCA2_NS) - 1) & 1);
+                    const uint32_t mb = smem_u32(b_full + st);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                                 "r"((uint32_t)(2 * TCA2_HB))
+                                 : "memory");
+                    const float *src = Bt + ((size_t)n * nkc + c) * (2 * TC_N * TC_KC) + rank * (TC_N / 2) * TC_KC;
+                    unsigned char *dst = sB + st * 2 * TCA2_HB;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(dst)),
+                        "l"(src), "r"((uint32_t)TCA2_HB), "r"(mb)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(dst + TCA2_HB)),
+                        "l"(src + TC_N * TC_KC), "r"((uint32_t)TCA2_HB), "r"(mb)
+                        : "memory");
+                }
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0 && rank == 1) {
+            // forwarder: this CTA's panel / chunk landed -> the leader's pa_full / pb_full
+            int cur_mp = -1;
+            uint32_t loads = 0, bc = 0;
+            for (int t = t0; t < t1; t++) {
+                const int mp = t / ntiles;
+                if (mp != cur_mp) {
+                    mbar_wait(smem_u32(a_full), loads & 1);
+                    remote_arrive(smem_u32(pa_full), 0);
+                    loads++;
+                    cur_mp = mp;
+                }
+                for (int c = 0; c < nkc; c++, bc++) {
+                    const int st = bc % TCA2_NS;
+                    mbar_wait(smem_u32(b_full + st), (bc / TCA2_NS) & 1);
+                    remote_arrive(smem_u32(pb_full + st), 0);
+                }
+            }
+        } else if (lane == 0 && rank == 0) {
+            const uint32_t idesc = tc_idesc_tf32_m256();
+            int cur_mp = -1;
+            uint32_t loads = 0, bc = 0, tc = 0;
+            for (int t = t0; t < t1; t++, tc++) {
+                const int mp = t / ntiles;
+                if (mp != cur_mp) {
+                    mbar_wait(smem_u32(a_full), loads & 1);
+                    mbar_wait_cl(smem_u32(pa_full), loads & 1);
+                    loads++;
+                    cur_mp = mp;
+                }
+                const int ab = tc & 1;
+                if (tc >= 2) mbar_wait_cl(smem_u32(t_empty + ab), ((tc >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t dmain = tmem + ab * 2 * TC_N, dcross = dmain + TC_N;
+                for (int c = 0; c < nkc; c++, bc++) {
+                    const int st = bc % TCA2_NS;
+                    mbar_wait(smem_u32(b_full + st), (bc / TCA2_NS) & 1);
+                    mbar_wait_cl(smem_u32(pb_full + st), (bc / TCA2_NS) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+                    const uint32_t ah0 = smem_u32(sA + c * CHB), al0 = ah0 + TC_OPB;
+                    const uint32_t bh0 = smem_u32(sB + st * 2 * TCA2_HB), bl0 = bh0 + TCA2_HB;
+#pragma unroll
+                    for (int ks = 0; ks < TC_KC / 8; ks++) {
+                        const uint32_t off = ks * 32;
+                        tc_mma2(dmain, tc_desc(ah0 + off), tc_desc(bh0 + off), idesc, (c | ks) != 0);
+                        tc_mma2(dcross, tc_desc(ah0 + off), tc_desc(bl0 + off), idesc, (c | ks) != 0);
+                        tc_mma2(dcross, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
+                    }
+                    tc_commit2_mc(smem_u32(b_empty + st));
+                }
+                tc_commit2_mc(smem_u32(t_full + ab));
+                if (t + 1 == t1 || (t + 1) / ntiles != mp) tc_commit2_mc(smem_u32(a_empty));
+            }
+        }
+    } else {
+        float *buf = ebuf + warp * (32 * 33);
+        const int cq = 4 * (lane & 7);
+        uint32_t tc = 0;
+        for (int t = t0; t < t1; t++, tc++) {
+            const int mp = t / ntiles, n = t % ntiles;
+            const int ab = tc & 1;
+            mbar_wait(smem_u32(t_full + ab), (tc >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const int m0 = (2 * mp + (int)rank) * TC_M, n0 = n * TC_N;
+            const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 2 * TC_N);
+            uint32_t r[32], x[32];
+            tmem_ld32(tbase, r);
+            tmem_ld32(tbase + TC_N, x);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll 1
+            for (int c0 = 0; c0 < TC_N; c0 += 32) {
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                if (c0 + 32 < TC_N) {
+                    tmem_ld32(tbase + c0 + 32, r);
+                    tmem_ld32(tbase + TC_N + c0 + 32, x);
+                }
                 __syncwarp();
                 const int nn = n0 + c0 + cq;
 #pragma unroll 4
@@ -461,15 +715,17 @@ __global__ void __launch_bounds__(TCA_T, 1) k_tc_gemm_ar(int M, int N, int nkc, 
                             for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
                     }
                 }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
+            if (lane == 0) remote_arrive(smem_u32(t_empty + ab), 0);  // the leader's (rank 0: its own)
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    cluster_sync_all();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
 // ---- split-K GEMM with a streamed fp32 A (long K): C[z] = A B^T over split z --

@@ -37,3 +37,21 @@ def test_repeat_bitwise(ci, monkeypatch):
     G.backward(w, b)
     assert torch.equal(b, b0)
     G.close()
+
+
+def test_cta_pair_w_gemm_bitwise(monkeypatch):
+    """The cta_group::2 W GEMM (CACSI_WGEMM=ar2: M = 256 per CTA pair, half of
+    each B chunk per SM, multicast commits) gives the same bits as the
+    single-CTA A-resident GEMM."""
+    cfg = make_config(1)
+    G = P.Geometry(cfg.desc())
+    f = torch.as_tensor(cfg.f).cuda()
+    out = []
+    for mode in ("ar", "ar2"):
+        monkeypatch.setenv("CACSI_WGEMM", mode)
+        g = torch.empty(G.g_shape, device="cuda")
+        G.forward(f, g)
+        torch.cuda.synchronize()
+        out.append(g)
+    assert torch.equal(out[0], out[1])
+    G.close()
