@@ -1810,9 +1810,31 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
             const char *gv = getenv("CACSI_B2GEMM");  // "tiles": the per-tile kernel (A/B reference)
             if (p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
                 tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw)) {
-                cudaFuncSetAttribute(k_tc_gemm_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
-                k_tc_gemm_splitk<<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
-                    tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq);
+                // CACSI_B2_MC=1: CTA pairs share each B chunk by cluster multicast (bit-identical,
+                // measured no faster: the GEMM is latency-bound, not L2-bound)
+                const char *mc = getenv("CACSI_B2_MC");
+                if (mc && strcmp(mc, "1") == 0) {
+                    const int mte = (mt + 1) & ~1;
+                    cudaFuncSetAttribute(k_tc_gemm_splitk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(std::max(2, std::min(S_eff * mte, sm_count(g->device)) & ~1));
+                    cfg.blockDim = dim3(TCS_T);
+                    cfg.dynamicSmemBytes = tcs_smem();
+                    cfg.stream = s;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeClusterDimension;
+                    at[0].val.clusterDim.x = 2;
+                    at[0].val.clusterDim.y = 1;
+                    at[0].val.clusterDim.z = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    e = cudaLaunchKernelEx(&cfg, k_tc_gemm_splitk<true>, tm, p.n_vox, p.nq, nkc, cps, S_eff, mte,
+                                           (const float *)E.tc_b, part, p.nq);
+                } else {
+                    cudaFuncSetAttribute(k_tc_gemm_splitk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
+                    k_tc_gemm_splitk<false><<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
+                        tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq);
+                }
             } else {
                 dim3 gg((p.nq + TC_N - 1) / TC_N, mt, S_eff);
                 cudaFuncSetAttribute(k_tc_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
