@@ -110,3 +110,19 @@ def test_per_list_forward_config1(monkeypatch):
     assert np.array_equal(np.asarray(bp), np.asarray(bo))  # integer sums: the record order is irrelevant
     G.close()
     Gp.close()
+
+
+def test_wide_detector_uint32_pixels():
+    """n_det > 65536: the pair cache stores the pixel as uint32 (12-byte records)
+    and both pair-cache kernels take their uint32 instantiation."""
+    cfg = make_config(0)
+    d = cfg.desc()
+    d.update(ny=4, nz=3, nq=8, det_nx=260, det_ny=256, det_pitch=0.1)
+    G, O = P.Geometry(d), oracle.Geometry(d)
+    assert G.n_det > 65536
+    assert G.query("pair_cache_records") > 0
+    assert G.query("pair_cache_record_bytes") == 12
+    f, w = rnd(G.f_shape, 0, 80), rnd(G.g_shape, 0, 81)
+    assert_parity(gpu_forward(G, f), O.forward(f), "wide detector forward")
+    assert_parity(gpu_backward(G, w), O.backward(w), "wide detector backward")
+    G.close()
