@@ -79,7 +79,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -645,6 +645,8 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "esai_max_window")) return g->esai.enabled ? g->esai.max_win : 0;
     if (!strcmp(key, "esai_lut_cells")) return g->esai.enabled ? g->esai.nl : 0;
     if (!strcmp(key, "esai_lut_slow_cells")) return g->esai.enabled ? g->esai.n_slow : 0;
+    if (!strcmp(key, "esai_window_permille")) return g->esai.enabled ? g->esai.stat_win_permille : 0;
+    if (!strcmp(key, "esai_tile_span_permille")) return g->esai.enabled ? g->esai.stat_tile_permille : 0;
     if (!strcmp(key, "pair_cache_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_nopen : 0;
     if (!strcmp(key, "pair_cache_padded_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_n : 0;
     if (!strcmp(key, "pair_cache_record_bytes"))

@@ -1100,6 +1100,8 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
         }
         __syncthreads();
         const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        // whole rows (zeros outside the window): writing only the tile's chunk range that
+        // the b2 GEMM reads measured slower (gaps between the rows of neighbouring voxels)
         float *Ar = A + (size_t)v * e.ldw;
         for (int b = tid; b < e.ldw; b += PBT_T) {
             const int i = b - win.x;
@@ -1299,9 +1301,30 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     // per-voxel breakpoint windows (deposits land in [locate(min), locate(max) + 1])
     std::vector<int2> vwin(nv);
     int max_win = 1;
+    long long win_sum = 0;
     for (int v = 0; v < nv; v++) {
         vwin[v] = make_int2(host_locate(sb, shmin[v]), host_locate(sb, shmax[v]) + 1);
         max_win = std::max(max_win, vwin[v].y - vwin[v].x + 1);
+        win_sum += vwin[v].y - vwin[v].x + 1;
+    }
+    // per 128-voxel GEMM tile: the union of its voxels' windows.  Neither contraction
+    // needs W or A outside it (the forward reads W only inside each voxel's window,
+    // the backward deposits only there), so the W GEMM skips N tiles and the b2 GEMM
+    // K chunks outside it, and the backward writes A rows only inside it.
+    std::vector<int2> trng((nv + 127) / 128);
+    {
+        long long tile_span = 0;
+        for (int m0 = 0; m0 < nv; m0 += 128) {
+            int lo = 1 << 30, hi = 0;
+            for (int v = m0; v < std::min(nv, m0 + 128); v++) {
+                lo = std::min(lo, vwin[v].x);
+                hi = std::max(hi, vwin[v].y + 1);
+            }
+            trng[m0 / 128] = make_int2(lo, hi);
+            tile_span += (long long)(((hi + 31) / 32) - lo / 32) * 32;
+        }
+        g->esai.stat_win_permille = (int)(1000 * win_sum / ((long long)nv * nb));
+        g->esai.stat_tile_permille = (int)(1000 * tile_span / ((long long)((nv + 127) / 128) * nb));
     }
     e = cudaMalloc(&g->d_esai_bp, nb * sizeof(float2));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_bp, bp.data(), nb * sizeof(float2), cudaMemcpyHostToDevice);
@@ -1316,6 +1339,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         e = cudaMemcpy(g->d_esai_stab, stab.data(), stab.size() * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_vwin, nv * sizeof(int2));
     if (e == cudaSuccess) e = cudaMemcpy(g->d_esai_vwin, vwin.data(), nv * sizeof(int2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_trng, trng.size() * sizeof(int2));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g->d_esai_trng, trng.data(), trng.size() * sizeof(int2), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
     Esai &E = g->esai;
     E.nb = nb;
@@ -1328,6 +1354,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.sb = (const float *)g->d_esai_sb;
     E.stab = (const float *)g->d_esai_stab;
     E.vwin = (const int2 *)g->d_esai_vwin;
+    E.trng = (const int2 *)g->d_esai_trng;
     E.ptot = (const float *)g->d_esai_ptot;
     E.max_win = max_win;
     // tensor-core operands: S~ (N = nb, K = nq) for W = F S~^T and S~^T (N = nq, K = nb) for b2 = A S~,
@@ -1768,6 +1795,13 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.ldw * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
+    // the contraction: the persistent split-K GEMM skips each tile's chunks outside the
+    // union of its voxels' windows (A is zero there); the per-tile GEMM reads whole rows
+    const int mt = (p.n_vox + TC_M - 1) / TC_M;
+    CUtensorMap tm;
+    const char *gv = getenv("CACSI_B2GEMM");  // "tiles": the per-tile kernel (A/B reference)
+    const bool splitk = p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
+                        tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw);
     if (e == cudaSuccess) {
         {
             KScope kt_(g, s, "k_absmax");
@@ -1805,35 +1839,11 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
-            const int mt = (p.n_vox + TC_M - 1) / TC_M;
-            CUtensorMap tm;
-            const char *gv = getenv("CACSI_B2GEMM");  // "tiles": the per-tile kernel (A/B reference)
-            if (p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
-                tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw)) {
-                // CACSI_B2_MC=1: CTA pairs share each B chunk by cluster multicast (bit-identical,
-                // measured no faster: the GEMM is latency-bound, not L2-bound)
-                const char *mc = getenv("CACSI_B2_MC");
-                if (mc && strcmp(mc, "1") == 0) {
-                    const int mte = (mt + 1) & ~1;
-                    cudaFuncSetAttribute(k_tc_gemm_splitk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
-                    cudaLaunchConfig_t cfg = {};
-                    cfg.gridDim = dim3(std::max(2, std::min(S_eff * mte, sm_count(g->device)) & ~1));
-                    cfg.blockDim = dim3(TCS_T);
-                    cfg.dynamicSmemBytes = tcs_smem();
-                    cfg.stream = s;
-                    cudaLaunchAttribute at[1];
-                    at[0].id = cudaLaunchAttributeClusterDimension;
-                    at[0].val.clusterDim.x = 2;
-                    at[0].val.clusterDim.y = 1;
-                    at[0].val.clusterDim.z = 1;
-                    cfg.attrs = at;
-                    cfg.numAttrs = 1;
-                    e = cudaLaunchKernelEx(&cfg, k_tc_gemm_splitk<true>, tm, p.n_vox, p.nq, nkc, cps, S_eff, mte,
-                                           (const float *)E.tc_b, part, p.nq);
-                } else {
-                    cudaFuncSetAttribute(k_tc_gemm_splitk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
-                    k_tc_gemm_splitk<false><<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
-                        tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq);
+            if (splitk) {
+                {
+                    cudaFuncSetAttribute(k_tc_gemm_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
+                    k_tc_gemm_splitk<<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
+                        tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq, E.trng, mt);
                 }
             } else {
                 dim3 gg((p.nq + TC_N - 1) / TC_N, mt, S_eff);

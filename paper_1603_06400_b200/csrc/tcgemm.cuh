@@ -743,16 +743,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
 //     fp32 partial), arrive t_empty.
 constexpr int TCS_T = 320, TCS_NS = 3;
 constexpr int tcs_smem() { return TCS_NS * TC_STAGE + 4 * 32 * 33 * 4 + 1024 + 256; }
-// MC: clusters of two CTAs that run units (z, 2j) and (z, 2j + 1) in lock-step
-// and share each B chunk: each CTA loads one half (hi or lo) and multicasts it
-// into both CTAs' stages (B bytes from L2 halved); every MMA commit is
-// multicast to both CTAs' "empty" barriers, since a stage is refilled in both.
-// mtiles is then even (a spare tile reads zeros through the tensor map).
-template <bool MC>
 __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_constant__ CUtensorMap tmA, int M, int N,
                                                              int nkc, int cps, int nsplit, int mtiles,
                                                              const float *__restrict__ Bt, float *__restrict__ C,
-                                                             int ldc) {
+                                                             int ldc, const int2 *__restrict__ trng, int mreal) {
+    // the K chunks of unit (z, m): the split's range cut to the tile's column range
+    // (trng, optional: A is written only there); tiles m >= mreal are empty
+    auto krange = [&](int z, int m, int &c0, int &c1) {
+        c0 = z * cps;
+        c1 = min(nkc, (z + 1) * cps);
+        if (m >= mreal) {
+            c1 = c0;
+        } else if (trng) {
+            const int2 r = trng[m];
+            c0 = max(c0, r.x / TC_KC);
+            c1 = min(c1, (r.y + TC_KC - 1) / TC_KC);
+        }
+    };
     extern __shared__ __align__(1024) unsigned char tcs_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tcs_raw + 1023) & ~(uintptr_t)1023);
     float *ebuf = (float *)(base + TCS_NS * TC_STAGE);
@@ -762,10 +769,7 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
     uint32_t *tmem_slot = (uint32_t *)(t_empty + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nunits = nsplit * mtiles;
-    const uint32_t rank = MC ? cluster_rank() : 0u;
-    // this CTA's units: u0, u0 + ustep, ...
-    const int u0 = MC ? (int)(blockIdx.x & ~1u) + (int)rank : (int)blockIdx.x;
-    const int ustep = gridDim.x;
+    const int u0 = (int)blockIdx.x, ustep = gridDim.x;  // this CTA's units: u0, u0 + ustep, ...
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
@@ -775,7 +779,7 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
         for (int i = 0; i < TCS_NS; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(load_full + i)));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(smem_u32(conv_full + i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(MC ? 2 : 1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(empty + i)));
         }
         for (int i = 0; i < 2; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(t_full + i)));
@@ -786,7 +790,6 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
     if (tid == 256) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (MC) cluster_sync_all();  // the peer's multicast copies and commits target our barriers
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = *tmem_slot;
 
@@ -795,10 +798,11 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
             uint32_t cnt = 0;
             for (int u = u0; u < nunits; u += ustep) {
                 const int z = u / mtiles, m = u % mtiles;
-                const int c1 = min(nkc, (z + 1) * cps);
-                for (int c = z * cps; c < c1; c++, cnt++) {
+                int cA, c1;
+                krange(z, m, cA, c1);
+                for (int c = cA; c < c1; c++, cnt++) {
                     const int st = cnt % TCS_NS;
-                    if (cnt >= TCS_NS) mbar_wait_cl(smem_u32(empty + st), ((cnt / TCS_NS) - 1) & 1);
+                    if (cnt >= TCS_NS) mbar_wait(smem_u32(empty + st), ((cnt / TCS_NS) - 1) & 1);
                     unsigned char *sa = base + st * TC_STAGE;
                     const uint32_t mb = smem_u32(load_full + st);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
@@ -809,21 +813,11 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
                         "[%4];\n" ::"r"(smem_u32(sa)),
                         "l"(&tmA), "r"(c * TC_KC), "r"(m * TC_M), "r"(mb)
                         : "memory");
-                    if (MC) {
-                        // this CTA's half of the B chunk (rank 0: hi, rank 1: lo) into both CTAs
-                        asm volatile(
-                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
-                            "[%1], %2, [%3], %4;\n" ::"r"(smem_u32(sa + (2 + rank) * TC_OPB)),
-                            "l"(Bt + (size_t)c * (2 * TC_N * TC_KC) + rank * (TC_N * TC_KC)), "r"((uint32_t)TC_OPB),
-                            "r"(mb), "h"((uint16_t)3)
-                            : "memory");
-                    } else {
-                        asm volatile(
-                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                                smem_u32(sa + 2 * TC_OPB)),
-                            "l"(Bt + (size_t)c * (2 * TC_N * TC_KC)), "r"((uint32_t)(2 * TC_OPB)), "r"(mb)
-                            : "memory");
-                    }
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(sa + 2 * TC_OPB)),
+                        "l"(Bt + (size_t)c * (2 * TC_N * TC_KC)), "r"((uint32_t)(2 * TC_OPB)), "r"(mb)
+                        : "memory");
                 }
             }
         }
@@ -831,9 +825,10 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
         const int row = tid - 128;
         uint32_t cnt = 0;
         for (int u = u0; u < nunits; u += ustep) {
-            const int z = u / mtiles;
-            const int c1 = min(nkc, (z + 1) * cps);
-            for (int c = z * cps; c < c1; c++, cnt++) {
+            const int z = u / mtiles, m = u % mtiles;
+            int cA, c1;
+            krange(z, m, cA, c1);
+            for (int c = cA; c < c1; c++, cnt++) {
                 const int st = cnt % TCS_NS;
                 mbar_wait(smem_u32(load_full + st), (cnt / TCS_NS) & 1);
                 unsigned char *sa = base + st * TC_STAGE;
@@ -856,8 +851,9 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
             const uint32_t idesc = tc_idesc_tf32();
             uint32_t cnt = 0, uc = 0;
             for (int u = u0; u < nunits; u += ustep, uc++) {
-                const int z = u / mtiles;
-                const int c0 = z * cps, c1 = min(nkc, (z + 1) * cps);
+                const int z = u / mtiles, m = u % mtiles;
+                int c0, c1;
+                krange(z, m, c0, c1);
                 const int ab = uc & 1;
                 if (uc >= 2) mbar_wait(smem_u32(t_empty + ab), ((uc >> 1) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -876,16 +872,9 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
                         tc_mma(dcross, tc_desc(ah0 + off), tc_desc(bl0 + off), idesc, accf);
                         tc_mma(dcross, tc_desc(al0 + off), tc_desc(bh0 + off), idesc, 1);
                     }
-                    if (MC)
-                        asm volatile(
-                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
-                            "%1;\n" ::"r"(smem_u32(empty + st)),
-                            "h"((uint16_t)3)
-                            : "memory");
-                    else
-                        asm volatile(
-                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                                smem_u32(empty + st)));
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                            smem_u32(empty + st)));
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                     smem_u32(t_full + ab)));
@@ -898,6 +887,9 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
         uint32_t uc = 0;
         for (int u = u0; u < nunits; u += ustep, uc++) {
             const int z = u / mtiles, m = u % mtiles;
+            int cA, cB;
+            krange(z, m, cA, cB);
+            const bool empty_unit = cB <= cA;  // no MMA wrote the accumulator: store zeros
             const int ab = uc & 1;
             mbar_wait(smem_u32(t_full + ab), (uc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -912,7 +904,8 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                for (int j = 0; j < 32; j++)
+                    buf[lane * 33 + j] = empty_unit ? 0.0f : __uint_as_float(r[j]) + __uint_as_float(x[j]);
                 __syncwarp();
                 const int nn = c0 + cq;
 #pragma unroll 4
@@ -936,7 +929,6 @@ __global__ void __launch_bounds__(TCS_T, 1) k_tc_gemm_splitk(const __grid_consta
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (MC) cluster_sync_all();  // no CTA leaves while its peer may still write into it
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 

@@ -55,20 +55,3 @@ def test_cta_pair_w_gemm_bitwise(monkeypatch):
         out.append(g)
     assert torch.equal(out[0], out[1])
     G.close()
-
-
-def test_b2_multicast_gemm_bitwise(monkeypatch):
-    """The b2 split-K GEMM with B shared by cluster multicast across CTA pairs
-    (CACSI_B2_MC=1) gives the same bits as the unicast one."""
-    cfg = make_config(1)
-    G = P.Geometry(cfg.desc())
-    w = torch.as_tensor(np.random.default_rng(5).uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
-    out = []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("CACSI_B2_MC", mode)
-        b = torch.empty(G.f_shape, device="cuda")
-        G.backward(w, b)
-        torch.cuda.synchronize()
-        out.append(b)
-    assert torch.equal(out[0], out[1])
-    G.close()
