@@ -465,13 +465,19 @@ __global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Es
     }
 }
 
-// out[list[i]] = sum_s partial[s][i]   (fixed order, fp64)
+// out[list[i]] = sum_s partial[s][i] in fp64: one warp per listed pixel, lane l
+// sums splits l, l + 32, ... and a fixed shuffle tree combines the lanes
+// (deterministic; a subset has few pixels and up to ~n_vox / 32 splits, so one
+// thread per pixel would be a long chain of dependent loads)
 __global__ void k_sum_list(const double *__restrict__ part, int S, const int32_t *__restrict__ list, int n,
                            float *__restrict__ out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
         double s = 0.0;
-        for (int j = 0; j < S; j++) s += part[(size_t)j * n + i];
-        out[list[i]] = (float)s;
+        for (int j = lane; j < S; j += 32) s += part[(size_t)j * n + i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+        if (lane == 0) out[list[i]] = (float)s;
     }
 }
 
@@ -590,6 +596,59 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
             const int i = b - win.x;
             Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * unit : 0.0f;
         }
+    }
+}
+
+// Subset backward (Alg. 6) over a pixel LIST: one warp per voxel with its own
+// fixed-point histogram in shared memory (no CTA-wide barriers: the voxels of a
+// CTA proceed independently), lanes take the listed pixels, test the pair's
+// transmission bit and deposit as k_esai_bwd (same scale rule, so the same
+// integers).  A subset has few pixels, so k_esai_bwd's per-voxel scan of the
+// whole detector bitmap and its CTA-wide phases dominated there.
+template <bool SAI>
+__global__ void __launch_bounds__(256) k_esai_bwd_list(const Params p, const Esai e, const float *__restrict__ w,
+                                                       const float *__restrict__ wmax, const int32_t *__restrict__ list,
+                                                       int n, float *__restrict__ A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
+    const int hstride = (e.max_win + 3) & ~3;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int *hist = (int *)(smem + bp_smem_bytes(e)) + warp * hstride;
+    load_bp(e, sb, lut);
+    __syncthreads();
+    const float wm = *wmax;
+    const int nw = (p.n_det + 31) / 32;
+    for (int v = blockIdx.x * nwarps + warp; v < p.n_vox; v += gridDim.x * nwarps) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        for (int i = lane; i < nwin; i += 32) hist[i] = 0;
+        __syncwarp();
+        const double bound = (double)e.vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+        const VoxelRec vr = p.vox[v];
+        int *hv = hist - win.x;
+        const uint32_t *tbv = e.tb_bwd + (size_t)v * nw;
+        for (int k = lane; scale > 0.0f && k < n; k += 32) {
+            const int q = __ldg(list + k);
+            if ((__ldg(tbv + (q >> 5)) >> (q & 31)) & 1u) {
+                float P, sh, t;
+                pair_geom(p, vr, p.det[q], P, sh, !SAI);
+                const int b = locate_pair<SAI>(p, e, sb, lut, sh, v, q, t);
+                const float a = P * __ldg(w + q) * scale;
+                const int x1 = __float2int_rn(a * t);
+                atomicAdd(hv + b, __float2int_rn(a) - x1);
+                atomicAdd(hv + b + 1, x1);
+            }
+        }
+        __syncwarp();
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = lane; b < e.ldw; b += 32) {
+            const int i = b - win.x;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist[i] * unit : 0.0f;
+        }
+        __syncwarp();
     }
 }
 
@@ -1660,7 +1719,8 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             }
             {
                 KScope kt_(g, s, "k_sum_list");
-                k_sum_list<<<(n_pix + 255) / 256, 256, 0, s>>>(part, S, pixels, n_pix, out);
+                k_sum_list<<<std::min((n_pix + 7) / 8, 8 * sm_count(g->device)), 256, 0, s>>>(part, S, pixels, n_pix,
+                                                                                               out);
             }
         }
         if (e == cudaSuccess) e = cudaGetLastError();
@@ -1759,7 +1819,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
 }
 
 cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
-    return esai_backward_masked(g, w, nullptr, b, s, launches);
+    return esai_backward_masked(g, w, nullptr, b, s, launches, nullptr, 0);
 }
 
 // TMA tensor map of a row-major fp32 matrix (rows x cols, row stride ld floats),
@@ -1783,7 +1843,7 @@ static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uin
 }
 
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
-                                 cudaStream_t s, int *launches) {
+                                 cudaStream_t s, int *launches, const int32_t *list, int n_list) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
@@ -1828,6 +1888,17 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
             kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, pf, A);
             }
+        } else if (list != nullptr && !(getenv("CACSI_SUBSET_BWD") && strcmp(getenv("CACSI_SUBSET_BWD"), "mask") == 0)) {
+            // warps per CTA: as many voxel histograms as fit next to the breakpoint tables
+            const size_t bpb = host_bp_bytes(E), hb = (size_t)((E.max_win + 3) & ~3) * sizeof(int);
+            const int nwarps = (int)std::max((size_t)1, std::min((size_t)8, ((size_t)200 * 1024 - bpb) / hb));
+            const size_t smem = bpb + nwarps * hb;
+            KScope kt_(g, s, "k_esai_bwd");
+            auto kb = p.sai_n > 0 ? k_esai_bwd_list<true> : k_esai_bwd_list<false>;
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, nwarps * 32, smem);
+            kb<<<std::max(1, nb) * sm_count(g->device), nwarps * 32, smem, s>>>(p, E, w, wmax, list, n_list, A);
         } else {
         const size_t smem = bwd_smem_bytes(host_bp_bytes(E), E.max_win);
         {
@@ -1915,7 +1986,7 @@ cudaError_t launch_backward_subset(const cacsi_geometry *g, const float *w, cons
     cudaError_t e = make_mask(g, pixels, n, &mask, s);
     *launches += 1;
     if (e == cudaSuccess && g->esai.enabled) {
-        e = esai_backward_masked(g, w, mask, b, s, launches);
+        e = esai_backward_masked(g, w, mask, b, s, launches, pixels, n);
     } else if (e == cudaSuccess) {
         float *wr = nullptr;
         e = cudaMallocAsync(&wr, g->n_detout * sizeof(float), s);

@@ -172,7 +172,7 @@ cudaError_t launch_backward_subset(const cacsi_geometry *g, const float *w, cons
 cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
                               cudaStream_t s, int *launches);
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
-                                 cudaStream_t s, int *launches);
+                                 cudaStream_t s, int *launches, const int32_t *list = nullptr, int n_list = 0);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 int pcv_row_blocks(const cacsi_geometry *g);
