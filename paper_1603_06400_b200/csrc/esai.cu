@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
 constexpr int PL_T = 256;
 
 template <bool SAI>
-__global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Esai e, const float2 *__restrict__ W,
+__global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Esai e, const float *__restrict__ W,
                                                         const int32_t *__restrict__ list, int n, int vox_per_split,
                                                         int n_items, double *__restrict__ partial) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -456,8 +456,10 @@ __global__ void __launch_bounds__(PL_T) k_esai_fwd_list(const Params p, const Es
                 float P, sh, t;
                 pair_geom(p, p.vox[c0 + k], d, P, sh, !SAI);
                 const int b = locate_pair<SAI>(p, e, sb, lut, sh, c0 + k, pix, t);
-                const float2 w = __ldg(W + (size_t)(c0 + k) * e.ldw + b);
-                acc = fmaf(P, fmaf(t, w.y - w.x, w.x), acc);
+                // plain W rows (the A-resident GEMM's output): W_b and W_{b+1}
+                const float *wp = W + (size_t)(c0 + k) * e.ldw + b;
+                const float wa = __ldg(wp), wb = __ldg(wp + 1);
+                acc = fmaf(P, fmaf(t, wb - wa, wa), acc);
             }
             tot += (double)acc;
         }
@@ -1672,8 +1674,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     {
         // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
         KScope kt_(g, s, "k_tc_gemm_W");
-        if (E.pc && pixels == nullptr) {
-            // plain W rows (n_vox x ldw fp32): the pair-cache forward gathers W_b and W_{b+1}
+        if ((E.pc && pixels == nullptr) || pixels != nullptr) {
+            // plain W rows (n_vox x ldw fp32): the pair-cache and the subset forwards gather W_b
+            // and W_{b+1}; the pair layout below serves the full on-the-fly kernels
             const int nt = tc_ntiles(E.nb, TC_N), mt = (p.n_vox + TC_M - 1) / TC_M;
             const char *gv = getenv("CACSI_WGEMM");  // "tiles": the per-tile kernel (A/B reference)
             if (nkcA <= 4 && gv && strcmp(gv, "ar2") == 0) {
@@ -1715,7 +1718,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 KScope kt_(g, s, "k_esai_fwd_list");
                 auto kl = p.sai_n > 0 ? k_esai_fwd_list<true> : k_esai_fwd_list<false>;
                 cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bpb);
-                kl<<<grid, PL_T, bpb, s>>>(p, E, (const float2 *)W, pixels, n_pix, vps, n_chunks * S, part);
+                kl<<<grid, PL_T, bpb, s>>>(p, E, W, pixels, n_pix, vps, n_chunks * S, part);
             }
             {
                 KScope kt_(g, s, "k_sum_list");
