@@ -631,16 +631,30 @@ __global__ void __launch_bounds__(256) k_esai_bwd_list(const Params p, const Esa
         const VoxelRec vr = p.vox[v];
         int *hv = hist - win.x;
         const uint32_t *tbv = e.tb_bwd + (size_t)v * nw;
-        for (int k = lane; scale > 0.0f && k < n; k += 32) {
-            const int q = __ldg(list + k);
-            if ((__ldg(tbv + (q >> 5)) >> (q & 31)) & 1u) {
-                float P, sh, t;
-                pair_geom(p, vr, p.det[q], P, sh, !SAI);
-                const int b = locate_pair<SAI>(p, e, sb, lut, sh, v, q, t);
-                const float a = P * __ldg(w + q) * scale;
-                const int x1 = __float2int_rn(a * t);
-                atomicAdd(hv + b, __float2int_rn(a) - x1);
-                atomicAdd(hv + b + 1, x1);
+        // two listed pixels per lane per iteration: independent chains (bit test, geometry,
+        // locate, deposit) whose latencies overlap
+        for (int k = lane; scale > 0.0f && k < n; k += 64) {
+            const bool two = k + 32 < n;
+            const int q1 = __ldg(list + k), q2 = two ? __ldg(list + k + 32) : q1;
+            const bool o1 = (__ldg(tbv + (q1 >> 5)) >> (q1 & 31)) & 1u;
+            const bool o2 = two && ((__ldg(tbv + (q2 >> 5)) >> (q2 & 31)) & 1u);
+            if (o1 || o2) {
+                float P1, s1, P2, s2, t1, t2;
+                pair_geom(p, vr, p.det[q1], P1, s1, !SAI);
+                pair_geom(p, vr, p.det[q2], P2, s2, !SAI);
+                const int b1 = locate_pair<SAI>(p, e, sb, lut, s1, v, q1, t1);
+                const int b2 = locate_pair<SAI>(p, e, sb, lut, s2, v, q2, t2);
+                const float a1 = o1 ? P1 * __ldg(w + q1) * scale : 0.0f;
+                const float a2 = o2 ? P2 * __ldg(w + q2) * scale : 0.0f;
+                const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
+                if (o1) {
+                    atomicAdd(hv + b1, __float2int_rn(a1) - x1);
+                    atomicAdd(hv + b1 + 1, x1);
+                }
+                if (o2) {
+                    atomicAdd(hv + b2, __float2int_rn(a2) - x2);
+                    atomicAdd(hv + b2 + 1, x2);
+                }
             }
         }
         __syncwarp();
@@ -1708,9 +1722,11 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         e = cudaMemsetAsync(out, 0, (size_t)p.n_det * sizeof(float), s);
         const int n_chunks = (n_pix + PL_T - 1) / PL_T;
         const int grid = persistent_grid(g, bpb, PL_T);
-        S = std::max(1, std::min((4 * grid + n_chunks - 1) / n_chunks, (p.n_vox + 31) / 32));
+        // voxel splits of 16 (half a bit batch): twice the threads of 32-voxel splits and
+        // half the dependent pair chain per thread (a subset has few pixels)
+        S = std::max(1, std::min((8 * grid + n_chunks - 1) / n_chunks, (p.n_vox + 15) / 16));
         int vps = (p.n_vox + S - 1) / S;
-        vps = (vps + 31) / 32 * 32;
+        vps = (vps + 15) / 16 * 16;
         S = (p.n_vox + vps - 1) / vps;
         if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S * n_pix * sizeof(double), s);
         if (e == cudaSuccess) {
