@@ -250,7 +250,11 @@ CACSI_API cacsi_status cacsi_backward_subset(const cacsi_geometry *geom, const f
  * caller).  Each sub-iteration: z_p = A_p f + r, b2_p = A_p^T (y ./ z_p),
  * f <- Eq. f_update(f, b1_p, b2_p) with penalty weight beta / n_subsets
  * (reading R20: the subset data term stands for 1/P of L).  Subsets are swept
- * in index order.  ws: cacsi_workspace_bytes() bytes.                      */
+ * in index order.  ws: cacsi_workspace_bytes() bytes.
+ * One outer iteration is captured into a CUDA graph on first use and replayed;
+ * the graph is cached in the handle (one per handle, guarded by a mutex) and
+ * re-captured when any argument (pointers, offsets, beta, penalty) changes.
+ * CACSI_GRAPHS=0 or cacsi_set_timing(1) selects plain stream launches.     */
 CACSI_API cacsi_status cacsi_osem(const cacsi_geometry *geom, float *f, const float *y, const float *r,
                                   const float *b1_subsets, const int32_t *pixels, const int32_t *offsets,
                                   int32_t n_subsets, float beta, const cacsi_penalty *pen, int32_t n_outer,

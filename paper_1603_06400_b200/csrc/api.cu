@@ -9,6 +9,9 @@
 #include <cstring>
 #include <vector>
 
+#include <mutex>
+#include <vector>
+
 #include "internal.h"
 
 using cacsi::Params;
@@ -21,6 +24,11 @@ namespace {
 double centre(double lo, double hi, int n, int i) {
     double pitch = (hi - lo) / n;
     return lo + (i + 0.5) * pitch;
+}
+static uint32_t __float_as_uint_host(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    return u;
 }
 double det_centre(double c, int n, double p, int i) { return c + ((i + 0.5) - 0.5 * n) * p; }
 
@@ -302,6 +310,7 @@ void cacsi_geometry_destroy(cacsi_geometry *g) {
         cacsi_kernel_times(g, 64, names, ms, n);  // releases the recorded events
         delete (cacsi::Timers *)g->timers;
     }
+    cacsi::osem_graph_free(g);
     if (g->stage_stream) cudaStreamDestroy(g->stage_stream);
     for (int i = 0; i < 3; i++)
         if (g->stage_ev[i]) cudaEventDestroy(g->stage_ev[i]);
@@ -467,6 +476,52 @@ cacsi_status cacsi_backward_subset(const cacsi_geometry *g, const float *w, cons
     return map_err(e);
 }
 
+}  // extern "C"
+
+// ---- cacsi_osem: one outer iteration (P subset sub-iterations, ~11 launches each)
+// is captured once into a CUDA graph and replayed; the capture is cached per handle
+// and reused while the call's arguments (pointers, subset offsets, beta, penalty)
+// are the same -- the launch-bound loop then costs one graph launch per outer
+// iteration instead of ~700 stream launches.
+namespace cacsi {
+struct OsemGraph {
+    std::mutex mu;
+    cudaStream_t cap = nullptr;  // capture stream (the caller's may be the legacy stream)
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint64_t> key;
+    int launches = 0;
+};
+void osem_graph_free(cacsi_geometry *g) {
+    OsemGraph *og = (OsemGraph *)g->osem_graph;
+    if (!og) return;
+    if (og->exec) cudaGraphExecDestroy(og->exec);
+    if (og->cap) cudaStreamDestroy(og->cap);
+    delete og;
+    g->osem_graph = nullptr;
+}
+static cudaError_t osem_outer(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1_subsets,
+                              const int32_t *pixels, const int32_t *offsets, int32_t n_subsets, float beta_p,
+                              double delta, float *l, float *b2, float *fnew, cudaStream_t s, int *n) {
+    // ping-pong between f and fnew; an odd subset count ends with one copy back into f
+    float *fc = f, *fn = fnew;
+    cudaError_t e = cudaSuccess;
+    for (int p = 0; p < n_subsets && e == cudaSuccess; p++) {
+        const int32_t *px = pixels + offsets[p];
+        const int np = offsets[p + 1] - offsets[p];
+        e = launch_forward_subset(g, fc, px, np, l, s, n);                    // z_p = A_p f (+ r_p)
+        if (e == cudaSuccess) e = launch_ratio(g, l, y, r, l, nullptr, 0, s, n);  // y_p ./ z_p
+        if (e == cudaSuccess) e = launch_backward_subset(g, l, px, np, b2, s, n);  // b2_p
+        if (e == cudaSuccess)
+            e = launch_update(g, fc, b1_subsets + (size_t)p * g->n_obj, b2, beta_p, delta, fn, s, n);
+        std::swap(fc, fn);
+    }
+    if (e == cudaSuccess && fc != f) e = cudaMemcpyAsync(f, fc, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    return e;
+}
+}  // namespace cacsi
+
+extern "C" {
+
 cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1_subsets,
                         const int32_t *pixels, const int32_t *offsets, int32_t n_subsets, float beta,
                         const cacsi_penalty *pen, int32_t n_outer, void *ws, void *stream) {
@@ -484,17 +539,53 @@ cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const
     const float beta_p = beta / (float)n_subsets;  // reading R20: the subset term stands for 1/P of L
     int n = 0;
     cudaError_t e = cudaSuccess;
-    for (int t = 0; t < n_outer && e == cudaSuccess; t++)
-        for (int p = 0; p < n_subsets && e == cudaSuccess; p++) {
-            const int32_t *px = pixels + offsets[p];
-            const int np = offsets[p + 1] - offsets[p];
-            e = cacsi::launch_forward_subset(g, f, px, np, l, s, &n);                  // z_p = A_p f (+ r_p)
-            if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, &n);  // y_p ./ z_p
-            if (e == cudaSuccess) e = cacsi::launch_backward_subset(g, l, px, np, b2, s, &n);  // b2_p
-            if (e == cudaSuccess)
-                e = cacsi::launch_update(g, f, b1_subsets + (size_t)p * g->n_obj, b2, beta_p, delta, fnew, s, &n);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(f, fnew, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    const char *gv = getenv("CACSI_GRAPHS");  // "0": plain stream launches
+    const bool use_graph = n_outer > 0 && !g->timing && !(gv && strcmp(gv, "0") == 0);
+    if (use_graph) {
+        cacsi_geometry *gm = const_cast<cacsi_geometry *>(g);
+        if (!gm->osem_graph) gm->osem_graph = new cacsi::OsemGraph();
+        cacsi::OsemGraph *og = (cacsi::OsemGraph *)gm->osem_graph;
+        std::lock_guard<std::mutex> lock(og->mu);
+        std::vector<uint64_t> key = {(uint64_t)f, (uint64_t)y, (uint64_t)r, (uint64_t)b1_subsets, (uint64_t)pixels,
+                                     (uint64_t)ws, (uint64_t)n_subsets, (uint64_t)__float_as_uint_host(beta_p),
+                                     (uint64_t)(delta * 1e12)};
+        for (int p = 0; p <= n_subsets; p++) key.push_back((uint64_t)offsets[p]);
+        if (!og->exec || og->key != key) {
+            if (og->exec) cudaGraphExecDestroy(og->exec);
+            og->exec = nullptr;
+            if (!og->cap) e = cudaStreamCreateWithFlags(&og->cap, cudaStreamNonBlocking);
+            cudaGraph_t graph = nullptr;
+            if (e == cudaSuccess) e = cudaStreamBeginCapture(og->cap, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                int nl = 0;
+                cudaError_t ec = cacsi::osem_outer(g, f, y, r, b1_subsets, pixels, offsets, n_subsets, beta_p, delta, l,
+                                                   b2, fnew, og->cap, &nl);
+                e = cudaStreamEndCapture(og->cap, &graph);
+                if (ec != cudaSuccess) e = ec;
+                og->launches = nl;
+            }
+            if (e == cudaSuccess) e = cudaGraphInstantiate(&og->exec, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            if (e == cudaSuccess) og->key = key;
         }
+        for (int t = 0; t < n_outer && e == cudaSuccess; t++) {
+            e = cudaGraphLaunch(og->exec, s);
+            n += og->launches;
+        }
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();  // capture unsupported here: fall back to stream launches
+            if (og->exec) cudaGraphExecDestroy(og->exec);
+            og->exec = nullptr;
+            og->key.clear();
+            e = cudaSuccess;
+            n = 0;
+        } else {
+            g->last_launches = n;
+            return CACSI_OK;
+        }
+    }
+    for (int t = 0; t < n_outer && e == cudaSuccess; t++)
+        e = cacsi::osem_outer(g, f, y, r, b1_subsets, pixels, offsets, n_subsets, beta_p, delta, l, b2, fnew, s, &n);
     if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
 }

@@ -130,6 +130,7 @@ struct cacsi_geometry {
     // per-kernel CUDA-event timing (cacsi_set_timing / cacsi_kernel_times)
     mutable int32_t timing;
     void *timers;  // cacsi::Timers*
+    void *osem_graph;  // cacsi::OsemGraph*: the captured outer iteration of cacsi_osem (api.cu)
 };
 
 namespace cacsi {
@@ -176,6 +177,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 int pcv_row_blocks(const cacsi_geometry *g);
+void osem_graph_free(cacsi_geometry *g);
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
 cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 
