@@ -788,7 +788,7 @@ __global__ void k_pc_perm(const Params p, const Esai e, int R, int win, const ui
         const size_t l0 = (size_t)v * p.det_nx;
         const long long a = e.pc_off[l0 + s * R], z = e.pc_off[l0 + min(p.det_nx, (s + 1) * R)];
         for (long long w0 = a + (long long)win * lane; w0 < z; w0 += (long long)win * 32) {
-            const int n = (int)min((long long)win, z - w0), ng = n >> 5;
+            const int n = (int)min((long long)win, z - w0), ng = 4;
 
             uint8_t cb[4][32], cq[4][32], fill[4];
             for (int g = 0; g < 4; g++) {
@@ -800,11 +800,12 @@ __global__ void k_pc_perm(const Params p, const Esai e, int R, int win, const ui
                 const int b = (int)(k >> e.pc_tbits) & 31, qq = (int)q_in[w0 + i] & 31;
                 int best = -1, bs = 1 << 30;
                 for (int g = 0; g < ng; g++)
-                    if (fill[g] < 32) {
+                    if (fill[g] < n / ng) {
                         const int sc = 2 * cb[g][b] + cq[g][qq];
                         if (sc < bs) { bs = sc; best = g; }
                     }
-                const long long o = w0 + best * 32 + fill[best];
+                // group g = the g-th record of every lane's 4 (lanes load 4 consecutive records)
+                const long long o = w0 + 4 * fill[best] + best;
                 fill[best]++;
                 cb[best][b]++;
                 cq[best][qq]++;
@@ -914,6 +915,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
     const QT *pq = (const QT *)e.pc_q;
+    const bool vec = e.pc_R > 0;  // bank-ordered layout: segments 128-record aligned (vector loads)
     if (tid == 0) {
         for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + i)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
@@ -952,35 +954,44 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             const float *Pb = e.pc_P + o0;
             const QT *qb = pq + o0;
             const int n = (int)(o1 - o0);
-            int i = tid;
-            for (; i + (U - 1) * PCV_T < n; i += U * PCV_T) {
-                uint32_t k[U], q[U];
-                float P[U];
+            // each thread takes 4 CONSECUTIVE records (16-byte vector loads); the bank-aware
+            // order puts record j of every lane's four in one conflict-light group, so the
+            // warp's j-th shared-memory access touches distinct banks
+            const uint32_t kpad = (uint32_t)(e.vwin[v].x & ~3) << tb;
+            for (int i = 4 * tid; i < n; i += 4 * PCV_T) {
+                uint32_t k[4], q[4];
+                float P[4];
+                if (vec && i + 3 < n) {
+                    const uint4 kv = __ldg((const uint4 *)(kb + i));
+                    const float4 pv = __ldg((const float4 *)(Pb + i));
+                    k[0] = kv.x, k[1] = kv.y, k[2] = kv.z, k[3] = kv.w;
+                    P[0] = pv.x, P[1] = pv.y, P[2] = pv.z, P[3] = pv.w;
+                    if (sizeof(QT) == 2) {
+                        const uint2 qv = __ldg((const uint2 *)(qb + i));
+                        q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
+                    } else {
+                        const uint4 qv = __ldg((const uint4 *)(qb + i));
+                        q[0] = qv.x, q[1] = qv.y, q[2] = qv.z, q[3] = qv.w;
+                    }
+                } else {
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    k[u] = __ldg(kb + i + u * PCV_T);
-                    P[u] = __ldg(Pb + i + u * PCV_T);
-                    q[u] = (uint32_t)__ldg(qb + i + u * PCV_T);
+                    for (int u = 0; u < 4; u++) {
+                        const bool in = i + u < n;
+                        k[u] = in ? __ldg(kb + i + u) : kpad;
+                        P[u] = in ? __ldg(Pb + i + u) : 0.0f;
+                        q[u] = in ? (uint32_t)__ldg(qb + i + u) : 0u;
+                    }
                 }
                 // P = 0: segment padding, whose pixel may repeat a real record's -- it
                 // adds into the lane's dummy slot past the row block (branch-free)
 #pragma unroll
-                for (int u = 0; u < U; u++) {
+                for (int u = 0; u < 4; u++) {
                     const int b = (int)(k[u] >> tb);
                     const float wa = wv[b], wb = wv[b + 1];
                     const float t = (float)(k[u] & tmask) * tunit;
                     float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
-            }
-            for (; i < n; i += PCV_T) {
-                const uint32_t k = __ldg(kb + i);
-                const float P = __ldg(Pb + i);
-                const int b = (int)(k >> tb);
-                const float wa = wv[b], wb = wv[b + 1];
-                const float t = (float)(k & tmask) * tunit;
-                float *ap = P != 0.0f ? accq + __ldg(qb + i) : dummy;
-                *ap = fmaf(P, fmaf(t, wb - wa, wa), *ap);
             }
             // this thread's reads of the W buffer (generic proxy) before its next
             // bulk copy (async proxy), then the barrier that hands it to thread 0
@@ -1144,15 +1155,32 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             const unsigned char *src = smb + st * SB;
             // this chunk's valid slots [lo, hi) (32-bit)
             const int lo = (int)max(o0 - a, 0ll), hi = (int)min(o1 - a, (long long)PBT_CH);
+            // each thread takes 4 CONSECUTIVE records (vector reads of the stage): record u of
+            // every lane's four forms one bank-aware group (k_pc_perm)
+            static_assert(PBT_U == 4, "4 consecutive records per thread");
             uint32_t k[PBT_U], q[PBT_U];
             float P[PBT_U];
+            {
+                const uint4 kv = ((const uint4 *)src)[tid];
+                const float4 pv = ((const float4 *)(src + PBT_CH * 4))[tid];
+                k[0] = kv.x, k[1] = kv.y, k[2] = kv.z, k[3] = kv.w;
+                P[0] = pv.x, P[1] = pv.y, P[2] = pv.z, P[3] = pv.w;
+                if (sizeof(QT) == 2) {
+                    const uint2 qv = ((const uint2 *)(src + PBT_CH * 8))[tid];
+                    q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
+                } else {
+                    const uint4 qv = ((const uint4 *)(src + PBT_CH * 8))[tid];
+                    q[0] = qv.x, q[1] = qv.y, q[2] = qv.z, q[3] = qv.w;
+                }
 #pragma unroll
-            for (int u = 0; u < PBT_U; u++) {
-                const int i = tid + u * PBT_T;
-                const bool in = i >= lo && i < hi;
-                k[u] = in ? ((const uint32_t *)src)[i] : kinv;
-                P[u] = in ? ((const float *)(src + PBT_CH * 4))[i] : 0.0f;
-                q[u] = in ? (uint32_t)((const QT *)(src + PBT_CH * 8))[i] : 0u;
+                for (int u = 0; u < PBT_U; u++) {
+                    const int i = 4 * tid + u;
+                    if (!(i >= lo && i < hi)) {
+                        k[u] = kinv;
+                        P[u] = 0.0f;
+                        q[u] = 0u;
+                    }
+                }
             }
             // every thread orders its reads (generic proxy) before the next bulk copy
             // into the stage (async proxy); then one arrival per warp
@@ -1539,7 +1567,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         for (size_t i = 0; i < nl; i++) {
             off[i + 1] = off[i] + hc[i];
             const int ix = (int)(i % p.det_nx);
-            if (segR > 0 && ((ix + 1) % segR == 0 || ix + 1 == p.det_nx)) off[i + 1] = (off[i + 1] + 31) & ~31ll;
+            if (segR > 0 && ((ix + 1) % segR == 0 || ix + 1 == p.det_nx)) off[i + 1] = (off[i + 1] + 127) & ~127ll;
         }
         const long long nrec = off[nl];
         size_t free_b = 0, total_b = 0;
@@ -1891,9 +1919,9 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
             const size_t hs = (size_t)E.max_win * sizeof(int);
             const char *bv = getenv("CACSI_PC_BWD");  // "flat": the register-fed kernel (A/B reference)
             if (!(bv && strcmp(bv, "flat") == 0)) {
-                // 256 threads x 3 records, two stages: ~49 KB of shared memory with the
+                // 256 threads x 4 records, two stages: ~49 KB of shared memory with the
                 // histogram, four CTAs per SM (measured best of 10 ring shapes)
-                constexpr int T = 256, U = 3, NS = 2;
+                constexpr int T = 256, U = 4, NS = 2;
                 auto kb = E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
                 const size_t sm = (size_t)NS * T * U * (8 + E.pc_qb) + 2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
