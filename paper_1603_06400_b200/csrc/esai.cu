@@ -1784,7 +1784,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
             const int R = (p.det_nx + n_rb - 1) / n_rb;
             const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
-            const int ipsm = is ? atoi(is) : 4;
+            const int ipsm = is ? atoi(is) : 2;
             int Sv = std::max(1, std::min(p.n_vox, (ipsm * sm_count(g->device) + n_rb - 1) / n_rb));
             const int vchunk = (p.n_vox + Sv - 1) / Sv;
             const int n_chunks = (p.n_vox + vchunk - 1) / vchunk;
