@@ -954,38 +954,42 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             const float *Pb = e.pc_P + o0;
             const QT *qb = pq + o0;
             const int n = (int)(o1 - o0);
-            // each thread takes 4 CONSECUTIVE records (16-byte vector loads); the bank-aware
-            // order puts record j of every lane's four in one conflict-light group, so the
-            // warp's j-th shared-memory access touches distinct banks
+            // each thread takes U CONSECUTIVE records (16-byte vector loads, U / 4 quads); the
+            // bank-aware order puts record j of every lane's quad in one conflict-light group,
+            // so the warp's j-th shared-memory access touches distinct banks
             const uint32_t kpad = (uint32_t)(e.vwin[v].x & ~3) << tb;
-            for (int i = 4 * tid; i < n; i += 4 * PCV_T) {
-                uint32_t k[4], q[4];
-                float P[4];
-                if (vec && i + 3 < n) {
-                    const uint4 kv = __ldg((const uint4 *)(kb + i));
-                    const float4 pv = __ldg((const float4 *)(Pb + i));
-                    k[0] = kv.x, k[1] = kv.y, k[2] = kv.z, k[3] = kv.w;
-                    P[0] = pv.x, P[1] = pv.y, P[2] = pv.z, P[3] = pv.w;
-                    if (sizeof(QT) == 2) {
-                        const uint2 qv = __ldg((const uint2 *)(qb + i));
-                        q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
-                    } else {
-                        const uint4 qv = __ldg((const uint4 *)(qb + i));
-                        q[0] = qv.x, q[1] = qv.y, q[2] = qv.z, q[3] = qv.w;
-                    }
-                } else {
+            for (int i = U * tid; i < n; i += U * PCV_T) {
+                uint32_t k[U], q[U];
+                float P[U];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const bool in = i + u < n;
-                        k[u] = in ? __ldg(kb + i + u) : kpad;
-                        P[u] = in ? __ldg(Pb + i + u) : 0.0f;
-                        q[u] = in ? (uint32_t)__ldg(qb + i + u) : 0u;
+                for (int h = 0; h < U; h += 4) {
+                    const int ih = i + h;
+                    if (vec && ih + 3 < n) {
+                        const uint4 kv = __ldg((const uint4 *)(kb + ih));
+                        const float4 pv = __ldg((const float4 *)(Pb + ih));
+                        k[h] = kv.x, k[h + 1] = kv.y, k[h + 2] = kv.z, k[h + 3] = kv.w;
+                        P[h] = pv.x, P[h + 1] = pv.y, P[h + 2] = pv.z, P[h + 3] = pv.w;
+                        if (sizeof(QT) == 2) {
+                            const uint2 qv = __ldg((const uint2 *)(qb + ih));
+                            q[h] = qv.x & 0xFFFFu, q[h + 1] = qv.x >> 16, q[h + 2] = qv.y & 0xFFFFu, q[h + 3] = qv.y >> 16;
+                        } else {
+                            const uint4 qv = __ldg((const uint4 *)(qb + ih));
+                            q[h] = qv.x, q[h + 1] = qv.y, q[h + 2] = qv.z, q[h + 3] = qv.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const bool in = ih + u < n;
+                            k[h + u] = in ? __ldg(kb + ih + u) : kpad;
+                            P[h + u] = in ? __ldg(Pb + ih + u) : 0.0f;
+                            q[h + u] = in ? (uint32_t)__ldg(qb + ih + u) : 0u;
+                        }
                     }
                 }
                 // P = 0: segment padding, whose pixel may repeat a real record's -- it
                 // adds into the lane's dummy slot past the row block (branch-free)
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
                     const float wa = wv[b], wb = wv[b + 1];
                     const float t = (float)(k[u] & tmask) * tunit;
@@ -1801,6 +1805,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int n_items = n_chunks * n_rb;
                 const char *us = getenv("CACSI_PCV_U");  // tuning knob (records per thread per step)
                 const int U = us ? atoi(us) : 4;
+                // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
                 auto kf = E.pc_qb == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024>
                                                     : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512> : k_pc_fwd_v<uint16_t, 4, 512>)
