@@ -1,0 +1,559 @@
+// pair_cache.cuh -- the pair-cache kernels: records built once at
+// create (k_pc_count, k_pc_fill, k_pc_perm) and streamed by the operators (the
+// voxel-major forward k_pc_fwd_v, its per-list fallback k_pc_fwd, the bulk-copy-ring
+// backward k_pc_bwd_tma and its register-fed reference k_pc_bwd).
+//
+// Not a self-contained header: esai.cu includes it inside namespace cacsi::{anonymous},
+// after the breakpoint-location helpers (locate_pair, load_bp, ...) it uses.
+#pragma once
+
+// bulk prefetch of [ptr, ptr + bytes) into L2 by the TMA unit (one thread issues
+// it; no registers, no completion to wait for): the next voxel's record ranges
+// are in L2 by the time the CTA's loads reach them
+__device__ __forceinline__ void l2_prefetch(const void *ptr, size_t bytes) {
+    uintptr_t a = (uintptr_t)ptr & ~(uintptr_t)15;
+    const uintptr_t end = ((uintptr_t)ptr + bytes + 15) & ~(uintptr_t)15;
+    while (a < end) {
+        const uint32_t n = (uint32_t)min((uintptr_t)65536, end - a);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+        a += n;
+    }
+}
+
+// ---- pair cache: the online/offline trade-off taken to HBM --
+// Every open pair's interpolation weights into the breakpoint basis depend on
+// the geometry only, so they can be computed ONCE at create and streamed by
+// every later operator call: per list (voxel v, detector row ix), the open
+// pixels in increasing jy, each a record of P (fp32), (b, tau) packed in 32 bits
+// (b in the high bits, tau in the remaining >= 16 fraction bits: |tau error| <=
+// 2^-(tbits+1), i.e. a weight error P |dtau| |W_{b+1} - W_b|, below fp32
+// rounding for tbits = 20) and the pixel q (2 bytes for n_det <= 65536, else
+// 4): 10 bytes per open pair on config 2 (5.8e8 pairs, 5.8 GB of 180 GB).  A
+// voxel's records are contiguous (lists v * det_nx + ix), so both operators
+// stream them flat.
+// The paper precomputes what is cheaper to load than to recompute ("if the cost
+// of computing the factor is equivalent to the speed of loading the factor from
+// main memory, then the computations should be performed online"); on a B200,
+// streaming 10 bytes is cheaper than the ~100 instructions of pair geometry and
+// breakpoint location.  Both operators read the same records: the forward by
+// (z, row, y) with the W gathers of one list on one W row, the backward by
+// voxel.  Built only if it fits (cacsi_query "pair_cache_records" > 0).
+
+// records per list (v, ix) = open pixels of row ix (transmission bitmap tb_bwd)
+__global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) {
+    const int nw = (p.n_det + 31) / 32;
+    const size_t n = (size_t)p.n_vox * p.det_nx;
+    for (size_t l = blockIdx.x * (size_t)blockDim.x + threadIdx.x; l < n; l += (size_t)gridDim.x * blockDim.x) {
+        const int v = (int)(l / p.det_nx), ix = (int)(l % p.det_nx);
+        const uint32_t *tb = e.tb_bwd + (size_t)v * nw;
+        const int q0 = ix * p.det_ny, q1 = q0 + p.det_ny;  // [q0, q1)
+        int c = 0;
+        for (int wd = q0 >> 5; wd <= (q1 - 1) >> 5; wd++) {
+            uint32_t m = __ldg(tb + wd);
+            const int lo = max(q0 - 32 * wd, 0), hi = min(q1 - 32 * wd, 32);  // bits [lo, hi)
+            m &= (hi == 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & (0xFFFFFFFFu << lo);
+            c += __popc(m);
+        }
+        cnt[l] = c;
+    }
+}
+
+// fill: one warp per list, 32 pixels per step, ballot-compacted records
+template <bool SAI, typename QT>
+__global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ bt,
+                                                 float *__restrict__ Pout, QT *__restrict__ qout) {
+    const float tone = (float)(1u << e.pc_tbits);
+    const uint32_t tmax = (1u << e.pc_tbits) - 1u;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sb = (float *)smem;
+    uint16_t *lut = (uint16_t *)(sb + e.nb + kLocD);
+    load_bp(e, sb, lut);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (p.n_det + 31) / 32;
+    const size_t n = (size_t)p.n_vox * p.det_nx;
+    for (size_t l = (size_t)blockIdx.x * 8 + warp; l < n; l += (size_t)gridDim.x * 8) {
+        const int v = (int)(l / p.det_nx), ix = (int)(l % p.det_nx);
+        const VoxelRec vr = p.vox[v];
+        long long base = e.pc_off[l];
+        for (int jy0 = 0; jy0 < p.det_ny; jy0 += 32) {
+            const int jy = jy0 + lane, q = ix * p.det_ny + jy;
+            const bool open = jy < p.det_ny && ((__ldg(e.tb_bwd + (size_t)v * nw + (q >> 5)) >> (q & 31)) & 1u);
+            float P = 0.0f, sh = 0.0f, t = 0.0f;
+            int b = 0;
+            if (open) {
+                pair_geom(p, vr, p.det[q], P, sh, !SAI);
+                b = locate_pair<SAI>(p, e, sb, lut, sh, v, q, t);
+            }
+            const uint32_t m = __ballot_sync(FULL, open);
+            if (open) {
+                const long long o = base + __popc(m & ((1u << lane) - 1u));
+                bt[o] = ((uint32_t)b << e.pc_tbits) | min(__float2uint_rn(t * tone), tmax);
+                Pout[o] = P;
+                qout[o] = (QT)q;
+            }
+            base += __popc(m);
+        }
+        // segment padding (last list of a segment): P = 0 records, bins spread over
+        // the voxel's window (their zero deposits must not pile onto one bank)
+        const long long end = e.pc_off[l + 1];
+        if (base < end) {
+            const int2 win = e.vwin[v];
+            const int span = max(1, win.y - win.x);
+            for (long long o = base + lane; o < end; o += 32) {
+                bt[o] = (uint32_t)(win.x + (int)((o - base) % span)) << e.pc_tbits;
+                Pout[o] = 0.0f;
+                qout[o] = (QT)(ix * p.det_ny);
+            }
+        }
+    }
+}
+
+// Bank-aware order (build time): within each 128-record window of a padded
+// segment, assign the records greedily to the window's 32-record groups (one
+// warp access each) so that within a group the breakpoint cells b (histogram /
+// W-window bank = b mod 32 up to a per-voxel shift) and the pixels q (forward
+// accumulator bank) repeat as little as possible.  One thread per window.
+template <typename QT>
+__global__ void k_pc_perm(const Params p, const Esai e, int R, int win, const uint32_t *__restrict__ bt_in,
+                          const float *__restrict__ P_in, const QT *__restrict__ q_in, uint32_t *__restrict__ bt_out,
+                          float *__restrict__ P_out, QT *__restrict__ q_out) {
+    const int nseg_v = (p.det_nx + R - 1) / R;
+    const size_t nseg = (size_t)p.n_vox * nseg_v;
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (size_t)blockDim.x) >> 5;
+    for (size_t sg = warp0; sg < nseg; sg += nwarps) {
+        const int v = (int)(sg / nseg_v), s = (int)(sg % nseg_v);
+        const size_t l0 = (size_t)v * p.det_nx;
+        const long long a = e.pc_off[l0 + s * R], z = e.pc_off[l0 + min(p.det_nx, (s + 1) * R)];
+        for (long long w0 = a + (long long)win * lane; w0 < z; w0 += (long long)win * 32) {
+            const int n = (int)min((long long)win, z - w0), ng = 4;
+
+            uint8_t cb[4][32], cq[4][32], fill[4];
+            for (int g = 0; g < 4; g++) {
+                fill[g] = 0;
+                for (int c = 0; c < 32; c++) cb[g][c] = cq[g][c] = 0;
+            }
+            for (int i = 0; i < n; i++) {
+                const uint32_t k = bt_in[w0 + i];
+                const int b = (int)(k >> e.pc_tbits) & 31, qq = (int)q_in[w0 + i] & 31;
+                int best = -1, bs = 1 << 30;
+                for (int g = 0; g < ng; g++)
+                    if (fill[g] < n / ng) {
+                        const int sc = 2 * cb[g][b] + cq[g][qq];
+                        if (sc < bs) { bs = sc; best = g; }
+                    }
+                // group g = the g-th record of every lane's 4 (lanes load 4 consecutive records)
+                const long long o = w0 + 4 * fill[best] + best;
+                fill[best]++;
+                cb[best][b]++;
+                cq[best][qq]++;
+                bt_out[o] = k;
+                P_out[o] = P_in[w0 + i];
+                q_out[o] = q_in[w0 + i];
+            }
+        }
+    }
+}
+
+// forward from the cache: items (z chunk, detector row); warps take voxel rows
+// y, lanes the list's records; per-warp row accumulators in shared memory (the
+// jy of one list are distinct: conflict-free, no atomics), fp64 partials per z chunk
+constexpr int PCF_W = 8;
+template <typename QT>
+__global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esai e, const float *__restrict__ W,
+                                                     int iz_per_chunk, int n_items, double *__restrict__ partial) {
+    extern __shared__ float acc_s[];  // [PCF_W][det_ny]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pc_q;
+    float *acc = acc_s + warp * p.det_ny;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int chunk = item / p.det_nx, ix = item % p.det_nx;
+        for (int i = lane; i < p.det_ny; i += 32) acc[i] = 0.0f;
+        __syncwarp();
+        const int iz0 = chunk * iz_per_chunk, iz1 = min(p.nz, iz0 + iz_per_chunk);
+        for (int iz = iz0; iz < iz1; iz++)
+            for (int iy = warp; iy < p.ny; iy += PCF_W) {
+                const int v = iy * p.nz + iz;
+                const size_t list = (size_t)v * p.det_nx + ix;
+                const long long o0 = e.pc_off[list], o1 = e.pc_off[list + 1];
+                const float *Wv = W + (size_t)v * e.ldw;
+                // four records per lane per step: their loads are issued together
+                // (memory-level parallelism); the jy of one list are distinct, so
+                // the four accumulator updates never alias
+                for (long long o = o0 + lane; o < o1; o += 128) {
+                    uint32_t k[4], jy[4];
+                    float P[4], wa[4], wb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const bool in = o + 32 * u < o1;
+                        k[u] = in ? __ldg(e.pc_bt + o + 32 * u) : 0u;
+                        P[u] = in ? __ldg(e.pc_P + o + 32 * u) : 0.0f;
+                        jy[u] = in ? (uint32_t)__ldg(pq + o + 32 * u) - (uint32_t)(ix * p.det_ny) : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float *wp = Wv + (k[u] >> tb);
+                        wa[u] = __ldg(wp);
+                        wb[u] = __ldg(wp + 1);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (o + 32 * u < o1) {
+                            const float t = (float)(k[u] & tmask) * tunit;
+                            float *ap = acc + jy[u];
+                            *ap = fmaf(P[u], fmaf(t, wb[u] - wa[u], wa[u]), *ap);
+                        }
+                }
+            }
+        __syncthreads();
+        for (int jy = threadIdx.x; jy < p.det_ny; jy += PCF_W * 32) {
+            double t = 0.0;
+            for (int ww = 0; ww < PCF_W; ww++) t += (double)acc_s[ww * p.det_ny + jy];
+            partial[(size_t)chunk * p.n_det + (size_t)ix * p.det_ny + jy] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// forward from the cache, voxel-major: items (voxel chunk, block of R detector
+// rows), chunks of consecutive voxels; per voxel the CTA holds the voxel's W
+// window in shared memory (one cp.async.bulk per voxel, issued a voxel ahead
+// into the other of two buffers, completion on an mbarrier) and streams the
+// voxel's records of those rows -- one contiguous range -- 4 per thread per
+// step; the W reads are shared-memory gathers and each record adds into the
+// CTA's row-block accumulator acc[q - q0].  The pixels of one voxel's records
+// are distinct (no two updates of one voxel alias); voxels are separated by a
+// barrier, so the sums are plain fp32 in a fixed order (deterministic).
+__device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, float *dst, uint64_t *mbar) {
+    const int2 win = e.vwin[v];
+    const int a = win.x & ~3;
+    const uint32_t bytes = (uint32_t)(((win.y + 1 - a) + 3) & ~3) * 4u;
+    const uint32_t mb = smem_u32(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(W + (size_t)v * e.ldw + a), "r"(bytes), "r"(mb)
+                 : "memory");
+}
+template <typename QT, int U, int PCV_T>
+__global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
+                                                     int R, int vchunk, int n_rb, int n_items, int pf,
+                                                     double *__restrict__ partial) {
+    extern __shared__ __align__(16) float smv[];
+    const int wcap = (e.max_win + 3 + 3) & ~3;
+    float *acc = smv;                                   // [R * det_ny] + 32 dummy slots
+    float *dummy = acc + R * p.det_ny + (threadIdx.x & 31);
+    float *ws = smv + ((R * p.det_ny + 32 + 3) & ~3);   // [2][wcap]
+    uint64_t *mbar = (uint64_t *)(ws + 2 * wcap);       // [2]
+    const int tid = threadIdx.x;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pc_q;
+    const bool vec = e.pc_R > 0;  // bank-ordered layout: segments 128-record aligned (vector loads)
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    __syncthreads();
+    uint32_t uses = 0;  // bit i: parity of buffer i's next completion
+    // gridDim.x = G n_rb: the CTA keeps ONE row block (blockIdx.x % n_rb) for all its
+    // voxel chunks, accumulates them in shared memory and writes one fp64 partial
+    // (index blockIdx.x / n_rb) at the end -- G partials, not one per chunk
+    const int rb = blockIdx.x % n_rb;
+    const int r0 = rb * R, r1 = min(p.det_nx, r0 + R);
+    const int q0 = r0 * p.det_ny, nacc = (r1 - r0) * p.det_ny;
+    for (int i = tid; i < nacc; i += PCV_T) acc[i] = 0.0f;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int c = item / n_rb;
+        const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);
+        if (tid == 0) pcv_stage(e, W, v0, ws, mbar);
+        for (int v = v0; v < v1; v++) {
+            const int buf = (v - v0) & 1;
+            if (tid == 0 && v + 1 < v1) pcv_stage(e, W, v + 1, ws + (buf ^ 1) * wcap, mbar + (buf ^ 1));
+            const size_t l0 = (size_t)v * p.det_nx;
+            const long long o0 = __ldg(e.pc_off + l0 + r0), o1 = __ldg(e.pc_off + l0 + r1);
+            if (tid == 0 && pf > 0 && v + pf < v1) {
+                const size_t l2 = (size_t)(v + pf) * p.det_nx;
+                const long long a0 = __ldg(e.pc_off + l2 + r0), a1 = __ldg(e.pc_off + l2 + r1);
+                l2_prefetch(e.pc_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
+                l2_prefetch(e.pc_P + a0, (size_t)(a1 - a0) * sizeof(float));
+                l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
+            }
+            mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
+            uses ^= 1u << buf;
+            const float *wv = ws + buf * wcap - (e.vwin[v].x & ~3);
+            float *accq = acc - q0;
+            // 32-bit indices from the voxel's first record; full steps unchecked, then the tail
+            const uint32_t *kb = e.pc_bt + o0;
+            const float *Pb = e.pc_P + o0;
+            const QT *qb = pq + o0;
+            const int n = (int)(o1 - o0);
+            // each thread takes U CONSECUTIVE records (16-byte vector loads, U / 4 quads); the
+            // bank-aware order puts record j of every lane's quad in one conflict-light group,
+            // so the warp's j-th shared-memory access touches distinct banks
+            const uint32_t kpad = (uint32_t)(e.vwin[v].x & ~3) << tb;
+            for (int i = U * tid; i < n; i += U * PCV_T) {
+                uint32_t k[U], q[U];
+                float P[U];
+#pragma unroll
+                for (int h = 0; h < U; h += 4) {
+                    const int ih = i + h;
+                    if (vec && ih + 3 < n) {
+                        const uint4 kv = __ldg((const uint4 *)(kb + ih));
+                        const float4 pv = __ldg((const float4 *)(Pb + ih));
+                        k[h] = kv.x, k[h + 1] = kv.y, k[h + 2] = kv.z, k[h + 3] = kv.w;
+                        P[h] = pv.x, P[h + 1] = pv.y, P[h + 2] = pv.z, P[h + 3] = pv.w;
+                        if (sizeof(QT) == 2) {
+                            const uint2 qv = __ldg((const uint2 *)(qb + ih));
+                            q[h] = qv.x & 0xFFFFu, q[h + 1] = qv.x >> 16, q[h + 2] = qv.y & 0xFFFFu, q[h + 3] = qv.y >> 16;
+                        } else {
+                            const uint4 qv = __ldg((const uint4 *)(qb + ih));
+                            q[h] = qv.x, q[h + 1] = qv.y, q[h + 2] = qv.z, q[h + 3] = qv.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const bool in = ih + u < n;
+                            k[h + u] = in ? __ldg(kb + ih + u) : kpad;
+                            P[h + u] = in ? __ldg(Pb + ih + u) : 0.0f;
+                            q[h + u] = in ? (uint32_t)__ldg(qb + ih + u) : 0u;
+                        }
+                    }
+                }
+                // P = 0: segment padding, whose pixel may repeat a real record's -- it
+                // adds into the lane's dummy slot past the row block (branch-free)
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int b = (int)(k[u] >> tb);
+                    const float wa = wv[b], wb = wv[b + 1];
+                    const float t = (float)(k[u] & tmask) * tunit;
+                    float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
+                    *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
+                }
+            }
+            // this thread's reads of the W buffer (generic proxy) before its next
+            // bulk copy (async proxy), then the barrier that hands it to thread 0
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+        }
+    }
+    for (int i = tid; i < nacc; i += PCV_T) partial[(size_t)(blockIdx.x / n_rb) * p.n_det + q0 + i] = (double)acc[i];
+}
+
+// backward from the cache: one CTA per voxel (grid-stride), warps take detector
+// rows, lanes the records; fixed-point deposits as k_esai_bwd (same scale rule)
+constexpr int PCB_T = 256;
+template <typename QT>
+__global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, const float *__restrict__ w,
+                                                  const float *__restrict__ wmax, int pf, float *__restrict__ A) {
+    extern __shared__ int hist_s[];  // [max_win]
+    const int tid = threadIdx.x;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pcb_q;
+    const float wm = *wmax;
+    for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        __syncthreads();
+        for (int i = tid; i < nwin; i += PCB_T) hist_s[i] = 0;
+        __syncthreads();
+        const double bound = (double)e.vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+        int *hv = hist_s - win.x;
+        // the voxel's records (all its lists) are one contiguous range, streamed flat
+        const long long o0 = __ldg(e.pc_off + (size_t)v * p.det_nx);
+        const long long o1 = scale > 0.0f ? __ldg(e.pc_off + (size_t)(v + 1) * p.det_nx) : o0;
+        for (long long o = o0 + tid; o < o1; o += 4 * PCB_T) {
+            if (tid == 0 && pf > 0) {
+                // rolling L2 prefetch of the records pf steps ahead
+                const long long a0 = o + (long long)pf * 4 * PCB_T, a1 = min(o1, a0 + 4 * PCB_T);
+                if (a0 < a1) {
+                    l2_prefetch(e.pcb_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
+                    l2_prefetch(e.pcb_P + a0, (size_t)(a1 - a0) * sizeof(float));
+                    l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
+                }
+            }
+            uint32_t k[4], q[4];
+            float P[4], wq[4];
+            // branch-free: slots past the end deposit zero into the window's first bin
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool in = o + u * PCB_T < o1;
+                k[u] = in ? __ldg(e.pcb_bt + o + u * PCB_T) : ((uint32_t)win.x << tb);
+                P[u] = in ? __ldg(e.pcb_P + o + u * PCB_T) : 0.0f;
+                q[u] = in ? (uint32_t)__ldg(pq + o + u * PCB_T) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) wq[u] = __ldg(w + q[u]) * scale;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                // the pair's P w scale split exactly between bins b and b + 1
+                const int b = (int)(k[u] >> tb);
+                const float a = P[u] * wq[u];
+                const int x1 = __float2int_rn(a * ((float)(k[u] & tmask) * tunit));
+                atomicAdd(hv + b, __float2int_rn(a) - x1);
+                atomicAdd(hv + b + 1, x1);
+            }
+        }
+        __syncthreads();
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = tid; b < e.ldw; b += PCB_T) {
+            const int i = b - win.x;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist_s[i] * unit : 0.0f;
+        }
+    }
+}
+
+// backward from the cache with the records fed through shared memory: thread 0
+// streams the CTA's chunks (PBT_CH records, 16-byte-aligned groups of 8) with
+// cp.async.bulk into a PBT_NS-stage ring ("full" mbarrier: bytes landed;
+// "empty" mbarrier: every warp has read the stage), PBT_NS - 1 chunks ahead of
+// the consumers and across voxel boundaries; the threads only gather w and
+// deposit.  Same deposits and order-free integer sums as k_pc_bwd.
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS>
+__global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
+                                                      const float *__restrict__ wmax, float *__restrict__ A) {
+    extern __shared__ __align__(16) unsigned char smb[];
+    constexpr int PBT_CH = PBT_T * PBT_U;
+    constexpr int SB = PBT_CH * (8 + (int)sizeof(QT));
+    uint64_t *full = (uint64_t *)(smb + PBT_NS * SB);
+    uint64_t *empty = full + PBT_NS;
+    int *hist_s = (int *)(empty + PBT_NS);
+    const int tid = threadIdx.x;
+    const int tb = e.pc_tbits;
+    const uint32_t tmask = (1u << tb) - 1u;
+    const float tunit = 1.0f / (float)(1u << tb);
+    const QT *pq = (const QT *)e.pcb_q;
+    const float wm = *wmax;
+    if (tid == 0) {
+        for (int i = 0; i < PBT_NS; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(PBT_T / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    __syncthreads();
+    // producer state (thread 0): voxel pv, next chunk start pa, range end pe, chunks issued
+    int pv = blockIdx.x;
+    long long pa = 0, pe = 0;
+    uint32_t issued = 0;
+    if (tid == 0 && pv < p.n_vox) {
+        pa = __ldg(e.pc_off + (size_t)pv * p.det_nx) & ~7ll;
+        pe = __ldg(e.pc_off + (size_t)(pv + 1) * p.det_nx);
+    }
+    auto produce = [&](uint32_t limit) {
+        while (issued < limit) {
+            while (pv < p.n_vox && pa >= pe) {
+                pv += gridDim.x;
+                if (pv < p.n_vox) {
+                    pa = __ldg(e.pc_off + (size_t)pv * p.det_nx) & ~7ll;
+                    pe = __ldg(e.pc_off + (size_t)(pv + 1) * p.det_nx);
+                }
+            }
+            if (pv >= p.n_vox) return;
+            const int st = issued % PBT_NS;
+            const uint32_t use = issued / PBT_NS;
+            if (use > 0) mbar_wait(smem_u32(empty + st), (use - 1) & 1);
+            const uint32_t n = (uint32_t)((min((long long)PBT_CH, pe - pa) + 7) & ~7ll);
+            const uint32_t mb = smem_u32(full + st);
+            unsigned char *dst = smb + st * SB;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"(n * (8u + (uint32_t)sizeof(QT))));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst)), "l"(e.pcb_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst + PBT_CH * 4)), "l"(e.pcb_P + pa), "r"(n * 4u), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
+            pa += PBT_CH;
+            issued++;
+        }
+    };
+    if (tid == 0) produce(PBT_NS - 1);
+    uint32_t consumed = 0;
+    for (int v = blockIdx.x; v < p.n_vox; v += gridDim.x) {
+        const int2 win = e.vwin[v];
+        const int nwin = win.y - win.x + 1;
+        for (int i = tid; i < nwin; i += PBT_T) hist_s[i] = 0;
+        __syncthreads();
+        const double bound = (double)e.vbound[v] * (double)wm;
+        const float scale = bound > 0.0 ? (float)(1073741824.0 / bound) : 0.0f;
+        int *hv = hist_s - win.x;
+        const long long o0 = __ldg(e.pc_off + (size_t)v * p.det_nx), o1 = __ldg(e.pc_off + (size_t)(v + 1) * p.det_nx);
+        // slots outside the voxel's range deposit zero (branch-free) into lane-spread bins,
+        // not all into one address
+        const uint32_t kinv = (uint32_t)(win.x + (tid & 31) % max(1, nwin - 1)) << tb;
+        for (long long a = o0 & ~7ll; a < o1; a += PBT_CH) {
+            if (tid == 0) produce(consumed + PBT_NS);
+            const int st = consumed % PBT_NS;
+            mbar_wait(smem_u32(full + st), (consumed / PBT_NS) & 1);
+            const unsigned char *src = smb + st * SB;
+            // this chunk's valid slots [lo, hi) (32-bit)
+            const int lo = (int)max(o0 - a, 0ll), hi = (int)min(o1 - a, (long long)PBT_CH);
+            // each thread takes 4 CONSECUTIVE records (vector reads of the stage): record u of
+            // every lane's four forms one bank-aware group (k_pc_perm)
+            static_assert(PBT_U == 4, "4 consecutive records per thread");
+            uint32_t k[PBT_U], q[PBT_U];
+            float P[PBT_U];
+            {
+                const uint4 kv = ((const uint4 *)src)[tid];
+                const float4 pv = ((const float4 *)(src + PBT_CH * 4))[tid];
+                k[0] = kv.x, k[1] = kv.y, k[2] = kv.z, k[3] = kv.w;
+                P[0] = pv.x, P[1] = pv.y, P[2] = pv.z, P[3] = pv.w;
+                if (sizeof(QT) == 2) {
+                    const uint2 qv = ((const uint2 *)(src + PBT_CH * 8))[tid];
+                    q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
+                } else {
+                    const uint4 qv = ((const uint4 *)(src + PBT_CH * 8))[tid];
+                    q[0] = qv.x, q[1] = qv.y, q[2] = qv.z, q[3] = qv.w;
+                }
+#pragma unroll
+                for (int u = 0; u < PBT_U; u++) {
+                    const int i = 4 * tid + u;
+                    if (!(i >= lo && i < hi)) {
+                        k[u] = kinv;
+                        P[u] = 0.0f;
+                        q[u] = 0u;
+                    }
+                }
+            }
+            // every thread orders its reads (generic proxy) before the next bulk copy
+            // into the stage (async proxy); then one arrival per warp
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + st)) : "memory");
+            consumed++;
+            float wq[PBT_U];
+#pragma unroll
+            for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]) * scale;
+#pragma unroll
+            for (int u = 0; u < PBT_U; u++) {
+                const int b = (int)(k[u] >> tb);
+                const float av = P[u] * wq[u];
+                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                atomicAdd(hv + b, __float2int_rn(av) - x1);
+                atomicAdd(hv + b + 1, x1);
+            }
+        }
+        __syncthreads();
+        const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
+        // whole rows (zeros outside the window): writing only the tile's chunk range that
+        // the b2 GEMM reads measured slower (gaps between the rows of neighbouring voxels)
+        float *Ar = A + (size_t)v * e.ldw;
+        for (int b = tid; b < e.ldw; b += PBT_T) {
+            const int i = b - win.x;
+            Ar[b] = (i >= 0 && i < nwin) ? (float)hist_s[i] * unit : 0.0f;
+        }
+        __syncthreads();
+    }
+}
+
