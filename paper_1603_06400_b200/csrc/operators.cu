@@ -33,10 +33,15 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
                                                    void *__restrict__ partial) {
     extern __shared__ float4 smem4[];
     const int Q = p.nq, K = p.ne, Q3 = Q + 3;
-    const int K4 = (K + FWD_KU - 1) / FWD_KU * FWD_KU;
+    // energy rows padded so that every unrolled batch stays inside: a batch starts at most
+    // at whi <= K - 1 and reads FWD_KU (+ 1 for the even start of the pair layout) rows
+    const int K4 = (K + 2 * FWD_KU) / FWD_KU * FWD_KU;
     float2 *en = (float2 *)smem4;          // [K4] (alpha_k, c_k), padded with copies of the last energy
     float2 *tab = en + K4;                 // [VC][Q + 3] (mid, slope), entry n at index n + 2
-    float *acc_s = (float *)(tab + FWD_VC * Q3 + (FWD_VC * Q3 & 1));  // RES: [K4][FWD_T]
+    // RES: accumulators as energy pairs [K4 / 2][FWD_T] float2 (one 8-byte read-modify-write per two
+    // terms), alpha_k [K4] padded with 1e30 (a padding energy's u clamps onto the zero entry)
+    float2 *acc2 = (float2 *)(tab + FWD_VC * Q3 + (FWD_VC * Q3 & 1));
+    float *alpha = (float *)(acc2 + (RES ? (K4 / 2) * FWD_T : 0));
     const int tid = threadIdx.x;
     const int pix = blockIdx.x * FWD_T + tid;
     const bool valid = pix < p.n_det;
@@ -44,8 +49,10 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
     const int v0 = blockIdx.y * vox_per_split;
     const int v1 = min(p.n_vox, v0 + vox_per_split);
     for (int k = tid; k < K4; k += FWD_T) en[k] = p.energy[min(k, K - 1)];
-    if (RES)
-        for (int k = 0; k < K4; k++) acc_s[k * FWD_T + tid] = 0.0f;
+    if (RES) {
+        for (int k = tid; k < K4; k += FWD_T) alpha[k] = k < K ? p.energy[k].x : 1e30f;
+        for (int k = 0; k < K4 / 2; k++) acc2[k * FWD_T + tid] = make_float2(0.0f, 0.0f);
+    }
     double tot = 0.0;
     for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
         const int nc = min(FWD_VC, v1 - c0);
@@ -87,20 +94,23 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
                 // are independent (no read-after-write through shared memory
                 // between them), so their latencies overlap; the accumulator
                 // rows are padded to a multiple of FWD_KU (acc_s has K4 rows)
-                for (int k = wlo; k <= whi; k += FWD_KU) {
-                    float tt[FWD_KU], a[FWD_KU];
-                    float2 t[FWD_KU];
+                for (int k = wlo & ~1; k <= whi; k += FWD_KU) {
+                    // energies past the lanes' windows (and the padding) land on the zero
+                    // entries of the clamped hat table: no predicate needed
+                    float tt[FWD_KU];
+                    float2 t[FWD_KU], a[FWD_KU / 2];
 #pragma unroll
                     for (int j = 0; j < FWD_KU; j++) {
-                        const int n = hat_coord(p, en[k + j].x, sh, tt[j]);
+                        const int n = hat_coord(p, alpha[k + j], sh, tt[j]);
                         t[j] = tv[n];
-                        a[j] = acc_s[(k + j) * FWD_T + tid];
                     }
 #pragma unroll
-                    for (int j = 0; j < FWD_KU; j++) {
-                        // energies past the window end: P is applied only inside it
-                        const float Pj = (k + j <= whi) ? P : 0.0f;
-                        acc_s[(k + j) * FWD_T + tid] = fmaf(Pj, fmaf(tt[j], t[j].y, t[j].x), a[j]);
+                    for (int j = 0; j < FWD_KU / 2; j++) a[j] = acc2[((k >> 1) + j) * FWD_T + tid];
+#pragma unroll
+                    for (int j = 0; j < FWD_KU / 2; j++) {
+                        a[j].x = fmaf(P, fmaf(tt[2 * j], t[2 * j].y, t[2 * j].x), a[j].x);
+                        a[j].y = fmaf(P, fmaf(tt[2 * j + 1], t[2 * j + 1].y, t[2 * j + 1].x), a[j].y);
+                        acc2[((k >> 1) + j) * FWD_T + tid] = a[j];
                     }
                 }
             }
@@ -116,7 +126,8 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
         const int npx = min(FWD_T, p.n_det - (int)blockIdx.x * FWD_T);
         for (int i = tid; i < npx * K; i += FWD_T) {
             const int px = i / K, k = i - px * K;
-            out[i] = en[k].y * acc_s[k * FWD_T + px];
+            const float2 a2 = acc2[(k >> 1) * FWD_T + px];
+            out[i] = en[k].y * ((k & 1) ? a2.y : a2.x);
         }
     }
 }
@@ -333,9 +344,9 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     S = (p.n_vox + vps - 1) / vps;
     const size_t n_out = (size_t)p.n_det * (res ? p.ne : 1);
     const size_t part_bytes = (size_t)S * n_out * (res ? sizeof(float) : sizeof(double));
-    const size_t K4 = (size_t)(p.ne + FWD_KU - 1) / FWD_KU * FWD_KU;
+    const size_t K4 = (size_t)(p.ne + 2 * FWD_KU) / FWD_KU * FWD_KU;  // as in k_forward
     size_t smem = K4 * sizeof(float2) + (size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2);
-    if (res) smem += K4 * FWD_T * sizeof(float);
+    if (res) smem += K4 * FWD_T * sizeof(float) + K4 * sizeof(float);
     void *part = nullptr;
     cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
     if (e != cudaSuccess) return e;
