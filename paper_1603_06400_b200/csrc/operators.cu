@@ -267,7 +267,9 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_c(const Params p, const f
             const float2 en_k = en[k];
             float tt;
             const int n = hat_coord(p, en_k.x, e.sh, tt);
-            const float ca = (k >= klo && k <= khi) ? e.P * en_k.y * __ldg(wp + (size_t)k * p.n_det) : 0.0f;
+            // no window test: a term outside this lane's [klo, khi] has its hat coordinate
+            // clamped onto the padding rows (node -2 / nq), which the readout skips
+            const float ca = e.P * en_k.y * __ldg(wp + (size_t)k * p.n_det);
             const float hi = fmaf(tt, ca, 0.5f * ca);
             float *h0 = hb + (n + 2) * BWD_T;
             h0[0] += ca - hi;
