@@ -694,20 +694,67 @@ __global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ A1, in
     }
 }
 
-__global__ void k_sum_parts_f64(const double *__restrict__ part, int S, size_t n, float *__restrict__ out) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int j = 0; j < S; j++) s += part[j * n + i];
-        out[i] = (float)s;
+// out[i] = sum_j part[j][i] (j < S), in double, in a fixed order: warp w of the block
+// sums the slices j = w, w + 8, ... in increasing j for SP_U x 32 outputs (coalesced
+// loads, SP_U x 2 in flight per thread), then one thread per output adds the 8
+// warp sums in warp order -- deterministic, and the S-long loop is split 8 ways
+// (a thread per output walking all S slices was latency-bound: 0.033 ms for
+// S = 296 on config 1)
+constexpr int SP_U = 2;
+template <typename T>
+__global__ void __launch_bounds__(256) k_sum_parts(const T *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+    __shared__ double red[8][32 * SP_U];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t i0 = (size_t)blockIdx.x * (32 * SP_U);
+    double acc[SP_U];
+#pragma unroll
+    for (int u = 0; u < SP_U; u++) acc[u] = 0.0;
+    int j = warp;
+    for (; j + 8 < S; j += 16) {
+        T x[SP_U], y[SP_U];
+#pragma unroll
+        for (int u = 0; u < SP_U; u++) {
+            const size_t i = i0 + lane + 32 * u;
+            x[u] = i < n ? part[(size_t)j * n + i] : (T)0;
+            y[u] = i < n ? part[(size_t)(j + 8) * n + i] : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < SP_U; u++) acc[u] = (acc[u] + (double)x[u]) + (double)y[u];
+    }
+    if (j < S) {
+#pragma unroll
+        for (int u = 0; u < SP_U; u++) {
+            const size_t i = i0 + lane + 32 * u;
+            acc[u] += i < n ? (double)part[(size_t)j * n + i] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < SP_U; u++) red[warp][lane + 32 * u] = acc[u];
+    __syncthreads();
+    if (threadIdx.x < 32 * SP_U && i0 + threadIdx.x < n) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) t += red[w][threadIdx.x];
+        out[i0 + threadIdx.x] = (float)t;
     }
 }
-
-__global__ void k_sum_parts_f32(const float *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+// few slices or many outputs (the b2 split-K partials: 2M outputs on config 2, where
+// the thread-per-output loop already streams at ~4.6 TB/s): one thread per output
+// walks the slices in order
+template <typename T>
+__global__ void k_sum_parts_seq(const T *__restrict__ part, int S, size_t n, float *__restrict__ out) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int j = 0; j < S; j++) s += (double)part[j * n + i];
         out[i] = (float)s;
     }
+}
+template <typename T>
+void sum_parts(const T *part, int S, size_t n, float *out, cudaStream_t s) {
+    if (S >= 16 && n < 200000)
+        k_sum_parts<T><<<(unsigned)((n + 32 * SP_U - 1) / (32 * SP_U)), 256, 0, s>>>(part, S, n, out);
+    else
+        k_sum_parts_seq<T><<<(unsigned)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S, n, out);
 }
 
 int sm_count(int dev) {
@@ -1182,11 +1229,15 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int mp = (int)(mt_even / 2);
                 cudaFuncSetAttribute(k_tc_gemm_ar2, cudaFuncAttributeMaxDynamicSharedMemorySize, tca2_smem(nkcA));
                 const int npairs = std::max(1, std::min(mp * nt, sm_count(g->device) / 2));
-                k_tc_gemm_ar2<<<2 * npairs, TCA_T, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
+                k_tc_gemm_ar2<<<2 * npairs, TCA_T1, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
                                                                         E.ldw);
             } else if (nkcA <= 4 && !(gv && strcmp(gv, "tiles") == 0)) {
-                cudaFuncSetAttribute(k_tc_gemm_ar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA));
-                k_tc_gemm_ar<<<std::min(mt * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA), s>>>(
+                // B ring depth: 3 stages where they fit beside the resident A panel (nkc <= 2), else 2
+                // (config 2, nq = 128: nkc = 4, the 128 KB panel leaves room for 2)
+                const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
+                auto kar = nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>;
+                cudaFuncSetAttribute(kar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA, nsb));
+                kar<<<std::min(mt * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
                     p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw);
             } else {
                 dim3 gg(nt, mt, 1);
@@ -1312,7 +1363,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     }
     if (e == cudaSuccess) {
         KScope kt_(g, s, "k_sum_parts_f64");
-        k_sum_parts_f64<<<(p.n_det + 255) / 256, 256, 0, s>>>(part, S, p.n_det, out);
+        sum_parts(part, S, (size_t)p.n_det, out, s);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     *launches += 3;
@@ -1430,7 +1481,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         const size_t n = (size_t)p.n_vox * p.nq;
         {
             KScope kt_(g, s, "k_sum_parts_f32");
-            k_sum_parts_f32<<<(int)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S_eff, n, b);
+            sum_parts(part, S_eff, n, b, s);
         }
         e = cudaGetLastError();
         *launches += 4;

@@ -319,21 +319,21 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
 // shared buffer -> coalesced row stores), so loads, MMAs and stores of
 // consecutive tiles overlap.  Barriers: a_full / a_empty (panel), b_full /
 // b_empty (ring), t_full / t_empty (accumulators).
-constexpr int TCA_T = 192;   // warp roles of k_tc_gemm_ar2 (4 epilogue warps)
-constexpr int TCA_T1 = 320;  // k_tc_gemm_ar: 8 epilogue warps
-constexpr int tca_smem(int nkc) { return nkc * TC_STAGE / 2 + TC_STAGE + 8 * 32 * 33 * 4 + 1024 + 256; }
+constexpr int TCA_T1 = 320;  // k_tc_gemm_ar / _ar2: 8 epilogue warps
+constexpr int tca_smem(int nkc, int nsb = 2) { return nkc * TC_STAGE / 2 + nsb * TC_STAGE / 2 + 8 * 32 * 33 * 4 + 1024 + 256; }
+template <int NSB>
 __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
                                                          const float *__restrict__ Ap, const float *__restrict__ Bt,
                                                          float *__restrict__ C, int ldc) {
     extern __shared__ __align__(1024) unsigned char tca_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                              // [nkc][hi, lo] 32 KB each
-    unsigned char *sB = sA + nkc * (TC_STAGE / 2);         // [2][hi, lo]
-    float *ebuf = (float *)(sB + TC_STAGE);                // [8][32][33]
+    unsigned char *sB = sA + nkc * (TC_STAGE / 2);         // [NSB][hi, lo]
+    float *ebuf = (float *)(sB + NSB * (TC_STAGE / 2));    // [8][32][33]
     uint64_t *bars = (uint64_t *)(ebuf + 8 * 32 * 33);
-    uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 4, *t_full = bars + 6,
-             *t_empty = bars + 8;
-    uint32_t *tmem_slot = (uint32_t *)(bars + 10);
+    uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 2 + NSB,
+             *t_full = bars + 2 + 2 * NSB, *t_empty = bars + 4 + 2 * NSB;
+    uint32_t *tmem_slot = (uint32_t *)(bars + 6 + 2 * NSB);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long T = (long long)mtiles * ntiles;
     const int t0 = (int)(T * blockIdx.x / gridDim.x), t1 = (int)(T * (blockIdx.x + 1) / gridDim.x);
@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 32) {
-        for (int i = 0; i < 10; i++)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 8 ? 8 : 1));
+        for (int i = 0; i < 6 + 2 * NSB; i++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 4 + 2 * NSB ? 8 : 1));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -374,8 +374,8 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                     loads++;
                 }
                 for (int c = 0; c < nkc; c++, bc++) {
-                    const int st = bc & 1;
-                    if (bc >= 2) mbar_wait(smem_u32(b_empty + st), ((bc >> 1) - 1) & 1);
+                    const int st = bc % NSB;
+                    if (bc >= NSB) mbar_wait(smem_u32(b_empty + st), ((bc / NSB) - 1) & 1);
                     const uint32_t mb = smem_u32(b_full + st);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(CHB)
                                  : "memory");
@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const uint32_t dmain = tmem + ab * 2 * TC_N, dcross = dmain + TC_N;
                 for (int c = 0; c < nkc; c++, bc++) {
-                    const int st = bc & 1;
-                    mbar_wait(smem_u32(b_full + st), (bc >> 1) & 1);
+                    const int st = bc % NSB;
+                    mbar_wait(smem_u32(b_full + st), (bc / NSB) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n");
                     const uint32_t ah0 = smem_u32(sA + c * CHB), al0 = ah0 + TC_OPB;
                     const uint32_t bh0 = smem_u32(sB + st * CHB), bl0 = bh0 + TC_OPB;
@@ -449,8 +449,15 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
 #pragma unroll 1
             for (int c0 = ch; c0 < ch + TC_N / 2; c0 += 32) {
                 __syncwarp();
+                // row `lane` of the 32 x 32 block as 8 float4, 16-byte chunk j at j ^ (lane & 7):
+                // the stores (8 lanes span all 32 banks) and the row reads below are conflict-free
 #pragma unroll
-                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
+                for (int j = 0; j < 8; j++)
+                    *(float4 *)(buf + lane * 32 + 4 * (j ^ (lane & 7))) =
+                        make_float4(__uint_as_float(r[4 * j]) + __uint_as_float(x[4 * j]),
+                                    __uint_as_float(r[4 * j + 1]) + __uint_as_float(x[4 * j + 1]),
+                                    __uint_as_float(r[4 * j + 2]) + __uint_as_float(x[4 * j + 2]),
+                                    __uint_as_float(r[4 * j + 3]) + __uint_as_float(x[4 * j + 3]));
                 if (c0 + 32 < ch + TC_N / 2) {
                     tmem_ld32(tbase + c0 + 32, r);
                     tmem_ld32(tbase + TC_N + c0 + 32, x);
@@ -462,12 +469,14 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                     const int rr = 4 * i + (lane >> 3);
                     const int grow = m0 + lq * 32 + rr;
                     if (grow < M && nn < N) {
-                        const float *br = buf + rr * 33 + cq;
+                        const float4 v4 = *(const float4 *)(buf + rr * 32 + 4 * ((lane & 7) ^ (rr & 7)));
                         float *dst = C + (size_t)grow * ldc + nn;
                         if (nn + 4 <= N && (ldc & 3) == 0)
-                            *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
-                        else
-                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
+                            *(float4 *)dst = v4;
+                        else {
+                            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = vv[j];
+                        }
                     }
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
 // CTAs' barriers by multicast; both epilogues arrive on the leader's t_empty.
 constexpr int TCA2_NS = 4;
 constexpr int TCA2_HB = TC_OPB / 2;  // one 64-row half of a 128 x 32 operand tile (8 KB)
-constexpr int tca2_smem(int nkc) { return nkc * TC_STAGE / 2 + TCA2_NS * 2 * TCA2_HB + 4 * 32 * 33 * 4 + 1024 + 256; }
+constexpr int tca2_smem(int nkc) { return nkc * TC_STAGE / 2 + TCA2_NS * 2 * TCA2_HB + 8 * 32 * 33 * 4 + 1024 + 256; }
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -534,15 +543,15 @@ __device__ __forceinline__ void tc_commit2_mc(uint32_t bar) {
 __host__ __device__ constexpr uint32_t tc_idesc_tf32_m256() {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T1, 1)
     k_tc_gemm_ar2(int M, int N, int nkc, int mpairs, int ntiles, const float *__restrict__ Ap,
                   const float *__restrict__ Bt, float *__restrict__ C, int ldc) {
     extern __shared__ __align__(1024) unsigned char tca_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                                  // [nkc][hi, lo] 32 KB each
     unsigned char *sB = sA + nkc * (TC_STAGE / 2);             // [NS][hi, lo] 8 KB each
-    float *ebuf = (float *)(sB + TCA2_NS * 2 * TCA2_HB);       // [4][32][33]
-    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    float *ebuf = (float *)(sB + TCA2_NS * 2 * TCA2_HB);       // [8][32][33]
+    uint64_t *bars = (uint64_t *)(ebuf + 8 * 32 * 33);
     uint64_t *a_full = bars, *a_empty = bars + 1, *pa_full = bars + 2, *t_full = bars + 3, *t_empty = bars + 5,
              *b_full = bars + 7, *b_empty = b_full + TCA2_NS, *pb_full = b_empty + TCA2_NS;
     uint32_t *tmem_slot = (uint32_t *)(pb_full + TCA2_NS);
@@ -563,7 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(pa_full)));
         for (int i = 0; i < 2; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(t_full + i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(t_empty + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 16;\n" ::"r"(smem_u32(t_empty + i)));
         }
         for (int i = 0; i < TCA2_NS; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b_full + i)));
@@ -677,7 +686,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
             }
         }
     } else {
-        float *buf = ebuf + warp * (32 * 33);
+        // epilogue warps 0-3 and 6-9 (as in k_tc_gemm_ar): TMEM lanes 32 (warp % 4) ..,
+        // warps 0-3 drain columns 0-63, warps 6-9 columns 64-127
+        const int ew = warp < 4 ? warp : warp - 2, lq = warp & 3, ch = warp < 4 ? 0 : TC_N / 2;
+        float *buf = ebuf + ew * (32 * 33);
         const int cq = 4 * (lane & 7);
         uint32_t tc = 0;
         for (int t = t0; t < t1; t++, tc++) {
@@ -686,17 +698,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
             mbar_wait(smem_u32(t_full + ab), (tc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const int m0 = (2 * mp + (int)rank) * TC_M, n0 = n * TC_N;
-            const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 2 * TC_N);
+            const uint32_t tbase = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(ab * 2 * TC_N);
             uint32_t r[32], x[32];
-            tmem_ld32(tbase, r);
-            tmem_ld32(tbase + TC_N, x);
+            tmem_ld32(tbase + ch, r);
+            tmem_ld32(tbase + TC_N + ch, x);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll 1
-            for (int c0 = 0; c0 < TC_N; c0 += 32) {
+            for (int c0 = ch; c0 < ch + TC_N / 2; c0 += 32) {
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 32; j++) buf[lane * 33 + j] = __uint_as_float(r[j]) + __uint_as_float(x[j]);
-                if (c0 + 32 < TC_N) {
+                for (int j = 0; j < 8; j++)
+                    *(float4 *)(buf + lane * 32 + 4 * (j ^ (lane & 7))) =
+                        make_float4(__uint_as_float(r[4 * j]) + __uint_as_float(x[4 * j]),
+                                    __uint_as_float(r[4 * j + 1]) + __uint_as_float(x[4 * j + 1]),
+                                    __uint_as_float(r[4 * j + 2]) + __uint_as_float(x[4 * j + 2]),
+                                    __uint_as_float(r[4 * j + 3]) + __uint_as_float(x[4 * j + 3]));
+                if (c0 + 32 < ch + TC_N / 2) {
                     tmem_ld32(tbase + c0 + 32, r);
                     tmem_ld32(tbase + TC_N + c0 + 32, x);
                 }
@@ -705,14 +722,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TCA_T, 1)
 #pragma unroll 4
                 for (int i = 0; i < 8; i++) {
                     const int rr = 4 * i + (lane >> 3);
-                    const int grow = m0 + warp * 32 + rr;
+                    const int grow = m0 + lq * 32 + rr;
                     if (grow < M && nn < N) {
-                        const float *br = buf + rr * 33 + cq;
+                        const float4 v4 = *(const float4 *)(buf + rr * 32 + 4 * ((lane & 7) ^ (rr & 7)));
                         float *dst = C + (size_t)grow * ldc + nn;
                         if (nn + 4 <= N && (ldc & 3) == 0)
-                            *(float4 *)dst = make_float4(br[0], br[1], br[2], br[3]);
-                        else
-                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = br[j];
+                            *(float4 *)dst = v4;
+                        else {
+                            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+                            for (int j = 0; j < 4 && nn + j < N; j++) dst[j] = vv[j];
+                        }
                     }
                 }
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");

@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--kernels", action="store_true", help="also print per-kernel averages (forward and backward)")
     args = ap.parse_args()
     out = {}
     for ci in [int(c) for c in args.configs.split(",")]:
@@ -41,6 +42,12 @@ def main():
             G.backward(w, b)
         tf = time_op(lambda: G.forward(f, g), args.reps)
         tb = time_op(lambda: G.backward(w, b), args.reps)
+        if args.kernels:
+            G.kernel_times()
+            G.set_timing(True)
+            time_op(lambda: (G.forward(f, g), G.backward(w, b)), args.reps)
+            G.set_timing(False)
+            print(json.dumps({k: round(v[0] / max(v[1], 1), 4) for k, v in G.kernel_times().items()}), flush=True)
         pairs = cfg.n_vox * cfg.n_det
         out[ci] = dict(fwd_ms=tf[len(tf) // 2], bwd_ms=tb[len(tb) // 2], pairs=pairs,
                        fwd_pairs_per_s=pairs / tf[len(tf) // 2] * 1e3, bwd_pairs_per_s=pairs / tb[len(tb) // 2] * 1e3,
