@@ -380,6 +380,33 @@ cacsi_status cacsi_neg_loglik(const cacsi_geometry *g, const float *f, const flo
     return cacsi_neg_loglik_ex(g, f, y, r, beta, nullptr, out_dev, ws, stream);
 }
 
+// One Alg. 5 iteration f -> f_new.  ESAI handles run it fused: the
+// forward's final partial sum writes w = y ./ (A f + r) and max |w| into *wmax_scratch,
+// the backward's final sum the update (Eq. f_update) -- the same bits as the unfused
+// forward -> ratio -> backward -> update sequence the other handles run.  wait_yr /
+// wait_b1 (optional): events the ratio / the update must wait for (staged inputs).
+static cudaError_t iterate_once(const cacsi_geometry *g, const float *fc, const float *y, const float *r,
+                                const float *b1, float beta, double delta, float *fn, float *l, float *b2,
+                                float *wmax_scratch, cudaStream_t s, int *n, cudaEvent_t wait_yr, cudaEvent_t wait_b1) {
+    cudaError_t e = cudaSuccess;
+    if (g->esai.enabled) {
+        if (wait_yr) e = cudaStreamWaitEvent(s, wait_yr, 0);
+        if (e == cudaSuccess) e = cudaMemsetAsync(wmax_scratch, 0, sizeof(float), s);
+        if (e == cudaSuccess) e = cacsi::esai_forward_ratio(g, fc, cacsi::FwdRatioEpi{y, r, wmax_scratch}, l, s, n);
+        if (e == cudaSuccess && wait_b1) e = cudaStreamWaitEvent(s, wait_b1, 0);
+        const cacsi::BwdUpdateEpi up{wmax_scratch, fc, b1, beta, delta, fn};
+        if (e == cudaSuccess) e = cacsi::esai_backward_masked(g, l, nullptr, b2, s, n, nullptr, 0, &up);
+        return e;
+    }
+    e = cacsi::launch_forward(g, fc, l, s, n);                                     // z = A f (+ r below)
+    if (e == cudaSuccess && wait_yr) e = cudaStreamWaitEvent(s, wait_yr, 0);
+    if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, n);  // y ./ z
+    if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, n);             // b2 = A^T (y ./ z)
+    if (e == cudaSuccess && wait_b1) e = cudaStreamWaitEvent(s, wait_b1, 0);
+    if (e == cudaSuccess) e = cacsi::launch_update(g, fc, b1, b2, beta, delta, fn, s, n);  // Eq. f_update
+    return e;
+}
+
 cacsi_status cacsi_iterate_ex(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
                               float beta, const cacsi_penalty *pen, int32_t n_iter, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1 || !ws) return CACSI_ERR_NULL;
@@ -391,13 +418,13 @@ cacsi_status cacsi_iterate_ex(const cacsi_geometry *g, float *f, const float *y,
     cudaStream_t s = (cudaStream_t)stream;
     int n = 0;
     cudaError_t e = cudaSuccess;
+    // ping-pong between f and fnew; an odd iteration count ends with one copy back into f
+    float *fc = f, *fn = fnew;
     for (int t = 0; t < n_iter && e == cudaSuccess; t++) {
-        e = cacsi::launch_forward(g, f, l, s, &n);                                   // z = A f (+ r below)
-        if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, y, r, l, nullptr, 0, s, &n);  // y ./ z
-        if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, &n);           // b2 = A^T (y ./ z)
-        if (e == cudaSuccess) e = cacsi::launch_update(g, f, b1, b2, beta, delta, fnew, s, &n);  // Eq. f_update
-        if (e == cudaSuccess) e = cudaMemcpyAsync(f, fnew, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
+        e = iterate_once(g, fc, y, r, b1, beta, delta, fn, l, b2, (float *)part, s, &n, nullptr, nullptr);
+        std::swap(fc, fn);
     }
+    if (e == cudaSuccess && fc != f) e = cudaMemcpyAsync(f, fc, g->n_obj * sizeof(float), cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) g->last_launches = n;
     return map_err(e);
 }
@@ -659,12 +686,8 @@ cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float 
     float *fc = g->d_stage_a, *fn = fnew;  // ping-pong: no device copy between iterations
     int n = 0;
     for (int t = 0; t < n_iter && e == cudaSuccess; t++) {
-        e = cacsi::launch_forward(g, fc, l, s, &n);
-        if (e == cudaSuccess && t == 0) e = cudaStreamWaitEvent(s, g->stage_ev[1], 0);
-        if (e == cudaSuccess) e = cacsi::launch_ratio(g, l, g->d_stage_b, g->d_stage_c, l, nullptr, 0, s, &n);
-        if (e == cudaSuccess) e = cacsi::launch_backward(g, l, b2, s, &n);
-        if (e == cudaSuccess && t == 0) e = cudaStreamWaitEvent(s, g->stage_ev[2], 0);
-        if (e == cudaSuccess) e = cacsi::launch_update(g, fc, g->d_stage_d, b2, beta, 0.0, fn, s, &n);
+        e = iterate_once(g, fc, g->d_stage_b, g->d_stage_c, g->d_stage_d, beta, 0.0, fn, l, b2, (float *)part, s, &n,
+                         t == 0 ? g->stage_ev[1] : nullptr, t == 0 ? g->stage_ev[2] : nullptr);
         std::swap(fc, fn);
     }
     if (e == cudaSuccess && n_iter == 0) e = cudaStreamWaitEvent(s, g->stage_ev[2], 0);

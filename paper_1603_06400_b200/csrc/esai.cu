@@ -694,6 +694,53 @@ __global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ A1, in
     }
 }
 
+#include "elementwise.cuh"
+
+// What the final partial sum t_i = sum_j part[j][i] writes: the operator output
+// (EpiStore), or -- inside cacsi_iterate -- the ratio w_i = y_i / (t_i + r_i) and
+// max |w| (EpiRatio, for the backward's fixed-point scale), or the f update with
+// b2_i = t_i (EpiUpdate).  The stand-alone kernels (k_ratio, k_absmax, k_update)
+// compute the same bits from the stored t_i (elementwise.cuh).
+struct EpiStore {
+    float *out;
+    static constexpr bool kMax = false;
+    __device__ float operator()(size_t i, double t) const {
+        out[i] = (float)t;
+        return 0.0f;
+    }
+};
+struct EpiRatio {
+    const float *y, *r;
+    float *out;
+    unsigned *wmax;  // bits of max |w| (non-negative floats order as unsigned); zeroed by the caller
+    static constexpr bool kMax = true;
+    __device__ float operator()(size_t i, double t) const {
+        const float v = guarded_ratio(y[i], (float)t + r[i]);
+        out[i] = v;
+        return fabsf(v);
+    }
+};
+struct EpiUpdate {
+    Params p;
+    const float *f_hat, *b1;
+    float beta;
+    double delta;
+    float *f_new;
+    static constexpr bool kMax = false;
+    __device__ float operator()(size_t i, double t) const {
+        f_new[i] = update_at(p, f_hat, b1, (float)t, beta, delta, (unsigned)i);
+        return 0.0f;
+    }
+};
+template <class Epi>
+__device__ __forceinline__ void epi_max(const Epi &epi, float m) {
+    if constexpr (Epi::kMax) {
+        // fmaxf drops NaN (as k_absmax does); one atomic per warp
+        const unsigned bits = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(m));
+        if ((threadIdx.x & 31) == 0 && bits != 0u) atomicMax(epi.wmax, bits);
+    }
+}
+
 // out[i] = sum_j part[j][i] (j < S), in double, in a fixed order: warp w of the block
 // sums the slices j = w, w + 8, ... in increasing j for SP_U x 32 outputs (coalesced
 // loads, SP_U x 2 in flight per thread), then one thread per output adds the 8
@@ -701,8 +748,8 @@ __global__ void __launch_bounds__(256) k_vbound(const float *__restrict__ A1, in
 // (a thread per output walking all S slices was latency-bound: 0.033 ms for
 // S = 296 on config 1)
 constexpr int SP_U = 2;
-template <typename T>
-__global__ void __launch_bounds__(256) k_sum_parts(const T *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+template <typename T, class Epi>
+__global__ void __launch_bounds__(256) k_sum_parts(const T *__restrict__ part, int S, size_t n, Epi epi) {
     __shared__ double red[8][32 * SP_U];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t i0 = (size_t)blockIdx.x * (32 * SP_U);
@@ -731,30 +778,34 @@ __global__ void __launch_bounds__(256) k_sum_parts(const T *__restrict__ part, i
 #pragma unroll
     for (int u = 0; u < SP_U; u++) red[warp][lane + 32 * u] = acc[u];
     __syncthreads();
+    float m = 0.0f;
     if (threadIdx.x < 32 * SP_U && i0 + threadIdx.x < n) {
         double t = 0.0;
 #pragma unroll
         for (int w = 0; w < 8; w++) t += red[w][threadIdx.x];
-        out[i0 + threadIdx.x] = (float)t;
+        m = epi(i0 + threadIdx.x, t);
     }
+    epi_max(epi, m);
 }
 // few slices or many outputs (the b2 split-K partials: 2M outputs on config 2, where
 // the thread-per-output loop already streams at ~4.6 TB/s): one thread per output
 // walks the slices in order
-template <typename T>
-__global__ void k_sum_parts_seq(const T *__restrict__ part, int S, size_t n, float *__restrict__ out) {
+template <typename T, class Epi>
+__global__ void k_sum_parts_seq(const T *__restrict__ part, int S, size_t n, Epi epi) {
+    float m = 0.0f;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int j = 0; j < S; j++) s += (double)part[j * n + i];
-        out[i] = (float)s;
+        m = fmaxf(m, epi(i, s));
     }
+    epi_max(epi, m);
 }
-template <typename T>
-void sum_parts(const T *part, int S, size_t n, float *out, cudaStream_t s) {
+template <typename T, class Epi>
+void sum_parts(const T *part, int S, size_t n, Epi epi, cudaStream_t s) {
     if (S >= 16 && n < 200000)
-        k_sum_parts<T><<<(unsigned)((n + 32 * SP_U - 1) / (32 * SP_U)), 256, 0, s>>>(part, S, n, out);
+        k_sum_parts<T, Epi><<<(unsigned)((n + 32 * SP_U - 1) / (32 * SP_U)), 256, 0, s>>>(part, S, n, epi);
     else
-        k_sum_parts_seq<T><<<(unsigned)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S, n, out);
+        k_sum_parts_seq<T, Epi><<<(unsigned)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S, n, epi);
 }
 
 int sm_count(int dev) {
@@ -1158,7 +1209,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
 }
 
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
-                                     float *out, cudaStream_t s, int *launches);
+                                     float *out, cudaStream_t s, int *launches, const FwdRatioEpi *epi = nullptr);
 
 // Row blocks of the voxel-major pair-cache forward (0: the W windows do not fit
 // shared memory, the per-list kernel runs).  One 1024-thread CTA per SM with a
@@ -1187,8 +1238,13 @@ cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int
     return esai_forward_impl(g, f, pixels, n, out, s, launches);
 }
 
+cudaError_t esai_forward_ratio(const cacsi_geometry *g, const float *f, const FwdRatioEpi &epi, float *w,
+                               cudaStream_t s, int *launches) {
+    return esai_forward_impl(g, f, nullptr, 0, w, s, launches, &epi);
+}
+
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
-                                     float *out, cudaStream_t s, int *launches) {
+                                     float *out, cudaStream_t s, int *launches, const FwdRatioEpi *epi) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *W = nullptr;
@@ -1363,7 +1419,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     }
     if (e == cudaSuccess) {
         KScope kt_(g, s, "k_sum_parts_f64");
-        sum_parts(part, S, (size_t)p.n_det, out, s);
+        if (epi)
+            sum_parts(part, S, (size_t)p.n_det, EpiRatio{epi->y, epi->r, out, (unsigned *)epi->wmax}, s);
+        else
+            sum_parts(part, S, (size_t)p.n_det, EpiStore{out}, s);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     *launches += 3;
@@ -1398,7 +1457,8 @@ static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uin
 }
 
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
-                                 cudaStream_t s, int *launches, const int32_t *list, int n_list) {
+                                 cudaStream_t s, int *launches, const int32_t *list, int n_list,
+                                 const BwdUpdateEpi *epi) {
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
@@ -1409,7 +1469,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     const int S_eff = (nkc + cps - 1) / cps;
     cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.ldw * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
-    if (e == cudaSuccess) e = cudaMallocAsync(&wmax, sizeof(float), s);
+    if (e == cudaSuccess && !epi) e = cudaMallocAsync(&wmax, sizeof(float), s);
     // the contraction: the persistent split-K GEMM skips each tile's chunks outside the
     // union of its voxels' windows (A is zero there); the per-tile GEMM reads whole rows
     const int mt = (p.n_vox + TC_M - 1) / TC_M;
@@ -1418,7 +1478,9 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     const bool splitk = p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
                         tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw);
     if (e == cudaSuccess) {
-        {
+        if (epi) {
+            wmax = (float *)epi->wmax;  // computed by the fused forward (not freed here)
+        } else {
             KScope kt_(g, s, "k_absmax");
             k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, pmask, wmax);
         }
@@ -1481,12 +1543,15 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         const size_t n = (size_t)p.n_vox * p.nq;
         {
             KScope kt_(g, s, "k_sum_parts_f32");
-            sum_parts(part, S_eff, n, b, s);
+            if (epi)
+                sum_parts(part, S_eff, n, EpiUpdate{p, epi->f_hat, epi->b1, epi->beta, epi->delta, epi->f_new}, s);
+            else
+                sum_parts(part, S_eff, n, EpiStore{b}, s);
         }
         e = cudaGetLastError();
-        *launches += 4;
+        *launches += epi ? 3 : 4;
     }
-    if (wmax) cudaFreeAsync(wmax, s);
+    if (wmax && !epi) cudaFreeAsync(wmax, s);
     if (part) cudaFreeAsync(part, s);
     if (A) cudaFreeAsync(A, s);
     return e;

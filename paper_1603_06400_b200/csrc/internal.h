@@ -172,8 +172,27 @@ cudaError_t launch_backward_subset(const cacsi_geometry *g, const float *w, cons
                                    cudaStream_t s, int *launches);
 cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n, float *out,
                               cudaStream_t s, int *launches);
+// Fused epilogues of cacsi_iterate on ESAI handles: the forward's final partial sum
+// writes w = y ./ (A f + r) and max |w| (as unsigned bits; *wmax zeroed by the
+// caller) instead of A f; the backward takes that max (no k_absmax) and its final
+// partial sum writes the f update (Eq. f_update) instead of b2.  Same bits as the
+// unfused forward -> k_ratio -> backward -> k_update sequence (elementwise.cuh).
+struct FwdRatioEpi {
+    const float *y, *r;
+    float *wmax;
+};
+struct BwdUpdateEpi {
+    const float *wmax;
+    const float *f_hat, *b1;
+    float beta;
+    double delta;
+    float *f_new;
+};
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
-                                 cudaStream_t s, int *launches, const int32_t *list = nullptr, int n_list = 0);
+                                 cudaStream_t s, int *launches, const int32_t *list = nullptr, int n_list = 0,
+                                 const BwdUpdateEpi *epi = nullptr);
+cudaError_t esai_forward_ratio(const cacsi_geometry *g, const float *f, const FwdRatioEpi &epi, float *w,
+                               cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 int pcv_row_blocks(const cacsi_geometry *g);

@@ -16,11 +16,7 @@ namespace {
 constexpr int RT = 256;          // threads per reduction / elementwise block
 constexpr int RED_BLOCKS = 592;  // fixed partial count (4 x 148)
 
-__device__ __forceinline__ float guarded_ratio(float y, float z) {
-    // y/z; 0 where y = 0 and z = 0; y / 1e-12 where z = 0 < y (reading R14/SPEC.md:452)
-    if (z > 0.0f) return y / z;
-    return y > 0.0f ? y * 1e12f : 0.0f;
-}
+#include "elementwise.cuh"
 
 __global__ void k_ratio(const float *__restrict__ l, const float *__restrict__ y, const float *__restrict__ r,
                         float *__restrict__ out, size_t n) {
@@ -53,24 +49,6 @@ __global__ void __launch_bounds__(RT) k_loglik_part(const float *__restrict__ l,
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-// Edge-preserving potential (Eq. 7): psi, psi_dot and the
-// surrogate curvature omega = psi_dot / x.  delta <= 0
-// selects the quadratic psi(x) = x^2/2 (reading R13), else Huber (R21).
-__device__ __forceinline__ double pen_psi(double x, double delta) {
-    const double ax = fabs(x);
-    return (delta <= 0.0 || ax <= delta) ? 0.5 * x * x : delta * ax - 0.5 * delta * delta;
-}
-__device__ __forceinline__ void pen_dot_omega(double x, double delta, double &pd, double &om) {
-    const double ax = fabs(x);
-    if (delta <= 0.0 || ax <= delta) {
-        pd = x;
-        om = 1.0;
-    } else {
-        pd = x > 0.0 ? delta : -delta;
-        om = delta / ax;
-    }
-}
-
 // partial[blockIdx] = sum over elements j of sum_{k in N_j} psi(f_j - f_k)
 __global__ void __launch_bounds__(RT) k_penalty_part(const Params p, const float *__restrict__ f, double delta,
                                                      double *partial) {
@@ -101,44 +79,11 @@ __global__ void k_loglik_final(const double *lpart, const double *rpart, int nb,
     }
 }
 
-// Eq. f_update, 4-connected (y, z) neighbours, w = 1,
-// symmetric (N^b = N, so b4 = b3 and b6 = b5):
-//   b3 = 2 sum_k omega(f^_j - f^_k),  b5 = sum_k psi_dot(f^_j - f^_k)
-//   chi1 = beta (b3 + b4),  chi2 = b1 + beta (-f^ (b3 + b4) + b5 + b6),  chi3 = f^ b2
-// (quadratic psi: chi1 = 4 beta |N_j|, chi2 = b1 - 2 beta (|N_j| f^ + sum_k f^_k)).
-// root = 2 chi3 / (chi2 + sqrt(D)) if chi2 > 0 (same number as the paper's
-// (-chi2 + sqrt D)/(2 chi1), no cancellation), else (-chi2 + sqrt D)/(2 chi1);
-// chi1 = 0 and chi2 <= 0 (voxel never seen): keep f^ (reading R14).
 __global__ void k_update(const Params p, const float *__restrict__ f_hat, const float *__restrict__ b1,
                          const float *__restrict__ b2, float beta, double delta, float *__restrict__ f_new) {
-    // 32-bit index arithmetic (n_vox * nq < 2^31, checked at create): the 64-bit
-    // divisions of the neighbour indexing dominated this kernel
     const unsigned n = (unsigned)p.n_vox * (unsigned)p.nq;
-    const unsigned sz = (unsigned)p.nq, sy = (unsigned)p.nz * (unsigned)p.nq;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned vq = i / sz;  // voxel index iy * nz + iz
-        const int iy = (int)(vq / (unsigned)p.nz), iz = (int)(vq - (unsigned)iy * (unsigned)p.nz);
-        const double fj = f_hat[i];
-        double som = 0.0, spd = 0.0, pd, om;
-        if (iy > 0) { pen_dot_omega(fj - f_hat[i - sy], delta, pd, om); som += om; spd += pd; }
-        if (iy + 1 < p.ny) { pen_dot_omega(fj - f_hat[i + sy], delta, pd, om); som += om; spd += pd; }
-        if (iz > 0) { pen_dot_omega(fj - f_hat[i - sz], delta, pd, om); som += om; spd += pd; }
-        if (iz + 1 < p.nz) { pen_dot_omega(fj - f_hat[i + sz], delta, pd, om); som += om; spd += pd; }
-        const double bt = beta;
-        const double b34 = 4.0 * som, b56 = 2.0 * spd;
-        const double chi1 = bt * b34;
-        const double chi2 = (double)b1[i] + bt * (-fj * b34 + b56);
-        const double chi3 = fj * (double)b2[i];
-        const double sq = sqrt(fmax(chi2 * chi2 + 4.0 * chi1 * chi3, 0.0));
-        double x;
-        if (chi2 > 0.0)
-            x = 2.0 * chi3 / (chi2 + sq);
-        else if (chi1 > 0.0)
-            x = (-chi2 + sq) / (2.0 * chi1);
-        else
-            x = fj;
-        f_new[i] = (float)x;
-    }
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        f_new[i] = update_at(p, f_hat, b1, b2[i], beta, delta, i);
 }
 
 int grid_for(size_t n) { return (int)min((n + RT - 1) / RT, (size_t)RED_BLOCKS * 4); }

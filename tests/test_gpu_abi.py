@@ -157,6 +157,39 @@ def test_iterate_host_matches_device_iterate(n_iter):
     G.close()
 
 
+@pytest.mark.parametrize("ci,delta", [(1, 0.0), (1, 0.05), (2, 0.0)])
+def test_fused_iterate_matches_operator_sequence(ci, delta):
+    """cacsi_iterate on an ESAI handle fuses the ratio (and max |w|) into the
+    forward's final partial sum and the update into the backward's: the iterate
+    is bit-identical to calling cacsi_forward, cacsi_ratio, cacsi_backward and
+    cacsi_update in turn (two iterations: the ping-pong buffers are exercised)."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    rng = np.random.default_rng(21)
+    f0 = rng.uniform(0.5, 1.5, G.f_shape).astype(np.float32)
+    y = torch.as_tensor(rng.poisson(50.0, G.g_shape).astype(np.float32)).cuda()
+    r = torch.full(G.g_shape, 2.0, device="cuda")
+    b1 = torch.as_tensor(rng.uniform(1.0, 2.0, G.f_shape).astype(np.float32)).cuda()
+    beta = 1e-3
+    pen = ("huber", delta) if delta > 0.0 else ("quadratic", 0.0)
+    fd = torch.as_tensor(f0).cuda()
+    ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
+    G.iterate_ex(fd, y, r, b1, beta, pen, 2, ws)
+    fs = torch.as_tensor(f0).cuda()
+    l = torch.empty(G.g_shape, device="cuda")
+    b2 = torch.empty(G.f_shape, device="cuda")
+    fn = torch.empty(G.f_shape, device="cuda")
+    for _ in range(2):
+        G.forward(fs, l)
+        G.ratio(l, y, r, l)
+        G.backward(l, b2)
+        G.update_ex(fs, b1, b2, beta, pen, fn)
+        fs.copy_(fn)
+    torch.cuda.synchronize()
+    assert torch.equal(fd, fs)
+    G.close()
+
+
 def test_subset_backward_list_matches_mask(monkeypatch):
     """The list-driven subset backward (warp per voxel over the listed pixels)
     and the bitmap-masked one deposit the same integers: bit-identical."""
