@@ -314,6 +314,8 @@ void cacsi_geometry_destroy(cacsi_geometry *g) {
     if (g->stage_stream) cudaStreamDestroy(g->stage_stream);
     for (int i = 0; i < 3; i++)
         if (g->stage_ev[i]) cudaEventDestroy(g->stage_ev[i]);
+    for (int i = 0; i < 4; i++)
+        if (g->stage_fev[i]) cudaEventDestroy(g->stage_fev[i]);
     free_all(g);
     free(g);
 }
@@ -387,12 +389,16 @@ cacsi_status cacsi_neg_loglik(const cacsi_geometry *g, const float *f, const flo
 // wait_b1 (optional): events the ratio / the update must wait for (staged inputs).
 static cudaError_t iterate_once(const cacsi_geometry *g, const float *fc, const float *y, const float *r,
                                 const float *b1, float beta, double delta, float *fn, float *l, float *b2,
-                                float *wmax_scratch, cudaStream_t s, int *n, cudaEvent_t wait_yr, cudaEvent_t wait_b1) {
+                                float *wmax_scratch, cudaStream_t s, int *n, cudaEvent_t wait_yr, cudaEvent_t wait_b1,
+                                const cudaEvent_t *f_ready = nullptr, int f_chunks = 0) {
     cudaError_t e = cudaSuccess;
     if (g->esai.enabled) {
-        if (wait_yr) e = cudaStreamWaitEvent(s, wait_yr, 0);
-        if (e == cudaSuccess) e = cudaMemsetAsync(wmax_scratch, 0, sizeof(float), s);
-        if (e == cudaSuccess) e = cacsi::esai_forward_ratio(g, fc, cacsi::FwdRatioEpi{y, r, wmax_scratch}, l, s, n);
+        e = cudaMemsetAsync(wmax_scratch, 0, sizeof(float), s);
+        cacsi::FwdRatioEpi fe{y, r, wmax_scratch};
+        fe.f_ready = f_ready;
+        fe.f_chunks = f_chunks;
+        fe.yr_ready = wait_yr;  // y, r are read only by the forward's final sum
+        if (e == cudaSuccess) e = cacsi::esai_forward_ratio(g, fc, fe, l, s, n);
         if (e == cudaSuccess && wait_b1) e = cudaStreamWaitEvent(s, wait_b1, 0);
         const cacsi::BwdUpdateEpi up{wmax_scratch, fc, b1, beta, delta, fn};
         if (e == cudaSuccess) e = cacsi::esai_backward_masked(g, l, nullptr, b2, s, n, nullptr, 0, &up);
@@ -666,14 +672,31 @@ cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float 
         e = cudaStreamCreateWithFlags(&gm->stage_stream, cudaStreamNonBlocking);
         for (int i = 0; i < 3 && e == cudaSuccess; i++)
             e = cudaEventCreateWithFlags(&gm->stage_ev[i], cudaEventDisableTiming);
+        for (int i = 0; i < 4 && e == cudaSuccess; i++)
+            e = cudaEventCreateWithFlags(&gm->stage_fev[i], cudaEventDisableTiming);
     }
     if (e != cudaSuccess) return map_err(e);
     cudaStream_t s2 = g->stage_stream;
-    // f first on the caller's stream (the forward needs only f); y, r, then b1 on the
-    // side stream, overlapping the forward -- the ratio waits for y, r, the update for b1
+    // the side stream first waits for the caller's earlier work (it may still read the
+    // staging buffers), then uploads f, y, r, b1 in that order.  ESAI handles: f in four
+    // row chunks, the forward's W GEMM starting on each as it lands; others: f whole
+    // before the forward.  The ratio waits for y, r, the update for b1.
+    const bool fchunks = g->esai.enabled && n_iter > 0;
+    const int nfc = fchunks ? 4 : 0;
     e = cudaEventRecord(g->stage_ev[0], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, g->stage_ev[0], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    if (fchunks) {
+        const size_t rows = (size_t)cacsi::fchunk_rows(g->p.n_vox, nfc), row_b = (size_t)g->p.nq * 4;
+        for (int c = 0; c < nfc && e == cudaSuccess; c++) {
+            const size_t r0 = std::min((size_t)g->p.n_vox, c * rows), r1 = std::min((size_t)g->p.n_vox, r0 + rows);
+            if (r1 > r0)
+                e = cudaMemcpyAsync((char *)g->d_stage_a + r0 * row_b, (const char *)fh + r0 * row_b, (r1 - r0) * row_b,
+                                    cudaMemcpyHostToDevice, s2);
+            if (e == cudaSuccess) e = cudaEventRecord(g->stage_fev[c], s2);
+        }
+    } else {
+        e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
+    }
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, yh, g->n_detout * 4, cudaMemcpyHostToDevice, s2);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_c, rh, g->n_detout * 4, cudaMemcpyHostToDevice, s2);
     if (e == cudaSuccess) e = cudaEventRecord(g->stage_ev[1], s2);
@@ -687,7 +710,8 @@ cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float 
     int n = 0;
     for (int t = 0; t < n_iter && e == cudaSuccess; t++) {
         e = iterate_once(g, fc, g->d_stage_b, g->d_stage_c, g->d_stage_d, beta, 0.0, fn, l, b2, (float *)part, s, &n,
-                         t == 0 ? g->stage_ev[1] : nullptr, t == 0 ? g->stage_ev[2] : nullptr);
+                         t == 0 ? g->stage_ev[1] : nullptr, t == 0 ? g->stage_ev[2] : nullptr,
+                         t == 0 ? g->stage_fev : nullptr, t == 0 ? nfc : 0);
         std::swap(fc, fn);
     }
     if (e == cudaSuccess && n_iter == 0) e = cudaStreamWaitEvent(s, g->stage_ev[2], 0);

@@ -1267,12 +1267,43 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         return e;
     }
     const int nkcA = ldf / TC_KC;
-    {
+    const char *gv0 = getenv("CACSI_WGEMM");
+    const bool ar_path = ((E.pc && pixels == nullptr) || pixels != nullptr) && nkcA <= 4 &&
+                         !(gv0 && (strcmp(gv0, "ar2") == 0 || strcmp(gv0, "tiles") == 0));
+    const int nfc = (epi && epi->f_chunks > 0) ? epi->f_chunks : 0;
+    if (nfc > 0 && !ar_path)
+        for (int c = 0; c < nfc && e == cudaSuccess; c++) e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
+    if (nfc > 0 && ar_path) {
+        // f staged from the host in row chunks: pack + W GEMM per chunk as it lands, so the
+        // upload of chunk c + 1 overlaps the contraction of chunk c (cacsi_iterate_host)
+        const int rows = fchunk_rows(p.n_vox, nfc), nt = tc_ntiles(E.nb, TC_N);
+        const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
+        auto kar = nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>;
+        cudaFuncSetAttribute(kar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA, nsb));
+        for (int c = 0; c < nfc && e == cudaSuccess; c++) {
+            const int r0 = c * rows;
+            e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
+            if (r0 >= p.n_vox || e != cudaSuccess) continue;
+            const int nr = std::min(rows, p.n_vox - r0), mtc = (nr + TC_M - 1) / TC_M;
+            float *fpc = fp + (size_t)(r0 / TC_M) * nkcA * (2 * TC_M * TC_KC);
+            {
+                KScope kt_(g, s, "k_tc_pack_a");
+                k_tc_pack_a<<<4 * sm_count(g->device), 256, 0, s>>>(f + (size_t)r0 * p.nq, nr, p.nq, p.nq, nkcA, fpc);
+            }
+            {
+                KScope kt_(g, s, "k_tc_gemm_W");
+                kar<<<std::min(mtc * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
+                    nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw);
+            }
+            *launches += 2;
+        }
+        *launches -= 2;  // counted again below (pack + GEMM)
+    } else {
         // f -> pre-split (TF32 hi / lo), pre-swizzled A tiles: the GEMM lands them by bulk copy
         KScope kt_(g, s, "k_tc_pack_a");
         k_tc_pack_a<<<4 * sm_count(g->device), 256, 0, s>>>(f, p.n_vox, p.nq, p.nq, nkcA, fp);
     }
-    {
+    if (!(nfc > 0 && ar_path)) {
         // W[v][b] = sum_j f[v][j] S~[b][j] on the tensor cores (3xTF32)
         KScope kt_(g, s, "k_tc_gemm_W");
         if ((E.pc && pixels == nullptr) || pixels != nullptr) {
@@ -1419,6 +1450,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     }
     if (e == cudaSuccess) {
         KScope kt_(g, s, "k_sum_parts_f64");
+        if (epi && epi->yr_ready) e = cudaStreamWaitEvent(s, epi->yr_ready, 0);
         if (epi)
             sum_parts(part, S, (size_t)p.n_det, EpiRatio{epi->y, epi->r, out, (unsigned *)epi->wmax}, s);
         else

@@ -126,6 +126,7 @@ struct cacsi_geometry {
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs
     cudaStream_t stage_stream;
     cudaEvent_t stage_ev[3];
+    cudaEvent_t stage_fev[4];  // f row chunks landed (cacsi_iterate_host, ESAI handles)
     mutable int32_t last_launches;
     // per-kernel CUDA-event timing (cacsi_set_timing / cacsi_kernel_times)
     mutable int32_t timing;
@@ -180,7 +181,16 @@ cudaError_t esai_forward_list(const cacsi_geometry *g, const float *f, const int
 struct FwdRatioEpi {
     const float *y, *r;
     float *wmax;
+    // optional: f arrives in f_chunks row chunks of fchunk_rows() rows (f_ready[c] recorded
+    // when chunk c is on the device); the W GEMM starts on each chunk as it lands
+    const cudaEvent_t *f_ready = nullptr;
+    int f_chunks = 0;
+    cudaEvent_t yr_ready = nullptr;  // optional: waited before the final sum (y, r staged)
 };
+inline int fchunk_rows(int n_vox, int n_chunks) {
+    const int mt = (n_vox + 127) / 128;
+    return (mt + n_chunks - 1) / n_chunks * 128;
+}
 struct BwdUpdateEpi {
     const float *wmax;
     const float *f_hat, *b1;
