@@ -297,36 +297,9 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             // bank-aware order puts record j of every lane's quad in one conflict-light group,
             // so the warp's j-th shared-memory access touches distinct banks
             const uint32_t kpad = (uint32_t)(e.vwin[v].x & ~3) << tb;
-            for (int i = U * tid; i < n; i += U * PCV_T) {
-                uint32_t k[U], q[U];
-                float P[U];
-#pragma unroll
-                for (int h = 0; h < U; h += 4) {
-                    const int ih = i + h;
-                    if (vec && ih + 3 < n) {
-                        const uint4 kv = __ldg((const uint4 *)(kb + ih));
-                        const float4 pv = __ldg((const float4 *)(Pb + ih));
-                        k[h] = kv.x, k[h + 1] = kv.y, k[h + 2] = kv.z, k[h + 3] = kv.w;
-                        P[h] = pv.x, P[h + 1] = pv.y, P[h + 2] = pv.z, P[h + 3] = pv.w;
-                        if (sizeof(QT) == 2) {
-                            const uint2 qv = __ldg((const uint2 *)(qb + ih));
-                            q[h] = qv.x & 0xFFFFu, q[h + 1] = qv.x >> 16, q[h + 2] = qv.y & 0xFFFFu, q[h + 3] = qv.y >> 16;
-                        } else {
-                            const uint4 qv = __ldg((const uint4 *)(qb + ih));
-                            q[h] = qv.x, q[h + 1] = qv.y, q[h + 2] = qv.z, q[h + 3] = qv.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const bool in = ih + u < n;
-                            k[h + u] = in ? __ldg(kb + ih + u) : kpad;
-                            P[h + u] = in ? __ldg(Pb + ih + u) : 0.0f;
-                            q[h + u] = in ? (uint32_t)__ldg(qb + ih + u) : 0u;
-                        }
-                    }
-                }
-                // P = 0: segment padding, whose pixel may repeat a real record's -- it
-                // adds into the lane's dummy slot past the row block (branch-free)
+            // P = 0: segment padding, whose pixel may repeat a real record's -- it
+            // adds into the lane's dummy slot past the row block (branch-free)
+            auto deposit = [&](const uint32_t (&k)[U], const float (&P)[U], const uint32_t (&q)[U]) {
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
@@ -334,6 +307,42 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     const float t = (float)(k[u] & tmask) * tunit;
                     float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
+                }
+            };
+            if (vec) {
+                // bank-ordered layout: the voxel's range is whole 128-record windows (n % 128 == 0),
+                // so every thread's U records are in range -- no bounds test in the loop
+                for (int i = U * tid; i < n; i += U * PCV_T) {
+                    uint32_t k[U], q[U];
+                    float P[U];
+#pragma unroll
+                    for (int h = 0; h < U; h += 4) {
+                        const uint4 kv = __ldg((const uint4 *)(kb + i + h));
+                        const float4 pv = __ldg((const float4 *)(Pb + i + h));
+                        k[h] = kv.x, k[h + 1] = kv.y, k[h + 2] = kv.z, k[h + 3] = kv.w;
+                        P[h] = pv.x, P[h + 1] = pv.y, P[h + 2] = pv.z, P[h + 3] = pv.w;
+                        if (sizeof(QT) == 2) {
+                            const uint2 qv = __ldg((const uint2 *)(qb + i + h));
+                            q[h] = qv.x & 0xFFFFu, q[h + 1] = qv.x >> 16, q[h + 2] = qv.y & 0xFFFFu, q[h + 3] = qv.y >> 16;
+                        } else {
+                            const uint4 qv = __ldg((const uint4 *)(qb + i + h));
+                            q[h] = qv.x, q[h + 1] = qv.y, q[h + 2] = qv.z, q[h + 3] = qv.w;
+                        }
+                    }
+                    deposit(k, P, q);
+                }
+            } else {
+                for (int i = U * tid; i < n; i += U * PCV_T) {
+                    uint32_t k[U], q[U];
+                    float P[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const bool in = i + u < n;
+                        k[u] = in ? __ldg(kb + i + u) : kpad;
+                        P[u] = in ? __ldg(Pb + i + u) : 0.0f;
+                        q[u] = in ? (uint32_t)__ldg(qb + i + u) : 0u;
+                    }
+                    deposit(k, P, q);
                 }
             }
             // this thread's reads of the W buffer (generic proxy) before its next
@@ -432,6 +441,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
     const QT *pq = (const QT *)e.pcb_q;
+    const bool vec = e.pc_R > 0;  // bank-ordered layout (segments 128-record aligned)
     const float wm = *wmax;
     if (tid == 0) {
         for (int i = 0; i < PBT_NS; i++) {
@@ -515,13 +525,22 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     const uint4 qv = ((const uint4 *)(src + PBT_CH * 8))[tid];
                     q[0] = qv.x, q[1] = qv.y, q[2] = qv.z, q[3] = qv.w;
                 }
+                if (vec) {
+                    // bank-ordered layout: voxel ranges are whole 128-record windows (lo = 0,
+                    // hi % 128 == 0), so a thread's four records are all in range or all out
+                    if (4 * tid >= hi) {
 #pragma unroll
-                for (int u = 0; u < PBT_U; u++) {
-                    const int i = 4 * tid + u;
-                    if (!(i >= lo && i < hi)) {
-                        k[u] = kinv;
-                        P[u] = 0.0f;
-                        q[u] = 0u;
+                        for (int u = 0; u < PBT_U; u++) k[u] = kinv, P[u] = 0.0f, q[u] = 0u;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < PBT_U; u++) {
+                        const int i = 4 * tid + u;
+                        if (!(i >= lo && i < hi)) {
+                            k[u] = kinv;
+                            P[u] = 0.0f;
+                            q[u] = 0u;
+                        }
                     }
                 }
             }
