@@ -233,6 +233,9 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
     const int a = win.x & ~3;
     const uint32_t bytes = (uint32_t)(((win.y + 1 - a) + 3) & ~3) * 4u;
     const uint32_t mb = smem_u32(mbar);
+    // the threads' earlier reads of dst (generic proxy, ordered before this thread by
+    // the CTA barrier) before the bulk copy (async proxy) that overwrites it
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)),
@@ -345,9 +348,8 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     deposit(k, P, q);
                 }
             }
-            // this thread's reads of the W buffer (generic proxy) before its next
-            // bulk copy (async proxy), then the barrier that hands it to thread 0
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            // the barrier orders every thread's reads of this W buffer before thread 0's
+            // next bulk copy into it (pcv_stage fences the proxies first)
             __syncthreads();
         }
     }
@@ -471,7 +473,13 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             if (pv >= p.n_vox) return;
             const int st = issued % PBT_NS;
             const uint32_t use = issued / PBT_NS;
-            if (use > 0) mbar_wait(smem_u32(empty + st), (use - 1) & 1);
+            if (use > 0) {
+                // every warp's reads of the stage (generic proxy) were released by its arrival
+                // on "empty" and acquired by this wait: one proxy fence here orders them
+                // before the bulk copy (async proxy) that overwrites the stage
+                mbar_wait(smem_u32(empty + st), (use - 1) & 1);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            }
             const uint32_t n = (uint32_t)((min((long long)PBT_CH, pe - pa) + 7) & ~7ll);
             const uint32_t mb = smem_u32(full + st);
             unsigned char *dst = smb + st * SB;
@@ -544,9 +552,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     }
                 }
             }
-            // every thread orders its reads (generic proxy) before the next bulk copy
-            // into the stage (async proxy); then one arrival per warp
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            // one arrival per warp (release: this warp's stage reads happen before it)
             __syncwarp();
             if ((tid & 31) == 0)
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + st)) : "memory");
