@@ -999,6 +999,22 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     if (e == cudaSuccess) e = cudaMalloc(&g->d_esai_trng, trng.size() * sizeof(int2));
     if (e == cudaSuccess)
         e = cudaMemcpy(g->d_esai_trng, trng.data(), trng.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    // the W GEMM's tile list: per M tile the N tiles (128 bins) covering [lo & ~3, hi) -- the
+    // forward stages each voxel's W window from win.x & ~3 -- and their prefix count
+    const int mtl = (int)trng.size();
+    std::vector<int> wtl(2 * mtl + mtl + 1);  // [mtl] int2 ranges, then [mtl + 1] prefix
+    {
+        int2 *ntr = (int2 *)wtl.data();
+        int *pre = wtl.data() + 2 * mtl;
+        pre[0] = 0;
+        for (int m = 0; m < mtl; m++) {
+            const int lo = trng[m].x & ~3, hi = trng[m].y;
+            ntr[m] = hi > lo ? make_int2(lo / 128, (hi - 1) / 128) : make_int2(0, -1);
+            pre[m + 1] = pre[m] + (ntr[m].y - ntr[m].x + 1);
+        }
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_w_tiles, wtl.size() * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_w_tiles, wtl.data(), wtl.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
     Esai &E = g->esai;
     E.nb = nb;
@@ -1012,6 +1028,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.stab = (const float *)g->d_esai_stab;
     E.vwin = (const int2 *)g->d_esai_vwin;
     E.trng = (const int2 *)g->d_esai_trng;
+    E.w_ntr = (const int2 *)g->d_w_tiles;
+    E.w_pre = (const int *)g->d_w_tiles + 2 * mtl;
     E.ptot = (const float *)g->d_esai_ptot;
     E.max_win = max_win;
     // tensor-core operands: S~ (N = nb, K = nq) for W = F S~^T and S~^T (N = nq, K = nb) for b2 = A S~,
@@ -1293,7 +1311,8 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             {
                 KScope kt_(g, s, "k_tc_gemm_W");
                 kar<<<std::min(mtc * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
-                    nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw);
+                    nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw, E.w_pre + r0 / TC_M,
+                    E.w_ntr + r0 / TC_M);
             }
             *launches += 2;
         }
@@ -1324,8 +1343,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
                 auto kar = nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>;
                 cudaFuncSetAttribute(kar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA, nsb));
+                // only the N tiles inside each M tile's window union (E.w_pre / w_ntr; ~84 % on
+                // config 2), split evenly over the CTAs; W outside them is never read
                 kar<<<std::min(mt * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
-                    p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw);
+                    p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw, E.w_pre, E.w_ntr);
             } else {
                 dim3 gg(nt, mt, 1);
                 cudaFuncSetAttribute(k_tc_gemm<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));

@@ -321,10 +321,47 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
 // b_empty (ring), t_full / t_empty (accumulators).
 constexpr int TCA_T1 = 320;  // k_tc_gemm_ar / _ar2: 8 epilogue warps
 constexpr int tca_smem(int nkc, int nsb = 2) { return nkc * TC_STAGE / 2 + nsb * TC_STAGE / 2 + 8 * 32 * 33 * 4 + 1024 + 256; }
+// Output tiles of k_tc_gemm_ar in M-major order, either all mtiles x ntiles or -- with
+// a tile list (pre, ntr) -- only N tiles ntr[m].x .. ntr[m].y of each M tile (pre: the
+// exclusive prefix count of listed tiles, pre[0] the base; the CTAs split the LISTED
+// tiles evenly).  start(t) positions on the t-th tile of the walk, next() steps.
+struct TileWalk {
+    const int *pre;
+    const int2 *ntr;
+    int mtiles, ntiles, m, n;
+    __device__ long long count() const { return pre ? (long long)(pre[mtiles] - pre[0]) : (long long)mtiles * ntiles; }
+    __device__ void start(int t) {
+        if (!pre) {
+            m = t / ntiles;
+            n = t % ntiles;
+            return;
+        }
+        const int g = pre[0] + t;
+        int lo = 0, hi = mtiles;  // the last m with pre[m] <= g (empty M tiles share their successor's prefix)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= g) lo = mid; else hi = mid;
+        }
+        m = lo;
+        n = ntr[m].x + (g - pre[m]);
+    }
+    __device__ void next() {
+        if (!pre) {
+            if (++n == ntiles) n = 0, m++;
+            return;
+        }
+        if (++n > ntr[m].y) {
+            do m++; while (m < mtiles && pre[m + 1] == pre[m]);
+            if (m < mtiles) n = ntr[m].x;
+        }
+    }
+};
+
 template <int NSB>
 __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
                                                          const float *__restrict__ Ap, const float *__restrict__ Bt,
-                                                         float *__restrict__ C, int ldc) {
+                                                         float *__restrict__ C, int ldc, const int *__restrict__ tpre,
+                                                         const int2 *__restrict__ tntr) {
     extern __shared__ __align__(1024) unsigned char tca_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                              // [nkc][hi, lo] 32 KB each
@@ -335,8 +372,10 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
              *t_full = bars + 2 + 2 * NSB, *t_empty = bars + 4 + 2 * NSB;
     uint32_t *tmem_slot = (uint32_t *)(bars + 6 + 2 * NSB);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long T = (long long)mtiles * ntiles;
+    TileWalk tw{tpre, tntr, mtiles, ntiles, 0, 0};
+    const long long T = tw.count();
     const int t0 = (int)(T * blockIdx.x / gridDim.x), t1 = (int)(T * (blockIdx.x + 1) / gridDim.x);
+    tw.start(t0);
     constexpr uint32_t CHB = TC_STAGE / 2;  // bytes of one hi + lo chunk (32 KB)
 
     if (warp == 0) {
@@ -357,8 +396,9 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
         if (lane == 0) {
             int cur_m = -1;
             uint32_t loads = 0, bc = 0;
-            for (int t = t0; t < t1; t++) {
-                const int m = t / ntiles, n = t % ntiles;
+            TileWalk w = tw;
+            for (int t = t0; t < t1; t++, w.next()) {
+                const int m = w.m, n = w.n;
                 if (m != cur_m) {
                     if (loads > 0) mbar_wait(smem_u32(a_empty), (loads - 1) & 1);
                     const uint32_t mb = smem_u32(a_full);
@@ -392,8 +432,10 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
             const uint32_t idesc = tc_idesc_tf32();
             int cur_m = -1;
             uint32_t loads = 0, bc = 0, tc = 0;
+            TileWalk w = tw;
             for (int t = t0; t < t1; t++, tc++) {
-                const int m = t / ntiles;
+                const int m = w.m;
+                w.next();  // w: the next tile (its M tile decides whether the A panel is released)
                 if (m != cur_m) {
                     mbar_wait(smem_u32(a_full), loads & 1);
                     loads++;
@@ -421,7 +463,7 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                     smem_u32(t_full + ab)));
-                if (t + 1 == t1 || (t + 1) / ntiles != m)
+                if (t + 1 == t1 || w.m != m)
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                         smem_u32(a_empty)));
             }
@@ -433,8 +475,9 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
         float *buf = ebuf + ew * (32 * 33);
         const int cq = 4 * (lane & 7);
         uint32_t tc = 0;
-        for (int t = t0; t < t1; t++, tc++) {
-            const int m = t / ntiles, n = t % ntiles;
+        TileWalk w = tw;
+        for (int t = t0; t < t1; t++, tc++, w.next()) {
+            const int m = w.m, n = w.n;
             const int ab = tc & 1;
             mbar_wait(smem_u32(t_full + ab), (tc >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
