@@ -162,7 +162,13 @@ CACSI_API cacsi_status cacsi_neg_loglik(const cacsi_geometry *geom, const float 
  * unit weights.  b1 = A^T 1 is supplied by the caller (computed once,
  * PAPER.md:370).  Ratio guard: y/z = 0 where y = 0 and z = 0, y / 1e-12
  * where z = 0 < y.  f must be >= 0 on entry and stays >= 0.
- * ws: device workspace of cacsi_workspace_bytes() bytes.                    */
+ * ws: device workspace of cacsi_workspace_bytes() bytes.
+ * On ESAI handles the iteration runs as two operator calls whose final
+ * partial sums carry the elementwise steps (the forward's writes y ./ z and
+ * max |y ./ z|, the backward's writes the update) -- the same bits as
+ * cacsi_forward, cacsi_ratio, cacsi_backward, cacsi_update in turn.  The
+ * iterates alternate between f and the workspace; an odd n_iter ends with one
+ * device copy into f.                                                       */
 CACSI_API cacsi_status cacsi_iterate(const cacsi_geometry *geom, float *f, const float *y, const float *r,
                            const float *b1, float beta, int32_t n_iter, void *ws, void *stream);
 
@@ -181,9 +187,12 @@ CACSI_API cacsi_status cacsi_update(const cacsi_geometry *geom, const float *f_h
  * to device scratch owned by the handle, run the device call, copy the output
  * back, and synchronise `stream` before returning.  Same shapes as above.
  * Not re-entrant on one handle (they share the handle's staging buffers).
- * cacsi_iterate_host uploads f on `stream` and y, r, b1 on a side stream the
- * handle owns (created on first use), so those copies overlap the first
- * forward; the ratio and the update wait on events for them.               */
+ * cacsi_iterate_host uploads f, y, r, b1 (in that order) on a side stream the
+ * handle owns (created on first use, after waiting for earlier work on
+ * `stream`): on ESAI handles f goes in four row chunks and the forward's
+ * tensor-core contraction starts on each chunk as it lands; y, r are waited
+ * for only before the ratio, b1 only before the update (other handles: f is
+ * uploaded whole on `stream` first).                                        */
 CACSI_API cacsi_status cacsi_forward_host(const cacsi_geometry *geom, const float *f_host, float *g_host, void *stream);
 CACSI_API cacsi_status cacsi_backward_host(const cacsi_geometry *geom, const float *w_host, float *b_host, void *stream);
 CACSI_API cacsi_status cacsi_iterate_host(const cacsi_geometry *geom, float *f_host, const float *y_host,
