@@ -1228,6 +1228,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
 
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
                                      float *out, cudaStream_t s, int *launches, const FwdRatioEpi *epi = nullptr);
+static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld);
 
 // Row blocks of the voxel-major pair-cache forward (0: the W windows do not fit
 // shared memory, the per-list kernel runs).  One 1024-thread CTA per SM with a
@@ -1289,6 +1290,12 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     const bool ar_path = ((E.pc && pixels == nullptr) || pixels != nullptr) && nkcA <= 4 &&
                          !(gv0 && (strcmp(gv0, "ar2") == 0 || strcmp(gv0, "tiles") == 0));
     const int nfc = (epi && epi->f_chunks > 0) ? epi->f_chunks : 0;
+    // the A-resident W GEMM reads f itself (TMA tensor loads + in-kernel TF32 split) when
+    // f's rows are 16-byte multiples; otherwise k_tc_pack_a pre-splits it
+    CUtensorMap tmF;
+    memset(&tmF, 0, sizeof(tmF));
+    const bool raw = ar_path && (p.nq % 4) == 0 && !(getenv("CACSI_WGEMM_PACK")) &&
+                     tmap_rows_f32(&tmF, f, (uint64_t)p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq);
     if (nfc > 0 && !ar_path)
         for (int c = 0; c < nfc && e == cudaSuccess; c++) e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
     if (nfc > 0 && ar_path) {
@@ -1296,7 +1303,8 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         // upload of chunk c + 1 overlaps the contraction of chunk c (cacsi_iterate_host)
         const int rows = fchunk_rows(p.n_vox, nfc), nt = tc_ntiles(E.nb, TC_N);
         const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
-        auto kar = nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>;
+        auto kar = raw ? (nsb == 3 ? k_tc_gemm_ar<3, true> : k_tc_gemm_ar<2, true>)
+                       : (nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>);
         cudaFuncSetAttribute(kar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA, nsb));
         for (int c = 0; c < nfc && e == cudaSuccess; c++) {
             const int r0 = c * rows;
@@ -1304,19 +1312,22 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             if (r0 >= p.n_vox || e != cudaSuccess) continue;
             const int nr = std::min(rows, p.n_vox - r0), mtc = (nr + TC_M - 1) / TC_M;
             float *fpc = fp + (size_t)(r0 / TC_M) * nkcA * (2 * TC_M * TC_KC);
-            {
+            if (!raw) {
                 KScope kt_(g, s, "k_tc_pack_a");
                 k_tc_pack_a<<<4 * sm_count(g->device), 256, 0, s>>>(f + (size_t)r0 * p.nq, nr, p.nq, p.nq, nkcA, fpc);
+                *launches += 1;
             }
             {
                 KScope kt_(g, s, "k_tc_gemm_W");
-                kar<<<std::min(mtc * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
+                kar<<<std::min(mtc * nt, sm_count(g->device)), raw ? TCA_T1R : TCA_T1, tca_smem(nkcA, nsb), s>>>(
                     nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw, E.w_pre + r0 / TC_M,
-                    E.w_ntr + r0 / TC_M);
+                    E.w_ntr + r0 / TC_M, tmF, r0);
             }
-            *launches += 2;
+            *launches += 1;
         }
         *launches -= 2;  // counted again below (pack + GEMM)
+    } else if (raw) {
+        *launches -= 1;  // no pack pass: the W GEMM loads and splits f itself
     } else {
         // f -> pre-split (TF32 hi / lo), pre-swizzled A tiles: the GEMM lands them by bulk copy
         KScope kt_(g, s, "k_tc_pack_a");
@@ -1341,12 +1352,13 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 // B ring depth: 3 stages where they fit beside the resident A panel (nkc <= 2), else 2
                 // (config 2, nq = 128: nkc = 4, the 128 KB panel leaves room for 2)
                 const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
-                auto kar = nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>;
+                auto kar = raw ? (nsb == 3 ? k_tc_gemm_ar<3, true> : k_tc_gemm_ar<2, true>)
+                               : (nsb == 3 ? k_tc_gemm_ar<3> : k_tc_gemm_ar<2>);
                 cudaFuncSetAttribute(kar, cudaFuncAttributeMaxDynamicSharedMemorySize, tca_smem(nkcA, nsb));
                 // only the N tiles inside each M tile's window union (E.w_pre / w_ntr; ~84 % on
                 // config 2), split evenly over the CTAs; W outside them is never read
-                kar<<<std::min(mt * nt, sm_count(g->device)), TCA_T1, tca_smem(nkcA, nsb), s>>>(
-                    p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw, E.w_pre, E.w_ntr);
+                kar<<<std::min(mt * nt, sm_count(g->device)), raw ? TCA_T1R : TCA_T1, tca_smem(nkcA, nsb), s>>>(
+                    p.n_vox, E.nb, nkcA, mt, nt, fp, E.tc_w1, W, E.ldw, E.w_pre, E.w_ntr, tmF, 0);
             } else {
                 dim3 gg(nt, mt, 1);
                 cudaFuncSetAttribute(k_tc_gemm<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
@@ -1478,7 +1490,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             sum_parts(part, S, (size_t)p.n_det, EpiStore{out}, s);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
-    *launches += 3;
+    *launches += 4;  // pack, W GEMM, pair kernel, partial sum (adjusted above for the raw / chunked GEMM)
     if (part) cudaFreeAsync(part, s);
     cudaFreeAsync(fp, s);
     cudaFreeAsync(W, s);

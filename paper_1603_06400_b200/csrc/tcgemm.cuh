@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(TC_T) k_tc_gemm(int M, int N, int K, int lda, 
 // consecutive tiles overlap.  Barriers: a_full / a_empty (panel), b_full /
 // b_empty (ring), t_full / t_empty (accumulators).
 constexpr int TCA_T1 = 320;  // k_tc_gemm_ar / _ar2: 8 epilogue warps
+constexpr int TCA_T1R = 352; // k_tc_gemm_ar<NSB, true>: + warp 10, the A-panel converter
 constexpr int tca_smem(int nkc, int nsb = 2) { return nkc * TC_STAGE / 2 + nsb * TC_STAGE / 2 + 8 * 32 * 33 * 4 + 1024 + 256; }
 // Output tiles of k_tc_gemm_ar in M-major order, either all mtiles x ntiles or -- with
 // a tile list (pre, ntr) -- only N tiles ntr[m].x .. ntr[m].y of each M tile (pre: the
@@ -357,11 +358,16 @@ struct TileWalk {
     }
 };
 
-template <int NSB>
-__global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles,
-                                                         const float *__restrict__ Ap, const float *__restrict__ Bt,
-                                                         float *__restrict__ C, int ldc, const int *__restrict__ tpre,
-                                                         const int2 *__restrict__ tntr) {
+// RAW: the A panel is loaded from the raw fp32 matrix by TMA tensor loads (tmA: rows
+// x K, box 128 x 32, SWIZZLE_128B -- the operand layout; out-of-range rows and K
+// columns land as zeros) into the hi slots, and warp 10 splits it in place (hi =
+// TF32 truncation, lo = rest, the split k_tc_pack_a does), proxy-fences and arrives
+// a_conv -- no separate pack pass.  mrow0: the first M tile's row in tmA.
+template <int NSB, bool RAW = false>
+__global__ void __launch_bounds__(RAW ? TCA_T1R : TCA_T1, 1)
+    k_tc_gemm_ar(int M, int N, int nkc, int mtiles, int ntiles, const float *__restrict__ Ap,
+                 const float *__restrict__ Bt, float *__restrict__ C, int ldc, const int *__restrict__ tpre,
+                 const int2 *__restrict__ tntr, const __grid_constant__ CUtensorMap tmA, int mrow0) {
     extern __shared__ __align__(1024) unsigned char tca_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)tca_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                              // [nkc][hi, lo] 32 KB each
@@ -370,7 +376,8 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
     uint64_t *bars = (uint64_t *)(ebuf + 8 * 32 * 33);
     uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 2 + NSB,
              *t_full = bars + 2 + 2 * NSB, *t_empty = bars + 4 + 2 * NSB;
-    uint32_t *tmem_slot = (uint32_t *)(bars + 6 + 2 * NSB);
+    uint64_t *a_conv = bars + 6 + 2 * NSB;  // RAW: the A panel split
+    uint32_t *tmem_slot = (uint32_t *)(bars + 7 + 2 * NSB);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     TileWalk tw{tpre, tntr, mtiles, ntiles, 0, 0};
     const long long T = tw.count();
@@ -383,8 +390,9 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 32) {
-        for (int i = 0; i < 6 + 2 * NSB; i++)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)), "r"(i >= 4 + 2 * NSB ? 8 : 1));
+        for (int i = 0; i < 7 + 2 * NSB; i++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bars + i)),
+                         "r"(i >= 4 + 2 * NSB && i < 6 + 2 * NSB ? 8 : 1));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -402,14 +410,30 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                 if (m != cur_m) {
                     if (loads > 0) mbar_wait(smem_u32(a_empty), (loads - 1) & 1);
                     const uint32_t mb = smem_u32(a_full);
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nkc * CHB)
-                                 : "memory");
-                    for (int c = 0; c < nkc; c++)
-                        asm volatile(
-                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                                smem_u32(sA + c * CHB)),
-                            "l"(Ap + ((size_t)m * nkc + c) * (2 * TC_M * TC_KC)), "r"(CHB), "r"(mb)
-                            : "memory");
+                    if (RAW) {
+                        // (the converter's generic writes of the previous panel were ordered
+                        // before the MMAs that released it; the proxy fence orders them
+                        // before these async-proxy writes)
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                                     "r"(nkc * (uint32_t)TC_OPB)
+                                     : "memory");
+                        for (int c = 0; c < nkc; c++)
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+                                "{%2, %3}], [%4];\n" ::"r"(smem_u32(sA + c * CHB)),
+                                "l"(&tmA), "r"(c * TC_KC), "r"(mrow0 + m * TC_M), "r"(mb)
+                                : "memory");
+                    } else {
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nkc * CHB)
+                                     : "memory");
+                        for (int c = 0; c < nkc; c++)
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                    smem_u32(sA + c * CHB)),
+                                "l"(Ap + ((size_t)m * nkc + c) * (2 * TC_M * TC_KC)), "r"(CHB), "r"(mb)
+                                : "memory");
+                    }
                     cur_m = m;
                     loads++;
                 }
@@ -437,7 +461,7 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                 const int m = w.m;
                 w.next();  // w: the next tile (its M tile decides whether the A panel is released)
                 if (m != cur_m) {
-                    mbar_wait(smem_u32(a_full), loads & 1);
+                    mbar_wait(smem_u32(RAW ? a_conv : a_full), loads & 1);
                     loads++;
                     cur_m = m;
                 }
@@ -467,6 +491,30 @@ __global__ void __launch_bounds__(TCA_T1, 1) k_tc_gemm_ar(int M, int N, int nkc,
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                         smem_u32(a_empty)));
             }
+        }
+    } else if (warp == 10) {
+        // RAW only: split each landed A panel in place (position-independent: the hi and
+        // lo slots share the swizzled layout), then release it to the MMA thread
+        int cur_m = -1;
+        uint32_t loads = 0;
+        TileWalk w = tw;
+        for (int t = t0; t < t1; t++, w.next()) {
+            if (w.m == cur_m) continue;
+            cur_m = w.m;
+            mbar_wait(smem_u32(a_full), loads & 1);
+            loads++;
+            for (int c = 0; c < nkc; c++) {
+                float4 *hi = (float4 *)(sA + c * CHB), *lo = (float4 *)(sA + c * CHB + TC_OPB);
+                for (int i4 = lane; i4 < TC_OPB / 16; i4 += 32) {
+                    const float4 v = hi[i4];
+                    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                    hi[i4] = h;
+                    lo[i4] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(a_conv)) : "memory");
         }
     } else {
         // epilogue warps 0-3 and 6-9: TMEM lanes 32 (warp % 4) .. + 31 = tile rows; warps

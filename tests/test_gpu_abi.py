@@ -275,3 +275,38 @@ def test_osem_graph_replay_matches_stream_launches(monkeypatch):
         res[mode] = f.clone()
     assert torch.equal(res["1"], res["0"])
     G.close()
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_launch_count_matches_kernels(ci):
+    """cacsi_last_launch_count (bench.py's gpu_launches) equals the number of
+    libcacsi kernel launches the per-kernel event timer saw, for the operators
+    and the fused iteration (device and host-buffer entry points)."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    rng = np.random.default_rng(2)
+    f = torch.as_tensor(cfg.f).cuda()
+    g = torch.empty(G.g_shape, device="cuda")
+    b = torch.empty(G.f_shape, device="cuda")
+    y = torch.as_tensor(rng.poisson(20.0, G.g_shape).astype(np.float32)).cuda()
+    r = torch.full(G.g_shape, 1.0, device="cuda")
+    b1 = torch.as_tensor(rng.uniform(1.0, 2.0, G.f_shape).astype(np.float32)).cuda()
+    ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
+    host = [torch.as_tensor(t.cpu().numpy()).pin_memory() for t in (f, y, r, b1)]
+    calls = {
+        "forward": lambda: G.forward(f, g),
+        "backward": lambda: G.backward(g, b),
+        "iterate": lambda: G.iterate(f, y, r, b1, 1e-3, 1, ws),
+        "iterate_host": lambda: G.iterate_host(host[0], host[1], host[2], host[3], 1e-3, 1),
+    }
+    G.forward(f, g)
+    torch.cuda.synchronize()
+    for name, call in calls.items():
+        G.kernel_times()
+        G.set_timing(True)
+        call()
+        torch.cuda.synchronize()
+        G.set_timing(False)
+        seen = sum(n for _, n in G.kernel_times().values())
+        assert G.last_launch_count == seen, (name, G.last_launch_count, seen)
+    G.close()
