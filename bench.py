@@ -216,6 +216,7 @@ def run_gpu(args):
         step(evs[i])
     torch.cuda.synchronize()
     ck = clocks.stop()
+    launches_timed = launches_per_step[0]  # (step() is reused below on the comparison handle)
     t_step = [e[0].elapsed_time(e[1]) for e in evs]
     # per-kernel times (CUDA events around every libcacsi kernel, same stream) in a
     # separate pass, so the timed steps above carry no per-kernel events
@@ -317,14 +318,14 @@ def run_gpu(args):
     if ck.get("sm_mhz"):
         roofline["frac_at_observed_clock"] = round(achieved / (peak * ck["sm_mhz"] / 1965.0), 4)
     # DRAM traffic of the operator's kernels from the committed ncu --set full capture
-    # (profiles/r1s5_dram_traffic.json, bytes per launch); kernels it does not list are omitted
+    # (profiles/r1s6_dram_traffic.json, bytes per launch); kernels it does not list are omitted
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1s5_dram_traffic.json")))["kernels"]
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r1s6_dram_traffic.json")))["kernels"]
         ks = [k for k in (fwd_k if dom == "cacsi_forward" else bwd_k) if k in tr]
         if ks:
             roofline["traffic"] = float(sum(tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"] for k in ks))
             roofline["traffic_note"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch of " + " + ".join(ks) + \
-                " (profiles/r1s5_dram_traffic.json); compulsory bytes of the operator (f, g, w, b, tables) are ~0.1 GB -- " \
+                " (profiles/r1s6_dram_traffic.json); compulsory bytes of the operator (f, g, w, b, tables) are ~0.1 GB -- " \
                 "the rest is the W / A scratch of the ESAI contraction"
     except Exception:
         pass
@@ -359,7 +360,7 @@ def run_gpu(args):
                         "bytes_note": f"{rb} B per open pair (pair record) + list offsets + the gathered table "
                                       "once (DESIGN.md §8)"}
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r1s5_dram_traffic.json")))["kernels"]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r1s6_dram_traffic.json")))["kernels"]
             if kd in tr:
                 roofline_hbm["traffic"] = tr[kd]["dram_read_bytes"] + tr[kd]["dram_write_bytes"]
         except Exception:
@@ -380,7 +381,7 @@ def run_gpu(args):
         "forward_pairs_per_s": pairs / (mf / 1e3), "backward_pairs_per_s": pairs / (mb / 1e3),
         "nominal_terms_per_s": 2 * nominal_terms * world / (ms_per_step / 1e3),
         "effective_terms_per_s": 2 * float(eff) * world / (ms_per_step / 1e3),
-        "gpu_launches": launches_per_step[0] * args.steps,
+        "gpu_launches": launches_timed * args.steps,
         "kernels": kern, "esai_breakpoints": nb_bp, "ts_rho": G.query("ts_rho"),
         "clocks": ck, "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
