@@ -1114,6 +1114,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     }
     // pair cache (above): counts -> host scan -> fill, if it fits in half the free memory
     E.pc = 0;
+    E.pc_segwin = nullptr;
     const char *pce = getenv("CACSI_PAIR_CACHE");
     if (!(pce && strcmp(pce, "0") == 0) && (size_t)p.det_ny <= 65535) {
         const size_t nl = (size_t)nv * p.det_nx;
@@ -1218,6 +1219,18 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                 E.pcb_bt = E.pc_bt;
                 E.pcb_P = E.pc_P;
                 E.pcb_q = E.pc_q;
+                // per-segment W windows for the voxel-major forward (and the padding re-binned
+                // inside them)
+                const size_t nseg = (size_t)nv * ((p.det_nx + segR - 1) / segR);
+                e = cudaMalloc(&g->d_pc_segwin, nseg * sizeof(int2));
+                if (e == cudaSuccess) {
+                    k_pc_segwin<<<8 * sm_count(g->device), 256>>>(p, E, segR, (uint32_t *)g->d_pc_bt,
+                                                                 (const float *)g->d_pc_P, (int2 *)g->d_pc_segwin);
+                    e = cudaDeviceSynchronize();
+                }
+                if (e != cudaSuccess) return e;
+                if (!(getenv("CACSI_PC_SEGWIN") && strcmp(getenv("CACSI_PC_SEGWIN"), "0") == 0))
+                    E.pc_segwin = (const int2 *)g->d_pc_segwin;
             }
             E.pc = 1;
         }

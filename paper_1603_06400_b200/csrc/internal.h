@@ -77,6 +77,7 @@ struct Esai {
     const float *stab;  // S~ [nb][nq] (scale, phi_k, E_k folded in)
     const int2 *vwin;   // per voxel [b_lo, b_hi] reachable by any of its pairs
     const int2 *trng;   // per 128-voxel GEMM tile: the union of its voxels' windows, [lo, hi) in bins
+    const int2 *pc_segwin;  // bank-ordered cache: per (voxel, row block) segment, the W columns it reads (or null)
     const int *w_pre;   // W GEMM tile list: exclusive prefix count of the N tiles inside trng, per M tile [+1]
     const int2 *w_ntr;  // W GEMM tile list: first / last N tile inside trng, per M tile
     const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)
@@ -122,7 +123,7 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles;
+        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs

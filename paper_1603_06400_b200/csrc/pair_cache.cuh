@@ -228,8 +228,45 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
 // CTA's row-block accumulator acc[q - q0].  The pixels of one voxel's records
 // are distinct (no two updates of one voxel alias); voxels are separated by a
 // barrier, so the sums are plain fp32 in a fixed order (deterministic).
-__device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, float *dst, uint64_t *mbar) {
-    const int2 win = e.vwin[v];
+// Per (voxel, row block) segment of the bank-ordered cache: the W columns its real
+// records read, [min b, max b + 1] (one warp per segment), then the segment's
+// padding records (P = 0) re-binned inside that window (spread over it, as k_pc_fill
+// spreads them over the voxel's) -- so the voxel-major forward stages only the
+// segment's part of the voxel's W window (with two row blocks, each reads roughly
+// half of it instead of all of it).  Empty segments get [win.x, win.x + 1].
+__global__ void k_pc_segwin(const Params p, const Esai e, int R, uint32_t *__restrict__ bt,
+                            const float *__restrict__ P, int2 *__restrict__ segwin) {
+    const int nseg_v = (p.det_nx + R - 1) / R;
+    const size_t nseg = (size_t)p.n_vox * nseg_v;
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (size_t)blockDim.x) >> 5;
+    for (size_t sg = warp0; sg < nseg; sg += nwarps) {
+        const int v = (int)(sg / nseg_v), s = (int)(sg % nseg_v);
+        const size_t l0 = (size_t)v * p.det_nx;
+        const long long a = e.pc_off[l0 + s * R], z = e.pc_off[l0 + min(p.det_nx, (s + 1) * R)];
+        int lo = 1 << 30, hi = -1;
+        for (long long o = a + lane; o < z; o += 32)
+            if (P[o] != 0.0f) {
+                const int b = (int)(bt[o] >> e.pc_tbits);
+                lo = min(lo, b);
+                hi = max(hi, b + 1);
+            }
+        lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+        hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+        if (hi < 0) lo = e.vwin[v].x, hi = lo + 1;
+        if (lane == 0) segwin[sg] = make_int2(lo, hi);
+        const int span = hi - lo;  // padding bins b in [lo, hi - 1]: b + 1 <= hi stays inside
+        for (long long o = a + lane; o < z; o += 32)
+            if (P[o] == 0.0f) bt[o] = (uint32_t)(lo + (int)((o - a) % span)) << e.pc_tbits;
+    }
+}
+
+// the W columns a (voxel, row block) segment reads: its own window when the cache
+// recorded one (k_pc_segwin), else the voxel's
+__device__ __forceinline__ int2 seg_window(const Esai &e, int v, int n_rb, int rb) {
+    return e.pc_segwin ? e.pc_segwin[(size_t)v * n_rb + rb] : e.vwin[v];
+}
+__device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, int2 win, float *dst, uint64_t *mbar) {
     const int a = win.x & ~3;
     const uint32_t bytes = (uint32_t)(((win.y + 1 - a) + 3) & ~3) * 4u;
     const uint32_t mb = smem_u32(mbar);
@@ -274,10 +311,11 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int c = item / n_rb;
         const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);
-        if (tid == 0) pcv_stage(e, W, v0, ws, mbar);
+        if (tid == 0) pcv_stage(e, W, v0, seg_window(e, v0, n_rb, rb), ws, mbar);
         for (int v = v0; v < v1; v++) {
             const int buf = (v - v0) & 1;
-            if (tid == 0 && v + 1 < v1) pcv_stage(e, W, v + 1, ws + (buf ^ 1) * wcap, mbar + (buf ^ 1));
+            if (tid == 0 && v + 1 < v1)
+                pcv_stage(e, W, v + 1, seg_window(e, v + 1, n_rb, rb), ws + (buf ^ 1) * wcap, mbar + (buf ^ 1));
             const size_t l0 = (size_t)v * p.det_nx;
             const long long o0 = __ldg(e.pc_off + l0 + r0), o1 = __ldg(e.pc_off + l0 + r1);
             if (tid == 0 && pf > 0 && v + pf < v1) {
@@ -289,7 +327,8 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             }
             mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
             uses ^= 1u << buf;
-            const float *wv = ws + buf * wcap - (e.vwin[v].x & ~3);
+            const int2 swin = seg_window(e, v, n_rb, rb);
+            const float *wv = ws + buf * wcap - (swin.x & ~3);
             float *accq = acc - q0;
             // 32-bit indices from the voxel's first record; full steps unchecked, then the tail
             const uint32_t *kb = e.pc_bt + o0;
@@ -299,7 +338,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             // each thread takes U CONSECUTIVE records (16-byte vector loads, U / 4 quads); the
             // bank-aware order puts record j of every lane's quad in one conflict-light group,
             // so the warp's j-th shared-memory access touches distinct banks
-            const uint32_t kpad = (uint32_t)(e.vwin[v].x & ~3) << tb;
+            const uint32_t kpad = (uint32_t)swin.x << tb;
             // P = 0: segment padding, whose pixel may repeat a real record's -- it
             // adds into the lane's dummy slot past the row block (branch-free)
             auto deposit = [&](const uint32_t (&k)[U], const float (&P)[U], const uint32_t (&q)[U]) {
