@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="cacsi", choices=["cacsi", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--options", default=None, help="kernel-variant options (cacsi_geometry_create_ex)")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0, help="target seconds of oracle work")
     return ap.parse_args()
 
@@ -156,7 +157,7 @@ def run_gpu(args):
     d["scale"] = s
     torch.cuda.synchronize()
     t_setup = time.perf_counter()
-    G = P.Geometry(d, device=local)  # host tables, ESAI tables, bitmaps, pair cache (once per geometry)
+    G = P.Geometry(d, device=local, options=args.options)  # host tables, ESAI tables, bitmaps, pair cache
     torch.cuda.synchronize()
     setup_ms = (time.perf_counter() - t_setup) * 1e3
     y = torch.as_tensor(y_np).to(dev)
@@ -264,11 +265,7 @@ def run_gpu(args):
     # recomputed per pair inside the operators, CACSI_PAIR_CACHE=0), for comparison
     on_the_fly = None
     if G.query("pair_cache_records") > 0:
-        os.environ["CACSI_PAIR_CACHE"] = "0"
-        try:
-            G2 = P.Geometry(d, device=local)
-        finally:
-            del os.environ["CACSI_PAIR_CACHE"]
+        G2 = P.Geometry(d, device=local, options="pair_cache=0")
         G, Gc = G2, G
         f.fill_(f0)
         for _ in range(2):
@@ -281,7 +278,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         ms2 = float(np.mean([e[0].elapsed_time(e[1]) for e in ev2]))
         on_the_fly = {"ms_per_step": ms2, "value": 2 * pairs / (ms2 / 1e3),
-                      "note": "CACSI_PAIR_CACHE=0: pair geometry and breakpoint location recomputed per pair per call"}
+                      "note": "option pair_cache=0: pair geometry and breakpoint location recomputed per pair per call"}
         G.close()
         G = Gc
 

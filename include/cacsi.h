@@ -119,11 +119,34 @@ typedef struct {
 /* Validate `desc`, precompute the per-voxel / per-pixel / per-energy tables
  * in fp64 (the offline part of the online/offline
  * trade-off), bit-pack the mask and upload everything to `device`.
- * Synchronous.  On success *out owns the device tables.
+ * Synchronous.  On success *out owns the device tables.  Every call on the
+ * handle runs on `device` and restores the caller's current device on return.
  * Errors: CACSI_ERR_NULL (desc, out or a desc array NULL), CACSI_ERR_INVALID
  * (including ny nz nq >= 2^31 or det_nx det_ny ne >= 2^31: 32-bit element
  * indexing), CACSI_ERR_CUDA (no such device / not sm_100), CACSI_ERR_NOMEM. */
 CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, int device, cacsi_geometry **out);
+
+/* As cacsi_geometry_create, with kernel-variant options: NULL / "" = the
+ * defaults, else "key=value[,key=value...]" (integer values, no spaces).
+ * Every option selects among kernels that compute the same operator (A/B
+ * measurements and independent cross-checks; DESIGN.md 4.5 lists them).
+ * Create-time keys: pair_cache (1; 0 = recompute the pair geometry per call),
+ * ts (1; 0 = no translation-symmetric on-the-fly forward), direct (0; 1 = the
+ * per-term kernels instead of ESAI), pc_plain (0; 1 = list-ordered unpadded
+ * pair cache), pc_segwin (1), pcv_budget_kb (200).  Per-call keys (also
+ * settable with cacsi_set_option): wgemm (0 A-resident, 1 CTA-pair, 2 per-tile),
+ * wgemm_pack, b2gemm_tiles, pc_fwd_list, pcv_items, pcv_pf, pcv_u, pc_bwd_flat,
+ * pcb_pf, subset_bwd_mask, er_bwd_dense, graphs (1; 0 = cacsi_osem by stream
+ * launches).  An unknown key or out-of-range value -> CACSI_ERR_INVALID.
+ * The library never reads the process environment.                          */
+CACSI_API cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *desc, int device, const char *options,
+                                                cacsi_geometry **out);
+
+/* Change a per-call option of a handle (the keys above): later calls launch the
+ * selected kernel variant.  Not synchronised with calls running concurrently on
+ * the handle.  Errors: CACSI_ERR_NULL; CACSI_ERR_INVALID (unknown key, a
+ * create-time key, or a value out of range).                                */
+CACSI_API cacsi_status cacsi_set_option(cacsi_geometry *geom, const char *key, int64_t value);
 
 /* Free the handle and its device tables (synchronises the device).  NULL ok. */
 CACSI_API void cacsi_geometry_destroy(cacsi_geometry *geom);
@@ -263,7 +286,7 @@ CACSI_API cacsi_status cacsi_backward_subset(const cacsi_geometry *geom, const f
  * One outer iteration is captured into a CUDA graph on first use and replayed;
  * the graph is cached in the handle (one per handle, guarded by a mutex) and
  * re-captured when any argument (pointers, offsets, beta, penalty) changes.
- * CACSI_GRAPHS=0 or cacsi_set_timing(1) selects plain stream launches.     */
+ * Option graphs=0 or cacsi_set_timing(1) selects plain stream launches.    */
 CACSI_API cacsi_status cacsi_osem(const cacsi_geometry *geom, float *f, const float *y, const float *r,
                                   const float *b1_subsets, const int32_t *pixels, const int32_t *offsets,
                                   int32_t n_subsets, float beta, const cacsi_penalty *pen, int32_t n_outer,
@@ -286,15 +309,15 @@ CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, co
  * kernels are used), "esai_max_window", "esai_lut_cells",
  * "esai_lut_slow_cells", "esai_ldw" (row stride of the breakpoint tables),
  * "pair_cache_records" (open pairs held in the pair cache, 0 if not built),
- * "pair_cache_record_bytes" (bytes per record: P, packed (b, tau), jy),
+ * "pair_cache_record_bytes" (bytes per record: P, packed (b, tau), pixel q),
  * "pair_cache_tau_bits" (fraction bits of the stored tau),
  * "pair_cache_fwd_row_blocks" (detector row blocks of the voxel-major
  * forward; 0 = the per-list forward runs),
  * "ts_rho" (0 = no translation symmetry), "energy_resolving".  -1 for an
  * unknown key or NULL.
- * The pair cache (DESIGN.md 4.2) is built at create when it fits in half of the
- * free device memory; the environment variable CACSI_PAIR_CACHE=0 disables it
- * (the operators then recompute the pair geometry per call).               */
+ * The pair cache (DESIGN.md 4.2b) is built at create when it fits in half of the
+ * free device memory; the option pair_cache=0 disables it (the operators then
+ * recompute the pair geometry per call).                                    */
 CACSI_API int64_t cacsi_query(const cacsi_geometry *geom, const char *key);
 
 /* Static description of a status code (never NULL). */

@@ -79,6 +79,8 @@ def _L():
         lib.oracle_mask_cell.argtypes = [P(_Desc), ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, P(ctypes.c_int), P(ctypes.c_int)]
         lib.oracle_count_terms.argtypes = [P(_Desc), ctypes.c_long, i64p, i64p]
+        lib.oracle_voxel_centre.argtypes = [P(_Desc), ctypes.c_int, ctypes.c_int, dp]
+        lib.oracle_det_centre.argtypes = [P(_Desc), ctypes.c_int, ctypes.c_int, dp]
         lib.oracle_sai_angle.argtypes = [P(_Desc), ctypes.c_double]
         lib.oracle_sai_angle.restype = ctypes.c_double
         for fn in ("oracle_G_so", "oracle_G_od"):
@@ -190,6 +192,18 @@ class Geometry:
         out = np.zeros(3, dtype=np.int64)
         _L().oracle_count_terms(ctypes.byref(self.s), pix.size, _ip(pix), _ip(out))
         return tuple(int(v) for v in out)
+
+    def voxel_centre(self, iy, iz):
+        """(y, z) of voxel (iy, iz) as oracle.c computes it (reading R9)."""
+        out = np.zeros(2)
+        _L().oracle_voxel_centre(ctypes.byref(self.s), iy, iz, _dp(out))
+        return tuple(out.tolist())
+
+    def det_centre(self, ix, jy):
+        """(x, y) of detector pixel (ix, jy) as oracle.c computes it (reading R9)."""
+        out = np.zeros(2)
+        _L().oracle_det_centre(ctypes.byref(self.s), ix, jy, _dp(out))
+        return tuple(out.tolist())
 
     # -- centres (reading R9), for tests ------------------------------------
     def voxel_centres(self):

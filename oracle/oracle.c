@@ -78,6 +78,16 @@ static double det_y(const oracle_desc *d, int jy) {
 }
 static double q_step(const oracle_desc *d) { return (d->q_max - d->q_min) / (d->nq - 1); }
 
+/* the centre conventions above, exported for the tests' hand-value pins */
+void oracle_voxel_centre(const oracle_desc *d, int iy, int iz, double out[2]) {
+    out[0] = voxel_y(d, iy);
+    out[1] = voxel_z(d, iz);
+}
+void oracle_det_centre(const oracle_desc *d, int ix, int jy, double out[2]) {
+    out[0] = det_x(d, ix);
+    out[1] = det_y(d, jy);
+}
+
 /* ---- vector helpers ------------------------------------------------------ */
 static double dot3(const double a[3], const double b[3]) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 static double norm3(const double a[3]) { return sqrt(dot3(a, a)); }

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libcacsi.so")
 
 CACSI_OK, CACSI_ERR_NULL, CACSI_ERR_INVALID, CACSI_ERR_CUDA, CACSI_ERR_NOMEM = range(5)
 
-SYMBOLS = ["cacsi_geometry_create", "cacsi_geometry_destroy", "cacsi_workspace_bytes", "cacsi_object_size",
+SYMBOLS = ["cacsi_geometry_create", "cacsi_geometry_create_ex", "cacsi_set_option", "cacsi_geometry_destroy", "cacsi_workspace_bytes", "cacsi_object_size",
            "cacsi_detector_size", "cacsi_forward", "cacsi_backward", "cacsi_neg_loglik", "cacsi_iterate",
            "cacsi_forward_host", "cacsi_backward_host", "cacsi_iterate_host", "cacsi_last_launch_count",
            "cacsi_status_string", "cacsi_ratio", "cacsi_update", "cacsi_set_timing", "cacsi_kernel_times",
@@ -88,6 +88,11 @@ def lib():
         vp, fp = ctypes.c_void_p, ctypes.c_void_p
         L.cacsi_geometry_create.argtypes = [ctypes.POINTER(GeometryDesc), ctypes.c_int, ctypes.POINTER(vp)]
         L.cacsi_geometry_create.restype = ctypes.c_int
+        L.cacsi_geometry_create_ex.argtypes = [ctypes.POINTER(GeometryDesc), ctypes.c_int, ctypes.c_char_p,
+                                               ctypes.POINTER(vp)]
+        L.cacsi_geometry_create_ex.restype = ctypes.c_int
+        L.cacsi_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+        L.cacsi_set_option.restype = ctypes.c_int
         L.cacsi_geometry_destroy.argtypes = [vp]
         L.cacsi_geometry_destroy.restype = None
         for n in ("cacsi_workspace_bytes", "cacsi_object_size", "cacsi_detector_size"):
@@ -188,9 +193,11 @@ def _np_f32(a, n, writable=False):
 
 class Geometry:
     """A cacsi_geometry handle.  `desc` is a dict of the descriptor fields
-    (workloads.Config.desc()) with numpy arrays energy_kev, phi, mask."""
+    (workloads.Config.desc()) with numpy arrays energy_kev, phi, mask;
+    `options` the kernel-variant options of cacsi_geometry_create_ex, as a
+    "key=value,..." string or a dict."""
 
-    def __init__(self, desc: dict, device: int = 0):
+    def __init__(self, desc: dict, device: int = 0, options=None):
         d = dict(desc)
         d.setdefault("sai_n_theta", 0)
         d.setdefault("sai_theta_min", 0.0)
@@ -207,8 +214,10 @@ class Geometry:
         s.mask = self._mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
         self._desc = s
         self.handle = ctypes.c_void_p()
-        _check(lib().cacsi_geometry_create(ctypes.byref(s), device, ctypes.byref(self.handle)),
-               "cacsi_geometry_create")
+        if isinstance(options, dict):
+            options = ",".join(f"{k}={int(v)}" for k, v in options.items())
+        _check(lib().cacsi_geometry_create_ex(ctypes.byref(s), device, options.encode() if options else None,
+                                              ctypes.byref(self.handle)), "cacsi_geometry_create_ex")
         self.device = device
         self.f_shape = (d["ny"], d["nz"], d["nq"])
         self.g_shape = (d["det_nx"], d["det_ny"], d["ne"]) if d["energy_resolving"] else (d["det_nx"], d["det_ny"])
@@ -226,6 +235,10 @@ class Geometry:
             self.close()
         except Exception:
             pass
+
+    def set_option(self, key: str, value: int):
+        """cacsi_set_option: select a per-call kernel variant."""
+        _check(lib().cacsi_set_option(self.handle, key.encode(), int(value)), "cacsi_set_option")
 
     def set_timing(self, enable: bool = True):
         _check(lib().cacsi_set_timing(self.handle, int(enable)), "cacsi_set_timing")
@@ -347,5 +360,5 @@ class Geometry:
         return f
 
 
-def geometry_create(desc: dict, device: int = 0) -> Geometry:
-    return Geometry(desc, device)
+def geometry_create(desc: dict, device: int = 0, options=None) -> Geometry:
+    return Geometry(desc, device, options)

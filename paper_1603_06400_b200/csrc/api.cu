@@ -87,12 +87,82 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
 
+// ---- kernel-variant options (internal.h Opts) ----------------
+struct OptKey {
+    const char *name;
+    int cacsi::Opts::*field;
+    bool create_only;
+    int lo, hi;
+};
+const OptKey kOptKeys[] = {
+    {"pair_cache", &cacsi::Opts::pair_cache, true, 0, 1},
+    {"ts", &cacsi::Opts::ts, true, 0, 1},
+    {"direct", &cacsi::Opts::direct, true, 0, 1},
+    {"pc_plain", &cacsi::Opts::pc_plain, true, 0, 1},
+    {"pc_segwin", &cacsi::Opts::pc_segwin, true, 0, 1},
+    {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
+    {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
+    {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
+    {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},
+    {"pc_fwd_list", &cacsi::Opts::pc_fwd_list, false, 0, 1},
+    {"pcv_items", &cacsi::Opts::pcv_items, false, 1, 64},
+    {"pcv_pf", &cacsi::Opts::pcv_pf, false, 0, 16},
+    {"pcv_u", &cacsi::Opts::pcv_u, false, 4, 8},
+    {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
+    {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
+    {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
+    {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
+    {"graphs", &cacsi::Opts::graphs, false, 0, 1},
+};
+
+cacsi_status set_opt(cacsi::Opts &o, const char *key, size_t klen, long long v, bool at_create) {
+    for (const OptKey &k : kOptKeys)
+        if (strlen(k.name) == klen && strncmp(k.name, key, klen) == 0) {
+            if ((k.create_only && !at_create) || v < k.lo || v > k.hi) return CACSI_ERR_INVALID;
+            o.*(k.field) = (int)v;
+            return CACSI_OK;
+        }
+    return CACSI_ERR_INVALID;
+}
+
+// "key=value,key=value" (integers; spaces not allowed); NULL or "" = defaults
+cacsi_status parse_opts(const char *s, cacsi::Opts &o) {
+    o = cacsi::Opts();
+    if (!s) return CACSI_OK;
+    while (*s) {
+        const char *eq = strchr(s, '=');
+        if (!eq || eq == s) return CACSI_ERR_INVALID;
+        if (!((eq[1] >= '0' && eq[1] <= '9') || eq[1] == '-')) return CACSI_ERR_INVALID;
+        char *end = nullptr;
+        const long long v = strtoll(eq + 1, &end, 10);
+        if (end == eq + 1 || (*end != ',' && *end != '\0') || (*end == ',' && end[1] == '\0'))
+            return CACSI_ERR_INVALID;
+        const cacsi_status st = set_opt(o, s, (size_t)(eq - s), v, true);
+        if (st != CACSI_OK) return st;
+        s = *end == ',' ? end + 1 : end;
+    }
+    return CACSI_OK;
+}
+
 }  // namespace
+
+namespace cacsi {
+// Every entry point that touches a handle's device memory runs on the handle's
+// device and restores the caller's current device on return.
+DeviceGuard::DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+}
+DeviceGuard::~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+}
+}  // namespace cacsi
 
 extern "C" {
 
@@ -108,9 +178,17 @@ const char *cacsi_status_string(cacsi_status s) {
 }
 
 cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cacsi_geometry **out) {
+    return cacsi_geometry_create_ex(d, device, nullptr, out);
+}
+
+cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, const char *options,
+                                      cacsi_geometry **out) {
     if (!d || !out) return CACSI_ERR_NULL;
     *out = nullptr;
     cacsi_status st = validate(d);
+    if (st != CACSI_OK) return st;
+    cacsi::Opts opt;
+    st = parse_opts(options, opt);
     if (st != CACSI_OK) return st;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
@@ -119,7 +197,7 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     }
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return CACSI_ERR_CUDA;
-    if (cudaSetDevice(device) != cudaSuccess) return CACSI_ERR_CUDA;
+    cacsi::DeviceGuard dg(device);
     // keep stream-ordered scratch (W / A, split partials) cached across calls
     // instead of returning it to the OS at every synchronisation
     {
@@ -133,6 +211,7 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     cacsi_geometry *g = (cacsi_geometry *)calloc(1, sizeof(cacsi_geometry));
     if (!g) return CACSI_ERR_NOMEM;
     g->device = device;
+    g->opt = opt;
     g->ny = d->ny;
     g->nz = d->nz;
     g->nq = d->nq;
@@ -266,22 +345,21 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
         const double rho = std::floor(dyv / d->det_pitch + 0.5);
         p.ts_rho = 0;
         if (rho >= 1.0 && rho <= 64.0 && std::fabs(dyv - rho * d->det_pitch) <= 1e-9 * d->det_pitch &&
-            !getenv("CACSI_NO_TS") && d->sai_n_theta == 0) {  // SAI runs the tiled forward
+            g->opt.ts && d->sai_n_theta == 0) {  // SAI runs the tiled forward
             p.ts_rho = (int)rho;
             p.ts_c0 = (float)(det_centre(d->det_cy, d->det_ny, d->det_pitch, 0) - centre(d->y_min, d->y_max, d->ny, 0));
             p.vy0 = (float)centre(d->y_min, d->y_max, d->ny, 0);
             p.vy_step = (float)dyv;
         }
     }
-    // ESAI tables for the energy-integrating operators (CACSI_ALGO=direct keeps
+    // ESAI tables for the energy-integrating operators (option direct=1 keeps
     // the per-term kernels, used as a cross-check in the tests)
-    const char *algo = getenv("CACSI_ALGO");
-    if (d->sai_n_theta > 0 && algo && strcmp(algo, "direct") == 0) {  // SAI lives in the ESAI tables
+    if (d->sai_n_theta > 0 && g->opt.direct) {  // SAI lives in the ESAI tables
         free_all(g);
         free(g);
         return CACSI_ERR_INVALID;
     }
-    if (!d->energy_resolving && !(algo && strcmp(algo, "direct") == 0)) {
+    if (!d->energy_resolving && !g->opt.direct) {
         e = cacsi::esai_build(g, d);
         if (e == cudaSuccess && d->sai_n_theta > 0 && !g->esai.enabled) {  // beyond the table limits
             free_all(g);
@@ -299,9 +377,14 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
     return CACSI_OK;
 }
 
+cacsi_status cacsi_set_option(cacsi_geometry *g, const char *key, int64_t value) {
+    if (!g || !key) return CACSI_ERR_NULL;
+    return set_opt(g->opt, key, strlen(key), (long long)value, false);
+}
+
 void cacsi_geometry_destroy(cacsi_geometry *g) {
     if (!g) return;
-    cudaSetDevice(g->device);
+    cacsi::DeviceGuard dg(g->device);
     cudaDeviceSynchronize();
     if (g->timers) {
         const char *names[64];
@@ -327,6 +410,7 @@ int32_t cacsi_last_launch_count(const cacsi_geometry *g) { return g ? g->last_la
 
 cacsi_status cacsi_forward(const cacsi_geometry *g, const float *f, float *out, void *stream) {
     if (!g || !f || !out) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     int n = 0;
     cudaError_t e = cacsi::launch_forward(g, f, out, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -335,6 +419,7 @@ cacsi_status cacsi_forward(const cacsi_geometry *g, const float *f, float *out, 
 
 cacsi_status cacsi_backward(const cacsi_geometry *g, const float *w, float *b, void *stream) {
     if (!g || !w || !b) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     int n = 0;
     cudaError_t e = cacsi::launch_backward(g, w, b, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -364,6 +449,7 @@ static double pen_delta(const cacsi_penalty *pen) {
 cacsi_status cacsi_neg_loglik_ex(const cacsi_geometry *g, const float *f, const float *y, const float *r, float beta,
                                  const cacsi_penalty *pen, double *out_dev, void *ws, void *stream) {
     if (!g || !f || !y || !r || !out_dev || !ws) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     const double delta = pen_delta(pen);
     if (delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
@@ -416,6 +502,7 @@ static cudaError_t iterate_once(const cacsi_geometry *g, const float *fc, const 
 cacsi_status cacsi_iterate_ex(const cacsi_geometry *g, float *f, const float *y, const float *r, const float *b1,
                               float beta, const cacsi_penalty *pen, int32_t n_iter, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1 || !ws) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     const double delta = pen_delta(pen);
     if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
@@ -443,6 +530,7 @@ cacsi_status cacsi_iterate(const cacsi_geometry *g, float *f, const float *y, co
 cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y, const float *r, float *ratio,
                          void *stream) {
     if (!g || !l || !y || !r || !ratio) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     int n = 0;
     cudaError_t e = cacsi::launch_ratio(g, l, y, r, ratio, nullptr, 0, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -452,6 +540,7 @@ cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y
 cacsi_status cacsi_update_ex(const cacsi_geometry *g, const float *f_hat, const float *b1, const float *b2, float beta,
                              const cacsi_penalty *pen, float *f_new, void *stream) {
     if (!g || !f_hat || !b1 || !b2 || !f_new) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     const double delta = pen_delta(pen);
     if (!(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
     int n = 0;
@@ -492,6 +581,7 @@ cacsi_status cacsi_symmetric_subsets(int32_t det_nx, int32_t det_ny, int32_t rho
 cacsi_status cacsi_forward_subset(const cacsi_geometry *g, const float *f, const int32_t *pixels, int32_t n_pixels,
                                   float *out, void *stream) {
     if (!g || !f || !out || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
     int n = 0;
     cudaError_t e = cacsi::launch_forward_subset(g, f, pixels, n_pixels, out, (cudaStream_t)stream, &n);
@@ -502,6 +592,7 @@ cacsi_status cacsi_forward_subset(const cacsi_geometry *g, const float *f, const
 cacsi_status cacsi_backward_subset(const cacsi_geometry *g, const float *w, const int32_t *pixels, int32_t n_pixels,
                                    float *b, void *stream) {
     if (!g || !w || !b || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
     int n = 0;
     cudaError_t e = cacsi::launch_backward_subset(g, w, pixels, n_pixels, b, (cudaStream_t)stream, &n);
@@ -559,6 +650,7 @@ cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const
                         const int32_t *pixels, const int32_t *offsets, int32_t n_subsets, float beta,
                         const cacsi_penalty *pen, int32_t n_outer, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1_subsets || !pixels || !offsets || !ws) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     const double delta = pen_delta(pen);
     if (n_subsets < 1 || n_outer < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0)
         return CACSI_ERR_INVALID;
@@ -572,8 +664,7 @@ cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const
     const float beta_p = beta / (float)n_subsets;  // reading R20: the subset term stands for 1/P of L
     int n = 0;
     cudaError_t e = cudaSuccess;
-    const char *gv = getenv("CACSI_GRAPHS");  // "0": plain stream launches
-    const bool use_graph = n_outer > 0 && !g->timing && !(gv && strcmp(gv, "0") == 0);
+    const bool use_graph = n_outer > 0 && !g->timing && g->opt.graphs;
     if (use_graph) {
         cacsi_geometry *gm = const_cast<cacsi_geometry *>(g);
         if (!gm->osem_graph) gm->osem_graph = new cacsi::OsemGraph();
@@ -637,6 +728,7 @@ static cudaError_t ensure_stage(const cacsi_geometry *gc) {
 
 cacsi_status cacsi_forward_host(const cacsi_geometry *g, const float *fh, float *gh, void *stream) {
     if (!g || !fh || !gh) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = ensure_stage(g);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
@@ -650,6 +742,7 @@ cacsi_status cacsi_forward_host(const cacsi_geometry *g, const float *fh, float 
 
 cacsi_status cacsi_backward_host(const cacsi_geometry *g, const float *wh, float *bh, void *stream) {
     if (!g || !wh || !bh) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = ensure_stage(g);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, wh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
@@ -664,6 +757,7 @@ cacsi_status cacsi_backward_host(const cacsi_geometry *g, const float *wh, float
 cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float *yh, const float *rh,
                                 const float *b1h, float beta, int32_t n_iter, void *stream) {
     if (!g || !fh || !yh || !rh || !b1h) return CACSI_ERR_NULL;
+    cacsi::DeviceGuard dg_(g->device);
     if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     cacsi_geometry *gm = const_cast<cacsi_geometry *>(g);

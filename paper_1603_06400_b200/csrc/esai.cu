@@ -121,6 +121,19 @@ __global__ void k_tbits_fwd_ts(const Params p, uint32_t *tb) {
     }
 }
 
+// seen[j] = OR over voxels of tb_bwd[v][j]: the pixels at least one open pair reaches
+// (grid.y splits the voxels; seen is zeroed first, the chunks OR in)
+__global__ void k_seen(const Params p, const uint32_t *__restrict__ tb, uint32_t *__restrict__ seen) {
+    const int nw = (p.n_det + 31) / 32;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nw) return;
+    const int per = (p.n_vox + gridDim.y - 1) / gridDim.y;
+    const int v0 = blockIdx.y * per, v1 = min(p.n_vox, v0 + per);
+    uint32_t m = 0u;
+    for (int v = v0; v < v1; v++) m |= __ldg(tb + (size_t)v * nw + j);
+    if (m) atomicOr(seen + j, m);
+}
+
 __global__ void k_tbits_bwd(const Params p, uint32_t *tb) {
     // word v * nw + j (nw = ceil(n_det / 32)): bit i = T(v, pixel 32 j + i)
     const int nw = (p.n_det + 31) / 32;
@@ -492,12 +505,15 @@ __global__ void k_list_to_mask(const int32_t *__restrict__ list, int n, uint32_t
 // max |w| over the detector (fixed-point scale of the backward histogram)
 // (pmask != nullptr: only the subset's pixels count -- the fixed-point unit of a
 // subset backward must not be set by weights it never deposits)
+// (seen: only pixels with at least one open pair count -- the others never deposit)
 __global__ void __launch_bounds__(1024) k_absmax(const float *__restrict__ w, size_t n, const uint32_t *pmask,
-                                                 float *out) {
+                                                 const uint32_t *seen, float *out) {
     __shared__ float s[32];
     float m = 0.0f;
     for (size_t i = threadIdx.x; i < n; i += 1024)
-        if (pmask == nullptr || ((pmask[i >> 5] >> (i & 31)) & 1u)) m = fmaxf(m, fabsf(w[i]));
+        if ((pmask == nullptr || ((pmask[i >> 5] >> (i & 31)) & 1u)) &&
+            (seen == nullptr || ((seen[i >> 5] >> (i & 31)) & 1u)))
+            m = fmaxf(m, fabsf(w[i]));
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -713,11 +729,12 @@ struct EpiRatio {
     const float *y, *r;
     float *out;
     unsigned *wmax;  // bits of max |w| (non-negative floats order as unsigned); zeroed by the caller
+    const uint32_t *seen;  // the max runs over the pixels some open pair sees (k_absmax's rule)
     static constexpr bool kMax = true;
     __device__ float operator()(size_t i, double t) const {
         const float v = guarded_ratio(y[i], (float)t + r[i]);
         out[i] = v;
-        return fabsf(v);
+        return (seen == nullptr || ((__ldg(seen + (i >> 5)) >> (i & 31)) & 1u)) ? fabsf(v) : 0.0f;
     }
 };
 struct EpiUpdate {
@@ -1074,8 +1091,16 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         else
             k_tbits_fwd_tiled<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_fwd);
         k_tbits_bwd<<<blocks, 256>>>(p, (uint32_t *)g->d_tb_bwd);
-        e = cudaDeviceSynchronize();
+        const int nwd = (p.n_det + 31) / 32;
+        e = cudaMalloc(&g->d_seen, nwd * sizeof(uint32_t));
+        if (e == cudaSuccess) {
+            e = cudaMemset(g->d_seen, 0, nwd * sizeof(uint32_t));
+            k_seen<<<dim3((nwd + 127) / 128, std::min(p.n_vox, 256)), 128>>>(p, (const uint32_t *)g->d_tb_bwd,
+                                                                              (uint32_t *)g->d_seen);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        }
         if (e != cudaSuccess) return e;
+        E.seen = (const uint32_t *)g->d_seen;
         E.tb_fwd = (const uint32_t *)g->d_tb_fwd;
         E.tb_bwd = (const uint32_t *)g->d_tb_bwd;
     }
@@ -1115,8 +1140,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     // pair cache (above): counts -> host scan -> fill, if it fits in half the free memory
     E.pc = 0;
     E.pc_segwin = nullptr;
-    const char *pce = getenv("CACSI_PAIR_CACHE");
-    if (!(pce && strcmp(pce, "0") == 0) && (size_t)p.det_ny <= 65535) {
+    if (g->opt.pair_cache && (size_t)p.det_ny <= 65535) {
         const size_t nl = (size_t)nv * p.det_nx;
         int *cnt = nullptr;
         e = cudaMalloc(&cnt, nl * sizeof(int));
@@ -1134,8 +1158,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         for (size_t i = 0; i < nl; i++) nopen += hc[i];
         const int n_rb = pcv_row_blocks(g);
         const int R = n_rb > 0 ? (p.det_nx + n_rb - 1) / n_rb : 0;
-        const char *pl = getenv("CACSI_PC_LAYOUT");  // "plain": no padding / bank-aware order (A/B reference)
-        const int segR = (R > 0 && !(pl && strcmp(pl, "plain") == 0)) ? R : 0;
+        const int segR = (R > 0 && !g->opt.pc_plain) ? R : 0;  // pc_plain: no padding / bank-aware order
         std::vector<long long> off(nl + 1, 0);
         for (size_t i = 0; i < nl; i++) {
             off[i + 1] = off[i] + hc[i];
@@ -1229,8 +1252,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) return e;
-                if (!(getenv("CACSI_PC_SEGWIN") && strcmp(getenv("CACSI_PC_SEGWIN"), "0") == 0))
-                    E.pc_segwin = (const int2 *)g->d_pc_segwin;
+                if (g->opt.pc_segwin) E.pc_segwin = (const int2 *)g->d_pc_segwin;
             }
             E.pc = 1;
         }
@@ -1254,8 +1276,7 @@ int pcv_row_blocks(const cacsi_geometry *g) {
     // lists of a segment): the forward must use exactly those row blocks
     if (E.pc && E.pc_R > 0) return (p.det_nx + E.pc_R - 1) / E.pc_R;
     const int wcap = (E.max_win + 3 + 3) & ~3;
-    const char *bs = getenv("CACSI_PCV_BUDGET");  // tuning knob (KB of shared memory per CTA)
-    const size_t budget = (bs ? atoi(bs) : 200) * 1024;
+    const size_t budget = (size_t)g->opt.pcv_budget_kb * 1024;  // KB of shared memory per CTA
     const long long acc_max = (long long)budget - 2ll * wcap * (long long)sizeof(float) - 32 - 128;
     const int r_max = acc_max > 0 ? (int)(acc_max / ((long long)p.det_ny * sizeof(float))) : 0;
     return r_max >= 1 ? (p.det_nx + r_max - 1) / r_max : 0;
@@ -1299,15 +1320,14 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         return e;
     }
     const int nkcA = ldf / TC_KC;
-    const char *gv0 = getenv("CACSI_WGEMM");
-    const bool ar_path = ((E.pc && pixels == nullptr) || pixels != nullptr) && nkcA <= 4 &&
-                         !(gv0 && (strcmp(gv0, "ar2") == 0 || strcmp(gv0, "tiles") == 0));
+    const Opts &o = g->opt;
+    const bool ar_path = ((E.pc && pixels == nullptr) || pixels != nullptr) && nkcA <= 4 && o.wgemm == 0;
     const int nfc = (epi && epi->f_chunks > 0) ? epi->f_chunks : 0;
     // the A-resident W GEMM reads f itself (TMA tensor loads + in-kernel TF32 split) when
     // f's rows are 16-byte multiples; otherwise k_tc_pack_a pre-splits it
     CUtensorMap tmF;
     memset(&tmF, 0, sizeof(tmF));
-    const bool raw = ar_path && (p.nq % 4) == 0 && !(getenv("CACSI_WGEMM_PACK")) &&
+    const bool raw = ar_path && (p.nq % 4) == 0 && !o.wgemm_pack &&
                      tmap_rows_f32(&tmF, f, (uint64_t)p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq);
     if (nfc > 0 && !ar_path)
         for (int c = 0; c < nfc && e == cudaSuccess; c++) e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
@@ -1353,15 +1373,14 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             // plain W rows (n_vox x ldw fp32): the pair-cache and the subset forwards gather W_b
             // and W_{b+1}; the pair layout below serves the full on-the-fly kernels
             const int nt = tc_ntiles(E.nb, TC_N), mt = (p.n_vox + TC_M - 1) / TC_M;
-            const char *gv = getenv("CACSI_WGEMM");  // "tiles": the per-tile kernel (A/B reference)
-            if (nkcA <= 4 && gv && strcmp(gv, "ar2") == 0) {
+            if (nkcA <= 4 && o.wgemm == 1) {
                 // the CTA-pair (cta_group::2) variant: bit-identical, measured slower
                 const int mp = (int)(mt_even / 2);
                 cudaFuncSetAttribute(k_tc_gemm_ar2, cudaFuncAttributeMaxDynamicSharedMemorySize, tca2_smem(nkcA));
                 const int npairs = std::max(1, std::min(mp * nt, sm_count(g->device) / 2));
                 k_tc_gemm_ar2<<<2 * npairs, TCA_T1, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
                                                                         E.ldw);
-            } else if (nkcA <= 4 && !(gv && strcmp(gv, "tiles") == 0)) {
+            } else if (nkcA <= 4 && o.wgemm == 0) {
                 // B ring depth: 3 stages where they fit beside the resident A panel (nkc <= 2), else 2
                 // (config 2, nq = 128: nkc = 4, the 128 KB panel leaves room for 2)
                 const int nsb = tca_smem(nkcA, 3) <= 227 * 1024 ? 3 : 2;
@@ -1419,12 +1438,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     } else if (E.pc) {
         const int wcap = (E.max_win + 3 + 3) & ~3;
         const int n_rb = pcv_row_blocks(g);
-        const char *pv = getenv("CACSI_PC_FWD");  // "list": the per-list kernel (plain layout only)
-        if (n_rb > 0 && (E.pc_R > 0 || !(pv && strcmp(pv, "list") == 0))) {
+        if (n_rb > 0 && (E.pc_R > 0 || !o.pc_fwd_list)) {  // pc_fwd_list: per-list kernel (plain layout only)
             // voxel-major: items (voxel chunk, row block), fp64 partials per voxel chunk
             const int R = (p.det_nx + n_rb - 1) / n_rb;
-            const char *is = getenv("CACSI_PCV_ITEMS");  // tuning knob (items per SM)
-            const int ipsm = is ? atoi(is) : 2;
+            const int ipsm = o.pcv_items;  // voxel chunks per SM
             int Sv = std::max(1, std::min(p.n_vox, (ipsm * sm_count(g->device) + n_rb - 1) / n_rb));
             const int vchunk = (p.n_vox + Sv - 1) / Sv;
             const int n_chunks = (p.n_vox + vchunk - 1) / vchunk;
@@ -1436,11 +1453,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             e = cudaMallocAsync(&part, (size_t)S * p.n_det * sizeof(double), s);
             if (e == cudaSuccess) {
                 KScope kt_(g, s, "k_pc_fwd");
-                const char *pfs = getenv("CACSI_PCV_PF");  // tuning knob (voxels ahead)
-                const int pf = pfs ? atoi(pfs) : 1;
+                const int pf = o.pcv_pf;  // L2 prefetch distance (voxels ahead)
                 const int n_items = n_chunks * n_rb;
-                const char *us = getenv("CACSI_PCV_U");  // tuning knob (records per thread per step)
-                const int U = us ? atoi(us) : 4;
+                const int U = o.pcv_u;  // records per thread per step
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
                 auto kf = E.pc_qb == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024>
@@ -1498,7 +1513,7 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
         KScope kt_(g, s, "k_sum_parts_f64");
         if (epi && epi->yr_ready) e = cudaStreamWaitEvent(s, epi->yr_ready, 0);
         if (epi)
-            sum_parts(part, S, (size_t)p.n_det, EpiRatio{epi->y, epi->r, out, (unsigned *)epi->wmax}, s);
+            sum_parts(part, S, (size_t)p.n_det, EpiRatio{epi->y, epi->r, out, (unsigned *)epi->wmax, E.seen}, s);
         else
             sum_parts(part, S, (size_t)p.n_det, EpiStore{out}, s);
     }
@@ -1552,21 +1567,20 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     // union of its voxels' windows (A is zero there); the per-tile GEMM reads whole rows
     const int mt = (p.n_vox + TC_M - 1) / TC_M;
     CUtensorMap tm;
-    const char *gv = getenv("CACSI_B2GEMM");  // "tiles": the per-tile kernel (A/B reference)
-    const bool splitk = p.nq <= TC_N && !(gv && strcmp(gv, "tiles") == 0) &&
+    const Opts &o = g->opt;
+    const bool splitk = p.nq <= TC_N && !o.b2gemm_tiles &&
                         tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw);
     if (e == cudaSuccess) {
         if (epi) {
             wmax = (float *)epi->wmax;  // computed by the fused forward (not freed here)
         } else {
             KScope kt_(g, s, "k_absmax");
-            k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, pmask, wmax);
+            k_absmax<<<1, 1024, 0, s>>>(w, (size_t)p.n_det, pmask, E.seen, wmax);
         }
         if (E.pc && pmask == nullptr) {
             KScope kt_(g, s, "k_pc_bwd");
             const size_t hs = (size_t)E.max_win * sizeof(int);
-            const char *bv = getenv("CACSI_PC_BWD");  // "flat": the register-fed kernel (A/B reference)
-            if (!(bv && strcmp(bv, "flat") == 0)) {
+            if (!o.pc_bwd_flat) {  // pc_bwd_flat: the register-fed kernel (A/B reference)
                 // 512 threads x 4 records, two stages (measured best of 128/256/512/1024 threads
                 // and 2/3 stages with the vector mapping): ~69 KB with the histogram, 3 CTAs/SM
                 constexpr int U = 4, T = 512, NS = 2;
@@ -1577,13 +1591,12 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, T, sm);
                 kb<<<std::min(p.n_vox, std::max(1, nb) * sm_count(g->device)), T, sm, s>>>(p, E, w, wmax, A);
             } else {
-            const char *pfs = getenv("CACSI_PCB_PF");  // tuning knob (steps ahead)
-            const int pf = pfs ? atoi(pfs) : 2;
+            const int pf = o.pcb_pf;  // rolling L2 prefetch (steps ahead)
             auto kb = E.pc_qb == 2 ? k_pc_bwd<uint16_t> : k_pc_bwd<uint32_t>;
             cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
             kb<<<std::min(p.n_vox, 8 * sm_count(g->device)), PCB_T, hs, s>>>(p, E, w, wmax, pf, A);
             }
-        } else if (list != nullptr && !(getenv("CACSI_SUBSET_BWD") && strcmp(getenv("CACSI_SUBSET_BWD"), "mask") == 0)) {
+        } else if (list != nullptr && !o.subset_bwd_mask) {
             // warps per CTA: as many voxel histograms as fit next to the breakpoint tables
             const size_t bpb = host_bp_bytes(E), hb = (size_t)((E.max_win + 3) & ~3) * sizeof(int);
             const int nwarps = (int)std::max((size_t)1, std::min((size_t)8, ((size_t)200 * 1024 - bpb) / hb));

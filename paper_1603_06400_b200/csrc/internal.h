@@ -81,6 +81,11 @@ struct Esai {
     const int *w_pre;   // W GEMM tile list: exclusive prefix count of the N tiles inside trng, per M tile [+1]
     const int2 *w_ntr;  // W GEMM tile list: first / last N tile inside trng, per M tile
     const float *ptot;  // per voxel sum_pixels |P| (fixed-point bound)
+    // pixels seen by at least one open pair ([ceil(n_det / 32)] bits): only their
+    // weights can reach a backward histogram, so max |w| (the fixed-point scale) is
+    // taken over them -- a huge w on a pixel no voxel sees (e.g. the ratio guard
+    // y / 1e-12 where A f + r = 0) cannot wipe out every other deposit
+    const uint32_t *seen;
     // precomputed transmission bits T(r, r') (mask factors computed
     // offline), one bit per pair in the order each pair kernel visits them
     const uint32_t *tb_fwd;  // forward (TS or tiled layout, esai.cu)
@@ -110,10 +115,39 @@ struct Esai {
     int stat_win_permille, stat_tile_permille;  // mean voxel window / 128-voxel tile K span, per mille of nb
 };
 
+// Kernel-variant options of a handle (cacsi_geometry_create_ex "key=value,..." and
+// cacsi_set_option).  The defaults are the measured-best settings;
+// every other value selects a kernel that computes the same operator (an A/B
+// measurement or an independent cross-check in the tests).  Nothing in the
+// library reads the process environment.
+struct Opts {
+    // create-time (fixed for the life of the handle)
+    int pair_cache = 1;       // "pair_cache": 0 = recompute the pair geometry per call
+    int ts = 1;               // "ts": 0 = no translation-symmetric on-the-fly forward
+    int direct = 0;           // "direct": 1 = per-term kernels instead of ESAI
+    int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
+    int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
+    int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
+    // per call (cacsi_set_option may change them between calls)
+    int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
+    int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
+    int b2gemm_tiles = 0;     // "b2gemm_tiles": 1 = per-tile b2 GEMM instead of the persistent split-K one
+    int pc_fwd_list = 0;      // "pc_fwd_list": 1 = per-list pair-cache forward (plain layout only)
+    int pcv_items = 2;        // "pcv_items": voxel chunks per SM of the voxel-major forward
+    int pcv_pf = 1;           // "pcv_pf": L2 prefetch distance (voxels) of the voxel-major forward
+    int pcv_u = 4;            // "pcv_u": records per thread per step (4 or 8)
+    int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
+    int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
+    int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
+    int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
+    int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
+};
+
 }  // namespace cacsi
 
 struct cacsi_geometry {
     int device;
+    cacsi::Opts opt;
     cacsi::Params p;
     // copies of the descriptor scalars we need later
     int32_t ny, nz, nq, ne, det_nx, det_ny, energy_resolving;
@@ -123,7 +157,7 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin;
+        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs
@@ -138,6 +172,13 @@ struct cacsi_geometry {
 };
 
 namespace cacsi {
+
+// sets the handle's device for the scope of an entry point, restores the caller's after
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
 
 struct TimerRec {
     const char *name;

@@ -399,8 +399,7 @@ cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, c
             KScope kt_(g, s, "k_transpose");
             k_transpose<<<dim3((p.ne + 31) / 32, (p.n_det + 31) / 32), dim3(32, 8), 0, s>>>(w, p.n_det, p.ne, wT);
         }
-        const char *ev = getenv("CACSI_ER_BWD");  // "dense": lanes on all pixels (A/B reference)
-        if (!(ev && strcmp(ev, "dense") == 0)) {
+        if (!g->opt.er_bwd_dense) {  // er_bwd_dense: lanes on all pixels (A/B reference)
             const size_t smc = smem + (size_t)(BWD_T / 32) * ERQ_CAP * sizeof(ErQ);
             cudaFuncSetAttribute(k_backward_er_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
             KScope kt_(g, s, "k_backward_er");

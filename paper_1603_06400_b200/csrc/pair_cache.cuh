@@ -308,6 +308,9 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     const int r0 = rb * R, r1 = min(p.det_nx, r0 + R);
     const int q0 = r0 * p.det_ny, nacc = (r1 - r0) * p.det_ny;
     for (int i = tid; i < nacc; i += PCV_T) acc[i] = 0.0f;
+    // every thread's zeroing before any thread's first deposit (the mbarrier wait below
+    // orders only the bulk copy, not the other warps' stores)
+    __syncthreads();
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int c = item / n_rb;
         const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);

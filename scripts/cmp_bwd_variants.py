@@ -12,7 +12,7 @@ for ci in (1, 3, 2):
             w = torch.as_tensor(rng.uniform(0, 3000, G.g_shape).astype(np.float32)).cuda()
         outs = {}
         for mode in ("flat", "tma", "tma"):
-            os.environ["CACSI_PC_BWD"] = mode
+            G.set_option("pc_bwd_flat", int(mode == "flat"))
             b = torch.empty(G.f_shape, device="cuda")
             G.backward(w, b)
             torch.cuda.synchronize()

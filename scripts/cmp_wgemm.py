@@ -15,7 +15,7 @@ for ci in (0, 1, 2):
     f = torch.as_tensor(cfg.f).cuda()
     out = {}
     for mode in ("ar", "ar2"):
-        os.environ["CACSI_WGEMM"] = mode
+        G.set_option("wgemm", {"ar": 0, "ar2": 1}[mode])
         g = torch.empty(G.g_shape, device="cuda")
         G.forward(f, g)
         torch.cuda.synchronize()

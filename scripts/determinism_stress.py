@@ -24,7 +24,7 @@ for ci in (1, 2):
     torch.cuda.synchronize()
     bad_f = bad_b = 0
     for mode in ("flat", "tma"):
-        os.environ["CACSI_PC_BWD"] = mode
+        G.set_option("pc_bwd_flat", int(mode == "flat"))
         for r in range(reps):
             g = torch.empty_like(g0)
             b = torch.empty_like(b0)

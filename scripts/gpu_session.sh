@@ -8,13 +8,13 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/${TAG}_smi.txt
 echo "nproc=$(nproc)" >> $OUT/${TAG}_smi.txt
 if [[ $STAGES == *test* ]]; then
-  timeout 900 python -m pytest tests -m gpu -q -s -x > $OUT/${TAG}_pytest.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_pytest.log
+  timeout 2400 python -m pytest tests -m gpu -q -s > $OUT/${TAG}_pytest.log 2>&1; echo "rc=$?" >> $OUT/${TAG}_pytest.log
 fi
 if [[ $STAGES == *bench* ]]; then
   timeout 600 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "rc=$?" >> $OUT/${TAG}_bench.err
 fi
 if [[ $STAGES == *micro* ]]; then
-  ./scripts/micro/smem_atomic > $OUT/${TAG}_micro.log 2>&1
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/smem_atomic scripts/micro/smem_atomic.cu && /tmp/smem_atomic > $OUT/${TAG}_micro.log 2>&1
 fi
 if [[ $STAGES == *ncu* ]]; then
   CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"

@@ -1,11 +1,11 @@
 #!/bin/bash
-# Time bench.py under several environment settings (kernel-variant sweeps).
-# usage (on the GPU box): bash scripts/sweep_env.sh TAG "VAR=a VAR2=b" "VAR=c" ...
+# Time bench.py under several kernel-variant option sets (cacsi_geometry_create_ex).
+# usage (on the GPU box): bash scripts/sweep_opts.sh TAG "key=a,key2=b" "key=c" ...
 TAG=$1; shift
 mkdir -p gpurun_out
 for cfg in "$@"; do
-  name=$(echo "$cfg" | tr ' =' '_-')
-  env $cfg timeout 300 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err
+  name=$(echo "$cfg" | tr ',=' '_-')
+  timeout 300 python bench.py --no-cpu-baseline --steps 20 --options "$cfg" > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err
   python - "$cfg" gpurun_out/${TAG}_${name}.json >> gpurun_out/${TAG}_sweep.txt <<'PY'
 import json, sys
 try:

@@ -44,7 +44,7 @@ def _desc(**over):
     return d
 
 
-def _create(d):
+def _create(d, options=None):
     g = binding.GeometryDesc()
     e = np.ascontiguousarray(d["energy_kev"], np.float64)
     ph = np.ascontiguousarray(d["phi"], np.float64)
@@ -56,7 +56,7 @@ def _create(d):
     g.phi = ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     g.mask = m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
     h = ctypes.c_void_p()
-    st = P.lib().cacsi_geometry_create(ctypes.byref(g), 0, ctypes.byref(h))
+    st = P.lib().cacsi_geometry_create_ex(ctypes.byref(g), 0, options, ctypes.byref(h))
     if st == 0:
         P.lib().cacsi_geometry_destroy(h)
     return st
@@ -118,3 +118,25 @@ def test_symmetric_subsets_rejects_bad_steps(args):
     with pytest.raises(binding.CacsiError) as ei:
         binding.symmetric_subsets(*args)
     assert ei.value.status == binding.CACSI_ERR_INVALID
+
+
+@pytest.mark.parametrize("opts", [b"bogus=1", b"pair_cache=2", b"pair_cache", b"=1", b"ts=0,", b"ts=0;direct=1",
+                                  b"pcv_budget_kb=1000", b"wgemm=x", b"ts= 0"])
+def test_invalid_options_rejected(opts):
+    """Kernel-variant options are validated before any device is touched."""
+    assert _create(_desc(), opts) == binding.CACSI_ERR_INVALID
+
+
+@pytest.mark.parametrize("opts", [None, b"", b"pair_cache=0", b"ts=0,direct=1,wgemm=2", b"graphs=0,pcv_items=4"])
+def test_valid_options_reach_the_device_check(opts):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    assert _create(_desc(), opts) == binding.CACSI_ERR_CUDA
+
+
+def test_library_reads_no_environment():
+    """No getenv in the C ABI library (kernel variants are explicit options)."""
+    csrc = os.path.join(ROOT, "paper_1603_06400_b200", "csrc")
+    for fn in os.listdir(csrc):
+        assert "getenv" not in open(os.path.join(csrc, fn)).read(), fn

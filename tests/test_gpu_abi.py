@@ -225,7 +225,7 @@ def test_iterate_host_ragged_chunks(n_iter):
     G.close()
 
 
-def test_subset_backward_list_matches_mask(monkeypatch):
+def test_subset_backward_list_matches_mask():
     """The list-driven subset backward (warp per voxel over the listed pixels)
     and the bitmap-masked one deposit the same integers: bit-identical."""
     cfg = make_config(1)
@@ -236,7 +236,7 @@ def test_subset_backward_list_matches_mask(monkeypatch):
         px = torch.as_tensor(np.flatnonzero(sub == p).astype(np.int32)).cuda()
         out = []
         for mode in ("list", "mask"):
-            monkeypatch.setenv("CACSI_SUBSET_BWD", mode)
+            G.set_option("subset_bwd_mask", int(mode == "mask"))
             b = torch.empty(G.f_shape, device="cuda")
             G.backward_subset(w, px, b)
             torch.cuda.synchronize()
@@ -245,10 +245,10 @@ def test_subset_backward_list_matches_mask(monkeypatch):
     G.close()
 
 
-def test_osem_graph_replay_matches_stream_launches(monkeypatch):
+def test_osem_graph_replay_matches_stream_launches():
     """cacsi_osem replays a captured CUDA graph of the outer iteration (cached per
     handle while the arguments match); the iterates are bit-identical to plain
-    stream launches (CACSI_GRAPHS=0), including after the arguments change."""
+    stream launches (option graphs=0), including after the arguments change."""
     cfg = make_config(0)
     G = P.Geometry(cfg.desc())
     sub = P.binding.symmetric_subsets(cfg.det_nx, cfg.det_ny, 2, 4).ravel()
@@ -266,7 +266,7 @@ def test_osem_graph_replay_matches_stream_launches(monkeypatch):
     ws = torch.empty(G.workspace_bytes, dtype=torch.uint8, device="cuda")
     res = {}
     for mode in ("1", "0"):
-        monkeypatch.setenv("CACSI_GRAPHS", mode)
+        G.set_option("graphs", int(mode))
         f = torch.full(G.f_shape, 1.0, device="cuda")
         G.osem(f, y, r, b1s, allpix, offs, 1e-3, None, 2, ws)
         G.osem(f, y, r, b1s, allpix, offs, 1e-3, None, 1, ws)   # replay of the cached graph

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("ci", [1, 2])
-def test_repeat_bitwise(ci, monkeypatch):
+def test_repeat_bitwise(ci):
     cfg = make_config(ci)
     G = P.Geometry(cfg.desc())
     f = torch.as_tensor(cfg.f).cuda()
@@ -32,15 +32,15 @@ def test_repeat_bitwise(ci, monkeypatch):
         G.backward(w, b)
         assert torch.equal(g, g0)
         assert torch.equal(b, b0)
-    monkeypatch.setenv("CACSI_PC_BWD", "flat")
+    G.set_option("pc_bwd_flat", 1)
     b = torch.empty_like(b0)
     G.backward(w, b)
     assert torch.equal(b, b0)
     G.close()
 
 
-def test_cta_pair_w_gemm_bitwise(monkeypatch):
-    """The cta_group::2 W GEMM (CACSI_WGEMM=ar2: M = 256 per CTA pair, half of
+def test_cta_pair_w_gemm_bitwise():
+    """The cta_group::2 W GEMM (option wgemm=1: M = 256 per CTA pair, half of
     each B chunk per SM, multicast commits) gives the same bits as the
     single-CTA A-resident GEMM."""
     cfg = make_config(1)
@@ -48,7 +48,7 @@ def test_cta_pair_w_gemm_bitwise(monkeypatch):
     f = torch.as_tensor(cfg.f).cuda()
     out = []
     for mode in ("ar", "ar2"):
-        monkeypatch.setenv("CACSI_WGEMM", mode)
+        G.set_option("wgemm", {"ar": 0, "ar2": 1}[mode])
         g = torch.empty(G.g_shape, device="cuda")
         G.forward(f, g)
         torch.cuda.synchronize()

@@ -20,18 +20,16 @@ pytestmark = pytest.mark.gpu
 COUNTS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "workloads", "work_counts.json")))
 
 
-def handles(d, monkeypatch):
+def handles(d):
     Gc = P.Geometry(d)
-    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
-    Gn = P.Geometry(d)
-    monkeypatch.delenv("CACSI_PAIR_CACHE")
+    Gn = P.Geometry(d, options="pair_cache=0")
     return Gc, Gn
 
 
 @pytest.mark.parametrize("ci", [1, 2])
-def test_record_count_is_the_open_pair_count(ci, monkeypatch):
+def test_record_count_is_the_open_pair_count(ci):
     cfg = make_config(ci)
-    Gc, Gn = handles(cfg.desc(), monkeypatch)
+    Gc, Gn = handles(cfg.desc())
     assert Gc.query("pair_cache_records") == COUNTS[str(cfg.seed)]["open_pairs"]
     assert Gn.query("pair_cache_records") == 0
     # P (4 B) + packed (b, tau) (4 B) + pixel q (2 B for n_det <= 65536)
@@ -41,10 +39,10 @@ def test_record_count_is_the_open_pair_count(ci, monkeypatch):
     Gn.close()
 
 
-def test_cache_on_off_config1(monkeypatch):
+def test_cache_on_off_config1():
     cfg = make_config(1)
     O = oracle.Geometry(cfg)
-    Gc, Gn = handles(cfg.desc(), monkeypatch)
+    Gc, Gn = handles(cfg.desc())
     gr = O.forward(cfg.f)
     w = rnd(Gc.g_shape, 1, 70)
     br = O.backward(w)
@@ -56,13 +54,12 @@ def test_cache_on_off_config1(monkeypatch):
     Gn.close()
 
 
-def test_on_the_fly_config2_sampled(monkeypatch):
+def test_on_the_fly_config2_sampled():
     """Full-size config 2 on the kernels that recompute the pair geometry per
     call (the subset operators and the no-cache fallback use them)."""
     cfg = make_config(2)
     O = oracle.Geometry(cfg)
-    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
-    G = P.Geometry(cfg.desc())
+    G = P.Geometry(cfg.desc(), options="pair_cache=0")
     g = gpu_forward(G, cfg.f).ravel()
     pix = _sample(cfg.n_det, 96, 11)
     assert_parity(g[pix], O.forward_pixels(cfg.f, pix), "c2 on-the-fly forward sampled")
@@ -73,21 +70,20 @@ def test_on_the_fly_config2_sampled(monkeypatch):
     G.close()
 
 
-def test_sai_without_cache(monkeypatch):
+def test_sai_without_cache():
     cfg = make_config(1)
     d = cfg.desc()
     d.update(sai_n_theta=250, sai_theta_min=0.2 * math.pi / 180, sai_theta_max=math.pi / 6)
-    monkeypatch.setenv("CACSI_PAIR_CACHE", "0")
-    G, O = P.Geometry(d), oracle.Geometry(d)
+    G, O = P.Geometry(d, options="pair_cache=0"), oracle.Geometry(d)
     assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), "c1 SAI on-the-fly forward")
     w = rnd(G.g_shape, 1, 72)
     assert_parity(gpu_backward(G, w), O.backward(w), "c1 SAI on-the-fly backward")
     G.close()
 
 
-def test_per_list_forward_config1(monkeypatch):
+def test_per_list_forward_config1():
     """The per-list pair-cache forward (used when the voxel-major kernel's
-    shared-memory window does not fit; CACSI_PC_FWD=list forces it) against
+    shared-memory window does not fit; option pc_fwd_list=1 forces it) against
     the oracle and against the voxel-major kernel."""
     cfg = make_config(1)
     O = oracle.Geometry(cfg)
@@ -95,14 +91,12 @@ def test_per_list_forward_config1(monkeypatch):
     assert G.query("pair_cache_records") > 0
     gv = gpu_forward(G, cfg.f)
     # the per-list kernel needs the plain (list-ordered, unpadded) layout
-    monkeypatch.setenv("CACSI_PC_LAYOUT", "plain")
-    Gp = P.Geometry(cfg.desc())
-    monkeypatch.delenv("CACSI_PC_LAYOUT")
+    Gp = P.Geometry(cfg.desc(), options="pc_plain=1")
     assert Gp.query("pair_cache_padded_records") == Gp.query("pair_cache_records")
-    monkeypatch.setenv("CACSI_PC_FWD", "list")
+    Gp.set_option("pc_fwd_list", 1)
     gl = gpu_forward(Gp, cfg.f)
+    G.set_option("pc_fwd_list", 1)
     assert torch.equal(torch.as_tensor(gpu_forward(G, cfg.f)), torch.as_tensor(gv))  # ignored by a bank-ordered cache
-    monkeypatch.delenv("CACSI_PC_FWD")
     assert_parity(gl, O.forward(cfg.f), "c1 per-list cache forward")
     assert_parity(gl, gv, "c1 per-list vs voxel-major forward", l2=1e-6, mr=1e-5)
     w = rnd(G.g_shape, 1, 73)

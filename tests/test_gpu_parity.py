@@ -218,7 +218,9 @@ def test_config3_b1_and_iterates(config3):
             k = np.unravel_index(np.argmax(rel), rel.shape)
             print("worst", k, x[k], ref[k], "b1", b1.cpu().numpy()[k], b1_ref[k], "b2", b2g[k], b2r[k],
                   "f0", f0[k])
-        assert_parity(f.cpu().numpy(), ref_iters[t], f"c3 iterate {t + 1}", l2=1e-5 * (t + 1), mr=1e-4 * (t + 1))
+        # each iterate at the operators' own bar (1e-5 per iterate while the
+        # operator error stays below 3e-6; measured <= 5e-7, profiles/r1s3_parity_margins.json)
+        assert_parity(f.cpu().numpy(), ref_iters[t], f"c3 iterate {t + 1}")
 
 
 def test_config3_neg_loglik(config3):
@@ -232,7 +234,7 @@ def test_config3_neg_loglik(config3):
     v1 = out.item()
     G.neg_loglik(cuda(f), cuda(y), cuda(r), beta, out, ws)
     assert out.item() == v1  # deterministic
-    assert v1 == pytest.approx(ref, rel=1e-6)
+    assert v1 == pytest.approx(ref, rel=1e-7)
 
 
 def test_host_entry_points_match_device(config3):
@@ -257,63 +259,71 @@ def test_deterministic_operators():
 
 
 # ------------------------------------------------ direct per-term algorithm --
-def test_direct_algorithm_energy_resolving(monkeypatch):
-    """CACSI_ALGO=direct for the energy-resolving operators on a ragged shape
+def test_direct_algorithm_energy_resolving():
+    """Option direct=1 for the energy-resolving operators on a ragged shape
     (per-pixel forward threads, compacted-open-pair backward)."""
-    monkeypatch.setenv("CACSI_ALGO", "direct")
     cfg = make_config(0, energy_resolving=1)
     d = cfg.desc()
     d.update(ny=6, nz=5, nq=21, det_nx=7, det_ny=19)
-    G, O = geoms(d)
+    G, O = P.Geometry(d, options="direct=1"), oracle.Geometry(d)
     f, w = rnd(G.f_shape, 0, 70), rnd(G.g_shape, 0, 71)
     assert_parity(gpu_forward(G, f), O.forward(f), "direct er forward")
     assert_parity(gpu_backward(G, w), O.backward(w), "direct er backward")
 
 
 @pytest.mark.parametrize("ci", [0, 1])
-def test_direct_algorithm_parity(ci, monkeypatch):
-    """CACSI_ALGO=direct: the per-term kernels (no ESAI tables) for the
+def test_direct_algorithm_parity(ci):
+    """Option direct=1: the per-term kernels (no ESAI tables) for the
     energy-integrating operators, kept as an independent GPU cross-check."""
-    monkeypatch.setenv("CACSI_ALGO", "direct")
     cfg = make_config(ci)
-    G, O = geoms(cfg)
+    G, O = P.Geometry(cfg.desc(), options="direct=1"), oracle.Geometry(cfg)
     assert_parity(gpu_forward(G, cfg.f), O.forward(cfg.f), f"direct c{ci} forward")
     w = rnd(G.g_shape, ci, 50)
     assert_parity(gpu_backward(G, w), O.backward(w), f"direct c{ci} backward")
 
 
-def test_esai_matches_direct_config2(monkeypatch):
+def test_esai_matches_direct_config2():
     """The two GPU algorithms agree on the full config-2 operators (GPU-vs-GPU
     consistency; each is held to the oracle bar elsewhere).  5e-6 covers the
     3xTF32 tensor-core contraction's ~3e-6."""
     cfg = make_config(2)
     G = P.Geometry(cfg.desc())
-    monkeypatch.setenv("CACSI_ALGO", "direct")
-    D = P.Geometry(cfg.desc())
+    D = P.Geometry(cfg.desc(), options="direct=1")
     w = rnd(G.g_shape, 2, 51)
     assert rel_l2(gpu_forward(G, cfg.f), gpu_forward(D, cfg.f)) < 5e-6
     assert rel_l2(gpu_backward(G, w), gpu_backward(D, w)) < 5e-6
 
 
 # ------------------------------------------------- translation symmetry (TS) --
-@pytest.mark.parametrize("over", [
-    dict(det_pitch=1.0),                                  # rho = 2
-    dict(det_pitch=2.0, det_cx=28.0),                     # rho = 1
-    dict(det_pitch=0.5, det_nx=20, det_ny=150),           # rho = 4, two ragged 128-pixel segments
-    dict(det_pitch=1.0, ny=70, y_min=-70.0, y_max=70.0, det_ny=23, mask_ny=200),  # ny > 64 batch, ragged
+@pytest.mark.parametrize("over,rho", [
+    (dict(det_pitch=1.0), 2),
+    (dict(det_pitch=2.0, det_cx=28.0), 1),
+    (dict(det_pitch=0.5, det_nx=20, det_ny=150), 4),          # two ragged 128-pixel segments
+    (dict(det_pitch=1.0, ny=70, y_min=-70.0, y_max=70.0, det_ny=23, mask_ny=200), 2),  # ny > 64 batch, ragged
 ])
-def test_translation_symmetric_forward(over, monkeypatch):
-    """TS forward kernel (footprint per z row reused as integer shifts) vs the
-    oracle, and vs the same handle without TS."""
+def test_translation_symmetric_forward(over, rho):
+    """The on-the-fly TS forward kernel k_esai_fwd_ts (footprint per z row reused
+    as integer shifts) vs the oracle, and vs the tiled
+    on-the-fly forward (ts=0).  Both handles run without the pair cache, so the
+    TS kernel is the one that runs (the pair-cache forward takes precedence)."""
     cfg = make_config(0)
     d = cfg.desc()
     d.update(over)
     if "mask_ny" in over:
         d["mask"] = seeded_rng(0, 60).integers(0, 2, (d["mask_nx"], d["mask_ny"])).astype(np.uint8)
-    G, O = geoms(d)
+    G = P.Geometry(d, options="pair_cache=0")
+    G2 = P.Geometry(d, options="pair_cache=0,ts=0")
+    O = oracle.Geometry(d)
+    assert G.query("ts_rho") == rho and G.query("pair_cache_records") == 0
+    assert G2.query("ts_rho") == 0
     f = rnd(G.f_shape, 0, 61)
+    G.set_timing(True)
     g = gpu_forward(G, f)
-    assert_parity(g, O.forward(f), f"TS {over} forward")
-    monkeypatch.setenv("CACSI_NO_TS", "1")
-    G2 = P.Geometry(d)
-    assert rel_l2(g, gpu_forward(G2, f)) < 1e-6
+    assert "k_esai_fwd_ts" in G.kernel_times()
+    G2.set_timing(True)
+    g2 = gpu_forward(G2, f)
+    assert "k_esai_fwd" in G2.kernel_times()
+    ref = O.forward(f)
+    assert_parity(g, ref, f"TS {over} forward")
+    assert_parity(g2, ref, f"tiled {over} forward")
+    assert rel_l2(g, g2) < 1e-6

@@ -82,7 +82,7 @@ def test_iterate_and_objective_huber(em0):
     for t in range(3):
         G.iterate_ex(f, cuda(y), cuda(r), b1, beta, ("huber", 0.05), 1, ws)
         torch.cuda.synchronize()
-        assert_parity(f.cpu().numpy(), ref[t], f"huber iterate {t + 1}", l2=1e-5 * (t + 1), mr=1e-4 * (t + 1))
+        assert_parity(f.cpu().numpy(), ref[t], f"huber iterate {t + 1}")  # each iterate at the operators' bar
     fx = cfg.f.astype(np.float32)
     out = torch.zeros(1, dtype=torch.float64, device="cuda")
     G.neg_loglik_ex(cuda(fx), cuda(y), cuda(r), beta, ("huber", 0.05), out, ws)
@@ -97,15 +97,13 @@ def _subset_lists(cfg, rho_x, rho_y):
 
 
 @pytest.mark.parametrize("ci,er,algo", [(0, 0, None), (1, 0, None), (0, 1, None), (0, 0, "direct")])
-def test_subset_operators(ci, er, algo, monkeypatch):
+def test_subset_operators(ci, er, algo):
     """A_p f = (A f)|_p (zeros elsewhere) and A_p^T w = A^T (w 1_p), for ESAI
     handles (listed pairs only) and the restricted full operator of the
     energy-resolving / direct handles; subsets sum to the full operators."""
-    if algo:
-        monkeypatch.setenv("CACSI_ALGO", algo)
     cfg = make_config(ci, energy_resolving=er)
     O = oracle.Geometry(cfg)
-    G = P.Geometry(cfg.desc())
+    G = P.Geometry(cfg.desc(), options="direct=1" if algo == "direct" else None)
     rx, ry = (4, 8) if ci == 0 else (8, 16)
     sub, lists = _subset_lists(cfg, rx, ry)
     f = cfg.f

@@ -458,3 +458,96 @@ def test_effective_terms_config0():
     cfg = make_config(0)
     pairs, open_, terms = oracle.Geometry(cfg).count_terms()
     assert pairs == 64 * 256 and terms == open_ * 8
+
+
+# ---- round-2 pins: centres, objective, ratio guard, term counting, adjoint ----
+@pytest.mark.parametrize("ci,iy,iz,yz", [
+    # config 0 (BASELINE configs[0]): y in [-8, 8], z in [400, 416], 8 x 8 pixels of 2 mm
+    (0, 0, 0, (-7.0, 401.0)), (0, 7, 7, (7.0, 415.0)), (0, 3, 5, (-1.0, 411.0)),
+    # config 1: y in [-40, 40] (64 x 1.25 mm), z in [350, 550] (64 x 3.125 mm)
+    (1, 0, 0, (-39.375, 351.5625)), (1, 63, 63, (39.375, 548.4375)), (1, 32, 0, (0.625, 351.5625)),
+])
+def test_voxel_centres_hand_values(ci, iy, iz, yz):
+    """Reading R9 (pixel centres at min + (i + 1/2) pitch), pinned by hand values
+    of the configs' stated extents -- for oracle.c and the numpy restatement."""
+    G = oracle.Geometry(make_config(ci))
+    assert G.voxel_centre(iy, iz) == pytest.approx(yz, abs=1e-12)
+    yv, zv = G.voxel_centres()
+    assert (yv[iy], zv[iz]) == pytest.approx(yz, abs=1e-12)
+
+
+@pytest.mark.parametrize("ci,ix,jy,xy", [
+    # config 0: 16 x 16 pixels of 1.5 mm centred at x = +24 (near edge at x = 12 + 0.75), y = 0
+    (0, 0, 0, (12.75, -11.25)), (0, 15, 15, (35.25, 11.25)), (0, 8, 7, (24.75, -0.75)),
+    # config 1: 128 x 128 pixels of 0.8 mm, near x edge at 12 mm
+    (1, 0, 0, (12.4, -50.8)), (1, 127, 127, (114.0, 50.8)),
+])
+def test_detector_centres_hand_values(ci, ix, jy, xy):
+    G = oracle.Geometry(make_config(ci))
+    assert G.det_centre(ix, jy) == pytest.approx(xy, abs=1e-12)
+    xd, yd = G.det_centres()
+    assert (xd[ix], yd[jy]) == pytest.approx(xy, abs=1e-12)
+
+
+def test_neg_loglik_hand_values():
+    """L = sum_i (l_i + r_i) - y_i ln(l_i + r_i) (reading R15:
+    the constant sum ln y_i! dropped) at points computed by hand."""
+    assert recon.neg_loglik([1.0], [1.0], [0.0]) == pytest.approx(1.0, abs=1e-15)        # 1 - 1 ln 1
+    e = np.e
+    assert recon.neg_loglik([e - 1.0], [2.0], [1.0]) == pytest.approx(e - 2.0, rel=1e-15)  # z = e: e - 2
+    assert recon.neg_loglik([0.0], [0.0], [0.0]) == 0.0                                 # 0 ln 0 := 0
+    assert recon.neg_loglik([3.0], [0.0], [2.0]) == pytest.approx(5.0, rel=1e-15)         # y = 0: L = z
+    # r enters z: l = 1, r = 3, y = 4 -> 4 - 4 ln 4
+    assert recon.neg_loglik([1.0], [4.0], [3.0]) == pytest.approx(4.0 - 4.0 * np.log(4.0), rel=1e-14)
+    # a sum over pixels
+    assert recon.neg_loglik([1.0, 1.0, 0.5], [1.0, 0.0, 1.0], [0.0, 1.0, 0.5]) == pytest.approx(
+        1.0 + 2.0 + 1.0, rel=1e-15)
+    # J = L + beta R: two voxels (y neighbours) 1 and 3 in one q node -> R = psi(-2) + psi(2) = 4
+    f = np.array([1.0, 3.0]).reshape(2, 1, 1)
+    assert recon.penalty(f) == pytest.approx(4.0)
+    assert recon.objective([1.0], [1.0], [0.0], f, 0.25) == pytest.approx(1.0 + 0.25 * 4.0)
+
+
+def test_ratio_guard_branches():
+    """Reading R14: y / (l + r); 0 where y = z = 0; y / 1e-12 where z = 0 < y."""
+    out = recon.ratio([0.0, 0.0, 1.0, 2.0], [0.0, 5.0, 2.0, 0.0], [0.0, 0.0, 1.0, 0.0])
+    assert out[0] == 0.0
+    assert out[1] == pytest.approx(5e12, rel=1e-15)
+    assert out[2] == pytest.approx(1.0, rel=1e-15)
+    assert out[3] == 0.0
+
+
+@pytest.mark.parametrize("over", [dict(q_min=0.15, q_max=0.25, nq=9), dict(q_min=0.06, q_max=0.12, nq=5),
+                                  dict(q_min=0.0, q_max=0.9, nq=40)])
+def test_count_terms_out_of_range_energies(over):
+    """oracle_count_terms' in-range predicate (-1 < u_k < Q) against a count from
+    the dense matrix's own pair angles (oracle/dense.py: half-angle atan2, a
+    different formula) on geometries whose q grid cuts off part of the Bragg
+    reach (so some energies fall outside) and one that contains all of it."""
+    cfg = make_config(0)
+    d = cfg.desc()
+    d.update(over)
+    pairs, open_, terms = oracle.Geometry(d).count_terms()
+    pa = oracle.dense.pair_arrays(d)
+    E = np.asarray(d["energy_kev"], float)
+    dq = (d["q_max"] - d["q_min"]) / (d["nq"] - 1)
+    u = (E[None, None, :] * np.sin(0.5 * pa["theta"])[..., None] / oracle.HC - d["q_min"]) / dq
+    inr = (u > -1.0) & (u < d["nq"]) & (pa["T"][..., None] == 1.0)
+    assert pairs == pa["T"].size
+    assert open_ == int((pa["T"] == 1.0).sum())
+    assert terms == int(inr.sum())
+    if over["q_max"] < 0.5:
+        assert terms < open_ * d["ne"]  # the predicate actually cuts
+
+
+def test_adjoint_identity_config1_20_pairs():
+    """<A x, y> = <x, A^T y> to 1e-10 for 20 random pairs on config 1."""
+    cfg = make_config(1)
+    G = oracle.Geometry(cfg)
+    rng = seeded_rng(1, 6)
+    for _ in range(20):
+        x = rng.random(G.f_shape)
+        y = rng.random(G.g_shape) - 0.5  # signed y: no positivity to hide a sign error
+        lhs = np.vdot(G.forward(x), y)
+        rhs = np.vdot(x, G.backward(y))
+        assert abs(lhs - rhs) <= 1e-10 * np.sqrt(np.vdot(G.forward(x), G.forward(x)) * np.vdot(y, y))
