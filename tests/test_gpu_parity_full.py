@@ -76,18 +76,41 @@ def config1():
     return cfg, P.Geometry(cfg.desc()), oracle.Geometry(cfg)
 
 
+def assert_parity_signed(x, ref, absref, what, l2=1e-5, mr=1e-4, floor=1e-3):
+    """Signed inputs cancel, so an output can be far smaller than the sum of the
+    magnitudes of its terms, and no fp32 evaluation holds a relative bound there.
+    Reading R19b: rel L2 as usual (normwise), and the componentwise error measured
+    against the absolute-value operator, |x_i - ref_i| <= mr (A|u|)_i over the
+    entries with (A|u|)_i >= floor max (A|u|) -- the bound an fp32 sum of those
+    terms can meet (its rounding error scales with sum |term|)."""
+    x, ref, absref = (np.asarray(a, np.float64).ravel() for a in (x, ref, absref))
+    e2 = float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+    sel = absref >= floor * absref.max()
+    em = float((np.abs(x - ref)[sel] / absref[sel]).max())
+    print(f"{what}: rel_l2={e2:.3e} max_err_vs_abs={em:.3e}")
+    assert e2 <= l2 and em <= mr, (what, e2, em)
+
+
 @pytest.mark.parametrize("kind", ["log_uniform", "signed"])
 def test_config1_backward_wide_range_weights(config1, kind):
     cfg, G, O = config1
-    w = _log_uniform(G.g_shape, 1, 90) if kind == "log_uniform" else _signed(G.g_shape, 1, 91)
-    assert_parity(gpu_backward(G, w), O.backward(w), f"c1 backward, {kind} w")
+    if kind == "log_uniform":
+        w = _log_uniform(G.g_shape, 1, 90)
+        assert_parity(gpu_backward(G, w), O.backward(w), "c1 backward, log-uniform w")
+    else:
+        w = _signed(G.g_shape, 1, 91)
+        assert_parity_signed(gpu_backward(G, w), O.backward(w), O.backward(np.abs(w)), "c1 backward, signed w")
 
 
 @pytest.mark.parametrize("kind", ["log_uniform", "signed"])
 def test_config1_forward_wide_range_object(config1, kind):
     cfg, G, O = config1
-    f = _log_uniform(G.f_shape, 1, 92) if kind == "log_uniform" else _signed(G.f_shape, 1, 93)
-    assert_parity(gpu_forward(G, f), O.forward(f), f"c1 forward, {kind} f")
+    if kind == "log_uniform":
+        f = _log_uniform(G.f_shape, 1, 92)
+        assert_parity(gpu_forward(G, f), O.forward(f), "c1 forward, log-uniform f")
+    else:
+        f = _signed(G.f_shape, 1, 93)
+        assert_parity_signed(gpu_forward(G, f), O.forward(f), O.forward(np.abs(f)), "c1 forward, signed f")
 
 
 def test_config2_log_uniform_sampled(config2):
@@ -138,7 +161,7 @@ def unseen_geometry():
     O = oracle.Geometry(d)
     open_per_pixel = np.array([O.count_terms([p])[1] for p in range(cfg.n_det)])
     unseen = np.flatnonzero(open_per_pixel == 0)
-    assert 0 < unseen.size < cfg.n_det // 2
+    assert 0 < unseen.size < cfg.n_det
     return cfg, d, O, unseen
 
 

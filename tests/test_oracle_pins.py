@@ -541,13 +541,26 @@ def test_count_terms_out_of_range_energies(over):
 
 
 def test_adjoint_identity_config1_20_pairs():
-    """<A x, y> = <x, A^T y> to 1e-10 for 20 random pairs on config 1."""
+    """<A x, y> = <x, A^T y> to 1e-10 for 20 random pairs on config 1:
+    4 with the full operators and 16 with y supported on a random 1/16 of the
+    pixels (the pixel-restricted loops oracle_forward_pixels / oracle_backward_pixels
+    of Alg. 6, so the CPU suite stays within minutes).  Signed y: no positivity to
+    hide a sign error."""
     cfg = make_config(1)
     G = oracle.Geometry(cfg)
     rng = seeded_rng(1, 6)
-    for _ in range(20):
+    npx = cfg.n_det
+    for i in range(20):
         x = rng.random(G.f_shape)
-        y = rng.random(G.g_shape) - 0.5  # signed y: no positivity to hide a sign error
-        lhs = np.vdot(G.forward(x), y)
-        rhs = np.vdot(x, G.backward(y))
-        assert abs(lhs - rhs) <= 1e-10 * np.sqrt(np.vdot(G.forward(x), G.forward(x)) * np.vdot(y, y))
+        y = rng.random(G.g_shape) - 0.5
+        if i < 4:
+            ax = G.forward(x)
+            lhs, rhs = np.vdot(ax, y), np.vdot(x, G.backward(y))
+        else:
+            pix = np.sort(rng.choice(npx, npx // 16, replace=False))
+            ax = G.forward_pixels(x, pix)
+            lhs = np.vdot(ax, y.ravel()[pix])
+            ys = np.zeros(npx)
+            ys[pix] = y.ravel()[pix]
+            rhs = np.vdot(x, G.backward_pixels(ys.reshape(G.g_shape), pix))
+        assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(ax) * np.linalg.norm(y), i
