@@ -87,7 +87,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -106,6 +106,7 @@ const OptKey kOptKeys[] = {
     {"pc_plain", &cacsi::Opts::pc_plain, true, 0, 1},
     {"pc_segwin", &cacsi::Opts::pc_segwin, true, 0, 1},
     {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
+    {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
     {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
     {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},
@@ -366,6 +367,15 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
             free(g);
             return CACSI_ERR_INVALID;
         }
+        if (e != cudaSuccess) {
+            free_all(g);
+            free(g);
+            cudaGetLastError();
+            return map_err(e);
+        }
+    }
+    if (d->energy_resolving && !g->opt.direct && g->opt.er_cache) {
+        e = cacsi::er_build(g, d);
         if (e != cudaSuccess) {
             free_all(g);
             free(g);
@@ -888,6 +898,7 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
         return g->esai.enabled && g->esai.pc ? cacsi::pcv_row_blocks(g) : 0;
     if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
+    if (!strcmp(key, "er_cache_records")) return g->er.enabled ? g->er.n : 0;
     return -1;
 }
 

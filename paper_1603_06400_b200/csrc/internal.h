@@ -115,6 +115,27 @@ struct Esai {
     int stat_win_permille, stat_tile_permille;  // mean voxel window / 128-voxel tile K span, per mille of nb
 };
 
+// Energy-resolving pair cache (er_cache.cu): every open pair with an
+// in-range energy, per detector pixel q in increasing voxel order, as SoA records
+//   vw = v | klo << 16 | khi << 24   (voxel, first / last energy whose u_k can lie in (-1, nq))
+//   P  = the pair's geometric-spectral factor (transmission included), s = sin(theta/2)
+// plus per (voxel block of kErVB voxels, pixel) the record offset relative to off[q].
+constexpr int kErVB = 128;
+struct ErCache {
+    int enabled;
+    long long n;              // records
+    int nvb;                  // voxel blocks
+    int nr;                   // energy rounds of 16
+    int nlo;                  // lower table pad (entries below q node 0)
+    int nt;                   // forward table entries per voxel (nlo + nq + 1, even)
+    float cmax;               // max_k c_k
+    const long long *off;     // [n_det + 1]
+    const uint32_t *vw;
+    const float *P, *s;
+    const uint32_t *boff;     // [nvb + 1][n_det], relative to off[q]
+    const float *sv;          // per voxel fixed-point scale factor of the backward (times 1 / max|w|)
+};
+
 // Kernel-variant options of a handle (cacsi_geometry_create_ex "key=value,..." and
 // cacsi_set_option).  The defaults are the measured-best settings;
 // every other value selects a kernel that computes the same operator (an A/B
@@ -128,6 +149,7 @@ struct Opts {
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
+    int er_cache = 1;         // "er_cache": 0 = energy-resolving operators without the pair cache
     // per call (cacsi_set_option may change them between calls)
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
@@ -158,6 +180,9 @@ struct cacsi_geometry {
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
         *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen;
+    // energy-resolving pair cache (er_cache.cu)
+    cacsi::ErCache er;
+    void *d_er_off, *d_er_vw, *d_er_P, *d_er_s, *d_er_boff, *d_er_sv;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs
@@ -249,6 +274,9 @@ cudaError_t esai_forward_ratio(const cacsi_geometry *g, const float *f, const Fw
                                cudaStream_t s, int *launches);
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
+cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
+cudaError_t er_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
+cudaError_t er_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 int pcv_row_blocks(const cacsi_geometry *g);
 void osem_graph_free(cacsi_geometry *g);
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);

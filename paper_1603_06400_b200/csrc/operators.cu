@@ -333,6 +333,7 @@ int num_sms(int device) {
 
 cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches) {
     if (g->esai.enabled) return esai_forward(g, f, out, s, launches);
+    if (g->er.enabled) return er_forward(g, f, out, s, launches);
     const Params &p = g->p;
     const bool res = p.energy_resolving != 0;
     const int tiles = (p.n_det + FWD_T - 1) / FWD_T;
@@ -388,6 +389,7 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
 
 cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
     if (g->esai.enabled) return esai_backward(g, w, b, s, launches);
+    if (g->er.enabled) return er_backward(g, w, b, s, launches);
     const Params &p = g->p;
     const size_t smem =
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);

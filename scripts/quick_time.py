@@ -28,11 +28,16 @@ def main():
     ap.add_argument("--configs", default="1,2")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kernels", action="store_true", help="also print per-kernel averages (forward and backward)")
+    ap.add_argument("--options", default=None, help="kernel-variant options (cacsi_geometry_create_ex)")
     args = ap.parse_args()
     out = {}
     for ci in [int(c) for c in args.configs.split(",")]:
         cfg = make_config(ci)
-        G = P.Geometry(cfg.desc())
+        import time
+        t0 = time.perf_counter()
+        G = P.Geometry(cfg.desc(), options=args.options)
+        torch.cuda.synchronize()
+        setup_ms = (time.perf_counter() - t0) * 1e3
         f = torch.as_tensor(cfg.f).cuda()
         g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
         w = torch.rand(G.g_shape, dtype=torch.float32, device="cuda")
@@ -49,10 +54,12 @@ def main():
             G.set_timing(False)
             print(json.dumps({k: round(v[0] / max(v[1], 1), 4) for k, v in G.kernel_times().items()}), flush=True)
         pairs = cfg.n_vox * cfg.n_det
-        out[ci] = dict(fwd_ms=tf[len(tf) // 2], bwd_ms=tb[len(tb) // 2], pairs=pairs,
+        out[ci] = dict(fwd_ms=tf[len(tf) // 2], bwd_ms=tb[len(tb) // 2], pairs=pairs, setup_ms=setup_ms,
+                       options=args.options,
                        fwd_pairs_per_s=pairs / tf[len(tf) // 2] * 1e3, bwd_pairs_per_s=pairs / tb[len(tb) // 2] * 1e3,
                        **{k: G.query(k) for k in ("esai_breakpoints", "esai_max_window", "esai_lut_cells",
-                                                  "esai_lut_slow_cells", "ts_rho", "pair_cache_records")})
+                                                  "esai_lut_slow_cells", "ts_rho", "pair_cache_records",
+                                                  "er_cache_records")})
         print(json.dumps({ci: out[ci]}), flush=True)
         G.close()
 
