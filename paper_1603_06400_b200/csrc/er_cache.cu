@@ -41,9 +41,6 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int ER_VC = 32;     // voxels per forward table chunk (= one 32-record batch per pixel)
-constexpr int ER_NBUF = 3;    // forward table ring depth
-constexpr int ER_FW = 16;     // forward warps per CTA
-constexpr int ER_PW = 6;      // forward pixels per warp
 constexpr int ER_FL = 4;      // forward chunks between fp64 flushes
 constexpr int ER_BT = 512;    // backward threads
 constexpr int ER_SPLIT = 4;   // backward detector splits (integer partials)
@@ -170,146 +167,136 @@ __global__ void k_er_tab(const Params p, int nlo, int nt, const float *__restric
     }
 }
 
+// One CTA per item (a block of <= 32 PG consecutive pixels), NR x PG warps: warp (pg, r)
+// owns pixels 32 pg + lane and the energies k = 16 r + j (j < 16) -- 16 fp32 sums in
+// REGISTERS -- and walks the voxels in chunks of ER_VC with the whole CTA:
+//   fill:    the chunk's records of every pixel of the item (one 32-record batch per
+//            pixel) are scattered into a dense shared tile pt[voxel][pixel] = (P, sigma),
+//            closed pairs written as (0, 0);
+//   compute: per voxel, skip the round if no lane's energies reach the q grid (exact
+//            test, the u' bounds of the round's first / last energy), else 16
+//            independent terms per lane -- FFMA, clamp, round, one 8-byte table read
+//            (adjacent pixels of one voxel read nearby entries: few bank wavefronts),
+//            two FFMA.
+// The hat tables of the chunk are landed by cp.async.bulk one chunk ahead (2 buffers;
+// the CTA barrier that ends a chunk releases its buffer).  Every ER_FL chunks the fp32
+// register sums are added into fp64 sums in shared memory; the item's outputs are
+// written coalesced from there (c_k applied once).
 template <int NR>
-__global__ void __launch_bounds__(ER_FW * 32, 1) k_er_fwd(const Params p, const ErCache c, const float2 *__restrict__ tab,
-                                                          int gsize, int n_groups, float *__restrict__ out) {
+__global__ void __launch_bounds__(896, 1) k_er_fwd(const Params p, const ErCache c, const float2 *__restrict__ tab,
+                                                   int isize, int n_items, float *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char sm[];
-    const int NT = c.nt;
-    const int tabw = ER_VC * NT;  // float2 per buffer
-    float2 *tabs = (float2 *)sm;
-    double *acc64 = (double *)(tabs + ER_NBUF * tabw);                     // [warps][ER_PW][NR * 16]
-    uint64_t *full = (uint64_t *)(acc64 + ER_FW * ER_PW * NR * 16);
-    uint64_t *empty = full + ER_NBUF;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = lane >> 4, li = lane & 15;
+    const int NT = c.nt, tabw = ER_VC * NT;
+    const int nwarps = blockDim.x >> 5, PG = nwarps / NR, NPX = 32 * PG;
+    float2 *tabs = (float2 *)sm;                                   // [2][ER_VC * NT]
+    double *acc64 = (double *)(tabs + 2 * tabw);                   // [NPX][NR * 16]
+    float2 *pt = (float2 *)(acc64 + (size_t)NPX * NR * 16);        // [ER_VC][NPX]
+    int *cur = (int *)(pt + ER_VC * NPX);                          // [NPX]
+    uint64_t *full = (uint64_t *)(((uintptr_t)(cur + NPX) + 7) & ~(uintptr_t)7);  // [2]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int pg = warp / NR, r = warp % NR;
     const int nch = (p.n_vox + ER_VC - 1) / ER_VC;
-    const int my_groups = blockIdx.x < n_groups ? (n_groups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const long long total = (long long)my_groups * nch;  // chunks this CTA consumes
+    const int my_items = (int)blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const long long total = (long long)my_items * nch;
     if (tid == 0) {
-        for (int i = 0; i < ER_NBUF; i++) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(empty + i)), "r"(ER_FW));
-        }
+        for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
-    double *myacc = acc64 + (size_t)warp * ER_PW * NR * 16;
-    for (int i = lane; i < ER_PW * NR * 16; i += 32) myacc[i] = 0.0;
-    __syncthreads();
-    // producer (thread 0): chunk gc of the CTA's sequence -> buffer gc % ER_NBUF
-    auto issue = [&](long long gc) {
+    auto issue = [&](long long gc) {  // chunk gc of this CTA's sequence -> buffer gc & 1
         const int ch = (int)(gc % nch);
         const int v0 = ch * ER_VC, nv = min(ER_VC, p.n_vox - v0);
         const uint32_t bytes = (uint32_t)nv * NT * 8u;
-        const int b = (int)(gc % ER_NBUF);
-        const uint32_t mb = smem_u32(full + b);
+        const uint32_t mb = smem_u32(full + (gc & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                         smem_u32(tabs + (size_t)b * tabw)),
+                         smem_u32(tabs + (size_t)(gc & 1) * tabw)),
                      "l"(tab + (size_t)v0 * NT), "r"(bytes), "r"(mb)
                      : "memory");
     };
-    if (tid == 0)
-        for (long long gc = 0; gc < min((long long)ER_NBUF, total); gc++) issue(gc);
-    float al[NR];
-    er_alphas<NR>(p, li, al);
+    // this warp's energies: alpha of k = 16 r + j (padding energies: 1e30, their u clamps
+    // onto the table's zero top entry)
+    float al[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const int k = 16 * r + j;
+        al[j] = k < p.ne ? __ldg(&p.energy[k].x) : 1e30f;
+    }
+    const float a_lo = al[0], a_hi = __ldg(&p.energy[min(p.ne - 1, 16 * r + 15)].x);
     const float nb = p.nb, qm = p.qm;
+    const int px = pg * 32 + lane;  // this thread's pixel within the item
+    double *my64 = acc64 + (size_t)px * NR * 16 + 16 * r;
+    __syncthreads();
+    if (tid == 0 && total > 0) issue(0);
     long long gc = 0;
-    for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
-        // this warp's pixels: q0 + s, s < npx
-        const int q0 = g * gsize + warp * ER_PW;
-        const int npx = max(0, min(ER_PW, min(p.n_det, (g + 1) * gsize) - q0));
-        int cur[ER_PW];
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int P0 = it * isize, npx = min(isize, p.n_det - P0);
+        __syncthreads();  // the previous item's output pass (reads every thread's fp64 sums) is done
+        for (int i = tid; i < NPX; i += blockDim.x) cur[i] = 0;
 #pragma unroll
-        for (int s = 0; s < ER_PW; s++) cur[s] = 0;
-        float acc[ER_PW][NR];
+        for (int j = 0; j < 16; j++) my64[j] = 0.0;
+        float acc[16];
 #pragma unroll
-        for (int s = 0; s < ER_PW; s++)
-#pragma unroll
-            for (int r = 0; r < NR; r++) acc[s][r] = 0.0f;
-        // this chunk's records of pixel slot s: at most ER_VC = 32, so one 32-record batch
-        // (records in voxel order: the chunk's are a prefix of the batch)
-        auto load = [&](int s, uint32_t &rv, float &rP, float &rs) {
-            rv = 0xFFFFFFFFu, rP = 0.0f, rs = 0.0f;
-            if (s < npx) {
-                const long long b0 = __ldg(c.off + q0 + s), b1 = __ldg(c.off + q0 + s + 1);
-                const long long idx = b0 + cur[s] + lane;
-                if (idx < b1) rv = __ldg(c.vw + idx), rP = __ldg(c.P + idx), rs = __ldg(c.s + idx);
-            }
-        };
+        for (int j = 0; j < 16; j++) acc[j] = 0.0f;
         for (int ch = 0; ch < nch; ch++, gc++) {
-            const int buf = (int)(gc % ER_NBUF);
             const int v0 = ch * ER_VC, v_end = v0 + ER_VC;
-            uint32_t rv;
-            float rP, rs;
-            load(0, rv, rP, rs);  // issued before the table wait: its latency overlaps it
-            mbar_wait(smem_u32(full + buf), (uint32_t)((gc / ER_NBUF) & 1));
-            const uint32_t tb0 = smem_u32(tabs + (size_t)buf * tabw);
+            __syncthreads();  // the previous chunk's tile reads and this item's cursor resets are done
+            if (tid == 0 && gc + 1 < total) issue(gc + 1);  // its buffer's last reader was chunk gc - 1
+            // fill: warp w takes pixels w, w + nwarps, ...; lanes = the pixel's next 32 records
+            for (int q = warp; q < NPX; q += nwarps) {
+                uint32_t vw = 0xFFFFFFFFu;
+                float P = 0.0f, sg = 0.0f;
+                int n = 0;
+                if (q < npx) {
+                    const long long b0 = __ldg(c.off + P0 + q), b1 = __ldg(c.off + P0 + q + 1);
+                    const long long idx = b0 + cur[q] + lane;
+                    if (idx < b1) {
+                        vw = __ldg(c.vw + idx);
+                        if ((int)(vw & 0xFFFFu) < v_end) P = __ldg(c.P + idx), sg = __ldg(c.s + idx);
+                    }
+                }
+                const bool rec = vw != 0xFFFFFFFFu && (int)(vw & 0xFFFFu) < v_end;
+                n = __popc(__ballot_sync(FULL, rec));  // voxel order: the chunk's records are a prefix
+                const unsigned have = __reduce_or_sync(FULL, rec ? 1u << ((vw & 0xFFFFu) - v0) : 0u);
+                if (rec) pt[((vw & 0xFFFFu) - v0) * NPX + q] = make_float2(P, sg);
+                if (!((have >> lane) & 1u)) pt[lane * NPX + q] = make_float2(0.0f, 0.0f);
+                if (lane == 0) cur[q] += n;
+            }
+            __syncthreads();
+            mbar_wait(smem_u32(full + (gc & 1)), (uint32_t)((gc >> 1) & 1));
+            const uint32_t tb0 = smem_u32(tabs + (size_t)(gc & 1) * tabw) + (uint32_t)c.nlo * 8u -
+                                 (uint32_t)kMagicBits * 8u;
+            const int nv = min(ER_VC, p.n_vox - v0);
+            for (int vl = 0; vl < nv; vl++) {
+                const float2 ps = pt[vl * NPX + px];
+                // exact skip test: u' of the round's first / last energy against (-3/2, qm)
+                const bool act = ps.x > 0.0f && fmaf(a_hi, ps.y, nb) > -1.5f && fmaf(a_lo, ps.y, nb) < qm;
+                if (!__any_sync(FULL, act)) continue;
+                const uint32_t tb = tb0 + (uint32_t)(vl * NT) * 8u;
+                const float P = act ? ps.x : 0.0f;
 #pragma unroll
-            for (int s = 0; s < ER_PW; s++) {
-                const unsigned m = __ballot_sync(FULL, rv != 0xFFFFFFFFu && (int)(rv & 0xFFFFu) < v_end);
-                const int n = __popc(m);
-                cur[s] += n;
-                const uint32_t cv = rv;
-                const float cP = rP, cs = rs;
-                if (s + 1 < ER_PW) load(s + 1, rv, rP, rs);  // next slot's batch in flight
-                for (int t = 0; t < n; t += 2) {
-                    const int src = t + half;
-                    const uint32_t w = __shfl_sync(FULL, cv, src & 31);
-                    float P = __shfl_sync(FULL, cP, src & 31);
-                    const float sg = __shfl_sync(FULL, cs, src & 31);
-                    const bool act = src < n;
-                    if (!act) P = 0.0f;
-                    int rlo = act ? (int)((w >> 16) & 0xFFu) >> 4 : 1 << 20;
-                    int rhi = act ? (int)(w >> 24) >> 4 : -1;
-                    rlo = min(rlo, __shfl_xor_sync(FULL, rlo, 16));
-                    rhi = max(rhi, __shfl_xor_sync(FULL, rhi, 16));
-                    // byte address of table entry n = round(u') of voxel (w & 0xFFFF), folded with
-                    // the magic constant's bits: addr = base + 8 * bits(u' + 1.5 * 2^23)
-                    const int vl = act ? (int)(w & 0xFFFFu) - v0 : 0;
-                    const uint32_t tb = tb0 + (uint32_t)(vl * NT + c.nlo) * 8u - (uint32_t)kMagicBits * 8u;
-#pragma unroll
-                    for (int r = 0; r < NR; r++)
-                        if (r >= rlo && r <= rhi) {
-                            const float u = fminf(fmaf(al[r], sg, nb), qm);
-                            const float vm = u + kMagic;
-                            const float tt = u - (vm - kMagic);
-                            const float2 e = lds_f2(tb + (uint32_t)__float_as_int(vm) * 8u);
-                            acc[s][r] = fmaf(P, fmaf(tt, e.y, e.x), acc[s][r]);
-                        }
+                for (int j = 0; j < 16; j++) {
+                    const float u = fminf(fmaf(al[j], ps.y, nb), qm);
+                    const float vm = u + kMagic;
+                    const float tt = u - (vm - kMagic);
+                    const float2 e = lds_f2(tb + (uint32_t)__float_as_int(vm) * 8u);
+                    acc[j] = fmaf(P, fmaf(tt, e.y, e.x), acc[j]);
                 }
             }
-            // release the buffer: one arrival per warp after all its reads
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(empty + buf)) : "memory");
-            if (tid == 0 && gc + ER_NBUF < total) {
-                mbar_wait(smem_u32(empty + buf), (uint32_t)((gc / ER_NBUF) & 1));
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                issue(gc + ER_NBUF);
-            }
-            // fp64 flush of the fp32 sums (both halves' sums of the same pixel and energy
-            // added first), every ER_FL chunks and at the end
             if ((ch + 1) % ER_FL == 0 || ch + 1 == nch) {
 #pragma unroll
-                for (int s = 0; s < ER_PW; s++)
-#pragma unroll
-                    for (int r = 0; r < NR; r++) {
-                        const float o = __shfl_xor_sync(FULL, acc[s][r], 16);
-                        if (half == 0) myacc[(s * NR + r) * 16 + li] += (double)(acc[s][r] + o);
-                        acc[s][r] = 0.0f;
-                    }
+                for (int j = 0; j < 16; j++) {
+                    my64[j] += (double)acc[j];
+                    acc[j] = 0.0f;
+                }
             }
         }
-        // g[q][k] = c_k sum (c_k applied once per output)
-        __syncwarp();
-        for (int s = 0; s < npx; s++) {
-            float *o = out + (size_t)(q0 + s) * p.ne;
-            for (int k = lane; k < p.ne; k += 32) {
-                const int r = k >> 4, i = k & 15;
-                o[k] = (float)((double)__ldg(&p.energy[k].y) * myacc[(s * NR + r) * 16 + i]);
-            }
+        __syncthreads();
+        // g[q][k] = c_k sum, coalesced over the item's [npx][ne] block
+        for (int i = tid; i < npx * p.ne; i += blockDim.x) {
+            const int q = i / p.ne, k = i - q * p.ne;
+            out[(size_t)P0 * p.ne + i] = (float)((double)__ldg(&p.energy[k].y) * acc64[(size_t)q * NR * 16 + k]);
         }
-        __syncwarp();
-        for (int i = lane; i < ER_PW * NR * 16; i += 32) myacc[i] = 0.0;
-        __syncwarp();
     }
 }
 
@@ -331,6 +318,17 @@ __global__ void __launch_bounds__(1024) k_er_absmax(const Params p, const long l
     }
 }
 
+__device__ __forceinline__ void red_s32(uint32_t addr, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// Items (block of kErVB voxels, quarter of the detector); one warp per pixel of the
+// quarter, lanes = energies: lane i of half h owns k = 16 r + i and holds w[q, k] c_k in
+// registers.  The pixel's records in the voxel block go through a per-warp stage, 32 at a
+// time; for each round r in the union of the batch's energy windows (one uniform branch
+// per batch and round) the two halves sweep the staged pairs two by two (two pairs per
+// half per step: independent chains), each term depositing exactly-rounded fixed-point
+// integers into the voxel's histogram row with red.shared.add (no return value).
 // ONES: w = 1 everywhere and scale = sv (the create-time bound measurement);
 // else scale = sv / max|w|
 template <int NR, bool ONES>
@@ -338,11 +336,13 @@ __global__ void __launch_bounds__(ER_BT) k_er_bwd(const Params p, const ErCache 
                                                   const float *__restrict__ wmax, const float *__restrict__ sv,
                                                   int *__restrict__ part) {
     extern __shared__ __align__(16) unsigned char sm[];
-    const int HB = p.nq + 4;                        // rows -2 .. nq + 1 (pads)
-    int *hist = (int *)sm;                          // [kErVB][HB]
-    float *scl = (float *)(hist + kErVB * HB);      // [kErVB]
+    const int HB = p.nq + 4;                             // rows -2 .. nq + 1 (pads)
+    float4 *stage_all = (float4 *)sm;                    // [warps][36]
+    int *hist = (int *)(stage_all + (ER_BT / 32) * 36);  // [kErVB][HB]
+    float *scl = (float *)(hist + kErVB * HB);           // [kErVB]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = lane >> 4, li = lane & 15;
     const int nwarps = ER_BT / 32;
+    float4 *stage = stage_all + warp * 36;
     const float wm = ONES ? 1.0f : *wmax;
     float al[NR], ck[NR];
     er_alphas<NR>(p, li, al);
@@ -353,6 +353,8 @@ __global__ void __launch_bounds__(ER_BT) k_er_bwd(const Params p, const ErCache 
     }
     const float nbb = p.nb + 0.5f;  // -q_min / dq: u = alpha sigma + nbb
     const float qf = (float)p.nq;
+    const uint32_t hbase = smem_u32(hist) + 8u - (uint32_t)kMagicBits * 4u;  // row offset + j0 bits folded in
+    if (lane < 4) stage[32 + lane] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);    // pads: Ps = 0
     const int n_items = c.nvb * ER_SPLIT;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int vb = it / ER_SPLIT, sp = it % ER_SPLIT;
@@ -378,36 +380,44 @@ __global__ void __launch_bounds__(ER_BT) k_er_bwd(const Params p, const ErCache 
             }
             for (int a = a0; a < a1; a += 32) {
                 const int n = min(32, a1 - a);
-                const bool in = lane < n;
-                const uint32_t rv = in ? __ldg(c.vw + b0 + a + lane) : 0u;
-                const float rP = in ? __ldg(c.P + b0 + a + lane) : 0.0f;
-                const float rs = in ? __ldg(c.s + b0 + a + lane) : 0.0f;
-                for (int t = 0; t < n; t += 2) {
-                    const int src = t + half;
-                    const uint32_t wv = __shfl_sync(FULL, rv, src & 31);
-                    const float P = __shfl_sync(FULL, rP, src & 31);
-                    const float sg = __shfl_sync(FULL, rs, src & 31);
-                    const bool act = src < n;
-                    const int vl = act ? (int)(wv & 0xFFFFu) - V0 : 0;
-                    const float Ps = act ? P * scl[vl] : 0.0f;
-                    int rlo = act ? (int)((wv >> 16) & 0xFFu) >> 4 : 1 << 20;
-                    int rhi = act ? (int)(wv >> 24) >> 4 : -1;
-                    rlo = min(rlo, __shfl_xor_sync(FULL, rlo, 16));
-                    rhi = max(rhi, __shfl_xor_sync(FULL, rhi, 16));
-                    int *hrow = hist + vl * HB + 2;
+                int rlo = 1 << 20, rhi = -1;
+                {
+                    float4 st = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if (lane < n) {
+                        const uint32_t rv = __ldg(c.vw + b0 + a + lane);
+                        const int vl = (int)(rv & 0xFFFFu) - V0;
+                        // (row byte offset, sigma, P scale)
+                        st = make_float4(__int_as_float(vl * HB * 4), __ldg(c.s + b0 + a + lane),
+                                         __ldg(c.P + b0 + a + lane) * scl[vl], 0.0f);
+                        rlo = (int)((rv >> 16) & 0xFFu) >> 4;
+                        rhi = (int)(rv >> 24) >> 4;
+                    }
+                    __syncwarp();
+                    stage[lane] = st;
+                    rlo = __reduce_min_sync(FULL, rlo);
+                    rhi = __reduce_max_sync(FULL, rhi);
+                    __syncwarp();
+                }
 #pragma unroll
-                    for (int r = 0; r < NR; r++)
-                        if (r >= rlo && r <= rhi) {
-                            const float u = fminf(fmaxf(fmaf(al[r], sg, nbb), -1.0f), qf);
+                for (int r = 0; r < NR; r++) {
+                    if (r < rlo || r > rhi) continue;
+                    const float a_r = al[r], w_r = wc[r];
+                    for (int t = 0; t < n; t += 4) {
+                        const float4 d0 = stage[t + half], d1 = stage[t + 2 + half];
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const float4 d = h ? d1 : d0;
+                            const float u = fminf(fmaxf(fmaf(a_r, d.y, nbb), -1.0f), qf);
                             const float vm = (u - 0.5f) + kMagic;  // round(u - 1/2) = floor(u) up to ties
-                            const int j0 = __float_as_int(vm) - kMagicBits;
                             const float t1 = u - (vm - kMagic);    // in [0, 1]
-                            const float av = wc[r] * Ps;           // |av| <= 2^21 (scale rule)
+                            const float av = w_r * d.z;            // |av| <= 2^21 (scale rule)
                             const int xa = __float_as_int(av + kMagic);
                             const int x1 = __float_as_int(fmaf(av, t1, kMagic));
-                            atomicAdd(hrow + j0, xa - x1);
-                            atomicAdd(hrow + j0 + 1, x1 - kMagicBits);
+                            const uint32_t ad = hbase + (uint32_t)__float_as_int(d.x) + (uint32_t)__float_as_int(vm) * 4u;
+                            red_s32(ad, xa - x1);
+                            red_s32(ad + 4u, x1 - kMagicBits);
                         }
+                    }
                 }
             }
         }
@@ -453,18 +463,27 @@ int sms(int dev) {
     return n;
 }
 
+size_t er_bwd_smem(const Params &p) { return (size_t)(ER_BT / 32) * 36 * 16 + (size_t)kErVB * (p.nq + 4) * 4 + kErVB * 4; }
+int er_fwd_pg(int nr) { return std::max(1, std::min(8, 28 / nr)); }
+size_t er_fwd_smem(const ErCache &c, int nr) {
+    const int npx = 32 * er_fwd_pg(nr);
+    return (size_t)2 * ER_VC * c.nt * 8 + (size_t)npx * nr * 16 * 8 + (size_t)ER_VC * npx * 8 + npx * 4 + 64;
+}
+
 template <int NR>
 cudaError_t er_fwd_launch(const cacsi_geometry *g, const float2 *tab, float *out, cudaStream_t s) {
     const Params &p = g->p;
     const ErCache &c = g->er;
-    const size_t smem = (size_t)ER_NBUF * ER_VC * c.nt * 8 + (size_t)ER_FW * ER_PW * NR * 16 * 8 + 2 * ER_NBUF * 8;
+    const int PG = er_fwd_pg(NR), threads = 32 * PG * NR;
+    const size_t smem = er_fwd_smem(c, NR);
     const int nsm = sms(g->device);
-    int ng = (p.n_det + ER_FW * ER_PW - 1) / (ER_FW * ER_PW);
-    ng = (ng + nsm - 1) / nsm * nsm;                      // a whole number of groups per SM
-    const int gsize = (p.n_det + ng - 1) / ng;            // <= ER_FW * ER_PW
-    ng = (p.n_det + gsize - 1) / gsize;
+    // items: a whole number per SM (the persistent CTAs finish together), <= 32 PG pixels each
+    int ni = (p.n_det + 32 * PG - 1) / (32 * PG);
+    ni = (ni + nsm - 1) / nsm * nsm;
+    const int isize = (p.n_det + ni - 1) / ni;
+    ni = (p.n_det + isize - 1) / isize;
     cudaFuncSetAttribute(k_er_fwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_er_fwd<NR><<<std::min(ng, nsm), ER_FW * 32, smem, s>>>(p, c, tab, gsize, ng, out);
+    k_er_fwd<NR><<<std::min(ni, nsm), threads, smem, s>>>(p, c, tab, isize, ni, out);
     return cudaGetLastError();
 }
 
@@ -472,7 +491,7 @@ template <int NR, bool ONES>
 cudaError_t er_bwd_launch(const cacsi_geometry *g, const float *w, const float *wmax, const float *sv, int *part,
                           cudaStream_t s) {
     const Params &p = g->p;
-    const size_t smem = (size_t)kErVB * (p.nq + 4) * 4 + kErVB * 4;
+    const size_t smem = er_bwd_smem(p);
     auto kb = k_er_bwd<NR, ONES>;
     cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
@@ -525,8 +544,8 @@ cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     E.cmax = 0.0f;
     for (int k = 0; k < p.ne; k++) E.cmax = std::max(E.cmax, (float)(d->scale * d->phi[k] * d->energy_kev[k]));
     // forward shared memory (3 table buffers + fp64 sums) must fit
-    const size_t fsm = (size_t)ER_NBUF * ER_VC * E.nt * 8 + (size_t)ER_FW * ER_PW * E.nr * 16 * 8 + 64;
-    const size_t bsm = (size_t)kErVB * (p.nq + 4) * 4 + kErVB * 4;
+    const size_t fsm = er_fwd_smem(E, E.nr);
+    const size_t bsm = er_bwd_smem(p);
     if (fsm > 227 * 1024 || bsm > 227 * 1024) return cudaSuccess;
     const int nsm = sms(g->device);
     long long *cnt = nullptr;
