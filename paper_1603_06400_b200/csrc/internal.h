@@ -149,7 +149,7 @@ struct Opts {
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
-    int er_cache = 1;         // "er_cache": 0 = energy-resolving operators without the pair cache
+    int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     // per call (cacsi_set_option may change them between calls)
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split

@@ -1,7 +1,8 @@
 """Energy-resolving operators from the pair cache (er_cache.cu):
 lanes-as-energies forward with register sums, fixed-point integer-atomic backward.
-Held to the oracle bar and cross-checked against the direct per-term kernels
-(option er_cache=0), which share none of this code."""
+Option er_cache=1 (the default runs the direct per-term kernels, operators.cu,
+which measured as fast: DESIGN.md 4.3e).  Held to the oracle bar and
+cross-checked against the direct kernels, which share none of this code."""
 import numpy as np
 import pytest
 
@@ -38,8 +39,8 @@ def _desc(over):
 @pytest.mark.parametrize("over", SHAPES, ids=range(len(SHAPES)))
 def test_er_cache_vs_oracle_and_direct(over):
     d = _desc(over)
-    G = P.Geometry(d)
-    D = P.Geometry(d, options="er_cache=0")
+    G = P.Geometry(d, options="er_cache=1")
+    D = P.Geometry(d)
     O = oracle.Geometry(d)
     assert G.query("er_cache_records") > 0 and D.query("er_cache_records") == 0
     f, w = rnd(G.f_shape, 0, 110), rnd(G.g_shape, 0, 111)
@@ -57,7 +58,7 @@ def test_er_cache_records_are_open_pairs():
     """Every record is an open pair (at most the oracle's open-pair count; only pairs
     whose whole energy window misses the q grid are dropped)."""
     cfg = make_config(0, energy_resolving=1)
-    G = P.Geometry(cfg.desc())
+    G = P.Geometry(cfg.desc(), options="er_cache=1")
     pairs, open_, terms = oracle.Geometry(cfg).count_terms()
     assert 0 < G.query("er_cache_records") <= open_
     # config 0: every energy of every open pair is in range (test_effective_terms_config0)
@@ -68,10 +69,25 @@ def test_er_cache_deterministic_and_wide_range():
     cfg = make_config(0, energy_resolving=1)
     d = cfg.desc()
     d.update(ny=12, nz=10, det_nx=20, det_ny=24)
-    G, O = P.Geometry(d), oracle.Geometry(d)
+    G, O = P.Geometry(d, options="er_cache=1"), oracle.Geometry(d)
     f = rnd(G.f_shape, 0, 112)
     w = (10.0 ** seeded_rng(0, 113).uniform(-3, 3, G.g_shape)).astype(np.float32)
     g1, g2 = gpu_forward(G, f), gpu_forward(G, f)
     b1, b2 = gpu_backward(G, w), gpu_backward(G, w)
     assert np.array_equal(g1, g2) and np.array_equal(b1, b2)
     assert_parity(b1, O.backward(w), "er cache backward, log-uniform w")
+
+
+def test_er_cache_config4_sampled():
+    """Config 4 at full size through the pair-cache kernels (sampled outputs)."""
+    from test_gpu_parity import _sample
+    cfg = make_config(4)
+    G, O = P.Geometry(cfg.desc(), options="er_cache=1"), oracle.Geometry(cfg)
+    assert G.query("er_cache_records") > 0
+    g = gpu_forward(G, cfg.f).reshape(cfg.n_det, cfg.ne)
+    pix = _sample(cfg.n_det, 2048, 43)
+    assert_parity(g[pix], O.forward_pixels(cfg.f, pix), "c4 er-cache forward, 2048 pixels")
+    w = rnd(G.g_shape, 4, 10)
+    b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
+    vox = _sample(cfg.n_vox, 64, 44)
+    assert_parity(b[vox], O.backward_voxels(w, vox), "c4 er-cache backward, 64 voxels")
