@@ -1217,11 +1217,11 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                 if (e == cudaSuccess) {
                     const int gr2 = 8 * sm_count(g->device);
                     if (jyb == 2)
-                        k_pc_perm<uint16_t><<<gr2, 256>>>(p, E, segR, 128, (const uint32_t *)g->d_pc_bt,
+                        k_pc_perm<uint16_t><<<gr2, PERM_W * 32>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
                                                           (const float *)g->d_pc_P, (const uint16_t *)g->d_pc_q,
                                                           (uint32_t *)arr[0], (float *)arr[1], (uint16_t *)arr[2]);
                     else
-                        k_pc_perm<uint32_t><<<gr2, 256>>>(p, E, segR, 128, (const uint32_t *)g->d_pc_bt,
+                        k_pc_perm<uint32_t><<<gr2, PERM_W * 32>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
                                                           (const float *)g->d_pc_P, (const uint32_t *)g->d_pc_q,
                                                           (uint32_t *)arr[0], (float *)arr[1], (uint32_t *)arr[2]);
                     e = cudaDeviceSynchronize();
