@@ -4,6 +4,7 @@
 // (PAPER.md:236-241): per-voxel G_so, r^ and mask-plane parameters, per-pixel
 // centres, per-energy constants and the bit-packed mask are computed ONCE in
 // fp64 and uploaded; everything per pair is computed online by the kernels.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -184,6 +185,7 @@ cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *d, int device, cac
 
 cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, const char *options,
                                       cacsi_geometry **out) {
+    const auto t_start = std::chrono::steady_clock::now();
     if (!d || !out) return CACSI_ERR_NULL;
     *out = nullptr;
     cacsi_status st = validate(d);
@@ -374,6 +376,9 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
             return map_err(e);
         }
     }
+    g->setup_us[6] = std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t_start)
+                         .count();
+    for (int i = 0; i < 6; i++) g->setup_us[6] -= g->setup_us[i];  // host tables, uploads, validation
     if (d->energy_resolving && !g->opt.direct && g->opt.er_cache) {
         e = cacsi::er_build(g, d);
         if (e != cudaSuccess) {
@@ -383,6 +388,8 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
             return map_err(e);
         }
     }
+    g->setup_us[7] = std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t_start)
+                         .count();
     *out = g;
     return CACSI_OK;
 }
@@ -899,6 +906,10 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
     if (!strcmp(key, "er_cache_records")) return g->er.enabled ? g->er.n : 0;
+    static const char *stages[8] = {"setup_us_tables", "setup_us_bitmaps", "setup_us_bound", "setup_us_pc_fill",
+                                    "setup_us_pc_perm", "setup_us_pc_segwin", "setup_us_host", "setup_us_total"};
+    for (int i = 0; i < 8; i++)
+        if (!strcmp(key, stages[i])) return g->setup_us[i];
     return -1;
 }
 

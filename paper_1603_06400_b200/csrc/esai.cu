@@ -19,6 +19,7 @@
 // The per-term energy loop disappears from the pair loop; the q contraction
 // becomes a dense GEMM.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -856,8 +857,20 @@ static int persistent_grid(const cacsi_geometry *g, size_t smem, int threads) {
 
 // Build the ESAI tables (energy-integrating handles).  Host fp64 arithmetic
 // for the breakpoints and S~; DESIGN.md "ESAI tables".
+// setup stage clock: stage i's wall time since the previous mark (setup_us[i])
+struct SetupClock {
+    cacsi_geometry *g;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(int i) {
+        const auto n = std::chrono::steady_clock::now();
+        g->setup_us[i] += std::chrono::duration_cast<std::chrono::microseconds>(n - t).count();
+        t = n;
+    }
+};
+
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     const Params &p = g->p;
+    SetupClock clk{g};
     const int nv = p.n_vox, Q = p.nq, K = p.ne;
     float *dmin = nullptr, *dmax = nullptr, *dpt = nullptr;
     cudaError_t e = cudaMalloc(&dmin, nv * sizeof(float));
@@ -1077,6 +1090,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         E.tc_w1 = (const float *)g->d_tc_w1;
         E.tc_b = (const float *)g->d_tc_b;
     }
+    clk.mark(0);  // pair stats, breakpoints, S~, LUT, windows, tensor-core operand tiles
     // transmission bitmaps
     {
         const size_t nfw = p.ts_rho > 0 ? (size_t)p.nz * p.det_nx * ((p.ny + 31) / 32) * p.det_ny
@@ -1101,6 +1115,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         }
         if (e != cudaSuccess) return e;
         E.seen = (const uint32_t *)g->d_seen;
+        clk.mark(1);  // transmission bitmaps
         E.tb_fwd = (const uint32_t *)g->d_tb_fwd;
         E.tb_bwd = (const uint32_t *)g->d_tb_bwd;
     }
@@ -1136,6 +1151,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         cudaFree(A1);
         if (e != cudaSuccess) return e;
         E.vbound = (const float *)g->d_esai_vbound;
+        clk.mark(2);  // fixed-point bound pass
     }
     // pair cache (above): counts -> host scan -> fill, if it fits in half the free memory
     E.pc = 0;
@@ -1204,6 +1220,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             }
             e = cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
+            clk.mark(3);  // pair cache: count, scan, allocation, fill
             E.pcb_bt = E.pc_bt;
             E.pcb_P = E.pc_P;
             E.pcb_q = E.pc_q;
@@ -1230,6 +1247,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     for (void *x : arr) cudaFree(x);
                     return e;
                 }
+                clk.mark(4);  // bank-aware permutation
                 cudaFree(g->d_pc_bt);
                 cudaFree(g->d_pc_P);
                 cudaFree(g->d_pc_q);
@@ -1252,6 +1270,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) return e;
+                clk.mark(5);  // free the list-order copy, per-segment windows
                 if (g->opt.pc_segwin) E.pc_segwin = (const int2 *)g->d_pc_segwin;
             }
             E.pc = 1;

@@ -190,6 +190,8 @@ struct cacsi_geometry {
     cudaEvent_t stage_ev[3];
     cudaEvent_t stage_fev[4];  // f row chunks landed (cacsi_iterate_host, ESAI handles)
     mutable int32_t last_launches;
+    // geometry_create stage times (host wall clock, microseconds; cacsi_query "setup_us_<stage>")
+    long long setup_us[8];
     // per-kernel CUDA-event timing (cacsi_set_timing / cacsi_kernel_times)
     mutable int32_t timing;
     void *timers;  // cacsi::Timers*
