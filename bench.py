@@ -297,10 +297,11 @@ def run_gpu(args):
     nb_bp = G.query("esai_breakpoints")
     kern = {k: {"avg_ms": v[0] / v[1], "launches": v[1]} for k, v in ktimes.items()}
     fwd_k = [k for k in kern if k in ("k_pad_rows", "k_tc_pack_a", "k_tc_gemm_W", "k_esai_fwd", "k_esai_fwd_ts", "k_pc_fwd",
-                                      "k_sum_parts_f64",
-                                      "k_forward", "k_sum_f64")]
+                                      "k_sum_parts_f64", "k_forward", "k_sum_f64", "k_forward_er", "k_sum_f32",
+                                      "k_er_tab", "k_er_fwd")]
     bwd_k = [k for k in kern if k in ("k_absmax", "k_esai_bwd", "k_pc_bwd", "k_tc_gemm_b2", "k_sum_parts_f32",
-                                      "k_backward")]
+                                      "k_backward", "k_transpose", "k_backward_er", "k_er_absmax", "k_er_bwd",
+                                      "k_er_bsum")]
     op_ms = {"cacsi_forward": sum(kern[k]["avg_ms"] for k in fwd_k),
              "cacsi_backward": sum(kern[k]["avg_ms"] for k in bwd_k)}
     dom = max(op_ms, key=op_ms.get)
@@ -530,6 +531,12 @@ def alg_flops(kernel, cfg, counts, nb):
         "k_pc_bwd": 6 * open_,                         # pair cache: w scale, two weighted deposits
         "k_forward": 10 * pairs + 46 * open_ + 7 * counts["effective_terms"],
         "k_backward": 10 * pairs + 46 * open_ + 9 * counts["effective_terms"],
+        # energy-resolving per-term kernels: per effective term 4 flops forward (hat lerp 2 +
+        # accumulate 2), 6 backward (weight 2 + two deposits 4); geometry per open pair
+        "k_forward_er": 10 * pairs + 46 * open_ + 4 * counts["effective_terms"],
+        "k_backward_er": 10 * pairs + 46 * open_ + 6 * counts["effective_terms"],
+        "k_er_fwd": 4 * counts["effective_terms"],
+        "k_er_bwd": 6 * counts["effective_terms"],
     }
     return float(table.get(kernel, 0.0))
 

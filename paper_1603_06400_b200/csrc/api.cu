@@ -112,6 +112,7 @@ const OptKey kOptKeys[] = {
     {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
     {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},
     {"pc_fwd_list", &cacsi::Opts::pc_fwd_list, false, 0, 1},
+    {"pc_fwd_geom", &cacsi::Opts::pc_fwd_geom, false, 0, 1},
     {"pcv_items", &cacsi::Opts::pcv_items, false, 1, 64},
     {"pcv_pf", &cacsi::Opts::pcv_pf, false, 0, 16},
     {"pcv_u", &cacsi::Opts::pcv_u, false, 4, 8},
@@ -253,6 +254,9 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
     p.sai_tmin = d->sai_theta_min;
     p.sai_h = d->sai_n_theta > 1 ? (d->sai_theta_max - d->sai_theta_min) / (d->sai_n_theta - 1) : 1.0;
     p.pitch_d = (float)d->det_pitch;
+    p.det_x0 = (float)det_centre(d->det_cx, d->det_nx, d->det_pitch, 0);
+    p.det_y0 = (float)det_centre(d->det_cy, d->det_ny, d->det_pitch, 0);
+    p.det_div = (uint32_t)(4294967296.0 / d->det_ny) + 1u;
     p.quarter_p2 = (float)(0.25 * d->det_pitch * d->det_pitch);
     p.ax = (float)(-m0x / mp);
     const double beta0 = d->q_min / dq;

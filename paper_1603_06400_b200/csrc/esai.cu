@@ -1477,8 +1477,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int U = o.pcv_u;  // records per thread per step
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
-                auto kf = E.pc_qb == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024>
-                                                    : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512> : k_pc_fwd_v<uint16_t, 4, 512>)
+                const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536;
+                auto kf = E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true> : k_pc_fwd_v<uint16_t, 4, 1024>)
+                                                    : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512>
+                                                             : (geom ? k_pc_fwd_v<uint16_t, 4, 512, true> : k_pc_fwd_v<uint16_t, 4, 512>))
                                        : (T == 1024 ? k_pc_fwd_v<uint32_t, 4, 1024> : k_pc_fwd_v<uint32_t, 4, 512>);
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 kf<<<G * n_rb, T, smem, s>>>(p, E, W, R, vchunk, n_rb, n_items, pf, part);

@@ -47,6 +47,8 @@ struct Params {
     int ts_rho;
     float ts_c0;
     float vy0, vy_step;                // voxel centre y = vy0 + iy * vy_step (fp32, the TS forward's r^)
+    float det_x0, det_y0;              // pixel (0, 0) centre (fp32): x = det_x0 + ix p, y = det_y0 + jy p
+    uint32_t det_div;                  // ix = umulhi(q, det_div) for q < 2^16 (floor(2^32 / det_ny) + 1)
     // fp64 guard path (exact oracle op order, reading R8)
     double m0x, m0y, mask_pitch64;
     double det_z64;
@@ -155,6 +157,7 @@ struct Opts {
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
     int b2gemm_tiles = 0;     // "b2gemm_tiles": 1 = per-tile b2 GEMM instead of the persistent split-K one
     int pc_fwd_list = 0;      // "pc_fwd_list": 1 = per-list pair-cache forward (plain layout only)
+    int pc_fwd_geom = 0;      // "pc_fwd_geom": 1 = the voxel-major forward recomputes P (6-byte records)
     int pcv_items = 2;        // "pcv_items": voxel chunks per SM of the voxel-major forward
     int pcv_pf = 1;           // "pcv_pf": L2 prefetch distance (voxels) of the voxel-major forward
     int pcv_u = 4;            // "pcv_u": records per thread per step (4 or 8)

@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
             const uint32_t m = __ballot_sync(FULL, open);
             if (open) {
                 const long long o = base + __popc(m & ((1u << lane) - 1u));
-                bt[o] = ((uint32_t)b << e.pc_tbits) | min(__float2uint_rn(t * tone), tmax);
+                // tau fraction all-ones is reserved for padding records (k_pc_fwd_v<..., GEOM>)
+                bt[o] = ((uint32_t)b << e.pc_tbits) | min(__float2uint_rn(t * tone), tmax - 1u);
                 Pout[o] = P;
                 qout[o] = (QT)q;
             }
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
             const int2 win = e.vwin[v];
             const int span = max(1, win.y - win.x);
             for (long long o = base + lane; o < end; o += 32) {
-                bt[o] = (uint32_t)(win.x + (int)((o - base) % span)) << e.pc_tbits;
+                bt[o] = ((uint32_t)(win.x + (int)((o - base) % span)) << e.pc_tbits) | tmax;
                 Pout[o] = 0.0f;
                 qout[o] = (QT)(ix * p.det_ny);
             }
@@ -289,8 +290,9 @@ __global__ void k_pc_segwin(const Params p, const Esai e, int R, uint32_t *__res
         if (hi < 0) lo = e.vwin[v].x, hi = lo + 1;
         if (lane == 0) segwin[sg] = make_int2(lo, hi);
         const int span = hi - lo;  // padding bins b in [lo, hi - 1]: b + 1 <= hi stays inside
+        const uint32_t tmax = (1u << e.pc_tbits) - 1u;  // padding marker (k_pc_fill)
         for (long long o = a + lane; o < z; o += 32)
-            if (P[o] == 0.0f) bt[o] = (uint32_t)(lo + (int)((o - a) % span)) << e.pc_tbits;
+            if (P[o] == 0.0f) bt[o] = ((uint32_t)(lo + (int)((o - a) % span)) << e.pc_tbits) | tmax;
     }
 }
 
@@ -312,7 +314,11 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
                  "l"(W + (size_t)v * e.ldw + a), "r"(bytes), "r"(mb)
                  : "memory");
 }
-template <typename QT, int U, int PCV_T>
+// GEOM: the records' P is not read -- the pair's geometric factor is recomputed from the
+// pixel index and the voxel (translation-symmetric s_y = c0 + p (jy - rho iy) when
+// ts_rho > 0), 6 instead of 10 bytes per record (padding records carry the all-ones tau
+// marker and contribute 0).  An A/B variant (option pc_fwd_geom): DESIGN.md 4.2b.
+template <typename QT, int U, int PCV_T, bool GEOM = false>
 __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
@@ -374,10 +380,31 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
             // each thread takes U CONSECUTIVE records (16-byte vector loads, U / 4 quads); the
             // bank-aware order puts record j of every lane's quad in one conflict-light group,
             // so the warp's j-th shared-memory access touches distinct banks
-            const uint32_t kpad = (uint32_t)swin.x << tb;
+            const uint32_t kpad = ((uint32_t)swin.x << tb) | tmask;  // padding marker
             // P = 0: segment padding, whose pixel may repeat a real record's -- it
             // adds into the lane's dummy slot past the row block (branch-free)
-            auto deposit = [&](const uint32_t (&k)[U], const float (&P)[U], const uint32_t (&q)[U]) {
+            const VoxelRec vr = GEOM ? p.vox[v] : VoxelRec{};
+            const int iyr = GEOM ? p.ts_rho * (v / p.nz) : 0;
+            auto geom_P = [&](uint32_t k, uint32_t q) {
+                const uint32_t ix = __umulhi(q, p.det_div), jy = q - ix * (uint32_t)p.det_ny;
+                const float sx = fmaf(exact_float((int)ix), p.pitch_d, p.det_x0);
+                const float sy = p.ts_rho > 0 ? fmaf(p.pitch_d, exact_float((int)jy - iyr), p.ts_c0)
+                                              : fmaf(exact_float((int)jy), p.pitch_d, p.det_y0) - vr.y;
+                const float sz = vr.sz;
+                const float syz2 = fmaf(sy, sy, sz * sz);
+                const float rs = rsqrtf(fmaf(sx, sx, syz2));
+                const float rs2 = rs * rs;
+                const float cos_t = fmaf(vr.ry, sy, vr.rz * sz) * rs;
+                const float h = fmaf(0.5f, cos_t, 0.5f);
+                const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
+                const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
+                const float P = vr.gso * (sz * rs * rs2) * dth * fmaf(cos_t, cos_t, 1.0f) * (h * rsqrtf(h));
+                return (k & tmask) == tmask ? 0.0f : P;
+            };
+            auto deposit = [&](const uint32_t (&k)[U], const float (&P0)[U], const uint32_t (&q)[U]) {
+                float P[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) P[u] = GEOM ? geom_P(k[u], q[u]) : P0[u];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
@@ -396,7 +423,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
 #pragma unroll
                     for (int h = 0; h < U; h += 4) {
                         const uint4 kv = __ldg((const uint4 *)(kb + i + h));
-                        const float4 pv = __ldg((const float4 *)(Pb + i + h));
+                        const float4 pv = GEOM ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg((const float4 *)(Pb + i + h));
                         k[h] = kv.x, k[h + 1] = kv.y, k[h + 2] = kv.z, k[h + 3] = kv.w;
                         P[h] = pv.x, P[h + 1] = pv.y, P[h + 2] = pv.z, P[h + 3] = pv.w;
                         if (sizeof(QT) == 2) {

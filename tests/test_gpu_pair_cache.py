@@ -120,3 +120,19 @@ def test_wide_detector_uint32_pixels():
     assert_parity(gpu_forward(G, f), O.forward(f), "wide detector forward")
     assert_parity(gpu_backward(G, w), O.backward(w), "wide detector backward")
     G.close()
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_forward_recomputed_P_matches_stored(ci):
+    """Option pc_fwd_geom=1: the voxel-major forward recomputes each record's P from the
+    pixel index and the voxel (6-byte records, translation-symmetric s_y) instead of
+    reading it; same operator up to fp32 rounding of P, and the oracle bar (config 1)."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    g0 = gpu_forward(G, cfg.f)
+    G.set_option("pc_fwd_geom", 1)
+    g1 = gpu_forward(G, cfg.f)
+    assert_parity(g1, g0, f"c{ci} recomputed-P vs stored-P forward", l2=1e-6, mr=1e-5)
+    if ci == 1:
+        assert_parity(g1, oracle.Geometry(cfg).forward(cfg.f), "c1 recomputed-P forward")
+    G.close()
