@@ -5,6 +5,7 @@
 // centres, per-energy constants and the bit-packed mask are computed ONCE in
 // fp64 and uploaded; everything per pair is computed online by the kernels.
 #include <chrono>
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -32,6 +33,38 @@ static uint32_t __float_as_uint_host(float x) {
     return u;
 }
 double det_centre(double c, int n, double p, int i) { return c + ((i + 0.5) - 0.5 * n) * p; }
+
+// Fast-path preconditions, from the descriptor alone.
+// (1) dtheta's series: x = p |s_yz| / (|s|^2 - p^2/4) <= p / (s - p^2 / (4 s)) with
+//     s = det_z - z_max <= |s_yz|; atan(x) = x (1 - x^2/3) is used up to kAtanXMax.
+double atan_xmax_of(const cacsi_geometry_desc *d) {
+    const double sz = d->det_z - d->z_max, pp = d->det_pitch;
+    return sz > pp ? pp / (sz - pp * pp / (4.0 * sz)) : INFINITY;
+}
+// (2) the fp32 mask-cell coordinate u = fma(tq, x, a) (pair.cuh mask_fast) has error
+//     <= 1/2 ulp(|u|max) + 2^-23 |tq x|max + 1/2 ulp(|a|max) per axis (tq, x, a rounded
+//     to fp32 once, as create rounds them); the guard band is 4x that, at least kMaskGuard.
+double mask_guard_of(const cacsi_geometry_desc *d) {
+    auto ulp = [](double v) { return v > 0.0 ? std::ldexp(1.0, std::ilogb(v) - 23) : 0.0; };
+    const double mp = d->mask_pitch;
+    const double m0x = d->mask_cx - (0.5 * d->mask_nx) * mp, m0y = d->mask_cy - (0.5 * d->mask_ny) * mp;
+    double tqm = 0.0, aym = 0.0, xdm = 0.0, ydm = 0.0;
+    for (int iy = 0; iy < d->ny; iy += std::max(1, d->ny - 1))  // t and |y| are extreme at the ends
+        for (int iz = 0; iz < d->nz; iz++) {
+            const double y = centre(d->y_min, d->y_max, d->ny, iy), z = centre(d->z_min, d->z_max, d->nz, iz);
+            const double t = (d->mask_z - z) / (d->det_z - z);
+            tqm = std::fmax(tqm, std::fabs((double)(float)(t / mp)));
+            aym = std::fmax(aym, std::fabs((double)(float)((y * (1.0 - t) - m0y) / mp)));
+        }
+    for (int i = 0; i < d->det_nx; i += std::max(1, d->det_nx - 1))
+        xdm = std::fmax(xdm, std::fabs((double)(float)det_centre(d->det_cx, d->det_nx, d->det_pitch, i)));
+    for (int j = 0; j < d->det_ny; j += std::max(1, d->det_ny - 1))
+        ydm = std::fmax(ydm, std::fabs((double)(float)det_centre(d->det_cy, d->det_ny, d->det_pitch, j)));
+    const double axm = std::fabs((double)(float)(-m0x / mp));
+    const double bx = 0.5 * ulp(tqm * xdm + axm) + std::ldexp(tqm * xdm, -23) + 0.5 * ulp(axm);
+    const double by = 0.5 * ulp(tqm * ydm + aym) + std::ldexp(tqm * ydm, -23) + 0.5 * ulp(aym);
+    return std::fmax((double)cacsi::kMaskGuard, 4.0 * std::fmax(bx, by));
+}
 
 cacsi_status validate(const cacsi_geometry_desc *d) {
     if (!d->energy_kev || !d->phi || !d->mask) return CACSI_ERR_NULL;
@@ -68,6 +101,8 @@ cacsi_status validate(const cacsi_geometry_desc *d) {
                         d->mask_cx, d->mask_cy, d->det_z, d->det_pitch, d->det_cx, d->det_cy};
     for (double x : v)
         if (!std::isfinite(x)) return CACSI_ERR_INVALID;
+    if (!(atan_xmax_of(d) <= cacsi::kAtanXMax)) return CACSI_ERR_INVALID;  // pixel too wide for the dtheta series
+    if (!(mask_guard_of(d) < 0.25)) return CACSI_ERR_INVALID;              // fp32 mask coordinates too coarse
     return CACSI_OK;
 }
 
@@ -315,6 +350,7 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
             p.inv_da = (float)((cacsi::kHc * dq) / de);
         }
     }
+    p.mask_guard = (float)mask_guard_of(d);  // fast-path guard band (validated above)
     // bit-packed mask: word w of row i holds cells (i, 32w .. 32w+31)
     std::vector<uint32_t> bits((size_t)d->mask_nx * p.mask_words, 0u);
     for (int i = 0; i < d->mask_nx; i++)
@@ -910,6 +946,7 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
     if (!strcmp(key, "er_cache_records")) return g->er.enabled ? g->er.n : 0;
+    if (!strcmp(key, "mask_guard_ppm")) return (int64_t)std::llround(g->p.mask_guard * 1e6);
     static const char *stages[8] = {"setup_us_tables", "setup_us_bitmaps", "setup_us_bound", "setup_us_pc_fill",
                                     "setup_us_pc_perm", "setup_us_pc_segwin", "setup_us_host", "setup_us_total"};
     for (int i = 0; i < 8; i++)

@@ -13,7 +13,8 @@ namespace cacsi {
 constexpr double kHc = 12.3984193;          // keV Angstrom
 constexpr float kMagic = 12582912.0f;        // 1.5 * 2^23: x + kMagic rounds x to an integer
 constexpr int kMagicBits = 0x4B400000;       // __float_as_int(kMagic)
-constexpr float kMaskGuard = 5e-4f;          // mask-cell guard band, cells (K2)
+constexpr float kMaskGuard = 5e-4f;          // minimum mask-cell guard band, cells
+constexpr double kAtanXMax = 0.0149;         // dtheta's atan(x) = x (1 - x^2/3) is used for x <= this (x^4/5 < 1e-8)
 
 // fp32 per-voxel record (32 B, two float4 loads).  All derived in fp64 on the
 // host from the descriptor ("precompute G_so").
@@ -38,6 +39,7 @@ struct Params {
     float pitch_d;                     // detector pitch p
     float quarter_p2;                  // p^2 / 4
     float ax;                          // -m0x / mask_pitch: u_x = tq * x_d + ax
+    float mask_guard;                  // fp32 cell coordinates within this of an edge take the fp64 rule
     float nb;                          // -(q_min / dq) - 1/2   (u' = alpha_k sh + nb = u - 1/2)
     float qm;                          // nq - 1/2               (clamp bound of u')
     float klo_num, khi_num;            // (q_min/dq - 1), (q_min/dq + nq): alpha range numerators

@@ -34,15 +34,15 @@ __device__ __forceinline__ bool mask_exact(const Params &p, int v, int q) {
 }
 
 // fp32 fast path of T: u = (t/p) x + const per axis, cell = floor(u).  *near is
-// set when u lies within kMaskGuard cells of a cell edge (the fp32 error bound
-// is well below the guard, K2); the result is then undefined and the
-// caller must use mask_exact.  Kept branch-free so batched callers stay
+// set when u lies within p.mask_guard cells of a cell edge (4x the fp32 error bound
+// of u derived at create from the geometry's extents, at least kMaskGuard; DESIGN.md
+// 4.1); the result is then undefined and the caller must use mask_exact.  Kept branch-free so batched callers stay
 // converged; the exact re-tests run in a separate pass.
 __device__ __forceinline__ bool mask_fast(const Params &p, const VoxelRec &vr, float2 d, bool &near) {
     const float ux = fmaf(vr.tq, d.x, p.ax);
     const float uy = fmaf(vr.tq, d.y, vr.ay);
     const float fx = floorf(ux), fy = floorf(uy);
-    near = fabsf(ux - fx - 0.5f) > 0.5f - kMaskGuard || fabsf(uy - fy - 0.5f) > 0.5f - kMaskGuard;
+    near = fabsf(ux - fx - 0.5f) > 0.5f - p.mask_guard || fabsf(uy - fy - 0.5f) > 0.5f - p.mask_guard;
     const int ix = (int)fx, iy = (int)fy;
     if ((unsigned)ix >= (unsigned)p.mask_nx || (unsigned)iy >= (unsigned)p.mask_ny) return false;
     const uint32_t w = __ldg(p.maskbits + (size_t)ix * p.mask_words + (iy >> 5));
@@ -73,8 +73,8 @@ __device__ __forceinline__ void pair_geom(const Params &p, const VoxelRec &vr, f
     const float rh = rsqrtf(h);
     const float ch = h * rh;
     sh = 0.5f * sin_t * rh;
-    // dtheta = atan(x), x = p sqrt(sy^2+sz^2) / (|s|^2 - p^2/4); x <= ~1e-2 so
-    // atan(x) = x (1 - x^2/3) to ~x^4/5 and 1/(s2 - p^2/4) = rs2 (1 + p^2/4 rs2)
+    // dtheta = atan(x), x = p sqrt(sy^2+sz^2) / (|s|^2 - p^2/4); x <= kAtanXMax (checked
+    // at create) so atan(x) = x (1 - x^2/3) to x^4/5 < 1e-8 and 1/(s2 - p^2/4) = rs2 (1 + p^2/4 rs2)
     const float x = p.pitch_d * fast_sqrt(syz2) * rs2 * fmaf(p.quarter_p2, rs2, 1.0f);
     const float dth = x * fmaf(-0.33333334f * x, x, 1.0f);
     P = angular ? vr.gso * god * dth * fmaf(cos_t, cos_t, 1.0f) * ch : vr.gso * god * dth;

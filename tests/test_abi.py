@@ -72,6 +72,8 @@ def _create(d, options=None):
     dict(sai_n_theta=250, sai_theta_min=0.0, sai_theta_max=4.0),
     dict(sai_n_theta=250, sai_theta_min=-0.1, sai_theta_max=0.5),
     dict(sai_n_theta=250, sai_theta_min=0.01, sai_theta_max=0.5, energy_resolving=1),
+    # a pixel too wide for dtheta's series atan(x) = x (1 - x^2/3) (x <= 0.0149)
+    dict(det_pitch=20.0), dict(det_z=820.0, mask_z=810.0, det_pitch=7.0),
 ])
 def test_invalid_descriptors_rejected(over):
     assert _create(_desc(**over)) == binding.CACSI_ERR_INVALID

@@ -327,3 +327,20 @@ def test_translation_symmetric_forward(over, rho):
     assert_parity(g, ref, f"TS {over} forward")
     assert_parity(g2, ref, f"tiled {over} forward")
     assert rel_l2(g, g2) < 1e-6
+
+
+def test_fine_4096_cell_mask():
+    """A 2400 x 4096-cell mask (0.01 mm cells): the fp32 cell coordinate's rounding grows
+    with the coordinate's size, so the guard band widens beyond the 5e-4-cell minimum
+    (create derives it from the extents) and T stays exact."""
+    cfg = make_config(0)
+    d = cfg.desc()
+    d.update(mask_nx=2400, mask_ny=4096, mask_pitch=0.01)
+    d["mask"] = seeded_rng(0, 62).integers(0, 2, (2400, 4096)).astype(np.uint8)
+    G, O = geoms(d)
+    assert G.query("mask_guard_ppm") > 500
+    f, w = rnd(G.f_shape, 0, 63), rnd(G.g_shape, 0, 64)
+    assert_parity(gpu_forward(G, f), O.forward(f), "4096-cell mask forward")
+    assert_parity(gpu_backward(G, w), O.backward(w), "4096-cell mask backward")
+    G2 = P.Geometry(d, options="pair_cache=0")
+    assert_parity(gpu_forward(G2, f), O.forward(f), "4096-cell mask on-the-fly forward")
