@@ -14,6 +14,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 using cacsi::Params;
@@ -190,6 +192,11 @@ cacsi_status parse_opts(const char *s, cacsi::Opts &o) {
 }  // namespace
 
 namespace cacsi {
+// NVTX range per entry point (visible in Nsight Systems / ncu --nvtx; no cost without a tool)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 // Every entry point that touches a handle's device memory runs on the handle's
 // device and restores the caller's current device on return.
 DeviceGuard::DeviceGuard(int dev) {
@@ -237,6 +244,7 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return CACSI_ERR_CUDA;
     cacsi::DeviceGuard dg(device);
+    cacsi::Nvtx nv_("cacsi_geometry_create");
     // keep stream-ordered scratch (W / A, split partials) cached across calls
     // instead of returning it to the OS at every synchronisation
     {
@@ -468,6 +476,7 @@ int32_t cacsi_last_launch_count(const cacsi_geometry *g) { return g ? g->last_la
 cacsi_status cacsi_forward(const cacsi_geometry *g, const float *f, float *out, void *stream) {
     if (!g || !f || !out) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_forward");
     int n = 0;
     cudaError_t e = cacsi::launch_forward(g, f, out, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -477,6 +486,7 @@ cacsi_status cacsi_forward(const cacsi_geometry *g, const float *f, float *out, 
 cacsi_status cacsi_backward(const cacsi_geometry *g, const float *w, float *b, void *stream) {
     if (!g || !w || !b) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_backward");
     int n = 0;
     cudaError_t e = cacsi::launch_backward(g, w, b, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -507,6 +517,7 @@ cacsi_status cacsi_neg_loglik_ex(const cacsi_geometry *g, const float *f, const 
                                  const cacsi_penalty *pen, double *out_dev, void *ws, void *stream) {
     if (!g || !f || !y || !r || !out_dev || !ws) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_neg_loglik_ex");
     const double delta = pen_delta(pen);
     if (delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
@@ -560,6 +571,7 @@ cacsi_status cacsi_iterate_ex(const cacsi_geometry *g, float *f, const float *y,
                               float beta, const cacsi_penalty *pen, int32_t n_iter, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1 || !ws) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_iterate_ex");
     const double delta = pen_delta(pen);
     if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
     float *l, *b2, *fnew;
@@ -588,6 +600,7 @@ cacsi_status cacsi_ratio(const cacsi_geometry *g, const float *l, const float *y
                          void *stream) {
     if (!g || !l || !y || !r || !ratio) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_ratio");
     int n = 0;
     cudaError_t e = cacsi::launch_ratio(g, l, y, r, ratio, nullptr, 0, (cudaStream_t)stream, &n);
     if (e == cudaSuccess) g->last_launches = n;
@@ -598,6 +611,7 @@ cacsi_status cacsi_update_ex(const cacsi_geometry *g, const float *f_hat, const 
                              const cacsi_penalty *pen, float *f_new, void *stream) {
     if (!g || !f_hat || !b1 || !b2 || !f_new) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_update_ex");
     const double delta = pen_delta(pen);
     if (!(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0) return CACSI_ERR_INVALID;
     int n = 0;
@@ -639,6 +653,7 @@ cacsi_status cacsi_forward_subset(const cacsi_geometry *g, const float *f, const
                                   float *out, void *stream) {
     if (!g || !f || !out || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_forward_subset");
     if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
     int n = 0;
     cudaError_t e = cacsi::launch_forward_subset(g, f, pixels, n_pixels, out, (cudaStream_t)stream, &n);
@@ -650,6 +665,7 @@ cacsi_status cacsi_backward_subset(const cacsi_geometry *g, const float *w, cons
                                    float *b, void *stream) {
     if (!g || !w || !b || (n_pixels > 0 && !pixels)) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_backward_subset");
     if (n_pixels < 0 || n_pixels > g->p.n_det) return CACSI_ERR_INVALID;
     int n = 0;
     cudaError_t e = cacsi::launch_backward_subset(g, w, pixels, n_pixels, b, (cudaStream_t)stream, &n);
@@ -708,6 +724,7 @@ cacsi_status cacsi_osem(const cacsi_geometry *g, float *f, const float *y, const
                         const cacsi_penalty *pen, int32_t n_outer, void *ws, void *stream) {
     if (!g || !f || !y || !r || !b1_subsets || !pixels || !offsets || !ws) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_osem");
     const double delta = pen_delta(pen);
     if (n_subsets < 1 || n_outer < 0 || !(beta >= 0.0f) || !std::isfinite(beta) || delta < 0.0)
         return CACSI_ERR_INVALID;
@@ -786,6 +803,7 @@ static cudaError_t ensure_stage(const cacsi_geometry *gc) {
 cacsi_status cacsi_forward_host(const cacsi_geometry *g, const float *fh, float *gh, void *stream) {
     if (!g || !fh || !gh) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_forward_host");
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = ensure_stage(g);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_a, fh, g->n_obj * 4, cudaMemcpyHostToDevice, s);
@@ -800,6 +818,7 @@ cacsi_status cacsi_forward_host(const cacsi_geometry *g, const float *fh, float 
 cacsi_status cacsi_backward_host(const cacsi_geometry *g, const float *wh, float *bh, void *stream) {
     if (!g || !wh || !bh) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_backward_host");
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = ensure_stage(g);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->d_stage_b, wh, g->n_detout * 4, cudaMemcpyHostToDevice, s);
@@ -815,6 +834,7 @@ cacsi_status cacsi_iterate_host(const cacsi_geometry *g, float *fh, const float 
                                 const float *b1h, float beta, int32_t n_iter, void *stream) {
     if (!g || !fh || !yh || !rh || !b1h) return CACSI_ERR_NULL;
     cacsi::DeviceGuard dg_(g->device);
+    cacsi::Nvtx nv_("cacsi_iterate_host");
     if (n_iter < 0 || !(beta >= 0.0f) || !std::isfinite(beta)) return CACSI_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     cacsi_geometry *gm = const_cast<cacsi_geometry *>(g);
