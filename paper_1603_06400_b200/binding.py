@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcacsi.so")
+# CACSI_CHECKED=1 loads the bounds-checked build (python -m paper_1603_06400_b200.build --checked)
+LIB_PATH = os.path.join(_HERE, "libcacsi_checked.so" if os.environ.get("CACSI_CHECKED") == "1" else "libcacsi.so")
 
 CACSI_OK, CACSI_ERR_NULL, CACSI_ERR_INVALID, CACSI_ERR_CUDA, CACSI_ERR_NOMEM = range(5)
 

@@ -37,17 +37,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+LIB_CHECKED = os.path.join(HERE, "libcacsi_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: libcacsi_checked.so with the device-side bounds checks (CACSI_CHECK)."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not checked and not _stale():
+        return lib
     extra = ["-Xptxas", "-v"] if verbose else []
-    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB + ".tmp", *sources()]
+    if checked:
+        extra += ["-DCACSI_CHECKS"]
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", lib + ".tmp", *sources()]
     # exported symbols: only the extern "C" cacsi_* entry points
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="--verbose" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="--verbose" in sys.argv, checked="--checked" in sys.argv))

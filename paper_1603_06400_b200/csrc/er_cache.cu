@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(896, 1) k_er_fwd(const Params p, const ErCache
                     const float u = fminf(fmaf(al[j], ps.y, nb), qm);
                     const float vm = u + kMagic;
                     const float tt = u - (vm - kMagic);
+                    CACSI_CHECK(__float_as_int(vm) - kMagicBits + c.nlo >= 0 && __float_as_int(vm) - kMagicBits + c.nlo < NT);
                     const float2 e = lds_f2(tb + (uint32_t)__float_as_int(vm) * 8u);
                     acc[j] = fmaf(P, fmaf(tt, e.y, e.x), acc[j]);
                 }
@@ -413,6 +414,8 @@ __global__ void __launch_bounds__(ER_BT) k_er_bwd(const Params p, const ErCache 
                             const float av = w_r * d.z;            // |av| <= 2^21 (scale rule)
                             const int xa = __float_as_int(av + kMagic);
                             const int x1 = __float_as_int(fmaf(av, t1, kMagic));
+                            CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -2 && __float_as_int(vm) - kMagicBits + 1 <= p.nq + 1 &&
+                                        __float_as_int(d.x) >= 0 && __float_as_int(d.x) < kErVB * HB * 4);
                             const uint32_t ad = hbase + (uint32_t)__float_as_int(d.x) + (uint32_t)__float_as_int(vm) * 4u;
                             red_s32(ad, xa - x1);
                             red_s32(ad + 4u, x1 - kMagicBits);

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(TS_T * TS_R, 2) k_esai_fwd_ts(const Params p, 
 #pragma unroll
                     for (int u = 0; u < 2; u++) {
                         const int iy = iyb + (u ? k2 : k1);
+                        CACSI_CHECK(tid + rho * (ny - 1 - iy) >= 0 && tid + rho * (ny - 1 - iy) < nfoot);
                         const float2 f = foot[tid + rho * (ny - 1 - iy)];
                         const float fiy = exact_float(iy);
                         const float sy = fmaf(p.pitch_d, exact_float(jy - rho * iy), p.ts_c0);
@@ -601,6 +602,7 @@ __global__ void __launch_bounds__(PB_T) k_esai_bwd(const Params p, const Esai e,
                 const float a1 = BOUND ? P1 * scale : P1 * __ldg(w + q1) * scale;
                 const float a2 = two ? (BOUND ? P2 * scale : P2 * __ldg(w + q2) * scale) : 0.0f;
                 const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
+                CACSI_CHECK(b1 >= win.x && b1 + 1 <= win.y && b2 >= win.x && b2 + 1 <= win.y);
                 atomicAdd(hv + b1, __float2int_rn(a1) - x1);
                 atomicAdd(hv + b1 + 1, x1);
                 atomicAdd(hv + b2, __float2int_rn(a2) - x2);
@@ -664,6 +666,8 @@ __global__ void __launch_bounds__(256) k_esai_bwd_list(const Params p, const Esa
                 const float a1 = o1 ? P1 * __ldg(w + q1) * scale : 0.0f;
                 const float a2 = o2 ? P2 * __ldg(w + q2) * scale : 0.0f;
                 const int x1 = __float2int_rn(a1 * t1), x2 = __float2int_rn(a2 * t2);
+                CACSI_CHECK(!o1 || (b1 >= win.x && b1 + 1 <= win.y));
+                CACSI_CHECK(!o2 || (b2 >= win.x && b2 + 1 <= win.y));
                 if (o1) {
                     atomicAdd(hv + b1, __float2int_rn(a1) - x1);
                     atomicAdd(hv + b1 + 1, x1);

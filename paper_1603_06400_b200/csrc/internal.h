@@ -3,10 +3,30 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <vector>
 
 #include "cacsi.h"
+
+// Device-side bounds checks of the hot kernels' shared-memory and table indices,
+// compiled in only for the checked build (python -m paper_1603_06400_b200.build --checked
+// -> libcacsi_checked.so, loaded by the binding when CACSI_CHECKED=1): the stand-in for
+// compute-sanitizer, which this pool does not run.  A failed check prints and traps.
+#ifdef CACSI_CHECKS
+#define CACSI_CHECK(c)                                                                          \
+    do {                                                                                        \
+        if (!(c)) {                                                                             \
+            printf("CACSI_CHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define CACSI_CHECK(c) \
+    do {               \
+    } while (0)
+#endif
 
 namespace cacsi {
 

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
                     const float2 e = en[k];
                     float tt;
                     const int n = hat_coord(p, e.x, sh, tt);
+                    CACSI_CHECK(n >= -2 && n <= Q);
                     const float2 t = tv[n];
                     ap = fmaf(e.y, fmaf(tt, t.y, t.x), ap);
                 }
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
 #pragma unroll
                     for (int j = 0; j < FWD_KU; j++) {
                         const int n = hat_coord(p, alpha[k + j], sh, tt[j]);
+                        CACSI_CHECK(n >= -2 && n <= Q && k + j < K4);
                         t[j] = tv[n];
                     }
 #pragma unroll

@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(PCF_W * 32) k_pc_fwd(const Params p, const Esa
                     for (int u = 0; u < 4; u++)
                         if (o + 32 * u < o1) {
                             const float t = (float)(k[u] & tmask) * tunit;
+                            CACSI_CHECK(jy[u] < (uint32_t)p.det_ny && (k[u] >> tb) + 1 < (uint32_t)e.ldw);
                             float *ap = acc + jy[u];
                             *ap = fmaf(P[u], fmaf(t, wb[u] - wa[u], wa[u]), *ap);
                         }
@@ -408,6 +409,8 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
+                    CACSI_CHECK(b >= (swin.x & ~3) && b + 1 < (swin.x & ~3) + wcap);
+                    CACSI_CHECK(P[u] == 0.0f || (q[u] >= (uint32_t)q0 && q[u] < (uint32_t)(q0 + nacc)));
                     const float wa = wv[b], wb = wv[b + 1];
                     const float t = (float)(k[u] & tmask) * tunit;
                     float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
                 const int b = (int)(k[u] >> tb);
                 const float a = P[u] * wq[u];
                 const int x1 = __float2int_rn(a * ((float)(k[u] & tmask) * tunit));
+                CACSI_CHECK(b >= win.x && b + 1 <= win.y);
                 atomicAdd(hv + b, __float2int_rn(a) - x1);
                 atomicAdd(hv + b + 1, x1);
             }
@@ -667,6 +671,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                 const int b = (int)(k[u] >> tb);
                 const float av = P[u] * wq[u];
                 const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                CACSI_CHECK(b >= win.x && b + 1 <= win.y);
                 atomicAdd(hv + b, __float2int_rn(av) - x1);
                 atomicAdd(hv + b + 1, x1);
             }
