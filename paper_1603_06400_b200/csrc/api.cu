@@ -153,6 +153,7 @@ const OptKey kOptKeys[] = {
     {"pcv_items", &cacsi::Opts::pcv_items, false, 1, 64},
     {"pcv_pf", &cacsi::Opts::pcv_pf, false, 0, 16},
     {"pcv_u", &cacsi::Opts::pcv_u, false, 4, 8},
+    {"pcv_pipe", &cacsi::Opts::pcv_pipe, false, 0, 1},
     {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},

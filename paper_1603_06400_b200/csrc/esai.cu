@@ -1482,7 +1482,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
                 const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536;
-                auto kf = E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true> : k_pc_fwd_v<uint16_t, 4, 1024>)
+                auto kf = E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true>
+                                                            : o.pcv_pipe ? k_pc_fwd_v<uint16_t, 4, 1024, false, true>
+                                                                         : k_pc_fwd_v<uint16_t, 4, 1024>)
                                                     : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512>
                                                              : (geom ? k_pc_fwd_v<uint16_t, 4, 512, true> : k_pc_fwd_v<uint16_t, 4, 512>))
                                        : (T == 1024 ? k_pc_fwd_v<uint32_t, 4, 1024> : k_pc_fwd_v<uint32_t, 4, 512>);

@@ -319,7 +319,9 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
 // pixel index and the voxel (translation-symmetric s_y = c0 + p (jy - rho iy) when
 // ts_rho > 0), 6 instead of 10 bytes per record (padding records carry the all-ones tau
 // marker and contribute 0).  An A/B variant (option pc_fwd_geom): DESIGN.md 4.2b.
-template <typename QT, int U, int PCV_T, bool GEOM = false>
+// PIPE: the vector record loop is software-pipelined -- each thread's next 4 records are
+// loaded before the current 4 are deposited (two steps of loads in flight per thread).
+template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false>
 __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
@@ -417,7 +419,30 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
             };
-            if (vec) {
+            if (vec && PIPE && U == 4 && sizeof(QT) == 2) {
+                int i = 4 * tid;
+                uint4 kv = make_uint4(0u, 0u, 0u, 0u);
+                float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+                uint2 qv = make_uint2(0u, 0u);
+                auto ld = [&](int j) {
+                    kv = __ldg((const uint4 *)(kb + j));
+                    if (!GEOM) pv = __ldg((const float4 *)(Pb + j));
+                    qv = __ldg((const uint2 *)(qb + j));
+                };
+                if (i < n) ld(i);
+                for (; i < n; i += 4 * PCV_T) {
+                    const uint4 ck = kv;
+                    const float4 cp = pv;
+                    const uint2 cq = qv;
+                    if (i + 4 * PCV_T < n) ld(i + 4 * PCV_T);
+                    uint32_t k[U], q[U];
+                    float P[U];
+                    k[0] = ck.x, k[1] = ck.y, k[2] = ck.z, k[3] = ck.w;
+                    P[0] = cp.x, P[1] = cp.y, P[2] = cp.z, P[3] = cp.w;
+                    q[0] = cq.x & 0xFFFFu, q[1] = cq.x >> 16, q[2] = cq.y & 0xFFFFu, q[3] = cq.y >> 16;
+                    deposit(k, P, q);
+                }
+            } else if (vec) {
                 // bank-ordered layout: the voxel's range is whole 128-record windows (n % 128 == 0),
                 // so every thread's U records are in range -- no bounds test in the loop
                 for (int i = U * tid; i < n; i += U * PCV_T) {

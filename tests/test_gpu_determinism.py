@@ -55,3 +55,21 @@ def test_cta_pair_w_gemm_bitwise():
         out.append(g)
     assert torch.equal(out[0], out[1])
     G.close()
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_pipelined_forward_bitwise(ci):
+    """Option pcv_pipe=1 (software-pipelined record loads in the voxel-major forward)
+    gives the same bits as the default loop."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    f = torch.as_tensor(cfg.f).cuda()
+    out = []
+    for mode in (0, 1):
+        G.set_option("pcv_pipe", mode)
+        g = torch.empty(G.g_shape, device="cuda")
+        G.forward(f, g)
+        torch.cuda.synchronize()
+        out.append(g)
+    assert torch.equal(out[0], out[1])
+    G.close()
