@@ -183,7 +183,7 @@ struct Opts {
     int pcv_items = 2;        // "pcv_items": voxel chunks per SM of the voxel-major forward
     int pcv_pf = 1;           // "pcv_pf": L2 prefetch distance (voxels) of the voxel-major forward
     int pcv_u = 4;            // "pcv_u": records per thread per step (4 or 8)
-    int pcv_pipe = 0;         // "pcv_pipe": 1 = software-pipelined record loads in the voxel-major forward
+    int pcv_pipe = 1;         // "pcv_pipe": 0 = the voxel-major forward without software-pipelined record loads
     int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
     int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
