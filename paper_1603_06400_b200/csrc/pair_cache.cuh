@@ -353,13 +353,6 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     // every thread's zeroing before any thread's first deposit (the mbarrier wait below
     // orders only the bulk copy, not the other warps' stores)
     __syncthreads();
-    // PIPE: the next 4 records of this thread, loaded one step ahead -- across voxel
-    // boundaries too (the first step of voxel v + 1 is loaded during voxel v's last step,
-    // before the barrier); pref = the registers hold this thread's first records of v
-    uint4 kv = make_uint4(0u, 0u, 0u, 0u);
-    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint2 qv = make_uint2(0u, 0u);
-    bool pref = false;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int c = item / n_rb;
         const int v0 = c * vchunk, v1 = min(p.n_vox, v0 + vchunk);
@@ -427,35 +420,21 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                 }
             };
             if (vec && PIPE && U == 4 && sizeof(QT) == 2) {
-                // the next voxel's range (its first step is loaded during this voxel's last)
-                long long no0 = 0;
-                int nn = 0;
-                if (v + 1 < v1) {
-                    no0 = __ldg(e.pc_off + l0 + p.det_nx + r0);
-                    nn = (int)(__ldg(e.pc_off + l0 + p.det_nx + r1) - no0);
-                }
-                auto ld = [&](long long o) {
-                    kv = __ldg((const uint4 *)(e.pc_bt + o));
-                    if (!GEOM) pv = __ldg((const float4 *)(e.pc_P + o));
-                    qv = __ldg((const uint2 *)(pq + o));
-                };
                 int i = 4 * tid;
-                if (!pref && i < n) ld(o0 + i);
-                pref = false;
-                if (i >= n && 4 * tid < nn) {  // no records of this voxel: prefetch the next one's
-                    ld(no0 + 4 * tid);
-                    pref = true;
-                }
+                uint4 kv = make_uint4(0u, 0u, 0u, 0u);
+                float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+                uint2 qv = make_uint2(0u, 0u);
+                auto ld = [&](int j) {
+                    kv = __ldg((const uint4 *)(kb + j));
+                    if (!GEOM) pv = __ldg((const float4 *)(Pb + j));
+                    qv = __ldg((const uint2 *)(qb + j));
+                };
+                if (i < n) ld(i);
                 for (; i < n; i += 4 * PCV_T) {
                     const uint4 ck = kv;
                     const float4 cp = pv;
                     const uint2 cq = qv;
-                    if (i + 4 * PCV_T < n) {
-                        ld(o0 + i + 4 * PCV_T);
-                    } else if (4 * tid < nn) {
-                        ld(no0 + 4 * tid);
-                        pref = true;
-                    }
+                    if (i + 4 * PCV_T < n) ld(i + 4 * PCV_T);
                     uint32_t k[U], q[U];
                     float P[U];
                     k[0] = ck.x, k[1] = ck.y, k[2] = ck.z, k[3] = ck.w;
