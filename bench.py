@@ -325,7 +325,7 @@ def run_gpu(args):
     # DRAM traffic of the operator's kernels from the committed ncu --set full capture
     # (profiles/r2k_dram_traffic.json, bytes per launch); kernels it does not list are omitted
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1s7_dram_traffic.json")))["kernels"]
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r2k_dram_traffic.json")))["kernels"]
         ks = [k for k in (fwd_k if dom == "cacsi_forward" else bwd_k) if k in tr]
         if ks:
             roofline["traffic"] = float(sum(tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"] for k in ks))
@@ -365,7 +365,7 @@ def run_gpu(args):
                         "bytes_note": f"{rb} B per open pair (pair record) + list offsets + the gathered table "
                                       "once (DESIGN.md §8)"}
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r1s7_dram_traffic.json")))["kernels"]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r2k_dram_traffic.json")))["kernels"]
             if kd in tr:
                 roofline_hbm["traffic"] = tr[kd]["dram_read_bytes"] + tr[kd]["dram_write_bytes"]
         except Exception:
