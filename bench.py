@@ -341,7 +341,7 @@ def run_gpu(args):
     except Exception:
         pass
     # HBM roofline of the dominant pair-cache kernel: algorithmic bytes
-    # per launch = the record bytes per open pair (P, packed (b, tau), jy: 9 B on
+    # per launch = the record bytes per open pair (P, packed (b, tau), pixel q: 10 B on
     # config 2, read once) + the 8-byte list offsets
     # + the operator's table it gathers from once (k_pc_fwd: the W rows,
     # n_vox x ldw x 4 B; k_pc_bwd: w, n_det x 4 B, and the A rows it writes,

@@ -3,7 +3,9 @@
 // Host setup = the offline half of the paper's online/offline trade-off
 // (PAPER.md:236-241): per-voxel G_so, r^ and mask-plane parameters, per-pixel
 // centres, per-energy constants and the bit-packed mask are computed ONCE in
-// fp64 and uploaded; everything per pair is computed online by the kernels.
+// fp64 and uploaded; esai_build (esai.cu) then builds the ESAI tables, the
+// transmission bitmaps and the pair cache (each open pair's P and breakpoint
+// cell, computed once on the device and streamed by every operator call).
 #include <chrono>
 #include <algorithm>
 #include <cmath>
