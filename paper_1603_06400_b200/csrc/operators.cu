@@ -265,13 +265,20 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_c(const Params p, const f
         const int wlo = __reduce_min_sync(FULL, klo);
         const int whi = __reduce_max_sync(FULL, khi);
         const float *wp = w + e.q;
+        // w of the next two energies in flight while this one deposits (the gathers'
+        // L2 latency was the kernel's main stall: profiles/r2l_er_direct_ncu.json)
+        float w0 = wlo <= whi ? __ldg(wp + (size_t)wlo * p.n_det) : 0.0f;
+        float w1 = wlo + 1 <= whi ? __ldg(wp + (size_t)(wlo + 1) * p.n_det) : 0.0f;
         for (int k = wlo; k <= whi; k++) {
+            const float wk = w0;
+            w0 = w1;
+            w1 = k + 2 <= whi ? __ldg(wp + (size_t)(k + 2) * p.n_det) : 0.0f;
             const float2 en_k = en[k];
             float tt;
             const int n = hat_coord(p, en_k.x, e.sh, tt);
             // no window test: a term outside this lane's [klo, khi] has its hat coordinate
             // clamped onto the padding rows (node -2 / nq), which the readout skips
-            const float ca = e.P * en_k.y * __ldg(wp + (size_t)k * p.n_det);
+            const float ca = e.P * en_k.y * wk;
             const float hi = fmaf(tt, ca, 0.5f * ca);
             float *h0 = hb + (n + 2) * BWD_T;
             h0[0] += ca - hi;
