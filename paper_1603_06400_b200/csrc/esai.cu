@@ -24,6 +24,7 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
 #include <cudaTypedefs.h>
 
 #include "pair.cuh"
@@ -1070,27 +1071,24 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     // pre-split into TF32 hi / lo and pre-swizzled (tcgemm.cuh)
     E.ldw = (nb + 31) / 32 * 32;
     {
+        // packed on the device from S~ (already uploaded): the same arithmetic as the host
+        // tc_pack_b (tf32 truncation and an exact subtraction), so the same bits
         const int nkcW = (Q + TC_KC - 1) / TC_KC, nkcB = E.ldw / TC_KC;
-        // W2 = F S~^T as (W_b, W_{b+1}) pairs: overlapping tiles of stride 126
-        std::vector<float> tW((size_t)tc_ntiles(nb, TC_PSTRIDE) * nkcW * 2 * TC_N * TC_KC);
-        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW.data(), TC_PSTRIDE);
-        std::vector<float> stT((size_t)Q * nb);
-        for (int b = 0; b < nb; b++)
-            for (int j = 0; j < Q; j++) stT[(size_t)j * nb + b] = stab[(size_t)b * Q + j];
-        std::vector<float> tB((size_t)((Q + TC_N - 1) / TC_N) * nkcB * 2 * TC_N * TC_KC);
-        tc_pack_b(stT.data(), Q, nb, nb, nkcB, tB.data());
-        e = cudaMalloc(&g->d_tc_w, tW.size() * sizeof(float));
-        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_w, tW.data(), tW.size() * sizeof(float), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMalloc(&g->d_tc_b, tB.size() * sizeof(float));
-        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_b, tB.data(), tB.size() * sizeof(float), cudaMemcpyHostToDevice);
+        const size_t nW = (size_t)tc_ntiles(nb, TC_PSTRIDE) * nkcW * 2 * TC_N * TC_KC;  // W2 pairs (stride 126)
+        const size_t nB = (size_t)((Q + TC_N - 1) / TC_N) * nkcB * 2 * TC_N * TC_KC;    // S~^T for b2 = A S~
+        const size_t nW1 = (size_t)tc_ntiles(nb, TC_N) * nkcW * 2 * TC_N * TC_KC;      // plain W tiles
+        e = cudaMalloc(&g->d_tc_w, nW * sizeof(float));
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_tc_b, nB * sizeof(float));
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_tc_w1, nW1 * sizeof(float));
+        if (e != cudaSuccess) return e;
+        const float *st = (const float *)g->d_esai_stab;
+        const int gp = 8 * sm_count(g->device);
+        k_tc_pack_b<<<gp, 256>>>(st, nb, Q, Q, 1, nkcW, (float *)g->d_tc_w, TC_PSTRIDE);
+        k_tc_pack_b<<<gp, 256>>>(st, Q, nb, 1, Q, nkcB, (float *)g->d_tc_b, TC_N);   // B = S~^T (transposed read)
+        k_tc_pack_b<<<gp, 256>>>(st, nb, Q, Q, 1, nkcW, (float *)g->d_tc_w1, TC_N);
+        e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         E.tc_w = (const float *)g->d_tc_w;
-        // the same S~ packed in disjoint tiles: the plain W = F S~^T read by the pair-cache forward
-        std::vector<float> tW1((size_t)tc_ntiles(nb, TC_N) * nkcW * 2 * TC_N * TC_KC);
-        tc_pack_b(stab.data(), nb, Q, Q, nkcW, tW1.data(), TC_N);
-        e = cudaMalloc(&g->d_tc_w1, tW1.size() * sizeof(float));
-        if (e == cudaSuccess) e = cudaMemcpy(g->d_tc_w1, tW1.data(), tW1.size() * sizeof(float), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return e;
         E.tc_w1 = (const float *)g->d_tc_w1;
         E.tc_b = (const float *)g->d_tc_b;
     }
@@ -1157,47 +1155,52 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         E.vbound = (const float *)g->d_esai_vbound;
         clk.mark(2);  // fixed-point bound pass
     }
-    // pair cache (above): counts -> host scan -> fill, if it fits in half the free memory
+    // pair cache (above): counts -> device scan -> fill, if it fits in half the free memory
     E.pc = 0;
     E.pc_segwin = nullptr;
     if (g->opt.pair_cache && (size_t)p.det_ny <= 65535) {
         const size_t nl = (size_t)nv * p.det_nx;
-        int *cnt = nullptr;
-        e = cudaMalloc(&cnt, nl * sizeof(int));
-        if (e == cudaSuccess) {
-            k_pc_count<<<8 * sm_count(g->device), 256>>>(p, E, cnt);
-            e = cudaDeviceSynchronize();
-        }
-        std::vector<int> hc(nl);
-        if (e == cudaSuccess) e = cudaMemcpy(hc.data(), cnt, nl * sizeof(int), cudaMemcpyDeviceToHost);
-        cudaFree(cnt);
-        if (e != cudaSuccess) return e;
         // segments (voxel, block of R rows) of the voxel-major forward, padded to
-        // multiples of 32 records (the padding belongs to the segment's last list)
-        long long nopen = 0;
-        for (size_t i = 0; i < nl; i++) nopen += hc[i];
+        // multiples of 128 records (the padding belongs to the segment's last list)
         const int n_rb = pcv_row_blocks(g);
         const int R = n_rb > 0 ? (p.det_nx + n_rb - 1) / n_rb : 0;
         const int segR = (R > 0 && !g->opt.pc_plain) ? R : 0;  // pc_plain: no padding / bank-aware order
-        std::vector<long long> off(nl + 1, 0);
-        for (size_t i = 0; i < nl; i++) {
-            off[i + 1] = off[i] + hc[i];
-            const int ix = (int)(i % p.det_nx);
-            if (segR > 0 && ((ix + 1) % segR == 0 || ix + 1 == p.det_nx)) off[i + 1] = (off[i + 1] + 127) & ~127ll;
+        long long *cnt = nullptr, *tot = nullptr;
+        void *tmp = nullptr;
+        size_t tmp_b = 0;
+        e = cudaMalloc(&g->d_pc_off, (nl + 1) * sizeof(long long));
+        if (e == cudaSuccess) e = cudaMalloc(&cnt, (nl + 1) * sizeof(long long));
+        if (e == cudaSuccess) e = cudaMalloc(&tot, 2 * sizeof(long long));
+        if (e == cudaSuccess)
+            e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_b, cnt, (long long *)g->d_pc_off, (int)(nl + 1));
+        if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_b);
+        long long ht[2] = {0, 0};
+        if (e == cudaSuccess) {
+            e = cudaMemset(tot, 0, 2 * sizeof(long long));
+            k_pc_count<<<8 * sm_count(g->device), 256>>>(p, E, cnt, nl);
+            k_pc_pad<<<8 * sm_count(g->device), 256>>>(p, segR, cnt, tot);
+            if (e == cudaSuccess)
+                e = cub::DeviceScan::ExclusiveSum(tmp, tmp_b, cnt, (long long *)g->d_pc_off, (int)(nl + 1));
+            if (e == cudaSuccess) e = cudaMemcpy(ht, tot, sizeof(ht), cudaMemcpyDeviceToHost);  // syncs
         }
-        const long long nrec = off[nl];
+        cudaFree(cnt);
+        cudaFree(tot);
+        cudaFree(tmp);
+        if (e != cudaSuccess) return e;
+        const long long nopen = ht[0], nrec = ht[1];
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
         const size_t jyb = p.n_det <= 65536 ? 2 : 4;
         // + 8 records of padding: bulk copies read whole 8-record groups (16-byte aligned)
         const size_t rec = (size_t)std::max(nrec, 1ll) + 8;
-        const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb) + (nl + 1) * sizeof(long long);
+        const size_t need = rec * (sizeof(uint32_t) + sizeof(float) + jyb);
         int bbits = 1;
         while ((1 << bbits) < E.nb) bbits++;
-        // transient peak at build: the fill's arrays + the ordered copy
-        if (2 * need <= free_b / 2 && bbits <= 16) {
-            e = cudaMalloc(&g->d_pc_off, (nl + 1) * sizeof(long long));
-            if (e == cudaSuccess) e = cudaMemcpy(g->d_pc_off, off.data(), (nl + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+        // the cache may take half of the free memory (the permutation runs in place)
+        if (!(need <= free_b / 2 && bbits <= 16)) {
+            cudaFree(g->d_pc_off);
+            g->d_pc_off = nullptr;
+        } else {
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_bt, rec * sizeof(uint32_t));
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_P, rec * sizeof(float));
             if (e == cudaSuccess) e = cudaMalloc(&g->d_pc_q, rec * jyb);
@@ -1229,38 +1232,20 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             E.pcb_P = E.pc_P;
             E.pcb_q = E.pc_q;
             if (segR > 0) {
-                // bank-aware order, permuted into fresh arrays (one copy serves both
-                // operators: a separate cells-only copy for the backward measured no faster)
-                void *arr[3] = {nullptr, nullptr, nullptr};
-                e = cudaMalloc(&arr[0], rec * sizeof(uint32_t));
-                if (e == cudaSuccess) e = cudaMalloc(&arr[1], rec * sizeof(float));
-                if (e == cudaSuccess) e = cudaMalloc(&arr[2], rec * jyb);
-                if (e == cudaSuccess) {
+                // bank-aware order, permuted in place (one copy serves both operators: a
+                // separate cells-only copy for the backward measured no faster)
+                {
                     const int gr2 = 8 * sm_count(g->device);
                     if (jyb == 2)
-                        k_pc_perm<uint16_t><<<gr2, PERM_W * 32>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
-                                                          (const float *)g->d_pc_P, (const uint16_t *)g->d_pc_q,
-                                                          (uint32_t *)arr[0], (float *)arr[1], (uint16_t *)arr[2]);
+                        k_pc_perm<uint16_t><<<gr2, PERM_W * 32>>>(p, E, segR, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P,
+                                                                  (uint16_t *)g->d_pc_q);
                     else
-                        k_pc_perm<uint32_t><<<gr2, PERM_W * 32>>>(p, E, segR, (const uint32_t *)g->d_pc_bt,
-                                                          (const float *)g->d_pc_P, (const uint32_t *)g->d_pc_q,
-                                                          (uint32_t *)arr[0], (float *)arr[1], (uint32_t *)arr[2]);
+                        k_pc_perm<uint32_t><<<gr2, PERM_W * 32>>>(p, E, segR, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P,
+                                                                  (uint32_t *)g->d_pc_q);
                     e = cudaDeviceSynchronize();
                 }
-                if (e != cudaSuccess) {
-                    for (void *x : arr) cudaFree(x);
-                    return e;
-                }
+                if (e != cudaSuccess) return e;
                 clk.mark(4);  // bank-aware permutation
-                cudaFree(g->d_pc_bt);
-                cudaFree(g->d_pc_P);
-                cudaFree(g->d_pc_q);
-                g->d_pc_bt = arr[0];
-                g->d_pc_P = arr[1];
-                g->d_pc_q = arr[2];
-                E.pc_bt = (const uint32_t *)g->d_pc_bt;
-                E.pc_P = (const float *)g->d_pc_P;
-                E.pc_q = g->d_pc_q;
                 E.pcb_bt = E.pc_bt;
                 E.pcb_P = E.pc_P;
                 E.pcb_q = E.pc_q;
@@ -1274,7 +1259,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) return e;
-                clk.mark(5);  // free the list-order copy, per-segment windows
+                clk.mark(5);  // per-segment windows
                 if (g->opt.pc_segwin) E.pc_segwin = (const int2 *)g->d_pc_segwin;
             }
             E.pc = 1;

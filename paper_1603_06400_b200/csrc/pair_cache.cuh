@@ -39,8 +39,10 @@ __device__ __forceinline__ void l2_prefetch(const void *ptr, size_t bytes) {
 // (z, row, y) with the W gathers of one list on one W row, the backward by
 // voxel.  Built only if it fits (cacsi_query "pair_cache_records" > 0).
 
-// records per list (v, ix) = open pixels of row ix (transmission bitmap tb_bwd)
-__global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) {
+// records per list (v, ix) = open pixels of row ix (transmission bitmap tb_bwd); cnt[n] = 0
+// (the exclusive scan over n + 1 entries then ends with the total)
+__global__ void k_pc_count(const Params p, const Esai e, long long *__restrict__ cnt, size_t n_lists) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[n_lists] = 0;
     const int nw = (p.n_det + 31) / 32;
     const size_t n = (size_t)p.n_vox * p.det_nx;
     for (size_t l = blockIdx.x * (size_t)blockDim.x + threadIdx.x; l < n; l += (size_t)gridDim.x * blockDim.x) {
@@ -55,6 +57,31 @@ __global__ void k_pc_count(const Params p, const Esai e, int *__restrict__ cnt) 
             c += __popc(m);
         }
         cnt[l] = c;
+    }
+}
+
+// segment padding: the last list of each (voxel, block of R rows) segment gets the records
+// that round the segment up to a multiple of 128 (R = 0: no padding); tot[0] += open pairs,
+// tot[1] += records incl. padding (one warp per segment)
+__global__ void k_pc_pad(const Params p, int R, long long *__restrict__ cnt, long long *tot) {
+    const int Rs = R > 0 ? R : p.det_nx;
+    const int nseg_v = (p.det_nx + Rs - 1) / Rs;
+    const size_t nseg = (size_t)p.n_vox * nseg_v;
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (size_t)blockDim.x) >> 5;
+    for (size_t sg = warp0; sg < nseg; sg += nwarps) {
+        const int v = (int)(sg / nseg_v), s = (int)(sg % nseg_v);
+        const size_t l0 = (size_t)v * p.det_nx + (size_t)s * Rs;
+        const int nlst = min(Rs, p.det_nx - s * Rs);
+        long long c = 0;
+        for (int i = lane; i < nlst; i += 32) c += cnt[l0 + i];
+        c = __reduce_add_sync(0xFFFFFFFFu, (unsigned)c);  // a segment holds < 2^32 records
+        if (lane == 0) {
+            const long long pad = R > 0 ? ((c + 127) & ~127ll) - c : 0;
+            cnt[l0 + nlst - 1] += pad;
+            atomicAdd((unsigned long long *)tot, (unsigned long long)c);
+            atomicAdd((unsigned long long *)(tot + 1), (unsigned long long)(c + pad));
+        }
     }
 }
 
@@ -124,11 +151,16 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // state in local memory and read the window uncoalesced: ~108 ms per geometry on
 // config 2.)
 constexpr int PERM_W = 8;  // warps per CTA
+// In place: a warp reads its whole window into registers before it writes any record back.
 template <typename QT>
-__global__ void __launch_bounds__(PERM_W * 32) k_pc_perm(const Params p, const Esai e, int R, const uint32_t *__restrict__ bt_in,
-                                                         const float *__restrict__ P_in, const QT *__restrict__ q_in,
-                                                         uint32_t *__restrict__ bt_out, float *__restrict__ P_out,
-                                                         QT *__restrict__ q_out) {
+__global__ void __launch_bounds__(PERM_W * 32) k_pc_perm(const Params p, const Esai e, int R, uint32_t *bt, float *Pr,
+                                                         QT *qr) {
+    const uint32_t *bt_in = bt;
+    const float *P_in = Pr;
+    const QT *q_in = qr;
+    uint32_t *bt_out = bt;
+    float *P_out = Pr;
+    QT *q_out = qr;
     __shared__ uint8_t s_cb[PERM_W][4][32], s_cq[PERM_W][4][32];
     __shared__ uint8_t s_b[PERM_W][128], s_q[PERM_W][128];
     __shared__ uint8_t s_pos[PERM_W][128];  // output slot of record i (within the window)

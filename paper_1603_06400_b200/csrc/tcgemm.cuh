@@ -1060,27 +1060,30 @@ __global__ void k_tc_pack_a(const float *__restrict__ A, int M, int K, int lda, 
     }
 }
 
-// Host: pack B (N x K, row-major, ldb) into pre-split swizzled tiles
-// [ceil(N/128)][nkc][hi, lo][128 x 32].  out must hold ntiles * nkc * 8192 floats.
-// stride = TC_N (disjoint tiles) or TC_PSTRIDE (overlapping tiles of k_tc_gemm<true>);
-// ntiles = ceil(N / 128) resp. ceil((N - 1) / TC_PSTRIDE).
+// Packing of B (N x K) into pre-split swizzled tiles [ntiles][nkc][hi, lo][128 x 32] (k_tc_pack_b
+// above, on the device at create): stride = TC_N (disjoint tiles) or TC_PSTRIDE (overlapping
+// tiles of k_tc_gemm<true>); ntiles = ceil(N / 128) resp. ceil((N - 1) / TC_PSTRIDE).
 inline int tc_ntiles(int N, int stride) { return stride == TC_N ? (N + TC_N - 1) / TC_N : (N - 1 + stride - 1) / stride; }
 // (PAIRS tiles: pairs n = 0 .. N - 2, stride TC_PSTRIDE per tile)
 
-inline void tc_pack_b(const float *B, int N, int K, int ldb, int nkc, float *out, int stride = TC_N) {
-    const int ntiles = tc_ntiles(N, stride);
-    for (int nt = 0; nt < ntiles; nt++)
-        for (int c = 0; c < nkc; c++) {
-            unsigned char *tile = (unsigned char *)(out + ((size_t)nt * nkc + c) * (2 * TC_N * TC_KC));
-            for (int r = 0; r < TC_N; r++)
-                for (int k = 0; k < TC_KC; k++) {
-                    const int n = nt * stride + r, kk = c * TC_KC + k;
-                    const float x = (n < N && kk < K) ? B[(size_t)n * ldb + kk] : 0.0f;
-                    const float h = tf32_hi(x);
-                    *(float *)(tile + tc_swz(r, k)) = h;
-                    *(float *)(tile + TC_OPB + tc_swz(r, k)) = x - h;
-                }
-        }
+// Device version of tc_pack_b: element (n, kk) of B read at B[n * sn + kk * sk] (sn = ldb,
+// sk = 1 for row-major B; sn = 1, sk = ld for B given transposed), one thread per packed
+// element pair (hi, lo); the same tf32 truncation and exact subtraction as the host's.
+__global__ void __launch_bounds__(256) k_tc_pack_b(const float *__restrict__ B, int N, int K, int sn, int sk,
+                                                   int nkc, float *__restrict__ out, int stride) {
+    const int ntiles = stride == TC_N ? (N + TC_N - 1) / TC_N : (N - 1 + stride - 1) / stride;
+    const size_t total = (size_t)ntiles * nkc * TC_N * TC_KC;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % TC_KC), r = (int)((i / TC_KC) % TC_N);
+        const size_t tc = i / (TC_KC * TC_N);  // tile * nkc + chunk
+        const int c = (int)(tc % nkc), nt = (int)(tc / nkc);
+        const int n = nt * stride + r, kk = c * TC_KC + k;
+        const float x = (n < N && kk < K) ? B[(size_t)n * sn + (size_t)kk * sk] : 0.0f;
+        const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+        unsigned char *tile = (unsigned char *)(out + tc * (2 * TC_N * TC_KC));
+        *(float *)(tile + tc_swz(r, k)) = h;
+        *(float *)(tile + TC_OPB + tc_swz(r, k)) = x - h;
+    }
 }
 
 }  // namespace cacsi
