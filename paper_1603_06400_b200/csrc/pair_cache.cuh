@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 // PIPE: the w gathers of chunk c are issued before chunk c - 1 is deposited (one chunk of
 // records and weights kept in registers), so their latency overlaps the next stage wait
 template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool PIPE = false>
-__global__ void __launch_bounds__(PBT_T, PIPE ? 1536 / PBT_T : 1) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
+__global__ void __launch_bounds__(PBT_T, 1536 / PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
     constexpr int PBT_CH = PBT_T * PBT_U;
