@@ -158,7 +158,6 @@ const OptKey kOptKeys[] = {
     {"pcv_pipe", &cacsi::Opts::pcv_pipe, false, 0, 1},
     {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
-    {"pcb_pipe", &cacsi::Opts::pcb_pipe, false, 0, 1},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},

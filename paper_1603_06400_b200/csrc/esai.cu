@@ -1596,8 +1596,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 // 512 threads x 4 records, two stages (measured best of 128/256/512/1024 threads
                 // and 2/3 stages with the vector mapping): ~69 KB with the histogram, 3 CTAs/SM
                 constexpr int U = 4, T = 512, NS = 2;
-                auto kb = E.pc_qb == 2 ? (o.pcb_pipe ? k_pc_bwd_tma<uint16_t, T, U, NS, true> : k_pc_bwd_tma<uint16_t, T, U, NS>)
-                                       : k_pc_bwd_tma<uint32_t, T, U, NS>;
+                auto kb = E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
                 const size_t sm = (size_t)NS * T * U * (8 + E.pc_qb) + 2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 int nb = 0;

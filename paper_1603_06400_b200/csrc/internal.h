@@ -186,7 +186,6 @@ struct Opts {
     int pcv_pipe = 1;         // "pcv_pipe": 0 = the voxel-major forward without software-pipelined record loads
     int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
-    int pcb_pipe = 0;         // "pcb_pipe": 1 = the ring backward issues chunk c's w gathers before depositing c - 1
     int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches

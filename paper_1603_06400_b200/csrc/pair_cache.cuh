@@ -592,10 +592,8 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 // "empty" mbarrier: every warp has read the stage), PBT_NS - 1 chunks ahead of
 // the consumers and across voxel boundaries; the threads only gather w and
 // deposit.  Same deposits and order-free integer sums as k_pc_bwd.
-// PIPE: the w gathers of chunk c are issued before chunk c - 1 is deposited (one chunk of
-// records and weights kept in registers), so their latency overlaps the next stage wait
-template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool PIPE = false>
-__global__ void __launch_bounds__(PBT_T, 1536 / PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS>
+__global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
     constexpr int PBT_CH = PBT_T * PBT_U;
@@ -674,20 +672,6 @@ __global__ void __launch_bounds__(PBT_T, 1536 / PBT_T) k_pc_bwd_tma(const Params
         // slots outside the voxel's range deposit zero (branch-free) into lane-spread bins,
         // not all into one address
         const uint32_t kinv = (uint32_t)(win.x + (tid & 31) % max(1, nwin - 1)) << tb;
-        uint32_t pk[PBT_U];
-        float pP[PBT_U], pw[PBT_U];
-        bool have = false;
-        auto deposit = [&](const uint32_t (&k)[PBT_U], const float (&P)[PBT_U], const float (&wv)[PBT_U]) {
-#pragma unroll
-            for (int u = 0; u < PBT_U; u++) {
-                const int b = (int)(k[u] >> tb);
-                const float av = P[u] * (wv[u] * scale);
-                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
-                CACSI_CHECK(b >= win.x && b + 1 <= win.y);
-                atomicAdd(hv + b, __float2int_rn(av) - x1);
-                atomicAdd(hv + b + 1, x1);
-            }
-        };
         for (long long a = o0 & ~7ll; a < o1; a += PBT_CH) {
             if (tid == 0) produce(consumed + PBT_NS);
             const int st = consumed % PBT_NS;
@@ -738,17 +722,17 @@ __global__ void __launch_bounds__(PBT_T, 1536 / PBT_T) k_pc_bwd_tma(const Params
             consumed++;
             float wq[PBT_U];
 #pragma unroll
-            for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]);
-            if (PIPE) {
-                if (have) deposit(pk, pP, pw);
+            for (int u = 0; u < PBT_U; u++) wq[u] = __ldg(w + q[u]) * scale;
 #pragma unroll
-                for (int u = 0; u < PBT_U; u++) pk[u] = k[u], pP[u] = P[u], pw[u] = wq[u];
-                have = true;
-            } else {
-                deposit(k, P, wq);
+            for (int u = 0; u < PBT_U; u++) {
+                const int b = (int)(k[u] >> tb);
+                const float av = P[u] * wq[u];
+                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                CACSI_CHECK(b >= win.x && b + 1 <= win.y);
+                atomicAdd(hv + b, __float2int_rn(av) - x1);
+                atomicAdd(hv + b + 1, x1);
             }
         }
-        if (PIPE && have) deposit(pk, pP, pw);
         __syncthreads();
         const float unit = scale > 0.0f ? (float)(bound / 1073741824.0) : 0.0f;
         // whole rows (zeros outside the window): writing only the tile's chunk range that

@@ -73,21 +73,3 @@ def test_pipelined_forward_bitwise(ci):
         out.append(g)
     assert torch.equal(out[0], out[1])
     G.close()
-
-
-@pytest.mark.parametrize("ci", [1, 2])
-def test_pipelined_backward_bitwise(ci):
-    """Option pcb_pipe=1 (the ring backward issues the next chunk's w gathers before it
-    deposits the current one) adds the same integers: bit-identical."""
-    cfg = make_config(ci)
-    G = P.Geometry(cfg.desc())
-    w = torch.as_tensor(np.random.default_rng(5).uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
-    out = []
-    for mode in (0, 1):
-        G.set_option("pcb_pipe", mode)
-        b = torch.empty(G.f_shape, device="cuda")
-        G.backward(w, b)
-        torch.cuda.synchronize()
-        out.append(b)
-    assert torch.equal(out[0], out[1])
-    G.close()
