@@ -145,6 +145,7 @@ const OptKey kOptKeys[] = {
     {"direct", &cacsi::Opts::direct, true, 0, 1},
     {"pc_plain", &cacsi::Opts::pc_plain, true, 0, 1},
     {"pc_segwin", &cacsi::Opts::pc_segwin, true, 0, 1},
+    {"pc_win", &cacsi::Opts::pc_win, true, 128, 512},
     {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
     {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
@@ -239,6 +240,7 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
     cacsi::Opts opt;
     st = parse_opts(options, opt);
     if (st != CACSI_OK) return st;
+    if (opt.pc_win != 128 && opt.pc_win != 256 && opt.pc_win != 512) return CACSI_ERR_INVALID;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         cudaGetLastError();

@@ -1178,7 +1178,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         if (e == cudaSuccess) {
             e = cudaMemset(tot, 0, 2 * sizeof(long long));
             k_pc_count<<<8 * sm_count(g->device), 256>>>(p, E, cnt, nl);
-            k_pc_pad<<<8 * sm_count(g->device), 256>>>(p, segR, cnt, tot);
+            k_pc_pad<<<8 * sm_count(g->device), 256>>>(p, segR, g->opt.pc_win, cnt, tot);
             if (e == cudaSuccess)
                 e = cub::DeviceScan::ExclusiveSum(tmp, tmp_b, cnt, (long long *)g->d_pc_off, (int)(nl + 1));
             if (e == cudaSuccess) e = cudaMemcpy(ht, tot, sizeof(ht), cudaMemcpyDeviceToHost);  // syncs
@@ -1236,12 +1236,20 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                 // separate cells-only copy for the backward measured no faster)
                 {
                     const int gr2 = 8 * sm_count(g->device);
-                    if (jyb == 2)
-                        k_pc_perm<uint16_t><<<gr2, PERM_W * 32>>>(p, E, segR, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P,
-                                                                  (uint16_t *)g->d_pc_q);
-                    else
-                        k_pc_perm<uint32_t><<<gr2, PERM_W * 32>>>(p, E, segR, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P,
-                                                                  (uint32_t *)g->d_pc_q);
+                    uint32_t *kb = (uint32_t *)g->d_pc_bt;
+                    float *Pb = (float *)g->d_pc_P;
+                    const int wn = g->opt.pc_win;
+                    if (jyb == 2) {
+                        uint16_t *qb = (uint16_t *)g->d_pc_q;
+                        if (wn == 512) k_pc_perm<uint16_t, 512><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                        else if (wn == 256) k_pc_perm<uint16_t, 256><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                        else k_pc_perm<uint16_t, 128><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                    } else {
+                        uint32_t *qb = (uint32_t *)g->d_pc_q;
+                        if (wn == 512) k_pc_perm<uint32_t, 512><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                        else if (wn == 256) k_pc_perm<uint32_t, 256><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                        else k_pc_perm<uint32_t, 128><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
+                    }
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) return e;

@@ -172,6 +172,7 @@ struct Opts {
     int direct = 0;           // "direct": 1 = per-term kernels instead of ESAI
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
+    int pc_win = 128;         // "pc_win": records per bank-aware permutation window (128, 256, 512)
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     // per call (cacsi_set_option may change them between calls)

@@ -61,9 +61,9 @@ __global__ void k_pc_count(const Params p, const Esai e, long long *__restrict__
 }
 
 // segment padding: the last list of each (voxel, block of R rows) segment gets the records
-// that round the segment up to a multiple of 128 (R = 0: no padding); tot[0] += open pairs,
+// that round the segment up to a multiple of win (R = 0: no padding); tot[0] += open pairs,
 // tot[1] += records incl. padding (one warp per segment)
-__global__ void k_pc_pad(const Params p, int R, long long *__restrict__ cnt, long long *tot) {
+__global__ void k_pc_pad(const Params p, int R, int win, long long *__restrict__ cnt, long long *tot) {
     const int Rs = R > 0 ? R : p.det_nx;
     const int nseg_v = (p.det_nx + Rs - 1) / Rs;
     const size_t nseg = (size_t)p.n_vox * nseg_v;
@@ -77,7 +77,7 @@ __global__ void k_pc_pad(const Params p, int R, long long *__restrict__ cnt, lon
         for (int i = lane; i < nlst; i += 32) c += cnt[l0 + i];
         c = __reduce_add_sync(0xFFFFFFFFu, (unsigned)c);  // a segment holds < 2^32 records
         if (lane == 0) {
-            const long long pad = R > 0 ? ((c + 127) & ~127ll) - c : 0;
+            const long long pad = R > 0 ? ((c + win - 1) / win) * win - c : 0;
             cnt[l0 + nlst - 1] += pad;
             atomicAdd((unsigned long long *)tot, (unsigned long long)c);
             atomicAdd((unsigned long long *)(tot + 1), (unsigned long long)(c + pad));
@@ -151,56 +151,54 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
 // state in local memory and read the window uncoalesced: ~108 ms per geometry on
 // config 2.)
 constexpr int PERM_W = 8;  // warps per CTA
+// WIN (128, 256 or 512) records per window = WIN / 32 groups: group g = (warp g / 4 of the
+// WIN / 128 warps that stream the window, record slot g % 4 of every lane's four); a wider
+// window gives the greedy more records to spread over the banks (option pc_win).
 // In place: a warp reads its whole window into registers before it writes any record back.
-template <typename QT>
+template <typename QT, int WIN>
 __global__ void __launch_bounds__(PERM_W * 32) k_pc_perm(const Params p, const Esai e, int R, uint32_t *bt, float *Pr,
                                                          QT *qr) {
-    const uint32_t *bt_in = bt;
-    const float *P_in = Pr;
-    const QT *q_in = qr;
-    uint32_t *bt_out = bt;
-    float *P_out = Pr;
-    QT *q_out = qr;
-    __shared__ uint8_t s_cb[PERM_W][4][32], s_cq[PERM_W][4][32];
-    __shared__ uint8_t s_b[PERM_W][128], s_q[PERM_W][128];
-    __shared__ uint8_t s_pos[PERM_W][128];  // output slot of record i (within the window)
+    constexpr int G = WIN / 32, PL = WIN / 32;  // groups; records per lane
+    __shared__ uint8_t s_cb[PERM_W][G][32], s_cq[PERM_W][G][32];
+    __shared__ uint8_t s_b[PERM_W][WIN], s_q[PERM_W][WIN];
+    __shared__ uint16_t s_pos[PERM_W][WIN];  // output slot of record i (within the window)
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int nseg_v = (p.det_nx + R - 1) / R;
     const size_t nseg = (size_t)p.n_vox * nseg_v;
-    // windows: (segment, 128-record window of it); segments are whole windows (padded)
+    // windows: (segment, WIN-record window of it); segments are whole windows (padded)
     for (size_t sg = blockIdx.x * (size_t)PERM_W + wl; sg < nseg; sg += (size_t)gridDim.x * PERM_W) {
         const int v = (int)(sg / nseg_v), sgi = (int)(sg % nseg_v);
         const size_t l0 = (size_t)v * p.det_nx;
         const long long a = e.pc_off[l0 + sgi * R], z = e.pc_off[l0 + min(p.det_nx, (sgi + 1) * R)];
-        for (long long w0 = a; w0 < z; w0 += 128) {
-            const int n = (int)min(128ll, z - w0), cap = n / 4;
-            uint32_t k[4];
-            float P[4];
-            QT q[4];
+        for (long long w0 = a; w0 < z; w0 += WIN) {
+            const int n = (int)min((long long)WIN, z - w0), cap = n / G;
+            uint32_t k[PL];
+            float P[PL];
+            QT q[PL];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < PL; u++) {
                 const int i = lane + 32 * u;
                 if (i < n) {
-                    k[u] = bt_in[w0 + i];
-                    P[u] = P_in[w0 + i];
-                    q[u] = q_in[w0 + i];
+                    k[u] = bt[w0 + i];
+                    P[u] = Pr[w0 + i];
+                    q[u] = qr[w0 + i];
                     s_b[wl][i] = (uint8_t)((k[u] >> e.pc_tbits) & 31u);
                     s_q[wl][i] = (uint8_t)((uint32_t)q[u] & 31u);
                 }
             }
 #pragma unroll
-            for (int g = 0; g < 4; g++) s_cb[wl][g][lane] = 0, s_cq[wl][g][lane] = 0;
+            for (int g = 0; g < G; g++) s_cb[wl][g][lane] = 0, s_cq[wl][g][lane] = 0;
             __syncwarp();
-            int fill = 0;  // lane g < 4: records placed in group g
+            int fill = 0;  // lane g < G: records placed in group g
             for (int i = 0; i < n; i++) {
                 const int b = s_b[wl][i], qq = s_q[wl][i];
-                int sc = 1 << 28;
-                if (lane < 4 && fill < cap) sc = 2 * s_cb[wl][lane][b] + s_cq[wl][lane][qq];
-                // argmin over lanes 0..3, lowest lane on ties: key = score * 4 + lane
-                const int key = __reduce_min_sync(0xFFFFFFFFu, lane < 4 ? sc * 4 + lane : 0x7FFFFFFF);
-                const int best = key & 3;
+                int sc = 1 << 24;
+                if (lane < G && fill < cap) sc = 2 * s_cb[wl][lane][b] + s_cq[wl][lane][qq];
+                // argmin over lanes 0..G-1, lowest lane on ties: key = score * 32 + lane
+                const int key = __reduce_min_sync(0xFFFFFFFFu, lane < G ? sc * 32 + lane : 0x7FFFFFFF);
+                const int best = key & 31;
                 if (lane == best) {
-                    s_pos[wl][i] = (uint8_t)(4 * fill + best);  // group j = the j-th of every lane's 4
+                    s_pos[wl][i] = (uint16_t)(128 * (best >> 2) + 4 * fill + (best & 3));
                     fill++;
                     s_cb[wl][best][b]++;
                     s_cq[wl][best][qq]++;
@@ -208,13 +206,13 @@ __global__ void __launch_bounds__(PERM_W * 32) k_pc_perm(const Params p, const E
                 __syncwarp();
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < PL; u++) {
                 const int i = lane + 32 * u;
                 if (i < n) {
                     const long long o = w0 + s_pos[wl][i];
-                    bt_out[o] = k[u];
-                    P_out[o] = P[u];
-                    q_out[o] = q[u];
+                    bt[o] = k[u];
+                    Pr[o] = P[u];
+                    qr[o] = q[u];
                 }
             }
             __syncwarp();

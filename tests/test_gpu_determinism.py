@@ -73,3 +73,21 @@ def test_pipelined_forward_bitwise(ci):
         out.append(g)
     assert torch.equal(out[0], out[1])
     G.close()
+
+
+@pytest.mark.parametrize("win", [256, 512])
+def test_permutation_window_bitwise(win):
+    """Option pc_win (the bank-aware permutation over 256- or 512-record windows,
+    segments padded to the window) moves records only within windows and adds padding
+    records with P = 0: the operators give the same bits as the default."""
+    cfg = make_config(1)
+    G, Gw = P.Geometry(cfg.desc()), P.Geometry(cfg.desc(), options=f"pc_win={win}")
+    assert Gw.query("pair_cache_padded_records") >= G.query("pair_cache_padded_records")
+    f = torch.as_tensor(cfg.f).cuda()
+    w = torch.as_tensor(np.random.default_rng(6).uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
+    for H in (G, Gw):
+        H.g, H.b = torch.empty(G.g_shape, device="cuda"), torch.empty(G.f_shape, device="cuda")
+        H.forward(f, H.g)
+        H.backward(w, H.b)
+    torch.cuda.synchronize()
+    assert torch.equal(G.g, Gw.g) and torch.equal(G.b, Gw.b)
