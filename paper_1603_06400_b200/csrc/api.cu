@@ -161,6 +161,7 @@ const OptKey kOptKeys[] = {
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
+    {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},
 };
 

@@ -301,6 +301,171 @@ __global__ void __launch_bounds__(896, 1) k_er_fwd(const Params p, const ErCache
     }
 }
 
+// Compacted forward (option er_fwd=1): items (block of F2_R pixels, segment of F2_VS * 128
+// voxels); per chunk of 32 voxels the CTA scatters the chunk's records of its pixels into a
+// shared (voxel x pixel) tile and appends each record's pixel to its voxel's list (shared
+// atomic slot -- the order within a voxel's list does not matter: its pixels are distinct,
+// and voxels are taken in order, so every sum is accumulated in voxel order); then every
+// warp walks every voxel's list with LANES = the voxel's OPEN pairs (no closed-pair slots)
+// and adds its energy blocks (4 energies each, blocks w, w + 8, ...) into the item's shared
+// accumulators acc[k][pixel] (warps own disjoint energies: no races).  fp32 partial images
+// per segment, summed in fp64 in a fixed order by k_er_fsum.
+constexpr int F2_R = 128, F2_RS = F2_R + 1;  // pixels per item; accumulator row stride (bank spread, pad column)
+constexpr int F2_VS = 16;                    // voxel blocks of kErVB per segment (2048 voxels)
+constexpr int F2_W = 8;                      // warps
+template <int NB>
+__global__ void __launch_bounds__(F2_W * 32, 1) k_er_fwd2(const Params p, const ErCache c, const float2 *__restrict__ tab,
+                                                          int n_pb, int n_items, float *__restrict__ part) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int NT = c.nt, tabw = ER_VC * NT, KP = 4 * ((p.ne + 3) / 4);
+    float2 *tabs = (float2 *)sm;                                 // [2][ER_VC * NT]
+    float *acc = (float *)(tabs + 2 * tabw);                     // [KP][F2_RS]
+    float2 *pt = (float2 *)(acc + (size_t)KP * F2_RS + (KP * F2_RS & 1));  // [ER_VC][F2_R]
+    uint8_t *lst = (uint8_t *)(pt + ER_VC * F2_R);               // [ER_VC][F2_R]
+    int *cnt = (int *)(lst + ER_VC * F2_R);                      // [2][ER_VC]
+    int *rs = cnt + 2 * ER_VC;                                   // [F2_R] record start (relative to off[q])
+    int *rn = rs + F2_R;                                         // [F2_R] record end
+    int *cur = rn + F2_R;                                        // [F2_R] cursor
+    uint64_t *full = (uint64_t *)(((uintptr_t)(cur + F2_R) + 7) & ~(uintptr_t)7);  // [2]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nbk = KP / 4;
+    const int segv = F2_VS * kErVB;
+    // this warp's energy blocks b = warp + F2_W i: alpha per energy (padding: 1e30) and the
+    // first / last real alpha per block (the exact skip test)
+    float al[NB][4], alo[NB], ahi[NB];
+#pragma unroll
+    for (int i = 0; i < NB; i++) {
+        const int b = warp + F2_W * i;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int k = 4 * b + j;
+            al[i][j] = (b < nbk && k < p.ne) ? __ldg(&p.energy[k].x) : 1e30f;
+        }
+        alo[i] = al[i][0];
+        ahi[i] = (b < nbk) ? __ldg(&p.energy[min(p.ne - 1, 4 * b + 3)].x) : 1e30f;
+    }
+    const float nb = p.nb, qm = p.qm;
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(full + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    // chunks of this CTA in sequence (gc): item it, chunk ch
+    const int nsegs = (p.n_vox + segv - 1) / segv;
+    auto seg_chunks = [&](int it) {
+        const int sg = it / n_pb;
+        const int V0 = sg * segv, V1 = min(p.n_vox, V0 + segv);
+        return (V1 - V0 + ER_VC - 1) / ER_VC;
+    };
+    // issue chunk ch of item it into buffer (gc & 1)
+    auto issue = [&](int it, int ch, long long gc) {
+        const int V0 = (it / n_pb) * segv;
+        const int v0 = V0 + ch * ER_VC, nv = min(ER_VC, min(p.n_vox, V0 + segv) - v0);
+        const uint32_t bytes = (uint32_t)nv * NT * 8u;
+        const uint32_t mb = smem_u32(full + (gc & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         smem_u32(tabs + (size_t)(gc & 1) * tabw)),
+                     "l"(tab + (size_t)v0 * NT), "r"(bytes), "r"(mb)
+                     : "memory");
+    };
+    (void)nsegs;
+    __syncthreads();
+    if (tid == 0 && (int)blockIdx.x < n_items) issue(blockIdx.x, 0, 0);
+    long long gc = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int sg = it / n_pb, pb = it % n_pb;
+        const int P0 = pb * F2_R, npx = min(F2_R, p.n_det - P0);
+        const int V0 = sg * segv, vb0 = V0 / kErVB, vb1 = min(c.nvb, vb0 + F2_VS);
+        const int nch = seg_chunks(it);
+        __syncthreads();  // the previous item's output pass is done
+        for (int i = tid; i < KP * F2_RS; i += blockDim.x) acc[i] = 0.0f;
+        for (int i = tid; i < F2_R; i += blockDim.x) {
+            int a = 0, z = 0;
+            if (i < npx) {
+                a = (int)__ldg(c.boff + (size_t)vb0 * p.n_det + P0 + i);
+                z = (int)__ldg(c.boff + (size_t)vb1 * p.n_det + P0 + i);
+            }
+            rs[i] = a, rn[i] = z, cur[i] = a;
+        }
+        for (int i = tid; i < 2 * ER_VC; i += blockDim.x) cnt[i] = 0;
+        for (int ch = 0; ch < nch; ch++, gc++) {
+            const int v0 = V0 + ch * ER_VC, v_end = v0 + ER_VC;
+            const int par = ch & 1;
+            __syncthreads();  // previous chunk's lists / tile / table buffer reads are done
+            if (tid == 0) {
+                // next chunk of this CTA's sequence (this item's next, or the next item's first)
+                if (ch + 1 < nch) issue(it, ch + 1, gc + 1);
+                else if (it + (int)gridDim.x < n_items) issue(it + gridDim.x, 0, gc + 1);
+            }
+            if (tid < ER_VC) cnt[(par ^ 1) * ER_VC + tid] = 0;  // the next chunk's list counts
+            // fill: warp w takes pixels w, w + 8, ...; lanes = the pixel's next 32 records
+            for (int px = warp; px < npx; px += F2_W) {
+                const long long b0 = __ldg(c.off + P0 + px);
+                const int idx = cur[px] + lane;
+                uint32_t vw = 0xFFFFFFFFu;
+                if (idx < rn[px]) vw = __ldg(c.vw + b0 + idx);
+                const bool rec = vw != 0xFFFFFFFFu && (int)(vw & 0xFFFFu) < v_end;
+                const int n = __popc(__ballot_sync(FULL, rec));
+                if (rec) {
+                    const int vl = (int)(vw & 0xFFFFu) - v0;
+                    pt[vl * F2_R + px] = make_float2(__ldg(c.P + b0 + idx), __ldg(c.s + b0 + idx));
+                    lst[vl * F2_R + atomicAdd(cnt + par * ER_VC + vl, 1)] = (uint8_t)px;
+                }
+                __syncwarp();
+                if (lane == 0) cur[px] += n;
+            }
+            __syncthreads();
+            mbar_wait(smem_u32(full + (gc & 1)), (uint32_t)((gc >> 1) & 1));
+            const uint32_t tb0 = smem_u32(tabs + (size_t)(gc & 1) * tabw) + (uint32_t)c.nlo * 8u -
+                                 (uint32_t)kMagicBits * 8u;
+            const int nv = min(ER_VC, p.n_vox - v0);
+            for (int vl = 0; vl < nv; vl++) {
+                const int n = cnt[par * ER_VC + vl];
+                const uint32_t tb = tb0 + (uint32_t)(vl * NT) * 8u;
+                for (int r = 0; r < n; r += 32) {
+                    const bool act = r + lane < n;
+                    const int px = act ? lst[vl * F2_R + r + lane] : F2_R;  // inactive lanes: the pad column
+                    const float2 ps = act ? pt[vl * F2_R + px] : make_float2(0.0f, 0.0f);
+                    float *ap = acc + px;
+#pragma unroll
+                    for (int i = 0; i < NB; i++) {
+                        const bool in = act && fmaf(ahi[i], ps.y, nb) > -1.5f && fmaf(alo[i], ps.y, nb) < qm;
+                        if (!__any_sync(FULL, in)) continue;
+                        const int k0 = 4 * (warp + F2_W * i);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const float u = fminf(fmaf(al[i][j], ps.y, nb), qm);
+                            const float vm = u + kMagic;
+                            const float tt = u - (vm - kMagic);
+                            const float2 e = lds_f2(tb + (uint32_t)__float_as_int(vm) * 8u);
+                            float *a = ap + (k0 + j) * F2_RS;
+                            *a = fmaf(ps.x, fmaf(tt, e.y, e.x), *a);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // the segment's fp32 partial image of this pixel block, [q][k] (coalesced)
+        float *o = part + ((size_t)sg * p.n_det + P0) * p.ne;
+        for (int i = tid; i < npx * p.ne; i += blockDim.x) {
+            const int q = i / p.ne, k = i - q * p.ne;
+            o[i] = acc[k * F2_RS + q];
+        }
+    }
+}
+
+// g[q][k] = c_k sum_seg part[seg][q][k] (fp64, segments in order)
+__global__ void k_er_fsum(const Params p, const float *__restrict__ part, int nseg, float *__restrict__ g) {
+    const size_t n = (size_t)p.n_det * p.ne;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nseg; k++) s += (double)part[(size_t)k * n + i];
+        g[i] = (float)((double)__ldg(&p.energy[i % p.ne].y) * s);
+    }
+}
+
 // -------------------------------------------------------------- backward ----
 // max |w| over the pixels with at least one record (only their weights deposit)
 __global__ void __launch_bounds__(1024) k_er_absmax(const Params p, const long long *__restrict__ off,
@@ -466,6 +631,21 @@ int sms(int dev) {
     return n;
 }
 
+size_t er_fwd2_smem(const Params &p, const ErCache &c) {
+    const int KP = 4 * ((p.ne + 3) / 4);
+    return (size_t)2 * ER_VC * c.nt * 8 + ((size_t)KP * F2_RS + 1) * 4 + (size_t)ER_VC * F2_R * 8 + ER_VC * F2_R +
+           2 * ER_VC * 4 + 3 * F2_R * 4 + 64;
+}
+template <int NB>
+cudaError_t er_fwd2_launch(const cacsi_geometry *g, const float2 *tab, float *part, int n_pb, int n_items,
+                           cudaStream_t s) {
+    const size_t smem = er_fwd2_smem(g->p, g->er);
+    cudaFuncSetAttribute(k_er_fwd2<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    k_er_fwd2<NB><<<std::min(n_items, nsm), F2_W * 32, smem, s>>>(g->p, g->er, tab, n_pb, n_items, part);
+    return cudaGetLastError();
+}
 size_t er_bwd_smem(const Params &p) { return (size_t)(ER_BT / 32) * 36 * 16 + (size_t)kErVB * (p.nq + 4) * 4 + kErVB * 4; }
 int er_fwd_pg(int nr) { return std::max(1, std::min(8, 28 / nr)); }
 size_t er_fwd_smem(const ErCache &c, int nr) {
@@ -633,11 +813,31 @@ cudaError_t er_forward(const cacsi_geometry *g, const float *f, float *out, cuda
         KScope kt_(g, s, "k_er_tab");
         k_er_tab<<<4 * sms(g->device), 256, 0, s>>>(p, c.nlo, c.nt, f, tab);
     }
-    {
+    if (g->opt.er_fwd == 1 && er_fwd2_smem(p, c) <= 227 * 1024) {
+        const int segv = F2_VS * kErVB, nseg = (p.n_vox + segv - 1) / segv;
+        const int n_pb = (p.n_det + F2_R - 1) / F2_R;
+        float *part = nullptr;
+        e = cudaMallocAsync(&part, (size_t)nseg * p.n_det * p.ne * sizeof(float), s);
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_er_fwd");
+            const int nbk = (p.ne + 3) / 4, NB = (nbk + F2_W - 1) / F2_W;
+            e = NB <= 1 ? er_fwd2_launch<1>(g, tab, part, n_pb, n_pb * nseg, s)
+                : NB == 2 ? er_fwd2_launch<2>(g, tab, part, n_pb, n_pb * nseg, s)
+                : NB == 3 ? er_fwd2_launch<3>(g, tab, part, n_pb, n_pb * nseg, s)
+                          : er_fwd2_launch<4>(g, tab, part, n_pb, n_pb * nseg, s);
+        }
+        if (e == cudaSuccess) {
+            KScope kt_(g, s, "k_er_fsum");
+            k_er_fsum<<<8 * sms(g->device), 256, 0, s>>>(p, part, nseg, out);
+            e = cudaGetLastError();
+        }
+        if (part) cudaFreeAsync(part, s);
+        *launches += 3;
+    } else {
         KScope kt_(g, s, "k_er_fwd");
         e = er_fwd_any(g, tab, out, s);
+        *launches += 2;
     }
-    *launches += 2;
     cudaFreeAsync(tab, s);
     return e == cudaSuccess ? cudaGetLastError() : e;
 }

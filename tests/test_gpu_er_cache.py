@@ -52,6 +52,10 @@ def test_er_cache_vs_oracle_and_direct(over):
     assert_parity(gb, O.backward(w), f"er cache {over} backward")
     assert rel_l2(gf, gpu_forward(D, f)) < 1e-6
     assert rel_l2(gb, gpu_backward(D, w)) < 2e-6
+    G.set_option("er_fwd", 1)  # the compacted forward k_er_fwd2
+    gf2 = gpu_forward(G, f)
+    assert_parity(gf2, O.forward(f), f"er cache compacted {over} forward")
+    assert rel_l2(gf2, gf) < 1e-6
 
 
 def test_er_cache_records_are_open_pairs():
@@ -86,7 +90,11 @@ def test_er_cache_config4_sampled():
     assert G.query("er_cache_records") > 0
     g = gpu_forward(G, cfg.f).reshape(cfg.n_det, cfg.ne)
     pix = _sample(cfg.n_det, 2048, 43)
-    assert_parity(g[pix], O.forward_pixels(cfg.f, pix), "c4 er-cache forward, 2048 pixels")
+    ref = O.forward_pixels(cfg.f, pix)
+    assert_parity(g[pix], ref, "c4 er-cache forward, 2048 pixels")
+    G.set_option("er_fwd", 1)
+    g2 = gpu_forward(G, cfg.f).reshape(cfg.n_det, cfg.ne)
+    assert_parity(g2[pix], ref, "c4 er-cache compacted forward, 2048 pixels")
     w = rnd(G.g_shape, 4, 10)
     b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
     vox = _sample(cfg.n_vox, 64, 44)
