@@ -354,7 +354,7 @@ def run_gpu(args):
         nrec = G.query("pair_cache_records")
         tab = cfg.n_vox * ldw * 4 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
         rb = G.query("pair_cache_record_bytes")
-        bytes_ = float(rb) * nrec + 8.0 * cfg.n_vox * cfg.det_nx + tab
+        bytes_ = float(rb) * nrec + 8.0 * cfg.n_vox * cfg.det_nx + tab + float(G.query("pair_cache_window_base_bytes"))
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         ach = bytes_ / (kern[kd]["avg_ms"] / 1e3) / 1e9
         roofline_hbm = {"bound": "hbm", "kernel": kd, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
@@ -362,8 +362,8 @@ def run_gpu(args):
                         "avg_launch_ms": kern[kd]["avg_ms"],
                         "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else
                         "fallback 6650 GB/s (B200_PROFILING.md)",
-                        "bytes_note": f"{rb} B per open pair (pair record) + list offsets + the gathered table "
-                                      "once (DESIGN.md §8)"}
+                        "bytes_note": f"{rb} B per record (pair cache, incl. padding) + 2 B per 128-record window "
+                                      "(pixel bases) + list offsets + the gathered table once (DESIGN.md §8)"}
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "r2k_dram_traffic.json")))["kernels"]
             if kd in tr:

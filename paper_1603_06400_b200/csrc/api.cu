@@ -127,7 +127,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_pc_qbase};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -146,6 +146,7 @@ const OptKey kOptKeys[] = {
     {"pc_plain", &cacsi::Opts::pc_plain, true, 0, 1},
     {"pc_segwin", &cacsi::Opts::pc_segwin, true, 0, 1},
     {"pc_win", &cacsi::Opts::pc_win, true, 128, 512},
+    {"pc_q8", &cacsi::Opts::pc_q8, true, 0, 1},
     {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
     {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
@@ -965,7 +966,9 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "pair_cache_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_nopen : 0;
     if (!strcmp(key, "pair_cache_padded_records")) return g->esai.enabled && g->esai.pc ? g->esai.pc_n : 0;
     if (!strcmp(key, "pair_cache_record_bytes"))
-        return g->esai.enabled && g->esai.pc ? 2 * (long long)sizeof(float) + g->esai.pc_qb : 0;
+        return g->esai.enabled && g->esai.pc ? 2 * (long long)sizeof(float) + (g->esai.pc_q8 ? 0 : g->esai.pc_qb) : 0;
+    if (!strcmp(key, "pair_cache_window_base_bytes"))  // the 8-byte format's per-window pixel bases
+        return g->esai.enabled && g->esai.pc && g->esai.pc_q8 ? 2 * (g->esai.pc_n / 128) : 0;
     if (!strcmp(key, "pair_cache_tau_bits")) return g->esai.enabled && g->esai.pc ? g->esai.pc_tbits : 0;
     if (!strcmp(key, "pair_cache_fwd_row_blocks"))
         return g->esai.enabled && g->esai.pc ? cacsi::pcv_row_blocks(g) : 0;

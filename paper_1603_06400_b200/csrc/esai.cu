@@ -1267,8 +1267,43 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     e = cudaDeviceSynchronize();
                 }
                 if (e != cudaSuccess) return e;
-                clk.mark(5);  // per-segment windows
                 if (g->opt.pc_segwin) E.pc_segwin = (const int2 *)g->d_pc_segwin;
+                // 8-byte records: a 9-bit pixel offset per record and a base per 128-record
+                // window, if every window's pixel span fits and tau keeps >= 9 bits
+                E.pc_q8 = 0;
+                E.pc_tb8 = E.pc_tbits - 9;
+                if (g->opt.pc_q8 && jyb == 2 && E.pc_tb8 >= 9 && (nrec % 128) == 0) {
+                    const long long nwin = nrec / 128;
+                    unsigned *span = nullptr;
+                    unsigned hs = 0;
+                    e = cudaMalloc(&span, sizeof(unsigned));
+                    if (e == cudaSuccess) e = cudaMemset(span, 0, sizeof(unsigned));
+                    if (e == cudaSuccess) {
+                        k_pc_qspan<<<8 * sm_count(g->device), 256>>>(nwin, (const uint16_t *)g->d_pc_q, span);
+                        e = cudaMemcpy(&hs, span, sizeof(unsigned), cudaMemcpyDeviceToHost);
+                    }
+                    cudaFree(span);
+                    if (e == cudaSuccess && hs <= 511) {
+                        // + 16 bases of slack: the backward reads one base per warp of a chunk
+                        e = cudaMalloc(&g->d_pc_qbase, (size_t)(nwin + 16) * sizeof(uint16_t));
+                        if (e == cudaSuccess) e = cudaMemset(g->d_pc_qbase, 0, (size_t)(nwin + 16) * sizeof(uint16_t));
+                        if (e == cudaSuccess) {
+                            k_pc_pack8<<<8 * sm_count(g->device), 256>>>(nwin, E.pc_tbits, E.pc_tb8,
+                                                                          (const uint16_t *)g->d_pc_q, (uint32_t *)g->d_pc_bt,
+                                                                          (uint16_t *)g->d_pc_qbase);
+                            e = cudaDeviceSynchronize();
+                        }
+                        if (e == cudaSuccess) {
+                            cudaFree(g->d_pc_q);
+                            g->d_pc_q = nullptr;
+                            E.pc_q = E.pcb_q = nullptr;
+                            E.pc_qbase = (const uint16_t *)g->d_pc_qbase;
+                            E.pc_q8 = 1;
+                        }
+                    }
+                    if (e != cudaSuccess) return e;
+                }
+                clk.mark(5);  // per-segment windows, 8-byte packing
             }
             E.pc = 1;
         }
@@ -1474,8 +1509,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int U = o.pcv_u;  // records per thread per step
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
-                const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536;
-                auto kf = E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true>
+                const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536 && !E.pc_q8;
+                auto kf = E.pc_q8 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, true>
+                                               : k_pc_fwd_v<uint16_t, 4, 512, false, true, true>)
+                        : E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true>
                                                             : o.pcv_pipe ? k_pc_fwd_v<uint16_t, 4, 1024, false, true>
                                                                          : k_pc_fwd_v<uint16_t, 4, 1024>)
                                                     : U == 8 ? k_pc_fwd_v<uint16_t, 8, 512>
@@ -1600,12 +1637,13 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         if (E.pc && pmask == nullptr) {
             KScope kt_(g, s, "k_pc_bwd");
             const size_t hs = (size_t)E.max_win * sizeof(int);
-            if (!o.pc_bwd_flat) {  // pc_bwd_flat: the register-fed kernel (A/B reference)
+            if (!o.pc_bwd_flat || E.pc_q8) {  // pc_bwd_flat: the register-fed kernel (A/B reference, 10-byte records)
                 // 512 threads x 4 records, two stages (measured best of 128/256/512/1024 threads
                 // and 2/3 stages with the vector mapping): ~69 KB with the histogram, 3 CTAs/SM
                 constexpr int U = 4, T = 512, NS = 2;
-                auto kb = E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
-                const size_t sm = (size_t)NS * T * U * (8 + E.pc_qb) + 2 * NS * sizeof(uint64_t) + hs;
+                auto kb = E.pc_q8 ? k_pc_bwd_tma<uint16_t, T, U, NS, true>
+                        : E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
+                const size_t sm = (size_t)NS * T * U * (8 + (E.pc_q8 ? 0 : E.pc_qb)) + 2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 int nb = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, T, sm);

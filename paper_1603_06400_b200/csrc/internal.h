@@ -134,7 +134,13 @@ struct Esai {
     const uint32_t *pcb_bt;
     const float *pcb_P;
     const void *pcb_q;
-    int pc_tbits;             // fraction bits of tau (>= 16)
+    int pc_tbits;             // fraction bits of tau (>= 16); also b's shift in the packed word
+    // 8-byte records (pc_q8): the pixel is stored as a 9-bit offset (bits 0-8) from a per-window
+    // base (pc_qbase, one uint16 per 128-record window) and tau keeps pc_tb8 bits (bits 9 ..),
+    // b stays at bit pc_tbits; the pixel array pc_q is then not kept
+    int pc_q8;
+    int pc_tb8;
+    const uint16_t *pc_qbase;
     int pc_qb;                // bytes per q (2 or 4)
     int stat_win_permille, stat_tile_permille;  // mean voxel window / 128-voxel tile K span, per mille of nb
 };
@@ -173,6 +179,7 @@ struct Opts {
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
     int pc_win = 128;         // "pc_win": records per bank-aware permutation window (128, 256, 512)
+    int pc_q8 = 1;            // "pc_q8": 0 = 10-byte records (P, (b, tau), pixel) instead of the packed 8-byte ones
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     // per call (cacsi_set_option may change them between calls)
@@ -207,7 +214,7 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen;
+        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen, *d_pc_qbase;
     // energy-resolving pair cache (er_cache.cu)
     cacsi::ErCache er;
     void *d_er_off, *d_er_vw, *d_er_P, *d_er_s, *d_er_boff, *d_er_sv;

@@ -327,6 +327,42 @@ __global__ void k_pc_segwin(const Params p, const Esai e, int R, uint32_t *__res
     }
 }
 
+// 8-byte records (build time, after the permutation and the segment windows): one warp per
+// 128-record window.  Pass 1 measures the largest pixel span of a window; if it fits 9 bits,
+// pass 2 rewrites every record word in place as (b << tbits) | (tau8 << 9) | (q - qbase)
+// with tau rounded to tau8 = tbits - 9 bits, and stores the window's base pixel.
+__global__ void k_pc_qspan(long long nwin, const uint16_t *__restrict__ q, unsigned *maxspan) {
+    const int lane = threadIdx.x & 31;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nwin;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const uint2 v = *(const uint2 *)(q + w * 128 + 4 * lane);
+        const unsigned a = v.x & 0xFFFFu, b = v.x >> 16, c = v.y & 0xFFFFu, d = v.y >> 16;
+        const unsigned lo = __reduce_min_sync(0xFFFFFFFFu, min(min(a, b), min(c, d)));
+        const unsigned hi = __reduce_max_sync(0xFFFFFFFFu, max(max(a, b), max(c, d)));
+        if (lane == 0) atomicMax(maxspan, hi - lo);
+    }
+}
+__global__ void k_pc_pack8(long long nwin, int tbits, int tb8, const uint16_t *__restrict__ q, uint32_t *bt,
+                           uint16_t *__restrict__ qbase) {
+    const int lane = threadIdx.x & 31, sh = tbits - tb8;
+    const uint32_t tmax8 = (1u << tb8) - 1u, tmask = (1u << tbits) - 1u;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nwin;
+         w += ((long long)gridDim.x * blockDim.x) >> 5) {
+        const uint2 v = *(const uint2 *)(q + w * 128 + 4 * lane);
+        const unsigned qq[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+        const unsigned lo = __reduce_min_sync(0xFFFFFFFFu, min(min(qq[0], qq[1]), min(qq[2], qq[3])));
+        uint4 k = *(const uint4 *)(bt + w * 128 + 4 * lane);
+        uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t t8 = min(((kk[u] & tmask) + (1u << (sh - 1))) >> sh, tmax8);
+            kk[u] = (kk[u] & ~tmask) | (t8 << 9) | (qq[u] - lo);
+        }
+        *(uint4 *)(bt + w * 128 + 4 * lane) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+        if (lane == 0) qbase[w] = (uint16_t)lo;
+    }
+}
+
 // the W columns a (voxel, row block) segment reads: its own window when the cache
 // recorded one (k_pc_segwin), else the voxel's
 __device__ __forceinline__ int2 seg_window(const Esai &e, int v, int n_rb, int rb) {
@@ -351,7 +387,8 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
 // marker and contribute 0).  An A/B variant (option pc_fwd_geom): DESIGN.md 4.2b.
 // PIPE: the vector record loop is software-pipelined -- each thread's next 4 records are
 // loaded before the current 4 are deposited (two steps of loads in flight per thread).
-template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false>
+// Q8: 8-byte records (pixel = window base + 9-bit offset, tau in bits 9 .. 9 + pc_tb8)
+template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false, bool Q8 = false>
 __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
@@ -365,6 +402,8 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
     const int tb = e.pc_tbits;
     const uint32_t tmask = (1u << tb) - 1u;
     const float tunit = 1.0f / (float)(1u << tb);
+    const uint32_t tmask8 = (1u << e.pc_tb8) - 1u;
+    const float tunit8 = 1.0f / (float)(1u << e.pc_tb8);
     const QT *pq = (const QT *)e.pc_q;
     const bool vec = e.pc_R > 0;  // bank-ordered layout: segments 128-record aligned (vector loads)
     if (tid == 0) {
@@ -444,7 +483,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     CACSI_CHECK(b >= (swin.x & ~3) && b + 1 < (swin.x & ~3) + wcap);
                     CACSI_CHECK(P[u] == 0.0f || (q[u] >= (uint32_t)q0 && q[u] < (uint32_t)(q0 + nacc)));
                     const float wa = wv[b], wb = wv[b + 1];
-                    const float t = (float)(k[u] & tmask) * tunit;
+                    const float t = Q8 ? (float)((k[u] >> 9) & tmask8) * tunit8 : (float)(k[u] & tmask) * tunit;
                     float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
@@ -457,7 +496,10 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                 auto ld = [&](int j) {
                     kv = __ldg((const uint4 *)(kb + j));
                     if (!GEOM) pv = __ldg((const float4 *)(Pb + j));
-                    qv = __ldg((const uint2 *)(qb + j));
+                    if (Q8)  // the warp's 128 records are one window: one base per warp step
+                        qv.x = __ldg(e.pc_qbase + ((o0 + j) >> 7));
+                    else
+                        qv = __ldg((const uint2 *)(qb + j));
                 };
                 if (i < n) ld(i);
                 for (; i < n; i += 4 * PCV_T) {
@@ -469,7 +511,12 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     float P[U];
                     k[0] = ck.x, k[1] = ck.y, k[2] = ck.z, k[3] = ck.w;
                     P[0] = cp.x, P[1] = cp.y, P[2] = cp.z, P[3] = cp.w;
-                    q[0] = cq.x & 0xFFFFu, q[1] = cq.x >> 16, q[2] = cq.y & 0xFFFFu, q[3] = cq.y >> 16;
+                    if (Q8) {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) q[u] = cq.x + (k[u] & 511u);
+                    } else {
+                        q[0] = cq.x & 0xFFFFu, q[1] = cq.x >> 16, q[2] = cq.y & 0xFFFFu, q[3] = cq.y >> 16;
+                    }
                     deposit(k, P, q);
                 }
             } else if (vec) {
@@ -590,19 +637,22 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 // "empty" mbarrier: every warp has read the stage), PBT_NS - 1 chunks ahead of
 // the consumers and across voxel boundaries; the threads only gather w and
 // deposit.  Same deposits and order-free integer sums as k_pc_bwd.
-template <typename QT, int PBT_T, int PBT_U, int PBT_NS>
+// Q8: 8-byte records -- the stage holds (b, tau, pixel offset) and P only; each warp's 128
+// records are one window, whose pixel base it reads once per chunk
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool Q8 = false>
 __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
     constexpr int PBT_CH = PBT_T * PBT_U;
-    constexpr int SB = PBT_CH * (8 + (int)sizeof(QT));
+    constexpr int SB = PBT_CH * (8 + (Q8 ? 0 : (int)sizeof(QT)));
     uint64_t *full = (uint64_t *)(smb + PBT_NS * SB);
     uint64_t *empty = full + PBT_NS;
     int *hist_s = (int *)(empty + PBT_NS);
     const int tid = threadIdx.x;
     const int tb = e.pc_tbits;
-    const uint32_t tmask = (1u << tb) - 1u;
-    const float tunit = 1.0f / (float)(1u << tb);
+    const uint32_t tmask = Q8 ? (1u << e.pc_tb8) - 1u : (1u << tb) - 1u;
+    const float tunit = Q8 ? 1.0f / (float)(1u << e.pc_tb8) : 1.0f / (float)(1u << tb);
+    const int tsh = Q8 ? 9 : 0;  // tau's position in the record word
     const QT *pq = (const QT *)e.pcb_q;
     const bool vec = e.pc_R > 0;  // bank-ordered layout (segments 128-record aligned)
     const float wm = *wmax;
@@ -645,13 +695,14 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             const uint32_t mb = smem_u32(full + st);
             unsigned char *dst = smb + st * SB;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                         "r"(n * (8u + (uint32_t)sizeof(QT))));
+                         "r"(n * (8u + (Q8 ? 0u : (uint32_t)sizeof(QT)))));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                              smem_u32(dst)), "l"(e.pcb_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                              smem_u32(dst + PBT_CH * 4)), "l"(e.pcb_P + pa), "r"(n * 4u), "r"(mb) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                             smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
+            if (!Q8)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                 smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
             pa += PBT_CH;
             issued++;
         }
@@ -687,7 +738,14 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                 const float4 pv = ((const float4 *)(src + PBT_CH * 4))[tid];
                 k[0] = kv.x, k[1] = kv.y, k[2] = kv.z, k[3] = kv.w;
                 P[0] = pv.x, P[1] = pv.y, P[2] = pv.z, P[3] = pv.w;
-                if (sizeof(QT) == 2) {
+                if (Q8) {
+                    // chunks start on window boundaries in the bank-ordered layout: warp w's 128
+                    // records are window (a >> 7) + w (a read past the table's end only for
+                    // slots outside the voxel, which are masked below)
+                    const uint32_t qb = 4 * tid < hi ? __ldg(e.pc_qbase + (a >> 7) + (tid >> 5)) : 0u;
+#pragma unroll
+                    for (int u = 0; u < PBT_U; u++) q[u] = qb + (k[u] & 511u);
+                } else if (sizeof(QT) == 2) {
                     const uint2 qv = ((const uint2 *)(src + PBT_CH * 8))[tid];
                     q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
                 } else {
@@ -725,7 +783,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             for (int u = 0; u < PBT_U; u++) {
                 const int b = (int)(k[u] >> tb);
                 const float av = P[u] * wq[u];
-                const int x1 = __float2int_rn(av * ((float)(k[u] & tmask) * tunit));
+                const int x1 = __float2int_rn(av * ((float)((k[u] >> tsh) & tmask) * tunit));
                 CACSI_CHECK(b >= win.x && b + 1 <= win.y);
                 atomicAdd(hv + b, __float2int_rn(av) - x1);
                 atomicAdd(hv + b + 1, x1);
