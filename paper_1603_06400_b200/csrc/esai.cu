@@ -1284,9 +1284,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     }
                     cudaFree(span);
                     if (e == cudaSuccess && hs <= 511) {
-                        // + 16 bases of slack: the backward reads one base per warp of a chunk
-                        e = cudaMalloc(&g->d_pc_qbase, (size_t)(nwin + 16) * sizeof(uint16_t));
-                        if (e == cudaSuccess) e = cudaMemset(g->d_pc_qbase, 0, (size_t)(nwin + 16) * sizeof(uint16_t));
+                        // + 32 bases of slack: the backward's bulk copy of a chunk's bases reads whole 16-byte groups
+                        e = cudaMalloc(&g->d_pc_qbase, (size_t)(nwin + 32) * sizeof(uint16_t));
+                        if (e == cudaSuccess) e = cudaMemset(g->d_pc_qbase, 0, (size_t)(nwin + 32) * sizeof(uint16_t));
                         if (e == cudaSuccess) {
                             k_pc_pack8<<<8 * sm_count(g->device), 256>>>(nwin, E.pc_tbits, E.pc_tb8,
                                                                           (const uint16_t *)g->d_pc_q, (uint32_t *)g->d_pc_bt,
@@ -1643,7 +1643,8 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 constexpr int U = 4, T = 512, NS = 2;
                 auto kb = E.pc_q8 ? k_pc_bwd_tma<uint16_t, T, U, NS, true>
                         : E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
-                const size_t sm = (size_t)NS * T * U * (8 + (E.pc_q8 ? 0 : E.pc_qb)) + 2 * NS * sizeof(uint64_t) + hs;
+                const size_t sm = (size_t)NS * (T * U * (8 + (E.pc_q8 ? 0 : E.pc_qb)) + (E.pc_q8 ? ((T * U / 128 + 14) & ~7) * 2 : 0)) +
+                                  2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 int nb = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, T, sm);

@@ -179,7 +179,7 @@ struct Opts {
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
     int pc_win = 128;         // "pc_win": records per bank-aware permutation window (128, 256, 512)
-    int pc_q8 = 1;            // "pc_q8": 0 = 10-byte records (P, (b, tau), pixel) instead of the packed 8-byte ones
+    int pc_q8 = 0;            // "pc_q8": 1 = packed 8-byte records (pixel offset from a per-window base, 10-bit tau)
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     // per call (cacsi_set_option may change them between calls)

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                 const long long a0 = __ldg(e.pc_off + l2 + r0), a1 = __ldg(e.pc_off + l2 + r1);
                 l2_prefetch(e.pc_bt + a0, (size_t)(a1 - a0) * sizeof(uint32_t));
                 l2_prefetch(e.pc_P + a0, (size_t)(a1 - a0) * sizeof(float));
-                l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));
+                if (!Q8) l2_prefetch(pq + a0, (size_t)(a1 - a0) * sizeof(QT));  // (Q8: no pixel array)
             }
             mbar_wait(smem_u32(mbar + buf), (uses >> buf) & 1u);
             uses ^= 1u << buf;
@@ -644,7 +644,9 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
     constexpr int PBT_CH = PBT_T * PBT_U;
-    constexpr int SB = PBT_CH * (8 + (Q8 ? 0 : (int)sizeof(QT)));
+    // Q8: + the chunk's window bases, copied from a 16-byte-aligned start (up to 7 extra)
+    constexpr int QBN = (PBT_CH / 128 + 7 + 7) & ~7;
+    constexpr int SB = PBT_CH * (8 + (Q8 ? 0 : (int)sizeof(QT))) + (Q8 ? QBN * 2 : 0);
     uint64_t *full = (uint64_t *)(smb + PBT_NS * SB);
     uint64_t *empty = full + PBT_NS;
     int *hist_s = (int *)(empty + PBT_NS);
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             const uint32_t mb = smem_u32(full + st);
             unsigned char *dst = smb + st * SB;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                         "r"(n * (8u + (Q8 ? 0u : (uint32_t)sizeof(QT)))));
+                         "r"(n * (8u + (Q8 ? 0u : (uint32_t)sizeof(QT))) + (Q8 ? QBN * 2u : 0u)));
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                              smem_u32(dst)), "l"(e.pcb_bt + pa), "r"(n * 4u), "r"(mb) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -703,6 +705,10 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
             if (!Q8)
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                                  smem_u32(dst + PBT_CH * 8)), "l"(pq + pa), "r"(n * (uint32_t)sizeof(QT)), "r"(mb) : "memory");
+            else
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                 smem_u32(dst + PBT_CH * 8)), "l"(e.pc_qbase + ((pa >> 7) & ~7ll)), "r"(QBN * 2u),
+                             "r"(mb) : "memory");
             pa += PBT_CH;
             issued++;
         }
@@ -742,7 +748,8 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     // chunks start on window boundaries in the bank-ordered layout: warp w's 128
                     // records are window (a >> 7) + w (a read past the table's end only for
                     // slots outside the voxel, which are masked below)
-                    const uint32_t qb = 4 * tid < hi ? __ldg(e.pc_qbase + (a >> 7) + (tid >> 5)) : 0u;
+                    const uint16_t *qbs = (const uint16_t *)(src + PBT_CH * 8) + ((a >> 7) & 7);
+                    const uint32_t qb = 4 * tid < hi ? qbs[tid >> 5] : 0u;
 #pragma unroll
                     for (int u = 0; u < PBT_U; u++) q[u] = qb + (k[u] & 511u);
                 } else if (sizeof(QT) == 2) {

@@ -32,14 +32,15 @@ def test_record_count_is_the_open_pair_count(ci):
     Gc, Gn = handles(cfg.desc())
     assert Gc.query("pair_cache_records") == COUNTS[str(cfg.seed)]["open_pairs"]
     assert Gn.query("pair_cache_records") == 0
-    # P (4 B) + (b, tau, 9-bit pixel offset from the window's base) (4 B); the bases: 2 B per
-    # 128-record window
-    assert Gc.query("pair_cache_record_bytes") == 8
-    assert Gc.query("pair_cache_window_base_bytes") == 2 * Gc.query("pair_cache_padded_records") // 128
+    # P (4 B) + packed (b, tau) (4 B) + pixel q (2 B for n_det <= 65536)
+    assert Gc.query("pair_cache_record_bytes") == 8 + (2 if cfg.n_det <= 65536 else 4)
     assert Gc.query("pair_cache_tau_bits") >= 16
-    G10 = P.Geometry(cfg.desc(), options="pc_q8=0")  # the 10-byte format: P, (b, tau), pixel q
-    assert G10.query("pair_cache_record_bytes") == 8 + (2 if cfg.n_det <= 65536 else 4)
-    G10.close()
+    # option pc_q8=1: P (4 B) + (b, tau, 9-bit pixel offset from the window's base) (4 B), and
+    # 2 B of pixel base per 128-record window
+    G8 = P.Geometry(cfg.desc(), options="pc_q8=1")
+    assert G8.query("pair_cache_record_bytes") == 8
+    assert G8.query("pair_cache_window_base_bytes") == 2 * G8.query("pair_cache_padded_records") // 128
+    G8.close()
     Gc.close()
     Gn.close()
 
@@ -149,7 +150,7 @@ def test_8_byte_records_match_10_byte(ci):
     """The packed 8-byte records (tau rounded to fewer bits, the pixel as an offset from the
     window's base) against the 10-byte format and, on config 1, the oracle."""
     cfg = make_config(ci)
-    G8, G10 = P.Geometry(cfg.desc()), P.Geometry(cfg.desc(), options="pc_q8=0")
+    G8, G10 = P.Geometry(cfg.desc(), options="pc_q8=1"), P.Geometry(cfg.desc())
     assert G8.query("pair_cache_record_bytes") == 8 and G10.query("pair_cache_record_bytes") == 10
     w = rnd(G8.g_shape, ci, 74)
     assert_parity(gpu_forward(G8, cfg.f), gpu_forward(G10, cfg.f), f"c{ci} 8-byte vs 10-byte forward", l2=1e-6, mr=1e-5)
