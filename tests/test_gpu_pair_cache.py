@@ -148,13 +148,15 @@ def test_forward_recomputed_P_matches_stored(ci):
 @pytest.mark.parametrize("ci", [1, 2])
 def test_8_byte_records_match_10_byte(ci):
     """The packed 8-byte records (tau rounded to fewer bits, the pixel as an offset from the
-    window's base) against the 10-byte format and, on config 1, the oracle."""
+    window's base) against the 10-byte format and, on config 1, the oracle.  Rounding tau to
+    pc_tb8 bits changes each interpolation weight by up to 2^-(pc_tb8+1) (about 3e-5 at 14 bits),
+    so the two formats are held to each other at the oracle bar, not bit for bit."""
     cfg = make_config(ci)
     G8, G10 = P.Geometry(cfg.desc(), options="pc_q8=1"), P.Geometry(cfg.desc())
     assert G8.query("pair_cache_record_bytes") == 8 and G10.query("pair_cache_record_bytes") == 10
     w = rnd(G8.g_shape, ci, 74)
-    assert_parity(gpu_forward(G8, cfg.f), gpu_forward(G10, cfg.f), f"c{ci} 8-byte vs 10-byte forward", l2=1e-6, mr=1e-5)
-    assert_parity(gpu_backward(G8, w), gpu_backward(G10, w), f"c{ci} 8-byte vs 10-byte backward", l2=1e-6, mr=1e-5)
+    assert_parity(gpu_forward(G8, cfg.f), gpu_forward(G10, cfg.f), f"c{ci} 8-byte vs 10-byte forward")
+    assert_parity(gpu_backward(G8, w), gpu_backward(G10, w), f"c{ci} 8-byte vs 10-byte backward")
     if ci == 1:
         O = oracle.Geometry(cfg)
         assert_parity(gpu_forward(G8, cfg.f), O.forward(cfg.f), "c1 8-byte forward")
