@@ -127,7 +127,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_pc_qbase};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_pc_qbase, g->d_tc16_w1, g->d_tc16_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -152,6 +152,8 @@ const OptKey kOptKeys[] = {
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
     {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
     {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},
+    {"gemm16", &cacsi::Opts::gemm16, false, 0, 1},
+    {"b2_splits", &cacsi::Opts::b2_splits, false, 1, 64},
     {"pc_fwd_list", &cacsi::Opts::pc_fwd_list, false, 0, 1},
     {"pc_fwd_geom", &cacsi::Opts::pc_fwd_geom, false, 0, 1},
     {"pcv_items", &cacsi::Opts::pcv_items, false, 1, 64},

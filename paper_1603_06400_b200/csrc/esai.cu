@@ -29,6 +29,7 @@
 
 #include "pair.cuh"
 #include "tcgemm.cuh"
+#include "tcgemm16.cuh"
 
 namespace cacsi {
 
@@ -1091,6 +1092,23 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         E.tc_w = (const float *)g->d_tc_w;
         E.tc_w1 = (const float *)g->d_tc_w1;
         E.tc_b = (const float *)g->d_tc_b;
+        // fp16 two-term split of the same operands (tcgemm16.cuh, option gemm16), one global
+        // power-of-two scale from max |S~|
+        float smax = 0.0f;
+        for (float x : stab) smax = std::max(smax, std::fabs(x));
+        E.s16_exp = f16_scale_exp(smax);
+        const int nk16W = (Q + TC16_KC - 1) / TC16_KC, nk16B = (E.ldw + TC16_KC - 1) / TC16_KC;
+        const size_t n16W = (size_t)tc_ntiles(nb, TC_N) * nk16W * 2 * TC_N * TC16_KC;
+        const size_t n16B = (size_t)((Q + TC_N - 1) / TC_N) * nk16B * 2 * TC_N * TC16_KC;
+        e = cudaMalloc(&g->d_tc16_w1, n16W * sizeof(__half));
+        if (e == cudaSuccess) e = cudaMalloc(&g->d_tc16_b, n16B * sizeof(__half));
+        if (e != cudaSuccess) return e;
+        k_tc_pack_b16<<<gp, 256>>>(st, nb, Q, Q, 1, nk16W, (__half *)g->d_tc16_w1, E.s16_exp);
+        k_tc_pack_b16<<<gp, 256>>>(st, Q, nb, 1, Q, nk16B, (__half *)g->d_tc16_b, E.s16_exp);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        E.tc16_w1 = g->d_tc16_w1;
+        E.tc16_b = g->d_tc16_b;
     }
     clk.mark(0);  // pair stats, breakpoints, S~, LUT, windows, tensor-core operand tiles
     // transmission bitmaps
@@ -1153,6 +1171,13 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
         cudaFree(A1);
         if (e != cudaSuccess) return e;
         E.vbound = (const float *)g->d_esai_vbound;
+        {
+            std::vector<float> vb(nv);
+            e = cudaMemcpy(vb.data(), g->d_esai_vbound, nv * sizeof(float), cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return e;
+            E.vbmax = 0.0f;
+            for (float x : vb) E.vbmax = std::max(E.vbmax, x);
+        }
         clk.mark(2);  // fixed-point bound pass
     }
     // pair cache (above): counts -> device scan -> fill, if it fits in half the free memory
@@ -1380,6 +1405,12 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     memset(&tmF, 0, sizeof(tmF));
     const bool raw = ar_path && (p.nq % 4) == 0 && !o.wgemm_pack &&
                      tmap_rows_f32(&tmF, f, (uint64_t)p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq);
+    // option gemm16: the same A-resident GEMM on a two-term fp16 split (tcgemm16.cuh)
+    const bool f16 = raw && o.gemm16;
+    const int nk16 = (p.nq + TC16_KC - 1) / TC16_KC;
+    const int nsb16 = tca16_smem(nk16, 4) <= 227 * 1024 ? 4 : 3;
+    auto kar16 = nsb16 == 4 ? k_tc_gemm_ar16<4> : k_tc_gemm_ar16<3>;
+    if (f16) cudaFuncSetAttribute(kar16, cudaFuncAttributeMaxDynamicSharedMemorySize, tca16_smem(nk16, nsb16));
     if (nfc > 0 && !ar_path)
         for (int c = 0; c < nfc && e == cudaSuccess; c++) e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
     if (nfc > 0 && ar_path) {
@@ -1403,9 +1434,14 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             }
             {
                 KScope kt_(g, s, "k_tc_gemm_W");
-                kar<<<std::min(mtc * nt, sm_count(g->device)), raw ? TCA_T1R : TCA_T1, tca_smem(nkcA, nsb), s>>>(
-                    nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw, E.w_pre + r0 / TC_M,
-                    E.w_ntr + r0 / TC_M, tmF, r0);
+                if (f16)
+                    kar16<<<std::min(mtc * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16), s>>>(
+                        nr, E.nb, nk16, mtc, nt, (const __half *)E.tc16_w1, W + (size_t)r0 * E.ldw, E.ldw,
+                        E.w_pre + r0 / TC_M, E.w_ntr + r0 / TC_M, tmF, r0, E.s16_exp);
+                else
+                    kar<<<std::min(mtc * nt, sm_count(g->device)), raw ? TCA_T1R : TCA_T1, tca_smem(nkcA, nsb), s>>>(
+                        nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw, E.w_pre + r0 / TC_M,
+                        E.w_ntr + r0 / TC_M, tmF, r0);
             }
             *launches += 1;
         }
@@ -1431,6 +1467,10 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 const int npairs = std::max(1, std::min(mp * nt, sm_count(g->device) / 2));
                 k_tc_gemm_ar2<<<2 * npairs, TCA_T1, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
                                                                         E.ldw);
+            } else if (f16) {
+                kar16<<<std::min(mt * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16), s>>>(
+                    p.n_vox, E.nb, nk16, mt, nt, (const __half *)E.tc16_w1, W, E.ldw, E.w_pre, E.w_ntr, tmF, 0,
+                    E.s16_exp);
             } else if (nkcA <= 4 && o.wgemm == 0) {
                 // B ring depth: 3 stages where they fit beside the resident A panel (nkc <= 2), else 2
                 // (config 2, nq = 128: nkc = 4, the 128 KB panel leaves room for 2)
@@ -1612,10 +1652,15 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
-    // split-K of the A S~ contraction: 16 splits keep the TMEM accumulation
-    // error ~3e-6 (tcgemm.cuh); fp32 partials, fp64 sum
-    const int nkc = E.ldw / TC_KC;
-    const int cps = (nkc + 15) / 16;
+    // split-K of the A S~ contraction: fp32 partials, fp64 sum.  3xTF32 (gemm16=0): 16
+    // splits keep the TMEM accumulation error ~3e-6 (tcgemm.cuh); the fp16 GEMM (default)
+    // takes K = 16 per accumulate, so its 8 splits (option b2_splits) make the same ~60
+    // accumulates per split -- and half the partials to sum
+    const Opts &o = g->opt;
+    const bool f16 = o.gemm16 && p.nq <= TC_N && !o.b2gemm_tiles;
+    const int nkc = f16 ? (E.ldw + TC16_KC - 1) / TC16_KC : E.ldw / TC_KC;
+    const int nsp = f16 ? o.b2_splits : 16;
+    const int cps = (nkc + nsp - 1) / nsp;
     const int S_eff = (nkc + cps - 1) / cps;
     cudaError_t e = cudaMallocAsync(&A, (size_t)p.n_vox * E.ldw * sizeof(float), s);
     if (e == cudaSuccess) e = cudaMallocAsync(&part, (size_t)S_eff * p.n_vox * p.nq * sizeof(float), s);
@@ -1624,7 +1669,6 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     // union of its voxels' windows (A is zero there); the per-tile GEMM reads whole rows
     const int mt = (p.n_vox + TC_M - 1) / TC_M;
     CUtensorMap tm;
-    const Opts &o = g->opt;
     const bool splitk = p.nq <= TC_N && !o.b2gemm_tiles &&
                         tmap_rows_f32(&tm, A, (uint64_t)p.n_vox, (uint64_t)E.ldw, (uint64_t)E.ldw);
     if (e == cudaSuccess) {
@@ -1677,12 +1721,19 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         }
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
-            if (splitk) {
+            if (splitk && f16) {
+                cudaFuncSetAttribute(k_tc_gemm_splitk16, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs16_smem());
+                k_tc_gemm_splitk16<<<std::min(S_eff * mt, sm_count(g->device)), TCS16_T, tcs16_smem(), s>>>(
+                    tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, (const __half *)E.tc16_b, part, p.nq, E.trng, mt, wmax,
+                    E.vbmax, E.s16_exp);
+            } else if (splitk) {
                 {
                     cudaFuncSetAttribute(k_tc_gemm_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());
                     k_tc_gemm_splitk<<<std::min(S_eff * mt, sm_count(g->device)), TCS_T, tcs_smem(), s>>>(
                         tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, E.tc_b, part, p.nq, E.trng, mt);
                 }
+            } else if (f16) {
+                e = cudaErrorInvalidValue;  // (the fp16 GEMM needs the TMA tensor map of A)
             } else {
                 dim3 gg((p.nq + TC_N - 1) / TC_N, mt, S_eff);
                 cudaFuncSetAttribute(k_tc_gemm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
@@ -1698,7 +1749,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
             else
                 sum_parts(part, S_eff, n, EpiStore{b}, s);
         }
-        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
         *launches += epi ? 3 : 4;
     }
     if (wmax && !epi) cudaFreeAsync(wmax, s);

@@ -117,6 +117,11 @@ struct Esai {
     const float *tc_w;       // S~ as pre-split, pre-swizzled tensor-core B tiles (W = F S~^T), pair tiles
     const float *tc_w1;      // the same in disjoint tiles (plain W rows)
     const float *tc_b;       // S~^T likewise (b2 = A S~)
+    // the same operands split into fp16 hi / lo (scaled by 2^s16_exp) for the fp16-rate
+    // GEMMs of tcgemm16.cuh (option gemm16): S~ in disjoint 128 x 64 tiles, S~^T
+    const void *tc16_w1, *tc16_b;
+    int s16_exp;             // 2^s16_exp max|S~| < 2^14
+    float vbmax;             // max_v vbound[v] (the b2 GEMM's A scale: |A| <= vbmax max|w|)
     const uint32_t *tb_bwd;  // backward: [voxel][ceil(n_det/32)], bit i of word j = pixel 32 j + i
     // pair cache (esai.cu "pair cache"): per open pair of list (voxel v, detector row ix),
     // pixels; with pc_R > 0 each (voxel, block of pc_R rows) segment
@@ -186,6 +191,8 @@ struct Opts {
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
     int b2gemm_tiles = 0;     // "b2gemm_tiles": 1 = per-tile b2 GEMM instead of the persistent split-K one
+    int gemm16 = 1;           // "gemm16": 0 = W and b2 GEMMs on 3xTF32 (tcgemm.cuh) instead of the fp16 split (tcgemm16.cuh)
+    int b2_splits = 8;        // "b2_splits": split-K count of the fp16 b2 GEMM (8: profiles/r2w_gemm16_splits.txt)
     int pc_fwd_list = 0;      // "pc_fwd_list": 1 = per-list pair-cache forward (plain layout only)
     int pc_fwd_geom = 0;      // "pc_fwd_geom": 1 = the voxel-major forward recomputes P (6-byte records)
     int pcv_items = 2;        // "pcv_items": voxel chunks per SM of the voxel-major forward
@@ -214,7 +221,8 @@ struct cacsi_geometry {
     // ESAI (energy-integrating only)
     cacsi::Esai esai;
     void *d_esai_bp, *d_esai_lut, *d_esai_sb, *d_esai_stab, *d_esai_vwin, *d_esai_ptot, *d_tb_fwd, *d_tb_bwd, *d_tc_w, *d_tc_b,
-        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen, *d_pc_qbase;
+        *d_esai_vbound, *d_pc_off, *d_pc_bt, *d_pc_P, *d_pc_q, *d_tc_w1, *d_esai_trng, *d_w_tiles, *d_pc_segwin, *d_seen, *d_pc_qbase,
+        *d_tc16_w1, *d_tc16_b;
     // energy-resolving pair cache (er_cache.cu)
     cacsi::ErCache er;
     void *d_er_off, *d_er_vw, *d_er_P, *d_er_s, *d_er_boff, *d_er_sv;

@@ -42,9 +42,9 @@ def test_repeat_bitwise(ci):
 def test_cta_pair_w_gemm_bitwise():
     """The cta_group::2 W GEMM (option wgemm=1: M = 256 per CTA pair, half of
     each B chunk per SM, multicast commits) gives the same bits as the
-    single-CTA A-resident GEMM."""
+    single-CTA A-resident GEMM (both 3xTF32: option gemm16=0)."""
     cfg = make_config(1)
-    G = P.Geometry(cfg.desc())
+    G = P.Geometry(cfg.desc(), options="gemm16=0")
     f = torch.as_tensor(cfg.f).cuda()
     out = []
     for mode in ("ar", "ar2"):
