@@ -139,7 +139,7 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * wgemm_pack, b2gemm_tiles, pc_fwd_list, pcv_items, pcv_pf, pcv_u, pc_bwd_flat,
  * pcb_pf, subset_bwd_mask, er_bwd_dense, graphs (1; 0 = cacsi_osem by stream
  * launches), gemm16 (1: the ESAI contractions on a two-term fp16 split at the
- * fp16 tensor-core rate; 0 = 3xTF32), b2_splits (8: split-K count of the fp16
+ * fp16 tensor-core rate; 0 = 3xTF32), b2_splits (16: split-K count of the fp16
  * b2 GEMM).  An unknown key or out-of-range value -> CACSI_ERR_INVALID.
  * The library never reads the process environment.                          */
 CACSI_API cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *desc, int device, const char *options,

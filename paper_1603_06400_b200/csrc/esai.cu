@@ -1652,10 +1652,10 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
     const Params &p = g->p;
     const Esai &E = g->esai;
     float *A = nullptr, *part = nullptr, *wmax = nullptr;
-    // split-K of the A S~ contraction: fp32 partials, fp64 sum.  3xTF32 (gemm16=0): 16
-    // splits keep the TMEM accumulation error ~3e-6 (tcgemm.cuh); the fp16 GEMM (default)
-    // takes K = 16 per accumulate, so its 8 splits (option b2_splits) make the same ~60
-    // accumulates per split -- and half the partials to sum
+    // split-K of the A S~ contraction: fp32 partials, fp64 sum.  16 splits keep the TMEM
+    // accumulation error ~3e-6 (tcgemm.cuh); the fp16 GEMM (default) keeps 16 (option
+    // b2_splits): 8 would halve the partials (-0.016 ms) but doubled the measured backward
+    // error on configs 1-2
     const Opts &o = g->opt;
     const bool f16 = o.gemm16 && p.nq <= TC_N && !o.b2gemm_tiles;
     const int nkc = f16 ? (E.ldw + TC16_KC - 1) / TC16_KC : E.ldw / TC_KC;
