@@ -140,7 +140,9 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * pcb_pf, subset_bwd_mask, er_bwd_dense, graphs (1; 0 = cacsi_osem by stream
  * launches), gemm16 (1: the ESAI contractions on a two-term fp16 split at the
  * fp16 tensor-core rate; 0 = 3xTF32), b2_splits (16: split-K count of the fp16
- * b2 GEMM).  An unknown key or out-of-range value -> CACSI_ERR_INVALID.
+ * b2 GEMM), w_tmast / b2_tmast (1: the fp16 GEMMs' epilogues store by TMA
+ * tensor stores; 0 = per-lane stores).  An unknown key or out-of-range value
+ * -> CACSI_ERR_INVALID.
  * The library never reads the process environment.                          */
 CACSI_API cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *desc, int device, const char *options,
                                                 cacsi_geometry **out);

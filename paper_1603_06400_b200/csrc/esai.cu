@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -824,10 +825,43 @@ __global__ void k_sum_parts_seq(const T *__restrict__ part, int S, size_t n, Epi
     }
     epi_max(epi, m);
 }
+// the same per-output order (j = 0, 1, ... from 0.0, so the same bits as k_sum_parts_seq)
+// for fp32 partials with n % 4 == 0: four consecutive outputs per thread (16-byte loads),
+// the slices loaded 8 at a time before they are added, so 8 x 16 B are in flight per
+// thread instead of one dependent load per slice (config 2's b2 partials: 16 x 8 MB)
+template <class Epi>
+__global__ void __launch_bounds__(256) k_sum_parts_v4(const float *__restrict__ part, int S, size_t n, Epi epi) {
+    float m = 0.0f;
+    const size_t n4 = n / 4;
+    for (size_t i4 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i4 < n4; i4 += (size_t)gridDim.x * blockDim.x) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const float4 *p4 = (const float4 *)part + i4;
+        int j = 0;
+        for (; j + 8 <= S; j += 8) {
+            float4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = __ldcs(p4 + (size_t)(j + u) * n4);
+#pragma unroll
+            for (int u = 0; u < 8; u++) s0 += (double)x[u].x, s1 += (double)x[u].y, s2 += (double)x[u].z, s3 += (double)x[u].w;
+        }
+        for (; j < S; j++) {
+            const float4 x = __ldcs(p4 + (size_t)j * n4);
+            s0 += (double)x.x, s1 += (double)x.y, s2 += (double)x.z, s3 += (double)x.w;
+        }
+        m = fmaxf(m, epi(4 * i4, s0));
+        m = fmaxf(m, epi(4 * i4 + 1, s1));
+        m = fmaxf(m, epi(4 * i4 + 2, s2));
+        m = fmaxf(m, epi(4 * i4 + 3, s3));
+    }
+    epi_max(epi, m);
+}
 template <typename T, class Epi>
 void sum_parts(const T *part, int S, size_t n, Epi epi, cudaStream_t s) {
     if (S >= 16 && n < 200000)
         k_sum_parts<T, Epi><<<(unsigned)((n + 32 * SP_U - 1) / (32 * SP_U)), 256, 0, s>>>(part, S, n, epi);
+    else if (std::is_same<T, float>::value && n % 4 == 0 && (uintptr_t)part % 16 == 0)
+        k_sum_parts_v4<Epi><<<(unsigned)std::min((n / 4 + 255) / 256, (size_t)8 * 148), 256, 0, s>>>(
+            (const float *)part, S, n, epi);
     else
         k_sum_parts_seq<T, Epi><<<(unsigned)std::min((n + 255) / 256, (size_t)4096), 256, 0, s>>>(part, S, n, epi);
 }
@@ -1339,7 +1373,8 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
 
 static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, const int32_t *pixels, int n_pix,
                                      float *out, cudaStream_t s, int *launches, const FwdRatioEpi *epi = nullptr);
-static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld);
+static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t box_rows = TC_M);
 
 // Row blocks of the voxel-major pair-cache forward (0: the W windows do not fit
 // shared memory, the per-list kernel runs).  One 1024-thread CTA per SM with a
@@ -1406,11 +1441,16 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
     const bool raw = ar_path && (p.nq % 4) == 0 && !o.wgemm_pack &&
                      tmap_rows_f32(&tmF, f, (uint64_t)p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq);
     // option gemm16: the same A-resident GEMM on a two-term fp16 split (tcgemm16.cuh)
+    // (option w_tmast: the epilogue stores W by TMA tensor stores, tmW: box 32 x 32)
+    CUtensorMap tmW;
+    memset(&tmW, 0, sizeof(tmW));
     const bool f16 = raw && o.gemm16;
+    const bool tmast = f16 && o.w_tmast && tmap_rows_f32(&tmW, W, (uint64_t)p.n_vox, (uint64_t)E.nb, (uint64_t)E.ldw, 32);
     const int nk16 = (p.nq + TC16_KC - 1) / TC16_KC;
-    const int nsb16 = tca16_smem(nk16, 4) <= 227 * 1024 ? 4 : 3;
-    auto kar16 = nsb16 == 4 ? k_tc_gemm_ar16<4> : k_tc_gemm_ar16<3>;
-    if (f16) cudaFuncSetAttribute(kar16, cudaFuncAttributeMaxDynamicSharedMemorySize, tca16_smem(nk16, nsb16));
+    const int nsb16 = tca16_smem(nk16, 4, tmast) <= 227 * 1024 ? 4 : 3;
+    auto kar16 = tmast ? (nsb16 == 4 ? k_tc_gemm_ar16<4, true> : k_tc_gemm_ar16<3, true>)
+                       : (nsb16 == 4 ? k_tc_gemm_ar16<4> : k_tc_gemm_ar16<3>);
+    if (f16) cudaFuncSetAttribute(kar16, cudaFuncAttributeMaxDynamicSharedMemorySize, tca16_smem(nk16, nsb16, tmast));
     if (nfc > 0 && !ar_path)
         for (int c = 0; c < nfc && e == cudaSuccess; c++) e = cudaStreamWaitEvent(s, epi->f_ready[c], 0);
     if (nfc > 0 && ar_path) {
@@ -1435,9 +1475,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
             {
                 KScope kt_(g, s, "k_tc_gemm_W");
                 if (f16)
-                    kar16<<<std::min(mtc * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16), s>>>(
+                    kar16<<<std::min(mtc * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16, tmast), s>>>(
                         nr, E.nb, nk16, mtc, nt, (const __half *)E.tc16_w1, W + (size_t)r0 * E.ldw, E.ldw,
-                        E.w_pre + r0 / TC_M, E.w_ntr + r0 / TC_M, tmF, r0, E.s16_exp);
+                        E.w_pre + r0 / TC_M, E.w_ntr + r0 / TC_M, tmF, r0, E.s16_exp, tmW);
                 else
                     kar<<<std::min(mtc * nt, sm_count(g->device)), raw ? TCA_T1R : TCA_T1, tca_smem(nkcA, nsb), s>>>(
                         nr, E.nb, nkcA, mtc, nt, fpc, E.tc_w1, W + (size_t)r0 * E.ldw, E.ldw, E.w_pre + r0 / TC_M,
@@ -1468,9 +1508,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 k_tc_gemm_ar2<<<2 * npairs, TCA_T1, tca2_smem(nkcA), s>>>(p.n_vox, E.nb, nkcA, mp, nt, fp, E.tc_w1, W,
                                                                         E.ldw);
             } else if (f16) {
-                kar16<<<std::min(mt * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16), s>>>(
+                kar16<<<std::min(mt * nt, sm_count(g->device)), TCA16_T, tca16_smem(nk16, nsb16, tmast), s>>>(
                     p.n_vox, E.nb, nk16, mt, nt, (const __half *)E.tc16_w1, W, E.ldw, E.w_pre, E.w_ntr, tmF, 0,
-                    E.s16_exp);
+                    E.s16_exp, tmW);
             } else if (nkcA <= 4 && o.wgemm == 0) {
                 // B ring depth: 3 stages where they fit beside the resident A panel (nkc <= 2), else 2
                 // (config 2, nq = 128: nkc = 4, the 128 KB panel leaves room for 2)
@@ -1628,7 +1668,8 @@ cudaError_t esai_backward(const cacsi_geometry *g, const float *w, float *b, cud
 
 // TMA tensor map of a row-major fp32 matrix (rows x cols, row stride ld floats),
 // box 128 rows x 32 columns, 128-byte swizzle (the tcgen05 K-major operand layout)
-static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld) {
+static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -1639,7 +1680,7 @@ static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uin
     }
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {ld * sizeof(float)};
-    const cuuint32_t box[2] = {(cuuint32_t)TC_KC, (cuuint32_t)TC_M};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_KC, (cuuint32_t)box_rows};
     const cuuint32_t es[2] = {1, 1};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1722,10 +1763,16 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
         {
             KScope kt_(g, s, "k_tc_gemm_b2");
             if (splitk && f16) {
-                cudaFuncSetAttribute(k_tc_gemm_splitk16, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs16_smem());
-                k_tc_gemm_splitk16<<<std::min(S_eff * mt, sm_count(g->device)), TCS16_T, tcs16_smem(), s>>>(
+                // (option b2_tmast: the partials leave by TMA tensor stores, tmP: box 32 x 32)
+                CUtensorMap tmP;
+                memset(&tmP, 0, sizeof(tmP));
+                const bool tmast = o.b2_tmast && (p.nq % 4) == 0 &&
+                                   tmap_rows_f32(&tmP, part, (uint64_t)S_eff * p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq, 32);
+                auto ks = tmast ? k_tc_gemm_splitk16<true> : k_tc_gemm_splitk16<false>;
+                cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs16_smem(tmast));
+                ks<<<std::min(S_eff * mt, sm_count(g->device)), TCS16_T, tcs16_smem(tmast), s>>>(
                     tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, (const __half *)E.tc16_b, part, p.nq, E.trng, mt, wmax,
-                    E.vbmax, E.s16_exp);
+                    E.vbmax, E.s16_exp, tmP);
             } else if (splitk) {
                 {
                     cudaFuncSetAttribute(k_tc_gemm_splitk, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs_smem());

@@ -107,19 +107,25 @@ __device__ __forceinline__ void f16_store_row(unsigned char *cb, int r, const fl
 // it in place -- warp w converts rows 32 (w % 4) .. + 31 of K chunk (w < 4 ? 0 : 1), the
 // row maxima meet in shared memory -- then drain tiles (they own the same rows in TMEM,
 // so each thread keeps its row's output scale in a register).
+// TMAST: the epilogue stores each 32 x 32 block by a TMA tensor store (tmC: box 32 x 32,
+// SWIZZLE_128B -- the layout the transpose already writes) from one of two staging
+// buffers per warp, instead of 8 STG.128 per lane; rows past M / columns past N are
+// clipped by the tensor map (its rows are C's: mrow0 + tile row).
 constexpr int TCA16_T = 320;
-constexpr int tca16_smem(int nkc, int nsb) { return nkc * TC16_CH + nsb * TC16_CH + 8 * 32 * 32 * 4 + 128 * 2 * 4 + 1024 + 256; }
-template <int NSB>
+constexpr int tca16_smem(int nkc, int nsb, bool tmast = false) {
+    return nkc * TC16_CH + nsb * TC16_CH + (tmast ? 2 : 1) * 8 * 32 * 32 * 4 + 128 * 2 * 4 + 1024 + 256;
+}
+template <int NSB, bool TMAST = false>
 __global__ void __launch_bounds__(TCA16_T, 1)
     k_tc_gemm_ar16(int M, int N, int nkc, int mtiles, int ntiles, const __half *__restrict__ Bt, float *__restrict__ C,
                    int ldc, const int *__restrict__ tpre, const int2 *__restrict__ tntr,
-                   const __grid_constant__ CUtensorMap tmA, int mrow0, int bexp) {
+                   const __grid_constant__ CUtensorMap tmA, int mrow0, int bexp, const __grid_constant__ CUtensorMap tmC) {
     extern __shared__ __align__(1024) unsigned char t16_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)t16_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;                          // [nkc][hi, lo] 32 KB each (raw fp32 on arrival)
     unsigned char *sB = sA + nkc * TC16_CH;            // [NSB][hi, lo]
-    float *ebuf = (float *)(sB + NSB * TC16_CH);       // [8][32][32]
-    float *rmax = ebuf + 8 * 32 * 32;                  // [2][128]: per K half, per panel row
+    float *ebuf = (float *)(sB + NSB * TC16_CH);       // [8][TMAST ? 2 : 1][32][32]
+    float *rmax = ebuf + (TMAST ? 2 : 1) * 8 * 32 * 32;  // [2][128]: per K half, per panel row
     uint64_t *bars = (uint64_t *)(rmax + 2 * 128);
     uint64_t *a_full = bars, *a_empty = bars + 1, *b_full = bars + 2, *b_empty = bars + 2 + NSB,
              *t_full = bars + 2 + 2 * NSB, *t_empty = bars + 4 + 2 * NSB, *a_conv = bars + 6 + 2 * NSB;
@@ -233,7 +239,8 @@ __global__ void __launch_bounds__(TCA16_T, 1)
         // columns 0-63 and convert K chunk 0, warps 6-9 columns 64-127 and K chunk 1
         const int ew = warp < 4 ? warp : warp - 2, lq = warp & 3, ch = warp < 4 ? 0 : TC_N / 2, kh = warp < 4 ? 0 : 1;
         const int row = lq * 32 + lane;
-        float *buf = ebuf + ew * (32 * 32);
+        float *buf = ebuf + ew * (TMAST ? 2 : 1) * (32 * 32);
+        uint32_t bsel = 0;  // TMAST: staging buffer of the next block
         const int cq = 4 * (lane & 7);
         uint32_t tc = 0, loads = 0;
         int cur_m = -1;
@@ -273,10 +280,16 @@ __global__ void __launch_bounds__(TCA16_T, 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll 1
             for (int c0 = ch; c0 < ch + TC_N / 2; c0 += 32) {
+                float *bb = buf;
+                if (TMAST) {
+                    // the store issued from this buffer two blocks ago has finished reading it
+                    bb = buf + bsel * (32 * 32);
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                }
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < 8; j++)
-                    *(float4 *)(buf + lane * 32 + 4 * (j ^ (lane & 7))) =
+                    *(float4 *)(bb + lane * 32 + 4 * (j ^ (lane & 7))) =
                         make_float4((__uint_as_float(r[4 * j]) + __uint_as_float(x[4 * j])) * osc,
                                     (__uint_as_float(r[4 * j + 1]) + __uint_as_float(x[4 * j + 1])) * osc,
                                     (__uint_as_float(r[4 * j + 2]) + __uint_as_float(x[4 * j + 2])) * osc,
@@ -284,6 +297,20 @@ __global__ void __launch_bounds__(TCA16_T, 1)
                 if (c0 + 32 < ch + TC_N / 2) {
                     tmem_ld32(tbase + c0 + 32, r);
                     tmem_ld32(tbase + TC_N + c0 + 32, x);
+                }
+                if (TMAST) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(&tmC),
+                            "r"(n0 + c0), "r"(mrow0 + m0 + lq * 32), "r"(smem_u32(bb))
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                    }
+                    bsel ^= 1u;
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+                    continue;
                 }
                 __syncwarp();
                 const int nn = n0 + c0 + cq;
@@ -308,6 +335,7 @@ __global__ void __launch_bounds__(TCA16_T, 1)
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
         }
+        if (TMAST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
@@ -320,13 +348,19 @@ __global__ void __launch_bounds__(TCA16_T, 1)
 // produces, warp 9 lane 0 issues 12 MMAs per 64-wide chunk, warps 0-3 drain with the
 // output scale 2^-(ea + bexp).  ea comes from the fixed-point bound vbmax max|w| (the
 // device scalar *wmax the backward used).
+// TMAST: the partials are stored by TMA tensor stores (tmC over C as [nsplit M][ldc],
+// box 32 x 32, SWIZZLE_128B) from two 4 KB staging buffers per epilogue warp.
 constexpr int TCS16_T = 320, TCS16_NS = 3;
 constexpr int TCS16_STAGE = 2 * TC16_CH;  // A hi/lo + B hi/lo: 64 KB
-constexpr int tcs16_smem() { return TCS16_NS * TCS16_STAGE + 4 * 32 * 33 * 4 + 1024 + 256; }
+constexpr int tcs16_smem(bool tmast = false) {
+    return TCS16_NS * TCS16_STAGE + (tmast ? 4 * 2 * 32 * 32 * 4 : 4 * 32 * 33 * 4) + 1024 + 256;
+}
+template <bool TMAST = false>
 __global__ void __launch_bounds__(TCS16_T, 1)
     k_tc_gemm_splitk16(const __grid_constant__ CUtensorMap tmA, int M, int N, int nkc, int cps, int nsplit, int mtiles,
                        const __half *__restrict__ Bt, float *__restrict__ C, int ldc, const int2 *__restrict__ trng,
-                       int mreal, const float *__restrict__ wmax, float vbmax, int bexp) {
+                       int mreal, const float *__restrict__ wmax, float vbmax, int bexp,
+                       const __grid_constant__ CUtensorMap tmC) {
     auto krange = [&](int z, int m, int &c0, int &c1) {
         c0 = z * cps;
         c1 = min(nkc, (z + 1) * cps);
@@ -341,7 +375,7 @@ __global__ void __launch_bounds__(TCS16_T, 1)
     extern __shared__ __align__(1024) unsigned char s16_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)s16_raw + 1023) & ~(uintptr_t)1023);
     float *ebuf = (float *)(base + TCS16_NS * TCS16_STAGE);
-    uint64_t *bars = (uint64_t *)(ebuf + 4 * 32 * 33);
+    uint64_t *bars = (uint64_t *)(ebuf + (TMAST ? 4 * 2 * 32 * 32 : 4 * 32 * 33));
     uint64_t *load_full = bars, *conv_full = bars + TCS16_NS, *empty = bars + 2 * TCS16_NS,
              *t_full = bars + 3 * TCS16_NS, *t_empty = t_full + 2;
     uint32_t *tmem_slot = (uint32_t *)(t_empty + 2);
@@ -467,9 +501,9 @@ __global__ void __launch_bounds__(TCS16_T, 1)
         }
     } else if (warp < 4) {
         const float osc = ldexpf(1.0f, -(ea + bexp));
-        float *buf = ebuf + warp * (32 * 33);
+        float *buf = ebuf + warp * (TMAST ? 2 * 32 * 32 : 32 * 33);
         const int cq = 4 * (lane & 7);
-        uint32_t uc = 0;
+        uint32_t uc = 0, bsel = 0;
         for (int u = u0; u < nunits; u += ustep, uc++) {
             const int z = u / mtiles, m = u % mtiles;
             int cA, cB;
@@ -487,6 +521,32 @@ __global__ void __launch_bounds__(TCS16_T, 1)
                 tmem_ld32(taddr, r);
                 tmem_ld32(taddr + TC_N, x);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+                if (TMAST) {
+                    float *bb = buf + bsel * (32 * 32);
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (!empty_unit)
+                            v4 = make_float4((__uint_as_float(r[4 * j]) + __uint_as_float(x[4 * j])) * osc,
+                                             (__uint_as_float(r[4 * j + 1]) + __uint_as_float(x[4 * j + 1])) * osc,
+                                             (__uint_as_float(r[4 * j + 2]) + __uint_as_float(x[4 * j + 2])) * osc,
+                                             (__uint_as_float(r[4 * j + 3]) + __uint_as_float(x[4 * j + 3])) * osc);
+                        *(float4 *)(bb + lane * 32 + 4 * (j ^ (lane & 7))) = v4;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(&tmC),
+                            "r"(c0), "r"(z * M + m0 + warp * 32), "r"(smem_u32(bb))
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                    }
+                    bsel ^= 1u;
+                    continue;
+                }
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < 32; j++)
@@ -511,6 +571,7 @@ __global__ void __launch_bounds__(TCS16_T, 1)
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(t_empty + ab)) : "memory");
         }
+        if (TMAST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();

@@ -127,3 +127,28 @@ def test_gemm16_config2_vs_tf32_and_oracle_sampled():
     assert_parity(b16.reshape(cfg.n_vox, cfg.nq)[vox], O.backward_voxels(w, vox), "gemm16 c2 backward, 128 voxels")
     # deterministic
     assert np.array_equal(gpu_forward(G, cfg.f), g16) and np.array_equal(gpu_backward(G, w), b16)
+
+
+@pytest.mark.parametrize("over", [{}, dict(ny=13, nz=23, nq=70, det_nx=37, det_ny=41), dict(ny=5, nz=7, nq=13)])
+def test_w_tma_store_bitwise(over):
+    """The W GEMM's epilogue by TMA tensor stores (w_tmast=1, the default; clipped at the
+    map's edges) writes the same bits as the per-lane stores (w_tmast=0)."""
+    d = make_config(1 if not over else 0).desc()
+    d.update(over)
+    G = P.Geometry(d, options="w_tmast=0")
+    f = rnd(G.f_shape, 0, 130)
+    g0 = gpu_forward(G, f)
+    G.set_option("w_tmast", 1)
+    assert np.array_equal(gpu_forward(G, f), g0)
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_b2_tma_store_bitwise(ci):
+    """The b2 GEMM's partials by TMA tensor stores (b2_tmast=1, the default) carry the same
+    bits as the per-lane stores (b2_tmast=0); empty units (tiles whose windows miss a split) store zeros either way."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc(), options="b2_tmast=0")
+    w = rnd(G.g_shape, ci, 131)
+    b0 = gpu_backward(G, w)
+    G.set_option("b2_tmast", 1)
+    assert np.array_equal(gpu_backward(G, w), b0)
