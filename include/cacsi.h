@@ -141,7 +141,8 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * launches), gemm16 (1: the ESAI contractions on a two-term fp16 split at the
  * fp16 tensor-core rate; 0 = 3xTF32), b2_splits (16: split-K count of the fp16
  * b2 GEMM), w_tmast / b2_tmast (1: the fp16 GEMMs' epilogues store by TMA
- * tensor stores; 0 = per-lane stores).  An unknown key or out-of-range value
+ * tensor stores; 0 = per-lane stores), b2_rings (1: A / B ring depths of
+ * the fp16 b2 GEMM, 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4).  An unknown key or out-of-range value
  * -> CACSI_ERR_INVALID.
  * The library never reads the process environment.                          */
 CACSI_API cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *desc, int device, const char *options,

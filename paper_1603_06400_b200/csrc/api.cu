@@ -156,6 +156,7 @@ const OptKey kOptKeys[] = {
     {"b2_splits", &cacsi::Opts::b2_splits, false, 1, 64},
     {"w_tmast", &cacsi::Opts::w_tmast, false, 0, 1},
     {"b2_tmast", &cacsi::Opts::b2_tmast, false, 0, 1},
+    {"b2_rings", &cacsi::Opts::b2_rings, false, 0, 2},
     {"pc_fwd_list", &cacsi::Opts::pc_fwd_list, false, 0, 1},
     {"pc_fwd_geom", &cacsi::Opts::pc_fwd_geom, false, 0, 1},
     {"pcv_items", &cacsi::Opts::pcv_items, false, 1, 64},

@@ -1768,9 +1768,15 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 memset(&tmP, 0, sizeof(tmP));
                 const bool tmast = o.b2_tmast && (p.nq % 4) == 0 &&
                                    tmap_rows_f32(&tmP, part, (uint64_t)S_eff * p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq, 32);
-                auto ks = tmast ? k_tc_gemm_splitk16<true> : k_tc_gemm_splitk16<false>;
-                cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, tcs16_smem(tmast));
-                ks<<<std::min(S_eff * mt, sm_count(g->device)), TCS16_T, tcs16_smem(tmast), s>>>(
+                // A / B ring depths (option b2_rings: 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4)
+                const int na = o.b2_rings == 1 ? 4 : o.b2_rings == 2 ? 2 : 3, nbr = 6 - na;
+                auto ks = tmast ? (na == 4 ? k_tc_gemm_splitk16<true, 4, 2> : na == 2 ? k_tc_gemm_splitk16<true, 2, 4>
+                                                                                      : k_tc_gemm_splitk16<true, 3, 3>)
+                                : (na == 4 ? k_tc_gemm_splitk16<false, 4, 2> : na == 2 ? k_tc_gemm_splitk16<false, 2, 4>
+                                                                                       : k_tc_gemm_splitk16<false, 3, 3>);
+                const int sm16 = tcs16_smem(tmast, na, nbr);
+                cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm16);
+                ks<<<std::min(S_eff * mt, sm_count(g->device)), TCS16_T, sm16, s>>>(
                     tm, p.n_vox, p.nq, nkc, cps, S_eff, mt, (const __half *)E.tc16_b, part, p.nq, E.trng, mt, wmax,
                     E.vbmax, E.s16_exp, tmP);
             } else if (splitk) {

@@ -194,6 +194,7 @@ struct Opts {
     int gemm16 = 1;           // "gemm16": 0 = W and b2 GEMMs on 3xTF32 (tcgemm.cuh) instead of the fp16 split (tcgemm16.cuh)
     int w_tmast = 1;          // "w_tmast": 0 = the fp16 W GEMM stores W per lane (STG) instead of by TMA tensor stores
     int b2_tmast = 1;         // "b2_tmast": 0 = the fp16 b2 GEMM stores its partials per lane (STG) instead of by TMA tensor stores
+    int b2_rings = 1;         // "b2_rings": A / B ring depths of the fp16 b2 GEMM (0: 3 / 3, 1: 4 / 2, 2: 2 / 4)
     int b2_splits = 16;       // "b2_splits": split-K count of the fp16 b2 GEMM (16: accuracy)
     int pc_fwd_list = 0;      // "pc_fwd_list": 1 = per-list pair-cache forward (plain layout only)
     int pc_fwd_geom = 0;      // "pc_fwd_geom": 1 = the voxel-major forward recomputes P (6-byte records)

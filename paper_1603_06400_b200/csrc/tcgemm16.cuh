@@ -343,19 +343,19 @@ __global__ void __launch_bounds__(TCA16_T, 1)
 }
 
 // ---- b2 = A S~: split-K, streamed A (k_tc_gemm_splitk's structure) ------------------
-// Stage = A (two TMA boxes of raw fp32, split in place by warps 4-7, one row each, with
-// the global scale 2^ea) + the B chunk (pre-split fp16, one bulk copy); warp 8 lane 0
-// produces, warp 9 lane 0 issues 12 MMAs per 64-wide chunk, warps 0-3 drain with the
-// output scale 2^-(ea + bexp).  ea comes from the fixed-point bound vbmax max|w| (the
-// device scalar *wmax the backward used).
+// A ring of NA stages (two TMA boxes of raw fp32 A each, split in place by warps 4-7, one
+// row per thread, with the global scale 2^ea) and a separate ring of NB B chunks (pre-
+// split fp16, one bulk copy each): A streams from HBM and wants the deeper ring, B comes
+// from L2.  Warp 8 lane 0 produces A, warp 10 lane 0 produces B, warp 9 lane 0 issues 12
+// MMAs per 64-wide chunk, warps 0-3 drain with the output scale 2^-(ea + bexp).  ea comes
+// from the fixed-point bound vbmax max|w| (the device scalar *wmax the backward used).
 // TMAST: the partials are stored by TMA tensor stores (tmC over C as [nsplit M][ldc],
 // box 32 x 32, SWIZZLE_128B) from two 4 KB staging buffers per epilogue warp.
-constexpr int TCS16_T = 320, TCS16_NS = 3;
-constexpr int TCS16_STAGE = 2 * TC16_CH;  // A hi/lo + B hi/lo: 64 KB
-constexpr int tcs16_smem(bool tmast = false) {
-    return TCS16_NS * TCS16_STAGE + (tmast ? 4 * 2 * 32 * 32 * 4 : 4 * 32 * 33 * 4) + 1024 + 256;
+constexpr int TCS16_T = 352;
+constexpr int tcs16_smem(bool tmast, int na, int nb) {
+    return (na + nb) * TC16_CH + (tmast ? 4 * 2 * 32 * 32 * 4 : 4 * 32 * 33 * 4) + 1024 + 256;
 }
-template <bool TMAST = false>
+template <bool TMAST, int NA, int NB>
 __global__ void __launch_bounds__(TCS16_T, 1)
     k_tc_gemm_splitk16(const __grid_constant__ CUtensorMap tmA, int M, int N, int nkc, int cps, int nsplit, int mtiles,
                        const __half *__restrict__ Bt, float *__restrict__ C, int ldc, const int2 *__restrict__ trng,
@@ -374,10 +374,11 @@ __global__ void __launch_bounds__(TCS16_T, 1)
     };
     extern __shared__ __align__(1024) unsigned char s16_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)s16_raw + 1023) & ~(uintptr_t)1023);
-    float *ebuf = (float *)(base + TCS16_NS * TCS16_STAGE);
+    unsigned char *sA = base, *sB = base + NA * TC16_CH;
+    float *ebuf = (float *)(sB + NB * TC16_CH);
     uint64_t *bars = (uint64_t *)(ebuf + (TMAST ? 4 * 2 * 32 * 32 : 4 * 32 * 33));
-    uint64_t *load_full = bars, *conv_full = bars + TCS16_NS, *empty = bars + 2 * TCS16_NS,
-             *t_full = bars + 3 * TCS16_NS, *t_empty = t_full + 2;
+    uint64_t *a_full = bars, *conv_full = bars + NA, *a_empty = bars + 2 * NA, *b_full = bars + 3 * NA,
+             *b_empty = b_full + NB, *t_full = b_empty + NB, *t_empty = t_full + 2;
     uint32_t *tmem_slot = (uint32_t *)(t_empty + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nunits = nsplit * mtiles;
@@ -390,10 +391,14 @@ __global__ void __launch_bounds__(TCS16_T, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 32) {
-        for (int i = 0; i < TCS16_NS; i++) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(load_full + i)));
+        for (int i = 0; i < NA; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(a_full + i)));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(smem_u32(conv_full + i)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(empty + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(a_empty + i)));
+        }
+        for (int i = 0; i < NB; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b_full + i)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b_empty + i)));
         }
         for (int i = 0; i < 2; i++) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(t_full + i)));
@@ -407,37 +412,43 @@ __global__ void __launch_bounds__(TCS16_T, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 8) {
+    if (warp == 8 || warp == 10) {
+        // producers: warp 8 the A ring, warp 10 the B ring (the same chunk sequence)
         if (lane == 0) {
+            const bool pa = warp == 8;
+            const int ns = pa ? NA : NB;
             uint32_t cnt = 0;
             for (int u = u0; u < nunits; u += ustep) {
                 const int z = u / mtiles, m = u % mtiles;
                 int cA, c1;
                 krange(z, m, cA, c1);
                 for (int c = cA; c < c1; c++, cnt++) {
-                    const int st = cnt % TCS16_NS;
-                    if (cnt >= TCS16_NS) {
-                        mbar_wait(smem_u32(empty + st), ((cnt / TCS16_NS) - 1) & 1);
-                        // the converters' generic writes into this stage precede the MMAs
-                        // that released it; order them before the async-proxy refill
+                    const int st = cnt % ns;
+                    if (cnt >= (uint32_t)ns) {
+                        mbar_wait(smem_u32((pa ? a_empty : b_empty) + st), ((cnt / ns) - 1) & 1);
+                        // (A: the converters' generic writes into this stage precede the MMAs
+                        // that released it; order them before the async-proxy refill)
                         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     }
-                    unsigned char *sa = base + st * TCS16_STAGE;
-                    const uint32_t mb = smem_u32(load_full + st);
+                    const uint32_t mb = smem_u32((pa ? a_full : b_full) + st);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                                 "r"((uint32_t)TCS16_STAGE)
+                                 "r"((uint32_t)TC16_CH)
                                  : "memory");
-                    for (int hb = 0; hb < 2; hb++)
+                    if (pa) {
+                        unsigned char *sa = sA + st * TC16_CH;
+                        for (int hb = 0; hb < 2; hb++)
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+                                "{%2, %3}], [%4];\n" ::"r"(smem_u32(sa + hb * TC16_OPB)),
+                                "l"(&tmA), "r"(c * TC16_KC + 32 * hb), "r"(m * TC_M), "r"(mb)
+                                : "memory");
+                    } else {
                         asm volatile(
-                            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-                            "%3}], [%4];\n" ::"r"(smem_u32(sa + hb * TC16_OPB)),
-                            "l"(&tmA), "r"(c * TC16_KC + 32 * hb), "r"(m * TC_M), "r"(mb)
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                smem_u32(sB + st * TC16_CH)),
+                            "l"(Bt + (size_t)c * (2 * TC_N * TC16_KC)), "r"((uint32_t)TC16_CH), "r"(mb)
                             : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                            smem_u32(sa + TC16_CH)),
-                        "l"(Bt + (size_t)c * (2 * TC_N * TC16_KC)), "r"((uint32_t)TC16_CH), "r"(mb)
-                        : "memory");
+                    }
                 }
             }
         }
@@ -450,9 +461,9 @@ __global__ void __launch_bounds__(TCS16_T, 1)
             int cA, c1;
             krange(z, m, cA, c1);
             for (int c = cA; c < c1; c++, cnt++) {
-                const int st = cnt % TCS16_NS;
-                mbar_wait(smem_u32(load_full + st), (cnt / TCS16_NS) & 1);
-                unsigned char *sa = base + st * TCS16_STAGE;
+                const int st = cnt % NA;
+                mbar_wait(smem_u32(a_full + st), (cnt / NA) & 1);
+                unsigned char *sa = sA + st * TC16_CH;
                 float v[64];
                 f16_load_row(sa, row, v);
 #if CACSI_CHECKS
@@ -478,11 +489,12 @@ __global__ void __launch_bounds__(TCS16_T, 1)
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const uint32_t dmain = tmem + ab * 2 * TC_N, dcross = dmain + TC_N;
                 for (int c = c0; c < c1; c++, cnt++) {
-                    const int st = cnt % TCS16_NS;
-                    mbar_wait(smem_u32(conv_full + st), (cnt / TCS16_NS) & 1);
+                    const int sa = cnt % NA, sb = cnt % NB;
+                    mbar_wait(smem_u32(conv_full + sa), (cnt / NA) & 1);
+                    mbar_wait(smem_u32(b_full + sb), (cnt / NB) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n");
-                    const uint32_t ah0 = smem_u32(base + st * TCS16_STAGE), al0 = ah0 + TC16_OPB;
-                    const uint32_t bh0 = ah0 + TC16_CH, bl0 = bh0 + TC16_OPB;
+                    const uint32_t ah0 = smem_u32(sA + sa * TC16_CH), al0 = ah0 + TC16_OPB;
+                    const uint32_t bh0 = smem_u32(sB + sb * TC16_CH), bl0 = bh0 + TC16_OPB;
 #pragma unroll
                     for (int ks = 0; ks < TC16_KC / 16; ks++) {
                         const uint32_t off = ks * 32;
@@ -493,7 +505,10 @@ __global__ void __launch_bounds__(TCS16_T, 1)
                     }
                     asm volatile(
                         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                            smem_u32(empty + st)));
+                            smem_u32(a_empty + sa)));
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                            smem_u32(b_empty + sb)));
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                     smem_u32(t_full + ab)));

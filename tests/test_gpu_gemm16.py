@@ -152,3 +152,15 @@ def test_b2_tma_store_bitwise(ci):
     b0 = gpu_backward(G, w)
     G.set_option("b2_tmast", 1)
     assert np.array_equal(gpu_backward(G, w), b0)
+
+
+def test_b2_ring_depths_bitwise():
+    """The b2 GEMM's A / B ring depths (option b2_rings) change only the pipelining."""
+    cfg = make_config(1)
+    G = P.Geometry(cfg.desc())
+    w = rnd(G.g_shape, 1, 132)
+    out = []
+    for r in (0, 1, 2):
+        G.set_option("b2_rings", r)
+        out.append(gpu_backward(G, w))
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
