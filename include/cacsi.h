@@ -317,6 +317,8 @@ CACSI_API int32_t cacsi_kernel_times(const cacsi_geometry *geom, int32_t max, co
  * "pair_cache_records" (open pairs held in the pair cache, 0 if not built),
  * "pair_cache_record_bytes" (bytes per record: P, packed (b, tau), pixel q),
  * "pair_cache_tau_bits" (fraction bits of the stored tau),
+ * "pair_cache_padding_closed" (1: every padding record's pixel is closed for
+ * its voxel, so the forward adds its zero in place),
  * "pair_cache_fwd_row_blocks" (detector row blocks of the voxel-major
  * forward; 0 = the per-list forward runs),
  * "ts_rho" (0 = no translation symmetry), "energy_resolving".  -1 for an

@@ -163,6 +163,7 @@ const OptKey kOptKeys[] = {
     {"pcv_pf", &cacsi::Opts::pcv_pf, false, 0, 16},
     {"pcv_u", &cacsi::Opts::pcv_u, false, 4, 8},
     {"pcv_pipe", &cacsi::Opts::pcv_pipe, false, 0, 1},
+    {"pcv_padq", &cacsi::Opts::pcv_padq, false, 0, 1},
     {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
@@ -975,6 +976,7 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "pair_cache_window_base_bytes"))  // the 8-byte format's per-window pixel bases
         return g->esai.enabled && g->esai.pc && g->esai.pc_q8 ? 2 * (g->esai.pc_n / 128) : 0;
     if (!strcmp(key, "pair_cache_tau_bits")) return g->esai.enabled && g->esai.pc ? g->esai.pc_tbits : 0;
+    if (!strcmp(key, "pair_cache_padding_closed")) return g->esai.enabled && g->esai.pc ? g->esai.pc_padq : 0;
     if (!strcmp(key, "pair_cache_fwd_row_blocks"))
         return g->esai.enabled && g->esai.pc ? cacsi::pcv_row_blocks(g) : 0;
     if (!strcmp(key, "esai_ldw")) return g->esai.enabled ? g->esai.ldw : 0;

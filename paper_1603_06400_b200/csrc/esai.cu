@@ -1275,17 +1275,25 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
             E.pc_R = segR;
             const size_t smem = host_bp_bytes(E);
             const int gr = persistent_grid(g, smem, 256);
+            int *unsafe = nullptr;
+            e = cudaMalloc(&unsafe, sizeof(int));
+            if (e == cudaSuccess) e = cudaMemset(unsafe, 0, sizeof(int));
+            if (e != cudaSuccess) return e;
             if (jyb == 2) {
                 auto kf = sai ? k_pc_fill<true, uint16_t> : k_pc_fill<false, uint16_t>;
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint16_t *)g->d_pc_q);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint16_t *)g->d_pc_q, unsafe);
             } else {
                 auto kf = sai ? k_pc_fill<true, uint32_t> : k_pc_fill<false, uint32_t>;
                 cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint32_t *)g->d_pc_q);
+                kf<<<gr, 256, smem>>>(p, E, (uint32_t *)g->d_pc_bt, (float *)g->d_pc_P, (uint32_t *)g->d_pc_q, unsafe);
             }
             e = cudaDeviceSynchronize();
+            int hu = 1;
+            if (e == cudaSuccess) e = cudaMemcpy(&hu, unsafe, sizeof(int), cudaMemcpyDeviceToHost);
+            cudaFree(unsafe);
             if (e != cudaSuccess) return e;
+            E.pc_padq = (segR > 0 && hu == 0) ? 1 : 0;
             clk.mark(3);  // pair cache: count, scan, allocation, fill
             E.pcb_bt = E.pc_bt;
             E.pcb_P = E.pc_P;
@@ -1590,7 +1598,9 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
                 const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536 && !E.pc_q8;
-                auto kf = E.pc_q8 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, true>
+                const bool padq = E.pc_padq && o.pcv_padq && !geom && !E.pc_q8 && E.pc_qb == 2 && T == 1024 && o.pcv_pipe;
+                auto kf = padq ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, false, true>
+                        : E.pc_q8 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, true>
                                                : k_pc_fwd_v<uint16_t, 4, 512, false, true, true>)
                         : E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true>
                                                             : o.pcv_pipe ? k_pc_fwd_v<uint16_t, 4, 1024, false, true>

@@ -147,6 +147,7 @@ struct Esai {
     int pc_tb8;
     const uint16_t *pc_qbase;
     int pc_qb;                // bytes per q (2 or 4)
+    int pc_padq;              // every padding record's pixel is closed for its voxel (k_pc_fill)
     int stat_win_permille, stat_tile_permille;  // mean voxel window / 128-voxel tile K span, per mille of nb
 };
 
@@ -201,6 +202,7 @@ struct Opts {
     int pcv_items = 2;        // "pcv_items": voxel chunks per SM of the voxel-major forward
     int pcv_pf = 1;           // "pcv_pf": L2 prefetch distance (voxels) of the voxel-major forward
     int pcv_u = 4;            // "pcv_u": records per thread per step (4 or 8)
+    int pcv_padq = 1;         // "pcv_padq": 0 = the voxel-major forward redirects padding to dummy slots
     int pcv_pipe = 1;         // "pcv_pipe": 0 = the voxel-major forward without software-pipelined record loads
     int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance

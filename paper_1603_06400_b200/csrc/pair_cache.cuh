@@ -86,9 +86,15 @@ __global__ void k_pc_pad(const Params p, int R, int win, long long *__restrict__
 }
 
 // fill: one warp per list, 32 pixels per step, ballot-compacted records
+// Padding pixel (bank-ordered layout): a pixel of the segment's rows that is CLOSED for the
+// voxel -- no real record of the segment touches it, so the forward may add the padding's
+// zero there without a select (k_pc_fwd_v<..., PADQ>); the last list's row is searched
+// first, then the rows above it.  A segment with every pixel open keeps the list's first
+// pixel and raises *unsafe (the forward then keeps its dummy-slot select).
 template <bool SAI, typename QT>
 __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, uint32_t *__restrict__ bt,
-                                                 float *__restrict__ Pout, QT *__restrict__ qout) {
+                                                 float *__restrict__ Pout, QT *__restrict__ qout,
+                                                 int *__restrict__ unsafe) {
     const float tone = (float)(1u << e.pc_tbits);
     const uint32_t tmax = (1u << e.pc_tbits) - 1u;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -128,10 +134,23 @@ __global__ void __launch_bounds__(256) k_pc_fill(const Params p, const Esai e, u
         if (base < end) {
             const int2 win = e.vwin[v];
             const int span = max(1, win.y - win.x);
+            int padq = -1;
+            const int rs0 = e.pc_R > 0 ? (ix / e.pc_R) * e.pc_R : ix;
+            for (int r = ix; r >= rs0 && padq < 0; r--)
+                for (int jy0 = 0; jy0 < p.det_ny && padq < 0; jy0 += 32) {
+                    const int jy = jy0 + lane, q = r * p.det_ny + jy;
+                    const bool closed = jy < p.det_ny && !((__ldg(e.tb_bwd + (size_t)v * nw + (q >> 5)) >> (q & 31)) & 1u);
+                    const uint32_t m = __ballot_sync(FULL, closed);
+                    if (m) padq = r * p.det_ny + jy0 + __ffs(m) - 1;
+                }
+            if (padq < 0) {
+                padq = ix * p.det_ny;
+                if (lane == 0) atomicOr(unsafe, 1);
+            }
             for (long long o = base + lane; o < end; o += 32) {
                 bt[o] = ((uint32_t)(win.x + (int)((o - base) % span)) << e.pc_tbits) | tmax;
                 Pout[o] = 0.0f;
-                qout[o] = (QT)(ix * p.det_ny);
+                qout[o] = (QT)padq;
             }
         }
     }
@@ -388,7 +407,9 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
 // PIPE: the vector record loop is software-pipelined -- each thread's next 4 records are
 // loaded before the current 4 are deposited (two steps of loads in flight per thread).
 // Q8: 8-byte records (pixel = window base + 9-bit offset, tau in bits 9 .. 9 + pc_tb8)
-template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false, bool Q8 = false>
+// PADQ: every padding record's pixel is closed for its voxel (k_pc_fill, Esai.pc_padq):
+// its zero is added in place, without the select into the dummy slot.
+template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false, bool Q8 = false, bool PADQ = false>
 __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
@@ -481,43 +502,54 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                 for (int u = 0; u < U; u++) {
                     const int b = (int)(k[u] >> tb);
                     CACSI_CHECK(b >= (swin.x & ~3) && b + 1 < (swin.x & ~3) + wcap);
-                    CACSI_CHECK(P[u] == 0.0f || (q[u] >= (uint32_t)q0 && q[u] < (uint32_t)(q0 + nacc)));
+                    CACSI_CHECK((P[u] == 0.0f && !PADQ) || (q[u] >= (uint32_t)q0 && q[u] < (uint32_t)(q0 + nacc)));
                     const float wa = wv[b], wb = wv[b + 1];
                     const float t = Q8 ? (float)((k[u] >> 9) & tmask8) * tunit8 : (float)(k[u] & tmask) * tunit;
-                    float *ap = P[u] != 0.0f ? accq + q[u] : dummy;
+                    float *ap = PADQ ? accq + q[u] : P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
             };
             if (vec && PIPE && U == 4 && sizeof(QT) == 2) {
-                int i = 4 * tid;
-                uint4 kv = make_uint4(0u, 0u, 0u, 0u);
-                float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
-                uint2 qv = make_uint2(0u, 0u);
-                auto ld = [&](int j) {
-                    kv = __ldg((const uint4 *)(kb + j));
-                    if (!GEOM) pv = __ldg((const float4 *)(Pb + j));
-                    if (Q8)  // the warp's 128 records are one window: one base per warp step
-                        qv.x = __ldg(e.pc_qbase + ((o0 + j) >> 7));
-                    else
-                        qv = __ldg((const uint2 *)(qb + j));
+                // two register sets (A, B) in ping-pong: the next step's loads land in the
+                // set not being deposited, with no register copies between steps
+                struct Rec4 {
+                    uint4 k;
+                    float4 P;
+                    uint2 q;
                 };
-                if (i < n) ld(i);
-                for (; i < n; i += 4 * PCV_T) {
-                    const uint4 ck = kv;
-                    const float4 cp = pv;
-                    const uint2 cq = qv;
-                    if (i + 4 * PCV_T < n) ld(i + 4 * PCV_T);
+                auto ld = [&](Rec4 &r, int j) {
+                    r.k = __ldg((const uint4 *)(kb + j));
+                    if (!GEOM) r.P = __ldg((const float4 *)(Pb + j));
+                    if (Q8)  // the warp's 128 records are one window: one base per warp step
+                        r.q.x = __ldg(e.pc_qbase + ((o0 + j) >> 7));
+                    else
+                        r.q = __ldg((const uint2 *)(qb + j));
+                };
+                auto dep = [&](const Rec4 &r) {
                     uint32_t k[U], q[U];
                     float P[U];
-                    k[0] = ck.x, k[1] = ck.y, k[2] = ck.z, k[3] = ck.w;
-                    P[0] = cp.x, P[1] = cp.y, P[2] = cp.z, P[3] = cp.w;
+                    k[0] = r.k.x, k[1] = r.k.y, k[2] = r.k.z, k[3] = r.k.w;
+                    P[0] = r.P.x, P[1] = r.P.y, P[2] = r.P.z, P[3] = r.P.w;
                     if (Q8) {
 #pragma unroll
-                        for (int u = 0; u < 4; u++) q[u] = cq.x + (k[u] & 511u);
+                        for (int u = 0; u < 4; u++) q[u] = r.q.x + (k[u] & 511u);
                     } else {
-                        q[0] = cq.x & 0xFFFFu, q[1] = cq.x >> 16, q[2] = cq.y & 0xFFFFu, q[3] = cq.y >> 16;
+                        q[0] = r.q.x & 0xFFFFu, q[1] = r.q.x >> 16, q[2] = r.q.y & 0xFFFFu, q[3] = r.q.y >> 16;
                     }
                     deposit(k, P, q);
+                };
+                constexpr int ST = 4 * PCV_T;
+                Rec4 ra, rb;
+                ra.P = rb.P = make_float4(0.f, 0.f, 0.f, 0.f);
+                ra.q = rb.q = make_uint2(0u, 0u);
+                int i = 4 * tid;
+                if (i < n) ld(ra, i);
+                for (; i < n; i += 2 * ST) {
+                    if (i + ST < n) ld(rb, i + ST);
+                    dep(ra);
+                    if (i + ST >= n) break;
+                    if (i + 2 * ST < n) ld(ra, i + 2 * ST);
+                    dep(rb);
                 }
             } else if (vec) {
                 // bank-ordered layout: the voxel's range is whole 128-record windows (n % 128 == 0),

@@ -163,3 +163,22 @@ def test_8_byte_records_match_10_byte(ci):
         assert_parity(gpu_backward(G8, w), O.backward(w), "c1 8-byte backward")
     G8.close()
     G10.close()
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_padding_pixels_closed_bitwise(ci):
+    """Padding records carry a pixel that is closed for their voxel (k_pc_fill), so the
+    voxel-major forward adds their zero in place (pcv_padq=1, the default) -- the same
+    bits as redirecting them to the dummy slots (pcv_padq=0)."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    assert G.query("pair_cache_padding_closed") == 1
+    f = torch.as_tensor(cfg.f).cuda()
+    out = []
+    for v in (1, 0):
+        G.set_option("pcv_padq", v)
+        g = torch.empty(G.g_shape, device="cuda")
+        G.forward(f, g)
+        torch.cuda.synchronize()
+        out.append(g)
+    assert torch.equal(out[0], out[1])
