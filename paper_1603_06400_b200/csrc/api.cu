@@ -169,6 +169,7 @@ const OptKey kOptKeys[] = {
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},
+    {"er_fwd_reg", &cacsi::Opts::er_fwd_reg, false, 0, 1},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},
 };
 

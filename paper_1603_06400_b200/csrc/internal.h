@@ -208,6 +208,7 @@ struct Opts {
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
     int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
+    int er_fwd_reg = 1;       // "er_fwd_reg": 0 = the direct energy-resolving forward with shared-memory accumulators
     int er_fwd = 0;           // "er_fwd" (er_cache=1 only): 1 = the compacted pair-cache forward k_er_fwd2
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
 };

@@ -14,6 +14,7 @@
 // atomics); the columns are summed in fp64 at the end.
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "pair.cuh"
 
@@ -130,6 +131,89 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
             const int px = i / K, k = i - px * K;
             const float2 a2 = acc2[(k >> 1) * FWD_T + px];
             out[i] = en[k].y * ((k & 1) ? a2.y : a2.x);
+        }
+    }
+}
+
+// Energy-resolving forward with the per-pixel energy sums in REGISTERS: acc[KR] (KR >= ne, a
+// multiple of 8, fully unrolled), alpha_k as compile-time-indexed kernel parameters
+// (constant-bank operands), energy blocks of 8 outside the warp's window union skipped by a
+// warp-uniform branch.  The same arithmetic in the same order per (pixel, energy) as
+// k_forward<true> (acc = fmaf(P, hat, acc) voxel by voxel), without its shared-memory
+// read-modify-write per two terms; the final [pixels][ne] block is staged through shared
+// memory for coalesced stores.  Option er_fwd_reg.
+constexpr int KR_MAX = 128;
+struct AlphaTab {
+    float a[KR_MAX];  // alpha_k for k < ne, 1e30 (clamps onto the zero table entry) beyond
+};
+template <int KR>
+__global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const float *__restrict__ f,
+                                                          int vox_per_split, float *__restrict__ partial,
+                                                          const AlphaTab at) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne, Q3 = Q + 3;
+    float2 *tab = (float2 *)smem4;  // [VC][Q + 3] (mid, slope), entry n at index n + 2; reused to stage the output
+    const int tid = threadIdx.x;
+    const int pix = blockIdx.x * FWD_T + tid;
+    const bool valid = pix < p.n_det;
+    const float2 d = p.det[valid ? pix : 0];
+    const int v0 = blockIdx.y * vox_per_split;
+    const int v1 = min(p.n_vox, v0 + vox_per_split);
+    float acc[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) acc[k] = 0.0f;
+    for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
+        const int nc = min(FWD_VC, v1 - c0);
+        __syncthreads();
+        for (int i = tid; i < nc * Q3; i += FWD_T) {
+            const int vv = i / Q3, n = i - vv * Q3 - 2;
+            const float *fr = f + (size_t)(c0 + vv) * Q;
+            const float a = (n >= 0 && n < Q) ? fr[n] : 0.0f;
+            const float b = (n + 1 >= 0 && n + 1 < Q) ? fr[n + 1] : 0.0f;
+            tab[i] = make_float2(0.5f * (a + b), b - a);
+        }
+        __syncthreads();
+        for (int vv = 0; vv < nc; vv++) {
+            const int v = c0 + vv;
+            const VoxelRec vr = p.vox[v];
+            const bool open = valid && mask_open(p, v, pix, vr, d);
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1;
+            if (open) {
+                pair_geom(p, vr, d, P, sh);
+                k_range(p, sh, klo, khi);
+            }
+            const int wlo = __reduce_min_sync(FULL, klo);
+            const int whi = __reduce_max_sync(FULL, khi);
+            const float2 *tv = tab + vv * Q3 + 2;
+#pragma unroll
+            for (int kb = 0; kb < KR; kb += 8) {
+                if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    float tt;
+                    const int n = hat_coord(p, at.a[kb + j], sh, tt);
+                    CACSI_CHECK(n >= -2 && n <= Q);
+                    const float2 t = tv[n];
+                    acc[kb + j] = fmaf(P, fmaf(tt, t.y, t.x), acc[kb + j]);
+                }
+            }
+        }
+    }
+    // [pixels][K] block of this CTA through shared memory (coalesced stores), scaled by c_k
+    float *stage = (float *)smem4;
+    const int npx = min(FWD_T, p.n_det - (int)blockIdx.x * FWD_T);
+    float *out = partial + ((size_t)blockIdx.y * p.n_det + (size_t)blockIdx.x * FWD_T) * K;
+    for (int kb = 0; kb < KR; kb += 32) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            if (kb + j < KR) stage[j * (FWD_T + 1) + tid] = acc[kb + j];
+        __syncthreads();
+        const int kn = min(32, K - kb);
+        for (int i = tid; i < npx * kn; i += FWD_T) {
+            const int px = i / kn, k = i - px * kn;
+            out[(size_t)px * K + kb + k] = p.energy[kb + k].y * stage[k * (FWD_T + 1) + px];
         }
     }
 }
@@ -363,7 +447,25 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
     if (e != cudaSuccess) return e;
     dim3 grid(tiles, S);
-    if (res) {
+    if (res && g->opt.er_fwd_reg && p.ne <= KR_MAX) {
+        // register accumulators: the smallest instantiated KR >= ne
+        AlphaTab at;
+        std::vector<float2> en(p.ne);
+        e = cudaMemcpy(en.data(), p.energy, p.ne * sizeof(float2), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(part, s);
+            return e;
+        }
+        for (int k = 0; k < KR_MAX; k++) at.a[k] = k < p.ne ? en[k].x : 1e30f;
+        auto kf = p.ne <= 16 ? k_forward_reg<16> : p.ne <= 32 ? k_forward_reg<32> : p.ne <= 64 ? k_forward_reg<64>
+                : p.ne <= 104 ? k_forward_reg<104> : k_forward_reg<128>;
+        const size_t sm2 = std::max((size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2), (size_t)32 * (FWD_T + 1) * sizeof(float));
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        {
+            KScope kt_(g, s, "k_forward_er");
+            kf<<<grid, FWD_T, sm2, s>>>(p, f, vps, (float *)part, at);
+        }
+    } else if (res) {
         cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         {
             KScope kt_(g, s, "k_forward_er");
