@@ -39,3 +39,4 @@ def test_er_forward_registers_non_uniform_energies():
     G.set_option("er_fwd_reg", 0)
     assert np.array_equal(g1, gpu_forward(G, f))
     assert_parity(g1, oracle.Geometry(d).forward(f), "er forward registers, non-uniform energies")
+
