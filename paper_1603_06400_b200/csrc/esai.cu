@@ -1697,6 +1697,27 @@ static bool tmap_rows_f32(CUtensorMap *tm, const float *base, uint64_t rows, uin
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over the split-K partials C[S][rows][cols] (box 32 x 32 x 1, SWIZZLE_128B): a
+// store of tile rows past `rows` is clipped inside its own split instead of landing in the
+// next split's first rows
+static bool tmap_parts_f32(CUtensorMap *tm, const float *base, uint64_t S, uint64_t rows, uint64_t cols) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            enc = nullptr;
+        if (!enc) return false;
+    }
+    const cuuint64_t dims[3] = {cols, rows, S};
+    const cuuint64_t strides[2] = {cols * sizeof(float), rows * cols * sizeof(float)};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const uint32_t *pmask, float *b,
                                  cudaStream_t s, int *launches, const int32_t *list, int n_list,
                                  const BwdUpdateEpi *epi) {
@@ -1777,7 +1798,7 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 CUtensorMap tmP;
                 memset(&tmP, 0, sizeof(tmP));
                 const bool tmast = o.b2_tmast && (p.nq % 4) == 0 &&
-                                   tmap_rows_f32(&tmP, part, (uint64_t)S_eff * p.n_vox, (uint64_t)p.nq, (uint64_t)p.nq, 32);
+                                   tmap_parts_f32(&tmP, part, (uint64_t)S_eff, (uint64_t)p.n_vox, (uint64_t)p.nq);
                 // A / B ring depths (option b2_rings: 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4)
                 const int na = o.b2_rings == 1 ? 4 : o.b2_rings == 2 ? 2 : 3, nbr = 6 - na;
                 auto ks = tmast ? (na == 4 ? k_tc_gemm_splitk16<true, 4, 2> : na == 2 ? k_tc_gemm_splitk16<true, 2, 4>

@@ -349,8 +349,9 @@ __global__ void __launch_bounds__(TCA16_T, 1)
 // from L2.  Warp 8 lane 0 produces A, warp 10 lane 0 produces B, warp 9 lane 0 issues 12
 // MMAs per 64-wide chunk, warps 0-3 drain with the output scale 2^-(ea + bexp).  ea comes
 // from the fixed-point bound vbmax max|w| (the device scalar *wmax the backward used).
-// TMAST: the partials are stored by TMA tensor stores (tmC over C as [nsplit M][ldc],
-// box 32 x 32, SWIZZLE_128B) from two 4 KB staging buffers per epilogue warp.
+// TMAST: the partials are stored by TMA tensor stores (tmC: a 3-D map over C as
+// [nsplit][M][ldc], box 32 x 32 x 1, SWIZZLE_128B, so rows past M are clipped inside their
+// split) from two 4 KB staging buffers per epilogue warp.
 constexpr int TCS16_T = 352;
 constexpr int tcs16_smem(bool tmast, int na, int nb) {
     return (na + nb) * TC16_CH + (tmast ? 4 * 2 * 32 * 32 * 4 : 4 * 32 * 33 * 4) + 1024 + 256;
@@ -554,8 +555,8 @@ __global__ void __launch_bounds__(TCS16_T, 1)
                     __syncwarp();
                     if (lane == 0) {
                         asm volatile(
-                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(&tmC),
-                            "r"(c0), "r"(z * M + m0 + warp * 32), "r"(smem_u32(bb))
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(&tmC),
+                            "r"(c0), "r"(m0 + warp * 32), "r"(z), "r"(smem_u32(bb))
                             : "memory");
                         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                     }

@@ -164,3 +164,18 @@ def test_b2_ring_depths_bitwise():
         G.set_option("b2_rings", r)
         out.append(gpu_backward(G, w))
     assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+def test_b2_tma_store_split_boundaries():
+    """n_vox not a multiple of 128: the last M tile of every split overhangs into the next
+    split's rows, which the 3-D tensor map clips per split (a 2-D map over [S M][nq] let
+    those zero rows land in the next split's partials, a race).  Repeated, against the
+    per-lane stores."""
+    d = make_config(0).desc()
+    d.update(ny=5, nz=7, nq=40, det_nx=9, det_ny=23)
+    G = P.Geometry(d, options="b2_tmast=0")
+    w = rnd(G.g_shape, 0, 133)
+    ref = gpu_backward(G, w)
+    G.set_option("b2_tmast", 1)
+    for _ in range(30):
+        assert np.array_equal(gpu_backward(G, w), ref)
