@@ -756,7 +756,21 @@ struct EpiUpdate {
         f_new[i] = update_at(p, f_hat, b1, (float)t, beta, delta, (unsigned)i);
         return 0.0f;
     }
+    // four consecutive elements of one voxel (k_sum_parts_v4 when nq % 4 == 0): the same bits
+    __device__ bool quad(size_t i0, double t0, double t1, double t2, double t3) const {
+        if (p.nq % 4 != 0) return false;
+        *(float4 *)(f_new + i0) = update_at4(p, f_hat, b1, make_float4((float)t0, (float)t1, (float)t2, (float)t3), beta,
+                                             delta, (unsigned)i0);
+        return true;
+    }
 };
+template <class Epi>
+__device__ __forceinline__ bool epi_quad(const Epi &epi, size_t i0, double t0, double t1, double t2, double t3) {
+    if constexpr (std::is_same<Epi, EpiUpdate>::value)
+        return epi.quad(i0, t0, t1, t2, t3);
+    else
+        return false;
+}
 template <class Epi>
 __device__ __forceinline__ void epi_max(const Epi &epi, float m) {
     if constexpr (Epi::kMax) {
@@ -848,6 +862,7 @@ __global__ void __launch_bounds__(256) k_sum_parts_v4(const float *__restrict__ 
             const float4 x = __ldcs(p4 + (size_t)j * n4);
             s0 += (double)x.x, s1 += (double)x.y, s2 += (double)x.z, s3 += (double)x.w;
         }
+        if (epi_quad(epi, 4 * i4, s0, s1, s2, s3)) continue;
         m = fmaxf(m, epi(4 * i4, s0));
         m = fmaxf(m, epi(4 * i4 + 1, s1));
         m = fmaxf(m, epi(4 * i4 + 2, s2));
