@@ -166,6 +166,7 @@ const OptKey kOptKeys[] = {
     {"pcv_padq", &cacsi::Opts::pcv_padq, false, 0, 1},
     {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
+    {"pcb_pfl1", &cacsi::Opts::pcb_pfl1, false, 0, 1},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},

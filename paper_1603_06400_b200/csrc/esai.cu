@@ -1773,7 +1773,8 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 // and 2/3 stages with the vector mapping): ~69 KB with the histogram, 3 CTAs/SM
                 constexpr int U = 4, T = 512, NS = 2;
                 auto kb = E.pc_q8 ? k_pc_bwd_tma<uint16_t, T, U, NS, true>
-                        : E.pc_qb == 2 ? k_pc_bwd_tma<uint16_t, T, U, NS> : k_pc_bwd_tma<uint32_t, T, U, NS>;
+                        : E.pc_qb == 2 ? (o.pcb_pfl1 ? k_pc_bwd_tma<uint16_t, T, U, NS, false, true> : k_pc_bwd_tma<uint16_t, T, U, NS>)
+                                       : k_pc_bwd_tma<uint32_t, T, U, NS>;
                 const size_t sm = (size_t)NS * (T * U * (8 + (E.pc_q8 ? 0 : E.pc_qb)) + (E.pc_q8 ? ((T * U / 128 + 14) & ~7) * 2 : 0)) +
                                   2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -206,6 +206,7 @@ struct Opts {
     int pcv_pipe = 1;         // "pcv_pipe": 0 = the voxel-major forward without software-pipelined record loads
     int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
+    int pcb_pfl1 = 1;         // "pcb_pfl1": 0 = the ring backward does not prefetch the next chunk's w lines into L1
     int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
     int er_fwd_reg = 1;       // "er_fwd_reg": 0 = the direct energy-resolving forward with shared-memory accumulators

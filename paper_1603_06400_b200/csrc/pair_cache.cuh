@@ -671,7 +671,10 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 // deposit.  Same deposits and order-free integer sums as k_pc_bwd.
 // Q8: 8-byte records -- the stage holds (b, tau, pixel offset) and P only; each warp's 128
 // records are one window, whose pixel base it reads once per chunk
-template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool Q8 = false>
+// PFL1: warp 1 peeks at the NEXT ring stage (non-blocking); if it has landed, its lanes
+// sample 32 of its records' pixels and prefetch the w lines between their min and max into
+// L1 (prefetch.global.L1), so the next chunk's gathers can hit L1 (option pcb_pfl1).
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool Q8 = false, bool PFL1 = false>
 __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
@@ -807,6 +810,26 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                             P[u] = 0.0f;
                             q[u] = 0u;
                         }
+                    }
+                }
+            }
+            if (PFL1 && !Q8 && (tid >> 5) == 1 && PBT_NS >= 2) {
+                const int st2 = (consumed + 1) % PBT_NS;
+                uint32_t landed;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(landed)
+                    : "r"(smem_u32(full + st2)), "r"(((consumed + 1) / PBT_NS) & 1)
+                    : "memory");
+                if (landed) {
+                    const QT *qn = (const QT *)(smb + st2 * SB + PBT_CH * 8);
+                    const uint32_t qs = (uint32_t)qn[(tid & 31) * (PBT_CH / 32)];
+                    const uint32_t qlo = __reduce_min_sync(0xFFFFFFFFu, qs), qhi = __reduce_max_sync(0xFFFFFFFFu, qs);
+                    if (qhi >= qlo && qhi < (uint32_t)p.n_det && qhi - qlo < 16384u) {
+                        const uintptr_t l0 = (uintptr_t)(w + qlo) & ~(uintptr_t)127, l1 = (uintptr_t)(w + qhi);
+                        for (uintptr_t ad = l0 + 128 * (tid & 31); ad <= l1; ad += 128 * 32)
+                            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(ad));
                     }
                 }
             }

@@ -182,3 +182,15 @@ def test_padding_pixels_closed_bitwise(ci):
         torch.cuda.synchronize()
         out.append(g)
     assert torch.equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_backward_l1_prefetch_bitwise(ci):
+    """The ring backward's L1 prefetch of the next chunk's w lines (pcb_pfl1=1, the default)
+    changes no arithmetic: the same bits as without it."""
+    cfg = make_config(ci)
+    G = P.Geometry(cfg.desc())
+    w = rnd(G.g_shape, ci, 76)
+    b1 = gpu_backward(G, w)
+    G.set_option("pcb_pfl1", 0)
+    assert np.array_equal(gpu_backward(G, w), b1)
