@@ -359,7 +359,7 @@ def run_gpu(args):
     if kpc:
         kd = max(kpc, key=lambda k: kern[k]["avg_ms"])
         ldw = G.query("esai_ldw")
-        nrec = G.query("pair_cache_records")
+        nrec = G.query("pair_cache_padded_records")  # records streamed, padding included
         tab = cfg.n_vox * ldw * 4 if kd == "k_pc_fwd" else cfg.n_det * 4 + cfg.n_vox * ldw * 4
         rb = G.query("pair_cache_record_bytes")
         bytes_ = float(rb) * nrec + 8.0 * cfg.n_vox * cfg.det_nx + tab + float(G.query("pair_cache_window_base_bytes"))
@@ -373,7 +373,7 @@ def run_gpu(args):
                         "bytes_note": f"{rb} B per record (pair cache, incl. padding) + 2 B per 128-record window "
                                       "(pixel bases) + list offsets + the gathered table once (DESIGN.md §8)"}
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r2k_dram_traffic.json")))["kernels"]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r2q8_dram_traffic.json")))["kernels"]
             if kd in tr:
                 roofline_hbm["traffic"] = tr[kd]["dram_read_bytes"] + tr[kd]["dram_write_bytes"]
         except Exception:

@@ -133,7 +133,9 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * Create-time keys: pair_cache (1; 0 = recompute the pair geometry per call),
  * ts (1; 0 = no translation-symmetric on-the-fly forward), direct (0; 1 = the
  * per-term kernels instead of ESAI), pc_plain (0; 1 = list-ordered unpadded
- * pair cache), pc_segwin (1), pcv_budget_kb (200), er_cache (0; 1 = the
+ * pair cache), pc_segwin (1), pc_q8 (2: 8-byte records, P rounded to 28 bits
+ * carrying 4 pixel-offset bits; 1: 10-bit tau; 0: 10-byte records), pc_win
+ * (128), pcv_budget_kb (200), er_cache (0; 1 = the
  * energy-resolving operators from a pair cache).  Per-call keys (also
  * settable with cacsi_set_option): wgemm (0 A-resident, 1 CTA-pair, 2 per-tile),
  * wgemm_pack, b2gemm_tiles, pc_fwd_list, pcv_items, pcv_pf, pcv_u, pc_bwd_flat,

@@ -146,7 +146,7 @@ const OptKey kOptKeys[] = {
     {"pc_plain", &cacsi::Opts::pc_plain, true, 0, 1},
     {"pc_segwin", &cacsi::Opts::pc_segwin, true, 0, 1},
     {"pc_win", &cacsi::Opts::pc_win, true, 128, 512},
-    {"pc_q8", &cacsi::Opts::pc_q8, true, 0, 1},
+    {"pc_q8", &cacsi::Opts::pc_q8, true, 0, 2},
     {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
     {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
@@ -167,6 +167,8 @@ const OptKey kOptKeys[] = {
     {"pc_bwd_flat", &cacsi::Opts::pc_bwd_flat, false, 0, 1},
     {"pcb_pf", &cacsi::Opts::pcb_pf, false, 0, 64},
     {"pcb_pfl1", &cacsi::Opts::pcb_pfl1, false, 0, 1},
+    {"pcb_ctas", &cacsi::Opts::pcb_ctas, false, 0, 8},
+    {"pcb_carve", &cacsi::Opts::pcb_carve, false, 0, 100},
     {"subset_bwd_mask", &cacsi::Opts::subset_bwd_mask, false, 0, 1},
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},

@@ -1353,8 +1353,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                 // 8-byte records: a 9-bit pixel offset per record and a base per 128-record
                 // window, if every window's pixel span fits and tau keeps >= 9 bits
                 E.pc_q8 = 0;
-                E.pc_tb8 = E.pc_tbits - 9;
-                if (g->opt.pc_q8 && jyb == 2 && E.pc_tb8 >= 9 && (nrec % 128) == 0) {
+                const int q8mode = g->opt.pc_q8;
+                E.pc_tb8 = q8mode == 2 ? E.pc_tbits - 5 : E.pc_tbits - 9;
+                if (q8mode && jyb == 2 && E.pc_tb8 >= 9 && (nrec % 128) == 0) {
                     const long long nwin = nrec / 128;
                     unsigned *span = nullptr;
                     unsigned hs = 0;
@@ -1370,9 +1371,9 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                         e = cudaMalloc(&g->d_pc_qbase, (size_t)(nwin + 32) * sizeof(uint16_t));
                         if (e == cudaSuccess) e = cudaMemset(g->d_pc_qbase, 0, (size_t)(nwin + 32) * sizeof(uint16_t));
                         if (e == cudaSuccess) {
-                            k_pc_pack8<<<8 * sm_count(g->device), 256>>>(nwin, E.pc_tbits, E.pc_tb8,
+                            k_pc_pack8<<<8 * sm_count(g->device), 256>>>(nwin, E.pc_tbits, E.pc_tb8, q8mode,
                                                                           (const uint16_t *)g->d_pc_q, (uint32_t *)g->d_pc_bt,
-                                                                          (uint16_t *)g->d_pc_qbase);
+                                                                          (float *)g->d_pc_P, (uint16_t *)g->d_pc_qbase);
                             e = cudaDeviceSynchronize();
                         }
                         if (e == cudaSuccess) {
@@ -1380,7 +1381,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                             g->d_pc_q = nullptr;
                             E.pc_q = E.pcb_q = nullptr;
                             E.pc_qbase = (const uint16_t *)g->d_pc_qbase;
-                            E.pc_q8 = 1;
+                            E.pc_q8 = q8mode;
                         }
                     }
                     if (e != cudaSuccess) return e;
@@ -1613,10 +1614,14 @@ static cudaError_t esai_forward_impl(const cacsi_geometry *g, const float *f, co
                 // (768 threads x 8 records per thread measured slower: 1.23 vs 1.13 ms)
                 const int T = cps == 1 ? 1024 : 512;
                 const bool geom = o.pc_fwd_geom && E.pc_qb == 2 && p.n_det <= 65536 && !E.pc_q8;
-                const bool padq = E.pc_padq && o.pcv_padq && !geom && !E.pc_q8 && E.pc_qb == 2 && T == 1024 && o.pcv_pipe;
-                auto kf = padq ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, false, true>
-                        : E.pc_q8 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, true>
-                                               : k_pc_fwd_v<uint16_t, 4, 512, false, true, true>)
+                const bool padq = E.pc_padq && o.pcv_padq && !geom && E.pc_qb == 2 && T == 1024 && o.pcv_pipe;
+                auto kf = padq ? (E.pc_q8 == 2 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, 2, true>
+                                  : E.pc_q8 == 1 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, 1, true>
+                                                 : k_pc_fwd_v<uint16_t, 4, 1024, false, true, 0, true>)
+                        : E.pc_q8 == 2 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, 2>
+                                                    : k_pc_fwd_v<uint16_t, 4, 512, false, true, 2>)
+                        : E.pc_q8 ? (T == 1024 ? k_pc_fwd_v<uint16_t, 4, 1024, false, true, 1>
+                                               : k_pc_fwd_v<uint16_t, 4, 512, false, true, 1>)
                         : E.pc_qb == 2 ? (T == 1024 ? (geom ? k_pc_fwd_v<uint16_t, 4, 1024, true>
                                                             : o.pcv_pipe ? k_pc_fwd_v<uint16_t, 4, 1024, false, true>
                                                                          : k_pc_fwd_v<uint16_t, 4, 1024>)
@@ -1772,14 +1777,19 @@ cudaError_t esai_backward_masked(const cacsi_geometry *g, const float *w, const 
                 // 512 threads x 4 records, two stages (measured best of 128/256/512/1024 threads
                 // and 2/3 stages with the vector mapping): ~69 KB with the histogram, 3 CTAs/SM
                 constexpr int U = 4, T = 512, NS = 2;
-                auto kb = E.pc_q8 ? k_pc_bwd_tma<uint16_t, T, U, NS, true>
-                        : E.pc_qb == 2 ? (o.pcb_pfl1 ? k_pc_bwd_tma<uint16_t, T, U, NS, false, true> : k_pc_bwd_tma<uint16_t, T, U, NS>)
+                auto kb = E.pc_q8 == 2 ? (o.pcb_pfl1 ? k_pc_bwd_tma<uint16_t, T, U, NS, 2, true> : k_pc_bwd_tma<uint16_t, T, U, NS, 2>)
+                        : E.pc_q8 ? (o.pcb_pfl1 ? k_pc_bwd_tma<uint16_t, T, U, NS, 1, true> : k_pc_bwd_tma<uint16_t, T, U, NS, 1>)
+                        : E.pc_qb == 2 ? (o.pcb_pfl1 ? k_pc_bwd_tma<uint16_t, T, U, NS, 0, true> : k_pc_bwd_tma<uint16_t, T, U, NS>)
                                        : k_pc_bwd_tma<uint32_t, T, U, NS>;
                 const size_t sm = (size_t)NS * (T * U * (8 + (E.pc_q8 ? 0 : E.pc_qb)) + (E.pc_q8 ? ((T * U / 128 + 14) & ~7) * 2 : 0)) +
                                   2 * NS * sizeof(uint64_t) + hs;
                 cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                // (options pcb_ctas / pcb_carve: CTAs per SM and the shared-memory carveout
+                // preference -- fewer CTAs leave more of the SM's 256 KB to L1 for the w gathers)
+                if (o.pcb_carve > 0) cudaFuncSetAttribute(kb, cudaFuncAttributePreferredSharedMemoryCarveout, o.pcb_carve);
                 int nb = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kb, T, sm);
+                if (o.pcb_ctas > 0) nb = std::min(nb, o.pcb_ctas);
                 kb<<<std::min(p.n_vox, std::max(1, nb) * sm_count(g->device)), T, sm, s>>>(p, E, w, wmax, A);
             } else {
             const int pf = o.pcb_pf;  // rolling L2 prefetch (steps ahead)

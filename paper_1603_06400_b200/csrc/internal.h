@@ -143,8 +143,8 @@ struct Esai {
     // 8-byte records (pc_q8): the pixel is stored as a 9-bit offset (bits 0-8) from a per-window
     // base (pc_qbase, one uint16 per 128-record window) and tau keeps pc_tb8 bits (bits 9 ..),
     // b stays at bit pc_tbits; the pixel array pc_q is then not kept
-    int pc_q8;
-    int pc_tb8;
+    int pc_q8;                // 0: 10-byte records; 1, 2: 8-byte (k_pc_pack8 MODE)
+    int pc_tb8;               // tau bits of the 8-byte records (at bit 9 in mode 1, bit 5 in mode 2)
     const uint16_t *pc_qbase;
     int pc_qb;                // bytes per q (2 or 4)
     int pc_padq;              // every padding record's pixel is closed for its voxel (k_pc_fill)
@@ -185,7 +185,7 @@ struct Opts {
     int pc_plain = 0;         // "pc_plain": 1 = pair cache in list order, unpadded
     int pc_segwin = 1;        // "pc_segwin": 0 = stage whole voxel windows in the forward
     int pc_win = 128;         // "pc_win": records per bank-aware permutation window (128, 256, 512)
-    int pc_q8 = 0;            // "pc_q8": 1 = packed 8-byte records (pixel offset from a per-window base, 10-bit tau)
+    int pc_q8 = 2;            // "pc_q8": 8-byte records (pixel offset from a per-window base): 1 = 10-bit tau; 2 = P rounded to 28 bits carrying 4 offset bits, tau with tbits - 5 bits
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     // per call (cacsi_set_option may change them between calls)
@@ -206,6 +206,8 @@ struct Opts {
     int pcv_pipe = 1;         // "pcv_pipe": 0 = the voxel-major forward without software-pipelined record loads
     int pc_bwd_flat = 0;      // "pc_bwd_flat": 1 = register-fed pair-cache backward
     int pcb_pf = 2;           // "pcb_pf": its rolling L2 prefetch distance
+    int pcb_ctas = 0;         // "pcb_ctas": ring-backward CTAs per SM (0: as many as fit)
+    int pcb_carve = 0;        // "pcb_carve": its shared-memory carveout preference in percent (0: the driver's)
     int pcb_pfl1 = 1;         // "pcb_pfl1": 0 = the ring backward does not prefetch the next chunk's w lines into L1
     int subset_bwd_mask = 0;  // "subset_bwd_mask": 1 = bitmap-masked subset backward
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction

@@ -361,8 +361,12 @@ __global__ void k_pc_qspan(long long nwin, const uint16_t *__restrict__ q, unsig
         if (lane == 0) atomicMax(maxspan, hi - lo);
     }
 }
-__global__ void k_pc_pack8(long long nwin, int tbits, int tb8, const uint16_t *__restrict__ q, uint32_t *bt,
-                           uint16_t *__restrict__ qbase) {
+// MODE 1: (b | tau in tb8 = tbits - 9 bits at bit 9 | 9-bit pixel offset), P unchanged.
+// MODE 2 ("P-packed"): P rounded to 28 bits (19 explicit mantissa bits, relative error
+// <= 2^-20) carries the offset's low 4 bits in its low nibble; the b word keeps tau with
+// tb8 = tbits - 5 bits at bit 5 and the offset's high 5 bits in bits 0-4 (reading R23).
+__global__ void k_pc_pack8(long long nwin, int tbits, int tb8, int mode, const uint16_t *__restrict__ q, uint32_t *bt,
+                           float *Pr, uint16_t *__restrict__ qbase) {
     const int lane = threadIdx.x & 31, sh = tbits - tb8;
     const uint32_t tmax8 = (1u << tb8) - 1u, tmask = (1u << tbits) - 1u;
     for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < nwin;
@@ -372,14 +376,35 @@ __global__ void k_pc_pack8(long long nwin, int tbits, int tb8, const uint16_t *_
         const unsigned lo = __reduce_min_sync(0xFFFFFFFFu, min(min(qq[0], qq[1]), min(qq[2], qq[3])));
         uint4 k = *(const uint4 *)(bt + w * 128 + 4 * lane);
         uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+        if (mode == 2) {
+            float4 pv = *(const float4 *)(Pr + w * 128 + 4 * lane);
+            float pp[4] = {pv.x, pv.y, pv.z, pv.w};
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const uint32_t t8 = min(((kk[u] & tmask) + (1u << (sh - 1))) >> sh, tmax8);
-            kk[u] = (kk[u] & ~tmask) | (t8 << 9) | (qq[u] - lo);
+            for (int u = 0; u < 4; u++) {
+                const uint32_t off = qq[u] - lo;
+                const uint32_t t8 = min(((kk[u] & tmask) + (1u << (sh - 1))) >> sh, tmax8);
+                kk[u] = (kk[u] & ~tmask) | (t8 << 5) | (off >> 4);
+                const uint32_t pb = (__float_as_uint(pp[u]) + 0x8u) & 0xFFFFFFF0u;  // P >= 0: round to 28 bits
+                pp[u] = __uint_as_float(pb | (off & 0xFu));
+            }
+            *(float4 *)(Pr + w * 128 + 4 * lane) = make_float4(pp[0], pp[1], pp[2], pp[3]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t t8 = min(((kk[u] & tmask) + (1u << (sh - 1))) >> sh, tmax8);
+                kk[u] = (kk[u] & ~tmask) | (t8 << 9) | (qq[u] - lo);
+            }
         }
         *(uint4 *)(bt + w * 128 + 4 * lane) = make_uint4(kk[0], kk[1], kk[2], kk[3]);
         if (lane == 0) qbase[w] = (uint16_t)lo;
     }
+}
+// 8-byte record decode: the pixel offset from the window base and P (MODE from Esai.pc_q8)
+__device__ __forceinline__ uint32_t q8_off(int mode, uint32_t k, float P) {
+    return mode == 2 ? ((__float_as_uint(P) & 0xFu) | ((k & 0x1Fu) << 4)) : (k & 511u);
+}
+__device__ __forceinline__ float q8_P(int mode, float P) {
+    return mode == 2 ? __uint_as_float(__float_as_uint(P) & 0xFFFFFFF0u) : P;
 }
 
 // the W columns a (voxel, row block) segment reads: its own window when the cache
@@ -406,10 +431,11 @@ __device__ __forceinline__ void pcv_stage(const Esai &e, const float *W, int v, 
 // marker and contribute 0).  An A/B variant (option pc_fwd_geom): DESIGN.md 4.2b.
 // PIPE: the vector record loop is software-pipelined -- each thread's next 4 records are
 // loaded before the current 4 are deposited (two steps of loads in flight per thread).
-// Q8: 8-byte records (pixel = window base + 9-bit offset, tau in bits 9 .. 9 + pc_tb8)
+// Q8: 8-byte records (pixel = window base + 9-bit offset, tau with pc_tb8 bits at bit
+// pc_tsh8; MODE 2 keeps 8 offset bits in P's low byte -- k_pc_pack8)
 // PADQ: every padding record's pixel is closed for its voxel (k_pc_fill, Esai.pc_padq):
 // its zero is added in place, without the select into the dummy slot.
-template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false, bool Q8 = false, bool PADQ = false>
+template <typename QT, int U, int PCV_T, bool GEOM = false, bool PIPE = false, int Q8 = 0, bool PADQ = false>
 __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p, const Esai e, const float *__restrict__ W,
                                                      int R, int vchunk, int n_rb, int n_items, int pf,
                                                      double *__restrict__ partial) {
@@ -504,7 +530,7 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     CACSI_CHECK(b >= (swin.x & ~3) && b + 1 < (swin.x & ~3) + wcap);
                     CACSI_CHECK((P[u] == 0.0f && !PADQ) || (q[u] >= (uint32_t)q0 && q[u] < (uint32_t)(q0 + nacc)));
                     const float wa = wv[b], wb = wv[b + 1];
-                    const float t = Q8 ? (float)((k[u] >> 9) & tmask8) * tunit8 : (float)(k[u] & tmask) * tunit;
+                    const float t = Q8 ? (float)((k[u] >> (Q8 == 2 ? 5 : 9)) & tmask8) * tunit8 : (float)(k[u] & tmask) * tunit;
                     float *ap = PADQ ? accq + q[u] : P[u] != 0.0f ? accq + q[u] : dummy;
                     *ap = fmaf(P[u], fmaf(t, wb - wa, wa), *ap);
                 }
@@ -532,7 +558,10 @@ __global__ void __launch_bounds__(PCV_T, 1024 / PCV_T) k_pc_fwd_v(const Params p
                     P[0] = r.P.x, P[1] = r.P.y, P[2] = r.P.z, P[3] = r.P.w;
                     if (Q8) {
 #pragma unroll
-                        for (int u = 0; u < 4; u++) q[u] = r.q.x + (k[u] & 511u);
+                        for (int u = 0; u < 4; u++) {
+                            q[u] = r.q.x + q8_off(Q8, k[u], P[u]);
+                            P[u] = q8_P(Q8, P[u]);
+                        }
                     } else {
                         q[0] = r.q.x & 0xFFFFu, q[1] = r.q.x >> 16, q[2] = r.q.y & 0xFFFFu, q[3] = r.q.y >> 16;
                     }
@@ -674,7 +703,7 @@ __global__ void __launch_bounds__(PCB_T) k_pc_bwd(const Params p, const Esai e, 
 // PFL1: warp 1 peeks at the NEXT ring stage (non-blocking); if it has landed, its lanes
 // sample 32 of its records' pixels and prefetch the w lines between their min and max into
 // L1 (prefetch.global.L1), so the next chunk's gathers can hit L1 (option pcb_pfl1).
-template <typename QT, int PBT_T, int PBT_U, int PBT_NS, bool Q8 = false, bool PFL1 = false>
+template <typename QT, int PBT_T, int PBT_U, int PBT_NS, int Q8 = 0, bool PFL1 = false>
 __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai e, const float *__restrict__ w,
                                                       const float *__restrict__ wmax, float *__restrict__ A) {
     extern __shared__ __align__(16) unsigned char smb[];
@@ -689,7 +718,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
     const int tb = e.pc_tbits;
     const uint32_t tmask = Q8 ? (1u << e.pc_tb8) - 1u : (1u << tb) - 1u;
     const float tunit = Q8 ? 1.0f / (float)(1u << e.pc_tb8) : 1.0f / (float)(1u << tb);
-    const int tsh = Q8 ? 9 : 0;  // tau's position in the record word
+    const int tsh = Q8 == 2 ? 5 : Q8 == 1 ? 9 : 0;  // tau's position in the record word
     const QT *pq = (const QT *)e.pcb_q;
     const bool vec = e.pc_R > 0;  // bank-ordered layout (segments 128-record aligned)
     const float wm = *wmax;
@@ -786,7 +815,10 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     const uint16_t *qbs = (const uint16_t *)(src + PBT_CH * 8) + ((a >> 7) & 7);
                     const uint32_t qb = 4 * tid < hi ? qbs[tid >> 5] : 0u;
 #pragma unroll
-                    for (int u = 0; u < PBT_U; u++) q[u] = qb + (k[u] & 511u);
+                    for (int u = 0; u < PBT_U; u++) {
+                        q[u] = qb + q8_off(Q8, k[u], P[u]);
+                        P[u] = q8_P(Q8, P[u]);
+                    }
                 } else if (sizeof(QT) == 2) {
                     const uint2 qv = ((const uint2 *)(src + PBT_CH * 8))[tid];
                     q[0] = qv.x & 0xFFFFu, q[1] = qv.x >> 16, q[2] = qv.y & 0xFFFFu, q[3] = qv.y >> 16;
@@ -813,7 +845,7 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     }
                 }
             }
-            if (PFL1 && !Q8 && (tid >> 5) == 1 && PBT_NS >= 2) {
+            if (PFL1 && (tid >> 5) == 1 && PBT_NS >= 2) {
                 const int st2 = (consumed + 1) % PBT_NS;
                 uint32_t landed;
                 asm volatile(
@@ -823,8 +855,16 @@ __global__ void __launch_bounds__(PBT_T) k_pc_bwd_tma(const Params p, const Esai
                     : "r"(smem_u32(full + st2)), "r"(((consumed + 1) / PBT_NS) & 1)
                     : "memory");
                 if (landed) {
-                    const QT *qn = (const QT *)(smb + st2 * SB + PBT_CH * 8);
-                    const uint32_t qs = (uint32_t)qn[(tid & 31) * (PBT_CH / 32)];
+                    // (Q8: the stage's window bases, up to 8 + 7 of them from a 16-byte-aligned
+                    // start; a base plus the 9-bit offsets spans <= 512 pixels)
+                    uint32_t qs;
+                    if (Q8) {
+                        const uint16_t *qbn = (const uint16_t *)(smb + st2 * SB + PBT_CH * 8);
+                        qs = (uint32_t)qbn[(tid & 31) % QBN] + ((tid & 1) ? 511u : 0u);
+                    } else {
+                        const QT *qn = (const QT *)(smb + st2 * SB + PBT_CH * 8);
+                        qs = (uint32_t)qn[(tid & 31) * (PBT_CH / 32)];
+                    }
                     const uint32_t qlo = __reduce_min_sync(0xFFFFFFFFu, qs), qhi = __reduce_max_sync(0xFFFFFFFFu, qs);
                     if (qhi >= qlo && qhi < (uint32_t)p.n_det && qhi - qlo < 16384u) {
                         const uintptr_t l0 = (uintptr_t)(w + qlo) & ~(uintptr_t)127, l1 = (uintptr_t)(w + qhi);

@@ -10,8 +10,9 @@ import subprocess
 import sys
 
 # ncu kernel name (prefix, template arguments stripped) -> bench.py's KScope name
-NAMES = {"k_tc_gemm_ar": "k_tc_gemm_W", "k_pc_fwd_v": "k_pc_fwd", "k_pc_fwd": "k_pc_fwd",
-         "k_pc_bwd_tma": "k_pc_bwd", "k_pc_bwd": "k_pc_bwd", "k_tc_gemm_splitk": "k_tc_gemm_b2"}
+NAMES = {"k_tc_gemm_ar": "k_tc_gemm_W", "k_tc_gemm_ar16": "k_tc_gemm_W", "k_pc_fwd_v": "k_pc_fwd", "k_pc_fwd": "k_pc_fwd",
+         "k_pc_bwd_tma": "k_pc_bwd", "k_pc_bwd": "k_pc_bwd", "k_tc_gemm_splitk": "k_tc_gemm_b2",
+         "k_tc_gemm_splitk16": "k_tc_gemm_b2"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
