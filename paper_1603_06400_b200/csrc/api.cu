@@ -127,7 +127,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_pc_qbase, g->d_tc16_w1, g->d_tc16_b};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_erx_vb, g->d_erx_pm, g->d_erx_pw, g->d_pc_qbase, g->d_tc16_w1, g->d_tc16_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -173,6 +173,7 @@ const OptKey kOptKeys[] = {
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},
     {"er_fwd_reg", &cacsi::Opts::er_fwd_reg, false, 0, 1},
+    {"er_bwd_fx", &cacsi::Opts::er_bwd_fx, false, 0, 1},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},
 };
 
@@ -446,6 +447,15 @@ cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *d, int device, 
     for (int i = 0; i < 6; i++) g->setup_us[6] -= g->setup_us[i];  // host tables, uploads, validation
     if (d->energy_resolving && !g->opt.direct && g->opt.er_cache) {
         e = cacsi::er_build(g, d);
+        if (e != cudaSuccess) {
+            free_all(g);
+            free(g);
+            cudaGetLastError();
+            return map_err(e);
+        }
+    }
+    if (d->energy_resolving && !g->er.enabled) {  // tables of the fixed-point direct backward
+        e = cacsi::erx_build(g);
         if (e != cudaSuccess) {
             free_all(g);
             free(g);

@@ -213,6 +213,7 @@ struct Opts {
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
     int er_fwd_reg = 1;       // "er_fwd_reg": 0 = the direct energy-resolving forward with shared-memory accumulators
     int er_fwd = 0;           // "er_fwd" (er_cache=1 only): 1 = the compacted pair-cache forward k_er_fwd2
+    int er_bwd_fx = 1;        // "er_bwd_fx": 0 = the direct energy-resolving backward with fp32 shared-memory histograms
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
 };
 
@@ -235,6 +236,9 @@ struct cacsi_geometry {
     // energy-resolving pair cache (er_cache.cu)
     cacsi::ErCache er;
     void *d_er_off, *d_er_vw, *d_er_P, *d_er_s, *d_er_boff, *d_er_sv;
+    // fixed-point energy-resolving backward (operators.cu): per voxel bin bound
+    // and max P, per pixel energy-window union over its open pairs (built at create)
+    void *d_erx_vb, *d_erx_pm, *d_erx_pw;
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs
@@ -331,6 +335,7 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 cudaError_t er_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
 cudaError_t er_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
+cudaError_t erx_build(cacsi_geometry *g);
 int pcv_row_blocks(const cacsi_geometry *g);
 void osem_graph_free(cacsi_geometry *g);
 cudaError_t esai_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);

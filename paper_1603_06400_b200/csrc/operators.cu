@@ -12,6 +12,7 @@
 // over its whole detector footprint; each thread owns a private column of a
 // [nq+4][threads] shared-memory histogram (bank = lane, conflict-free, no
 // atomics); the columns are summed in fp64 at the end.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -143,16 +144,23 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
 // read-modify-write per two terms; the final [pixels][ne] block is staged through shared
 // memory for coalesced stores.  Option er_fwd_reg.
 constexpr int KR_MAX = 128;
+__device__ __forceinline__ float2 lds2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
 struct AlphaTab {
     float a[KR_MAX];  // alpha_k for k < ne, 1e30 (clamps onto the zero table entry) beyond
 };
 template <int KR>
 __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const float *__restrict__ f,
                                                           int vox_per_split, float *__restrict__ partial,
-                                                          const AlphaTab at) {
+                                                          const AlphaTab at, int nlo, int QR) {
     extern __shared__ float4 smem4[];
-    const int Q = p.nq, K = p.ne, Q3 = Q + 3;
-    float2 *tab = (float2 *)smem4;  // [VC][Q + 3] (mid, slope), entry n at index n + 2; reused to stage the output
+    const int Q = p.nq, K = p.ne;
+    // [VC][QR] (mid, slope), entry n at index n + nlo (n = -nlo .. Q): nlo covers u' down to
+    // -q_min/dq - 1/2 (sin(theta/2) >= 0), so only the upper clamp is needed; reused to stage the output
+    float2 *tab = (float2 *)smem4;
     const int tid = threadIdx.x;
     const int pix = blockIdx.x * FWD_T + tid;
     const bool valid = pix < p.n_det;
@@ -165,8 +173,8 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
     for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
         const int nc = min(FWD_VC, v1 - c0);
         __syncthreads();
-        for (int i = tid; i < nc * Q3; i += FWD_T) {
-            const int vv = i / Q3, n = i - vv * Q3 - 2;
+        for (int i = tid; i < nc * QR; i += FWD_T) {
+            const int vv = i / QR, n = i - vv * QR - nlo;
             const float *fr = f + (size_t)(c0 + vv) * Q;
             const float a = (n >= 0 && n < Q) ? fr[n] : 0.0f;
             const float b = (n + 1 >= 0 && n + 1 < Q) ? fr[n + 1] : 0.0f;
@@ -185,16 +193,21 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
             }
             const int wlo = __reduce_min_sync(FULL, klo);
             const int whi = __reduce_max_sync(FULL, khi);
-            const float2 *tv = tab + vv * Q3 + 2;
+            // byte address of entry n of this voxel's row, folded with the magic constant's bits:
+            // entry(n) = tb + 8 * bits(n + 1.5 * 2^23)  (one LEA per term)
+            uint32_t tb = (uint32_t)__cvta_generic_to_shared(tab + vv * QR + nlo) - (uint32_t)kMagicBits * 8u;
+            tb = __shfl_sync(FULL, tb, 0);  // a per-lane register for ptxas: keeps the folded base (LEA per term)
 #pragma unroll
             for (int kb = 0; kb < KR; kb += 8) {
                 if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
-                    float tt;
-                    const int n = hat_coord(p, at.a[kb + j], sh, tt);
-                    CACSI_CHECK(n >= -2 && n <= Q);
-                    const float2 t = tv[n];
+                    // u' = u - 1/2 >= -q_min/dq - 1/2 needs no lower clamp (entries down to -nlo are zero)
+                    const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
+                    const float vm = u + kMagic;
+                    const float tt = u - (vm - kMagic);
+                    CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits <= Q);
+                    const float2 t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
                     acc[kb + j] = fmaf(P, fmaf(tt, t.y, t.x), acc[kb + j]);
                 }
             }
@@ -413,6 +426,234 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_c(const Params p, const f
     }
 }
 
+// ------------------------------------------- fixed-point energy-resolving backward --
+// k_backward_er_x (option er_bwd_fx, default): the compacted open pairs of
+// k_backward_er_c, with each lane's histogram column kept in FIXED POINT and
+// updated by native shared-memory integer reductions (red.shared.add.s32):
+// no read-modify-write through shared memory, so consecutive deposits of a
+// lane no longer serialise on their load -> add -> store chains; the column
+// is private to the lane (bank = lane, no conflicts), and integer sums are
+// order-free.  Per term (u' = alpha_k sigma - q_min/dq - 1/2, n = round(u'),
+// tt = u' - n): a = P s_v c_k w[q][k] is rounded to an integer by the
+// 1.5 * 2^23 addition, hi = round((tt + 1/2) a) goes to node n + 1 and
+// lo = round(a) - hi to node n (exactly the hat split of PAPER.md:248-270 in
+// the energy-resolved form).  The per-voxel scale s_v keeps
+// every bin's total below 2^31 units (a bound on sum P c_k hat measured at
+// create, times max |w|) and every single deposit below 2^22 units (max P
+// times max |c_k w|: the range of the rounding addition); columns wrap
+// modulo 2^32, their int32 sum is exact because the true total fits.  w arrives pre-scaled by c_k in padded rows
+// ([n_det][ne4], k_erx_wprep) and is read as float4 per lane.
+__device__ __forceinline__ void red_s32(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// per pixel: union of the energy windows of its open pairs ([klo, khi], or (1, 0) if none)
+__global__ void __launch_bounds__(256) k_erx_pix(const Params p, int2 *__restrict__ pwin) {
+    const int lane = threadIdx.x & 31;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p.n_det; q += (gridDim.x * blockDim.x) >> 5) {
+        const float2 d = p.det[q];
+        int lo = p.ne, hi = -1;
+        for (int v = lane; v < p.n_vox; v += 32) {
+            const VoxelRec vr = p.vox[v];
+            if (!mask_open(p, v, q, vr, d)) continue;
+            float P, sh;
+            pair_geom(p, vr, d, P, sh);
+            int klo, khi;
+            k_range(p, sh, klo, khi);
+            if (klo <= khi && P > 0.0f) lo = min(lo, klo), hi = max(hi, khi);
+        }
+        lo = __reduce_min_sync(FULL, lo);
+        hi = __reduce_max_sync(FULL, hi);
+        if (lane == 0) pwin[q] = lo <= hi ? make_int2(lo, hi) : make_int2(1, 0);
+    }
+}
+
+// per voxel: sum_q P and max_q P over its open pairs with a non-empty window
+__global__ void __launch_bounds__(256) k_erx_vox(const Params p, float csum, float *__restrict__ vb,
+                                                 float *__restrict__ pm) {
+    __shared__ double ss[8];
+    __shared__ float sm[8];
+    const int v = blockIdx.x, tid = threadIdx.x;
+    const VoxelRec vr = p.vox[v];
+    double s = 0.0;
+    float m = 0.0f;
+    for (int q = tid; q < p.n_det; q += 256) {
+        const float2 d = p.det[q];
+        if (!mask_open(p, v, q, vr, d)) continue;
+        float P, sh;
+        pair_geom(p, vr, d, P, sh);
+        int klo, khi;
+        k_range(p, sh, klo, khi);
+        if (klo <= khi && P > 0.0f) s += (double)P, m = fmaxf(m, P);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o), m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+    if ((tid & 31) == 0) ss[tid >> 5] = s, sm[tid >> 5] = m;
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 1; i < 8; i++) s += ss[i], m = fmaxf(m, sm[i]);
+        vb[v] = (float)(s * (double)csum * (1.0 + 1e-5));  // loose bin bound: sum_k c_k hat <= sum_k c_k
+        pm[v] = m * (1.0f + 1e-6f);
+    }
+}
+
+// wt[q][k] = c_k w[q][k] (rows padded to ne4 with zeros; ONES: w = 1), and
+// mx[0] = max |w|, mx[1] = max |c_k w| over the entries inside each pixel's window
+// union (the only ones that can reach a real histogram bin)
+template <bool ONES>
+__global__ void __launch_bounds__(256) k_erx_wprep(const Params p, const float *__restrict__ w, int ne4,
+                                                   const int2 *__restrict__ pwin, float *__restrict__ wt,
+                                                   unsigned *__restrict__ mx) {
+    float m0 = 0.0f, m1 = 0.0f;
+    const size_t n = (size_t)p.n_det * ne4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int q = (int)(i / ne4), k = (int)(i - (size_t)q * ne4);
+        float o = 0.0f;
+        if (k < p.ne) {
+            const float wv = ONES ? 1.0f : w[(size_t)q * p.ne + k];
+            o = __ldg(&p.energy[k].y) * wv;
+            const int2 win = __ldg(pwin + q);
+            if (k >= win.x && k <= win.y) m0 = fmaxf(m0, fabsf(wv)), m1 = fmaxf(m1, fabsf(o));
+        }
+        wt[i] = o;
+    }
+    for (int o = 16; o; o >>= 1) m0 = fmaxf(m0, __shfl_xor_sync(FULL, m0, o)), m1 = fmaxf(m1, __shfl_xor_sync(FULL, m1, o));
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(mx, __float_as_uint(m0));  // nonnegative floats order as their bit patterns
+        atomicMax(mx + 1, __float_as_uint(m1));
+    }
+}
+
+struct ErxQ {
+    float cs, sh;  // P s_v, sin(theta/2)
+    int q, kw;     // pixel, klo | (khi + 1) << 16
+};
+constexpr int ERX_CAP = 96;
+constexpr int ERX_PF = 4;  // w~ blocks of look-ahead
+__global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const float *__restrict__ wt, int ne4,
+                                                         const float *__restrict__ vb, const float *__restrict__ pm,
+                                                         const unsigned *__restrict__ mx, float *__restrict__ b) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne;
+    float *alpha = (float *)smem4;                       // [ne4] (alpha_k; 1e30 beyond ne)
+    uint32_t *hist = (uint32_t *)(alpha + ne4);           // [Q + 4][BWD_T]; row = node + 2
+    ErxQ *queue = (ErxQ *)(hist + (Q + 4) * BWD_T);      // [BWD_T / 32][ERX_CAP]
+    __shared__ float s_scale;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int v = blockIdx.x;
+    for (int k = tid; k < ne4; k += BWD_T) alpha[k] = k < K ? p.energy[k].x : 1e30f;
+    for (int i = tid; i < (Q + 4) * BWD_T; i += BWD_T) hist[i] = 0u;
+    if (tid == 0) {
+        const double m0 = (double)__uint_as_float(mx[0]), m1 = (double)__uint_as_float(mx[1]);
+        const double bv = (double)vb[v], pv = (double)pm[v];
+        double s = 0.0;
+        if (m0 > 0.0 && bv > 0.0) {
+            s = 2.1e9 / (bv * m0);                                    // bin totals < 2^31 (int32 sum of the columns)
+            if (pv * m1 > 0.0) s = fmin(s, 4.19e6 / (pv * m1));       // single deposits < 2^22 (rounding by 1.5 * 2^23)
+        }
+        s_scale = (float)s;
+    }
+    __syncthreads();
+    const float sv = s_scale;
+    const VoxelRec vr = p.vox[v];
+    const float nb = p.nb, qm = p.qm;
+    // byte address of row (n + 2) of this thread's column, folded with the magic constant's
+    // bits: row(n) = hb0 + bits(n + 1.5 * 2^23) * 4 * BWD_T
+    const uint32_t hb0 = (uint32_t)__cvta_generic_to_shared(hist + tid) + (uint32_t)(2 - kMagicBits) * (uint32_t)(4 * BWD_T);
+    ErxQ *wq = queue + warp * ERX_CAP;
+    int qn = 0;
+    auto batch = [&](int cnt) {
+        ErxQ e = {0.0f, 1.0f, 0, K};
+        if (lane < cnt) e = wq[lane];
+        const int klo = e.kw & 0xFFFF, khi = (e.kw >> 16) - 1;
+        const int wlo = __reduce_min_sync(FULL, klo);
+        const int whi = __reduce_max_sync(FULL, khi);
+        if (wlo > whi) return;
+        const float4 *wr = (const float4 *)(wt + (size_t)e.q * ne4);
+        // w~ of the next ERX_PF blocks of 4 energies in flight (their L2 latency was the
+        // main stall with one block of look-ahead)
+        const int kb0 = wlo >> 2, kb1 = whi >> 2;
+        float4 wn[ERX_PF];
+#pragma unroll
+        for (int i = 0; i < ERX_PF; i++) wn[i] = kb0 + i <= kb1 ? __ldg(wr + kb0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int kb = kb0; kb <= kb1; kb++) {
+            const int k = kb << 2;
+            const float4 wc = wn[0];
+#pragma unroll
+            for (int i = 0; i + 1 < ERX_PF; i++) wn[i] = wn[i + 1];
+            if (kb + ERX_PF <= kb1) wn[ERX_PF - 1] = __ldg(wr + kb + ERX_PF);
+            const float4 a4 = *(const float4 *)(alpha + k);
+            const float al[4] = {a4.x, a4.y, a4.z, a4.w}, wk[4] = {wc.x, wc.y, wc.z, wc.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                // a term outside this lane's window clamps onto the padding rows (nodes -2 / nq;
+                // at u' = nq - 1/2 with odd nq, n = nq - 1 gets lo = 0 exactly)
+                const float u = fminf(fmaxf(fmaf(al[j], e.sh, nb), -1.5f), qm);
+                const float vm = u + kMagic;
+                const float tt = u - (vm - kMagic);
+                const float a = e.cs * wk[j];
+                const uint32_t ab = __float_as_uint(a + kMagic);
+                const uint32_t hb = __float_as_uint(fmaf(tt + 0.5f, a, kMagic));
+                const uint32_t addr = hb0 + (__float_as_uint(vm) << 9);
+                static_assert(4 * BWD_T == 512, "row stride");
+                CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -2 && __float_as_int(vm) - kMagicBits <= Q);
+                red_s32(addr, ab - hb);
+                red_s32(addr + 4 * BWD_T, hb - (uint32_t)kMagicBits);
+            }
+        }
+    };
+    for (int base = warp * 64; base < p.n_det; base += (BWD_T / 32) * 64) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = base + 32 * h + lane;
+            const bool valid = q < p.n_det;
+            const float2 d = p.det[valid ? q : 0];
+            bool open = valid && mask_open(p, v, q, vr, d);
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1;
+            if (open) {
+                pair_geom(p, vr, d, P, sh);
+                k_range(p, sh, klo, khi);
+                open = klo <= khi;
+            }
+            const unsigned m = __ballot_sync(FULL, open);
+            if (open) wq[qn + __popc(m & ((1u << lane) - 1u))] = ErxQ{P * sv, sh, q, klo | ((khi + 1) << 16)};
+            qn += __popc(m);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+            batch(32);
+            __syncwarp();
+            const int rem = qn - 32;
+            ErxQ t0, t1;
+            if (lane < rem) t0 = wq[32 + lane];
+            if (lane + 32 < rem) t1 = wq[64 + lane];
+            __syncwarp();
+            if (lane < rem) wq[lane] = t0;
+            if (lane + 32 < rem) wq[lane + 32] = t1;
+            __syncwarp();
+            qn = rem;
+        }
+    }
+    if (qn > 0) batch(qn);
+    __syncthreads();
+    const double inv = sv > 0.0f ? 1.0 / (double)sv : 0.0;
+    for (int j = tid; j < Q; j += BWD_T) {
+        const uint32_t *row = hist + (j + 2) * BWD_T;
+        uint32_t s = 0u;
+        for (int t = 0; t < BWD_T; t++) s += row[(t + j) % BWD_T];  // modulo 2^32; rotate: bank spread
+        b[(size_t)v * Q + j] = (float)((double)(int32_t)s * inv);
+    }
+}
+
+// vb[v] = 1.02 max_j b1[v][j] (+ a floor): the measured bin bound of the fixed-point backward
+__global__ void k_erx_vmax(const float *__restrict__ b1, int nq, int n_vox, float *__restrict__ vb) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n_vox; v += gridDim.x * blockDim.x) {
+        float m = 0.0f;
+        for (int j = 0; j < nq; j++) m = fmaxf(m, fabsf(b1[(size_t)v * nq + j]));
+        vb[v] = m > 0.0f ? 1.02f * m : vb[v];
+    }
+}
+
 int num_sms(int device) {
     static int cached[64] = {0};
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
@@ -447,7 +688,7 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
     if (e != cudaSuccess) return e;
     dim3 grid(tiles, S);
-    if (res && g->opt.er_fwd_reg && p.ne <= KR_MAX) {
+    if (res && g->opt.er_fwd_reg && p.ne <= KR_MAX && FWD_VC * ((p.nq + 4 + (int)std::ceil(-(double)p.nb)) | 1) * 8 <= 72 * 1024) {
         // register accumulators: the smallest instantiated KR >= ne
         AlphaTab at;
         std::vector<float2> en(p.ne);
@@ -459,11 +700,14 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
         for (int k = 0; k < KR_MAX; k++) at.a[k] = k < p.ne ? en[k].x : 1e30f;
         auto kf = p.ne <= 16 ? k_forward_reg<16> : p.ne <= 32 ? k_forward_reg<32> : p.ne <= 64 ? k_forward_reg<64>
                 : p.ne <= 104 ? k_forward_reg<104> : k_forward_reg<128>;
-        const size_t sm2 = std::max((size_t)(FWD_VC * (p.nq + 3) + 1) * sizeof(float2), (size_t)32 * (FWD_T + 1) * sizeof(float));
+        // table entries below node 0: u' >= nb = -q_min/dq - 1/2 rounds to n >= -(ceil(-nb) + 1)
+        const int nlo = std::max(2, (int)std::ceil(-(double)p.nb) + 2);
+        const int QR = (p.nq + 1 + nlo) | 1;  // odd row stride (float2): rows start on different banks
+        const size_t sm2 = std::max((size_t)(FWD_VC * QR) * sizeof(float2), (size_t)32 * (FWD_T + 1) * sizeof(float));
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         {
             KScope kt_(g, s, "k_forward_er");
-            kf<<<grid, FWD_T, sm2, s>>>(p, f, vps, (float *)part, at);
+            kf<<<grid, FWD_T, sm2, s>>>(p, f, vps, (float *)part, at, nlo, QR);
         }
     } else if (res) {
         cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -498,12 +742,75 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     return e;
 }
 
+namespace {
+// the fixed-point energy-resolving backward: w pre-scaled into padded rows, then one CTA per voxel
+cudaError_t erx_backward(const cacsi_geometry *g, const float *w, bool ones, float *b, cudaStream_t s, int *launches) {
+    const Params &p = g->p;
+    const int ne4 = (p.ne + 3) & ~3;
+    float *wt = nullptr;
+    cudaError_t e = cudaMallocAsync(&wt, (size_t)p.n_det * ne4 * sizeof(float) + 16, s);
+    if (e != cudaSuccess) return e;
+    unsigned *mx = (unsigned *)(wt + (size_t)p.n_det * ne4);
+    cudaMemsetAsync(mx, 0, 8, s);
+    const int nb = 4 * num_sms(g->device);
+    {
+        KScope kt_(g, s, "k_erx_wprep");
+        if (ones) k_erx_wprep<true><<<nb, 256, 0, s>>>(p, w, ne4, (const int2 *)g->d_erx_pw, wt, mx);
+        else k_erx_wprep<false><<<nb, 256, 0, s>>>(p, w, ne4, (const int2 *)g->d_erx_pw, wt, mx);
+    }
+    const size_t smem = (size_t)ne4 * sizeof(float) + (size_t)(p.nq + 4) * BWD_T * sizeof(uint32_t) +
+                        (size_t)(BWD_T / 32) * ERX_CAP * sizeof(ErxQ);
+    cudaFuncSetAttribute(k_backward_er_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        KScope kt_(g, s, "k_backward_er");
+        k_backward_er_x<<<p.n_vox, BWD_T, smem, s>>>(p, wt, ne4, (const float *)g->d_erx_vb, (const float *)g->d_erx_pm,
+                                                      mx, b);
+    }
+    e = cudaGetLastError();
+    cudaFreeAsync(wt, s);
+    *launches += 2;
+    return e;
+}
+}  // namespace
+
+// tables of the fixed-point backward (create time): per-pixel window unions, per-voxel max P and a
+// loose bin bound (sum P times sum_k c_k), then the bound measured by one backward of w = 1 with
+// the loose bound's scale (accurate to ~1e-5, so 1.02x of it is safe)
+cudaError_t erx_build(cacsi_geometry *g) {
+    const Params &p = g->p;
+    cudaError_t e = cudaMalloc(&g->d_erx_vb, (size_t)p.n_vox * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_pm, (size_t)p.n_vox * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_pw, (size_t)p.n_det * sizeof(int2));
+    if (e != cudaSuccess) return e;
+    std::vector<float2> en(p.ne);
+    e = cudaMemcpy(en.data(), p.energy, p.ne * sizeof(float2), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return e;
+    double csum = 0.0;
+    for (int k = 0; k < p.ne; k++) csum += std::fabs((double)en[k].y);
+    cudaStream_t s = 0;
+    k_erx_pix<<<(p.n_det + 7) / 8, 256, 0, s>>>(p, (int2 *)g->d_erx_pw);
+    k_erx_vox<<<p.n_vox, 256, 0, s>>>(p, (float)(csum * (1.0 + 1e-6)), (float *)g->d_erx_vb, (float *)g->d_erx_pm);
+    float *b1 = nullptr;
+    e = cudaMalloc(&b1, (size_t)p.n_vox * p.nq * sizeof(float));
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = erx_backward(g, nullptr, true, b1, s, &n);
+    if (e == cudaSuccess) {
+        k_erx_vmax<<<(p.n_vox + 255) / 256, 256, 0, s>>>(b1, p.nq, p.n_vox, (float *)g->d_erx_vb);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(b1);
+    return e;
+}
+
 cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches) {
     if (g->esai.enabled) return esai_backward(g, w, b, s, launches);
     if (g->er.enabled) return er_backward(g, w, b, s, launches);
     const Params &p = g->p;
     const size_t smem =
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
+    if (p.energy_resolving && g->opt.er_bwd_fx && g->d_erx_vb) return erx_backward(g, w, false, b, s, launches);
     if (p.energy_resolving) {
         float *wT = nullptr;
         cudaError_t e = cudaMallocAsync(&wT, (size_t)p.n_det * p.ne * sizeof(float), s);

@@ -11,7 +11,8 @@ from workloads import make_config
 torch = pytest.importorskip("torch")
 P = pytest.importorskip("paper_1603_06400_b200")
 
-from test_gpu_parity import assert_parity, gpu_forward, rnd  # noqa: E402
+from test_gpu_parity import assert_parity, gpu_backward, gpu_forward, rel_l2, rnd  # noqa: E402
+from workloads.configs import seeded_rng  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -40,3 +41,97 @@ def test_er_forward_registers_non_uniform_energies():
     assert np.array_equal(g1, gpu_forward(G, f))
     assert_parity(g1, oracle.Geometry(d).forward(f), "er forward registers, non-uniform energies")
 
+
+
+# ---- fixed-point energy-resolving backward (option er_bwd_fx=1, the default; k_backward_er_x) ----
+def _er_desc(**over):
+    d = make_config(0, energy_resolving=1).desc()
+    d.update(over)
+    return d
+
+
+ER_BWD_SHAPES = [
+    {},
+    dict(ne=17, energy_kev=np.linspace(21.0, 149.0, 17), phi=np.linspace(1.0, 0.3, 17), ny=6, nz=5, nq=21,
+         det_nx=7, det_ny=19),
+    dict(ne=100, energy_kev=np.linspace(21.0, 149.0, 100), phi=np.linspace(1.0, 0.3, 100), ny=5, nz=7, nq=33,
+         det_nx=9, det_ny=23),
+    dict(ne=128, energy_kev=np.linspace(21.0, 149.0, 128), phi=np.linspace(1.0, 0.3, 128)),
+    dict(energy_kev=np.array([30.0, 33.0, 41.0, 55.0, 60.0, 80.0, 101.0, 119.0])),
+    dict(q_min=0.15, q_max=0.25, nq=9),
+    dict(q_min=0.0, q_max=0.9, nq=40),
+]
+
+
+@pytest.mark.parametrize("si", range(len(ER_BWD_SHAPES)))
+def test_er_backward_fixed_point_oracle(si):
+    """Every output against the oracle, and against the fp32-histogram kernel (er_bwd_fx=0)
+    as an independent GPU cross-check; deterministic bits."""
+    d = _er_desc(**ER_BWD_SHAPES[si])
+    G = P.Geometry(d)
+    w = rnd(G.g_shape, 0, 150 + si)
+    b1 = gpu_backward(G, w)
+    assert np.array_equal(b1, gpu_backward(G, w))
+    assert_parity(b1, oracle.Geometry(d).backward(w), f"er backward fixed point {si}")
+    G.set_option("er_bwd_fx", 0)
+    b0 = gpu_backward(G, w)
+    assert_parity(b1, b0, f"er backward fixed point vs fp32 histograms {si}")
+
+
+@pytest.mark.parametrize("kind", ["log_uniform", "signed", "ones"])
+def test_er_backward_fixed_point_weights(kind):
+    """The per-voxel scale follows max |w|: weights over six decades, signed weights
+    (bar against the absolute-value operator, reading R19b), and w = 1 (the create-time
+    bound measurement's own input)."""
+    d = _er_desc(ny=6, nz=5, nq=21, det_nx=7, det_ny=19)
+    G, O = P.Geometry(d), oracle.Geometry(d)
+    rng = seeded_rng(0, 160)
+    if kind == "log_uniform":
+        w = (10.0 ** rng.uniform(-3, 3, G.g_shape)).astype(np.float32)
+    elif kind == "signed":
+        w = rng.uniform(-1, 1, G.g_shape).astype(np.float32)
+    else:
+        w = np.ones(G.g_shape, np.float32)
+    b = gpu_backward(G, w)
+    ref = O.backward(w.astype(np.float64))
+    if kind != "signed":
+        assert_parity(b, ref, f"er backward fixed point, {kind} w")
+        return
+    absref = O.backward(np.abs(w).astype(np.float64))
+    sel = absref >= 1e-3 * absref.max()
+    err = np.abs(b - ref)[sel] / absref[sel]
+    print(f"er backward fixed point, signed w: rel_l2={rel_l2(b, ref):.3e} max_err_vs_abs={err.max():.3e}")
+    assert rel_l2(b, ref) <= 1e-5 and err.max() <= 1e-4
+
+
+def test_er_backward_fixed_point_zero_and_outliers():
+    """w = 0 gives exact zeros; huge weights (the ratio guard's y / 1e-12) on pixels that no
+    open pair reaches never deposit, so they must not set the fixed-point scale."""
+    d = _er_desc()
+    m = d["mask"].copy()
+    m[:12, :] = 0
+    m[17:, :] = 0
+    d["mask"] = m
+    G, O = P.Geometry(d), oracle.Geometry(d)
+    assert not np.any(gpu_backward(G, np.zeros(G.g_shape, np.float32)))
+    n_det = d["det_nx"] * d["det_ny"]
+    unseen = np.flatnonzero(np.array([O.count_terms([q])[1] for q in range(n_det)]) == 0)
+    assert 0 < unseen.size < n_det
+    w = rnd(G.g_shape, 0, 161).reshape(n_det, -1)
+    ref = O.backward(w.reshape(G.g_shape).astype(np.float64))
+    w[unseen] = np.float32(3e12)
+    assert_parity(gpu_backward(G, w.reshape(G.g_shape)), ref, "er backward fixed point, unseen-pixel outliers")
+
+
+def test_er_backward_fixed_point_config4_sampled():
+    """Config 4 at full size: sampled voxels against the oracle, plus the fp32-histogram kernel."""
+    cfg = make_config(4)
+    G, O = P.Geometry(cfg.desc()), oracle.Geometry(cfg.desc())
+    w = rnd(G.g_shape, 4, 162)
+    b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
+    rng = np.random.default_rng(4)
+    vox = np.unique(np.concatenate([rng.choice(cfg.n_vox, 6, replace=False), [0, cfg.n_vox - 1]]))
+    assert_parity(b[vox], O.backward_voxels(w, vox), "c4 er backward fixed point sampled")
+    G.set_option("er_bwd_fx", 0)
+    b0 = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
+    assert_parity(b, b0, "c4 er backward fixed point vs fp32 histograms (every voxel)")
