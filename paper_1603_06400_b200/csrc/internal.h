@@ -239,6 +239,7 @@ struct cacsi_geometry {
     // fixed-point energy-resolving backward (operators.cu): per voxel bin bound
     // and max P, per pixel energy-window union over its open pairs (built at create)
     void *d_erx_vb, *d_erx_pm, *d_erx_pw;
+    int erx_nlo;  // its histogram rows below node 0: u' >= alpha_0 min(sin(theta/2)) - q_min/dq - 1/2
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;
     // side stream + events of cacsi_iterate_host: y, r, b1 upload while the forward runs

@@ -21,6 +21,12 @@
 
 namespace cacsi {
 
+static inline float __uint_as_float_host(unsigned u) {
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
 namespace {
 
 constexpr int FWD_T = 128;  // pixels per CTA
@@ -441,15 +447,20 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_c(const Params p, const f
 // every bin's total below 2^31 units (a bound on sum P c_k hat measured at
 // create, times max |w|) and every single deposit below 2^22 units (max P
 // times max |c_k w|: the range of the rounding addition); columns wrap
-// modulo 2^32, their int32 sum is exact because the true total fits.  w arrives pre-scaled by c_k in padded rows
-// ([n_det][ne4], k_erx_wprep) and is read as float4 per lane.
+// modulo 2^32, their int32 sum is exact because the true total fits.  w
+// arrives pre-scaled by c_k in energy blocks of 4 ([ne4 / 4][n_det] float4,
+// k_erx_wprep): lanes on nearby pixels read nearby 16-byte words, one load
+// per lane per 4 energies.
 __device__ __forceinline__ void red_s32(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    // no memory clobber: the histogram is read only after a CTA barrier, and table loads may
+    // move across the reductions
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
 // per pixel: union of the energy windows of its open pairs ([klo, khi], or (1, 0) if none)
-__global__ void __launch_bounds__(256) k_erx_pix(const Params p, int2 *__restrict__ pwin) {
+__global__ void __launch_bounds__(256) k_erx_pix(const Params p, int2 *__restrict__ pwin, unsigned *__restrict__ smin) {
     const int lane = threadIdx.x & 31;
+    float sm = 1e30f;
     for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p.n_det; q += (gridDim.x * blockDim.x) >> 5) {
         const float2 d = p.det[q];
         int lo = p.ne, hi = -1;
@@ -460,12 +471,13 @@ __global__ void __launch_bounds__(256) k_erx_pix(const Params p, int2 *__restric
             pair_geom(p, vr, d, P, sh);
             int klo, khi;
             k_range(p, sh, klo, khi);
-            if (klo <= khi && P > 0.0f) lo = min(lo, klo), hi = max(hi, khi);
+            if (klo <= khi && P > 0.0f) lo = min(lo, klo), hi = max(hi, khi), sm = fminf(sm, sh);
         }
         lo = __reduce_min_sync(FULL, lo);
         hi = __reduce_max_sync(FULL, hi);
         if (lane == 0) pwin[q] = lo <= hi ? make_int2(lo, hi) : make_int2(1, 0);
     }
+    atomicMin(smin, __float_as_uint(sm));  // positive floats order as their bit patterns
 }
 
 // per voxel: sum_q P and max_q P over its open pairs with a non-empty window
@@ -496,25 +508,32 @@ __global__ void __launch_bounds__(256) k_erx_vox(const Params p, float csum, flo
     }
 }
 
-// wt[q][k] = c_k w[q][k] (rows padded to ne4 with zeros; ONES: w = 1), and
-// mx[0] = max |w|, mx[1] = max |c_k w| over the entries inside each pixel's window
-// union (the only ones that can reach a real histogram bin)
+// wt[kb][q] = (c_k w[q][k], k = 4 kb .. 4 kb + 3) as float4 (energy blocks of 4, zero-padded past ne;
+// ONES: w = 1): lanes holding nearby pixels read nearby 16-byte words, 4 energies per load.
+// mx[0] = max |w|, mx[1] = max |c_k w| over the entries inside each pixel's window union
+// (the only ones that can reach a real histogram bin)
 template <bool ONES>
 __global__ void __launch_bounds__(256) k_erx_wprep(const Params p, const float *__restrict__ w, int ne4,
-                                                   const int2 *__restrict__ pwin, float *__restrict__ wt,
+                                                   const int2 *__restrict__ pwin, float4 *__restrict__ wt,
                                                    unsigned *__restrict__ mx) {
     float m0 = 0.0f, m1 = 0.0f;
-    const size_t n = (size_t)p.n_det * ne4;
+    const int nkb = ne4 >> 2;
+    const size_t n = (size_t)p.n_det * nkb;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int q = (int)(i / ne4), k = (int)(i - (size_t)q * ne4);
-        float o = 0.0f;
-        if (k < p.ne) {
-            const float wv = ONES ? 1.0f : w[(size_t)q * p.ne + k];
-            o = __ldg(&p.energy[k].y) * wv;
-            const int2 win = __ldg(pwin + q);
-            if (k >= win.x && k <= win.y) m0 = fmaxf(m0, fabsf(wv)), m1 = fmaxf(m1, fabsf(o));
+        const int kb = (int)(i / p.n_det), q = (int)(i - (size_t)kb * p.n_det);
+        const int2 win = __ldg(pwin + q);
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int k = 4 * kb + j;
+            o[j] = 0.0f;
+            if (k < p.ne) {
+                const float wv = ONES ? 1.0f : __ldg(w + (size_t)q * p.ne + k);
+                o[j] = __ldg(&p.energy[k].y) * wv;
+                if (k >= win.x && k <= win.y) m0 = fmaxf(m0, fabsf(wv)), m1 = fmaxf(m1, fabsf(o[j]));
+            }
         }
-        wt[i] = o;
+        wt[i] = make_float4(o[0], o[1], o[2], o[3]);
     }
     for (int o = 16; o; o >>= 1) m0 = fmaxf(m0, __shfl_xor_sync(FULL, m0, o)), m1 = fmaxf(m1, __shfl_xor_sync(FULL, m1, o));
     if ((threadIdx.x & 31) == 0) {
@@ -529,19 +548,21 @@ struct ErxQ {
 };
 constexpr int ERX_CAP = 96;
 constexpr int ERX_PF = 4;  // w~ blocks of look-ahead
-__global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const float *__restrict__ wt, int ne4,
-                                                         const float *__restrict__ vb, const float *__restrict__ pm,
-                                                         const unsigned *__restrict__ mx, float *__restrict__ b) {
+__global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const float4 *__restrict__ wt, int ne4,
+                                                         int nlo, const float *__restrict__ vb,
+                                                         const float *__restrict__ pm, const unsigned *__restrict__ mx,
+                                                         float *__restrict__ b) {
     extern __shared__ float4 smem4[];
-    const int Q = p.nq, K = p.ne;
+    const int Q = p.nq, K = p.ne, NR = Q + 2 + nlo;      // rows: nodes -nlo .. nq + 1
     float *alpha = (float *)smem4;                       // [ne4] (alpha_k; 1e30 beyond ne)
-    uint32_t *hist = (uint32_t *)(alpha + ne4);           // [Q + 4][BWD_T]; row = node + 2
-    ErxQ *queue = (ErxQ *)(hist + (Q + 4) * BWD_T);      // [BWD_T / 32][ERX_CAP]
+    uint32_t *hist = (uint32_t *)(alpha + ne4);           // [NR][BWD_T]; row = node + nlo
+    ErxQ *queue = (ErxQ *)(hist + NR * BWD_T);           // [BWD_T / 32][ERX_CAP]
     __shared__ float s_scale;
+    __shared__ int s_next;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int v = blockIdx.x;
     for (int k = tid; k < ne4; k += BWD_T) alpha[k] = k < K ? p.energy[k].x : 1e30f;
-    for (int i = tid; i < (Q + 4) * BWD_T; i += BWD_T) hist[i] = 0u;
+    for (int i = tid; i < NR * BWD_T; i += BWD_T) hist[i] = 0u;
     if (tid == 0) {
         const double m0 = (double)__uint_as_float(mx[0]), m1 = (double)__uint_as_float(mx[1]);
         const double bv = (double)vb[v], pv = (double)pm[v];
@@ -551,16 +572,34 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             if (pv * m1 > 0.0) s = fmin(s, 4.19e6 / (pv * m1));       // single deposits < 2^22 (rounding by 1.5 * 2^23)
         }
         s_scale = (float)s;
+        s_next = BWD_T / 32;  // groups 0 .. BWD_T/32 - 1 go to the warps in order, the rest on demand
     }
     __syncthreads();
     const float sv = s_scale;
     const VoxelRec vr = p.vox[v];
     const float nb = p.nb, qm = p.qm;
-    // byte address of row (n + 2) of this thread's column, folded with the magic constant's
+    const size_t wstride = (size_t)p.n_det * sizeof(float4);  // bytes between energy blocks of one pixel
+    // byte address of row (n + nlo) of this thread's column, folded with the magic constant's
     // bits: row(n) = hb0 + bits(n + 1.5 * 2^23) * 4 * BWD_T
-    const uint32_t hb0 = (uint32_t)__cvta_generic_to_shared(hist + tid) + (uint32_t)(2 - kMagicBits) * (uint32_t)(4 * BWD_T);
+    const uint32_t hb0 = (uint32_t)__cvta_generic_to_shared(hist + tid) + (uint32_t)(nlo - kMagicBits) * (uint32_t)(4 * BWD_T);
     ErxQ *wq = queue + warp * ERX_CAP;
     int qn = 0;
+    auto term = [&](float al, float wk, float sh, float cs) {
+        // u' = alpha sigma - q_min/dq - 1/2 >= -nlo + 1/2 (no lower clamp); a term outside this
+        // lane's window lands on the padding rows (nodes < 0 or >= nq; at u' = nq - 1/2 with
+        // odd nq, n = nq - 1 gets lo = 0 exactly)
+        const float u = fminf(fmaf(al, sh, nb), qm);
+        const float vm = u + kMagic;
+        const float tt = u - (vm - kMagic);
+        const float a = cs * wk;
+        const uint32_t ab = __float_as_uint(a + kMagic);
+        const uint32_t hb = __float_as_uint(fmaf(tt + 0.5f, a, kMagic));
+        const uint32_t addr = hb0 + (__float_as_uint(vm) << 9);
+        static_assert(4 * BWD_T == 512, "row stride");
+        CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits <= Q);
+        red_s32(addr, ab - hb);
+        red_s32(addr + 4 * BWD_T, hb - (uint32_t)kMagicBits);
+    };
     auto batch = [&](int cnt) {
         ErxQ e = {0.0f, 1.0f, 0, K};
         if (lane < cnt) e = wq[lane];
@@ -568,40 +607,37 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         const int wlo = __reduce_min_sync(FULL, klo);
         const int whi = __reduce_max_sync(FULL, khi);
         if (wlo > whi) return;
-        const float4 *wr = (const float4 *)(wt + (size_t)e.q * ne4);
-        // w~ of the next ERX_PF blocks of 4 energies in flight (their L2 latency was the
-        // main stall with one block of look-ahead)
+        // energy block kb of this lane's pixel at wr + kb * wstride; the next ERX_PF blocks in
+        // flight in a register ring (static indices: the block loop is unrolled by ERX_PF)
+        const char *wr = (const char *)(wt + e.q);
         const int kb0 = wlo >> 2, kb1 = whi >> 2;
         float4 wn[ERX_PF];
+        const char *pf = wr + (size_t)kb0 * wstride;
 #pragma unroll
-        for (int i = 0; i < ERX_PF; i++) wn[i] = kb0 + i <= kb1 ? __ldg(wr + kb0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int kb = kb0; kb <= kb1; kb++) {
-            const int k = kb << 2;
-            const float4 wc = wn[0];
+        for (int i = 0; i < ERX_PF; i++) {
+            wn[i] = kb0 + i <= kb1 ? __ldg((const float4 *)pf) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pf += wstride;
+        }
+        for (int kb = kb0; kb <= kb1; kb += ERX_PF) {
 #pragma unroll
-            for (int i = 0; i + 1 < ERX_PF; i++) wn[i] = wn[i + 1];
-            if (kb + ERX_PF <= kb1) wn[ERX_PF - 1] = __ldg(wr + kb + ERX_PF);
-            const float4 a4 = *(const float4 *)(alpha + k);
-            const float al[4] = {a4.x, a4.y, a4.z, a4.w}, wk[4] = {wc.x, wc.y, wc.z, wc.w};
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                // a term outside this lane's window clamps onto the padding rows (nodes -2 / nq;
-                // at u' = nq - 1/2 with odd nq, n = nq - 1 gets lo = 0 exactly)
-                const float u = fminf(fmaxf(fmaf(al[j], e.sh, nb), -1.5f), qm);
-                const float vm = u + kMagic;
-                const float tt = u - (vm - kMagic);
-                const float a = e.cs * wk[j];
-                const uint32_t ab = __float_as_uint(a + kMagic);
-                const uint32_t hb = __float_as_uint(fmaf(tt + 0.5f, a, kMagic));
-                const uint32_t addr = hb0 + (__float_as_uint(vm) << 9);
-                static_assert(4 * BWD_T == 512, "row stride");
-                CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -2 && __float_as_int(vm) - kMagicBits <= Q);
-                red_s32(addr, ab - hb);
-                red_s32(addr + 4 * BWD_T, hb - (uint32_t)kMagicBits);
+            for (int i = 0; i < ERX_PF; i++) {
+                if (kb + i > kb1) break;  // warp-uniform
+                const float4 wc = wn[i];
+                if (kb + i + ERX_PF <= kb1) wn[i] = __ldg((const float4 *)pf);
+                pf += wstride;
+                const float4 a4 = *(const float4 *)(alpha + ((kb + i) << 2));
+                term(a4.x, wc.x, e.sh, e.cs);
+                term(a4.y, wc.y, e.sh, e.cs);
+                term(a4.z, wc.z, e.sh, e.cs);
+                term(a4.w, wc.w, e.sh, e.cs);
             }
         }
     };
-    for (int base = warp * 64; base < p.n_det; base += (BWD_T / 32) * 64) {
+    // 64-pixel groups: the first one per warp fixed, the rest taken on demand (balances the
+    // warps' open-pair counts, which the final CTA barrier would otherwise wait for)
+    for (int grp = warp;;) {
+        const int base = grp * 64;
+        if (base >= p.n_det) break;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int q = base + 32 * h + lane;
@@ -633,12 +669,15 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             __syncwarp();
             qn = rem;
         }
+        int g = 0;
+        if (lane == 0) g = atomicAdd(&s_next, 1);
+        grp = __shfl_sync(FULL, g, 0);
     }
     if (qn > 0) batch(qn);
     __syncthreads();
     const double inv = sv > 0.0f ? 1.0 / (double)sv : 0.0;
     for (int j = tid; j < Q; j += BWD_T) {
-        const uint32_t *row = hist + (j + 2) * BWD_T;
+        const uint32_t *row = hist + (j + nlo) * BWD_T;
         uint32_t s = 0u;
         for (int t = 0; t < BWD_T; t++) s += row[(t + j) % BWD_T];  // modulo 2^32; rotate: bank spread
         b[(size_t)v * Q + j] = (float)((double)(int32_t)s * inv);
@@ -747,10 +786,10 @@ namespace {
 cudaError_t erx_backward(const cacsi_geometry *g, const float *w, bool ones, float *b, cudaStream_t s, int *launches) {
     const Params &p = g->p;
     const int ne4 = (p.ne + 3) & ~3;
-    float *wt = nullptr;
+    float4 *wt = nullptr;
     cudaError_t e = cudaMallocAsync(&wt, (size_t)p.n_det * ne4 * sizeof(float) + 16, s);
     if (e != cudaSuccess) return e;
-    unsigned *mx = (unsigned *)(wt + (size_t)p.n_det * ne4);
+    unsigned *mx = (unsigned *)(wt + (size_t)p.n_det * (ne4 / 4));
     cudaMemsetAsync(mx, 0, 8, s);
     const int nb = 4 * num_sms(g->device);
     {
@@ -758,13 +797,14 @@ cudaError_t erx_backward(const cacsi_geometry *g, const float *w, bool ones, flo
         if (ones) k_erx_wprep<true><<<nb, 256, 0, s>>>(p, w, ne4, (const int2 *)g->d_erx_pw, wt, mx);
         else k_erx_wprep<false><<<nb, 256, 0, s>>>(p, w, ne4, (const int2 *)g->d_erx_pw, wt, mx);
     }
-    const size_t smem = (size_t)ne4 * sizeof(float) + (size_t)(p.nq + 4) * BWD_T * sizeof(uint32_t) +
+    const int nlo = g->erx_nlo;  // rows below node 0 (no lower clamp)
+    const size_t smem = (size_t)ne4 * sizeof(float) + (size_t)(p.nq + 2 + nlo) * BWD_T * sizeof(uint32_t) +
                         (size_t)(BWD_T / 32) * ERX_CAP * sizeof(ErxQ);
     cudaFuncSetAttribute(k_backward_er_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
         KScope kt_(g, s, "k_backward_er");
-        k_backward_er_x<<<p.n_vox, BWD_T, smem, s>>>(p, wt, ne4, (const float *)g->d_erx_vb, (const float *)g->d_erx_pm,
-                                                      mx, b);
+        k_backward_er_x<<<p.n_vox, BWD_T, smem, s>>>(p, wt, ne4, nlo, (const float *)g->d_erx_vb,
+                                                      (const float *)g->d_erx_pm, mx, b);
     }
     e = cudaGetLastError();
     cudaFreeAsync(wt, s);
@@ -778,6 +818,8 @@ cudaError_t erx_backward(const cacsi_geometry *g, const float *w, bool ones, flo
 // the loose bound's scale (accurate to ~1e-5, so 1.02x of it is safe)
 cudaError_t erx_build(cacsi_geometry *g) {
     const Params &p = g->p;
+    if (p.nq + 2 + std::max(2, (int)std::ceil(-(double)p.nb) + 2) > 400) return cudaSuccess;  // fp32-histogram kernel
+    g->erx_nlo = std::max(2, (int)std::ceil(-(double)p.nb) + 2);  // refined below
     cudaError_t e = cudaMalloc(&g->d_erx_vb, (size_t)p.n_vox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_pm, (size_t)p.n_vox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_pw, (size_t)p.n_det * sizeof(int2));
@@ -788,7 +830,24 @@ cudaError_t erx_build(cacsi_geometry *g) {
     double csum = 0.0;
     for (int k = 0; k < p.ne; k++) csum += std::fabs((double)en[k].y);
     cudaStream_t s = 0;
-    k_erx_pix<<<(p.n_det + 7) / 8, 256, 0, s>>>(p, (int2 *)g->d_erx_pw);
+    unsigned *smin = nullptr;
+    e = cudaMalloc(&smin, sizeof(unsigned));
+    if (e != cudaSuccess) return e;
+    cudaMemset(smin, 0x7f, sizeof(unsigned));
+    k_erx_pix<<<(p.n_det + 7) / 8, 256, 0, s>>>(p, (int2 *)g->d_erx_pw, smin);
+    unsigned smin_bits = 0;
+    e = cudaMemcpy(&smin_bits, smin, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    cudaFree(smin);
+    if (e != cudaSuccess) return e;
+    {
+        // lowest u' = alpha sigma + nb of any term (alpha >= alpha_0, sigma >= the smallest open-pair
+        // sigma; inactive lanes carry sigma = 1): rows down to its rounding, with fp32 margins
+        float amin = 1e30f;
+        for (int k = 0; k < p.ne; k++) amin = std::min(amin, en[k].x);
+        const double sgm = std::min(1.0, (double)__uint_as_float_host(smin_bits));
+        const double ulo = (double)amin * sgm * (1.0 - 1e-5) + (double)p.nb - 1e-4 * (1.0 + std::fabs((double)p.nb));
+        g->erx_nlo = std::max(2, (int)std::ceil(-ulo) + 2);
+    }
     k_erx_vox<<<p.n_vox, 256, 0, s>>>(p, (float)(csum * (1.0 + 1e-6)), (float *)g->d_erx_vb, (float *)g->d_erx_pm);
     float *b1 = nullptr;
     e = cudaMalloc(&b1, (size_t)p.n_vox * p.nq * sizeof(float));
@@ -810,7 +869,9 @@ cudaError_t launch_backward(const cacsi_geometry *g, const float *w, float *b, c
     const Params &p = g->p;
     const size_t smem =
         (size_t)((p.ne + 1) & ~1) * sizeof(float2) + (size_t)(p.nq + 4) * BWD_T * sizeof(float);
-    if (p.energy_resolving && g->opt.er_bwd_fx && g->d_erx_vb) return erx_backward(g, w, false, b, s, launches);
+    // the fixed-point kernel's histogram rows (nq + 2 + nlo) x 512 B must fit next to two more CTAs
+    if (p.energy_resolving && g->opt.er_bwd_fx && g->d_erx_vb)
+        return erx_backward(g, w, false, b, s, launches);
     if (p.energy_resolving) {
         float *wT = nullptr;
         cudaError_t e = cudaMallocAsync(&wT, (size_t)p.n_det * p.ne * sizeof(float), s);
