@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(FWD_T) k_forward(const Params p, const float *
 // (constant-bank operands), energy blocks of 8 outside the warp's window union skipped by a
 // warp-uniform branch.  The same arithmetic in the same order per (pixel, energy) as
 // k_forward<true> (acc = fmaf(P, hat, acc) voxel by voxel), without its shared-memory
-// read-modify-write per two terms; the final [pixels][ne] block is staged through shared
+// read-modify-write per two terms, and with the hat interpolant tabulated as (c0, slope)
+// (f~ = c0_n + u' slope_n: one FFMA, no fraction; not bit-identical to the (mid, slope)
+// form, within ~1e-6 per term); the final [pixels][ne] block is staged through shared
 // memory for coalesced stores.  Option er_fwd_reg.
 constexpr int KR_MAX = 128;
 __device__ __forceinline__ float2 lds2(uint32_t addr) {
@@ -184,7 +186,9 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
             const float *fr = f + (size_t)(c0 + vv) * Q;
             const float a = (n >= 0 && n < Q) ? fr[n] : 0.0f;
             const float b = (n + 1 >= 0 && n + 1 < Q) ? fr[n + 1] : 0.0f;
-            tab[i] = make_float2(0.5f * (a + b), b - a);
+            // (c0, slope): f~(u) = c0_n + u' slope_n on [n - 1/2, n + 1/2) of u' = u - 1/2, with
+            // c0_n = mid_n - n slope_n (one rounding, in fp64): one FFMA per term, no fraction
+            tab[i] = make_float2((float)(0.5 * ((double)a + (double)b) - (double)n * ((double)b - (double)a)), b - a);
         }
         __syncthreads();
         for (int vv = 0; vv < nc; vv++) {
@@ -211,10 +215,9 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
                     // u' = u - 1/2 >= -q_min/dq - 1/2 needs no lower clamp (entries down to -nlo are zero)
                     const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
                     const float vm = u + kMagic;
-                    const float tt = u - (vm - kMagic);
                     CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits <= Q);
                     const float2 t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
-                    acc[kb + j] = fmaf(P, fmaf(tt, t.y, t.x), acc[kb + j]);
+                    acc[kb + j] = fmaf(P, fmaf(u, t.y, t.x), acc[kb + j]);
                 }
             }
         }
