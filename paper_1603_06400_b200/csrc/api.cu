@@ -149,6 +149,7 @@ const OptKey kOptKeys[] = {
     {"pc_q8", &cacsi::Opts::pc_q8, true, 0, 2},
     {"pcv_budget_kb", &cacsi::Opts::pcv_budget_kb, true, 16, 227},
     {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
+    {"pc_perm_lane", &cacsi::Opts::pc_perm_lane, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
     {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
     {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},

@@ -1321,7 +1321,19 @@ cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
                     uint32_t *kb = (uint32_t *)g->d_pc_bt;
                     float *Pb = (float *)g->d_pc_P;
                     const int wn = g->opt.pc_win;
-                    if (jyb == 2) {
+                    if (wn == 128 && g->opt.pc_perm_lane && E.pc_n % 128 == 0) {
+                        // one window per lane (bit-identical to k_pc_perm<., 128>)
+                        const size_t sm = (size_t)PERM2_W * 5 * 4096;
+                        const long long nwin = E.pc_n / 128;
+                        const int gr3 = 2 * sm_count(g->device);
+                        if (jyb == 2) {
+                            cudaFuncSetAttribute(k_pc_perm128<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                            k_pc_perm128<uint16_t><<<gr3, PERM2_W * 32, sm>>>(nwin, E.pc_tbits, kb, Pb, (uint16_t *)g->d_pc_q);
+                        } else {
+                            cudaFuncSetAttribute(k_pc_perm128<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                            k_pc_perm128<uint32_t><<<gr3, PERM2_W * 32, sm>>>(nwin, E.pc_tbits, kb, Pb, (uint32_t *)g->d_pc_q);
+                        }
+                    } else if (jyb == 2) {
                         uint16_t *qb = (uint16_t *)g->d_pc_q;
                         if (wn == 512) k_pc_perm<uint16_t, 512><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);
                         else if (wn == 256) k_pc_perm<uint16_t, 256><<<gr2, PERM_W * 32>>>(p, E, segR, kb, Pb, qb);

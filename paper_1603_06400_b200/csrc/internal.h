@@ -188,6 +188,7 @@ struct Opts {
     int pc_q8 = 2;            // "pc_q8": 8-byte records (pixel offset from a per-window base): 1 = 10-bit tau; 2 = P rounded to 28 bits carrying 4 offset bits, tau with tbits - 5 bits
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
+    int pc_perm_lane = 1;     // "pc_perm_lane": 0 = the bank-aware permutation one window per warp (k_pc_perm)
     // per call (cacsi_set_option may change them between calls)
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split

@@ -174,6 +174,84 @@ constexpr int PERM_W = 8;  // warps per CTA
 // WIN / 128 warps that stream the window, record slot g % 4 of every lane's four); a wider
 // window gives the greedy more records to spread over the banks (option pc_win).
 // In place: a warp reads its whole window into registers before it writes any record back.
+// The same greedy assignment for 128-record windows, one window per LANE: the greedy is
+// sequential within a window, so k_pc_perm's warp-per-window form spends each record on a
+// warp reduction with 4 of 32 lanes scoring; here 32 windows run side by side, each lane
+// scoring its window's four groups from lane-private counters in shared memory ([..][lane]
+// bytes: conflict-free).  Every segment is padded to whole windows, so window w is records
+// 128 w .. 128 w + 127.  Same scores, same tie rule (lowest group), same positions
+// (4 * fill + group): the cache comes out bit-identical to k_pc_perm<QT, 128>.
+constexpr int PERM2_W = 4;  // warps per CTA (80 KB of shared memory)
+template <typename QT>
+__global__ void __launch_bounds__(PERM2_W * 32) k_pc_perm128(long long nwin, int tbits, uint32_t *bt, float *Pr,
+                                                             QT *qr) {
+    extern __shared__ __align__(16) uint8_t sm8[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    uint8_t *s_b = sm8 + wl * 5 * 4096;   // [128 records][32 windows]
+    uint8_t *s_q = s_b + 4096;            // [128][32]
+    uint8_t *s_pos = s_q + 4096;          // [128][32]
+    uint8_t *s_cb = s_pos + 4096;         // [4 groups][32 colours][32 windows] -- cell colours
+    uint8_t *s_cq = s_cb + 4096;          // [4][32][32] -- pixel colours
+    for (long long wb = (long long)blockIdx.x * PERM2_W + wl; wb * 32 < nwin; wb += (long long)gridDim.x * PERM2_W) {
+        const long long w0 = wb * 32;                      // first window of this warp
+        const int nw = (int)min(32LL, nwin - w0);          // windows (lanes) with work
+        const size_t r0 = (size_t)w0 * 128;                // first record
+        // counters to zero (32-bit stores) and the windows' colours, record-major per lane
+        for (int i = lane; i < 2048; i += 32) ((uint32_t *)s_cb)[i] = 0u;  // s_cb and s_cq (8 KB)
+        for (int i = lane; i < nw * 128; i += 32) {
+            const int ww = i >> 7, r = i & 127;
+            s_b[r * 32 + ww] = (uint8_t)((bt[r0 + i] >> tbits) & 31u);
+            s_q[r * 32 + ww] = (uint8_t)((uint32_t)qr[r0 + i] & 31u);
+        }
+        __syncwarp();
+        if (lane < nw) {
+            int f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+            for (int r = 0; r < 128; r++) {
+                const int b = s_b[r * 32 + lane], qq = s_q[r * 32 + lane];
+                uint8_t *cb = s_cb + b * 32 + lane, *cq = s_cq + qq * 32 + lane;
+                const int b0 = cb[0], b1 = cb[1024], b2 = cb[2048], b3 = cb[3072];
+                const int q0 = cq[0], q1 = cq[1024], q2 = cq[2048], q3 = cq[3072];
+                const int s0 = f0 < 32 ? 2 * b0 + q0 : 1 << 24, s1 = f1 < 32 ? 2 * b1 + q1 : 1 << 24;
+                const int s2 = f2 < 32 ? 2 * b2 + q2 : 1 << 24, s3 = f3 < 32 ? 2 * b3 + q3 : 1 << 24;
+                // argmin, lowest group on ties
+                int g = 0, sc = s0, fb = f0, bb = b0, qb = q0;
+                if (s1 < sc) g = 1, sc = s1, fb = f1, bb = b1, qb = q1;
+                if (s2 < sc) g = 2, sc = s2, fb = f2, bb = b2, qb = q2;
+                if (s3 < sc) g = 3, sc = s3, fb = f3, bb = b3, qb = q3;
+                s_pos[r * 32 + lane] = (uint8_t)(4 * fb + g);
+                cb[g * 1024] = (uint8_t)(bb + 1);
+                cq[g * 1024] = (uint8_t)(qb + 1);
+                f0 += g == 0, f1 += g == 1, f2 += g == 2, f3 += g == 3;
+            }
+        }
+        __syncwarp();
+        // apply: window by window, each lane moves records 4 lane .. 4 lane + 3 of it
+        for (int ww = 0; ww < nw; ww++) {
+            const size_t base = r0 + (size_t)ww * 128;
+            uint32_t k[4];
+            float P[4];
+            QT q[4];
+            int pos[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int r = 4 * lane + j;
+                k[j] = bt[base + r];
+                P[j] = Pr[base + r];
+                q[j] = qr[base + r];
+                pos[j] = s_pos[r * 32 + ww];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                bt[base + pos[j]] = k[j];
+                Pr[base + pos[j]] = P[j];
+                qr[base + pos[j]] = q[j];
+            }
+            __syncwarp();
+        }
+    }
+}
+
 template <typename QT, int WIN>
 __global__ void __launch_bounds__(PERM_W * 32) k_pc_perm(const Params p, const Esai e, int R, uint32_t *bt, float *Pr,
                                                          QT *qr) {

@@ -3,6 +3,6 @@
 TAG=${1:-erxn}
 KS=${2:-"k_forward_reg|k_backward_er_x"}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1
-timeout 1500 ncu --set full --replay-mode application --clock-control none --import-source on -k "regex:${KS}" -s 1 -c 2 \
+timeout 1500 ncu --set full --replay-mode application --clock-control none --import-source on -k "regex:${KS}" -s ${3:-1} -c ${4:-2} \
   -o gpurun_out/${TAG}_prof python scripts/run_config4.py > gpurun_out/${TAG}_ncu.log 2>&1
 echo rc=$?; tail -2 gpurun_out/${TAG}_ncu.log

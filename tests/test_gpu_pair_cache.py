@@ -198,3 +198,20 @@ def test_backward_l1_prefetch_bitwise(ci):
     b1 = gpu_backward(G, w)
     G.set_option("pcb_pfl1", 0)
     assert np.array_equal(gpu_backward(G, w), b1)
+
+
+@pytest.mark.parametrize("ci", [1, 2])
+def test_lane_permutation_bitwise(ci):
+    """The bank-aware permutation with one window per lane (k_pc_perm128, pc_perm_lane=1, the
+    default) makes the same assignment as the warp-per-window greedy (pc_perm_lane=0): the
+    operators give the same bits."""
+    cfg = make_config(ci)
+    f = rnd(cfg.f_shape, ci, 77)
+    w = rnd((cfg.det_nx, cfg.det_ny), ci, 78)
+    res = []
+    for v in (1, 0):
+        G = P.Geometry(cfg.desc(), options=f"pc_perm_lane={v}")
+        res.append((gpu_forward(G, f), gpu_backward(G, w)))
+        G.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
