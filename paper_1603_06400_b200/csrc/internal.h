@@ -189,6 +189,7 @@ struct Opts {
     int pcv_budget_kb = 200;  // "pcv_budget_kb": shared memory of the voxel-major forward
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     int pc_perm_lane = 1;     // "pc_perm_lane": 0 = the bank-aware permutation one window per warp (k_pc_perm)
+    int er_vcache = 1;        // "er_vcache": 0 = no voxel-major open-pair cache for the energy-resolving backward
     // per call (cacsi_set_option may change them between calls)
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
@@ -215,6 +216,7 @@ struct Opts {
     int er_fwd_reg = 1;       // "er_fwd_reg": 0 = the direct energy-resolving forward with shared-memory accumulators
     int er_fwd = 0;           // "er_fwd" (er_cache=1 only): 1 = the compacted pair-cache forward k_er_fwd2
     int er_bwd_fx = 1;        // "er_bwd_fx": 0 = the direct energy-resolving backward with fp32 shared-memory histograms
+    int er_vcache_use = 1;    // "er_vcache_use": 0 = its pair geometry recomputed per call even when the cache exists
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
 };
 
@@ -240,6 +242,8 @@ struct cacsi_geometry {
     // fixed-point energy-resolving backward (operators.cu): per voxel bin bound
     // and max P, per pixel energy-window union over its open pairs (built at create)
     void *d_erx_vb, *d_erx_pm, *d_erx_pw;
+    void *d_erx_voff, *d_erx_vw, *d_erx_vP, *d_erx_vs;  // its voxel-major open-pair cache (option er_vcache)
+    long long erx_vc_n;
     int erx_nlo;  // its histogram rows below node 0: u' >= alpha_0 min(sin(theta/2)) - q_min/dq - 1/2
     // host staging for the *_host entry points (device scratch)
     float *d_stage_a, *d_stage_b, *d_stage_c, *d_stage_d, *d_stage_ws;

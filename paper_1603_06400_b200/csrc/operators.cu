@@ -551,10 +551,19 @@ struct ErxQ {
 };
 constexpr int ERX_CAP = 96;
 constexpr int ERX_PF = 4;  // w~ blocks of look-ahead
+// Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
+// open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
+// P, sin(theta/2) (12 B per open pair; 39 GB on config 4); vc_off[v] = first record of voxel v.
+struct ErxCache {
+    const long long *off;
+    const uint32_t *w;
+    const float *P, *s;
+};
+template <bool CACHE>
 __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const float4 *__restrict__ wt, int ne4,
                                                          int nlo, const float *__restrict__ vb,
                                                          const float *__restrict__ pm, const unsigned *__restrict__ mx,
-                                                         float *__restrict__ b) {
+                                                         const ErxCache vc, float *__restrict__ b) {
     extern __shared__ float4 smem4[];
     const int Q = p.nq, K = p.ne, NR = Q + 2 + nlo;      // rows: nodes -nlo .. nq + 1
     float *alpha = (float *)smem4;                       // [ne4] (alpha_k; 1e30 beyond ne)
@@ -636,6 +645,26 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             }
         }
     };
+    if constexpr (CACHE) {
+        // the voxel's open pairs straight from the cache, 32 per batch, batches on demand
+        const long long r0 = vc.off[v], r1 = vc.off[v + 1];
+        for (long long bi = warp;;) {
+            const long long r = r0 + bi * 32;
+            if (r >= r1) break;
+            const int cnt = (int)min(32LL, r1 - r);
+            if (lane < cnt) {
+                const uint32_t wv = __ldg(vc.w + r + lane);
+                const int klo = (int)((wv >> 17) & 127u), khi1 = (int)(wv >> 24);
+                wq[lane] = ErxQ{__ldg(vc.P + r + lane) * sv, __ldg(vc.s + r + lane), (int)(wv & 0x1FFFFu), klo | (khi1 << 16)};
+            }
+            __syncwarp();
+            batch(cnt);
+            __syncwarp();
+            int g = 0;
+            if (lane == 0) g = atomicAdd(&s_next, 1);
+            bi = __shfl_sync(FULL, g, 0);
+        }
+    } else {
     // 64-pixel groups: the first one per warp fixed, the rest taken on demand (balances the
     // warps' open-pair counts, which the final CTA barrier would otherwise wait for)
     for (int grp = warp;;) {
@@ -677,6 +706,7 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         grp = __shfl_sync(FULL, g, 0);
     }
     if (qn > 0) batch(qn);
+    }
     __syncthreads();
     const double inv = sv > 0.0f ? 1.0 / (double)sv : 0.0;
     for (int j = tid; j < Q; j += BWD_T) {
@@ -684,6 +714,61 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         uint32_t s = 0u;
         for (int t = 0; t < BWD_T; t++) s += row[(t + j) % BWD_T];  // modulo 2^32; rotate: bank spread
         b[(size_t)v * Q + j] = (float)((double)(int32_t)s * inv);
+    }
+}
+
+// open pairs with a non-empty window (the backward's queue criterion), per voxel in pixel order
+__device__ __forceinline__ bool erx_pair(const Params &p, int v, const VoxelRec &vr, int q, float &P, float &sh,
+                                        int &klo, int &khi) {
+    if (!mask_open(p, v, q, vr, p.det[q])) return false;
+    pair_geom(p, vr, p.det[q], P, sh);
+    k_range(p, sh, klo, khi);
+    return klo <= khi;
+}
+__global__ void __launch_bounds__(256) k_erx_vcount(const Params p, long long *__restrict__ cnt) {
+    __shared__ int sc[8];
+    const int v = blockIdx.x, tid = threadIdx.x;
+    const VoxelRec vr = p.vox[v];
+    int c = 0;
+    for (int q = tid; q < p.n_det; q += 256) {
+        float P, sh;
+        int klo, khi;
+        c += erx_pair(p, v, vr, q, P, sh, klo, khi);
+    }
+    c = __reduce_add_sync(FULL, c);
+    if ((tid & 31) == 0) sc[tid >> 5] = c;
+    __syncthreads();
+    if (tid == 0) {
+        long long t = 0;
+        for (int i = 0; i < 8; i++) t += sc[i];
+        cnt[v] = t;
+    }
+}
+__global__ void __launch_bounds__(256) k_erx_vfill(const Params p, const long long *__restrict__ off,
+                                                   uint32_t *__restrict__ vw, float *__restrict__ vP,
+                                                   float *__restrict__ vs) {
+    __shared__ int sc[8];
+    const int v = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const VoxelRec vr = p.vox[v];
+    long long o = off[v];
+    for (int q0 = 0; q0 < p.n_det; q0 += 256) {
+        const int q = q0 + tid;
+        float P = 0.0f, sh = 0.0f;
+        int klo = 0, khi = -1;
+        const bool op = q < p.n_det && erx_pair(p, v, vr, q, P, sh, klo, khi);
+        const unsigned m = __ballot_sync(FULL, op);
+        if (lane == 0) sc[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int i = 0; i < 8; i++) before += i < warp ? sc[i] : 0, tot += sc[i];
+        if (op) {
+            const long long i = o + before + __popc(m & ((1u << lane) - 1u));
+            vw[i] = (uint32_t)q | ((uint32_t)klo << 17) | ((uint32_t)(khi + 1) << 24);
+            vP[i] = P;
+            vs[i] = sh;
+        }
+        o += tot;
+        __syncthreads();
     }
 }
 
@@ -803,11 +888,15 @@ cudaError_t erx_backward(const cacsi_geometry *g, const float *w, bool ones, flo
     const int nlo = g->erx_nlo;  // rows below node 0 (no lower clamp)
     const size_t smem = (size_t)ne4 * sizeof(float) + (size_t)(p.nq + 2 + nlo) * BWD_T * sizeof(uint32_t) +
                         (size_t)(BWD_T / 32) * ERX_CAP * sizeof(ErxQ);
-    cudaFuncSetAttribute(k_backward_er_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool cache = g->d_erx_voff && g->opt.er_vcache_use;
+    auto kb = cache ? k_backward_er_x<true> : k_backward_er_x<false>;
+    const ErxCache vc{(const long long *)g->d_erx_voff, (const uint32_t *)g->d_erx_vw, (const float *)g->d_erx_vP,
+                      (const float *)g->d_erx_vs};
+    cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     {
         KScope kt_(g, s, "k_backward_er");
-        k_backward_er_x<<<p.n_vox, BWD_T, smem, s>>>(p, wt, ne4, nlo, (const float *)g->d_erx_vb,
-                                                      (const float *)g->d_erx_pm, mx, b);
+        kb<<<p.n_vox, BWD_T, smem, s>>>(p, wt, ne4, nlo, (const float *)g->d_erx_vb, (const float *)g->d_erx_pm, mx,
+                                        vc, b);
     }
     e = cudaGetLastError();
     cudaFreeAsync(wt, s);
@@ -852,6 +941,43 @@ cudaError_t erx_build(cacsi_geometry *g) {
         g->erx_nlo = std::max(2, (int)std::ceil(-ulo) + 2);
     }
     k_erx_vox<<<p.n_vox, 256, 0, s>>>(p, (float)(csum * (1.0 + 1e-6)), (float *)g->d_erx_vb, (float *)g->d_erx_pm);
+    // the voxel-major open-pair cache (option er_vcache): counts, exclusive scan, fill; skipped
+    // when it would not leave 8 GB of device memory free or the pixel index needs > 17 bits
+    if (g->opt.er_vcache && p.n_det <= (1 << 17) && p.ne <= 127) {
+        long long *cnt = nullptr;
+        e = cudaMalloc(&g->d_erx_voff, (size_t)(p.n_vox + 1) * sizeof(long long));
+        if (e != cudaSuccess) return e;
+        cnt = (long long *)g->d_erx_voff;
+        k_erx_vcount<<<p.n_vox, 256, 0, s>>>(p, cnt);
+        std::vector<long long> h(p.n_vox + 1);
+        e = cudaMemcpy(h.data(), cnt, (size_t)p.n_vox * sizeof(long long), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return e;
+        long long tot = 0;
+        for (int v = 0; v < p.n_vox; v++) {
+            const long long c = h[v];
+            h[v] = tot;
+            tot += c;
+        }
+        h[p.n_vox] = tot;
+        size_t fr = 0, totmem = 0;
+        cudaMemGetInfo(&fr, &totmem);
+        const size_t need = (size_t)tot * 12 + 64;
+        if (need + ((size_t)8 << 30) <= fr) {
+            e = cudaMemcpy(cnt, h.data(), (size_t)(p.n_vox + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_vw, (size_t)tot * 4 + 16);
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_vP, (size_t)tot * 4 + 16);
+            if (e == cudaSuccess) e = cudaMalloc(&g->d_erx_vs, (size_t)tot * 4 + 16);
+            if (e != cudaSuccess) return e;
+            k_erx_vfill<<<p.n_vox, 256, 0, s>>>(p, cnt, (uint32_t *)g->d_erx_vw, (float *)g->d_erx_vP,
+                                                 (float *)g->d_erx_vs);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            g->erx_vc_n = tot;
+        } else {
+            cudaFree(g->d_erx_voff);
+            g->d_erx_voff = nullptr;
+        }
+    }
     float *b1 = nullptr;
     e = cudaMalloc(&b1, (size_t)p.n_vox * p.nq * sizeof(float));
     if (e != cudaSuccess) return e;

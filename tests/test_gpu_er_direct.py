@@ -135,3 +135,25 @@ def test_er_backward_fixed_point_config4_sampled():
     G.set_option("er_bwd_fx", 0)
     b0 = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
     assert_parity(b, b0, "c4 er backward fixed point vs fp32 histograms (every voxel)")
+    # the voxel-major open-pair cache (er_vcache) holds every open pair once: the same integer sums
+    assert G.query("er_vcache_records") > 0
+    G.set_option("er_bwd_fx", 1)
+    G.set_option("er_vcache_use", 0)
+    assert np.array_equal(gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq), b)
+
+
+@pytest.mark.parametrize("si", [0, 1, 2, 5])
+def test_er_backward_open_pair_cache_bitwise(si):
+    """Backward from the voxel-major open-pair cache (er_vcache, default) vs recomputing the pair
+    geometry per call (er_vcache_use=0): the integer sums are order-free, so the bits agree; the
+    cache holds exactly the pairs with an open mask cell and a non-empty energy window."""
+    d = _er_desc(**ER_BWD_SHAPES[si])
+    G = P.Geometry(d)
+    assert 0 < G.query("er_vcache_records") <= oracle.Geometry(d).count_terms()[1]
+    w = rnd(G.g_shape, 0, 170 + si)
+    b1 = gpu_backward(G, w)
+    G.set_option("er_vcache_use", 0)
+    assert np.array_equal(gpu_backward(G, w), b1)
+    G2 = P.Geometry(d, options="er_vcache=0")
+    assert G2.query("er_vcache_records") == 0
+    assert np.array_equal(gpu_backward(G2, w), b1)
