@@ -550,7 +550,7 @@ struct ErxQ {
     int q, kw;     // pixel, klo | (khi + 1) << 16
 };
 constexpr int ERX_CAP = 96;
-constexpr int ERX_PF = 4;  // w~ blocks of look-ahead
+constexpr int ERX_PF = 8;  // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
 // Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
 // open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
 // P, sin(theta/2) (12 B per open pair; 39 GB on config 4); vc_off[v] = first record of voxel v.
@@ -648,21 +648,29 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
     if constexpr (CACHE) {
         // the voxel's open pairs straight from the cache, 32 per batch, batches on demand
         const long long r0 = vc.off[v], r1 = vc.off[v + 1];
-        for (long long bi = warp;;) {
-            const long long r = r0 + bi * 32;
-            if (r >= r1) break;
-            const int cnt = (int)min(32LL, r1 - r);
+        // records of the next batch loaded while the current one deposits
+        auto load = [&](long long bi, uint32_t &wv, float &P, float &sg) {
+            const long long r = r0 + bi * 32 + lane;
+            wv = 0u, P = 0.0f, sg = 1.0f;
+            if (r < r1) wv = __ldg(vc.w + r), P = __ldg(vc.P + r), sg = __ldg(vc.s + r);
+        };
+        long long bi = warp;
+        uint32_t wv;
+        float rP, rs;
+        load(bi, wv, rP, rs);
+        while (r0 + bi * 32 < r1) {
+            const int cnt = (int)min(32LL, r1 - (r0 + bi * 32));
             if (lane < cnt) {
-                const uint32_t wv = __ldg(vc.w + r + lane);
                 const int klo = (int)((wv >> 17) & 127u), khi1 = (int)(wv >> 24);
-                wq[lane] = ErxQ{__ldg(vc.P + r + lane) * sv, __ldg(vc.s + r + lane), (int)(wv & 0x1FFFFu), klo | (khi1 << 16)};
+                wq[lane] = ErxQ{rP * sv, rs, (int)(wv & 0x1FFFFu), klo | (khi1 << 16)};
             }
-            __syncwarp();
-            batch(cnt);
-            __syncwarp();
             int g = 0;
             if (lane == 0) g = atomicAdd(&s_next, 1);
             bi = __shfl_sync(FULL, g, 0);
+            load(bi, wv, rP, rs);
+            __syncwarp();
+            batch(cnt);
+            __syncwarp();
         }
     } else {
     // 64-pixel groups: the first one per warp fixed, the rest taken on demand (balances the
