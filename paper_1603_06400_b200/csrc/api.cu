@@ -175,6 +175,7 @@ const OptKey kOptKeys[] = {
     {"er_bwd_dense", &cacsi::Opts::er_bwd_dense, false, 0, 1},
     {"er_fwd", &cacsi::Opts::er_fwd, false, 0, 1},
     {"er_fwd_reg", &cacsi::Opts::er_fwd_reg, false, 0, 1},
+    {"er_fwd_lane", &cacsi::Opts::er_fwd_lane, false, 0, 1},
     {"er_bwd_fx", &cacsi::Opts::er_bwd_fx, false, 0, 1},
     {"er_vcache_use", &cacsi::Opts::er_vcache_use, false, 0, 1},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},

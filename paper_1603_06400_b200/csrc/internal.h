@@ -215,6 +215,7 @@ struct Opts {
     int er_bwd_dense = 0;     // "er_bwd_dense": 1 = energy-resolving backward without compaction
     int er_fwd_reg = 1;       // "er_fwd_reg": 0 = the direct energy-resolving forward with shared-memory accumulators
     int er_fwd = 0;           // "er_fwd" (er_cache=1 only): 1 = the compacted pair-cache forward k_er_fwd2
+    int er_fwd_lane = 1;      // "er_fwd_lane": 0 = the register forward with warp-uniform voxels (k_forward_reg)
     int er_bwd_fx = 1;        // "er_bwd_fx": 0 = the direct energy-resolving backward with fp32 shared-memory histograms
     int er_vcache_use = 1;    // "er_vcache_use": 0 = its pair geometry recomputed per call even when the cache exists
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches

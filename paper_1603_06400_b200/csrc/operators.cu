@@ -240,6 +240,92 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
     }
 }
 
+// The register forward with PER-LANE voxel streams (option er_fwd_lane, default): lanes stay
+// pixels with their KR energy sums in registers, but within each staged chunk of FWD_VC voxels a
+// lane walks only ITS open voxels (a 16-bit mask of mask tests), so a step costs one open pair
+// per busy lane instead of one voxel for all 32 lanes with about half of them closed (config 4:
+// ~0.6 instead of ~0.45 useful lane-slots, and the pair geometry only for open pairs).  Each lane
+// reads its own voxel's row of the (c0, slope) table (row stride QR odd: rows start on different
+// banks); the warp's energy blocks span the union of its lanes' windows.  Same per-term arithmetic
+// as k_forward_reg; the order of the voxels in each pixel's sum is unchanged (increasing v).
+template <int KR>
+__global__ void __launch_bounds__(FWD_T, 3) k_forward_lane(const Params p, const float *__restrict__ f,
+                                                           int vox_per_split, float *__restrict__ partial,
+                                                           const AlphaTab at, int nlo, int QR) {
+    extern __shared__ float4 smem4[];
+    const int Q = p.nq, K = p.ne;
+    float2 *tab = (float2 *)smem4;                          // [VC][QR] (c0, slope); reused to stage the output
+    VoxelRec *svox = (VoxelRec *)(tab + ((FWD_VC * QR + 1) & ~1));  // [VC]
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int pix = blockIdx.x * FWD_T + tid;
+    const bool valid = pix < p.n_det;
+    const float2 d = p.det[valid ? pix : 0];
+    const int v0 = blockIdx.y * vox_per_split;
+    const int v1 = min(p.n_vox, v0 + vox_per_split);
+    const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab + nlo) - (uint32_t)kMagicBits * 8u;
+    float acc[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) acc[k] = 0.0f;
+    for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
+        const int nc = min(FWD_VC, v1 - c0);
+        __syncthreads();
+        for (int i = tid; i < nc * QR; i += FWD_T) {
+            const int vv = i / QR, n = i - vv * QR - nlo;
+            const float *fr = f + (size_t)(c0 + vv) * Q;
+            const float a = (n >= 0 && n < Q) ? fr[n] : 0.0f;
+            const float b = (n + 1 >= 0 && n + 1 < Q) ? fr[n + 1] : 0.0f;
+            tab[i] = make_float2((float)(0.5 * ((double)a + (double)b) - (double)n * ((double)b - (double)a)), b - a);
+        }
+        if (tid < nc) svox[tid] = p.vox[c0 + tid];
+        __syncthreads();
+        // this lane's open voxels of the chunk
+        uint32_t m = 0u;
+        if (valid)
+            for (int vv = 0; vv < nc; vv++) m |= (uint32_t)mask_open(p, c0 + vv, pix, svox[vv], d) << vv;
+        while (__any_sync(FULL, m != 0u)) {
+            const int vv = m ? __ffs(m) - 1 : -1;
+            m &= m - 1u;
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1;
+            if (vv >= 0) {
+                pair_geom(p, svox[vv], d, P, sh);
+                k_range(p, sh, klo, khi);
+            }
+            const int wlo = __reduce_min_sync(FULL, klo);
+            const int whi = __reduce_max_sync(FULL, khi);
+            const uint32_t tb = tab0 + (uint32_t)(max(vv, 0) * QR) * 8u;  // this lane's row, folded with the magic bits
+#pragma unroll
+            for (int kb = 0; kb < KR; kb += 8) {
+                if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
+                    const float vm = u + kMagic;
+                    CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits <= Q);
+                    const float2 t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
+                    acc[kb + j] = fmaf(P, fmaf(u, t.y, t.x), acc[kb + j]);
+                }
+            }
+        }
+    }
+    // [pixels][K] block of this CTA through shared memory (coalesced stores), scaled by c_k
+    float *stage = (float *)smem4;
+    const int npx = min(FWD_T, p.n_det - (int)blockIdx.x * FWD_T);
+    float *out = partial + ((size_t)blockIdx.y * p.n_det + (size_t)blockIdx.x * FWD_T) * K;
+    for (int kb = 0; kb < KR; kb += 32) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            if (kb + j < KR) stage[j * (FWD_T + 1) + tid] = acc[kb + j];
+        __syncthreads();
+        const int kn = min(32, K - kb);
+        for (int i = tid; i < npx * kn; i += FWD_T) {
+            const int px = i / kn, k = i - px * kn;
+            out[(size_t)px * K + kb + k] = p.energy[kb + k].y * stage[k * (FWD_T + 1) + px];
+        }
+    }
+}
+
 // [rows][cols] -> [cols][rows] (32 x 32 shared-memory tiles)
 __global__ void k_transpose(const float *__restrict__ in, int rows, int cols, float *__restrict__ out) {
     __shared__ float t[32][33];
@@ -550,7 +636,7 @@ struct ErxQ {
     int q, kw;     // pixel, klo | (khi + 1) << 16
 };
 constexpr int ERX_CAP = 96;
-constexpr int ERX_PF = 8;  // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
+constexpr int ERX_PF = 8;   // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
 // Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
 // open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
 // P, sin(theta/2) (12 B per open pair; 39 GB on config 4); vc_off[v] = first record of voxel v.
@@ -835,10 +921,14 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
         for (int k = 0; k < KR_MAX; k++) at.a[k] = k < p.ne ? en[k].x : 1e30f;
         auto kf = p.ne <= 16 ? k_forward_reg<16> : p.ne <= 32 ? k_forward_reg<32> : p.ne <= 64 ? k_forward_reg<64>
                 : p.ne <= 104 ? k_forward_reg<104> : k_forward_reg<128>;
+        if (g->opt.er_fwd_lane)
+            kf = p.ne <= 16 ? k_forward_lane<16> : p.ne <= 32 ? k_forward_lane<32> : p.ne <= 64 ? k_forward_lane<64>
+               : p.ne <= 104 ? k_forward_lane<104> : k_forward_lane<128>;
         // table entries below node 0: u' >= nb = -q_min/dq - 1/2 rounds to n >= -(ceil(-nb) + 1)
         const int nlo = std::max(2, (int)std::ceil(-(double)p.nb) + 2);
         const int QR = (p.nq + 1 + nlo) | 1;  // odd row stride (float2): rows start on different banks
-        const size_t sm2 = std::max((size_t)(FWD_VC * QR) * sizeof(float2), (size_t)32 * (FWD_T + 1) * sizeof(float));
+        const size_t sm2 = std::max((size_t)((FWD_VC * QR + 1) & ~1) * sizeof(float2) + FWD_VC * sizeof(VoxelRec),
+                                    (size_t)32 * (FWD_T + 1) * sizeof(float));
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         {
             KScope kt_(g, s, "k_forward_er");

@@ -25,6 +25,9 @@ def test_er_forward_registers_bitwise_and_oracle(ne):
     G = P.Geometry(d)
     f = rnd(G.f_shape, 0, 140)
     g1 = gpu_forward(G, f)
+    # per-lane voxel streams (er_fwd_lane=1, the default) vs warp-uniform voxels: same sums, same order
+    G.set_option("er_fwd_lane", 0)
+    assert np.array_equal(gpu_forward(G, f), g1)
     G.set_option("er_fwd_reg", 0)
     g0 = gpu_forward(G, f)
     assert_parity(g1, g0, f"er forward registers vs shared accumulators ne={ne}", l2=1e-6, mr=1e-5)
@@ -124,9 +127,14 @@ def test_er_backward_fixed_point_zero_and_outliers():
 
 
 def test_er_backward_fixed_point_config4_sampled():
-    """Config 4 at full size: sampled voxels against the oracle, plus the fp32-histogram kernel."""
+    """Config 4 at full size: sampled voxels against the oracle, plus the fp32-histogram kernel;
+    the forward's per-lane voxel streams against warp-uniform voxels (bitwise)."""
     cfg = make_config(4)
     G, O = P.Geometry(cfg.desc()), oracle.Geometry(cfg.desc())
+    g1 = gpu_forward(G, cfg.f)
+    G.set_option("er_fwd_lane", 0)
+    assert np.array_equal(gpu_forward(G, cfg.f), g1)
+    G.set_option("er_fwd_lane", 1)
     w = rnd(G.g_shape, 4, 162)
     b = gpu_backward(G, w).reshape(cfg.n_vox, cfg.nq)
     rng = np.random.default_rng(4)
