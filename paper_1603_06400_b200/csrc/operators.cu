@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_reg(const Params p, const 
     }
 }
 
+constexpr int FWL_VC = 32;  // voxels per staged chunk of k_forward_lane (a 32-bit open mask per lane)
 // The register forward with PER-LANE voxel streams (option er_fwd_lane, default): lanes stay
 // pixels with their KR energy sums in registers, but within each staged chunk of FWD_VC voxels a
 // lane walks only ITS open voxels (a 16-bit mask of mask tests), so a step costs one open pair
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_lane(const Params p, const
     extern __shared__ float4 smem4[];
     const int Q = p.nq, K = p.ne;
     float2 *tab = (float2 *)smem4;                          // [VC][QR] (c0, slope); reused to stage the output
-    VoxelRec *svox = (VoxelRec *)(tab + ((FWD_VC * QR + 1) & ~1));  // [VC]
+    VoxelRec *svox = (VoxelRec *)(tab + ((FWL_VC * QR + 1) & ~1));  // [VC]
     const int tid = threadIdx.x, lane = tid & 31;
     const int pix = blockIdx.x * FWD_T + tid;
     const bool valid = pix < p.n_det;
@@ -266,8 +267,8 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_lane(const Params p, const
     float acc[KR];
 #pragma unroll
     for (int k = 0; k < KR; k++) acc[k] = 0.0f;
-    for (int c0 = v0; c0 < v1; c0 += FWD_VC) {
-        const int nc = min(FWD_VC, v1 - c0);
+    for (int c0 = v0; c0 < v1; c0 += FWL_VC) {
+        const int nc = min(FWL_VC, v1 - c0);
         __syncthreads();
         for (int i = tid; i < nc * QR; i += FWD_T) {
             const int vv = i / QR, n = i - vv * QR - nlo;
@@ -909,7 +910,8 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     cudaError_t e = cudaMallocAsync(&part, part_bytes, s);
     if (e != cudaSuccess) return e;
     dim3 grid(tiles, S);
-    if (res && g->opt.er_fwd_reg && p.ne <= KR_MAX && FWD_VC * ((p.nq + 4 + (int)std::ceil(-(double)p.nb)) | 1) * 8 <= 72 * 1024) {
+    if (res && g->opt.er_fwd_reg && p.ne <= KR_MAX &&
+        (g->opt.er_fwd_lane ? FWL_VC : FWD_VC) * ((p.nq + 4 + (int)std::ceil(-(double)p.nb)) | 1) * 8 <= 72 * 1024) {
         // register accumulators: the smallest instantiated KR >= ne
         AlphaTab at;
         std::vector<float2> en(p.ne);
@@ -927,7 +929,8 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
         // table entries below node 0: u' >= nb = -q_min/dq - 1/2 rounds to n >= -(ceil(-nb) + 1)
         const int nlo = std::max(2, (int)std::ceil(-(double)p.nb) + 2);
         const int QR = (p.nq + 1 + nlo) | 1;  // odd row stride (float2): rows start on different banks
-        const size_t sm2 = std::max((size_t)((FWD_VC * QR + 1) & ~1) * sizeof(float2) + FWD_VC * sizeof(VoxelRec),
+        const int vc = g->opt.er_fwd_lane ? FWL_VC : FWD_VC;
+        const size_t sm2 = std::max((size_t)((vc * QR + 1) & ~1) * sizeof(float2) + vc * sizeof(VoxelRec),
                                     (size_t)32 * (FWD_T + 1) * sizeof(float));
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         {
