@@ -127,7 +127,7 @@ void free_all(cacsi_geometry *g) {
     void *ptrs[] = {g->d_vox,  g->d_vy64, g->d_vz64,      g->d_vt64,      g->d_det,       g->d_dx64,
                     g->d_dy64, g->d_mask, g->d_energy,    g->d_stage_a,   g->d_stage_b,   g->d_stage_c,
                     g->d_stage_d, g->d_stage_ws, g->d_esai_bp, g->d_esai_lut, g->d_esai_sb, g->d_esai_stab,
-                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_erx_vb, g->d_erx_pm, g->d_erx_pw, g->d_erx_voff, g->d_erx_vw, g->d_erx_vP, g->d_erx_vs, g->d_pc_qbase, g->d_tc16_w1, g->d_tc16_b};
+                    g->d_esai_vwin, g->d_esai_ptot, g->d_esai_vbound, g->d_pc_off, g->d_pc_bt, g->d_pc_P, g->d_pc_q, g->d_tc_w1, g->d_esai_trng, g->d_w_tiles, g->d_pc_segwin, g->d_seen, g->d_tb_fwd, g->d_tb_bwd, g->d_tc_w, g->d_tc_b, g->d_er_off, g->d_er_vw, g->d_er_P, g->d_er_s, g->d_er_boff, g->d_er_sv, g->d_erx_vb, g->d_erx_pm, g->d_erx_pw, g->d_erx_voff, g->d_erx_vw, g->d_erx_vP, g->d_erx_vs, g->d_erf_off, g->d_erf_vw, g->d_erf_P, g->d_erf_s, g->d_erf_boff, g->d_pc_qbase, g->d_tc16_w1, g->d_tc16_b};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -151,6 +151,7 @@ const OptKey kOptKeys[] = {
     {"er_cache", &cacsi::Opts::er_cache, true, 0, 1},
     {"pc_perm_lane", &cacsi::Opts::pc_perm_lane, true, 0, 1},
     {"er_vcache", &cacsi::Opts::er_vcache, true, 0, 1},
+    {"er_fcache", &cacsi::Opts::er_fcache, true, 0, 1},
     {"wgemm", &cacsi::Opts::wgemm, false, 0, 2},
     {"wgemm_pack", &cacsi::Opts::wgemm_pack, false, 0, 1},
     {"b2gemm_tiles", &cacsi::Opts::b2gemm_tiles, false, 0, 1},
@@ -178,6 +179,8 @@ const OptKey kOptKeys[] = {
     {"er_fwd_lane", &cacsi::Opts::er_fwd_lane, false, 0, 1},
     {"er_bwd_fx", &cacsi::Opts::er_bwd_fx, false, 0, 1},
     {"er_vcache_use", &cacsi::Opts::er_vcache_use, false, 0, 1},
+    {"er_fwd_rec", &cacsi::Opts::er_fwd_rec, false, 0, 1},
+    {"er_fwd_win", &cacsi::Opts::er_fwd_win, false, 0, 1 << 20},
     {"graphs", &cacsi::Opts::graphs, false, 0, 1},
 };
 
@@ -1001,6 +1004,7 @@ int64_t cacsi_query(const cacsi_geometry *g, const char *key) {
     if (!strcmp(key, "energy_resolving")) return g->p.energy_resolving;
     if (!strcmp(key, "er_cache_records")) return g->er.enabled ? g->er.n : 0;
     if (!strcmp(key, "er_vcache_records")) return g->d_erx_voff ? g->erx_vc_n : 0;
+    if (!strcmp(key, "er_fcache_records")) return g->erf.enabled ? g->erf.n : 0;
     if (!strcmp(key, "mask_guard_ppm")) return (int64_t)std::llround(g->p.mask_guard * 1e6);
     static const char *stages[8] = {"setup_us_tables", "setup_us_bitmaps", "setup_us_bound", "setup_us_pc_fill",
                                     "setup_us_pc_perm", "setup_us_pc_segwin", "setup_us_host", "setup_us_total"};

@@ -125,6 +125,31 @@ __global__ void __launch_bounds__(256) k_er_fill(const Params p, const long long
     }
 }
 
+// the same records as one 16-byte word each (vw, P, s, 0): one 128-bit load per record
+__global__ void __launch_bounds__(256) k_er_fill16(const Params p, const long long *__restrict__ off, uint4 *rec,
+                                                   uint32_t *boff, int nvb) {
+    const int lane = threadIdx.x & 31;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p.n_det; q += (gridDim.x * blockDim.x) >> 5) {
+        const float2 d = p.det[q];
+        const long long base = off[q];
+        int c = 0;
+        for (int v0 = 0; v0 < p.n_vox; v0 += 32) {
+            if (v0 % kErVB == 0 && lane == 0) boff[(size_t)(v0 / kErVB) * p.n_det + q] = (uint32_t)c;
+            const int v = v0 + lane;
+            float P = 0.0f, sh = 0.0f;
+            int klo = 0, khi = -1;
+            const bool o = v < p.n_vox && er_pair(p, v, q, d, P, sh, klo, khi);
+            const unsigned m = __ballot_sync(FULL, o);
+            if (o)
+                rec[base + c + __popc(m & ((1u << lane) - 1u))] =
+                    make_uint4((uint32_t)v | ((uint32_t)klo << 16) | ((uint32_t)khi << 24), __float_as_uint(P),
+                               __float_as_uint(sh), 0u);
+            c += __popc(m);
+        }
+        if (lane == 0) boff[(size_t)nvb * p.n_det + q] = (uint32_t)c;
+    }
+}
+
 // ------------------------------------------------------------- helpers ----
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
@@ -798,6 +823,53 @@ cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d) {
     cudaFree(sv0);
     cudaFree(A1);
     cudaFree(part);
+    if (e != cudaSuccess) return e;
+    E.enabled = 1;
+    return cudaSuccess;
+}
+
+// The pixel-major records alone (no backward scales), for the default energy-resolving
+// forward k_forward_rec (operators.cu, option er_fcache): the records and per-block offsets of
+// er_build, each record one 16-byte word (vw, P, s, 0) read by a single 128-bit load; built only
+// when they leave `reserve` bytes of device memory free.
+// Leaves g->erf.enabled = 0 when skipped.
+cudaError_t er_fcache_build(cacsi_geometry *g, size_t reserve) {
+    const Params &p = g->p;
+    ErCache &E = g->erf;
+    E.enabled = 0;
+    if (p.n_vox > 65535 || p.ne > 128) return cudaSuccess;
+    E.nvb = (p.n_vox + kErVB - 1) / kErVB;
+    const int nsm = sms(g->device);
+    long long *cnt = nullptr;
+    cudaError_t e = cudaMalloc(&cnt, (size_t)p.n_det * sizeof(long long));
+    if (e != cudaSuccess) return e;
+    k_er_count<<<8 * nsm, 256>>>(p, cnt);
+    std::vector<long long> hc(p.n_det), off(p.n_det + 1, 0);
+    e = cudaMemcpy(hc.data(), cnt, p.n_det * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(cnt);
+    if (e != cudaSuccess) return e;
+    for (int q = 0; q < p.n_det; q++) off[q + 1] = off[q] + hc[q];
+    const long long nrec = off[p.n_det];
+    const size_t need = (size_t)(std::max(nrec, 1ll) + 2) * 16 + (size_t)(p.n_det + 1) * 8 +
+                        (size_t)(E.nvb + 1) * p.n_det * 4 + 64;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (need + reserve > free_b) return cudaSuccess;
+    e = cudaMalloc(&g->d_erf_off, (p.n_det + 1) * sizeof(long long));
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_erf_off, off.data(), (p.n_det + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_erf_vw, (std::max(nrec, 1ll) + 2) * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMalloc(&g->d_erf_boff, (size_t)(E.nvb + 1) * p.n_det * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    E.n = nrec;
+    E.off = (const long long *)g->d_erf_off;
+    E.vw = (const uint32_t *)g->d_erf_vw;  // uint4 records (vw, P, s, 0)
+    E.P = nullptr;
+    E.s = nullptr;
+    E.boff = (const uint32_t *)g->d_erf_boff;
+    E.sv = nullptr;
+    k_er_fill16<<<8 * nsm, 256>>>(p, E.off, (uint4 *)g->d_erf_vw, (uint32_t *)g->d_erf_boff, E.nvb);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return e;
     E.enabled = 1;
     return cudaSuccess;

@@ -190,6 +190,7 @@ struct Opts {
     int er_cache = 0;         // "er_cache": 1 = energy-resolving operators from the pair cache (er_cache.cu)
     int pc_perm_lane = 1;     // "pc_perm_lane": 0 = the bank-aware permutation one window per warp (k_pc_perm)
     int er_vcache = 1;        // "er_vcache": 0 = no voxel-major open-pair cache for the energy-resolving backward
+    int er_fcache = 1;        // "er_fcache": 0 = no pixel-major open-pair records for the energy-resolving forward (k_forward_rec)
     // per call (cacsi_set_option may change them between calls)
     int wgemm = 0;            // "wgemm": 0 A-resident, 1 CTA-pair (cta_group::2), 2 per-tile
     int wgemm_pack = 0;       // "wgemm_pack": 1 = pre-split f (k_tc_pack_a) instead of TMA + in-kernel split
@@ -218,6 +219,8 @@ struct Opts {
     int er_fwd_lane = 1;      // "er_fwd_lane": 0 = the register forward with warp-uniform voxels (k_forward_reg)
     int er_bwd_fx = 1;        // "er_bwd_fx": 0 = the direct energy-resolving backward with fp32 shared-memory histograms
     int er_vcache_use = 1;    // "er_vcache_use": 0 = its pair geometry recomputed per call even when the cache exists
+    int er_fwd_win = 8;       // "er_fwd_win": k_forward_rec lanes wait while more than this many voxels past the warp's lowest
+    int er_fwd_rec = 1;       // "er_fwd_rec": 0 = k_forward_lane (mask tests and pair geometry per call) even when the forward records exist
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
 };
 
@@ -240,6 +243,9 @@ struct cacsi_geometry {
     // energy-resolving pair cache (er_cache.cu)
     cacsi::ErCache er;
     void *d_er_off, *d_er_vw, *d_er_P, *d_er_s, *d_er_boff, *d_er_sv;
+    // the same pixel-major records alone, for the default energy-resolving forward (option er_fcache)
+    cacsi::ErCache erf;
+    void *d_erf_off, *d_erf_vw, *d_erf_P, *d_erf_s, *d_erf_boff;
     // fixed-point energy-resolving backward (operators.cu): per voxel bin bound
     // and max P, per pixel energy-window union over its open pairs (built at create)
     void *d_erx_vb, *d_erx_pm, *d_erx_pw;
@@ -340,6 +346,7 @@ cudaError_t esai_forward_ratio(const cacsi_geometry *g, const float *f, const Fw
 size_t recon_workspace_bytes(const cacsi_geometry *g);
 cudaError_t esai_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
 cudaError_t er_build(cacsi_geometry *g, const cacsi_geometry_desc *d);
+cudaError_t er_fcache_build(cacsi_geometry *g, size_t reserve);
 cudaError_t er_forward(const cacsi_geometry *g, const float *f, float *out, cudaStream_t s, int *launches);
 cudaError_t er_backward(const cacsi_geometry *g, const float *w, float *b, cudaStream_t s, int *launches);
 cudaError_t erx_build(cacsi_geometry *g);

@@ -327,6 +327,207 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_lane(const Params p, const
     }
 }
 
+// (c0, slope) table of every voxel for k_forward_rec: row v = entries n = -nlo .. QR - nlo - 1 of
+// f[v], exactly k_forward_lane's staging arithmetic (so the two forwards are bit-identical); one
+// zero row of padding past the last voxel (the bulk copies round their byte counts up to 16)
+__global__ void k_fl_tab(const Params p, const float *__restrict__ f, int nlo, int QR, float2 *__restrict__ tab) {
+    const size_t n = (size_t)(p.n_vox + 1) * QR;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int v = (int)(i / QR), n0 = (int)(i % QR) - nlo;
+        float a = 0.0f, b = 0.0f;
+        if (v < p.n_vox) {
+            const float *fr = f + (size_t)v * p.nq;
+            a = (n0 >= 0 && n0 < p.nq) ? fr[n0] : 0.0f;
+            b = (n0 + 1 >= 0 && n0 + 1 < p.nq) ? fr[n0 + 1] : 0.0f;
+        }
+        tab[i] = make_float2((float)(0.5 * ((double)a + (double)b) - (double)n0 * ((double)b - (double)a)), b - a);
+    }
+}
+
+__device__ __forceinline__ void fr_mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+}
+
+// The register forward fed by the pixel-major open-pair records (option er_fwd_rec, default when
+// the records exist): the same lanes = pixels, KR energy sums in registers, per-lane
+// voxel streams and per-term arithmetic as k_forward_lane, but
+//  * no mask tests and no pair geometry per call: each lane walks its pixel's records (voxel,
+//    energy window, P, sin(theta/2) as one 16-byte word; er_fcache_build) in increasing voxel
+//    order, loaded two records ahead into registers;
+//  * the (c0, slope) rows come from one table per call (k_fl_tab) by cp.async.bulk, two chunks of
+//    FWL_VC voxels in flight: while chunk c is worked on, a lane that has finished its chunk-c
+//    records goes on with chunk c + 1 once its rows have landed, so the warp's steps are bounded
+//    by the lane with the most records over two chunks rather than one;
+//  * no CTA barrier per chunk: each warp counts itself done with a buffer, and the last one
+//    refills it, so warps drift apart by up to a chunk instead of waiting for the slowest.
+// The voxels of each pixel's sum are added in the same order, so the result is bit-identical to
+// k_forward_lane with the same splits.
+template <int KR>
+__global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const ErCache c,
+                                                          const float2 *__restrict__ gtab, int vox_per_split,
+                                                          float *__restrict__ partial, const AlphaTab at, int nlo,
+                                                          int QR, int win) {
+    extern __shared__ float4 smem4[];
+    const int K = p.ne;
+    float2 *tab = (float2 *)smem4;  // [2][VC][QR] (c0, slope); reused to stage the output
+    uint64_t *full = (uint64_t *)(tab + 2 * FWL_VC * QR);  // [2] (2 * VC * QR * 8 is a multiple of 16)
+    int *cnt = (int *)(full + 2);                          // [2] warps done with each buffer (monotone); [4]: pad
+    const int tid = threadIdx.x;
+    const int pix = blockIdx.x * FWD_T + tid;
+    const bool valid = pix < p.n_det;
+    const int v0 = blockIdx.y * vox_per_split;
+    const int v1 = min(p.n_vox, v0 + vox_per_split);
+    const int nch = (v1 - v0 + FWL_VC - 1) / FWL_VC;
+    const uint32_t rowb = (uint32_t)QR * 8u;
+    const uint32_t tab0 = (uint32_t)__cvta_generic_to_shared(tab + nlo) - (uint32_t)kMagicBits * 8u;
+    auto issue = [&](int ci) {  // chunk ci -> buffer ci & 1
+        const int cb = v0 + ci * FWL_VC, nc = min(FWL_VC, v1 - cb);
+        const uint32_t bytes = ((uint32_t)nc * rowb + 15u) & ~15u;
+        const uint32_t mb = (uint32_t)__cvta_generic_to_shared(full + (ci & 1));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(tab + (size_t)(ci & 1) * FWL_VC * QR)),
+                     "l"(gtab + (size_t)cb * QR), "r"(bytes), "r"(mb)
+                     : "memory");
+    };
+    if (tid == 0) {
+        cnt[0] = cnt[1] = 0;
+        for (int i = 0; i < 2; i++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(full + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+        issue(0);
+        if (nch > 1) issue(1);
+    }
+    // this lane's records of the split (v0 and v1 are multiples of kErVB or v1 = n_vox)
+    long long r = 0, rend = 0;
+    if (valid) {
+        const long long o = c.off[pix];
+        r = o + c.boff[(size_t)(v0 / kErVB) * p.n_det + pix];
+        rend = o + c.boff[(size_t)(v1 == p.n_vox ? c.nvb : v1 / kErVB) * p.n_det + pix];
+    }
+    // records r, r + 1, r + 2 in a per-lane ring of three shared-memory slots filled by cp.async
+    // (16-byte words vw, P, s); the slot of the record in use is refilled with record r + 3, so
+    // each load has three steps to land.  One commit group per step (empty past the end), so
+    // wait_group 2 leaves only records r + 1, r + 2 in flight.
+    const uint4 *rec = (const uint4 *)c.vw;
+    uint4 *ring = (uint4 *)(cnt + 4) + tid;  // slot i at ring[i * FWD_T]
+    auto fetch = [&](long long i, int slot) {
+        if (i < rend)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(ring + slot * FWD_T)),
+                         "l"(rec + i)
+                         : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    fetch(r, 0);
+    fetch(r + 1, 1);
+    fetch(r + 2, 2);
+    int ph = 0;  // slot of record r
+    asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    uint4 cr = r < rend ? ring[0] : make_uint4(0u, 0u, 0x3f800000u, 0u);
+    int curv = r < rend ? (int)(cr.x & 0xFFFFu) : 0x7FFFFFFF;
+    float acc[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) acc[k] = 0.0f;
+    const int lane = tid & 31;
+    __syncthreads();  // mbarrier init visible
+    for (int ci = 0; ci < nch; ci++) {
+        const int cb = v0 + ci * FWL_VC;
+        const int endc = min(v1, cb + FWL_VC);
+        fr_mbar_wait((uint32_t)__cvta_generic_to_shared(full + (ci & 1)), (uint32_t)(ci >> 1) & 1u);
+        // a lane may run ahead into chunk ci + 1 once its rows have landed (they land when every
+        // warp has finished chunk ci - 1; tested without blocking)
+        const uint32_t mbn = (uint32_t)__cvta_generic_to_shared(full + ((ci + 1) & 1));
+        const uint32_t phn = (uint32_t)((ci + 1) >> 1) & 1u;
+        int endn = endc;
+        while (__any_sync(FULL, curv < endc)) {
+            if (endn == endc && ci + 1 < nch) {
+                uint32_t ok = 0u;
+                if (lane == 0)
+                    asm volatile(
+                        "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+                        : "=r"(ok)
+                        : "r"(mbn), "r"(phn)
+                        : "memory");
+                if (__shfl_sync(FULL, ok, 0)) endn = min(v1, cb + 2 * FWL_VC);
+            }
+            // lanes more than `win` voxels past the warp's lowest wait: fewer distinct table rows per
+            // step, so fewer shared-memory bank conflicts, at the price of a few more steps
+            const int vmin = __reduce_min_sync(FULL, curv);
+            const bool act = curv < endn && curv <= vmin + win;
+            float P = 0.0f, sh = 1.0f;
+            int klo = K, khi = -1, vv = 0;
+            if (act) {
+                P = __uint_as_float(cr.y), sh = __uint_as_float(cr.z);
+                klo = (int)((cr.x >> 16) & 0xFFu), khi = (int)(cr.x >> 24);
+                vv = curv - cb;
+            }
+            const int wlo = __reduce_min_sync(FULL, klo);
+            const int whi = __reduce_max_sync(FULL, khi);
+            // this lane's row: chunk ci + (vv >= VC) sits in buffer (ci + (vv >> 5)) & 1
+            const uint32_t tb = tab0 + (uint32_t)((((ci + (vv >> 5)) & 1) << 5) + (vv & 31)) * rowb;
+            static_assert(FWL_VC == 32, "row index split");
+#pragma unroll
+            for (int kb = 0; kb < KR; kb += 8) {
+                if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
+                    const float vm = u + kMagic;
+                    CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits < QR - nlo);
+                    const float2 t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
+                    acc[kb + j] = fmaf(P, fmaf(u, t.y, t.x), acc[kb + j]);
+                }
+            }
+            if (act) {
+                // refill the slot just used with record r + 3, then step to record r + 1
+                fetch(r + 3, ph);
+                r++;
+                ph = ph == 2 ? 0 : ph + 1;
+                asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+                if (r < rend) cr = ring[ph * FWD_T];
+                curv = r < rend ? (int)(cr.x & 0xFFFFu) : 0x7FFFFFFF;
+            }
+        }
+        // this warp is done with chunk ci; the last of the CTA's warps to get here refills its
+        // buffer with chunk ci + 2 (arrival counts only grow: round ci's last arrival is number
+        // NW (ci / 2 + 1) on counter ci & 1)
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            const int old = atomicAdd(cnt + (ci & 1), 1);
+            if (old == (FWD_T / 32) * ((ci >> 1) + 1) - 1 && ci + 2 < nch) {
+                __threadfence_block();  // the other warps' reads of the buffer before the async-proxy write
+                issue(ci + 2);
+            }
+        }
+    }
+    __syncthreads();  // every warp past its last chunk before the tables are reused for the output
+    // [pixels][K] block of this CTA through shared memory (coalesced stores), scaled by c_k
+    float *stage = (float *)smem4;
+    const int npx = min(FWD_T, p.n_det - (int)blockIdx.x * FWD_T);
+    float *out = partial + ((size_t)blockIdx.y * p.n_det + (size_t)blockIdx.x * FWD_T) * K;
+    for (int kb = 0; kb < KR; kb += 32) {
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            if (kb + j < KR) stage[j * (FWD_T + 1) + tid] = acc[kb + j];
+        __syncthreads();
+        const int kn = min(32, K - kb);
+        for (int i = tid; i < npx * kn; i += FWD_T) {
+            const int px = i / kn, k = i - px * kn;
+            out[(size_t)px * K + kb + k] = p.energy[kb + k].y * stage[k * (FWD_T + 1) + px];
+        }
+    }
+}
+
 // [rows][cols] -> [cols][rows] (32 x 32 shared-memory tiles)
 __global__ void k_transpose(const float *__restrict__ in, int rows, int cols, float *__restrict__ out) {
     __shared__ float t[32][33];
@@ -899,7 +1100,10 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
     if (res) S = max(S, (p.n_vox + 1023) / 1024);  // fp32 partial sums over <= 1024 voxels
     S = max(1, min(S, max_s));
     int vps = (p.n_vox + S - 1) / S;
-    vps = (vps + FWD_VC - 1) / FWD_VC * FWD_VC;
+    // energy-resolving register forwards: splits on record-block boundaries (k_forward_rec reads
+    // its records' offsets per kErVB voxels; k_forward_lane uses the same splits, same bits)
+    const int vround = res && g->opt.er_fwd_reg ? kErVB : FWD_VC;
+    vps = (vps + vround - 1) / vround * vround;
     S = (p.n_vox + vps - 1) / vps;
     const size_t n_out = (size_t)p.n_det * (res ? p.ne : 1);
     const size_t part_bytes = (size_t)S * n_out * (res ? sizeof(float) : sizeof(double));
@@ -932,8 +1136,33 @@ cudaError_t launch_forward(const cacsi_geometry *g, const float *f, float *out, 
         const int vc = g->opt.er_fwd_lane ? FWL_VC : FWD_VC;
         const size_t sm2 = std::max((size_t)((vc * QR + 1) & ~1) * sizeof(float2) + vc * sizeof(VoxelRec),
                                     (size_t)32 * (FWD_T + 1) * sizeof(float));
-        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-        {
+        if (g->erf.enabled && g->opt.er_fwd_rec && g->opt.er_fwd_lane && vps % kErVB == 0) {
+            // the record-fed forward: one (c0, slope) table per call, chunks landed by cp.async.bulk
+            auto kr = p.ne <= 16 ? k_forward_rec<16> : p.ne <= 32 ? k_forward_rec<32> : p.ne <= 64 ? k_forward_rec<64>
+                    : p.ne <= 104 ? k_forward_rec<104> : k_forward_rec<128>;
+            float2 *gt = nullptr;
+            e = cudaMallocAsync(&gt, (size_t)(p.n_vox + 1) * QR * sizeof(float2), s);
+            if (e == cudaSuccess) {
+                {
+                    KScope kt_(g, s, "k_fl_tab");
+                    k_fl_tab<<<4 * num_sms(g->device), 256, 0, s>>>(p, f, nlo, QR, gt);
+                }
+                const size_t sm3 = std::max((size_t)2 * FWL_VC * QR * sizeof(float2) + 32 + 3 * FWD_T * 16,
+                                            (size_t)32 * (FWD_T + 1) * sizeof(float));
+                cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+                {
+                    KScope kt_(g, s, "k_forward_er");
+                    kr<<<grid, FWD_T, sm3, s>>>(p, g->erf, gt, vps, (float *)part, at, nlo, QR, g->opt.er_fwd_win);
+                }
+                cudaFreeAsync(gt, s);
+                *launches += 1;
+            }
+            if (e != cudaSuccess) {
+                cudaFreeAsync(part, s);
+                return e;
+            }
+        } else {
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
             KScope kt_(g, s, "k_forward_er");
             kf<<<grid, FWD_T, sm2, s>>>(p, f, vps, (float *)part, at, nlo, QR);
         }
@@ -1078,6 +1307,11 @@ cudaError_t erx_build(cacsi_geometry *g) {
             cudaFree(g->d_erx_voff);
             g->d_erx_voff = nullptr;
         }
+    }
+    // the pixel-major records of the forward (option er_fcache; k_forward_rec), same 8 GB margin
+    if (g->opt.er_fcache) {
+        e = er_fcache_build(g, (size_t)8 << 30);
+        if (e != cudaSuccess) return e;
     }
     float *b1 = nullptr;
     e = cudaMalloc(&b1, (size_t)p.n_vox * p.nq * sizeof(float));

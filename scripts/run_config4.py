@@ -1,4 +1,6 @@
-"""Run the config-4 (energy-resolving) forward and backward once each (ncu target)."""
+"""Run the config-4 (energy-resolving) forward and backward once each (ncu target).
+
+    python scripts/run_config4.py [options]   (cacsi_geometry_create_ex kernel-variant options)"""
 import os
 import sys
 
@@ -10,7 +12,7 @@ import paper_1603_06400_b200 as P  # noqa: E402
 from workloads import make_config  # noqa: E402
 
 cfg = make_config(4)
-G = P.Geometry(cfg.desc())
+G = P.Geometry(cfg.desc(), options=sys.argv[1] if len(sys.argv) > 1 else None)
 f = torch.as_tensor(cfg.f).cuda()
 g = torch.empty(G.g_shape, dtype=torch.float32, device="cuda")
 b = torch.empty(G.f_shape, dtype=torch.float32, device="cuda")

@@ -23,15 +23,53 @@ def test_er_forward_registers_bitwise_and_oracle(ne):
     d.update(ne=ne, energy_kev=np.linspace(21.0, 149.0, ne), phi=np.linspace(1.0, 0.3, ne),
              ny=6, nz=5, nq=21, det_nx=7, det_ny=19)
     G = P.Geometry(d)
+    assert G.query("er_fcache_records") > 0  # the default forward is the record-fed k_forward_rec
     f = rnd(G.f_shape, 0, 140)
     g1 = gpu_forward(G, f)
-    # per-lane voxel streams (er_fwd_lane=1, the default) vs warp-uniform voxels: same sums, same order
+    # record-fed vs per-lane mask tests and pair geometry (k_forward_lane): same sums, same order
+    G.set_option("er_fwd_rec", 0)
+    assert np.array_equal(gpu_forward(G, f), g1)
+    # per-lane voxel streams vs warp-uniform voxels: same sums, same order
     G.set_option("er_fwd_lane", 0)
     assert np.array_equal(gpu_forward(G, f), g1)
     G.set_option("er_fwd_reg", 0)
     g0 = gpu_forward(G, f)
     assert_parity(g1, g0, f"er forward registers vs shared accumulators ne={ne}", l2=1e-6, mr=1e-5)
     assert_parity(g1, oracle.Geometry(d).forward(f), f"er forward registers ne={ne}")
+
+
+@pytest.mark.parametrize("shape", [
+    dict(ny=37, nz=41, det_nx=13, det_ny=29, ne=40),   # 2 splits, ragged chunks and pixel tile
+    dict(ny=64, nz=67, det_nx=9, det_ny=15, ne=100),   # 5 splits of 896 voxels, 135 pixels
+    dict(ny=3, nz=11, det_nx=40, det_ny=7, ne=17),     # one chunk, 280 pixels
+])
+def test_er_forward_records_multichunk(shape):
+    """k_forward_rec over many table chunks (two in flight, lanes running ahead into the next),
+    several voxel splits and ragged ends: bit-identical to k_forward_lane and k_forward_reg, and
+    the oracle bar."""
+    ne = shape["ne"]
+    d = make_config(0, energy_resolving=1).desc()
+    d.update(energy_kev=np.linspace(21.0, 149.0, ne), phi=np.linspace(1.0, 0.3, ne), nq=33, **shape)
+    G = P.Geometry(d)
+    assert G.query("er_fcache_records") > 0
+    f = rnd(G.f_shape, 0, 142)
+    g1 = gpu_forward(G, f)
+    assert np.array_equal(gpu_forward(G, f), g1)
+    G.set_option("er_fwd_rec", 0)
+    assert np.array_equal(gpu_forward(G, f), g1)
+    G.set_option("er_fwd_lane", 0)
+    assert np.array_equal(gpu_forward(G, f), g1)
+    assert_parity(g1, oracle.Geometry(d).forward(f), f"er forward records {shape}")
+
+
+def test_er_forward_records_off():
+    """er_fcache=0 at create: no records, the forward falls back to k_forward_lane (same bits)."""
+    d = make_config(0, energy_resolving=1).desc()
+    G = P.Geometry(d)
+    G0 = P.Geometry(d, options="er_fcache=0")
+    assert G0.query("er_fcache_records") == 0
+    f = rnd(G.f_shape, 0, 143)
+    assert np.array_equal(gpu_forward(G, f), gpu_forward(G0, f))
 
 
 def test_er_forward_registers_non_uniform_energies():
