@@ -839,6 +839,7 @@ struct ErxQ {
 };
 constexpr int ERX_CAP = 96;
 constexpr int ERX_PF = 8;   // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
+constexpr int ERX_F = 2;    // first w~ blocks of the next batch loaded during the current one (cached path)
 // Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
 // open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
 // P, sin(theta/2) (12 B per open pair; 39 GB on config 4); vc_off[v] = first record of voxel v.
@@ -884,17 +885,20 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
     const uint32_t hb0 = (uint32_t)__cvta_generic_to_shared(hist + tid) + (uint32_t)(nlo - kMagicBits) * (uint32_t)(4 * BWD_T);
     ErxQ *wq = queue + warp * ERX_CAP;
     int qn = 0;
+    // u = alpha sigma - q_min/dq (true coordinates: nb + 1/2, clamp qm + 1/2) rounded DOWN to its
+    // node n (FADD.RM against 1.5 * 2^23), fraction u - n exact: lower node (1 - frac) a, upper frac a
+    const float nb1 = nb + 0.5f, qm1 = qm + 0.5f;
+    const uint32_t hbl = __shfl_sync(FULL, hb0, lane);  // opaque to ptxas: one LEA per row address
     auto term = [&](float al, float wk, float sh, float cs) {
-        // u' = alpha sigma - q_min/dq - 1/2 >= -nlo + 1/2 (no lower clamp); a term outside this
-        // lane's window lands on the padding rows (nodes < 0 or >= nq; at u' = nq - 1/2 with
-        // odd nq, n = nq - 1 gets lo = 0 exactly)
-        const float u = fminf(fmaf(al, sh, nb), qm);
-        const float vm = u + kMagic;
-        const float tt = u - (vm - kMagic);
+        // u >= -nlo + 1 (no lower clamp); a term outside this lane's window lands on the padding
+        // rows (nodes < 0 or >= nq; at the clamp u = nq the whole deposit goes to node nq)
+        const float u = fminf(fmaf(al, sh, nb1), qm1);
+        const float vm = __fadd_rd(u, kMagic);
+        const float fr = u - (vm - kMagic);
         const float a = cs * wk;
         const uint32_t ab = __float_as_uint(a + kMagic);
-        const uint32_t hb = __float_as_uint(fmaf(tt + 0.5f, a, kMagic));
-        const uint32_t addr = hb0 + (__float_as_uint(vm) << 9);
+        const uint32_t hb = __float_as_uint(fmaf(fr, a, kMagic));
+        const uint32_t addr = hbl + (__float_as_uint(vm) << 9);
         static_assert(4 * BWD_T == 512, "row stride");
         CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits <= Q);
         red_s32(addr, ab - hb);
@@ -934,31 +938,87 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         }
     };
     if constexpr (CACHE) {
-        // the voxel's open pairs straight from the cache, 32 per batch, batches on demand
+        // the voxel's open pairs straight from the cache, 32 per batch, batches on demand.  Records
+        // are loaded two batches ahead; the first ERX_F energy blocks of w of the NEXT batch are
+        // loaded while the current one deposits (a batch no longer starts on an L2 round trip);
+        // each lane loads only the blocks of its own window (the union's other blocks deposit on
+        // the padding rows whatever w they use)
         const long long r0 = vc.off[v], r1 = vc.off[v + 1];
-        // records of the next batch loaded while the current one deposits
-        auto load = [&](long long bi, uint32_t &wv, float &P, float &sg) {
-            const long long r = r0 + bi * 32 + lane;
-            wv = 0u, P = 0.0f, sg = 1.0f;
-            if (r < r1) wv = __ldg(vc.w + r), P = __ldg(vc.P + r), sg = __ldg(vc.s + r);
+        struct Rec {
+            uint32_t w;
+            float P, s;
         };
-        long long bi = warp;
-        uint32_t wv;
-        float rP, rs;
-        load(bi, wv, rP, rs);
-        while (r0 + bi * 32 < r1) {
-            const int cnt = (int)min(32LL, r1 - (r0 + bi * 32));
-            if (lane < cnt) {
-                const int klo = (int)((wv >> 17) & 127u), khi1 = (int)(wv >> 24);
-                wq[lane] = ErxQ{rP * sv, rs, (int)(wv & 0x1FFFFu), klo | (khi1 << 16)};
-            }
+        auto load = [&](long long bi) {
+            const long long r = r0 + bi * 32 + lane;
+            Rec x{0u, 0.0f, 1.0f};
+            if (r < r1) x.w = __ldg(vc.w + r), x.P = __ldg(vc.P + r), x.s = __ldg(vc.s + r);
+            return x;
+        };
+        struct Dec {
+            const char *wr;
+            float cs, sh;
+            int klo, khi, kb0, kb1;  // own window; the warp's union in energy blocks of 4
+        };
+        auto decode = [&](const Rec &x, bool valid) {
+            Dec d;
+            d.klo = valid ? (int)((x.w >> 17) & 127u) : K;
+            d.khi = valid ? (int)(x.w >> 24) - 1 : -1;
+            d.wr = (const char *)(wt + (valid ? (x.w & 0x1FFFFu) : 0u));
+            d.cs = x.P * sv, d.sh = x.s;
+            d.kb0 = __reduce_min_sync(FULL, d.klo) >> 2;
+            const int hi = __reduce_max_sync(FULL, d.khi);
+            d.kb1 = hi < 0 ? -1 : hi >> 2;
+            return d;
+        };
+        auto wload = [&](const Dec &d, int kb) {  // block kb of this lane's pixel, if in its window
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (kb >= (d.klo >> 2) && kb <= (d.khi >> 2)) x = __ldg((const float4 *)(d.wr + (size_t)kb * wstride));
+            return x;
+        };
+        auto deposit4 = [&](const Dec &d, int kb, const float4 &wc) {
+            const float4 a4 = *(const float4 *)(alpha + (kb << 2));
+            term(a4.x, wc.x, d.sh, d.cs);
+            term(a4.y, wc.y, d.sh, d.cs);
+            term(a4.z, wc.z, d.sh, d.cs);
+            term(a4.w, wc.w, d.sh, d.cs);
+        };
+        auto next_batch = [&]() {
             int g = 0;
             if (lane == 0) g = atomicAdd(&s_next, 1);
-            bi = __shfl_sync(FULL, g, 0);
-            load(bi, wv, rP, rs);
-            __syncwarp();
-            batch(cnt);
-            __syncwarp();
+            return (long long)__shfl_sync(FULL, g, 0);
+        };
+        long long ba = warp, bb = next_batch();
+        Rec A = load(ba), B = load(bb);
+        Dec dA = decode(A, r0 + ba * 32 + lane < r1);
+        float4 fst[ERX_F];
+#pragma unroll
+        for (int i = 0; i < ERX_F; i++) fst[i] = wload(dA, dA.kb0 + i);
+        while (r0 + ba * 32 < r1) {
+            const long long bc = next_batch();
+            const Rec C = load(bc);
+            // the rest of this batch's blocks: the next ERX_PF in flight in a register ring
+            float4 wn[ERX_PF];
+            const int kr0 = dA.kb0 + ERX_F;
+#pragma unroll
+            for (int i = 0; i < ERX_PF; i++) wn[i] = kr0 + i <= dA.kb1 ? wload(dA, kr0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < ERX_F; i++)
+                if (dA.kb0 + i <= dA.kb1) deposit4(dA, dA.kb0 + i, fst[i]);  // warp-uniform
+            // the next batch: window union and its first blocks, landing while this one deposits
+            const Dec dB = decode(B, r0 + bb * 32 + lane < r1);
+#pragma unroll
+            for (int i = 0; i < ERX_F; i++) fst[i] = wload(dB, dB.kb0 + i);
+            for (int kb = kr0; kb <= dA.kb1; kb += ERX_PF) {
+#pragma unroll
+                for (int i = 0; i < ERX_PF; i++) {
+                    if (kb + i > dA.kb1) break;  // warp-uniform
+                    deposit4(dA, kb + i, wn[i]);
+                    if (kb + i + ERX_PF <= dA.kb1) wn[i] = wload(dA, kb + i + ERX_PF);
+                }
+            }
+            ba = bb, bb = bc;
+            dA = dB;
+            B = C;
         }
     } else {
     // 64-pixel groups: the first one per warp fixed, the rest taken on demand (balances the
