@@ -955,25 +955,36 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             return x;
         };
         struct Dec {
-            const char *wr;
+            uint32_t q;              // pixel
             float cs, sh;
-            int klo, khi, kb0, kb1;  // own window; the warp's union in energy blocks of 4
+            int lo4, span4;          // own window in energy blocks of 4: lo4 .. lo4 + span4 (none: lo4 huge)
+            int kb0, kb1;            // the warp's union in energy blocks of 4
         };
         auto decode = [&](const Rec &x, bool valid) {
             Dec d;
-            d.klo = valid ? (int)((x.w >> 17) & 127u) : K;
-            d.khi = valid ? (int)(x.w >> 24) - 1 : -1;
-            d.wr = (const char *)(wt + (valid ? (x.w & 0x1FFFFu) : 0u));
+            const int klo = valid ? (int)((x.w >> 17) & 127u) : K;
+            const int khi = valid ? (int)(x.w >> 24) - 1 : -1;
+            d.q = valid ? (x.w & 0x1FFFFu) : 0u;
             d.cs = x.P * sv, d.sh = x.s;
-            d.kb0 = __reduce_min_sync(FULL, d.klo) >> 2;
-            const int hi = __reduce_max_sync(FULL, d.khi);
+            d.lo4 = klo <= khi ? klo >> 2 : 0x40000000;
+            d.span4 = klo <= khi ? (khi >> 2) - (klo >> 2) : 0;
+            d.kb0 = __reduce_min_sync(FULL, klo) >> 2;
+            const int hi = __reduce_max_sync(FULL, khi);
             d.kb1 = hi < 0 ? -1 : hi >> 2;
             return d;
         };
-        auto wload = [&](const Dec &d, int kb) {  // block kb of this lane's pixel, if in its window
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (kb >= (d.klo >> 2) && kb <= (d.khi >> 2)) x = __ldg((const float4 *)(d.wr + (size_t)kb * wstride));
-            return x;
+        // block kb of this lane's pixel into x if it is in the lane's own window; otherwise x keeps
+        // the stale (finite) w of an earlier block: those terms land on the padding rows, or on
+        // node 0 with a weight of exactly 0 (u = -1)
+        const uint32_t ndet = (uint32_t)p.n_det;
+        auto wload = [&](float4 &x, const Dec &d, int kb) {
+            if ((uint32_t)(kb - d.lo4) <= (uint32_t)d.span4) x = __ldg(wt + ((uint32_t)kb * ndet + d.q));
+        };
+        auto deposit4a = [&](const Dec &d, const float4 &a4, const float4 &wc) {
+            term(a4.x, wc.x, d.sh, d.cs);
+            term(a4.y, wc.y, d.sh, d.cs);
+            term(a4.z, wc.z, d.sh, d.cs);
+            term(a4.w, wc.w, d.sh, d.cs);
         };
         auto deposit4 = [&](const Dec &d, int kb, const float4 &wc) {
             const float4 a4 = *(const float4 *)(alpha + (kb << 2));
@@ -990,30 +1001,39 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         long long ba = warp, bb = next_batch();
         Rec A = load(ba), B = load(bb);
         Dec dA = decode(A, r0 + ba * 32 + lane < r1);
-        float4 fst[ERX_F];
+        float4 fst[ERX_F], wn[ERX_PF];  // zeroed once; afterwards stale blocks stay finite
 #pragma unroll
-        for (int i = 0; i < ERX_F; i++) fst[i] = wload(dA, dA.kb0 + i);
+        for (int i = 0; i < ERX_F; i++) fst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < ERX_PF; i++) wn[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < ERX_F; i++) wload(fst[i], dA, dA.kb0 + i);
         while (r0 + ba * 32 < r1) {
             const long long bc = next_batch();
             const Rec C = load(bc);
             // the rest of this batch's blocks: the next ERX_PF in flight in a register ring
-            float4 wn[ERX_PF];
             const int kr0 = dA.kb0 + ERX_F;
 #pragma unroll
-            for (int i = 0; i < ERX_PF; i++) wn[i] = kr0 + i <= dA.kb1 ? wload(dA, kr0 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < ERX_PF; i++) wload(wn[i], dA, kr0 + i);
 #pragma unroll
             for (int i = 0; i < ERX_F; i++)
                 if (dA.kb0 + i <= dA.kb1) deposit4(dA, dA.kb0 + i, fst[i]);  // warp-uniform
             // the next batch: window union and its first blocks, landing while this one deposits
             const Dec dB = decode(B, r0 + bb * 32 + lane < r1);
 #pragma unroll
-            for (int i = 0; i < ERX_F; i++) fst[i] = wload(dB, dB.kb0 + i);
+            for (int i = 0; i < ERX_F; i++) wload(fst[i], dB, dB.kb0 + i);
+            // alpha of the next block read one block ahead (the shared-memory latency off the chain;
+            // past the last block it reads a harmless word of the histogram)
+            static_assert(ERX_PF % 2 == 0, "alpha double buffer");
+            float4 an[2];
+            an[0] = *(const float4 *)(alpha + (kr0 << 2));
             for (int kb = kr0; kb <= dA.kb1; kb += ERX_PF) {
 #pragma unroll
                 for (int i = 0; i < ERX_PF; i++) {
                     if (kb + i > dA.kb1) break;  // warp-uniform
-                    deposit4(dA, kb + i, wn[i]);
-                    if (kb + i + ERX_PF <= dA.kb1) wn[i] = wload(dA, kb + i + ERX_PF);
+                    an[(i + 1) & 1] = *(const float4 *)(alpha + ((kb + i + 1) << 2));
+                    deposit4a(dA, an[i & 1], wn[i]);
+                    wload(wn[i], dA, kb + i + ERX_PF);
                 }
             }
             ba = bb, bb = bc;
