@@ -477,12 +477,16 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const 
 #pragma unroll
             for (int kb = 0; kb < KR; kb += 8) {
                 if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
+                // lanes whose own window misses the block (or idle lanes) do not read the table:
+                // their terms are exact zeros, and their reads would only add bank conflicts
+                const bool mine = kb + 8 > klo && kb <= khi;
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
                     const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
                     const float vm = u + kMagic;
                     CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits < QR - nlo);
-                    const float2 t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
+                    float2 t = make_float2(0.0f, 0.0f);
+                    if (mine) t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
                     acc[kb + j] = fmaf(P, fmaf(u, t.y, t.x), acc[kb + j]);
                 }
             }
