@@ -28,7 +28,11 @@ def main():
     quick = "--quick" in sys.argv
     cases = [(0, {}, None), (0, {}, "pair_cache=0"), (0, {}, "direct=1"), (0, dict(energy_resolving=1), None),
              (0, dict(energy_resolving=1), "er_cache=1"),
-             (0, dict(sai_n_theta=250, sai_theta_min=0.0035, sai_theta_max=0.5236), None)]
+             (0, dict(sai_n_theta=250, sai_theta_min=0.0035, sai_theta_max=0.5236), None),
+             # energy-resolving, several table chunks and voxel splits: the record-fed forward
+             # (k_forward_rec, cp.async record ring, barrier-free chunk rounds) and the cached backward
+             (0, dict(energy_resolving=1, ny=37, nz=41, det_nx=13, det_ny=29, ne=40,
+                      energy_kev=np.linspace(21.0, 149.0, 40), phi=np.linspace(1.0, 0.3, 40), nq=33), None)]
     if not quick:
         cases += [(1, {}, None), (1, {}, "pair_cache=0")]
     rng = np.random.default_rng(0)
