@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_lane(const Params p, const
     const int Q = p.nq, K = p.ne;
     float2 *tab = (float2 *)smem4;                          // [VC][QR] (c0, slope); reused to stage the output
     VoxelRec *svox = (VoxelRec *)(tab + ((FWL_VC * QR + 1) & ~1));  // [VC]
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int pix = blockIdx.x * FWD_T + tid;
     const bool valid = pix < p.n_det;
     const float2 d = p.det[valid ? pix : 0];
@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const 
     float acc[KR];
 #pragma unroll
     for (int k = 0; k < KR; k++) acc[k] = 0.0f;
+    float2 tv[8];  // the block's table values (finite: zero, or an earlier read)
+#pragma unroll
+    for (int j = 0; j < 8; j++) tv[j] = make_float2(0.0f, 0.0f);
     const int lane = tid & 31;
     __syncthreads();  // mbarrier init visible
     for (int ci = 0; ci < nch; ci++) {
@@ -479,15 +482,17 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const 
                 if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
                 // lanes whose own window misses the block (or idle lanes) do not read the table:
                 // their terms are exact zeros, and their reads would only add bank conflicts
+                // (such a lane keeps the finite table values of an earlier read in tv[] and adds them
+                // with weight 0: no zeroing per term)
                 const bool mine = kb + 8 > klo && kb <= khi;
+                const float Pm = mine ? P : 0.0f;
 #pragma unroll
                 for (int j = 0; j < 8; j++) {
                     const float u = fminf(fmaf(at.a[kb + j], sh, p.nb), p.qm);
                     const float vm = u + kMagic;
                     CACSI_CHECK(__float_as_int(vm) - kMagicBits >= -nlo && __float_as_int(vm) - kMagicBits < QR - nlo);
-                    float2 t = make_float2(0.0f, 0.0f);
-                    if (mine) t = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
-                    acc[kb + j] = fmaf(P, fmaf(u, t.y, t.x), acc[kb + j]);
+                    if (mine) tv[j] = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
+                    acc[kb + j] = fmaf(Pm, fmaf(u, tv[j].y, tv[j].x), acc[kb + j]);
                 }
             }
             if (act) {
