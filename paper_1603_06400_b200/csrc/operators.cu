@@ -847,8 +847,14 @@ struct ErxQ {
     int q, kw;     // pixel, klo | (khi + 1) << 16
 };
 constexpr int ERX_CAP = 96;
-constexpr int ERX_PF = 8;   // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
-constexpr int ERX_F = 2;    // first w~ blocks of the next batch loaded during the current one (cached path)
+#ifndef CACSI_ERX_PF
+#define CACSI_ERX_PF 8
+#endif
+#ifndef CACSI_ERX_F
+#define CACSI_ERX_F 2
+#endif
+constexpr int ERX_PF = CACSI_ERX_PF;  // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
+constexpr int ERX_F = CACSI_ERX_F;    // first w~ blocks of the next batch loaded during the current one (cached path)
 // Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
 // open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
 // P, sin(theta/2) (12 B per open pair; 39 GB on config 4); vc_off[v] = first record of voxel v.
