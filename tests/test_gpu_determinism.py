@@ -94,3 +94,53 @@ def test_permutation_window_bitwise(win):
         H.backward(w, H.b)
     torch.cuda.synchronize()
     assert torch.equal(G.g, Gw.g) and torch.equal(G.b, Gw.b)
+
+
+def _er_medium():
+    d = make_config(0, energy_resolving=1).desc()
+    d.update(ny=64, nz=67, det_nx=21, det_ny=37, ne=100, nq=33,
+             energy_kev=np.linspace(21.0, 149.0, 100), phi=np.linspace(1.0, 0.3, 100))
+    return d
+
+
+def test_er_repeat_bitwise_medium():
+    """The energy-resolving operators repeated 40 times on a shape with many table chunks, 5 voxel
+    splits and a ragged pixel tile: the record-fed forward's barrier-free chunk rounds (warps
+    counting themselves done with a buffer, the last one refilling it; lanes running ahead once
+    the next chunk has landed) and the backward's two-batch prefetch must give the same bits
+    every time."""
+    G = P.Geometry(_er_medium())
+    assert G.query("er_fcache_records") > 0 and G.query("er_vcache_records") > 0
+    rng = np.random.default_rng(5)
+    f = torch.as_tensor(rng.uniform(0, 1, G.f_shape).astype(np.float32)).cuda()
+    w = torch.as_tensor(rng.uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
+    g0, b0 = torch.empty(G.g_shape, device="cuda"), torch.empty(G.f_shape, device="cuda")
+    G.forward(f, g0)
+    G.backward(w, b0)
+    for _ in range(40):
+        g, b = torch.empty_like(g0), torch.empty_like(b0)
+        G.forward(f, g)
+        G.backward(w, b)
+        assert torch.equal(g, g0)
+        assert torch.equal(b, b0)
+    G.close()
+
+
+def test_er_repeat_bitwise_config4():
+    """Config 4 at full size (BASELINE configs[4], the bench's launch configuration): forward and
+    backward three times each, bit-identical."""
+    cfg = make_config(4)
+    G = P.Geometry(cfg.desc())
+    assert G.query("er_fcache_records") > 0
+    f = torch.as_tensor(cfg.f).cuda()
+    w = torch.as_tensor(np.random.default_rng(6).uniform(0, 1, G.g_shape).astype(np.float32)).cuda()
+    g0, b0 = torch.empty(G.g_shape, device="cuda"), torch.empty(G.f_shape, device="cuda")
+    G.forward(f, g0)
+    G.backward(w, b0)
+    for _ in range(2):
+        g, b = torch.empty_like(g0), torch.empty_like(b0)
+        G.forward(f, g)
+        G.backward(w, b)
+        assert torch.equal(g, g0)
+        assert torch.equal(b, b0)
+    G.close()
