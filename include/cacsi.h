@@ -136,7 +136,11 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * pair cache), pc_segwin (1), pc_q8 (2: 8-byte records, P rounded to 28 bits
  * carrying 4 pixel-offset bits; 1: 10-bit tau; 0: 10-byte records), pc_win
  * (128), pcv_budget_kb (200), er_cache (0; 1 = the
- * energy-resolving operators from a pair cache).  Per-call keys (also
+ * energy-resolving operators from a pair cache), er_vcache (1:
+ * the energy-resolving backward's voxel-major open-pair records, 12 B each),
+ * er_fcache (1: the energy-resolving forward's pixel-major open-pair records,
+ * 16 B each; both built only with 8 GB of device memory to spare, DESIGN.md
+ * 4.3).  Per-call keys (also
  * settable with cacsi_set_option): wgemm (0 A-resident, 1 CTA-pair, 2 per-tile),
  * wgemm_pack, b2gemm_tiles, pc_fwd_list, pcv_items, pcv_pf, pcv_u, pc_bwd_flat,
  * pcb_pf, subset_bwd_mask, er_bwd_dense, graphs (1; 0 = cacsi_osem by stream
@@ -144,7 +148,10 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * fp16 tensor-core rate; 0 = 3xTF32), b2_splits (16: split-K count of the fp16
  * b2 GEMM), w_tmast / b2_tmast (1: the fp16 GEMMs' epilogues store by TMA
  * tensor stores; 0 = per-lane stores), b2_rings (1: A / B ring depths of
- * the fp16 b2 GEMM, 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4).  An unknown key or out-of-range value
+ * the fp16 b2 GEMM, 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4), er_fwd_rec (1: the
+ * record-fed energy-resolving forward; 0 = mask tests and pair geometry per
+ * call), er_fwd_win (8: its lanes' voxel window), er_fwd_lane, er_fwd_reg,
+ * er_bwd_fx, er_vcache_use (1).  An unknown key or out-of-range value
  * -> CACSI_ERR_INVALID.
  * The library never reads the process environment.                          */
 CACSI_API cacsi_status cacsi_geometry_create_ex(const cacsi_geometry_desc *desc, int device, const char *options,
