@@ -332,14 +332,19 @@ def run_gpu(args):
         roofline["frac_at_observed_clock"] = round(achieved / (peak * ck["sm_mhz"] / 1965.0), 4)
     # DRAM traffic of the operator's kernels from the committed ncu --set full capture
     # (profiles/r2k_dram_traffic.json, bytes per launch); kernels it does not list are omitted
+    # (profiles/r2s4_er_dram_traffic.json for the energy-resolving kernels of config 4)
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r2k_dram_traffic.json")))["kernels"]
+        er = bool(cfg.energy_resolving)
+        fn = "r2s4_er_dram_traffic.json" if er else "r2k_dram_traffic.json"
+        tr = json.load(open(os.path.join(ROOT, "profiles", fn)))["kernels"]
         ks = [k for k in (fwd_k if dom == "cacsi_forward" else bwd_k) if k in tr]
         if ks:
             roofline["traffic"] = float(sum(tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"] for k in ks))
             roofline["traffic_note"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch of " + " + ".join(ks) + \
-                " (profiles/r2k_dram_traffic.json); compulsory bytes of the operator (f, g, w, b, tables) are ~0.1 GB -- " \
-                "the rest is the W / A scratch of the ESAI contraction"
+                f" (profiles/{fn}); " + ("the operator's open-pair records (16 B per pair forward, 12 B backward) "
+                                         "read once" if er else
+                                         "compulsory bytes of the operator (f, g, w, b, tables) are ~0.1 GB -- "
+                                         "the rest is the W / A scratch of the ESAI contraction")
     except Exception:
         pass
     eff = counts["effective_terms"]
