@@ -953,38 +953,57 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         }
     };
     if constexpr (CACHE) {
-        // the voxel's open pairs straight from the cache, 32 per batch, batches on demand.  Records
-        // are loaded two batches ahead; the first ERX_F energy blocks of w of the NEXT batch are
-        // loaded while the current one deposits (a batch no longer starts on an L2 round trip);
-        // each lane loads only the blocks of its own window (the union's other blocks deposit on
-        // the padding rows whatever w they use)
+        // the voxel's open pairs straight from the cache, 64 per unit (two records per lane: pairs
+        // x = record base + lane and y = base + 32 + lane, deposited side by side so every energy
+        // block gives eight independent dependency chains), units on demand.  Records are loaded
+        // two units ahead; the first ERX_F energy blocks of w of the NEXT unit are loaded while the
+        // current one deposits; each lane loads only the blocks of its own windows (the union's
+        // other blocks deposit on the padding rows whatever w they use)
         const long long r0 = vc.off[v], r1 = vc.off[v + 1];
         struct Rec {
             uint32_t w;
             float P, s;
         };
-        auto load = [&](long long bi) {
-            const long long r = r0 + bi * 32 + lane;
+        struct Rec2 {
+            Rec x, y;
+        };
+        auto load1 = [&](long long r) {
             Rec x{0u, 0.0f, 1.0f};
             if (r < r1) x.w = __ldg(vc.w + r), x.P = __ldg(vc.P + r), x.s = __ldg(vc.s + r);
             return x;
+        };
+        auto load = [&](long long bi) {
+            Rec2 z;
+            z.x = load1(r0 + bi * 64 + lane);
+            z.y = load1(r0 + bi * 64 + 32 + lane);
+            return z;
         };
         struct Dec {
             uint32_t q;              // pixel
             float cs, sh;
             int lo4, span4;          // own window in energy blocks of 4: lo4 .. lo4 + span4 (none: lo4 huge)
-            int kb0, kb1;            // the warp's union in energy blocks of 4
         };
-        auto decode = [&](const Rec &x, bool valid) {
+        struct Dec2 {
+            Dec x, y;
+            int kb0, kb1;            // the warp's union over both records, in energy blocks of 4
+        };
+        auto decode1 = [&](const Rec &x, bool valid, int &klo, int &khi) {
             Dec d;
-            const int klo = valid ? (int)((x.w >> 17) & 127u) : K;
-            const int khi = valid ? (int)(x.w >> 24) - 1 : -1;
+            klo = valid ? (int)((x.w >> 17) & 127u) : K;
+            khi = valid ? (int)(x.w >> 24) - 1 : -1;
             d.q = valid ? (x.w & 0x1FFFFu) : 0u;
             d.cs = x.P * sv, d.sh = x.s;
             d.lo4 = klo <= khi ? klo >> 2 : 0x40000000;
             d.span4 = klo <= khi ? (khi >> 2) - (klo >> 2) : 0;
-            d.kb0 = __reduce_min_sync(FULL, klo) >> 2;
-            const int hi = __reduce_max_sync(FULL, khi);
+            return d;
+        };
+        auto decode = [&](const Rec2 &z, long long bi) {
+            Dec2 d;
+            int kx0, kx1, ky0, ky1;
+            d.x = decode1(z.x, r0 + bi * 64 + lane < r1, kx0, kx1);
+            d.y = decode1(z.y, r0 + bi * 64 + 32 + lane < r1, ky0, ky1);
+            d.kb0 = __reduce_min_sync(FULL, min(kx0, ky0)) >> 2;
+            const int hi = __reduce_max_sync(FULL, max(kx1, ky1));
             d.kb1 = hi < 0 ? -1 : hi >> 2;
             return d;
         };
@@ -1001,54 +1020,54 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             term(a4.z, wc.z, d.sh, d.cs);
             term(a4.w, wc.w, d.sh, d.cs);
         };
-        auto deposit4 = [&](const Dec &d, int kb, const float4 &wc) {
-            const float4 a4 = *(const float4 *)(alpha + (kb << 2));
-            term(a4.x, wc.x, d.sh, d.cs);
-            term(a4.y, wc.y, d.sh, d.cs);
-            term(a4.z, wc.z, d.sh, d.cs);
-            term(a4.w, wc.w, d.sh, d.cs);
-        };
-        auto next_batch = [&]() {
+        auto next_unit = [&]() {
             int g = 0;
             if (lane == 0) g = atomicAdd(&s_next, 1);
             return (long long)__shfl_sync(FULL, g, 0);
         };
-        long long ba = warp, bb = next_batch();
-        Rec A = load(ba), B = load(bb);
-        Dec dA = decode(A, r0 + ba * 32 + lane < r1);
-        float4 fst[ERX_F], wn[ERX_PF];  // zeroed once; afterwards stale blocks stay finite
+        constexpr int PF2 = ERX_PF / 2;  // ring depth per record (the same registers as one ring of ERX_PF)
+        static_assert(PF2 % 2 == 0, "alpha double buffer");
+        long long ba = warp, bb = next_unit();
+        Rec2 A = load(ba), B = load(bb);
+        Dec2 dA = decode(A, ba);
+        float4 fx[ERX_F], fy[ERX_F], wx[PF2], wy[PF2];  // zeroed once; afterwards stale blocks stay finite
 #pragma unroll
-        for (int i = 0; i < ERX_F; i++) fst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < ERX_F; i++) fx[i] = fy[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < ERX_PF; i++) wn[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < PF2; i++) wx[i] = wy[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < ERX_F; i++) wload(fst[i], dA, dA.kb0 + i);
-        while (r0 + ba * 32 < r1) {
-            const long long bc = next_batch();
-            const Rec C = load(bc);
-            // the rest of this batch's blocks: the next ERX_PF in flight in a register ring
+        for (int i = 0; i < ERX_F; i++) wload(fx[i], dA.x, dA.kb0 + i), wload(fy[i], dA.y, dA.kb0 + i);
+        while (r0 + ba * 64 < r1) {
+            const long long bc = next_unit();
+            const Rec2 C = load(bc);
+            // the rest of this unit's blocks: the next PF2 per record in flight in register rings
             const int kr0 = dA.kb0 + ERX_F;
 #pragma unroll
-            for (int i = 0; i < ERX_PF; i++) wload(wn[i], dA, kr0 + i);
+            for (int i = 0; i < PF2; i++) wload(wx[i], dA.x, kr0 + i), wload(wy[i], dA.y, kr0 + i);
 #pragma unroll
             for (int i = 0; i < ERX_F; i++)
-                if (dA.kb0 + i <= dA.kb1) deposit4(dA, dA.kb0 + i, fst[i]);  // warp-uniform
-            // the next batch: window union and its first blocks, landing while this one deposits
-            const Dec dB = decode(B, r0 + bb * 32 + lane < r1);
+                if (dA.kb0 + i <= dA.kb1) {  // warp-uniform
+                    const float4 a4 = *(const float4 *)(alpha + ((dA.kb0 + i) << 2));
+                    deposit4a(dA.x, a4, fx[i]);
+                    deposit4a(dA.y, a4, fy[i]);
+                }
+            // the next unit: window union and its first blocks, landing while this one deposits
+            const Dec2 dB = decode(B, bb);
 #pragma unroll
-            for (int i = 0; i < ERX_F; i++) wload(fst[i], dB, dB.kb0 + i);
-            // alpha of the next block read one block ahead (the shared-memory latency off the chain;
-            // past the last block it reads a harmless word of the histogram)
-            static_assert(ERX_PF % 2 == 0, "alpha double buffer");
+            for (int i = 0; i < ERX_F; i++) wload(fx[i], dB.x, dB.kb0 + i), wload(fy[i], dB.y, dB.kb0 + i);
+            // alpha of the next block read one block ahead (past the last block it reads a harmless
+            // word of the histogram)
             float4 an[2];
             an[0] = *(const float4 *)(alpha + (kr0 << 2));
-            for (int kb = kr0; kb <= dA.kb1; kb += ERX_PF) {
+            for (int kb = kr0; kb <= dA.kb1; kb += PF2) {
 #pragma unroll
-                for (int i = 0; i < ERX_PF; i++) {
+                for (int i = 0; i < PF2; i++) {
                     if (kb + i > dA.kb1) break;  // warp-uniform
                     an[(i + 1) & 1] = *(const float4 *)(alpha + ((kb + i + 1) << 2));
-                    deposit4a(dA, an[i & 1], wn[i]);
-                    wload(wn[i], dA, kb + i + ERX_PF);
+                    deposit4a(dA.x, an[i & 1], wx[i]);
+                    deposit4a(dA.y, an[i & 1], wy[i]);
+                    wload(wx[i], dA.x, kb + i + PF2);
+                    wload(wy[i], dA.y, kb + i + PF2);
                 }
             }
             ba = bb, bb = bc;
