@@ -853,7 +853,15 @@ constexpr int ERX_CAP = 96;
 #ifndef CACSI_ERX_F
 #define CACSI_ERX_F 2
 #endif
+#ifndef CACSI_ERX_NRL
+#define CACSI_ERX_NRL 4
+#endif
+#ifndef CACSI_ERX_PFR
+#define CACSI_ERX_PFR 2
+#endif
 constexpr int ERX_PF = CACSI_ERX_PF;  // w~ blocks of look-ahead (Little's law: ~20 sectors per request from L2)
+constexpr int ERX_NRL = CACSI_ERX_NRL;  // open-pair records per lane per unit (cached path)
+constexpr int ERX_PFR = CACSI_ERX_PFR;  // w~ ring depth per record (cached path)
 constexpr int ERX_F = CACSI_ERX_F;    // first w~ blocks of the next batch loaded during the current one (cached path)
 // Open-pair cache of the energy-resolving backward (option er_vcache): per voxel, its
 // open pairs with a non-empty energy window in pixel order, SoA: word = q | klo << 17 | (khi + 1) << 24,
@@ -953,29 +961,29 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
         }
     };
     if constexpr (CACHE) {
-        // the voxel's open pairs straight from the cache, 64 per unit (two records per lane: pairs
-        // x = record base + lane and y = base + 32 + lane, deposited side by side so every energy
-        // block gives eight independent dependency chains), units on demand.  Records are loaded
-        // two units ahead; the first ERX_F energy blocks of w of the NEXT unit are loaded while the
-        // current one deposits; each lane loads only the blocks of its own windows (the union's
-        // other blocks deposit on the padding rows whatever w they use)
+        // the voxel's open pairs straight from the cache, NRL records per lane per unit (record j =
+        // unit base + 32 j + lane), their deposits side by side so every energy block gives 4 NRL
+        // independent dependency chains; units on demand.  Records are loaded two units ahead; the
+        // first ERX_F energy blocks of w of the NEXT unit are loaded while the current one
+        // deposits; each lane loads only the blocks of its own windows (the union's other blocks
+        // deposit on the padding rows whatever w they use)
+        constexpr int NRL = ERX_NRL, UNIT = 32 * NRL;
         const long long r0 = vc.off[v], r1 = vc.off[v + 1];
         struct Rec {
             uint32_t w;
             float P, s;
         };
-        struct Rec2 {
-            Rec x, y;
-        };
-        auto load1 = [&](long long r) {
-            Rec x{0u, 0.0f, 1.0f};
-            if (r < r1) x.w = __ldg(vc.w + r), x.P = __ldg(vc.P + r), x.s = __ldg(vc.s + r);
-            return x;
+        struct RecN {
+            Rec x[NRL];
         };
         auto load = [&](long long bi) {
-            Rec2 z;
-            z.x = load1(r0 + bi * 64 + lane);
-            z.y = load1(r0 + bi * 64 + 32 + lane);
+            RecN z;
+#pragma unroll
+            for (int j = 0; j < NRL; j++) {
+                const long long r = r0 + bi * UNIT + 32 * j + lane;
+                z.x[j] = Rec{0u, 0.0f, 1.0f};
+                if (r < r1) z.x[j].w = __ldg(vc.w + r), z.x[j].P = __ldg(vc.P + r), z.x[j].s = __ldg(vc.s + r);
+            }
             return z;
         };
         struct Dec {
@@ -983,27 +991,26 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             float cs, sh;
             int lo4, span4;          // own window in energy blocks of 4: lo4 .. lo4 + span4 (none: lo4 huge)
         };
-        struct Dec2 {
-            Dec x, y;
-            int kb0, kb1;            // the warp's union over both records, in energy blocks of 4
+        struct DecN {
+            Dec x[NRL];
+            int kb0, kb1;            // the warp's union over the unit, in energy blocks of 4
         };
-        auto decode1 = [&](const Rec &x, bool valid, int &klo, int &khi) {
-            Dec d;
-            klo = valid ? (int)((x.w >> 17) & 127u) : K;
-            khi = valid ? (int)(x.w >> 24) - 1 : -1;
-            d.q = valid ? (x.w & 0x1FFFFu) : 0u;
-            d.cs = x.P * sv, d.sh = x.s;
-            d.lo4 = klo <= khi ? klo >> 2 : 0x40000000;
-            d.span4 = klo <= khi ? (khi >> 2) - (klo >> 2) : 0;
-            return d;
-        };
-        auto decode = [&](const Rec2 &z, long long bi) {
-            Dec2 d;
-            int kx0, kx1, ky0, ky1;
-            d.x = decode1(z.x, r0 + bi * 64 + lane < r1, kx0, kx1);
-            d.y = decode1(z.y, r0 + bi * 64 + 32 + lane < r1, ky0, ky1);
-            d.kb0 = __reduce_min_sync(FULL, min(kx0, ky0)) >> 2;
-            const int hi = __reduce_max_sync(FULL, max(kx1, ky1));
+        auto decode = [&](const RecN &z, long long bi) {
+            DecN d;
+            int lo = K, hi = -1;
+#pragma unroll
+            for (int j = 0; j < NRL; j++) {
+                const bool valid = r0 + bi * UNIT + 32 * j + lane < r1;
+                const int klo = valid ? (int)((z.x[j].w >> 17) & 127u) : K;
+                const int khi = valid ? (int)(z.x[j].w >> 24) - 1 : -1;
+                d.x[j].q = valid ? (z.x[j].w & 0x1FFFFu) : 0u;
+                d.x[j].cs = z.x[j].P * sv, d.x[j].sh = z.x[j].s;
+                d.x[j].lo4 = klo <= khi ? klo >> 2 : 0x40000000;
+                d.x[j].span4 = klo <= khi ? (khi >> 2) - (klo >> 2) : 0;
+                lo = min(lo, klo), hi = max(hi, khi);
+            }
+            d.kb0 = __reduce_min_sync(FULL, lo) >> 2;
+            hi = __reduce_max_sync(FULL, hi);
             d.kb1 = hi < 0 ? -1 : hi >> 2;
             return d;
         };
@@ -1025,36 +1032,43 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
             if (lane == 0) g = atomicAdd(&s_next, 1);
             return (long long)__shfl_sync(FULL, g, 0);
         };
-        constexpr int PF2 = ERX_PF / 2;  // ring depth per record (the same registers as one ring of ERX_PF)
+        constexpr int PF2 = ERX_PFR;  // ring depth per record
         static_assert(PF2 % 2 == 0, "alpha double buffer");
         long long ba = warp, bb = next_unit();
-        Rec2 A = load(ba), B = load(bb);
-        Dec2 dA = decode(A, ba);
-        float4 fx[ERX_F], fy[ERX_F], wx[PF2], wy[PF2];  // zeroed once; afterwards stale blocks stay finite
+        RecN A = load(ba), B = load(bb);
+        DecN dA = decode(A, ba);
+        float4 fw[NRL][ERX_F], rw[NRL][PF2];  // zeroed once; afterwards stale blocks stay finite
 #pragma unroll
-        for (int i = 0; i < ERX_F; i++) fx[i] = fy[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < NRL; j++) {
 #pragma unroll
-        for (int i = 0; i < PF2; i++) wx[i] = wy[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < ERX_F; i++) fw[j][i] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < ERX_F; i++) wload(fx[i], dA.x, dA.kb0 + i), wload(fy[i], dA.y, dA.kb0 + i);
-        while (r0 + ba * 64 < r1) {
+            for (int i = 0; i < PF2; i++) rw[j][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < ERX_F; i++) wload(fw[j][i], dA.x[j], dA.kb0 + i);
+        }
+        while (r0 + ba * UNIT < r1) {
             const long long bc = next_unit();
-            const Rec2 C = load(bc);
+            const RecN C = load(bc);
             // the rest of this unit's blocks: the next PF2 per record in flight in register rings
             const int kr0 = dA.kb0 + ERX_F;
 #pragma unroll
-            for (int i = 0; i < PF2; i++) wload(wx[i], dA.x, kr0 + i), wload(wy[i], dA.y, kr0 + i);
+            for (int i = 0; i < PF2; i++)
+#pragma unroll
+                for (int j = 0; j < NRL; j++) wload(rw[j][i], dA.x[j], kr0 + i);
 #pragma unroll
             for (int i = 0; i < ERX_F; i++)
                 if (dA.kb0 + i <= dA.kb1) {  // warp-uniform
                     const float4 a4 = *(const float4 *)(alpha + ((dA.kb0 + i) << 2));
-                    deposit4a(dA.x, a4, fx[i]);
-                    deposit4a(dA.y, a4, fy[i]);
+#pragma unroll
+                    for (int j = 0; j < NRL; j++) deposit4a(dA.x[j], a4, fw[j][i]);
                 }
             // the next unit: window union and its first blocks, landing while this one deposits
-            const Dec2 dB = decode(B, bb);
+            const DecN dB = decode(B, bb);
 #pragma unroll
-            for (int i = 0; i < ERX_F; i++) wload(fx[i], dB.x, dB.kb0 + i), wload(fy[i], dB.y, dB.kb0 + i);
+            for (int j = 0; j < NRL; j++)
+#pragma unroll
+                for (int i = 0; i < ERX_F; i++) wload(fw[j][i], dB.x[j], dB.kb0 + i);
             // alpha of the next block read one block ahead (past the last block it reads a harmless
             // word of the histogram)
             float4 an[2];
@@ -1064,10 +1078,10 @@ __global__ void __launch_bounds__(BWD_T) k_backward_er_x(const Params p, const f
                 for (int i = 0; i < PF2; i++) {
                     if (kb + i > dA.kb1) break;  // warp-uniform
                     an[(i + 1) & 1] = *(const float4 *)(alpha + ((kb + i + 1) << 2));
-                    deposit4a(dA.x, an[i & 1], wx[i]);
-                    deposit4a(dA.y, an[i & 1], wy[i]);
-                    wload(wx[i], dA.x, kb + i + PF2);
-                    wload(wy[i], dA.y, kb + i + PF2);
+#pragma unroll
+                    for (int j = 0; j < NRL; j++) deposit4a(dA.x[j], an[i & 1], rw[j][i]);
+#pragma unroll
+                    for (int j = 0; j < NRL; j++) wload(rw[j][i], dA.x[j], kb + i + PF2);
                 }
             }
             ba = bb, bb = bc;
