@@ -358,13 +358,17 @@ __device__ __forceinline__ void fr_mbar_wait(uint32_t mbar, uint32_t phase) {
 // voxel streams and per-term arithmetic as k_forward_lane, but
 //  * no mask tests and no pair geometry per call: each lane walks its pixel's records (voxel,
 //    energy window, P, sin(theta/2) as one 16-byte word; er_fcache_build) in increasing voxel
-//    order, loaded two records ahead into registers;
+//    order through a 3-slot per-lane ring in shared memory filled by cp.async (three records
+//    in flight);
 //  * the (c0, slope) rows come from one table per call (k_fl_tab) by cp.async.bulk, two chunks of
 //    FWL_VC voxels in flight: while chunk c is worked on, a lane that has finished its chunk-c
 //    records goes on with chunk c + 1 once its rows have landed, so the warp's steps are bounded
 //    by the lane with the most records over two chunks rather than one;
 //  * no CTA barrier per chunk: each warp counts itself done with a buffer, and the last one
-//    refills it, so warps drift apart by up to a chunk instead of waiting for the slowest.
+//    refills it, so warps drift apart by up to a chunk instead of waiting for the slowest;
+//  * lanes more than `win` voxels past the warp's lowest wait (fewer distinct table rows per
+//    step: fewer bank conflicts), and lanes whose window misses an energy block skip its table
+//    reads, adding earlier (finite) table values with weight 0.
 // The voxels of each pixel's sum are added in the same order, so the result is bit-identical to
 // k_forward_lane with the same splits.
 template <int KR>
