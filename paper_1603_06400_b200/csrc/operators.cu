@@ -481,13 +481,14 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const 
             // this lane's row: chunk ci + (vv >= VC) sits in buffer (ci + (vv >> 5)) & 1
             const uint32_t tb = tab0 + (uint32_t)((((ci + (vv >> 5)) & 1) << 5) + (vv & 31)) * rowb;
             static_assert(FWL_VC == 32, "row index split");
-#pragma unroll
-            for (int kb = 0; kb < KR; kb += 8) {
-                if (kb + 8 <= wlo || kb > whi) continue;  // warp-uniform
+            // energy blocks in PAIRS (16 independent terms per basic block): a pair is worked when
+            // either of its blocks meets the warp's window union; a block outside the union has no
+            // lane whose window meets it, so its terms are exact zeros with no table reads
+            auto block = [&](const int kb) {
                 // lanes whose own window misses the block (or idle lanes) do not read the table:
                 // their terms are exact zeros, and their reads would only add bank conflicts
-                // (such a lane keeps the finite table values of an earlier read in tv[] and adds them
-                // with weight 0: no zeroing per term)
+                // (such a lane keeps the finite table values of an earlier read in tv[] and adds
+                // them with weight 0: no zeroing per term)
                 const bool mine = kb + 8 > klo && kb <= khi;
                 const float Pm = mine ? P : 0.0f;
 #pragma unroll
@@ -498,6 +499,12 @@ __global__ void __launch_bounds__(FWD_T, 3) k_forward_rec(const Params p, const 
                     if (mine) tv[j] = lds2(tb + ((uint32_t)__float_as_int(vm) << 3));
                     acc[kb + j] = fmaf(Pm, fmaf(u, tv[j].y, tv[j].x), acc[kb + j]);
                 }
+            };
+#pragma unroll
+            for (int kb = 0; kb < KR; kb += 16) {
+                if (kb + 16 <= wlo || kb > whi) continue;  // warp-uniform
+                block(kb);
+                if (kb + 8 < KR) block(kb + 8);
             }
             if (act) {
                 // refill the slot just used with record r + 3, then step to record r + 1
