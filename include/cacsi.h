@@ -150,7 +150,7 @@ CACSI_API cacsi_status cacsi_geometry_create(const cacsi_geometry_desc *desc, in
  * tensor stores; 0 = per-lane stores), b2_rings (1: A / B ring depths of
  * the fp16 b2 GEMM, 0 = 3 / 3, 1 = 4 / 2, 2 = 2 / 4), er_fwd_rec (1: the
  * record-fed energy-resolving forward; 0 = mask tests and pair geometry per
- * call), er_fwd_win (8: its lanes' voxel window), er_fwd_lane, er_fwd_reg,
+ * call), er_fwd_win (6: its lanes' voxel window), er_fwd_lane, er_fwd_reg,
  * er_bwd_fx, er_vcache_use (1).  An unknown key or out-of-range value
  * -> CACSI_ERR_INVALID.
  * The library never reads the process environment.                          */

@@ -219,7 +219,7 @@ struct Opts {
     int er_fwd_lane = 1;      // "er_fwd_lane": 0 = the register forward with warp-uniform voxels (k_forward_reg)
     int er_bwd_fx = 1;        // "er_bwd_fx": 0 = the direct energy-resolving backward with fp32 shared-memory histograms
     int er_vcache_use = 1;    // "er_vcache_use": 0 = its pair geometry recomputed per call even when the cache exists
-    int er_fwd_win = 8;       // "er_fwd_win": k_forward_rec lanes wait while more than this many voxels past the warp's lowest
+    int er_fwd_win = 6;       // "er_fwd_win": k_forward_rec lanes wait while more than this many voxels past the warp's lowest
     int er_fwd_rec = 1;       // "er_fwd_rec": 0 = k_forward_lane (mask tests and pair geometry per call) even when the forward records exist
     int graphs = 1;           // "graphs": 0 = cacsi_osem by stream launches
 };
