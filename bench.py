@@ -11,6 +11,10 @@ the dominant kernel reported beside it.  Multi-GPU: the path does not shard
 (north_star: one GPU, no collectives) -> N independent replicas, value =
 all ranks' pairs / max-over-ranks time, scaling "weak".
 
+At N=1 the config-2 line also carries "config3" (BASELINE configs[3]: 50 EM
+iterations with setup, final relative error, OSEM-64) and "config4" (BASELINE
+configs[4], energy-resolving: this script with --config 4 in a child process).
+
 --impl reference times the fp64 CPU oracle (the reference arm of this tier) on
 a bounded sample of the same workload, on this box's host cores.
 """
@@ -46,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--options", default=None, help="kernel-variant options (cacsi_geometry_create_ex)")
     ap.add_argument("--no-config3", action="store_true", help="skip the config-3 reconstruction key")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 (energy-resolving) key")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0, help="target seconds of oracle work")
     return ap.parse_args()
 
@@ -422,12 +427,39 @@ def run_gpu(args):
     if rank == 0 and args.config == 2 and not args.no_config3:
         G.close()
         out["config3"] = run_config3(P, torch, dev, local)
+    if rank == 0 and world == 1 and args.config == 2 and not args.no_config4:
+        out["config4"] = run_config4()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     G.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+CONFIG4_KEYS = ("metric", "value", "unit", "steps", "warmup", "ms_per_step", "config", "forward_ms", "backward_ms",
+                "effective_terms_per_s", "gpu_launches", "clocks", "roofline", "e2e", "setup_ms",
+                "amortized_ms_per_step_50")
+
+
+def run_config4(steps=3, warmup=3, timeout_s=900):
+    """BASELINE.json configs[4] (energy-resolving, the regime SURVEY §8 calls the stress case)
+    measured in the default bench run, so the driver's line carries it: this script with
+    --config 4 in a child process (its own CUDA context and memory; the config-2 handle
+    is closed), the same timing rules (warm-up, L2 flush, CUDA events, clocks, e2e through
+    cacsi_iterate_host); the child's cpu_baseline is skipped (the config-4 oracle sample is
+    in profiles/r2s5a_bench4.json)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "4", "--steps", str(steps), "--warmup", str(warmup),
+           "--no-cpu-baseline"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, env=dict(os.environ))
+        line = [x for x in r.stdout.strip().splitlines() if x.startswith("{")]
+        if r.returncode != 0 or not line:
+            return {"error": f"rc={r.returncode}: {(r.stderr or '').strip().splitlines()[-1:]}"}
+        d = json.loads(line[-1])
+        return {k: d[k] for k in CONFIG4_KEYS if k in d}
+    except Exception as ex:  # reported, never hidden: the key then says why it is missing
+        return {"error": repr(ex)}
 
 
 def run_config3(P, torch, dev, local, n_iter=50, osem_outer=3):
