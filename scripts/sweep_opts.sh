@@ -5,7 +5,7 @@ TAG=$1; shift
 mkdir -p gpurun_out
 for cfg in "$@"; do
   name=$(echo "$cfg" | tr ',=' '_-')
-  timeout 300 python bench.py --no-cpu-baseline --steps 20 --options "$cfg" > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err
+  timeout 300 python bench.py --no-cpu-baseline --no-config3 --no-config4 --steps 20 --options "$cfg" > gpurun_out/${TAG}_${name}.json 2> gpurun_out/${TAG}_${name}.err
   python - "$cfg" gpurun_out/${TAG}_${name}.json >> gpurun_out/${TAG}_sweep.txt <<'PY'
 import json, sys
 try:
